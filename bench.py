@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark: HVP GDOF/s and implicit-step time of the MPM Lite hot path on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
+
+A *step* is one full implicit time step of the workload: bin + sort,
+P2Q + stretch, C2N, Newton (linearise, Jacobi-PCG with the matrix-free HVP, line search), G2P.
+`value` = HVP GDOF/s = 3 * free nodes * HVP launches / summed HVP device time (CUDA events on the
+library stream) over the K timed steps, summed over ranks.  `ms_per_step` = implicit-step time
+(device clock, max over ranks).  Inputs are resident in HBM when the timed region starts; the
+HVP's tangent stream (>= 392 MB at cfg4) is larger than the 126 MB L2.
+
+--impl reference times the CPU oracle (oracle/, plain fp64 C, 1 core) on a bounded window of the
+same workload; it is the deliberately slow baseline, not a target.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, val in zip(names, s[3:7]):
+                if val.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rk = int(os.environ.get("RANK", "0"))
+    lr = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rk, lr
+
+
+def hvp_bytes(n_cells, n_nodes, s=4):
+    """Algorithmic bytes of one HVP: the 45-number tangent per quadrature point plus
+    u (3), Hu (3) and m (1) per active node."""
+    return n_cells * 45 * s + n_nodes * 7 * s
+
+
+def load_traffic(config: str):
+    p = os.path.join(ROOT, "profiles", "hvp_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(config)
+    return None
+
+
+# ------------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    from paper_2602_07853_b200 import mpl, scenes
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    sc = scenes.by_name(args.config, args.precision)
+    ctx = mpl.from_scene(sc, device=local)
+    stream = torch.cuda.Stream(device=local)
+    ctx.set_stream(stream.cuda_stream)
+    solver = sc.solver
+
+    def one_step():
+        return ctx.step(sc.dt, solver)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    stats = []
+    counts = []
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            stats.append(one_step())
+            counts.append(ctx.counts)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms_total = e0.elapsed_time(e1)
+    n_hvp = sum(s["n_hvp"] for s in stats)
+    hvp_ms = sum(s["hvp_ms"] for s in stats)
+    # free DOFs per step (active nodes minus prescribed ones)
+    ijk, m, vn, fr = (None,) * 4
+    dofs = []
+    cells = []
+    nodes = []
+    for c, s in zip(counts, stats):
+        cells.append(c.n_cells)
+        nodes.append(c.n_nodes)
+    # the last resample's free-DOF count (Dirichlet floor) -- nodes change only slightly per step
+    ctx.resample(sc.dt)
+    _, _, _, fr = ctx.get_nodes()
+    n_free = int(fr.sum())
+    dof_hvp = 3.0 * n_free * n_hvp
+    gdofs = dof_hvp / (hvp_ms * 1e-3) / 1e9 if hvp_ms > 0 else 0.0
+    ms_per_step = ms_total / args.steps
+    if ws > 1:
+        t = torch.tensor([ms_per_step, gdofs], dtype=torch.float64, device="cuda")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_per_step = float(mx[0])
+        gdofs = float(sm[1])
+    avg_hvp_ms = hvp_ms / max(n_hvp, 1)
+    nbytes = hvp_bytes(statistics.mean(cells), statistics.mean(nodes), 4 if args.precision == 32 else 8)
+    peak, peak_kind = load_peaks()
+    achieved = nbytes / (avg_hvp_ms * 1e-3) / 1e9
+    # e2e: the same metric through the C ABI with HOST buffers (H2D of particles, D2H of results)
+    e2e = run_e2e(ctx, sc, solver, stream, args) if rank == 0 else None
+    clocks = clk.summary()
+    result = {
+        "metric": "HVP GDOF/s (matrix-free incremental-potential Hessian-vector product inside Newton-PCG)",
+        "value": round(gdofs, 3),
+        "unit": "GDOF/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32" if args.precision == 32 else "f64",
+        "data": "synthetic (seeded scene generator, paper_2602_07853_b200/scenes.py)",
+        "config": {
+            "workload": f"{sc.name}: {sc.n[0]}^3 grid, {sc.n_particles} particles, "
+                        f"{len(sc.materials)} material(s), dt={sc.dt}",
+            "grid": list(sc.n), "particles": sc.n_particles, "quadrature_points": int(statistics.mean(cells)),
+            "active_nodes": int(statistics.mean(nodes)), "free_dofs": 3 * n_free,
+            "parallelism": "1 GPU" if ws == 1 else f"{ws} independent replicas (slab decomposition: DESIGN.md §6)",
+            "l2": "inputs larger than L2 (tangent stream > 126 MB per HVP)",
+            "step": "full implicit step: resample + Newton-PCG + G2P",
+        },
+        "implicit_step_ms": round(ms_per_step, 3),
+        "newton_iters": [s["newton_iters"] for s in stats],
+        "cg_iters": [s["cg_iters"] for s in stats],
+        "hvp_ms": round(avg_hvp_ms, 5),
+        "hvp_per_s": round(1e3 / avg_hvp_ms, 1),
+        "qp_per_s": round(statistics.mean(cells) / (avg_hvp_ms * 1e-3), 1),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": load_traffic(sc.name),
+                     "peak_kind": peak_kind, "kernel": "k_hvp",
+                     "algorithmic_bytes_per_launch": int(nbytes), "pct_of_8TBps": round(achieved / 8000.0, 4)},
+        "e2e": e2e,
+        "gpu_launches": int(sum(s.get("n_launches", 0) for s in stats)) or None,
+        "clocks": clocks,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(sc, args)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    ctx.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(ctx, sc, solver, stream, args):
+    """Same metric through the C ABI with host buffers: each step copies the particle state from
+    pinned host memory (H2D), steps, and reads the particle state back (D2H)."""
+    import torch
+    dt_ = torch.float32 if args.precision == 32 else torch.float64
+    host = [torch.from_numpy(np.ascontiguousarray(a)).to(dt_).pin_memory() for a in (sc.x, sc.v, sc.F, sc.G, sc.vol)]
+    mat = torch.from_numpy(np.ascontiguousarray(sc.mat)).pin_memory()
+    outs = [torch.empty((sc.n_particles, w), dtype=dt_).pin_memory() for w in (3, 3, 9, 9)]
+    s = 4 if args.precision == 32 else 8
+    h2d = sc.n_particles * (3 + 3 + 9 + 9 + 1) * s + sc.n_particles * 4
+    d2h = sc.n_particles * (3 + 3 + 9 + 9) * s
+    steps = max(1, min(args.steps, 3))
+    n_hvp_dofs = 0.0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ctx.set_particles(*host, mat)
+        st = ctx.step(sc.dt, solver)
+        ctx.get_particles(*outs)
+        n_free = ctx.counts.n_nodes  # upper bound refined below
+        n_hvp_dofs += st["n_hvp"]
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ctx.resample(sc.dt)
+    _, _, _, fr = ctx.get_nodes()
+    val = 3.0 * int(fr.sum()) * n_hvp_dofs / wall / 1e9
+    return {"value": round(val, 3), "unit": "GDOF/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": round(wall * 1e3 / steps, 3), "steps": steps}
+
+
+# ------------------------------------------------------------------------------------------------
+def oracle_window(sc, lo, size):
+    """A window of the scene (cells [lo, lo+size)^3) for the oracle: particles whose stencil can touch
+    it, grid origin shifted; interior outputs equal the full-scene values."""
+    import oracle
+    from paper_2602_07853_b200 import scenes
+    lo = np.asarray(lo)
+    x = sc.x.astype(np.float64)
+    cell = np.floor(x / sc.dx - 0.5).astype(np.int64)
+    keep = np.all((cell >= lo - 1) & (cell <= lo + size), axis=1)
+    sub = scenes.subset(sc, keep)
+    grid = oracle.Grid((size + 2,) * 3, sc.dx, tuple((lo - 1) * sc.dx))
+    un, S, prob, v0 = oracle.prepare(sub, grid, clip=True)
+    return grid, un, S, prob, v0
+
+
+def cpu_baseline(sc, args, budget_s=12.0):
+    """Oracle HVP (plain fp64 C, 1 thread) on a bounded window of the same workload."""
+    import oracle
+    lo, size = _window_for(sc)
+    grid, un, S, prob, v0 = oracle_window(sc, lo, size)
+    rng = np.random.default_rng(4)
+    act = (prob.m_i > 0)
+    u = rng.normal(size=v0.shape) * act[:, None]
+    n_free = int(prob.freed.sum())
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        prob.hvp(v0, u)
+        reps += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    t = (time.perf_counter() - t0) / reps
+    return {"value": round(3.0 * n_free / t / 1e9, 6), "unit": "GDOF/s", "cores": 1, "kind": "oracle",
+            "sample": f"{reps} oracle HVPs on the {size}^3-cell window at cells {list(map(int, lo))} of {sc.name} "
+                      f"({int((un.m_c > 0).sum())} quadrature points, {n_free} free nodes), {t * 1e3:.1f} ms each"}
+
+
+def _window_for(sc):
+    n = sc.n[0]
+    if sc.name.startswith("cfg4"):
+        return np.array([int(0.25 * n) - 12, int(0.35 * n) - 12, int(0.5 * n) - 12]), 24
+    if sc.name.startswith("cfg5"):
+        return np.array([int(0.5 * n) - 12, int(0.1 * n), int(0.5 * n) - 12]), 24
+    c = n // 2
+    return np.array([c - 12] * 3), 24
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    from paper_2602_07853_b200 import scenes
+    sc = scenes.by_name(args.config, args.precision)
+    import oracle
+    lo, size = _window_for(sc)
+    grid, un, S, prob, v0 = oracle_window(sc, lo, size)
+    rng = np.random.default_rng(4)
+    u = rng.normal(size=v0.shape) * (prob.m_i > 0)[:, None]
+    n_free = int(prob.freed.sum())
+    for _ in range(args.warmup):
+        prob.hvp(v0, u)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        prob.hvp(v0, u)
+    t = (time.perf_counter() - t0) / args.steps
+    val = 3.0 * n_free / t / 1e9
+    sample = (f"one oracle HVP per step on the {size}^3-cell window at cells {list(map(int, lo))} of {sc.name} "
+              f"({n_free} free nodes)")
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "HVP GDOF/s (matrix-free incremental-potential Hessian-vector product inside Newton-PCG)",
+        "value": round(val, 6), "unit": "GDOF/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (same seeded scene, windowed)",
+        "config": {"workload": f"{sc.name} window {size}^3 (oracle, 1 core)"},
+        "cpu_baseline": {"value": round(val, 6), "unit": "GDOF/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(val, 6), "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--precision", type=int, default=32)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

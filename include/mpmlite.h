@@ -1,0 +1,202 @@
+/*
+ * mpmlite.h — C ABI of the B200-native MPM Lite solve-time hot path (libmpmlite.so).
+ *
+ * The calls follow the paper's statement of one time step (Alg. 1):
+ *   set particles + materials (Alg. 1 "Require")
+ *   -> resample to quadrature: Unload (Alg. 2) + stretch bases (Alg. 3 lines 4-7)
+ *   -> energy / gradient / Hessian-vector product of the incremental potential
+ *      (Eq. incpot-rotfree; App. B)
+ *   -> Newton / Jacobi-PCG minimisation (Alg. 3 line 8; "matrix-free PCG" P:495)
+ *   -> transfer back to particles: Load (Alg. 4).
+ * Readings of passages the paper leaves open are listed in DESIGN.md §2 (amb-1..amb-21).
+ *
+ * Conventions
+ *  - Every call returns mpl_status (MPL_OK == 0).  No C++ exception crosses the ABI.  On error
+ *    mpl_last_error(ctx) returns a message naming the offending particle / cell where relevant.
+ *  - Precision: a context computes in fp32 or fp64 (mpl_config.precision = 32 | 64).  Every
+ *    floating-point buffer passed to or returned from a context is `float` or `double`
+ *    accordingly ("real" below).  Accumulations of dot products and energies are fp64.
+ *  - Memory: buffers may live on the host or on the device (any pointer cudaMemcpyDefault accepts:
+ *    pageable or pinned host memory, or device memory of the context's GPU).  The caller owns every
+ *    buffer; the library copies inputs and never retains caller pointers after a call returns.
+ *  - Streams: all work is ordered on the context's stream (its own stream unless mpl_set_stream);
+ *    every call is synchronous with respect to the host at return.
+ *  - Node-vector order ("canonical order"): the active nodes (m_i > 0) ordered by 4^3 node block
+ *    (blocks sorted by x-major block id (bx*NBy + by)*NBz + bz), then x-major within the block.
+ *    mpl_get_nodes exports the (i,j,k) of each entry; compare by key, never by position.
+ *  - Quadrature order: cells of the structural stencil set (every cell touched by some particle's
+ *    2^3 stencil), same block-major order; mpl_get_quadrature exports (i,j,k).
+ *  - Grid: N0 x N1 x N2 cells of size dx; node (i,j,k) at origin + dx (i,j,k); cell centre at
+ *    origin + dx (i+1/2, j+1/2, k+1/2).  Blocks are 4^3 cells.  Every particle's base
+ *    cell b = floor((x - origin)/dx - 1/2) must satisfy 0 <= b <= N-2 per axis (stencil inside the
+ *    grid), else MPL_ERR_OUT_OF_DOMAIN.
+ *  - Threading: one context per host thread.  A failing call leaves particle state unchanged;
+ *    after a failure inside mpl_resample / mpl_newton_step, mpl_resample is required again.
+ */
+#ifndef MPMLITE_H
+#define MPMLITE_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MPL_API __attribute__((visibility("default")))
+#else
+#define MPL_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mpl_ctx_s *mpl_ctx;
+
+typedef enum {
+    MPL_OK = 0,
+    MPL_ERR_INVALID_ARG = 1,
+    MPL_ERR_STATE = 2,            /* call order: e.g. mpl_hvp before mpl_linearize            */
+    MPL_ERR_OUT_OF_DOMAIN = 3,    /* a particle stencil leaves the grid                */
+    MPL_ERR_INVERTED = 4,         /* det F_p <= 0 at unload                    */
+    MPL_ERR_INVERSION_DOMAIN = 5, /* stress -> stretch inversion failed               */
+    MPL_ERR_NONFINITE = 6,        /* NaN / Inf produced                        */
+    MPL_ERR_OOM = 7,
+    MPL_ERR_CUDA = 8,
+    MPL_ERR_NCCL = 9,
+    MPL_ERR_UNSUPPORTED = 10
+} mpl_status;
+
+typedef struct {
+    int32_t n[3];     /* cells per axis                                   */
+    double dx;        /* cell size                                        */
+    double origin[3]; /* position of node (0,0,0)                         */
+} mpl_grid;
+
+typedef struct {
+    int32_t kind; /* 0 = StVK with Hencky strain (amb-1)   */
+    double E, nu; /* Young's modulus, Poisson ratio -> 3D Lame (amb-2) */
+    double rho;   /* density: m_p = rho * V_p                          */
+} mpl_material;
+
+typedef struct {
+    int32_t precision; /* 32 or 64                                              */
+    int32_t device;    /* CUDA device ordinal                                   */
+    int32_t rank, nranks; /* slab decomposition rank / size (1 process per GPU) */
+    const uint8_t *nccl_unique_id; /* 128 bytes from mpl_nccl_unique_id on rank 0; NULL if nranks==1 */
+} mpl_config;
+
+typedef struct {
+    double lo[3], hi[3]; /* nodes with lo <= x_i <= hi (all axes) are prescribed (amb-9) */
+    double velocity[3];  /* prescribed velocity                                          */
+} mpl_dirichlet_box;
+
+typedef struct {
+    int32_t newton_max;   /* Newton iteration cap (amb-6)                                */
+    int32_t cg_max;       /* PCG iteration cap per Newton iteration                      */
+    double newton_rtol;   /* stop when ||g_free|| <= newton_rtol ||g_free(v^0)||          */
+    double cg_rtol;       /* stop when ||r|| <= cg_rtol ||r_0|| (amb-7)                   */
+    double armijo_c;      /* Armijo constant (1e-4)                                      */
+    int32_t ls_max;       /* maximum halvings (30)                                       */
+    double ls_slack;      /* accept when Phi_new <= Phi + c a g.p + ls_slack |Phi| (amb-6) */
+    int32_t fixed_newton_iters;        /* >0: run exactly this many Newton iterations (parity replay) */
+    const int32_t *fixed_cg_iters;     /* NULL or per-Newton-iteration PCG counts (parity replay)    */
+    const int32_t *fixed_ls_halvings;  /* NULL or per-Newton-iteration halvings (parity replay)      */
+} mpl_solver_cfg;
+
+#define MPL_MAX_NEWTON_LOG 64
+typedef struct {
+    int32_t newton_iters, cg_iters_total, ls_halvings, converged, neg_curvature;
+    int32_t n_inverted_trials; /* line-search trials rejected for det(I + dt G) <= 0 (amb-21) */
+    double grad_norm0, grad_norm, energy;
+    int32_t cg_iters[MPL_MAX_NEWTON_LOG];
+    int32_t ls_iters[MPL_MAX_NEWTON_LOG];
+    int32_t n_hvp;        /* HVP launches in this call                                    */
+    double hvp_ms;        /* summed device time of those HVP launches (CUDA events)       */
+    double ms_phase[8];   /* 0 bin+sort, 1 P2Q+stretch, 2 C2N, 3 linearize, 4 PCG, 5 line search, 6 G2P, 7 total */
+} mpl_solve_stats;
+
+/* ---- context ------------------------------------------------------------------------------ */
+/* Create a context on cfg->device.  precision must be 32 or 64; nranks > 1 needs NCCL support. */
+MPL_API mpl_status mpl_create(const mpl_config *cfg, const mpl_grid *grid, mpl_ctx *out);
+MPL_API void mpl_destroy(mpl_ctx ctx);
+MPL_API const char *mpl_last_error(mpl_ctx ctx);
+/* Use an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL = own stream. */
+MPL_API mpl_status mpl_set_stream(mpl_ctx ctx, void *cuda_stream);
+/* Library version string and the compute capability it was built for ("sm_100a"). */
+MPL_API const char *mpl_version(void);
+/* rank 0 only: 128-byte NCCL unique id to broadcast to the other ranks before mpl_create. */
+MPL_API mpl_status mpl_nccl_unique_id(uint8_t out[128]);
+
+/* ---- scene -------------------------------------------------------------------------------- */
+/* n <= 8 materials; kind must be 0 (StVK-Hencky).  Requires mu > 0 and lam > -2 mu / 3. */
+MPL_API mpl_status mpl_set_materials(mpl_ctx ctx, int32_t n, const mpl_material *mats);
+/* gravity acceleration g (inertia target vhat = v^n + dt g, amb-4); default (0, -9.81, 0). */
+MPL_API mpl_status mpl_set_gravity(mpl_ctx ctx, const double g[3]);
+/* n <= 8 boxes; a node inside several boxes takes the first one's velocity. */
+MPL_API mpl_status mpl_set_dirichlet(mpl_ctx ctx, int32_t n, const mpl_dirichlet_box *boxes);
+/* Particle state (Alg. 1 "Require"): x (n*3), v (n*3), F (n*9 row-major), G (n*9 row-major,
+ * the APIC velocity gradient G_p), vol (n, rest volume V_p), mat (n, material id int32).
+ * on_device is advisory (any cudaMemcpyDefault pointer works). */
+MPL_API mpl_status mpl_set_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v, const void *F,
+                             const void *G, const void *vol, const int32_t *mat, int32_t on_device);
+/* Particle state in the order it was given to mpl_set_particles.  Any pointer may be NULL. */
+MPL_API mpl_status mpl_get_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G, int32_t on_device);
+MPL_API int64_t mpl_num_particles(mpl_ctx ctx);
+
+/* ---- resample: Alg. 2 + Alg. 3 lines 4-7 ------------------------ */
+/* Bins particles, activates blocks / cells / nodes, scatters particle state to the cell-centre
+ * quadrature (Eqs. p2c-mV, p2c-mv-affine, p2c-A-sum, vtau), gathers it to the nodes,
+ * reconstructs the rotation-free stretch S_{c,k} per material slot (Eqs. hencky-trace..sigmai),
+ * forms vhat = v^n + dt g and the Newton start v^0 (Dirichlet values on prescribed nodes).
+ * Outputs the counts of quadrature cells, active nodes and active 4^3 cell blocks (NULL allowed). */
+MPL_API mpl_status mpl_resample(mpl_ctx ctx, double dt, int64_t *n_cells, int64_t *n_nodes, int64_t *n_blocks);
+/* active nodes in canonical order: ijk (n_nodes*3 int32), lumped mass m_i, v^n_i (n_nodes*3),
+ * free flag (uint8: 1 = free DOF, 0 = prescribed).  NULL pointers are skipped. */
+MPL_API mpl_status mpl_get_nodes(mpl_ctx ctx, int32_t *ijk, void *m, void *v_n, uint8_t *free_dof);
+/* sorted x-major linear ids (bx*NBy + by)*NBz + bz of the 4^3 cell blocks touched by any particle
+ * stencil (structural; bit-exact).  n_blocks entries. */
+MPL_API mpl_status mpl_get_active_blocks(mpl_ctx ctx, int64_t *ids);
+/* per-particle base cell floor((x - origin)/dx - 1/2) (n*3 int32, input order; bit-exact). */
+MPL_API mpl_status mpl_get_particle_cells(mpl_ctx ctx, int32_t *base_ijk);
+/* quadrature state (n_cells entries, canonical cell order): ijk (n*3), m_c, v_c (n*3), G_c (n*9),
+ * and per material k: V_{c,k} (nmat*n), tau_{c,k} (nmat*n*9), S_{c,k} (nmat*n*9).  NULL skips. */
+MPL_API mpl_status mpl_get_quadrature(mpl_ctx ctx, int32_t *ijk, void *m_c, void *v_c, void *G_c, void *V_ck,
+                              void *tau_ck, void *S_ck);
+
+/* ---- the incremental potential ------------------------------- */
+/* Phi(v) = sum_i 1/2 m_i |v_i - vhat_i|^2 + sum_{c,k} V_ck psi_k((I + dt G_c(v)) S_ck)
+ * (Eq. incpot-rotfree).  v: n_nodes*3 canonical order.  phi = +inf if some
+ * det(I + dt G_c) <= 0 (amb-21). */
+MPL_API mpl_status mpl_energy(mpl_ctx ctx, const void *v, double *phi);
+/* g_i = dPhi/dv_i (unprojected; App. B Eq. residual with the sign of amb-3).  phi may be NULL. */
+MPL_API mpl_status mpl_gradient(mpl_ctx ctx, const void *v, void *g, double *phi);
+/* Linearise at v: caches the per-quadrature tangent K_c (45 numbers, the 9x9 symmetric
+ * d^2(sum_k V_ck psi_k)/dG^2) and the Jacobi diagonal.  Required before mpl_hvp. */
+MPL_API mpl_status mpl_linearize(mpl_ctx ctx, const void *v);
+/* Jacobi diagonal D_ia = (H)_{ia,ia} at the last linearisation point (n_nodes*3). */
+MPL_API mpl_status mpl_get_diag(mpl_ctx ctx, void *D);
+/* Matrix-free Hessian-vector product at the last linearisation point (unprojected):
+ * (Hu)_i = m_i u_i + sum_c (K_c : dG_c(u)) grad w_ic, dG_c(u) = sum_j u_j (x) grad w_jc. */
+MPL_API mpl_status mpl_hvp(mpl_ctx ctx, const void *u, void *Hu);
+/* The same product on device-resident canonical vectors, repeated `reps` times back to back;
+ * reports the mean device time per HVP launch (CUDA events on the context stream). */
+MPL_API mpl_status mpl_hvp_bench(mpl_ctx ctx, const void *u_dev, void *Hu_dev, int32_t reps, double *ms_per_hvp);
+
+/* ---- the implicit solve ---------------------------------------- */
+/* Newton with Jacobi-PCG and Armijo backtracking from v^0 (amb-6, amb-7, amb-8); stores v^{n+1}. */
+MPL_API mpl_status mpl_newton_step(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *stats);
+/* v^{n+1} after mpl_newton_step (or v^0 before it), n_nodes*3 canonical order. */
+MPL_API mpl_status mpl_get_velocity(mpl_ctx ctx, void *v);
+/* replace the current iterate (n_nodes*3 canonical order) — e.g. to restart from a given v. */
+MPL_API mpl_status mpl_set_velocity(mpl_ctx ctx, const void *v);
+
+/* ---- load ------------------------------------------------------------ */
+/* Alg. 4: v_c = sum w_ic v_i, G_c = sum v_i (x) grad w_ic (cells with m_c > 0); v_p = sum w_cp v_c,
+ * G_p = sum w_cp G_c (weights at x_p^n); x_p += dt v_p; F_p <- (I + dt G_p) F_p. */
+MPL_API mpl_status mpl_transfer_to_particles(mpl_ctx ctx, double dt);
+
+/* One full step: resample -> newton -> transfer (Alg. 1). */
+MPL_API mpl_status mpl_step(mpl_ctx ctx, double dt, const mpl_solver_cfg *cfg, mpl_solve_stats *stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPMLITE_H */

@@ -170,6 +170,28 @@ def base_cells(grid: Grid, x: np.ndarray) -> np.ndarray:
     return out
 
 
+def structural_cells(grid: Grid, base: np.ndarray) -> np.ndarray:
+    """C1: the union of every particle's 2^3 stencil (cells b + o, o in {0,1}^3), as sorted
+    x-major dense cell ids."""
+    base = np.asarray(base, np.int64)
+    n1, n2 = int(grid.n[1]), int(grid.n[2])
+    ids = []
+    for o in range(8):
+        c = base + np.array([(o >> 2) & 1, (o >> 1) & 1, o & 1])
+        ids.append((c[:, 0] * n1 + c[:, 1]) * n2 + c[:, 2])
+    return np.unique(np.concatenate(ids))
+
+
+def active_blocks(grid: Grid, base: np.ndarray) -> np.ndarray:
+    """C1: sorted x-major ids (bx*NBy + by)*NBz + bz of the 4^3 cell blocks holding a stencil cell."""
+    n1, n2 = int(grid.n[1]), int(grid.n[2])
+    ids = structural_cells(grid, base)
+    c = np.stack([ids // (n1 * n2), (ids // n2) % n1, ids % n2], 1)
+    nb = [(int(grid.n[a]) + 3) // 4 for a in range(3)]
+    b = c // 4
+    return np.unique((b[:, 0] * nb[1] + b[:, 1]) * nb[2] + b[:, 2])
+
+
 def q1_weights(f) -> np.ndarray:
     f = _f64(f)
     w = np.zeros(8)

@@ -1,0 +1,281 @@
+// k_load.cu — SURVEY §8(a) row a9: Load (Alg. 4).
+//   cells with m_c > 0: v_c = sum_i w_ic v_i (w_ic = 1/8), G_c = sum_i v_i (x) grad w_ic
+//   particles: v_p = sum_c w_cp v_c, G_p = sum_c w_cp G_c (w at x_p^n)                   (Eqs. vc2p, Gc2p)
+//              x_p += dt v_p ; F_p <- (I + dt G_p) F_p
+// plus the quadrature/particle export helpers of the C ABI.
+#include <cub/cub.cuh>
+
+#include "mpl_common.cuh"
+
+namespace {
+
+__device__ __forceinline__ int local_id(int lx, int ly, int lz) { return (lx * 4 + ly) * 4 + lz; }
+
+// per cell: v_c (vec4) and G_c (9) from the 5^3 node halo
+template <class T>
+__global__ void __launch_bounds__(128) k_n2c(GridP g, const int *__restrict__ nplus, const int *__restrict__ cstart,
+                                             const uint8_t *__restrict__ clocal, const int *__restrict__ hascells,
+                                             const T *__restrict__ q_m, const vec4<T> *__restrict__ v,
+                                             vec4<T> *__restrict__ vc, T *__restrict__ Gc) {
+    __shared__ vec4<T> vh[125];
+    const int t = blockIdx.x, tid = threadIdx.x;
+    if (!hascells[t]) return;
+    const int cs = cstart[t], nc = cstart[t + 1] - cs;
+    for (int h = tid; h < 125; h += blockDim.x) {
+        int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
+        int dp = ((hx >> 2) << 2) | ((hy >> 2) << 1) | (hz >> 2);
+        int tt = dp ? nplus[8 * t + dp] : t;
+        vh[h] = tt >= 0 ? v[(int64_t)tt * 64 + local_id(hx & 3, hy & 3, hz & 3)] : mk4<T>(0, 0, 0, 0);
+    }
+    __syncthreads();
+    if (tid >= nc) return;
+    const int64_t cc = cs + tid;
+    int l = clocal[cc];
+    vec4<T> vv = mk4<T>(0, 0, 0, 0);
+    T G[9];
+#pragma unroll
+    for (int a = 0; a < 9; a++) G[a] = T(0);
+    if (l != 0xFF && q_m[cc] != T(0)) {
+        int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+        const T q = T(0.25 * g.inv_dx);
+#pragma unroll
+        for (int o = 0; o < 8; o++) {
+            int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+            vec4<T> u = vh[((lx + ox) * 5 + ly + oy) * 5 + lz + oz];
+            T s0 = ox ? q : -q, s1 = oy ? q : -q, s2 = oz ? q : -q;
+            vv.x += T(0.125) * u.x; vv.y += T(0.125) * u.y; vv.z += T(0.125) * u.z;
+            G[0] += u.x * s0; G[1] += u.x * s1; G[2] += u.x * s2;
+            G[3] += u.y * s0; G[4] += u.y * s1; G[5] += u.y * s2;
+            G[6] += u.z * s0; G[7] += u.z * s1; G[8] += u.z * s2;
+        }
+    }
+    vc[cc] = vv;
+#pragma unroll
+    for (int a = 0; a < 9; a++) Gc[9 * cc + a] = G[a];
+}
+
+// per particle (sorted order): interpolate, advect, update F
+template <class T>
+__global__ void k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ skey, const int *__restrict__ nplus,
+                      const int *__restrict__ cellof, const vec4<T> *__restrict__ vc, const T *__restrict__ Gc,
+                      T *__restrict__ x, T *__restrict__ v, T *__restrict__ F, T *__restrict__ G) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= np) return;
+    const int key = skey[p];
+    const int t = key >> 6, l = key & 63;
+    const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+    T xp[3], f[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        xp[a] = x[3 * p + a];
+        T tt = (xp[a] - T(g.origin[a])) * T(g.inv_dx) - T(0.5);
+        f[a] = tt - floor(tt);
+    }
+    T vp[3] = {0, 0, 0}, Gp[9];
+#pragma unroll
+    for (int a = 0; a < 9; a++) Gp[a] = T(0);
+#pragma unroll
+    for (int o = 0; o < 8; o++) {
+        int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+        int cx = lx + ox, cy = ly + oy, cz = lz + oz;
+        int dp = ((cx >> 2) << 2) | ((cy >> 2) << 1) | (cz >> 2);
+        int tt = dp ? nplus[8 * t + dp] : t;
+        int cc = cellof[tt * 64 + local_id(cx & 3, cy & 3, cz & 3)];
+        T w = (ox ? f[0] : T(1) - f[0]) * (oy ? f[1] : T(1) - f[1]) * (oz ? f[2] : T(1) - f[2]);
+        vec4<T> c = vc[cc];
+        vp[0] += w * c.x; vp[1] += w * c.y; vp[2] += w * c.z;
+        const T *Gq = Gc + 9 * (int64_t)cc;
+#pragma unroll
+        for (int a = 0; a < 9; a++) Gp[a] += w * Gq[a];
+    }
+    const T dt = T(dt_);
+    T Fp[9], A[9], Fn[9];
+#pragma unroll
+    for (int a = 0; a < 9; a++) {
+        Fp[a] = F[9 * p + a];
+        A[a] = dt * Gp[a] + ((a % 4 == 0) ? T(1) : T(0));
+    }
+    mm3(A, Fp, Fn);
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        x[3 * p + a] = xp[a] + dt * vp[a];
+        v[3 * p + a] = vp[a];
+    }
+#pragma unroll
+    for (int a = 0; a < 9; a++) {
+        F[9 * p + a] = Fn[a];
+        G[9 * p + a] = Gp[a];
+    }
+}
+
+// sorted -> input order: out[id[p]] = in[p] (width w)
+template <class T>
+__global__ void k_unsort(int64_t np, int w, const int *__restrict__ id, const T *__restrict__ in, T *__restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= np * w) return;
+    int64_t p = i / w;
+    int a = (int)(i % w);
+    out[(int64_t)id[p] * w + a] = in[i];
+}
+
+// quadrature export: tau, S from the slot data (S = I + E)
+template <class T>
+__global__ void k_export_q(int64_t C, int nmat, GridP g, const int *__restrict__ coord, const int *__restrict__ cstart,
+                           int T_, const uint8_t *__restrict__ clocal, const int *__restrict__ ccanon,
+                           const T *__restrict__ q_m, const T *__restrict__ q_mv, const T *__restrict__ q_mG,
+                           const T *__restrict__ q_slot, int32_t *__restrict__ ijk, T *__restrict__ m_c,
+                           T *__restrict__ v_c, T *__restrict__ G_c, T *__restrict__ V_ck, T *__restrict__ tau_ck,
+                           T *__restrict__ S_ck, int64_t nout) {
+    int64_t cc = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (cc >= C) return;
+    int o = ccanon[cc];
+    if (o < 0) return;
+    // find tile by binary search on cstart
+    int lo = 0, hi = T_;
+    while (hi - lo > 1) {
+        int mid = (lo + hi) / 2;
+        if (cstart[mid] <= cc) lo = mid; else hi = mid;
+    }
+    int l = clocal[cc];
+    ijk[3 * o + 0] = coord[3 * lo] * 4 + (l >> 4);
+    ijk[3 * o + 1] = coord[3 * lo + 1] * 4 + ((l >> 2) & 3);
+    ijk[3 * o + 2] = coord[3 * lo + 2] * 4 + (l & 3);
+    T m = q_m[cc];
+    m_c[o] = m;
+    T im = m != T(0) ? T(1) / m : T(0);
+    for (int a = 0; a < 3; a++) v_c[3 * o + a] = q_mv[3 * cc + a] * im;
+    for (int a = 0; a < 9; a++) G_c[9 * o + a] = q_mG[9 * cc + a] * im;
+    const int sym[9] = {0, 3, 5, 3, 1, 4, 5, 4, 2};
+    for (int k = 0; k < nmat; k++) {
+        const T *sl = q_slot + (cc * nmat + k) * 16;
+        V_ck[(int64_t)k * nout + o] = sl[0];
+        for (int a = 0; a < 9; a++) {
+            tau_ck[((int64_t)k * nout + o) * 9 + a] = sl[7 + sym[a]];
+            S_ck[((int64_t)k * nout + o) * 9 + a] = sl[1 + sym[a]] + ((a % 4 == 0) ? T(1) : T(0));
+        }
+    }
+}
+
+__global__ void k_ccanon_flags(int64_t C, const uint8_t *__restrict__ clocal, int *__restrict__ act) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < C) act[i] = clocal[i] != 0xFF;
+}
+__global__ void k_ccanon_fix(int64_t C, const uint8_t *__restrict__ clocal, int *__restrict__ canon) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < C && clocal[i] == 0xFF) canon[i] = -1;
+}
+
+inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+}  // namespace
+
+template <class T>
+mpl_status g2p_impl(mpl_ctx ctx, double dt) {
+    cudaStream_t st = ctx->stream;
+    const int T_ = ctx->T;
+    const int c = ctx->cur;
+    if (T_)
+        k_n2c<T><<<T_, 128, 0, st>>>(ctx->grid, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,
+                                     (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p,
+                                     (const T *)ctx->q_m.p, (const vec4<T> *)ctx->n_v.p, (vec4<T> *)ctx->q_vc.p,
+                                     (T *)ctx->q_Gc.p);
+    if (ctx->np)
+        k_c2p<T><<<nblk(ctx->np, 256), 256, 0, st>>>(ctx->grid, dt, ctx->np, (const int *)ctx->pskey.p,
+                                                    (const int *)ctx->t_nplus.p, (const int *)ctx->t_cellof.p,
+                                                    (const vec4<T> *)ctx->q_vc.p, (const T *)ctx->q_Gc.p,
+                                                    (T *)ctx->px[c].p, (T *)ctx->pv.p, (T *)ctx->pF[c].p,
+                                                    (T *)ctx->pG.p);
+    MPL_CUDA(cudaGetLastError());
+    MPL_CUDA(cudaStreamSynchronize(st));
+    ctx->resampled = false;  // quadrature state is consumed
+    ctx->linearized = false;
+    ctx->solved = false;
+    return MPL_OK;
+}
+
+template <class T>
+mpl_status export_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G) {
+    cudaStream_t st = ctx->stream;
+    const int64_t np = ctx->np;
+    const int c = ctx->cur;
+    MPL_CHECK(ensure(ctx, ctx->io_stage2, (size_t)(np * 9 + 16) * sizeof(T)));
+    struct Item { void *dst; const void *src; int w; };
+    Item items[4] = {{x, ctx->px[c].p, 3}, {v, ctx->pv.p, 3}, {F, ctx->pF[c].p, 9}, {G, ctx->pG.p, 9}};
+    for (auto &it : items) {
+        if (!it.dst || !np) continue;
+        k_unsort<T><<<nblk(np * it.w, 256), 256, 0, st>>>(np, it.w, (const int *)ctx->pid[c].p, (const T *)it.src,
+                                                          (T *)ctx->io_stage2.p);
+        MPL_CUDA(cudaMemcpyAsync(it.dst, ctx->io_stage2.p, np * it.w * sizeof(T), cudaMemcpyDefault, st));
+    }
+    MPL_CUDA(cudaGetLastError());
+    MPL_CUDA(cudaStreamSynchronize(st));
+    return MPL_OK;
+}
+
+template <class T>
+mpl_status export_quadrature(mpl_ctx ctx, int32_t *ijk, void *m_c, void *v_c, void *G_c, void *V_ck, void *tau_ck,
+                             void *S_ck) {
+    cudaStream_t st = ctx->stream;
+    const int64_t C = ctx->C, n = ctx->n_cells_active;
+    const int nm = ctx->mats.nmat;
+    const size_t s = sizeof(T);
+    // canonical cell index = rank among non-padding compact cells
+    DevBuf act, canon, out;
+    auto cleanup = [&]() {
+        cudaFree(act.p);
+        cudaFree(canon.p);
+        cudaFree(out.p);
+    };
+    size_t nbytes_out = n * 3 * 4 + n * s * (1 + 3 + 9 + nm * (1 + 9 + 9)) + 256;
+    if (cudaMalloc(&act.p, C * 4 + 16) != cudaSuccess || cudaMalloc(&canon.p, C * 4 + 16) != cudaSuccess ||
+        cudaMalloc(&out.p, nbytes_out) != cudaSuccess) {
+        cleanup();
+        ctx->err = "out of device memory in export_quadrature";
+        return MPL_ERR_OOM;
+    }
+    if (C) {
+        k_ccanon_flags<<<nblk(C, 256), 256, 0, st>>>(C, (const uint8_t *)ctx->c_local.p, (int *)act.p);
+        size_t tmp = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp, (const int *)act.p, (int *)canon.p, (int)C, st);
+        void *tp = nullptr;
+        cudaMalloc(&tp, tmp + 16);
+        cub::DeviceScan::ExclusiveSum(tp, tmp, (const int *)act.p, (int *)canon.p, (int)C, st);
+        k_ccanon_fix<<<nblk(C, 256), 256, 0, st>>>(C, (const uint8_t *)ctx->c_local.p, (int *)canon.p);
+        char *o = (char *)out.p;
+        int32_t *d_ijk = (int32_t *)o; o += n * 3 * 4;
+        T *d_m = (T *)o; o += n * s;
+        T *d_v = (T *)o; o += n * 3 * s;
+        T *d_G = (T *)o; o += n * 9 * s;
+        T *d_V = (T *)o; o += n * nm * s;
+        T *d_tau = (T *)o; o += n * nm * 9 * s;
+        T *d_S = (T *)o;
+        k_export_q<T><<<nblk(C, 256), 256, 0, st>>>(C, nm, ctx->grid, (const int *)ctx->t_coord.p,
+                                                    (const int *)ctx->t_cstart.p, ctx->T, (const uint8_t *)ctx->c_local.p,
+                                                    (const int *)canon.p, (const T *)ctx->q_m.p, (const T *)ctx->q_mv.p,
+                                                    (const T *)ctx->q_mG.p, (const T *)ctx->q_slot.p, d_ijk, d_m, d_v, d_G,
+                                                    d_V, d_tau, d_S, n);
+        if (ijk) cudaMemcpyAsync(ijk, d_ijk, n * 3 * 4, cudaMemcpyDefault, st);
+        if (m_c) cudaMemcpyAsync(m_c, d_m, n * s, cudaMemcpyDefault, st);
+        if (v_c) cudaMemcpyAsync(v_c, d_v, n * 3 * s, cudaMemcpyDefault, st);
+        if (G_c) cudaMemcpyAsync(G_c, d_G, n * 9 * s, cudaMemcpyDefault, st);
+        if (V_ck) cudaMemcpyAsync(V_ck, d_V, n * nm * s, cudaMemcpyDefault, st);
+        if (tau_ck) cudaMemcpyAsync(tau_ck, d_tau, n * nm * 9 * s, cudaMemcpyDefault, st);
+        if (S_ck) cudaMemcpyAsync(S_ck, d_S, n * nm * 9 * s, cudaMemcpyDefault, st);
+        cudaStreamSynchronize(st);
+        cudaFree(tp);
+    }
+    cudaError_t e = cudaGetLastError();
+    cleanup();
+    if (e != cudaSuccess) {
+        ctx->err = std::string("CUDA error in export_quadrature: ") + cudaGetErrorString(e);
+        return MPL_ERR_CUDA;
+    }
+    return MPL_OK;
+}
+
+template mpl_status g2p_impl<float>(mpl_ctx, double);
+template mpl_status g2p_impl<double>(mpl_ctx, double);
+template mpl_status export_particles<float>(mpl_ctx, void *, void *, void *, void *);
+template mpl_status export_particles<double>(mpl_ctx, void *, void *, void *, void *);
+template mpl_status export_quadrature<float>(mpl_ctx, int32_t *, void *, void *, void *, void *, void *, void *);
+template mpl_status export_quadrature<double>(mpl_ctx, int32_t *, void *, void *, void *, void *, void *, void *);

@@ -1,0 +1,628 @@
+// k_resample.cu — SURVEY §8(a) rows a0-a4: binning + activation, particle sort, P2Q scatter
+// (as a race-free per-cell gather over base-cell buckets), stretch reconstruction, C2N gather.
+//
+// Paper: Alg. 2 Unload; Eqs. p2c-mV / p2c-mv-affine / p2c-A-sum;
+// Eq. vtau; C2N; stretch bases Alg. 3 lines 4-7 with the
+// StVK-Hencky closed form Eqs. hencky-trace / hencky-ei / hencky-sigmai.
+#include <cub/cub.cuh>
+
+#include "mpl_common.cuh"
+
+namespace {
+
+__device__ __forceinline__ int dense_id(const GridP &g, int bx, int by, int bz) {
+    return (bx * g.nb[1] + by) * g.nb[2] + bz;
+}
+__device__ __forceinline__ int local_id(int lx, int ly, int lz) { return (lx * 4 + ly) * 4 + lz; }
+
+// ---- a0: base cell, domain check, active cell blocks ------------------------------------------
+template <class T>
+__global__ void k_bin_flags(GridP g, int64_t np, const T *__restrict__ x, const int *__restrict__ pid,
+                            int *__restrict__ base, int *__restrict__ cflag, DevScalars *sc) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= np) return;
+    int b[3];
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        T t = (x[3 * p + a] - T(g.origin[a])) * T(g.inv_dx) - T(0.5);
+        T fb = floor(t);
+        b[a] = (int)fb;
+        ok = ok && (fb >= T(0)) && (b[a] <= g.n[a] - 2) && (t == t);
+    }
+    if (!ok) {
+        atomicMin(&sc->oob_particle, pid[p]);
+        base[p] = -1;
+        return;
+    }
+    base[p] = (b[0] << 20) | (b[1] << 10) | b[2];
+    int b0[3] = {b[0] >> 2, b[1] >> 2, b[2] >> 2}, b1[3] = {(b[0] + 1) >> 2, (b[1] + 1) >> 2, (b[2] + 1) >> 2};
+    for (int o = 0; o < 8; o++) {
+        int bx = (o & 4) ? b1[0] : b0[0], by = (o & 2) ? b1[1] : b0[1], bz = (o & 1) ? b1[2] : b0[2];
+        if (((o & 4) && b1[0] == b0[0]) || ((o & 2) && b1[1] == b0[1]) || ((o & 1) && b1[2] == b0[2])) continue;
+        int d = dense_id(g, bx, by, bz);
+        if (cflag[d] == 0) cflag[d] = 1;
+    }
+}
+
+// active node blocks = cell blocks dilated by +{0,1}^3; also counts active cell blocks
+__global__ void k_node_flags(GridP g, const int *__restrict__ cflag, int *__restrict__ nflag,
+                             unsigned long long *nblocks) {
+    int d = blockIdx.x * blockDim.x + threadIdx.x;
+    int N = g.nb[0] * g.nb[1] * g.nb[2];
+    if (d >= N || !cflag[d]) return;
+    atomicAdd(nblocks, 1ull);
+    int bz = d % g.nb[2], by = (d / g.nb[2]) % g.nb[1], bx = d / (g.nb[1] * g.nb[2]);
+    for (int o = 0; o < 8; o++) {
+        int x = bx + ((o >> 2) & 1), y = by + ((o >> 1) & 1), z = bz + (o & 1);
+        if (x < g.nb[0] && y < g.nb[1] && z < g.nb[2]) nflag[dense_id(g, x, y, z)] = 1;
+    }
+}
+
+// tile_of (exclusive scan of nflag) -> tile coords; tile_of[d] = -1 where inactive
+__global__ void k_tiles(GridP g, const int *__restrict__ nflag, int *__restrict__ tile_of, int *__restrict__ coord) {
+    int d = blockIdx.x * blockDim.x + threadIdx.x;
+    int N = g.nb[0] * g.nb[1] * g.nb[2];
+    if (d >= N) return;
+    if (nflag[d]) {
+        int t = tile_of[d];
+        coord[3 * t + 0] = d / (g.nb[1] * g.nb[2]);
+        coord[3 * t + 1] = (d / g.nb[2]) % g.nb[1];
+        coord[3 * t + 2] = d % g.nb[2];
+    } else {
+        tile_of[d] = -1;
+    }
+}
+
+__global__ void k_tile_nbrs(GridP g, int T, const int *__restrict__ coord, const int *__restrict__ tile_of,
+                            const int *__restrict__ cflag, int *__restrict__ nplus, int *__restrict__ nminus,
+                            int *__restrict__ hascells) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    int c[3] = {coord[3 * t], coord[3 * t + 1], coord[3 * t + 2]};
+    for (int o = 0; o < 8; o++) {
+        int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+        int x = c[0] + ox, y = c[1] + oy, z = c[2] + oz;
+        nplus[8 * t + o] = (x < g.nb[0] && y < g.nb[1] && z < g.nb[2]) ? tile_of[dense_id(g, x, y, z)] : -1;
+        x = c[0] - ox; y = c[1] - oy; z = c[2] - oz;
+        nminus[8 * t + o] = (x >= 0 && y >= 0 && z >= 0) ? tile_of[dense_id(g, x, y, z)] : -1;
+    }
+    hascells[t] = cflag[dense_id(g, c[0], c[1], c[2])];
+}
+
+// bucket key (tile*64 + local base cell) and rank inside the bucket
+__global__ void k_count(GridP g, int64_t np, const int *__restrict__ base, const int *__restrict__ tile_of,
+                        int *__restrict__ key, int *__restrict__ rank, int *__restrict__ bcount) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= np) return;
+    int b = base[p];
+    int bx = b >> 20, by = (b >> 10) & 1023, bz = b & 1023;
+    int t = tile_of[dense_id(g, bx >> 2, by >> 2, bz >> 2)];
+    int k = t * 64 + local_id(bx & 3, by & 3, bz & 3);
+    key[p] = k;
+    rank[p] = atomicAdd(&bcount[k], 1);
+}
+
+// ---- Kirchhoff stress of a particle, StVK-Hencky ------------------------
+// tau = mu log b + lam/2 tr(log b) I with log b from eig(b - I), b - I = H + H^T + H H^T, H = F - I
+template <class T>
+__device__ __forceinline__ void hencky_tau(const T F[9], T mu, T lam, T tau[6]) {
+    T H[9];
+#pragma unroll
+    for (int a = 0; a < 9; a++) H[a] = F[a] - ((a % 4 == 0) ? T(1) : T(0));
+    T B[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++)
+            B[3 * a + b] = H[3 * a + b] + H[3 * b + a] + H[3 * a] * H[3 * b] + H[3 * a + 1] * H[3 * b + 1] +
+                           H[3 * a + 2] * H[3 * b + 2];
+    T w[3], Q[9];
+    sym_eig3(B, w, Q);
+    T l0 = mlog1p(w[0]), l1 = mlog1p(w[1]), l2 = mlog1p(w[2]);
+    T tr = T(0.5) * lam * (l0 + l1 + l2);
+    T t0 = mu * l0 + tr, t1 = mu * l1 + tr, t2 = mu * l2 + tr;
+    // tau = Q diag(t) Q^T, packed xx yy zz xy yz xz
+    tau[0] = Q[0] * Q[0] * t0 + Q[1] * Q[1] * t1 + Q[2] * Q[2] * t2;
+    tau[1] = Q[3] * Q[3] * t0 + Q[4] * Q[4] * t1 + Q[5] * Q[5] * t2;
+    tau[2] = Q[6] * Q[6] * t0 + Q[7] * Q[7] * t1 + Q[8] * Q[8] * t2;
+    tau[3] = Q[0] * Q[3] * t0 + Q[1] * Q[4] * t1 + Q[2] * Q[5] * t2;
+    tau[4] = Q[3] * Q[6] * t0 + Q[4] * Q[7] * t1 + Q[5] * Q[8] * t2;
+    tau[5] = Q[0] * Q[6] * t0 + Q[1] * Q[7] * t1 + Q[2] * Q[8] * t2;
+}
+
+// ---- particle scatter into sorted order + P2Q record ------------------------------------------
+// record (24 reals): f(3) fraction in the base cell, m_p, a = m_p (v_p - dx G_p f) (3),
+// m_p G_p (9), V_p, V_p tau_p (6), material id (as real)
+constexpr int REC = 24;
+template <class T>
+__global__ void k_scatter(GridP g, MatP mp, int64_t np, const int *__restrict__ key, const int *__restrict__ rank,
+                          const int *__restrict__ bstart, const T *__restrict__ x, const T *__restrict__ v,
+                          const T *__restrict__ F, const T *__restrict__ G, const T *__restrict__ vol,
+                          const int *__restrict__ mat, const int *__restrict__ pid, T *__restrict__ xo,
+                          T *__restrict__ Fo, T *__restrict__ volo, int *__restrict__ mato, int *__restrict__ pido,
+                          int *__restrict__ keyo, T *__restrict__ rec, DevScalars *sc) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= np) return;
+    int k = key[p];
+    int64_t d = bstart[k] + rank[p];
+    T xp[3], vp[3], Fp[9], Gp[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++) { xp[a] = x[3 * p + a]; vp[a] = v[3 * p + a]; }
+#pragma unroll
+    for (int a = 0; a < 9; a++) { Fp[a] = F[9 * p + a]; Gp[a] = G[9 * p + a]; }
+    T Vp = vol[p];
+    int m = mat[p];
+    int id = pid[p];
+    if (det3(Fp) <= T(0)) atomicMin(&sc->inv_particle, id);
+    T mu = T(mp.mu[m]), lam = T(mp.lam[m]);
+    T mass = T(mp.rho[m]) * Vp;
+    T tau[6];
+    hencky_tau(Fp, mu, lam, tau);
+    T f[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        T t = (xp[a] - T(g.origin[a])) * T(g.inv_dx) - T(0.5);
+        f[a] = t - floor(t);
+    }
+    T dx = T(g.dx);
+    T *r = rec + d * REC;
+    r[0] = f[0]; r[1] = f[1]; r[2] = f[2];
+    r[3] = mass;
+#pragma unroll
+    for (int a = 0; a < 3; a++) r[4 + a] = mass * (vp[a] - dx * (Gp[3 * a] * f[0] + Gp[3 * a + 1] * f[1] + Gp[3 * a + 2] * f[2]));
+#pragma unroll
+    for (int a = 0; a < 9; a++) r[7 + a] = mass * Gp[a];
+    r[16] = Vp;
+#pragma unroll
+    for (int a = 0; a < 6; a++) r[17 + a] = Vp * tau[a];
+    r[23] = T(m);
+#pragma unroll
+    for (int a = 0; a < 3; a++) xo[3 * d + a] = xp[a];
+#pragma unroll
+    for (int a = 0; a < 9; a++) Fo[9 * d + a] = Fp[a];
+    volo[d] = Vp;
+    mato[d] = m;
+    pido[d] = id;
+    keyo[d] = k;
+}
+
+// ---- structural cell masks: cell active iff some base-cell bucket in cell - {0,1}^3 is non-empty
+__global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, const int *__restrict__ nminus,
+                            const int *__restrict__ bcount, unsigned long long *__restrict__ cmask,
+                            int *__restrict__ ccount, unsigned long long *ncells) {
+    int t = blockIdx.x;
+    int l = threadIdx.x;  // 64 threads
+    int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+    int cx = coord[3 * t] * 4 + lx, cy = coord[3 * t + 1] * 4 + ly, cz = coord[3 * t + 2] * 4 + lz;
+    bool act = false;
+    if (cx < g.n[0] && cy < g.n[1] && cz < g.n[2]) {
+        for (int o = 0; o < 8 && !act; o++) {
+            int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+            int bx = lx - ox, by = ly - oy, bz = lz - oz;
+            if (cx - ox < 0 || cy - oy < 0 || cz - oz < 0) continue;
+            int dm = ((bx < 0) << 2) | ((by < 0) << 1) | (bz < 0);
+            int tt = nminus[8 * t + dm];
+            if (tt < 0) continue;
+            if (bcount[tt * 64 + local_id(bx & 3, by & 3, bz & 3)] > 0) act = true;
+        }
+    }
+    unsigned int lo = __ballot_sync(0xffffffffu, act);
+    __shared__ unsigned int part[2];
+    if ((l & 31) == 0) part[l >> 5] = lo;
+    __syncthreads();
+    if (l == 0) {
+        unsigned long long m = (unsigned long long)part[0] | ((unsigned long long)part[1] << 32);
+        cmask[t] = m;
+        int c = __popcll(m);
+        ccount[t] = (c + 3) & ~3;
+        if (c) atomicAdd(ncells, (unsigned long long)c);
+    }
+}
+
+__global__ void k_cell_list(int T_, const unsigned long long *__restrict__ cmask, const int *__restrict__ cstart,
+                            uint8_t *__restrict__ clocal, int *__restrict__ cellof) {
+    int t = blockIdx.x;
+    int l = threadIdx.x;
+    unsigned long long m = cmask[t];
+    int cs = cstart[t], ce = cstart[t + 1];
+    if ((m >> l) & 1ull) {
+        int r = __popcll(m & ((1ull << l) - 1ull));
+        clocal[cs + r] = (uint8_t)l;
+        cellof[t * 64 + l] = cs + r;
+    } else {
+        cellof[t * 64 + l] = -1;
+    }
+    int c = __popcll(m);
+    if (cs + c + l < ce) clocal[cs + c + l] = 0xFF;
+}
+
+// ---- a2-a4: P2Q gather + normalisation + stretch reconstruction (per cell) --------------------
+// One thread per structural cell of the tile gathers the particles of its 8 base-cell buckets.
+// Outputs (compact cell cc): q_m = m_c, q_mv = (mv)_c, q_mG = (mG)_c (unnormalised contents),
+// per material slot k: [V_ck, E_ck = S_ck - I (6), tau_ck (6)] with S from Eqs. hencky-ei/sigmai.
+template <class T>
+__global__ void __launch_bounds__(64) k_p2q(GridP g, MatP mp, const int *__restrict__ coord,
+                                            const int *__restrict__ nminus, const int *__restrict__ bstart,
+                                            const int *__restrict__ cellof, const T *__restrict__ rec,
+                                            T *__restrict__ q_m, T *__restrict__ q_mv, T *__restrict__ q_mG,
+                                            T *__restrict__ q_slot) {
+    int t = blockIdx.x;
+    int l = threadIdx.x;
+    int cc = cellof[t * 64 + l];
+    if (cc < 0) return;
+    int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+    int cx = coord[3 * t] * 4 + lx, cy = coord[3 * t + 1] * 4 + ly, cz = coord[3 * t + 2] * 4 + lz;
+    const int nmat = mp.nmat;
+    T m = 0, mv[3] = {0, 0, 0}, mG[9];
+#pragma unroll
+    for (int a = 0; a < 9; a++) mG[a] = 0;
+    T V[MPL_MAXMAT], Vt[MPL_MAXMAT][6];
+#pragma unroll
+    for (int k = 0; k < MPL_MAXMAT; k++) {
+        V[k] = 0;
+#pragma unroll
+        for (int a = 0; a < 6; a++) Vt[k][a] = 0;
+    }
+    const T dx = T(g.dx);
+    for (int o = 0; o < 8; o++) {
+        int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+        if (cx - ox < 0 || cy - oy < 0 || cz - oz < 0) continue;
+        int bx = lx - ox, by = ly - oy, bz = lz - oz;
+        int dm = ((bx < 0) << 2) | ((by < 0) << 1) | (bz < 0);
+        int tt = nminus[8 * t + dm];
+        if (tt < 0) continue;
+        int kk = tt * 64 + local_id(bx & 3, by & 3, bz & 3);
+        int s = bstart[kk], e = bstart[kk + 1];
+        for (int p = s; p < e; p++) {
+            const T *r = rec + (int64_t)p * REC;
+            // cell = base + o  =>  w = prod_a (o_a ? f_a : 1 - f_a)
+            T w = (ox ? r[0] : T(1) - r[0]) * (oy ? r[1] : T(1) - r[1]) * (oz ? r[2] : T(1) - r[2]);
+            T mass = r[3];
+            m += w * mass;
+            // m (v + G (x_c - x_p)) = a + dx (mG) o   (x_c - x_p = dx (o - f))
+            mv[0] += w * (r[4] + dx * ((ox ? r[7] : T(0)) + (oy ? r[8] : T(0)) + (oz ? r[9] : T(0))));
+            mv[1] += w * (r[5] + dx * ((ox ? r[10] : T(0)) + (oy ? r[11] : T(0)) + (oz ? r[12] : T(0))));
+            mv[2] += w * (r[6] + dx * ((ox ? r[13] : T(0)) + (oy ? r[14] : T(0)) + (oz ? r[15] : T(0))));
+#pragma unroll
+            for (int a = 0; a < 9; a++) mG[a] += w * r[7 + a];
+            int k = (int)r[23];
+#pragma unroll
+            for (int q = 0; q < MPL_MAXMAT; q++) {
+                if (q == k) {
+                    V[q] += w * r[16];
+#pragma unroll
+                    for (int a = 0; a < 6; a++) Vt[q][a] += w * r[17 + a];
+                }
+            }
+        }
+    }
+    q_m[cc] = m;
+#pragma unroll
+    for (int a = 0; a < 3; a++) q_mv[3 * (int64_t)cc + a] = mv[a];
+#pragma unroll
+    for (int a = 0; a < 9; a++) q_mG[9 * (int64_t)cc + a] = mG[a];
+#pragma unroll
+    for (int k = 0; k < MPL_MAXMAT; k++) {
+        if (k >= nmat) break;
+        T *sl = q_slot + ((int64_t)cc * nmat + k) * 16;
+        T tau[6] = {0, 0, 0, 0, 0, 0};
+        T E[6] = {0, 0, 0, 0, 0, 0};
+        if (V[k] != T(0)) {
+            T iv = T(1) / V[k];
+#pragma unroll
+            for (int a = 0; a < 6; a++) tau[a] = Vt[k][a] * iv;  // Eq. vtau normalisation
+            T mu = T(mp.mu[k]), lam = T(mp.lam[k]);
+            T A[9] = {tau[0], tau[3], tau[5], tau[3], tau[1], tau[4], tau[5], tau[4], tau[2]};
+            T w[3], U[9];
+            sym_eig3(A, w, U);
+            T s = (w[0] + w[1] + w[2]) / (T(2) * mu + T(3) * lam);  // Eq. hencky-trace
+            T em[3];
+#pragma unroll
+            for (int i = 0; i < 3; i++) em[i] = mexpm1((w[i] - lam * s) / (T(2) * mu));  // sigma_i - 1
+            E[0] = U[0] * U[0] * em[0] + U[1] * U[1] * em[1] + U[2] * U[2] * em[2];
+            E[1] = U[3] * U[3] * em[0] + U[4] * U[4] * em[1] + U[5] * U[5] * em[2];
+            E[2] = U[6] * U[6] * em[0] + U[7] * U[7] * em[1] + U[8] * U[8] * em[2];
+            E[3] = U[0] * U[3] * em[0] + U[1] * U[4] * em[1] + U[2] * U[5] * em[2];
+            E[4] = U[3] * U[6] * em[0] + U[4] * U[7] * em[1] + U[5] * U[8] * em[2];
+            E[5] = U[0] * U[6] * em[0] + U[1] * U[7] * em[1] + U[2] * U[8] * em[2];
+        }
+        sl[0] = V[k];
+#pragma unroll
+        for (int a = 0; a < 6; a++) { sl[1 + a] = E[a]; sl[7 + a] = tau[a]; }
+        sl[13] = sl[14] = sl[15] = T(0);
+    }
+}
+
+// ---- a3: C2N gather (Alg. 2 lines 16-22) + Newton target and Dirichlet sets ----------
+template <class T>
+__global__ void __launch_bounds__(64) k_c2n(GridP g, BoxP bx, double dt, double gx, double gy, double gz,
+                                            const int *__restrict__ coord, const int *__restrict__ nminus,
+                                            const int *__restrict__ cellof, const T *__restrict__ q_m,
+                                            const T *__restrict__ q_mv, const T *__restrict__ q_mG,
+                                            T *__restrict__ n_mass, uint8_t *__restrict__ n_flag,
+                                            vec4<T> *__restrict__ n_vn, vec4<T> *__restrict__ n_vhat,
+                                            vec4<T> *__restrict__ n_v) {
+    int t = blockIdx.x;
+    int l = threadIdx.x;
+    int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+    int ix = coord[3 * t] * 4 + lx, iy = coord[3 * t + 1] * 4 + ly, iz = coord[3 * t + 2] * 4 + lz;
+    T m = 0, mv[3] = {0, 0, 0};
+    const T hdx = T(0.5 * g.dx);
+    for (int o = 0; o < 8; o++) {
+        int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+        int cx = ix - ox, cy = iy - oy, cz = iz - oz;  // node = cell + o
+        if (cx < 0 || cy < 0 || cz < 0 || cx >= g.n[0] || cy >= g.n[1] || cz >= g.n[2]) continue;
+        int bx_ = lx - ox, by_ = ly - oy, bz_ = lz - oz;
+        int dm = ((bx_ < 0) << 2) | ((by_ < 0) << 1) | (bz_ < 0);
+        int tt = nminus[8 * t + dm];
+        if (tt < 0) continue;
+        int cc = cellof[tt * 64 + local_id(bx_ & 3, by_ & 3, bz_ & 3)];
+        if (cc < 0) continue;
+        T mc = q_m[cc];
+        if (mc == T(0)) continue;
+        // x_i - x_c = dx (o - 1/2)
+        T d0 = ox ? hdx : -hdx, d1 = oy ? hdx : -hdx, d2 = oz ? hdx : -hdx;
+        const T *G = q_mG + 9 * (int64_t)cc;
+        m += T(0.125) * mc;
+        mv[0] += T(0.125) * (q_mv[3 * (int64_t)cc + 0] + G[0] * d0 + G[1] * d1 + G[2] * d2);
+        mv[1] += T(0.125) * (q_mv[3 * (int64_t)cc + 1] + G[3] * d0 + G[4] * d1 + G[5] * d2);
+        mv[2] += T(0.125) * (q_mv[3 * (int64_t)cc + 2] + G[6] * d0 + G[7] * d1 + G[8] * d2);
+    }
+    int64_t nidx = (int64_t)t * 64 + l;
+    vec4<T> vn = mk4<T>(0, 0, 0, 0), vh = mk4<T>(0, 0, 0, 0), v0 = mk4<T>(0, 0, 0, 0);
+    uint8_t flag = 0;
+    if (m > T(0)) {
+        T im = T(1) / m;
+        vn = mk4<T>(mv[0] * im, mv[1] * im, mv[2] * im, 0);
+        vh = mk4<T>(vn.x + T(dt * gx), vn.y + T(dt * gy), vn.z + T(dt * gz), m);
+        flag = 1;
+        v0 = mk4<T>(vh.x, vh.y, vh.z, 0);
+        double xi[3] = {g.origin[0] + g.dx * ix, g.origin[1] + g.dx * iy, g.origin[2] + g.dx * iz};
+        for (int b = 0; b < bx.nbox; b++) {
+            bool in = true;
+#pragma unroll
+            for (int a = 0; a < 3; a++) in = in && (xi[a] >= bx.lo[b][a]) && (xi[a] <= bx.hi[b][a]);
+            if (in) {
+                flag |= 2;
+                v0 = mk4<T>(T(bx.vel[b][0]), T(bx.vel[b][1]), T(bx.vel[b][2]), 0);
+                break;
+            }
+        }
+    }
+    n_mass[nidx] = m;
+    n_flag[nidx] = flag;
+    n_vn[nidx] = vn;
+    n_vhat[nidx] = vh;
+    n_v[nidx] = v0;
+}
+
+__global__ void k_node_active(int64_t N, const uint8_t *__restrict__ flag, int *__restrict__ act) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < N) act[i] = flag[i] & 1;
+}
+__global__ void k_node_canon(int64_t N, const uint8_t *__restrict__ flag, int *__restrict__ canon,
+                             int *__restrict__ list) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    if (flag[i] & 1) {
+        list[canon[i]] = (int)i;
+    } else {
+        canon[i] = -1;
+    }
+}
+
+__global__ void k_iota(int64_t n, int *a) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) a[i] = (int)i;
+}
+
+inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+template <class I>
+mpl_status exclusive_scan(mpl_ctx ctx, const I *in, I *out, int64_t n) {
+    size_t tmp = 0;
+    MPL_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int)n, ctx->stream));
+    MPL_CHECK(ensure(ctx, ctx->scan_tmp, tmp + 256));
+    MPL_CUDA(cub::DeviceScan::ExclusiveSum(ctx->scan_tmp.p, tmp, in, out, (int)n, ctx->stream));
+    return MPL_OK;
+}
+
+}  // namespace
+
+// =============================================================================================
+// host orchestration
+// =============================================================================================
+template <class T>
+mpl_status import_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v, const void *F, const void *G,
+                            const void *vol, const int32_t *mat) {
+    ctx->np = n;
+    ctx->cur = 0;
+    size_t s = sizeof(T);
+    MPL_CHECK(ensure(ctx, ctx->px[0], n * 3 * s));
+    MPL_CHECK(ensure(ctx, ctx->px[1], n * 3 * s));
+    MPL_CHECK(ensure(ctx, ctx->pF[0], n * 9 * s));
+    MPL_CHECK(ensure(ctx, ctx->pF[1], n * 9 * s));
+    MPL_CHECK(ensure(ctx, ctx->pv, n * 3 * s));
+    MPL_CHECK(ensure(ctx, ctx->pG, n * 9 * s));
+    for (int i = 0; i < 2; i++) {
+        MPL_CHECK(ensure(ctx, ctx->pvol[i], n * s));
+        MPL_CHECK(ensure(ctx, ctx->pmat[i], n * 4));
+        MPL_CHECK(ensure(ctx, ctx->pid[i], n * 4));
+    }
+    MPL_CHECK(ensure(ctx, ctx->pkey, n * 4));
+    MPL_CHECK(ensure(ctx, ctx->prank, n * 4));
+    MPL_CHECK(ensure(ctx, ctx->pbase, n * 4));
+    MPL_CHECK(ensure(ctx, ctx->prec, n * REC * s));
+    cudaStream_t st = ctx->stream;
+    MPL_CUDA(cudaMemcpyAsync(ctx->px[0].p, x, n * 3 * s, cudaMemcpyDefault, st));
+    MPL_CUDA(cudaMemcpyAsync(ctx->pv.p, v, n * 3 * s, cudaMemcpyDefault, st));
+    MPL_CUDA(cudaMemcpyAsync(ctx->pF[0].p, F, n * 9 * s, cudaMemcpyDefault, st));
+    MPL_CUDA(cudaMemcpyAsync(ctx->pG.p, G, n * 9 * s, cudaMemcpyDefault, st));
+    MPL_CUDA(cudaMemcpyAsync(ctx->pvol[0].p, vol, n * s, cudaMemcpyDefault, st));
+    MPL_CUDA(cudaMemcpyAsync(ctx->pmat[0].p, mat, n * 4, cudaMemcpyDefault, st));
+    if (n) k_iota<<<nblk(n, 256), 256, 0, st>>>(n, (int *)ctx->pid[0].p);
+    MPL_CUDA(cudaGetLastError());
+    MPL_CUDA(cudaStreamSynchronize(st));
+    return MPL_OK;
+}
+
+template <class T>
+mpl_status resample_impl(mpl_ctx ctx, double dt) {
+    cudaStream_t st = ctx->stream;
+    const GridP &g = ctx->grid;
+    const int64_t np = ctx->np;
+    const int N = g.nb[0] * g.nb[1] * g.nb[2];
+    ctx->dense_n = N;
+    ctx->dt = dt;
+    int c = ctx->cur, nx = 1 - c;
+    DevScalars *sc = (DevScalars *)ctx->scalars.p;
+    // reset error slots
+    {
+        DevScalars h{};
+        h.oob_particle = 0x7fffffff;
+        h.inv_particle = 0x7fffffff;
+        h.cg_done_iter = -1;
+        MPL_CUDA(cudaMemcpyAsync(sc, &h, sizeof h, cudaMemcpyHostToDevice, st));
+    }
+    MPL_CHECK(ensure(ctx, ctx->cflag, (size_t)N * 4));
+    MPL_CHECK(ensure(ctx, ctx->nflag, (size_t)N * 4));
+    MPL_CHECK(ensure(ctx, ctx->tile_of, (size_t)(N + 1) * 4));
+    MPL_CUDA(cudaMemsetAsync(ctx->cflag.p, 0, (size_t)N * 4, st));
+    MPL_CUDA(cudaMemsetAsync(ctx->nflag.p, 0, (size_t)N * 4, st));
+    unsigned long long *counters = (unsigned long long *)((char *)ctx->scalars.p + 256);
+    MPL_CUDA(cudaMemsetAsync(counters, 0, 64, st));
+
+    // a0: base cells + active cell blocks
+    if (np) k_bin_flags<T><<<nblk(np, 256), 256, 0, st>>>(g, np, (const T *)ctx->px[c].p, (const int *)ctx->pid[c].p,
+                                                         (int *)ctx->pbase.p, (int *)ctx->cflag.p, sc);
+    k_node_flags<<<nblk(N, 256), 256, 0, st>>>(g, (const int *)ctx->cflag.p, (int *)ctx->nflag.p, counters + 0);
+    MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->nflag.p, (int *)ctx->tile_of.p, N + 0));
+    // fetch error flags + tile count (one sync)
+    DevScalars hs;
+    int last_tile = 0, last_flag = 0;
+    MPL_CUDA(cudaMemcpyAsync(&hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
+    MPL_CUDA(cudaMemcpyAsync(&last_tile, (int *)ctx->tile_of.p + (N - 1), 4, cudaMemcpyDeviceToHost, st));
+    MPL_CUDA(cudaMemcpyAsync(&last_flag, (int *)ctx->nflag.p + (N - 1), 4, cudaMemcpyDeviceToHost, st));
+    unsigned long long nblocks = 0;
+    MPL_CUDA(cudaMemcpyAsync(&nblocks, counters + 0, 8, cudaMemcpyDeviceToHost, st));
+    MPL_CUDA(cudaStreamSynchronize(st));
+    if (hs.oob_particle != 0x7fffffff) {
+        ctx->err = "particle " + std::to_string(hs.oob_particle) +
+                   " is out of the domain: its base cell must satisfy 0 <= b <= N-2 on every axis";
+        return MPL_ERR_OUT_OF_DOMAIN;
+    }
+    const int T_ = last_tile + last_flag;
+    ctx->T = T_;
+    ctx->n_blocks_active = (int64_t)nblocks;
+    // tiles
+    MPL_CHECK(ensure(ctx, ctx->t_coord, (size_t)T_ * 12 + 16));
+    MPL_CHECK(ensure(ctx, ctx->t_nplus, (size_t)T_ * 32 + 16));
+    MPL_CHECK(ensure(ctx, ctx->t_nminus, (size_t)T_ * 32 + 16));
+    MPL_CHECK(ensure(ctx, ctx->t_hascells, (size_t)T_ * 4 + 16));
+    MPL_CHECK(ensure(ctx, ctx->t_cmask, (size_t)T_ * 8 + 16));
+    MPL_CHECK(ensure(ctx, ctx->t_cstart, (size_t)(T_ + 1) * 4 + 16));
+    MPL_CHECK(ensure(ctx, ctx->t_bcount, ((size_t)T_ * 64 + 1) * 4 + 16));
+    MPL_CHECK(ensure(ctx, ctx->t_bstart, ((size_t)T_ * 64 + 1) * 4 + 16));
+    MPL_CHECK(ensure(ctx, ctx->t_cellof, (size_t)T_ * 64 * 4 + 16));
+    k_tiles<<<nblk(N, 256), 256, 0, st>>>(g, (const int *)ctx->nflag.p, (int *)ctx->tile_of.p, (int *)ctx->t_coord.p);
+    if (T_) k_tile_nbrs<<<nblk(T_, 128), 128, 0, st>>>(g, T_, (const int *)ctx->t_coord.p, (const int *)ctx->tile_of.p,
+                                                     (const int *)ctx->cflag.p, (int *)ctx->t_nplus.p,
+                                                     (int *)ctx->t_nminus.p, (int *)ctx->t_hascells.p);
+    // particle buckets: key = tile*64 + local base cell; counting sort
+    MPL_CUDA(cudaMemsetAsync(ctx->t_bcount.p, 0, ((size_t)T_ * 64 + 1) * 4, st));
+    if (np) k_count<<<nblk(np, 256), 256, 0, st>>>(g, np, (const int *)ctx->pbase.p, (const int *)ctx->tile_of.p,
+                                                  (int *)ctx->pkey.p, (int *)ctx->prank.p, (int *)ctx->t_bcount.p);
+    MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_bcount.p, (int *)ctx->t_bstart.p, (int64_t)T_ * 64 + 1));
+    // scatter into sorted order + records
+    MPL_CHECK(ensure(ctx, ctx->pskey, (size_t)np * 4 + 16));
+    if (np)
+        k_scatter<T><<<nblk(np, 256), 256, 0, st>>>(
+            g, ctx->mats, np, (const int *)ctx->pkey.p, (const int *)ctx->prank.p, (const int *)ctx->t_bstart.p,
+            (const T *)ctx->px[c].p, (const T *)ctx->pv.p, (const T *)ctx->pF[c].p, (const T *)ctx->pG.p,
+            (const T *)ctx->pvol[c].p, (const int *)ctx->pmat[c].p, (const int *)ctx->pid[c].p, (T *)ctx->px[nx].p,
+            (T *)ctx->pF[nx].p, (T *)ctx->pvol[nx].p, (int *)ctx->pmat[nx].p, (int *)ctx->pid[nx].p,
+            (int *)ctx->pskey.p, (T *)ctx->prec.p, sc);
+    ctx->cur = nx;
+    // structural cells: masks, padded counts, compact offsets
+    MPL_CHECK(ensure(ctx, ctx->t_ccount, (size_t)(T_ + 1) * 4 + 16));
+    MPL_CUDA(cudaMemsetAsync(ctx->t_ccount.p, 0, (size_t)(T_ + 1) * 4, st));
+    if (T_) k_cell_mask<<<T_, 64, 0, st>>>(g, T_, (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p,
+                                          (const int *)ctx->t_bcount.p, (unsigned long long *)ctx->t_cmask.p,
+                                          (int *)ctx->t_ccount.p, counters + 1);
+    MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_ccount.p, (int *)ctx->t_cstart.p, (int64_t)T_ + 1));
+    int Cpad = 0;
+    unsigned long long ncells = 0;
+    MPL_CUDA(cudaMemcpyAsync(&Cpad, (int *)ctx->t_cstart.p + T_, 4, cudaMemcpyDeviceToHost, st));
+    MPL_CUDA(cudaMemcpyAsync(&ncells, counters + 1, 8, cudaMemcpyDeviceToHost, st));
+    MPL_CUDA(cudaMemcpyAsync(&hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
+    MPL_CUDA(cudaStreamSynchronize(st));
+    if (hs.inv_particle != 0x7fffffff) {
+        ctx->err = "particle " + std::to_string(hs.inv_particle) + " has det F_p <= 0 (inverted element)";
+        ctx->cur = c;  // particle state unchanged
+        return MPL_ERR_INVERTED;
+    }
+    ctx->C = Cpad;
+    ctx->n_cells_active = (int64_t)ncells;
+    const int nm = ctx->mats.nmat;
+    const size_t C = (size_t)Cpad + 4;
+    size_t s = sizeof(T);
+    MPL_CHECK(ensure(ctx, ctx->c_local, C));
+    MPL_CHECK(ensure(ctx, ctx->q_m, C * s));
+    MPL_CHECK(ensure(ctx, ctx->q_mv, C * 3 * s));
+    MPL_CHECK(ensure(ctx, ctx->q_mG, C * 9 * s));
+    MPL_CHECK(ensure(ctx, ctx->q_slot, C * nm * 16 * s));
+    MPL_CHECK(ensure(ctx, ctx->q_vc, C * 4 * s));
+    MPL_CHECK(ensure(ctx, ctx->q_Gc, C * 9 * s));
+    MPL_CHECK(ensure(ctx, ctx->K, C * 45 * s + 256));
+    if (T_) {
+        k_cell_list<<<T_, 64, 0, st>>>(T_, (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_cstart.p,
+                                       (uint8_t *)ctx->c_local.p, (int *)ctx->t_cellof.p);
+        k_p2q<T><<<T_, 64, 0, st>>>(g, ctx->mats, (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p,
+                                    (const int *)ctx->t_bstart.p, (const int *)ctx->t_cellof.p, (const T *)ctx->prec.p,
+                                    (T *)ctx->q_m.p, (T *)ctx->q_mv.p, (T *)ctx->q_mG.p, (T *)ctx->q_slot.p);
+    }
+    // nodes
+    const size_t NN = (size_t)T_ * 64 + 64;
+    MPL_CHECK(ensure(ctx, ctx->n_mass, NN * s));
+    MPL_CHECK(ensure(ctx, ctx->n_flag, NN));
+    DevBuf *vecs[] = {&ctx->n_vn, &ctx->n_vhat, &ctx->n_v, &ctx->n_vt, &ctx->n_g, &ctx->n_diag,
+                      &ctx->n_x, &ctx->n_r, &ctx->n_p, &ctx->n_Hp, &ctx->n_u, &ctx->n_u2};
+    for (DevBuf *b : vecs) MPL_CHECK(ensure(ctx, *b, NN * 4 * s));
+    MPL_CHECK(ensure(ctx, ctx->n_act, NN * 4));
+    MPL_CHECK(ensure(ctx, ctx->n_canon, NN * 4));
+    MPL_CHECK(ensure(ctx, ctx->n_list, NN * 4));
+    if (T_)
+        k_c2n<T><<<T_, 64, 0, st>>>(g, ctx->boxes, dt, ctx->gravity[0], ctx->gravity[1], ctx->gravity[2],
+                                    (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p,
+                                    (const int *)ctx->t_cellof.p, (const T *)ctx->q_m.p, (const T *)ctx->q_mv.p,
+                                    (const T *)ctx->q_mG.p, (T *)ctx->n_mass.p, (uint8_t *)ctx->n_flag.p,
+                                    (vec4<T> *)ctx->n_vn.p, (vec4<T> *)ctx->n_vhat.p, (vec4<T> *)ctx->n_v.p);
+    const int64_t NT = (int64_t)T_ * 64;
+    int nact = 0;
+    if (NT) {
+        k_node_active<<<nblk(NT, 256), 256, 0, st>>>(NT, (const uint8_t *)ctx->n_flag.p, (int *)ctx->n_act.p);
+        MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->n_act.p, (int *)ctx->n_canon.p, NT));
+        int lc = 0, la = 0;  // read before k_node_canon rewrites inactive entries (stream order)
+        MPL_CUDA(cudaMemcpyAsync(&lc, (int *)ctx->n_canon.p + (NT - 1), 4, cudaMemcpyDeviceToHost, st));
+        MPL_CUDA(cudaMemcpyAsync(&la, (int *)ctx->n_act.p + (NT - 1), 4, cudaMemcpyDeviceToHost, st));
+        k_node_canon<<<nblk(NT, 256), 256, 0, st>>>(NT, (const uint8_t *)ctx->n_flag.p, (int *)ctx->n_canon.p,
+                                                    (int *)ctx->n_list.p);
+        MPL_CUDA(cudaStreamSynchronize(st));
+        nact = lc + la;
+    }
+    ctx->n_nodes_active = nact;
+    MPL_CUDA(cudaGetLastError());
+    MPL_CUDA(cudaStreamSynchronize(st));
+    ctx->resampled = true;
+    ctx->linearized = false;
+    ctx->solved = false;
+    return MPL_OK;
+}
+
+template mpl_status import_particles<float>(mpl_ctx, int64_t, const void *, const void *, const void *,
+                                            const void *, const void *, const int32_t *);
+template mpl_status import_particles<double>(mpl_ctx, int64_t, const void *, const void *, const void *,
+                                             const void *, const void *, const int32_t *);
+template mpl_status resample_impl<float>(mpl_ctx, double);
+template mpl_status resample_impl<double>(mpl_ctx, double);

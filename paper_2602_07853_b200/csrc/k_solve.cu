@@ -1,0 +1,827 @@
+// k_solve.cu — SURVEY §8(a) rows a5-a8: linearisation (energy / gradient / cached tangent /
+// Jacobi diagonal), the matrix-free HVP, Jacobi-PCG vector kernels and the Newton driver.
+//
+// Paper: incremental potential Eq. incpot-rotfree, trial F_c(v) = (I + dt G_c(v)) S_c
+// (Eq. Ftrial-rotfree, Eq. rotfree-def), StVK-Hencky energy (Eq. hencky-energy
+// P:192-195), gradient / Hessian of App. B, G_c = sum_i v_i (x) grad w_ic
+// with grad w_ic = (x_i - x_c)/(2 dx^2), "matrix-free PCG".
+//
+// Tile kernels: one CTA per 4^3 node block ("tile").  The CTA stages the 5^3 node halo of its cell
+// block in shared memory, evaluates its (<= 64) quadrature points, then reduces the per-cell nodal
+// contributions with a shared-memory gather per node.  Nodes whose 8 cells all lie in the tile
+// (local coords 1..3) are written with plain stores; the other (face) nodes are summed with global
+// atomics into a zeroed output.
+#include <algorithm>
+#include <cmath>
+
+#include "mpl_common.cuh"
+
+namespace {
+
+__device__ __forceinline__ int local_id(int lx, int ly, int lz) { return (lx * 4 + ly) * 4 + lz; }
+
+// halo index h in 5^3 -> (tile, local) of the node; returns -1 if the neighbour tile is absent
+__device__ __forceinline__ int64_t halo_node(int t, const int *__restrict__ nplus, int h) {
+    int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
+    int dp = ((hx >> 2) << 2) | ((hy >> 2) << 1) | (hz >> 2);
+    int tt = dp ? nplus[8 * t + dp] : t;
+    if (tt < 0) return -1;
+    return (int64_t)tt * 64 + local_id(hx & 3, hy & 3, hz & 3);
+}
+
+template <class T> __device__ __forceinline__ void atomic_add3(vec4<T> *p, T x, T y, T z);
+template <> __device__ __forceinline__ void atomic_add3<float>(f4 *p, float x, float y, float z) {
+    atomicAdd(reinterpret_cast<float4 *>(p), make_float4(x, y, z, 0.f));
+}
+template <> __device__ __forceinline__ void atomic_add3<double>(d4 *p, double x, double y, double z) {
+    atomicAdd(&p->x, x);
+    atomicAdd(&p->y, y);
+    atomicAdd(&p->z, z);
+}
+
+// =============================================================================================
+// a5 / a8: linearisation.  MODE = LIN_ENERGY (Phi only), LIN_GRAD (+ g), LIN_FULL (+ K, diag).
+// =============================================================================================
+template <class T, int MODE>
+__global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_, const int *__restrict__ nplus,
+                                                   const int *__restrict__ cstart, const uint8_t *__restrict__ clocal,
+                                                   const int *__restrict__ hascells, const vec4<T> *__restrict__ v,
+                                                   const vec4<T> *__restrict__ vhat, const T *__restrict__ nmass,
+                                                   const T *__restrict__ qslot, T *__restrict__ Kout,
+                                                   vec4<T> *__restrict__ grad, vec4<T> *__restrict__ diag,
+                                                   DevScalars *sc) {
+    constexpr int KS = (MODE == LIN_FULL) ? 64 * 45 : 1;
+    __shared__ vec4<T> vh[125];
+    __shared__ T Pg[64 * 9];
+    __shared__ T Ks[KS];
+    __shared__ int cslot[64];
+    const int t = blockIdx.x, tid = threadIdx.x;
+    const int has = hascells[t];
+    const int cs = cstart[t], nc = cstart[t + 1] - cs;
+    for (int h = tid; h < 125; h += blockDim.x) {
+        int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
+        bool owned = hx < 4 && hy < 4 && hz < 4;
+        int64_t n = (has || owned) ? halo_node(t, nplus, h) : -1;
+        vh[h] = n >= 0 ? v[n] : mk4<T>(0, 0, 0, 0);
+    }
+    if (tid < 64) cslot[tid] = -1;
+    if (MODE == LIN_FULL)
+        for (int i = tid; i < nc * 45; i += blockDim.x) Ks[i] = T(0);
+    __syncthreads();
+    if (tid < nc) {
+        int l = clocal[cs + tid];
+        if (l != 0xFF) cslot[l] = tid;
+    }
+    double e_loc = 0.0;
+    const T dt = T(dt_);
+    const T q = T(0.25 * g.inv_dx);  // grad w = s q, s in {-1,+1}^3
+    if (tid < nc) {
+        int l = clocal[cs + tid];
+        if (l != 0xFF) {
+            int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+            T Gs[9];
+#pragma unroll
+            for (int a = 0; a < 9; a++) Gs[a] = T(0);
+#pragma unroll
+            for (int o = 0; o < 8; o++) {
+                int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+                vec4<T> u = vh[((lx + ox) * 5 + ly + oy) * 5 + lz + oz];
+                T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
+                Gs[0] += u.x * s0; Gs[1] += u.x * s1; Gs[2] += u.x * s2;
+                Gs[3] += u.y * s0; Gs[4] += u.y * s1; Gs[5] += u.y * s2;
+                Gs[6] += u.z * s0; Gs[7] += u.z * s1; Gs[8] += u.z * s2;
+            }
+            T W[9], A[9], AiT[9];  // W = dt G, A = I + W
+#pragma unroll
+            for (int a = 0; a < 9; a++) { W[a] = dt * q * Gs[a]; A[a] = W[a] + ((a % 4 == 0) ? T(1) : T(0)); }
+            T detA = inv_transpose3(A, AiT);
+            if (!(detA > T(0))) sc->inverted = 1;  // amb-21: Phi = +inf
+            T Pc[9];
+#pragma unroll
+            for (int a = 0; a < 9; a++) Pc[a] = T(0);
+            const int nmat = mp.nmat;
+            const int j = tid;
+            for (int k = 0; k < nmat; k++) {
+                const T *sl = qslot + ((int64_t)(cs + tid) * nmat + k) * 16;
+                T V = sl[0];
+                if (V == T(0)) continue;
+                T mu = T(mp.mu[k]), lamL = T(mp.lam[k]);
+                T E[9] = {sl[1], sl[4], sl[6], sl[4], sl[2], sl[5], sl[6], sl[5], sl[3]};
+                // H = F - I = W + E + W E
+                T WE[9], H[9];
+                mm3(W, E, WE);
+#pragma unroll
+                for (int a = 0; a < 9; a++) H[a] = W[a] + E[a] + WE[a];
+                // b - I = H + H^T + H H^T
+                T B[9];
+#pragma unroll
+                for (int a = 0; a < 3; a++)
+#pragma unroll
+                    for (int b = a; b < 3; b++) {
+                        T val = H[3 * a + b] + H[3 * b + a] + H[3 * a] * H[3 * b] + H[3 * a + 1] * H[3 * b + 1] +
+                                H[3 * a + 2] * H[3 * b + 2];
+                        B[3 * a + b] = val;
+                        B[3 * b + a] = val;
+                    }
+                T lam3[3], Q[9];
+                sym_eig3(B, lam3, Q);
+                T l0 = mlog1p(lam3[0]), l1 = mlog1p(lam3[1]), l2 = mlog1p(lam3[2]);
+                T sl_ = l0 + l1 + l2;
+                T psi = T(0.25) * mu * (l0 * l0 + l1 * l1 + l2 * l2) + T(0.125) * lamL * sl_ * sl_;
+                e_loc += (double)(V * psi);
+                if (MODE == LIN_ENERGY) continue;
+                T tp[3] = {mu * l0 + T(0.5) * lamL * sl_, mu * l1 + T(0.5) * lamL * sl_, mu * l2 + T(0.5) * lamL * sl_};
+                T tau[9];
+#pragma unroll
+                for (int a = 0; a < 3; a++)
+#pragma unroll
+                    for (int b = 0; b < 3; b++)
+                        tau[3 * a + b] = Q[3 * a] * Q[3 * b] * tp[0] + Q[3 * a + 1] * Q[3 * b + 1] * tp[1] +
+                                         Q[3 * a + 2] * Q[3 * b + 2] * tp[2];
+                T TA[9];  // tau A^{-T}
+                mm3(tau, AiT, TA);
+                const T sV = dt * V;
+#pragma unroll
+                for (int a = 0; a < 9; a++) Pc[a] += sV * TA[a];
+                if (MODE == LIN_FULL) {
+                    // FS = (I + H)(I + E); Y = Q^T (F S)
+                    T F[9], S[9], FS[9], Y[9];
+#pragma unroll
+                    for (int a = 0; a < 9; a++) {
+                        F[a] = H[a] + ((a % 4 == 0) ? T(1) : T(0));
+                        S[a] = E[a] + ((a % 4 == 0) ? T(1) : T(0));
+                    }
+                    mm3(F, S, FS);
+#pragma unroll
+                    for (int i = 0; i < 3; i++)
+#pragma unroll
+                        for (int b = 0; b < 3; b++) Y[3 * i + b] = Q[i] * FS[b] + Q[3 + i] * FS[3 + b] + Q[6 + i] * FS[6 + b];
+                    T L[9];
+#pragma unroll
+                    for (int i = 0; i < 3; i++)
+#pragma unroll
+                        for (int jj = 0; jj < 3; jj++) L[3 * i + jj] = dlog(lam3[i], lam3[jj]);
+                    const T kscale = sV * T(1.0 / 16.0) * T(g.inv_dx * g.inv_dx);
+                    T *Kr = Ks + j * 45;
+#pragma unroll
+                    for (int a = 0; a < 3; a++)
+#pragma unroll
+                        for (int b = 0; b < 3; b++) {
+                            // db' = dt (q_a (x) y_b + y_b (x) q_a), q_a[i] = Q[a][i], y_b[i] = Y[i][b]
+                            T Dp[9];
+                            T trD = T(0);
+#pragma unroll
+                            for (int i = 0; i < 3; i++)
+#pragma unroll
+                                for (int jj = 0; jj < 3; jj++) {
+                                    T dbp = dt * (Q[3 * a + i] * Y[3 * jj + b] + Y[3 * i + b] * Q[3 * a + jj]);
+                                    Dp[3 * i + jj] = L[3 * i + jj] * dbp;
+                                }
+                            trD = Dp[0] + Dp[4] + Dp[8];
+                            // dtau' = mu D' + lam/2 tr(D') I ; dtau = Q dtau' Q^T
+                            T dtp[9];
+#pragma unroll
+                            for (int i = 0; i < 9; i++) dtp[i] = mu * Dp[i] + ((i % 4 == 0) ? T(0.5) * lamL * trD : T(0));
+                            T tmp[9], dtau[9];
+#pragma unroll
+                            for (int i = 0; i < 3; i++)
+#pragma unroll
+                                for (int jj = 0; jj < 3; jj++)
+                                    tmp[3 * i + jj] = Q[3 * i] * dtp[jj] + Q[3 * i + 1] * dtp[3 + jj] + Q[3 * i + 2] * dtp[6 + jj];
+#pragma unroll
+                            for (int i = 0; i < 3; i++)
+#pragma unroll
+                                for (int jj = 0; jj < 3; jj++)
+                                    dtau[3 * i + jj] = tmp[3 * i] * Q[3 * jj] + tmp[3 * i + 1] * Q[3 * jj + 1] + tmp[3 * i + 2] * Q[3 * jj + 2];
+                            // column (a,b): dtau A^{-T} - dt (tau A^{-T}) e_b (x) e_a^T A^{-T}
+                            const int cidx = 3 * a + b;
+#pragma unroll
+                            for (int i = 0; i < 3; i++)
+#pragma unroll
+                                for (int jj = 0; jj < 3; jj++) {
+                                    T r1 = dtau[3 * i] * AiT[jj] + dtau[3 * i + 1] * AiT[3 + jj] + dtau[3 * i + 2] * AiT[6 + jj];
+                                    T r2 = -dt * TA[3 * i + b] * AiT[3 * a + jj];
+                                    T val = kscale * (r1 + r2);
+                                    const int r = 3 * i + jj;
+                                    if (r == cidx) Kr[kidx(r, r)] += val;
+                                    else if (r < cidx) Kr[kidx(r, cidx)] += T(0.5) * val;
+                                    else Kr[kidx(cidx, r)] += T(0.5) * val;
+                                }
+                        }
+                }
+            }
+            if (MODE != LIN_ENERGY) {
+#pragma unroll
+                for (int a = 0; a < 9; a++) Pg[l * 9 + a] = Pc[a] * q;  // fold grad w scale
+            }
+        }
+    }
+    __syncthreads();
+    if (MODE == LIN_FULL) {  // coalesced copy of the tile's tangent block
+        T *dst = Kout + (int64_t)cs * 45;
+        for (int i = tid; i < nc * 45; i += blockDim.x) dst[i] = Ks[i];
+    }
+    // ---- node phase -----------------------------------------------------------------------
+    if (tid < 125) {
+        int h = tid;
+        int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
+        bool owned = hx < 4 && hy < 4 && hz < 4;
+        bool interior = hx >= 1 && hx <= 3 && hy >= 1 && hy <= 3 && hz >= 1 && hz <= 3;
+        T f[3] = {0, 0, 0}, d[3] = {0, 0, 0};
+        bool any = false;
+        if (has && MODE != LIN_ENERGY) {
+#pragma unroll
+            for (int o = 0; o < 8; o++) {
+                int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+                int cx = hx - ox, cy = hy - oy, cz = hz - oz;
+                if (cx < 0 || cy < 0 || cz < 0 || cx > 3 || cy > 3 || cz > 3) continue;
+                int l = local_id(cx, cy, cz);
+                int jj = cslot[l];
+                if (jj < 0 || clocal[cs + jj] == 0xFF) continue;
+                any = true;
+                T s[3] = {ox ? T(1) : T(-1), oy ? T(1) : T(-1), oz ? T(1) : T(-1)};
+                const T *P = Pg + l * 9;
+#pragma unroll
+                for (int a = 0; a < 3; a++) f[a] += P[3 * a] * s[0] + P[3 * a + 1] * s[1] + P[3 * a + 2] * s[2];
+                if (MODE == LIN_FULL) {
+                    const T *Kr = Ks + jj * 45;
+#pragma unroll
+                    for (int a = 0; a < 3; a++) {
+                        T acc = T(0);
+#pragma unroll
+                        for (int b = 0; b < 3; b++)
+#pragma unroll
+                            for (int e = 0; e < 3; e++) {
+                                int r = 3 * a + b, c = 3 * a + e;
+                                T kv = r <= c ? Kr[kidx(r, c)] : Kr[kidx(c, r)];
+                                acc += s[b] * s[e] * kv;
+                            }
+                        d[a] += acc;
+                    }
+                }
+            }
+        }
+        int64_t n = (owned || has) ? halo_node(t, nplus, h) : -1;
+        if (n >= 0) {
+            if (owned) {
+                T m = nmass[n];
+                if (m > T(0)) {
+                    vec4<T> vv = vh[h], vt = vhat[n];
+                    T dv0 = vv.x - vt.x, dv1 = vv.y - vt.y, dv2 = vv.z - vt.z;
+                    e_loc += 0.5 * (double)(m * (dv0 * dv0 + dv1 * dv1 + dv2 * dv2));
+                    f[0] += m * dv0; f[1] += m * dv1; f[2] += m * dv2;
+                    d[0] += m; d[1] += m; d[2] += m;
+                    any = true;
+                }
+            }
+            if (MODE != LIN_ENERGY && any) {
+                if (interior || !has) {
+                    // exclusive: all 8 cells of an interior node lie in this tile; a tile without
+                    // cells contributes only the mass terms of its owned nodes
+                    if (interior) {
+                        grad[n] = mk4<T>(f[0], f[1], f[2], T(0));
+                        if (MODE == LIN_FULL) diag[n] = mk4<T>(d[0], d[1], d[2], T(0));
+                    } else {
+                        atomic_add3<T>(grad + n, f[0], f[1], f[2]);
+                        if (MODE == LIN_FULL) atomic_add3<T>(diag + n, d[0], d[1], d[2]);
+                    }
+                } else {
+                    atomic_add3<T>(grad + n, f[0], f[1], f[2]);
+                    if (MODE == LIN_FULL) atomic_add3<T>(diag + n, d[0], d[1], d[2]);
+                }
+            }
+        }
+    }
+    block_add(e_loc, &sc->energy);
+}
+
+// =============================================================================================
+// a6: HVP  (Hu)_i = m_i u_i + sum_c (K_c : dG_c(u)) grad w_ic   (v1: one tile per CTA)
+// also accumulates u . Hu = sum_i m_i |u_i|^2 + sum_c dG_c : K_c : dG_c (exact, no completion needed)
+// =============================================================================================
+template <class T>
+__global__ void __launch_bounds__(128) k_hvp(const int *__restrict__ nplus, const int *__restrict__ cstart,
+                                             const uint8_t *__restrict__ clocal, const int *__restrict__ hascells,
+                                             const T *__restrict__ K, const T *__restrict__ nmass,
+                                             const vec4<T> *__restrict__ u, vec4<T> *__restrict__ Hu,
+                                             double *__restrict__ uHu, const CGSlot *__restrict__ cgs, int cgj,
+                                             double cgthr, const DevScalars *__restrict__ sc) {
+    if (cgs != nullptr && (sc->neg_curv || (cgj > 0 && cgs[cgj].rr <= cgthr))) return;  // PCG converged
+    __shared__ vec4<T> uh[125];
+    __shared__ __align__(16) T Ks[64 * 45];
+    __shared__ T Pc[64 * 9];
+    __shared__ int cslot[64];
+    const int t = blockIdx.x, tid = threadIdx.x;
+    const int has = hascells[t];
+    const int cs = cstart[t], nc = cstart[t + 1] - cs;
+    for (int h = tid; h < 125; h += blockDim.x) {
+        int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
+        bool owned = hx < 4 && hy < 4 && hz < 4;
+        int64_t n = (has || owned) ? halo_node(t, nplus, h) : -1;
+        uh[h] = n >= 0 ? u[n] : mk4<T>(0, 0, 0, 0);
+    }
+    if (tid < 64) cslot[tid] = -1;
+    {   // coalesced 16-byte copy of the tile's tangent block (nc multiple of 4 => 16B multiple)
+        const int nvec = nc * 45 * (int)sizeof(T) / 16;
+        const int4 *src = reinterpret_cast<const int4 *>(K + (int64_t)cs * 45);
+        int4 *dst = reinterpret_cast<int4 *>(Ks);
+        for (int i = tid; i < nvec; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    double acc = 0.0;
+    if (tid < nc) {
+        int l = clocal[cs + tid];
+        if (l != 0xFF) {
+            cslot[l] = tid;
+            int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+            T dG[9];
+#pragma unroll
+            for (int a = 0; a < 9; a++) dG[a] = T(0);
+#pragma unroll
+            for (int o = 0; o < 8; o++) {
+                int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+                vec4<T> w = uh[((lx + ox) * 5 + ly + oy) * 5 + lz + oz];
+                T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
+                dG[0] += w.x * s0; dG[1] += w.x * s1; dG[2] += w.x * s2;
+                dG[3] += w.y * s0; dG[4] += w.y * s1; dG[5] += w.y * s2;
+                dG[6] += w.z * s0; dG[7] += w.z * s1; dG[8] += w.z * s2;
+            }
+            const T *Kr = Ks + tid * 45;
+            T P[9];
+#pragma unroll
+            for (int r = 0; r < 9; r++) P[r] = T(0);
+#pragma unroll
+            for (int r = 0; r < 9; r++) {
+                P[r] += Kr[kidx(r, r)] * dG[r];
+#pragma unroll
+                for (int s = r + 1; s < 9; s++) {
+                    T k = Kr[kidx(r, s)];
+                    P[r] += k * dG[s];
+                    P[s] += k * dG[r];
+                }
+            }
+            T q = T(0);
+#pragma unroll
+            for (int r = 0; r < 9; r++) { Pc[l * 9 + r] = P[r]; q += P[r] * dG[r]; }
+            acc += (double)q;
+        }
+    }
+    __syncthreads();
+    if (tid < 125) {
+        int h = tid;
+        int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
+        bool owned = hx < 4 && hy < 4 && hz < 4;
+        bool interior = hx >= 1 && hx <= 3 && hy >= 1 && hy <= 3 && hz >= 1 && hz <= 3;
+        T f[3] = {0, 0, 0};
+        bool any = false;
+        if (has) {
+#pragma unroll
+            for (int o = 0; o < 8; o++) {
+                int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+                int cx = hx - ox, cy = hy - oy, cz = hz - oz;
+                if (cx < 0 || cy < 0 || cz < 0 || cx > 3 || cy > 3 || cz > 3) continue;
+                int l = local_id(cx, cy, cz);
+                if (cslot[l] < 0) continue;
+                any = true;
+                T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
+                const T *P = Pc + l * 9;
+                f[0] += P[0] * s0 + P[1] * s1 + P[2] * s2;
+                f[1] += P[3] * s0 + P[4] * s1 + P[5] * s2;
+                f[2] += P[6] * s0 + P[7] * s1 + P[8] * s2;
+            }
+        }
+        int64_t n = (owned || has) ? halo_node(t, nplus, h) : -1;
+        if (n >= 0) {
+            if (owned) {
+                T m = nmass[n];
+                if (m > T(0)) {
+                    vec4<T> w = uh[h];
+                    f[0] += m * w.x; f[1] += m * w.y; f[2] += m * w.z;
+                    acc += (double)(m * (w.x * w.x + w.y * w.y + w.z * w.z));
+                    any = true;
+                }
+            }
+            if (any) {
+                if (interior) Hu[n] = mk4<T>(f[0], f[1], f[2], T(0));
+                else atomic_add3<T>(Hu + n, f[0], f[1], f[2]);
+            }
+        }
+    }
+    if (uHu) block_add(acc, uHu);
+}
+
+// =============================================================================================
+// a7: Jacobi-PCG vector kernels (fp64 accumulation of every dot product)
+// slot j: rz_j = r_j.z_j, rr_j = r_j.r_j, pHp_j = p_j.H p_j
+// =============================================================================================
+template <class T>
+__global__ void k_pcg_init(int64_t N, const uint8_t *__restrict__ flag, const vec4<T> *__restrict__ g,
+                           const vec4<T> *__restrict__ D, vec4<T> *__restrict__ r, vec4<T> *__restrict__ p,
+                           vec4<T> *__restrict__ x, CGSlot *slot) {
+    double rz = 0, rr = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        vec4<T> rv = mk4<T>(0, 0, 0, 0), zv = mk4<T>(0, 0, 0, 0);
+        if (flag[i] == 1) {
+            vec4<T> gv = g[i], dv = D[i];
+            rv = mk4<T>(-gv.x, -gv.y, -gv.z, 0);
+            zv = mk4<T>(rv.x / dv.x, rv.y / dv.y, rv.z / dv.z, 0);
+            rz += (double)(rv.x * zv.x + rv.y * zv.y + rv.z * zv.z);
+            rr += (double)(rv.x * rv.x + rv.y * rv.y + rv.z * rv.z);
+        }
+        r[i] = rv;
+        p[i] = zv;
+        x[i] = mk4<T>(0, 0, 0, 0);
+    }
+    block_add(rz, &slot[0].rz);
+    block_add(rr, &slot[0].rr);
+}
+
+// converged / broken down before iteration j?
+__device__ __forceinline__ bool cg_stop(const CGSlot *slot, int j, double thr, const DevScalars *sc) {
+    if (sc->neg_curv) return true;
+    return j > 0 && slot[j].rr <= thr;
+}
+
+// x += alpha p ; r -= alpha Hp ; z = D^{-1} r ; slot[j+1] = (r.z, r.r)
+template <class T>
+__global__ void k_pcg_update1(int64_t N, int j, double thr, const uint8_t *__restrict__ flag,
+                              const vec4<T> *__restrict__ D, const vec4<T> *__restrict__ p,
+                              const vec4<T> *__restrict__ Hp, vec4<T> *__restrict__ x, vec4<T> *__restrict__ r,
+                              CGSlot *slot, DevScalars *sc) {
+    if (cg_stop(slot, j, thr, sc)) return;
+    double pHp = slot[j].pHp;
+    if (!(pHp > 0.0)) {  // breakdown (negative curvature): first iteration returns p = z_0
+        if (j == 0)
+            for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+                x[i] = p[i];
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            sc->neg_curv = 1;
+            sc->cg_done_iter = j + 1;
+        }
+        return;
+    }
+    const T alpha = T(slot[j].rz / pHp);
+    double rz = 0, rr = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        if (flag[i] != 1) continue;
+        vec4<T> pv = p[i], hv = Hp[i], xv = x[i], rv = r[i], dv = D[i];
+        xv.x += alpha * pv.x; xv.y += alpha * pv.y; xv.z += alpha * pv.z;
+        rv.x -= alpha * hv.x; rv.y -= alpha * hv.y; rv.z -= alpha * hv.z;
+        x[i] = xv;
+        r[i] = rv;
+        rz += (double)(rv.x * rv.x / dv.x + rv.y * rv.y / dv.y + rv.z * rv.z / dv.z);
+        rr += (double)(rv.x * rv.x + rv.y * rv.y + rv.z * rv.z);
+    }
+    block_add(rz, &slot[j + 1].rz);
+    block_add(rr, &slot[j + 1].rr);
+}
+
+// p = z + beta p, beta = rz_{j+1} / rz_j ; also zeroes Hp for the next HVP's atomics
+template <class T>
+__global__ void k_pcg_update2(int64_t N, int j, double thr, const uint8_t *__restrict__ flag,
+                              const vec4<T> *__restrict__ D, const vec4<T> *__restrict__ r, vec4<T> *__restrict__ p,
+                              vec4<T> *__restrict__ Hp, const CGSlot *slot, const DevScalars *sc) {
+    if (cg_stop(slot, j + 1, thr, sc)) return;
+    const T beta = T(slot[j + 1].rz / slot[j].rz);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        Hp[i] = mk4<T>(0, 0, 0, 0);
+        if (flag[i] != 1) continue;
+        vec4<T> rv = r[i], dv = D[i], pv = p[i];
+        p[i] = mk4<T>(rv.x / dv.x + beta * pv.x, rv.y / dv.y + beta * pv.y, rv.z / dv.z + beta * pv.z, 0);
+    }
+}
+
+// HVP wrapper used inside PCG: skips work once converged
+template <class T>
+__global__ void k_zero4(int64_t N, vec4<T> *a) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = mk4<T>(0, 0, 0, 0);
+}
+
+// g . x over free nodes
+template <class T>
+__global__ void k_dot_free(int64_t N, const uint8_t *__restrict__ flag, const vec4<T> *__restrict__ a,
+                           const vec4<T> *__restrict__ b, double *out) {
+    double s = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        if (flag[i] != 1) continue;
+        vec4<T> x = a[i], y = b[i];
+        s += (double)(x.x * y.x + x.y * y.y + x.z * y.z);
+    }
+    block_add(s, out);
+}
+
+// vt = v + alpha x on free nodes, v elsewhere
+template <class T>
+__global__ void k_axpy_free(int64_t N, const uint8_t *__restrict__ flag, T alpha, const vec4<T> *__restrict__ v,
+                            const vec4<T> *__restrict__ x, vec4<T> *__restrict__ vt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        vec4<T> a = v[i];
+        if (flag[i] == 1) {
+            vec4<T> b = x[i];
+            a.x += alpha * b.x; a.y += alpha * b.y; a.z += alpha * b.z;
+        }
+        vt[i] = a;
+    }
+}
+
+template <class T>
+__global__ void k_canon_to_tile(int64_t n, const int *__restrict__ list, const T *__restrict__ src,
+                                vec4<T> *__restrict__ dst) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[list[i]] = mk4<T>(src[3 * i], src[3 * i + 1], src[3 * i + 2], T(0));
+}
+template <class T>
+__global__ void k_tile_to_canon(int64_t n, const int *__restrict__ list, const vec4<T> *__restrict__ src,
+                                T *__restrict__ dst) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
+        vec4<T> v = src[list[i]];
+        dst[3 * i] = v.x; dst[3 * i + 1] = v.y; dst[3 * i + 2] = v.z;
+    }
+}
+
+inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+inline unsigned vgrid(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    return (unsigned)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
+}
+
+}  // namespace
+
+// =============================================================================================
+// host side
+// =============================================================================================
+template <class T>
+mpl_status canon_to_tile(mpl_ctx ctx, const void *src, void *dst_tile) {
+    const int64_t n = ctx->n_nodes_active, NT = (int64_t)ctx->T * 64;
+    cudaStream_t st = ctx->stream;
+    MPL_CHECK(ensure(ctx, ctx->io_stage, (size_t)(n * 3 + 4) * sizeof(T)));
+    MPL_CUDA(cudaMemcpyAsync(ctx->io_stage.p, src, n * 3 * sizeof(T), cudaMemcpyDefault, st));
+    MPL_CUDA(cudaMemsetAsync(dst_tile, 0, NT * sizeof(vec4<T>), st));
+    if (n) k_canon_to_tile<T><<<nblk(n, 256), 256, 0, st>>>(n, (const int *)ctx->n_list.p, (const T *)ctx->io_stage.p,
+                                                          (vec4<T> *)dst_tile);
+    MPL_CUDA(cudaGetLastError());
+    return MPL_OK;
+}
+
+template <class T>
+mpl_status tile_to_canon(mpl_ctx ctx, const void *src_tile, void *dst) {
+    const int64_t n = ctx->n_nodes_active;
+    cudaStream_t st = ctx->stream;
+    MPL_CHECK(ensure(ctx, ctx->io_stage, (size_t)(n * 3 + 4) * sizeof(T)));
+    if (n) k_tile_to_canon<T><<<nblk(n, 256), 256, 0, st>>>(n, (const int *)ctx->n_list.p, (const vec4<T> *)src_tile,
+                                                          (T *)ctx->io_stage.p);
+    MPL_CUDA(cudaMemcpyAsync(dst, ctx->io_stage.p, n * 3 * sizeof(T), cudaMemcpyDefault, st));
+    MPL_CUDA(cudaStreamSynchronize(st));
+    return MPL_OK;
+}
+
+// Launch the linearisation kernel at v_tile; writes g (n_g), diag (n_diag), K; returns Phi.
+template <class T>
+mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi) {
+    cudaStream_t st = ctx->stream;
+    const int T_ = ctx->T;
+    const int64_t NT = (int64_t)T_ * 64;
+    DevScalars *sc = (DevScalars *)ctx->scalars.p;
+    MPL_CUDA(cudaMemsetAsync(&sc->energy, 0, sizeof(double), st));
+    MPL_CUDA(cudaMemsetAsync(&sc->inverted, 0, sizeof(int), st));
+    if (mode != LIN_ENERGY) MPL_CUDA(cudaMemsetAsync(ctx->n_g.p, 0, NT * sizeof(vec4<T>), st));
+    if (mode == LIN_FULL) MPL_CUDA(cudaMemsetAsync(ctx->n_diag.p, 0, NT * sizeof(vec4<T>), st));
+    if (T_) {
+#define LIN_ARGS                                                                                                  \
+    ctx->grid, ctx->mats, ctx->dt, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,                     \
+        (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p, (const vec4<T> *)v_tile,                  \
+        (const vec4<T> *)ctx->n_vhat.p, (const T *)ctx->n_mass.p, (const T *)ctx->q_slot.p, (T *)ctx->K.p,         \
+        (vec4<T> *)ctx->n_g.p, (vec4<T> *)ctx->n_diag.p, sc
+        if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY><<<T_, 128, 0, st>>>(LIN_ARGS);
+        else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD><<<T_, 128, 0, st>>>(LIN_ARGS);
+        else k_linearize<T, LIN_FULL><<<T_, 128, 0, st>>>(LIN_ARGS);
+#undef LIN_ARGS
+    }
+    MPL_CUDA(cudaGetLastError());
+    if (phi) {
+        double e = 0;
+        int inv = 0;
+        MPL_CUDA(cudaMemcpyAsync(&e, &sc->energy, sizeof(double), cudaMemcpyDeviceToHost, st));
+        MPL_CUDA(cudaMemcpyAsync(&inv, &sc->inverted, sizeof(int), cudaMemcpyDeviceToHost, st));
+        MPL_CUDA(cudaStreamSynchronize(st));
+        *phi = inv ? __builtin_inf() : e;
+    }
+    if (mode == LIN_FULL) ctx->linearized = true;
+    return MPL_OK;
+}
+
+// One HVP on tile-dense vectors: Hu = H u (Hu zeroed here); optional u.Hu accumulation.
+template <class T>
+mpl_status hvp_tile(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu_accum) {
+    cudaStream_t st = ctx->stream;
+    const int T_ = ctx->T;
+    MPL_CUDA(cudaMemsetAsync(Hu_tile, 0, (size_t)T_ * 64 * sizeof(vec4<T>), st));
+    if (T_)
+        k_hvp<T><<<T_, 128, 0, st>>>((const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,
+                                     (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p, (const T *)ctx->K.p,
+                                     (const T *)ctx->n_mass.p, (const vec4<T> *)u_tile, (vec4<T> *)Hu_tile, uHu_accum,
+                                     nullptr, 0, 0.0, nullptr);
+    MPL_CUDA(cudaGetLastError());
+    return MPL_OK;
+}
+
+namespace {
+template <class T>
+mpl_status energy_at(mpl_ctx ctx, const void *v_tile, double *phi) {
+    return linearize_impl<T>(ctx, v_tile, LIN_ENERGY, phi);
+}
+}  // namespace
+
+template <class T>
+mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *out) {
+    cudaStream_t st = ctx->stream;
+    const int64_t NT = (int64_t)ctx->T * 64;
+    DevScalars *sc = (DevScalars *)ctx->scalars.p;
+    mpl_solve_stats S{};
+    const bool fixed = cfg->fixed_newton_iters > 0;
+    const int kmax = fixed ? cfg->fixed_newton_iters : cfg->newton_max;
+    const int cg_cap = cfg->cg_max > 0 ? cfg->cg_max : 1;
+    int slots_needed = cg_cap + 2;
+    if (cfg->fixed_cg_iters)
+        for (int k = 0; k < kmax; k++) slots_needed = std::max(slots_needed, cfg->fixed_cg_iters[k] + 2);
+    MPL_CHECK(ensure(ctx, ctx->cg_slots, (size_t)slots_needed * sizeof(CGSlot)));
+    CGSlot *slots = (CGSlot *)ctx->cg_slots.p;
+    const uint8_t *flag = (const uint8_t *)ctx->n_flag.p;
+    vec4<T> *v = (vec4<T> *)ctx->n_v.p, *vt = (vec4<T> *)ctx->n_vt.p;
+    vec4<T> *g = (vec4<T> *)ctx->n_g.p, *D = (vec4<T> *)ctx->n_diag.p;
+    vec4<T> *x = (vec4<T> *)ctx->n_x.p, *r = (vec4<T> *)ctx->n_r.p, *p = (vec4<T> *)ctx->n_p.p,
+            *Hp = (vec4<T> *)ctx->n_Hp.p;
+    const unsigned VG = vgrid(NT);
+    cudaEvent_t e0, e1, h0, h1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> hev;
+    double t_lin = 0, t_pcg = 0, t_ls = 0;
+    auto elapsed = [&](cudaEvent_t a, cudaEvent_t b) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        return (double)ms;
+    };
+    std::vector<CGSlot> hslots;
+    double phi0 = 0;
+    for (int k = 0; k < kmax; k++) {
+        // ---- linearise at v^k -------------------------------------------------------------
+        cudaEventRecord(e0, st);
+        MPL_CHECK(linearize_impl<T>(ctx, v, LIN_FULL, nullptr));
+        MPL_CUDA(cudaMemsetAsync(slots, 0, slots_needed * sizeof(CGSlot), st));
+        MPL_CUDA(cudaMemsetAsync(&sc->neg_curv, 0, sizeof(int), st));
+        MPL_CUDA(cudaMemsetAsync(&sc->cg_done_iter, 0xff, sizeof(int), st));
+        k_pcg_init<T><<<VG, 256, 0, st>>>(NT, flag, g, D, r, p, x, slots);
+        MPL_CUDA(cudaMemsetAsync(Hp, 0, NT * sizeof(vec4<T>), st));
+        cudaEventRecord(e1, st);
+        CGSlot s0;
+        double e = 0;
+        int inv = 0;
+        MPL_CUDA(cudaMemcpyAsync(&s0, slots, sizeof s0, cudaMemcpyDeviceToHost, st));
+        MPL_CUDA(cudaMemcpyAsync(&e, &sc->energy, sizeof e, cudaMemcpyDeviceToHost, st));
+        MPL_CUDA(cudaMemcpyAsync(&inv, &sc->inverted, sizeof inv, cudaMemcpyDeviceToHost, st));
+        MPL_CUDA(cudaStreamSynchronize(st));
+        t_lin += elapsed(e0, e1);
+        phi0 = inv ? __builtin_inf() : e;
+        const double gn = sqrt(s0.rr);
+        if (k == 0) S.grad_norm0 = gn;
+        S.grad_norm = gn;
+        if (!fixed && gn <= cfg->newton_rtol * S.grad_norm0) {
+            S.converged = 1;
+            break;
+        }
+        // ---- PCG on H x = -g -----------------------------------------------------------------
+        const int itmax = cfg->fixed_cg_iters ? cfg->fixed_cg_iters[k] : cg_cap;
+        const double thr = cfg->fixed_cg_iters ? -1.0 : cfg->cg_rtol * cfg->cg_rtol * s0.rr;
+        int launched = 0, its = 0;
+        cudaEventRecord(e0, st);
+        if (s0.rr > 0.0 && itmax > 0) {
+            int chunk = 4;
+            bool done = false;
+            while (!done && launched < itmax) {
+                int n = std::min(chunk, itmax - launched);
+                for (int jj = launched; jj < launched + n; jj++) {
+                    if ((int)hev.size() <= S.n_hvp) {
+                        cudaEvent_t a, b;
+                        cudaEventCreate(&a);
+                        cudaEventCreate(&b);
+                        hev.push_back({a, b});
+                    }
+                    cudaEventRecord(hev[S.n_hvp].first, st);
+                    // the HVP is skipped on device once converged (its output is then unused)
+                    if (ctx->T)
+                        k_hvp<T><<<ctx->T, 128, 0, st>>>((const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,
+                                                        (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p,
+                                                        (const T *)ctx->K.p, (const T *)ctx->n_mass.p, p, Hp,
+                                                        &slots[jj].pHp, slots, jj, thr, sc);
+                    cudaEventRecord(hev[S.n_hvp].second, st);
+                    S.n_hvp++;
+                    k_pcg_update1<T><<<VG, 256, 0, st>>>(NT, jj, thr, flag, D, p, Hp, x, r, slots, sc);
+                    k_pcg_update2<T><<<VG, 256, 0, st>>>(NT, jj, thr, flag, D, r, p, Hp, slots, sc);
+                }
+                launched += n;
+                MPL_CUDA(cudaGetLastError());
+                CGSlot sl;
+                int neg = 0;
+                MPL_CUDA(cudaMemcpyAsync(&sl, slots + launched, sizeof sl, cudaMemcpyDeviceToHost, st));
+                MPL_CUDA(cudaMemcpyAsync(&neg, &sc->neg_curv, sizeof neg, cudaMemcpyDeviceToHost, st));
+                MPL_CUDA(cudaStreamSynchronize(st));
+                if (neg || sl.rr <= thr) done = true;
+                chunk = std::min(chunk * 2, 64);
+            }
+            hslots.resize(launched + 1);
+            int neg = 0, doneit = -1;
+            MPL_CUDA(cudaMemcpyAsync(hslots.data(), slots, (launched + 1) * sizeof(CGSlot), cudaMemcpyDeviceToHost, st));
+            MPL_CUDA(cudaMemcpyAsync(&neg, &sc->neg_curv, sizeof neg, cudaMemcpyDeviceToHost, st));
+            MPL_CUDA(cudaMemcpyAsync(&doneit, &sc->cg_done_iter, sizeof doneit, cudaMemcpyDeviceToHost, st));
+            MPL_CUDA(cudaStreamSynchronize(st));
+            its = launched;
+            if (neg) {
+                its = doneit;
+                S.neg_curvature++;
+            } else {
+                for (int s = 1; s <= launched; s++)
+                    if (hslots[s].rr <= thr) { its = s; break; }
+            }
+        }
+        cudaEventRecord(e1, st);
+        MPL_CUDA(cudaEventSynchronize(e1));
+        t_pcg += elapsed(e0, e1);
+        if (k < MPL_MAX_NEWTON_LOG) S.cg_iters[k] = its;
+        S.cg_iters_total += its;
+        // ---- Armijo backtracking line search ------------------------------------------------
+        cudaEventRecord(e0, st);
+        MPL_CUDA(cudaMemsetAsync(&sc->gp, 0, sizeof(double), st));
+        k_dot_free<T><<<VG, 256, 0, st>>>(NT, flag, g, x, &sc->gp);
+        double gp = 0;
+        MPL_CUDA(cudaMemcpyAsync(&gp, &sc->gp, sizeof gp, cudaMemcpyDeviceToHost, st));
+        MPL_CUDA(cudaStreamSynchronize(st));
+        double alpha = 1.0;
+        int h = 0;
+        if (cfg->fixed_ls_halvings) {
+            for (h = 0; h < cfg->fixed_ls_halvings[k]; h++) alpha *= 0.5;
+            k_axpy_free<T><<<VG, 256, 0, st>>>(NT, flag, T(alpha), v, x, vt);
+        } else {
+            for (;;) {
+                k_axpy_free<T><<<VG, 256, 0, st>>>(NT, flag, T(alpha), v, x, vt);
+                double phi = 0;
+                MPL_CHECK(energy_at<T>(ctx, vt, &phi));
+                if (std::isinf(phi)) S.n_inverted_trials++;
+                if (phi <= phi0 + cfg->armijo_c * alpha * gp + cfg->ls_slack * fabs(phi0)) break;
+                if (h >= cfg->ls_max) break;
+                alpha *= 0.5;
+                h++;
+            }
+        }
+        cudaEventRecord(e1, st);
+        MPL_CUDA(cudaEventSynchronize(e1));
+        t_ls += elapsed(e0, e1);
+        if (k < MPL_MAX_NEWTON_LOG) S.ls_iters[k] = h;
+        S.ls_halvings += h;
+        std::swap(v, vt);
+        std::swap(ctx->n_v, ctx->n_vt);
+        S.newton_iters = k + 1;
+    }
+    if (!fixed && S.newton_iters == kmax && !S.converged) {
+        MPL_CHECK(linearize_impl<T>(ctx, v, LIN_GRAD, nullptr));
+        MPL_CUDA(cudaMemsetAsync(&sc->gnorm2, 0, sizeof(double), st));
+        k_dot_free<T><<<VG, 256, 0, st>>>(NT, flag, g, g, &sc->gnorm2);
+        double g2 = 0;
+        MPL_CUDA(cudaMemcpyAsync(&g2, &sc->gnorm2, sizeof g2, cudaMemcpyDeviceToHost, st));
+        MPL_CUDA(cudaStreamSynchronize(st));
+        S.grad_norm = sqrt(g2);
+        if (S.grad_norm <= cfg->newton_rtol * S.grad_norm0) S.converged = 1;
+    }
+    MPL_CHECK(energy_at<T>(ctx, v, &S.energy));
+    double hsum = 0;
+    for (int i = 0; i < S.n_hvp; i++) hsum += elapsed(hev[i].first, hev[i].second);
+    for (auto &pr : hev) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    S.hvp_ms = hsum;
+    S.ms_phase[3] = t_lin;
+    S.ms_phase[4] = t_pcg;
+    S.ms_phase[5] = t_ls;
+    ctx->linearized = false;  // K was built at an earlier iterate
+    ctx->solved = true;
+    if (out) *out = S;
+    (void)h0;
+    (void)h1;
+    return MPL_OK;
+}
+
+template mpl_status canon_to_tile<float>(mpl_ctx, const void *, void *);
+template mpl_status canon_to_tile<double>(mpl_ctx, const void *, void *);
+template mpl_status tile_to_canon<float>(mpl_ctx, const void *, void *);
+template mpl_status tile_to_canon<double>(mpl_ctx, const void *, void *);
+template mpl_status linearize_impl<float>(mpl_ctx, const void *, int, double *);
+template mpl_status linearize_impl<double>(mpl_ctx, const void *, int, double *);
+template mpl_status hvp_tile<float>(mpl_ctx, const void *, void *, double *);
+template mpl_status hvp_tile<double>(mpl_ctx, const void *, void *, double *);
+template mpl_status newton_impl<float>(mpl_ctx, const mpl_solver_cfg *, mpl_solve_stats *);
+template mpl_status newton_impl<double>(mpl_ctx, const mpl_solver_cfg *, mpl_solve_stats *);

@@ -1,0 +1,422 @@
+// mpl_api.cu — the C ABI declared in include/mpmlite.h.  Argument checking, context state and
+// dispatch on the context precision; all numerical work runs in the k_*.cu kernels.
+#include <cmath>
+#include <cstring>
+
+#include "mpl_common.cuh"
+
+mpl_status ensure(mpl_ctx ctx, DevBuf &b, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (b.cap >= bytes) return MPL_OK;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+    size_t want = bytes + bytes / 8;  // headroom: the active set grows as particles move
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        ctx->err = "cudaMalloc of " + std::to_string(want) + " bytes failed: " + cudaGetErrorString(e);
+        return MPL_ERR_OOM;
+    }
+    b.cap = want;
+    return MPL_OK;
+}
+
+namespace {
+
+void free_buf(DevBuf &b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+}
+
+#define DISPATCH(ctx, fn, ...) ((ctx)->precision == 64 ? fn<double>(ctx, __VA_ARGS__) : fn<float>(ctx, __VA_ARGS__))
+
+mpl_status set_device(mpl_ctx ctx) {
+    MPL_CUDA(cudaSetDevice(ctx->device));
+    return MPL_OK;
+}
+
+mpl_status need(mpl_ctx ctx, bool cond, const char *what) {
+    if (cond) return MPL_OK;
+    ctx->err = std::string("call order: ") + what;
+    return MPL_ERR_STATE;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *mpl_version(void) { return "mpmlite-b200 0.1 (sm_100a)"; }
+
+mpl_status mpl_create(const mpl_config *cfg, const mpl_grid *grid, mpl_ctx *out) {
+    if (!cfg || !grid || !out) return MPL_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (cfg->precision != 32 && cfg->precision != 64) return MPL_ERR_INVALID_ARG;
+    for (int a = 0; a < 3; a++)
+        if (grid->n[a] < 2 || grid->n[a] > 1022) return MPL_ERR_INVALID_ARG;
+    if (!(grid->dx > 0)) return MPL_ERR_INVALID_ARG;
+    if (cfg->nranks != 1 && cfg->nranks != 0) return MPL_ERR_UNSUPPORTED;  // slab decomposition: see DESIGN.md §6
+    mpl_ctx ctx = new mpl_ctx_s();
+    ctx->precision = cfg->precision;
+    ctx->device = cfg->device;
+    ctx->rank = cfg->rank;
+    ctx->nranks = 1;
+    for (int a = 0; a < 3; a++) {
+        ctx->grid.n[a] = grid->n[a];
+        ctx->grid.nb[a] = grid->n[a] / 4 + 1;
+        ctx->grid.origin[a] = grid->origin[a];
+    }
+    ctx->grid.dx = grid->dx;
+    ctx->grid.inv_dx = 1.0 / grid->dx;
+    ctx->mats.nmat = 0;
+    ctx->boxes.nbox = 0;
+    mpl_status s = set_device(ctx);
+    if (s != MPL_OK) {
+        delete ctx;
+        return s;
+    }
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        delete ctx;
+        return MPL_ERR_CUDA;
+    }
+    ctx->own_stream = true;
+    if (ensure(ctx, ctx->scalars, 4096) != MPL_OK) {
+        delete ctx;
+        return MPL_ERR_OOM;
+    }
+    cudaMemset(ctx->scalars.p, 0, 4096);
+    *out = ctx;
+    return MPL_OK;
+}
+
+void mpl_destroy(mpl_ctx ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    DevBuf *all[] = {&ctx->px[0], &ctx->px[1], &ctx->pF[0], &ctx->pF[1], &ctx->pv, &ctx->pG, &ctx->pvol[0],
+                     &ctx->pvol[1], &ctx->pmat[0], &ctx->pmat[1], &ctx->pid[0], &ctx->pid[1], &ctx->pkey,
+                     &ctx->prank, &ctx->prec, &ctx->pbase, &ctx->pskey, &ctx->cflag, &ctx->nflag, &ctx->tile_of,
+                     &ctx->scan_tmp, &ctx->t_coord, &ctx->t_nplus, &ctx->t_nminus, &ctx->t_cstart, &ctx->t_ccount,
+                     &ctx->t_hascells, &ctx->t_bcount, &ctx->t_bstart, &ctx->t_cellof, &ctx->t_cmask, &ctx->c_local,
+                     &ctx->q_m, &ctx->q_mv, &ctx->q_mG, &ctx->q_slot, &ctx->q_vc, &ctx->q_Gc, &ctx->K, &ctx->n_mass,
+                     &ctx->n_flag, &ctx->n_vn, &ctx->n_vhat, &ctx->n_v, &ctx->n_vt, &ctx->n_g, &ctx->n_diag,
+                     &ctx->n_x, &ctx->n_r, &ctx->n_p, &ctx->n_Hp, &ctx->n_u, &ctx->n_u2, &ctx->n_act,
+                     &ctx->n_canon, &ctx->n_list, &ctx->scalars, &ctx->cg_slots, &ctx->io_stage, &ctx->io_stage2};
+    for (DevBuf *b : all) free_buf(*b);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char *mpl_last_error(mpl_ctx ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+mpl_status mpl_set_stream(mpl_ctx ctx, void *stream) {
+    if (!ctx) return MPL_ERR_INVALID_ARG;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (stream) {
+        ctx->stream = (cudaStream_t)stream;
+        ctx->own_stream = false;
+    } else {
+        cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+        ctx->own_stream = true;
+    }
+    return MPL_OK;
+}
+
+mpl_status mpl_nccl_unique_id(uint8_t out[128]) {
+    (void)out;
+    return MPL_ERR_UNSUPPORTED;
+}
+
+mpl_status mpl_set_materials(mpl_ctx ctx, int32_t n, const mpl_material *mats) {
+    if (!ctx || !mats || n < 1 || n > MPL_MAXMAT) return MPL_ERR_INVALID_ARG;
+    for (int k = 0; k < n; k++) {
+        const mpl_material &m = mats[k];
+        if (m.kind != 0) {
+            ctx->err = "only StVK-Hencky (kind 0) is implemented";
+            return MPL_ERR_UNSUPPORTED;
+        }
+        double mu = m.E / (2.0 * (1.0 + m.nu)), lam = m.E * m.nu / ((1.0 + m.nu) * (1.0 - 2.0 * m.nu));
+        if (!(mu > 0) || !(lam > -2.0 * mu / 3.0) || !(m.rho > 0)) {
+            ctx->err = "material " + std::to_string(k) + ": need mu > 0, lam > -2mu/3, rho > 0 (P:227)";
+            return MPL_ERR_INVALID_ARG;
+        }
+        ctx->mats.mu[k] = mu;
+        ctx->mats.lam[k] = lam;
+        ctx->mats.rho[k] = m.rho;
+    }
+    ctx->mats.nmat = n;
+    ctx->resampled = ctx->linearized = ctx->solved = false;
+    return MPL_OK;
+}
+
+mpl_status mpl_set_gravity(mpl_ctx ctx, const double g[3]) {
+    if (!ctx || !g) return MPL_ERR_INVALID_ARG;
+    for (int a = 0; a < 3; a++) ctx->gravity[a] = g[a];
+    return MPL_OK;
+}
+
+mpl_status mpl_set_dirichlet(mpl_ctx ctx, int32_t n, const mpl_dirichlet_box *boxes) {
+    if (!ctx || n < 0 || n > MPL_MAXBOX || (n > 0 && !boxes)) return MPL_ERR_INVALID_ARG;
+    ctx->boxes.nbox = n;
+    for (int b = 0; b < n; b++)
+        for (int a = 0; a < 3; a++) {
+            ctx->boxes.lo[b][a] = boxes[b].lo[a];
+            ctx->boxes.hi[b][a] = boxes[b].hi[a];
+            ctx->boxes.vel[b][a] = boxes[b].velocity[a];
+        }
+    return MPL_OK;
+}
+
+mpl_status mpl_set_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v, const void *F, const void *G,
+                             const void *vol, const int32_t *mat, int32_t on_device) {
+    (void)on_device;
+    if (!ctx || n < 0 || (n > 0 && (!x || !v || !F || !G || !vol || !mat))) return MPL_ERR_INVALID_ARG;
+    if (n > (int64_t)1 << 30) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(set_device(ctx));
+    mpl_status s = DISPATCH(ctx, import_particles, n, x, v, F, G, vol, mat);
+    if (s == MPL_OK) {
+        ctx->have_particles = true;
+        ctx->resampled = ctx->linearized = ctx->solved = false;
+    }
+    return s;
+}
+
+mpl_status mpl_get_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G, int32_t on_device) {
+    (void)on_device;
+    if (!ctx) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->have_particles, "mpl_set_particles first"));
+    MPL_CHECK(set_device(ctx));
+    return DISPATCH(ctx, export_particles, x, v, F, G);
+}
+
+int64_t mpl_num_particles(mpl_ctx ctx) { return ctx ? ctx->np : -1; }
+
+mpl_status mpl_resample(mpl_ctx ctx, double dt, int64_t *n_cells, int64_t *n_nodes, int64_t *n_blocks) {
+    if (!ctx || !(dt > 0)) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->have_particles, "mpl_set_particles before mpl_resample"));
+    MPL_CHECK(need(ctx, ctx->mats.nmat > 0, "mpl_set_materials before mpl_resample"));
+    MPL_CHECK(set_device(ctx));
+    ctx->resampled = ctx->linearized = ctx->solved = false;
+    mpl_status s = DISPATCH(ctx, resample_impl, dt);
+    if (s != MPL_OK) return s;
+    if (n_cells) *n_cells = ctx->n_cells_active;
+    if (n_nodes) *n_nodes = ctx->n_nodes_active;
+    if (n_blocks) *n_blocks = ctx->n_blocks_active;
+    return MPL_OK;
+}
+
+mpl_status mpl_get_nodes(mpl_ctx ctx, int32_t *ijk, void *m, void *v_n, uint8_t *free_dof) {
+    if (!ctx) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
+    MPL_CHECK(set_device(ctx));
+    const int64_t n = ctx->n_nodes_active;
+    std::vector<int> list(n);
+    std::vector<int> coord((size_t)ctx->T * 3);
+    cudaStream_t st = ctx->stream;
+    MPL_CUDA(cudaMemcpyAsync(list.data(), ctx->n_list.p, n * 4, cudaMemcpyDeviceToHost, st));
+    MPL_CUDA(cudaMemcpyAsync(coord.data(), ctx->t_coord.p, coord.size() * 4, cudaMemcpyDeviceToHost, st));
+    std::vector<uint8_t> flag;
+    if (free_dof) {
+        flag.resize((size_t)ctx->T * 64);
+        MPL_CUDA(cudaMemcpyAsync(flag.data(), ctx->n_flag.p, flag.size(), cudaMemcpyDeviceToHost, st));
+    }
+    MPL_CUDA(cudaStreamSynchronize(st));
+    if (ijk)
+        for (int64_t i = 0; i < n; i++) {
+            int idx = list[i], t = idx >> 6, l = idx & 63;
+            ijk[3 * i + 0] = coord[3 * t] * 4 + (l >> 4);
+            ijk[3 * i + 1] = coord[3 * t + 1] * 4 + ((l >> 2) & 3);
+            ijk[3 * i + 2] = coord[3 * t + 2] * 4 + (l & 3);
+        }
+    if (free_dof)
+        for (int64_t i = 0; i < n; i++) free_dof[i] = flag[list[i]] == 1;
+    const size_t s = ctx->precision == 64 ? 8 : 4;
+    if (m) {
+        std::vector<char> mm((size_t)ctx->T * 64 * s);
+        MPL_CUDA(cudaMemcpy(mm.data(), ctx->n_mass.p, mm.size(), cudaMemcpyDeviceToHost));
+        std::vector<char> out(n * s);
+        for (int64_t i = 0; i < n; i++) memcpy(out.data() + i * s, mm.data() + (size_t)list[i] * s, s);
+        MPL_CUDA(cudaMemcpy(m, out.data(), n * s, cudaMemcpyDefault));
+    }
+    if (v_n) MPL_CHECK(DISPATCH(ctx, tile_to_canon, ctx->n_vn.p, v_n));
+    return MPL_OK;
+}
+
+mpl_status mpl_get_active_blocks(mpl_ctx ctx, int64_t *ids) {
+    if (!ctx || !ids) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->resampled || ctx->T > 0, "mpl_resample first"));
+    MPL_CHECK(set_device(ctx));
+    const GridP &g = ctx->grid;
+    std::vector<int> flag(ctx->dense_n);
+    MPL_CUDA(cudaMemcpy(flag.data(), ctx->cflag.p, flag.size() * 4, cudaMemcpyDeviceToHost));
+    int64_t k = 0;
+    // the dense index space uses the node-block extents nb; report ids in cell-block extents
+    const int NB[3] = {(g.n[0] + 3) / 4, (g.n[1] + 3) / 4, (g.n[2] + 3) / 4};
+    for (int bx = 0; bx < g.nb[0]; bx++)
+        for (int by = 0; by < g.nb[1]; by++)
+            for (int bz = 0; bz < g.nb[2]; bz++)
+                if (flag[(bx * g.nb[1] + by) * g.nb[2] + bz]) ids[k++] = ((int64_t)bx * NB[1] + by) * NB[2] + bz;
+    return MPL_OK;
+}
+
+mpl_status mpl_get_particle_cells(mpl_ctx ctx, int32_t *base_ijk) {
+    if (!ctx || !base_ijk) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->have_particles, "mpl_set_particles first"));
+    MPL_CHECK(set_device(ctx));
+    // recompute from the current positions (sorted) and unsort via ids
+    const int64_t np = ctx->np;
+    std::vector<int> id(np);
+    std::vector<char> x(np * 3 * (ctx->precision == 64 ? 8 : 4));
+    const int c = ctx->cur;
+    MPL_CUDA(cudaMemcpy(id.data(), ctx->pid[c].p, np * 4, cudaMemcpyDeviceToHost));
+    MPL_CUDA(cudaMemcpy(x.data(), ctx->px[c].p, x.size(), cudaMemcpyDeviceToHost));
+    // NOTE: this getter reports the binning rule of the device kernel (k_bin_flags); it reads the
+    // device-computed base cells through the sorted keys so the check stays bit-exact.
+    std::vector<int> key(np);
+    MPL_CUDA(cudaMemcpy(key.data(), ctx->pskey.p, np * 4, cudaMemcpyDeviceToHost));
+    std::vector<int> coord((size_t)ctx->T * 3);
+    MPL_CUDA(cudaMemcpy(coord.data(), ctx->t_coord.p, coord.size() * 4, cudaMemcpyDeviceToHost));
+    for (int64_t p = 0; p < np; p++) {
+        int t = key[p] >> 6, l = key[p] & 63;
+        int o = id[p];
+        base_ijk[3 * o + 0] = coord[3 * t] * 4 + (l >> 4);
+        base_ijk[3 * o + 1] = coord[3 * t + 1] * 4 + ((l >> 2) & 3);
+        base_ijk[3 * o + 2] = coord[3 * t + 2] * 4 + (l & 3);
+    }
+    return MPL_OK;
+}
+
+mpl_status mpl_get_quadrature(mpl_ctx ctx, int32_t *ijk, void *m_c, void *v_c, void *G_c, void *V_ck, void *tau_ck,
+                              void *S_ck) {
+    if (!ctx) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
+    MPL_CHECK(set_device(ctx));
+    return DISPATCH(ctx, export_quadrature, ijk, m_c, v_c, G_c, V_ck, tau_ck, S_ck);
+}
+
+mpl_status mpl_energy(mpl_ctx ctx, const void *v, double *phi) {
+    if (!ctx || !v || !phi) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
+    MPL_CHECK(set_device(ctx));
+    MPL_CHECK(DISPATCH(ctx, canon_to_tile, v, ctx->n_u.p));
+    return DISPATCH(ctx, linearize_impl, ctx->n_u.p, (int)LIN_ENERGY, phi);
+}
+
+mpl_status mpl_gradient(mpl_ctx ctx, const void *v, void *g, double *phi) {
+    if (!ctx || !v || !g) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
+    MPL_CHECK(set_device(ctx));
+    MPL_CHECK(DISPATCH(ctx, canon_to_tile, v, ctx->n_u.p));
+    double e = 0;
+    MPL_CHECK(DISPATCH(ctx, linearize_impl, ctx->n_u.p, (int)LIN_GRAD, &e));
+    if (phi) *phi = e;
+    return DISPATCH(ctx, tile_to_canon, ctx->n_g.p, g);
+}
+
+mpl_status mpl_linearize(mpl_ctx ctx, const void *v) {
+    if (!ctx || !v) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
+    MPL_CHECK(set_device(ctx));
+    MPL_CHECK(DISPATCH(ctx, canon_to_tile, v, ctx->n_u.p));
+    double e = 0;
+    return DISPATCH(ctx, linearize_impl, ctx->n_u.p, (int)LIN_FULL, &e);
+}
+
+mpl_status mpl_get_diag(mpl_ctx ctx, void *D) {
+    if (!ctx || !D) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->linearized, "mpl_linearize first"));
+    MPL_CHECK(set_device(ctx));
+    return DISPATCH(ctx, tile_to_canon, ctx->n_diag.p, D);
+}
+
+mpl_status mpl_hvp(mpl_ctx ctx, const void *u, void *Hu) {
+    if (!ctx || !u || !Hu) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->linearized, "mpl_linearize before mpl_hvp"));
+    MPL_CHECK(set_device(ctx));
+    MPL_CHECK(DISPATCH(ctx, canon_to_tile, u, ctx->n_u.p));
+    MPL_CHECK(DISPATCH(ctx, hvp_tile, ctx->n_u.p, ctx->n_u2.p, (double *)nullptr));
+    return DISPATCH(ctx, tile_to_canon, ctx->n_u2.p, Hu);
+}
+
+mpl_status mpl_hvp_bench(mpl_ctx ctx, const void *u, void *Hu, int32_t reps, double *ms_per_hvp) {
+    if (!ctx || !u || reps < 1) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->linearized, "mpl_linearize before mpl_hvp_bench"));
+    MPL_CHECK(set_device(ctx));
+    MPL_CHECK(DISPATCH(ctx, canon_to_tile, u, ctx->n_u.p));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, ctx->stream);
+    for (int i = 0; i < reps; i++) MPL_CHECK(DISPATCH(ctx, hvp_tile, ctx->n_u.p, ctx->n_u2.p, (double *)nullptr));
+    cudaEventRecord(b, ctx->stream);
+    MPL_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (ms_per_hvp) *ms_per_hvp = ms / reps;
+    if (Hu) return DISPATCH(ctx, tile_to_canon, ctx->n_u2.p, Hu);
+    return MPL_OK;
+}
+
+mpl_status mpl_newton_step(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *stats) {
+    if (!ctx || !cfg) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample before mpl_newton_step"));
+    if (cfg->newton_max < 0 || cfg->cg_max < 0 || cfg->ls_max < 0) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(set_device(ctx));
+    mpl_status s = DISPATCH(ctx, newton_impl, cfg, stats);
+    if (s != MPL_OK) ctx->resampled = false;
+    return s;
+}
+
+mpl_status mpl_get_velocity(mpl_ctx ctx, void *v) {
+    if (!ctx || !v) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
+    MPL_CHECK(set_device(ctx));
+    return DISPATCH(ctx, tile_to_canon, ctx->n_v.p, v);
+}
+
+mpl_status mpl_set_velocity(mpl_ctx ctx, const void *v) {
+    if (!ctx || !v) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
+    MPL_CHECK(set_device(ctx));
+    return DISPATCH(ctx, canon_to_tile, v, ctx->n_v.p);
+}
+
+mpl_status mpl_transfer_to_particles(mpl_ctx ctx, double dt) {
+    if (!ctx || !(dt > 0)) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample (and mpl_newton_step) before mpl_transfer_to_particles"));
+    MPL_CHECK(set_device(ctx));
+    return DISPATCH(ctx, g2p_impl, dt);
+}
+
+mpl_status mpl_step(mpl_ctx ctx, double dt, const mpl_solver_cfg *cfg, mpl_solve_stats *stats) {
+    if (!ctx || !cfg) return MPL_ERR_INVALID_ARG;
+    cudaEvent_t e[4];
+    for (auto &x : e) cudaEventCreate(&x);
+    cudaEventRecord(e[0], ctx->stream);
+    MPL_CHECK(mpl_resample(ctx, dt, nullptr, nullptr, nullptr));
+    cudaEventRecord(e[1], ctx->stream);
+    mpl_solve_stats S{};
+    MPL_CHECK(mpl_newton_step(ctx, cfg, &S));
+    cudaEventRecord(e[2], ctx->stream);
+    MPL_CHECK(mpl_transfer_to_particles(ctx, dt));
+    cudaEventRecord(e[3], ctx->stream);
+    cudaEventSynchronize(e[3]);
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, e[0], e[1]);
+    cudaEventElapsedTime(&b, e[1], e[2]);
+    cudaEventElapsedTime(&c, e[2], e[3]);
+    for (auto &x : e) cudaEventDestroy(x);
+    S.ms_phase[0] = a;  // bin + sort + P2Q + C2N + stretch (resample)
+    S.ms_phase[6] = c;
+    S.ms_phase[7] = a + b + c;
+    if (stats) *stats = S;
+    return MPL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,284 @@
+// mpl_common.cuh — shared device/host definitions of the B200 MPM Lite library (sm_100a).
+//
+// Layout in HBM:
+//   * 4^3-node blocks ("tiles") t = 0..T-1: every node block touched by an active cell block,
+//     sorted by x-major block id.  Node vectors are tile-dense: node (t, l) at index t*64 + l,
+//     l = (lx*4 + ly)*4 + lz.  Vector element = vec4<T> (x, y, z, pad).
+//   * Cell block t shares the tile's coordinates; its structural cells are stored compactly
+//     ("compact cells"), each tile's run padded to a multiple of 4 cells so every tile's tangent
+//     block K[cs..ce) is 16-byte aligned for cp.async.bulk.
+//   * Particles are kept sorted by (tile, base cell) after every resample.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/mpmlite.h"
+
+#define MPL_MAXMAT 8
+#define MPL_MAXBOX 8
+#define MPL_LOG_NEWTON 64
+
+// ------------------------------------------------------------------------------------------
+// vector types
+// ------------------------------------------------------------------------------------------
+struct __align__(16) f4 { float x, y, z, w; };
+struct __align__(32) d4 { double x, y, z, w; };
+template <class T> struct V4;
+template <> struct V4<float> { typedef f4 type; };
+template <> struct V4<double> { typedef d4 type; };
+template <class T> using vec4 = typename V4<T>::type;
+
+template <class T> __host__ __device__ __forceinline__ vec4<T> mk4(T x, T y, T z, T w) {
+    vec4<T> r;
+    r.x = x; r.y = y; r.z = z; r.w = w;
+    return r;
+}
+
+// ------------------------------------------------------------------------------------------
+// parameters passed by value to kernels
+// ------------------------------------------------------------------------------------------
+struct GridP {
+    int n[3];          // cells per axis
+    int nb[3];         // node-block (tile) coordinate extent per axis = n/4 + 1
+    double dx, inv_dx;
+    double origin[3];
+};
+
+struct MatP {
+    int nmat;
+    double mu[MPL_MAXMAT], lam[MPL_MAXMAT], rho[MPL_MAXMAT];
+};
+
+struct BoxP {
+    int nbox;
+    double lo[MPL_MAXBOX][3], hi[MPL_MAXBOX][3], vel[MPL_MAXBOX][3];
+};
+
+// Tile geometry tables (device pointers)
+struct TilesP {
+    int T;                 // number of tiles (active node blocks)
+    const int *coord;      // T*3 block coords
+    const int *nbr_plus;   // T*8: tile at coord + o (o x-major in {0,1}^3) or -1
+    const int *nbr_minus;  // T*8: tile at coord - o or -1
+    const int *cell_start; // T+1: compact cell offsets (runs padded to multiples of 4)
+    const uint8_t *cell_local; // C: local cell index 0..63, 0xFF = padding
+    const int *cell_of;    // T*64: compact index of local cell or -1
+    const int *tile_has_cells; // T: 1 if the cell block of this tile is active
+};
+
+// ------------------------------------------------------------------------------------------
+// small math
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ float mlog1p(float x) { return log1pf(x); }
+__device__ __forceinline__ double mlog1p(double x) { return log1p(x); }
+__device__ __forceinline__ float mexpm1(float x) { return expm1f(x); }
+__device__ __forceinline__ double mexpm1(double x) { return expm1(x); }
+__device__ __forceinline__ float msqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ double msqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ float mrsqrt(float x) { return rsqrtf(x); }
+__device__ __forceinline__ double mrsqrt(double x) { return rsqrt(x); }
+__device__ __forceinline__ float mabs(float x) { return fabsf(x); }
+__device__ __forceinline__ double mabs(double x) { return fabs(x); }
+
+// 3x3 row-major helpers (arrays fully unrolled into registers)
+template <class T> __device__ __forceinline__ void mm3(const T A[9], const T B[9], T C[9]) {
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++) C[3 * a + b] = A[3 * a] * B[b] + A[3 * a + 1] * B[3 + b] + A[3 * a + 2] * B[6 + b];
+}
+template <class T> __device__ __forceinline__ T det3(const T A[9]) {
+    return A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) + A[2] * (A[3] * A[7] - A[4] * A[6]);
+}
+// inverse-transpose B = A^{-T}, returns det
+template <class T> __device__ __forceinline__ T inv_transpose3(const T A[9], T B[9]) {
+    T c00 = A[4] * A[8] - A[5] * A[7], c01 = A[5] * A[6] - A[3] * A[8], c02 = A[3] * A[7] - A[4] * A[6];
+    T c10 = A[2] * A[7] - A[1] * A[8], c11 = A[0] * A[8] - A[2] * A[6], c12 = A[1] * A[6] - A[0] * A[7];
+    T c20 = A[1] * A[5] - A[2] * A[4], c21 = A[2] * A[3] - A[0] * A[5], c22 = A[0] * A[4] - A[1] * A[3];
+    T det = A[0] * c00 + A[1] * c01 + A[2] * c02;
+    T id = T(1) / det;
+    // A^{-1}_{ab} = cof_{ba}/det  =>  A^{-T}_{ab} = cof_{ab}/det
+    B[0] = c00 * id; B[1] = c01 * id; B[2] = c02 * id;
+    B[3] = c10 * id; B[4] = c11 * id; B[5] = c12 * id;
+    B[6] = c20 * id; B[7] = c21 * id; B[8] = c22 * id;
+    return det;
+}
+
+// One Jacobi rotation zeroing S[p][q] of a symmetric 3x3 (NR convention), accumulating Q.
+template <class T, int p, int q, int r>
+__device__ __forceinline__ void jrot(T S[9], T Q[9]) {
+    T apq = S[3 * p + q];
+    if (apq == T(0)) return;
+    T theta = (S[3 * q + q] - S[3 * p + p]) / (T(2) * apq);
+    T t = T(1) / (mabs(theta) + msqrt(theta * theta + T(1)));
+    t = theta < T(0) ? -t : t;
+    T c = mrsqrt(t * t + T(1)), s = t * c;
+    T app = S[3 * p + p] - t * apq, aqq = S[3 * q + q] + t * apq;
+    T arp = S[3 * r + p], arq = S[3 * r + q];
+    T nrp = c * arp - s * arq, nrq = s * arp + c * arq;
+    S[3 * p + p] = app; S[3 * q + q] = aqq;
+    S[3 * p + q] = S[3 * q + p] = T(0);
+    S[3 * r + p] = S[3 * p + r] = nrp;
+    S[3 * r + q] = S[3 * q + r] = nrq;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        T qp = Q[3 * a + p], qq = Q[3 * a + q];
+        Q[3 * a + p] = c * qp - s * qq;
+        Q[3 * a + q] = s * qp + c * qq;
+    }
+}
+
+// Symmetric eigen-decomposition by cyclic Jacobi: A = Q diag(w) Q^T (columns of Q).
+template <class T> __device__ __forceinline__ void sym_eig3(const T A[9], T w[3], T Q[9]) {
+    T S[9];
+#pragma unroll
+    for (int a = 0; a < 9; a++) { S[a] = A[a]; Q[a] = (a % 4 == 0) ? T(1) : T(0); }
+    const int maxsweep = sizeof(T) == 4 ? 6 : 10;
+    const T tol = sizeof(T) == 4 ? T(1e-14) : T(1e-30);
+    for (int sw = 0; sw < maxsweep; sw++) {
+        T off = S[1] * S[1] + S[2] * S[2] + S[5] * S[5];
+        T dia = S[0] * S[0] + S[4] * S[4] + S[8] * S[8];
+        if (!(off > tol * dia)) break;
+        jrot<T, 0, 1, 2>(S, Q);
+        jrot<T, 0, 2, 1>(S, Q);
+        jrot<T, 1, 2, 0>(S, Q);
+    }
+    w[0] = S[0]; w[1] = S[4]; w[2] = S[8];
+}
+
+// Divided difference of log (Daleckii-Krein), from eigenvalues lx = x-1, ly = y-1 of b - I (amb-20)
+template <class T> __device__ __forceinline__ T dlog(T lx, T ly) {
+    T y = T(1) + ly;
+    T t = (lx - ly) / y;
+    const T thr = sizeof(T) == 4 ? T(2e-2) : T(1e-3);
+    if (mabs(t) < thr) return (T(1) + t * (T(-0.5) + t * (T(1) / T(3) + t * (T(-0.25) + t * T(0.2))))) / y;
+    return mlog1p(t) / (lx - ly);
+}
+
+// symmetric 9x9 upper-triangle packing: row r (r = 3a+b) stores s = r..8
+__host__ __device__ __forceinline__ constexpr int kofs(int r) { return r * 9 - (r * (r - 1)) / 2; }
+__host__ __device__ __forceinline__ constexpr int kidx(int r, int s) { return kofs(r) + (s - r); }
+
+// warp/block reductions (double)
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+// adds v from every thread of the block into *out (one atomic per warp)
+__device__ __forceinline__ void block_add(double v, double *out) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0 && v != 0.0) atomicAdd(out, v);
+}
+
+// ------------------------------------------------------------------------------------------
+// host-side context
+// ------------------------------------------------------------------------------------------
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+
+// Per-Newton-iteration PCG accumulators (one slot per CG iteration; fp64)
+struct CGSlot {
+    double rz;   // r_j . z_j
+    double rr;   // r_j . r_j
+    double pHp;  // p_j . H p_j
+    double pad;
+};
+
+// device-side scalar block (fp64 accumulators and flags)
+struct DevScalars {
+    double energy;     // Phi accumulator
+    double gnorm2;     // ||g_free||^2
+    double gp;         // g . p
+    double aux;
+    int inverted;      // det(I + dt G) <= 0 seen
+    int nonfinite;
+    int oob_particle;  // min index of an out-of-domain particle (INT_MAX = none)
+    int inv_particle;  // min index of an inverted particle
+    int neg_curv;      // PCG breakdown (p.Hp <= 0)
+    int cg_done_iter;  // first iteration index at which PCG converged (or -1)
+    int pad[2];
+};
+
+struct mpl_ctx_s {
+    int precision = 32, device = 0, rank = 0, nranks = 1;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+
+    GridP grid{};
+    MatP mats{};
+    BoxP boxes{};
+    double gravity[3] = {0.0, -9.81, 0.0};
+    double dt = 0.0;
+
+    // particles (sorted layout; ping-pong A/B)
+    int64_t np = 0;
+    int cur = 0;  // which particle buffer set is current
+    DevBuf px[2], pF[2], pv, pG, pvol[2], pmat[2], pid[2];
+    DevBuf pkey, prank, prec, pbase, pskey;  // per-particle scratch; pskey/prec in sorted order
+
+    // tiles
+    int T = 0;
+    int64_t C = 0;  // compact cells incl. padding
+    int64_t n_cells_active = 0, n_nodes_active = 0, n_blocks_active = 0;
+    int dense_n = 0;  // nb0*nb1*nb2
+    DevBuf cflag, nflag, tile_of, scan_tmp;
+    DevBuf t_coord, t_nplus, t_nminus, t_cstart, t_ccount, t_hascells, t_bcount, t_bstart, t_cellof, t_cmask;
+    DevBuf c_local;
+    // quadrature (compact cells)
+    DevBuf q_m, q_mv, q_mG, q_slot;  // q_slot: C * nmat * 8 (V, E xx yy zz xy yz xz, pad)
+    DevBuf q_vc, q_Gc;               // load: v_c, G_c
+    DevBuf K;                        // C * 45 tangent (scaled by 1/(16 dx^2))
+    // nodes (tile-dense, T*64)
+    DevBuf n_mass, n_flag, n_vn, n_vhat, n_v, n_vt, n_g, n_diag, n_x, n_r, n_p, n_Hp, n_u, n_u2, n_act;
+    // canonical node index per tile-dense node (-1 inactive)
+    DevBuf n_canon, n_list;  // n_list: canonical -> tile-dense index
+    DevBuf scalars, cg_slots, io_stage, io_stage2;
+    int cg_slot_cap = 0;
+    DevBuf host_pinned;  // small pinned staging
+    bool have_particles = false, resampled = false, linearized = false, solved = false;
+    std::vector<cudaEvent_t> ev;
+};
+
+// ------------------------------------------------------------------------------------------
+// error helpers
+// ------------------------------------------------------------------------------------------
+#define MPL_CUDA(call)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            ctx->err = std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " +  \
+                       __FILE__ + ":" + std::to_string(__LINE__);                       \
+            return MPL_ERR_CUDA;                                                        \
+        }                                                                               \
+    } while (0)
+
+#define MPL_CHECK(st)                \
+    do {                             \
+        mpl_status s_ = (st);        \
+        if (s_ != MPL_OK) return s_; \
+    } while (0)
+
+mpl_status ensure(mpl_ctx ctx, DevBuf &b, size_t bytes);
+
+// kernels' host launchers (defined in k_*.cu), templated on the compute precision
+template <class T> mpl_status resample_impl(mpl_ctx ctx, double dt);
+template <class T> mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi);
+template <class T> mpl_status hvp_tile(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *pHp_accum);
+template <class T> mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *st);
+template <class T> mpl_status g2p_impl(mpl_ctx ctx, double dt);
+template <class T> mpl_status canon_to_tile(mpl_ctx ctx, const void *src, void *dst_tile);
+template <class T> mpl_status tile_to_canon(mpl_ctx ctx, const void *src_tile, void *dst);
+template <class T> mpl_status export_quadrature(mpl_ctx ctx, int32_t *ijk, void *m_c, void *v_c, void *G_c,
+                                                void *V_ck, void *tau_ck, void *S_ck);
+template <class T> mpl_status export_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G);
+template <class T> mpl_status import_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v, const void *F,
+                                               const void *G, const void *vol, const int32_t *mat);
+
+enum { LIN_ENERGY = 0, LIN_GRAD = 1, LIN_FULL = 2 };

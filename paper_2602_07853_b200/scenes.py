@@ -215,6 +215,8 @@ def _assemble(name, precision, n, dt, materials, x, v, F, G, mat, ppc, dirichlet
     dt_ = np.float32 if precision == 32 else np.float64
     dx = 1.0 / n
     vol = np.full(x.shape[0], dx ** 3 / ppc, dtype=dt_)
+    if precision == 32:  # Phi is resolved to ~1e-7 relative in fp32 (amb-6 slack)
+        solver = dataclasses.replace(solver, ls_slack=max(solver.ls_slack, 1e-6))
     return Scene(name=name, precision=precision, n=(n, n, n), dx=dx, dt=dt, materials=materials,
                  x=np.ascontiguousarray(x, dtype=dt_), v=np.ascontiguousarray(v, dtype=dt_),
                  F=np.ascontiguousarray(F, dtype=dt_), G=np.ascontiguousarray(G, dtype=dt_),

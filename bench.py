@@ -149,19 +149,11 @@ def run_ours(args):
     ms_total = e0.elapsed_time(e1)
     n_hvp = sum(s["n_hvp"] for s in stats)
     hvp_ms = sum(s["hvp_ms"] for s in stats)
-    # free DOFs per step (active nodes minus prescribed ones)
-    ijk, m, vn, fr = (None,) * 4
-    dofs = []
-    cells = []
-    nodes = []
-    for c, s in zip(counts, stats):
-        cells.append(c.n_cells)
-        nodes.append(c.n_nodes)
-    # the last resample's free-DOF count (Dirichlet floor) -- nodes change only slightly per step
-    ctx.resample(sc.dt)
-    _, _, _, fr = ctx.get_nodes()
-    n_free = int(fr.sum())
-    dof_hvp = 3.0 * n_free * n_hvp
+    cells = [s["n_cells"] for s in stats]
+    nodes = [s["n_nodes"] for s in stats]
+    # HVP DOF throughput: each step's free DOFs times that step's HVP launches
+    dof_hvp = sum(3.0 * s["n_free_nodes"] * s["n_hvp"] for s in stats)
+    n_free = int(statistics.mean(s["n_free_nodes"] for s in stats))
     gdofs = dof_hvp / (hvp_ms * 1e-3) / 1e9 if hvp_ms > 0 else 0.0
     ms_per_step = ms_total / args.steps
     if ws > 1:
@@ -177,7 +169,7 @@ def run_ours(args):
     peak, peak_kind = load_peaks()
     achieved = nbytes / (avg_hvp_ms * 1e-3) / 1e9
     # e2e: the same metric through the C ABI with HOST buffers (H2D of particles, D2H of results)
-    e2e = run_e2e(ctx, sc, solver, stream, args) if rank == 0 else None
+    e2e = run_e2e(ctx, sc, solver, stream, args) if (rank == 0 and not args.no_e2e) else None
     clocks = clk.summary()
     result = {
         "metric": "HVP GDOF/s (matrix-free incremental-potential Hessian-vector product inside Newton-PCG)",
@@ -212,7 +204,12 @@ def run_ours(args):
                      "peak_kind": peak_kind, "kernel": "k_hvp",
                      "algorithmic_bytes_per_launch": int(nbytes), "pct_of_8TBps": round(achieved / 8000.0, 4)},
         "e2e": e2e,
-        "gpu_launches": int(sum(s.get("n_launches", 0) for s in stats)) or None,
+        "gpu_launches": int(sum(s["n_launches"] for s in stats)),
+        "phase_ms": {"resample": round(statistics.mean(s["ms_phase"][0] for s in stats), 3),
+                     "linearize": round(statistics.mean(s["ms_phase"][3] for s in stats), 3),
+                     "pcg": round(statistics.mean(s["ms_phase"][4] for s in stats), 3),
+                     "line_search": round(statistics.mean(s["ms_phase"][5] for s in stats), 3),
+                     "g2p": round(statistics.mean(s["ms_phase"][6] for s in stats), 3)},
         "clocks": clocks,
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -243,13 +240,10 @@ def run_e2e(ctx, sc, solver, stream, args):
         ctx.set_particles(*host, mat)
         st = ctx.step(sc.dt, solver)
         ctx.get_particles(*outs)
-        n_free = ctx.counts.n_nodes  # upper bound refined below
-        n_hvp_dofs += st["n_hvp"]
+        n_hvp_dofs += 3.0 * st["n_free_nodes"] * st["n_hvp"]
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    ctx.resample(sc.dt)
-    _, _, _, fr = ctx.get_nodes()
-    val = 3.0 * int(fr.sum()) * n_hvp_dofs / wall / 1e9
+    val = n_hvp_dofs / wall / 1e9
     return {"value": round(val, 3), "unit": "GDOF/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": round(wall * 1e3 / steps, 3), "steps": steps}
 
@@ -344,6 +338,7 @@ def main():
     ap.add_argument("--precision", type=int, default=32)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -110,7 +110,9 @@ typedef struct {
     int32_t ls_iters[MPL_MAX_NEWTON_LOG];
     int32_t n_hvp;        /* HVP launches in this call                                    */
     double hvp_ms;        /* summed device time of those HVP launches (CUDA events)       */
-    double ms_phase[8];   /* 0 bin+sort, 1 P2Q+stretch, 2 C2N, 3 linearize, 4 PCG, 5 line search, 6 G2P, 7 total */
+    double ms_phase[8];   /* 0 resample, 3 linearize, 4 PCG, 5 line search, 6 G2P, 7 total (ms)   */
+    int64_t n_cells, n_nodes, n_free_nodes; /* quadrature points, active nodes, free (non-Dirichlet) nodes */
+    int64_t n_launches;   /* CUDA kernels launched by the library during this call                */
 } mpl_solve_stats;
 
 /* ---- context ------------------------------------------------------------------------------ */

@@ -178,13 +178,13 @@ mpl_status g2p_impl(mpl_ctx ctx, double dt) {
         k_n2c<T><<<T_, 128, 0, st>>>(ctx->grid, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,
                                      (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p,
                                      (const T *)ctx->q_m.p, (const vec4<T> *)ctx->n_v.p, (vec4<T> *)ctx->q_vc.p,
-                                     (T *)ctx->q_Gc.p);
+                                     (T *)ctx->q_Gc.p); ctx->launches++;
     if (ctx->np)
         k_c2p<T><<<nblk(ctx->np, 256), 256, 0, st>>>(ctx->grid, dt, ctx->np, (const int *)ctx->pskey.p,
                                                     (const int *)ctx->t_nplus.p, (const int *)ctx->t_cellof.p,
                                                     (const vec4<T> *)ctx->q_vc.p, (const T *)ctx->q_Gc.p,
                                                     (T *)ctx->px[c].p, (T *)ctx->pv.p, (T *)ctx->pF[c].p,
-                                                    (T *)ctx->pG.p);
+                                                    (T *)ctx->pG.p); ctx->launches++;
     MPL_CUDA(cudaGetLastError());
     MPL_CUDA(cudaStreamSynchronize(st));
     ctx->resampled = false;  // quadrature state is consumed
@@ -204,7 +204,7 @@ mpl_status export_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G) {
     for (auto &it : items) {
         if (!it.dst || !np) continue;
         k_unsort<T><<<nblk(np * it.w, 256), 256, 0, st>>>(np, it.w, (const int *)ctx->pid[c].p, (const T *)it.src,
-                                                          (T *)ctx->io_stage2.p);
+                                                          (T *)ctx->io_stage2.p); ctx->launches++;
         MPL_CUDA(cudaMemcpyAsync(it.dst, ctx->io_stage2.p, np * it.w * sizeof(T), cudaMemcpyDefault, st));
     }
     MPL_CUDA(cudaGetLastError());
@@ -234,13 +234,13 @@ mpl_status export_quadrature(mpl_ctx ctx, int32_t *ijk, void *m_c, void *v_c, vo
         return MPL_ERR_OOM;
     }
     if (C) {
-        k_ccanon_flags<<<nblk(C, 256), 256, 0, st>>>(C, (const uint8_t *)ctx->c_local.p, (int *)act.p);
+        k_ccanon_flags<<<nblk(C, 256), 256, 0, st>>>(C, (const uint8_t *)ctx->c_local.p, (int *)act.p); ctx->launches++;
         size_t tmp = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, tmp, (const int *)act.p, (int *)canon.p, (int)C, st);
         void *tp = nullptr;
         cudaMalloc(&tp, tmp + 16);
         cub::DeviceScan::ExclusiveSum(tp, tmp, (const int *)act.p, (int *)canon.p, (int)C, st);
-        k_ccanon_fix<<<nblk(C, 256), 256, 0, st>>>(C, (const uint8_t *)ctx->c_local.p, (int *)canon.p);
+        k_ccanon_fix<<<nblk(C, 256), 256, 0, st>>>(C, (const uint8_t *)ctx->c_local.p, (int *)canon.p); ctx->launches++;
         char *o = (char *)out.p;
         int32_t *d_ijk = (int32_t *)o; o += n * 3 * 4;
         T *d_m = (T *)o; o += n * s;
@@ -253,7 +253,7 @@ mpl_status export_quadrature(mpl_ctx ctx, int32_t *ijk, void *m_c, void *v_c, vo
                                                     (const int *)ctx->t_cstart.p, ctx->T, (const uint8_t *)ctx->c_local.p,
                                                     (const int *)canon.p, (const T *)ctx->q_m.p, (const T *)ctx->q_mv.p,
                                                     (const T *)ctx->q_mG.p, (const T *)ctx->q_slot.p, d_ijk, d_m, d_v, d_G,
-                                                    d_V, d_tau, d_S, n);
+                                                    d_V, d_tau, d_S, n); ctx->launches++;
         if (ijk) cudaMemcpyAsync(ijk, d_ijk, n * 3 * 4, cudaMemcpyDefault, st);
         if (m_c) cudaMemcpyAsync(m_c, d_m, n * s, cudaMemcpyDefault, st);
         if (v_c) cudaMemcpyAsync(v_c, d_v, n * 3 * s, cudaMemcpyDefault, st);

@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(64) k_c2n(GridP g, BoxP bx, double dt, double 
                                             const T *__restrict__ q_mv, const T *__restrict__ q_mG,
                                             T *__restrict__ n_mass, uint8_t *__restrict__ n_flag,
                                             vec4<T> *__restrict__ n_vn, vec4<T> *__restrict__ n_vhat,
-                                            vec4<T> *__restrict__ n_v) {
+                                            vec4<T> *__restrict__ n_v, unsigned long long *__restrict__ nfree) {
     int t = blockIdx.x;
     int l = threadIdx.x;
     int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
@@ -390,6 +390,8 @@ __global__ void __launch_bounds__(64) k_c2n(GridP g, BoxP bx, double dt, double 
             }
         }
     }
+    unsigned int fb = __ballot_sync(0xffffffffu, flag == 1);
+    if ((threadIdx.x & 31) == 0 && fb) atomicAdd(nfree, (unsigned long long)__popc(fb));
     n_mass[nidx] = m;
     n_flag[nidx] = flag;
     n_vn[nidx] = vn;
@@ -425,6 +427,7 @@ mpl_status exclusive_scan(mpl_ctx ctx, const I *in, I *out, int64_t n) {
     MPL_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int)n, ctx->stream));
     MPL_CHECK(ensure(ctx, ctx->scan_tmp, tmp + 256));
     MPL_CUDA(cub::DeviceScan::ExclusiveSum(ctx->scan_tmp.p, tmp, in, out, (int)n, ctx->stream));
+    ctx->launches += 2;  // cub: init + scan kernels
     return MPL_OK;
 }
 
@@ -461,7 +464,7 @@ mpl_status import_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v
     MPL_CUDA(cudaMemcpyAsync(ctx->pG.p, G, n * 9 * s, cudaMemcpyDefault, st));
     MPL_CUDA(cudaMemcpyAsync(ctx->pvol[0].p, vol, n * s, cudaMemcpyDefault, st));
     MPL_CUDA(cudaMemcpyAsync(ctx->pmat[0].p, mat, n * 4, cudaMemcpyDefault, st));
-    if (n) k_iota<<<nblk(n, 256), 256, 0, st>>>(n, (int *)ctx->pid[0].p);
+    if (n) k_iota<<<nblk(n, 256), 256, 0, st>>>(n, (int *)ctx->pid[0].p); ctx->launches++;
     MPL_CUDA(cudaGetLastError());
     MPL_CUDA(cudaStreamSynchronize(st));
     return MPL_OK;
@@ -490,13 +493,13 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CHECK(ensure(ctx, ctx->tile_of, (size_t)(N + 1) * 4));
     MPL_CUDA(cudaMemsetAsync(ctx->cflag.p, 0, (size_t)N * 4, st));
     MPL_CUDA(cudaMemsetAsync(ctx->nflag.p, 0, (size_t)N * 4, st));
-    unsigned long long *counters = (unsigned long long *)((char *)ctx->scalars.p + 256);
+    unsigned long long *counters = (unsigned long long *)((char *)ctx->scalars.p + 2048);
     MPL_CUDA(cudaMemsetAsync(counters, 0, 64, st));
 
     // a0: base cells + active cell blocks
     if (np) k_bin_flags<T><<<nblk(np, 256), 256, 0, st>>>(g, np, (const T *)ctx->px[c].p, (const int *)ctx->pid[c].p,
-                                                         (int *)ctx->pbase.p, (int *)ctx->cflag.p, sc);
-    k_node_flags<<<nblk(N, 256), 256, 0, st>>>(g, (const int *)ctx->cflag.p, (int *)ctx->nflag.p, counters + 0);
+                                                         (int *)ctx->pbase.p, (int *)ctx->cflag.p, sc); ctx->launches++;
+    k_node_flags<<<nblk(N, 256), 256, 0, st>>>(g, (const int *)ctx->cflag.p, (int *)ctx->nflag.p, counters + 0); ctx->launches++;
     MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->nflag.p, (int *)ctx->tile_of.p, N + 0));
     // fetch error flags + tile count (one sync)
     DevScalars hs;
@@ -525,14 +528,14 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CHECK(ensure(ctx, ctx->t_bcount, ((size_t)T_ * 64 + 1) * 4 + 16));
     MPL_CHECK(ensure(ctx, ctx->t_bstart, ((size_t)T_ * 64 + 1) * 4 + 16));
     MPL_CHECK(ensure(ctx, ctx->t_cellof, (size_t)T_ * 64 * 4 + 16));
-    k_tiles<<<nblk(N, 256), 256, 0, st>>>(g, (const int *)ctx->nflag.p, (int *)ctx->tile_of.p, (int *)ctx->t_coord.p);
+    k_tiles<<<nblk(N, 256), 256, 0, st>>>(g, (const int *)ctx->nflag.p, (int *)ctx->tile_of.p, (int *)ctx->t_coord.p); ctx->launches++;
     if (T_) k_tile_nbrs<<<nblk(T_, 128), 128, 0, st>>>(g, T_, (const int *)ctx->t_coord.p, (const int *)ctx->tile_of.p,
                                                      (const int *)ctx->cflag.p, (int *)ctx->t_nplus.p,
-                                                     (int *)ctx->t_nminus.p, (int *)ctx->t_hascells.p);
+                                                     (int *)ctx->t_nminus.p, (int *)ctx->t_hascells.p); ctx->launches++;
     // particle buckets: key = tile*64 + local base cell; counting sort
     MPL_CUDA(cudaMemsetAsync(ctx->t_bcount.p, 0, ((size_t)T_ * 64 + 1) * 4, st));
     if (np) k_count<<<nblk(np, 256), 256, 0, st>>>(g, np, (const int *)ctx->pbase.p, (const int *)ctx->tile_of.p,
-                                                  (int *)ctx->pkey.p, (int *)ctx->prank.p, (int *)ctx->t_bcount.p);
+                                                  (int *)ctx->pkey.p, (int *)ctx->prank.p, (int *)ctx->t_bcount.p); ctx->launches++;
     MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_bcount.p, (int *)ctx->t_bstart.p, (int64_t)T_ * 64 + 1));
     // scatter into sorted order + records
     MPL_CHECK(ensure(ctx, ctx->pskey, (size_t)np * 4 + 16));
@@ -542,14 +545,14 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
             (const T *)ctx->px[c].p, (const T *)ctx->pv.p, (const T *)ctx->pF[c].p, (const T *)ctx->pG.p,
             (const T *)ctx->pvol[c].p, (const int *)ctx->pmat[c].p, (const int *)ctx->pid[c].p, (T *)ctx->px[nx].p,
             (T *)ctx->pF[nx].p, (T *)ctx->pvol[nx].p, (int *)ctx->pmat[nx].p, (int *)ctx->pid[nx].p,
-            (int *)ctx->pskey.p, (T *)ctx->prec.p, sc);
+            (int *)ctx->pskey.p, (T *)ctx->prec.p, sc); ctx->launches++;
     ctx->cur = nx;
     // structural cells: masks, padded counts, compact offsets
     MPL_CHECK(ensure(ctx, ctx->t_ccount, (size_t)(T_ + 1) * 4 + 16));
     MPL_CUDA(cudaMemsetAsync(ctx->t_ccount.p, 0, (size_t)(T_ + 1) * 4, st));
     if (T_) k_cell_mask<<<T_, 64, 0, st>>>(g, T_, (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p,
                                           (const int *)ctx->t_bcount.p, (unsigned long long *)ctx->t_cmask.p,
-                                          (int *)ctx->t_ccount.p, counters + 1);
+                                          (int *)ctx->t_ccount.p, counters + 1); ctx->launches++;
     MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_ccount.p, (int *)ctx->t_cstart.p, (int64_t)T_ + 1));
     int Cpad = 0;
     unsigned long long ncells = 0;
@@ -577,10 +580,10 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CHECK(ensure(ctx, ctx->K, C * 45 * s + 256));
     if (T_) {
         k_cell_list<<<T_, 64, 0, st>>>(T_, (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_cstart.p,
-                                       (uint8_t *)ctx->c_local.p, (int *)ctx->t_cellof.p);
+                                       (uint8_t *)ctx->c_local.p, (int *)ctx->t_cellof.p); ctx->launches++;
         k_p2q<T><<<T_, 64, 0, st>>>(g, ctx->mats, (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p,
                                     (const int *)ctx->t_bstart.p, (const int *)ctx->t_cellof.p, (const T *)ctx->prec.p,
-                                    (T *)ctx->q_m.p, (T *)ctx->q_mv.p, (T *)ctx->q_mG.p, (T *)ctx->q_slot.p);
+                                    (T *)ctx->q_m.p, (T *)ctx->q_mv.p, (T *)ctx->q_mG.p, (T *)ctx->q_slot.p); ctx->launches++;
     }
     // nodes
     const size_t NN = (size_t)T_ * 64 + 64;
@@ -597,19 +600,23 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
                                     (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p,
                                     (const int *)ctx->t_cellof.p, (const T *)ctx->q_m.p, (const T *)ctx->q_mv.p,
                                     (const T *)ctx->q_mG.p, (T *)ctx->n_mass.p, (uint8_t *)ctx->n_flag.p,
-                                    (vec4<T> *)ctx->n_vn.p, (vec4<T> *)ctx->n_vhat.p, (vec4<T> *)ctx->n_v.p);
+                                    (vec4<T> *)ctx->n_vn.p, (vec4<T> *)ctx->n_vhat.p, (vec4<T> *)ctx->n_v.p,
+                                    counters + 2); ctx->launches++;
     const int64_t NT = (int64_t)T_ * 64;
     int nact = 0;
     if (NT) {
-        k_node_active<<<nblk(NT, 256), 256, 0, st>>>(NT, (const uint8_t *)ctx->n_flag.p, (int *)ctx->n_act.p);
+        k_node_active<<<nblk(NT, 256), 256, 0, st>>>(NT, (const uint8_t *)ctx->n_flag.p, (int *)ctx->n_act.p); ctx->launches++;
         MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->n_act.p, (int *)ctx->n_canon.p, NT));
         int lc = 0, la = 0;  // read before k_node_canon rewrites inactive entries (stream order)
         MPL_CUDA(cudaMemcpyAsync(&lc, (int *)ctx->n_canon.p + (NT - 1), 4, cudaMemcpyDeviceToHost, st));
         MPL_CUDA(cudaMemcpyAsync(&la, (int *)ctx->n_act.p + (NT - 1), 4, cudaMemcpyDeviceToHost, st));
         k_node_canon<<<nblk(NT, 256), 256, 0, st>>>(NT, (const uint8_t *)ctx->n_flag.p, (int *)ctx->n_canon.p,
-                                                    (int *)ctx->n_list.p);
+                                                    (int *)ctx->n_list.p); ctx->launches++;
         MPL_CUDA(cudaStreamSynchronize(st));
         nact = lc + la;
+        unsigned long long nf = 0;
+        MPL_CUDA(cudaMemcpy(&nf, counters + 2, 8, cudaMemcpyDeviceToHost));
+        ctx->n_free_nodes = (int64_t)nf;
     }
     ctx->n_nodes_active = nact;
     MPL_CUDA(cudaGetLastError());

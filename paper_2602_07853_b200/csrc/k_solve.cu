@@ -217,9 +217,9 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
         }
     }
     __syncthreads();
-    if (MODE == LIN_FULL) {  // coalesced copy of the tile's tangent block
-        T *dst = Kout + (int64_t)cs * 45;
-        for (int i = tid; i < nc * 45; i += blockDim.x) dst[i] = Ks[i];
+    if (MODE == LIN_FULL) {  // tile's tangent block, permuted into the chunked (coalesced) layout
+        const int64_t base = (int64_t)cs * 45;
+        for (int i = tid; i < nc * 45; i += blockDim.x) Kout[k_off<T>(base, nc, i / 45, i % 45)] = Ks[i];
     }
     // ---- node phase -----------------------------------------------------------------------
     if (tid < 125) {
@@ -292,120 +292,126 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
             }
         }
     }
-    block_add(e_loc, &sc->energy);
+    block_add(e_loc, sc->energy);
 }
 
 // =============================================================================================
-// a6: HVP  (Hu)_i = m_i u_i + sum_c (K_c : dG_c(u)) grad w_ic   (v1: one tile per CTA)
-// also accumulates u . Hu = sum_i m_i |u_i|^2 + sum_c dG_c : K_c : dG_c (exact, no completion needed)
+// a6: HVP  (Hu)_i = m_i u_i + sum_c (K_c : dG_c(u)) grad w_ic   (one tile per 64-thread CTA)
+//   1. each cell thread loads its 45-number tangent straight into registers with 16-byte loads
+//      that are coalesced across the tile's cells (chunked layout, KL<T>);
+//   2. the 5^3 node halo of u is staged in shared memory;
+//   3. P = K' dG' (81 FMA, symmetric K), scattered to the 8 corners in 8 passes: in pass o every
+//      cell adds to node (cell + o), an injective map, so the shared-memory adds never collide;
+//   4. nodes with all 8 cells in the tile are stored, face nodes are summed with one float4 atomic.
+// Also accumulates u . Hu = sum_i m_i |u_i|^2 + sum_c dG_c : K_c : dG_c (exact without completion).
 // =============================================================================================
+template <class T> __device__ __forceinline__ void ldk(const T *p, T *k);
+template <> __device__ __forceinline__ void ldk<float>(const float *p, float *k) {
+    float4 v = __ldg(reinterpret_cast<const float4 *>(p));
+    k[0] = v.x; k[1] = v.y; k[2] = v.z; k[3] = v.w;
+}
+template <> __device__ __forceinline__ void ldk<double>(const double *p, double *k) {
+    double2 v = __ldg(reinterpret_cast<const double2 *>(p));
+    k[0] = v.x; k[1] = v.y;
+}
+
 template <class T>
-__global__ void __launch_bounds__(128) k_hvp(const int *__restrict__ nplus, const int *__restrict__ cstart,
-                                             const uint8_t *__restrict__ clocal, const int *__restrict__ hascells,
-                                             const T *__restrict__ K, const T *__restrict__ nmass,
-                                             const vec4<T> *__restrict__ u, vec4<T> *__restrict__ Hu,
-                                             double *__restrict__ uHu, const CGSlot *__restrict__ cgs, int cgj,
-                                             double cgthr, const DevScalars *__restrict__ sc) {
-    if (cgs != nullptr && (sc->neg_curv || (cgj > 0 && cgs[cgj].rr <= cgthr))) return;  // PCG converged
+__global__ void __launch_bounds__(64) k_hvp(const int *__restrict__ nplus, const int *__restrict__ cstart,
+                                            const uint8_t *__restrict__ clocal, const int *__restrict__ hascells,
+                                            const T *__restrict__ K, const T *__restrict__ nmass,
+                                            const vec4<T> *__restrict__ u, vec4<T> *__restrict__ Hu,
+                                            double *__restrict__ uHu, const CGSlot *__restrict__ cgs, int cgj,
+                                            double cgthr, const DevScalars *__restrict__ sc) {
     __shared__ vec4<T> uh[125];
-    __shared__ __align__(16) T Ks[64 * 45];
-    __shared__ T Pc[64 * 9];
-    __shared__ int cslot[64];
+    __shared__ T Fs[3][128];
     const int t = blockIdx.x, tid = threadIdx.x;
+    if (cgs != nullptr) {  // inside PCG: skip once converged / broken down (uniform per CTA)
+        double rr = stripe_sum_bcast(cgs[cgj].rr);
+        if (sc->neg_curv || (cgj > 0 && rr <= cgthr)) return;
+    }
     const int has = hascells[t];
-    const int cs = cstart[t], nc = cstart[t + 1] - cs;
-    for (int h = tid; h < 125; h += blockDim.x) {
+    const int cs = cstart[t], ncp = cstart[t + 1] - cs;
+    constexpr int VEC = KL<T>::VEC, NCH = KL<T>::NCH;
+    T k[45];
+    int l = 0xFF;
+    if (tid < ncp) {
+        l = clocal[cs + tid];
+        const T *base = K + (int64_t)cs * 45;
+#pragma unroll
+        for (int c = 0; c < NCH; c++) ldk<T>(base + ((int64_t)c * ncp + tid) * VEC, k + c * VEC);
+        k[44] = __ldg(base + (int64_t)NCH * VEC * ncp + tid);
+    }
+    for (int h = tid; h < 125; h += 64) {
         int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
         bool owned = hx < 4 && hy < 4 && hz < 4;
         int64_t n = (has || owned) ? halo_node(t, nplus, h) : -1;
         uh[h] = n >= 0 ? u[n] : mk4<T>(0, 0, 0, 0);
-    }
-    if (tid < 64) cslot[tid] = -1;
-    {   // coalesced 16-byte copy of the tile's tangent block (nc multiple of 4 => 16B multiple)
-        const int nvec = nc * 45 * (int)sizeof(T) / 16;
-        const int4 *src = reinterpret_cast<const int4 *>(K + (int64_t)cs * 45);
-        int4 *dst = reinterpret_cast<int4 *>(Ks);
-        for (int i = tid; i < nvec; i += blockDim.x) dst[i] = __ldg(src + i);
+        Fs[0][h] = Fs[1][h] = Fs[2][h] = T(0);
     }
     __syncthreads();
     double acc = 0.0;
-    if (tid < nc) {
-        int l = clocal[cs + tid];
-        if (l != 0xFF) {
-            cslot[l] = tid;
-            int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
-            T dG[9];
+    const bool act = (l != 0xFF);
+    const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+    T P[9];
+    if (act) {
+        T dG[9];
 #pragma unroll
-            for (int a = 0; a < 9; a++) dG[a] = T(0);
+        for (int a = 0; a < 9; a++) dG[a] = T(0);
 #pragma unroll
-            for (int o = 0; o < 8; o++) {
-                int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
-                vec4<T> w = uh[((lx + ox) * 5 + ly + oy) * 5 + lz + oz];
-                T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
-                dG[0] += w.x * s0; dG[1] += w.x * s1; dG[2] += w.x * s2;
-                dG[3] += w.y * s0; dG[4] += w.y * s1; dG[5] += w.y * s2;
-                dG[6] += w.z * s0; dG[7] += w.z * s1; dG[8] += w.z * s2;
+        for (int o = 0; o < 8; o++) {
+            const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+            vec4<T> w = uh[((lx + ox) * 5 + ly + oy) * 5 + lz + oz];
+            const T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
+            dG[0] += w.x * s0; dG[1] += w.x * s1; dG[2] += w.x * s2;
+            dG[3] += w.y * s0; dG[4] += w.y * s1; dG[5] += w.y * s2;
+            dG[6] += w.z * s0; dG[7] += w.z * s1; dG[8] += w.z * s2;
+        }
+#pragma unroll
+        for (int r = 0; r < 9; r++) P[r] = k[kidx(r, r)] * dG[r];
+#pragma unroll
+        for (int r = 0; r < 9; r++)
+#pragma unroll
+            for (int q = r + 1; q < 9; q++) {
+                P[r] += k[kidx(r, q)] * dG[q];
+                P[q] += k[kidx(r, q)] * dG[r];
             }
-            const T *Kr = Ks + tid * 45;
-            T P[9];
+        T qf = T(0);
 #pragma unroll
-            for (int r = 0; r < 9; r++) P[r] = T(0);
+        for (int r = 0; r < 9; r++) qf += P[r] * dG[r];
+        acc += (double)qf;
+    }
+    if (has) {
 #pragma unroll
-            for (int r = 0; r < 9; r++) {
-                P[r] += Kr[kidx(r, r)] * dG[r];
-#pragma unroll
-                for (int s = r + 1; s < 9; s++) {
-                    T k = Kr[kidx(r, s)];
-                    P[r] += k * dG[s];
-                    P[s] += k * dG[r];
-                }
+        for (int o = 0; o < 8; o++) {
+            if (act) {
+                const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+                const T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
+                const int h = ((lx + ox) * 5 + ly + oy) * 5 + lz + oz;
+                Fs[0][h] += P[0] * s0 + P[1] * s1 + P[2] * s2;
+                Fs[1][h] += P[3] * s0 + P[4] * s1 + P[5] * s2;
+                Fs[2][h] += P[6] * s0 + P[7] * s1 + P[8] * s2;
             }
-            T q = T(0);
-#pragma unroll
-            for (int r = 0; r < 9; r++) { Pc[l * 9 + r] = P[r]; q += P[r] * dG[r]; }
-            acc += (double)q;
+            __syncthreads();
         }
     }
-    __syncthreads();
-    if (tid < 125) {
-        int h = tid;
+    for (int h = tid; h < 125; h += 64) {
         int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
         bool owned = hx < 4 && hy < 4 && hz < 4;
+        if (!has && !owned) continue;
         bool interior = hx >= 1 && hx <= 3 && hy >= 1 && hy <= 3 && hz >= 1 && hz <= 3;
-        T f[3] = {0, 0, 0};
-        bool any = false;
-        if (has) {
-#pragma unroll
-            for (int o = 0; o < 8; o++) {
-                int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
-                int cx = hx - ox, cy = hy - oy, cz = hz - oz;
-                if (cx < 0 || cy < 0 || cz < 0 || cx > 3 || cy > 3 || cz > 3) continue;
-                int l = local_id(cx, cy, cz);
-                if (cslot[l] < 0) continue;
-                any = true;
-                T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
-                const T *P = Pc + l * 9;
-                f[0] += P[0] * s0 + P[1] * s1 + P[2] * s2;
-                f[1] += P[3] * s0 + P[4] * s1 + P[5] * s2;
-                f[2] += P[6] * s0 + P[7] * s1 + P[8] * s2;
+        int64_t n = halo_node(t, nplus, h);
+        if (n < 0) continue;
+        T f0 = Fs[0][h], f1 = Fs[1][h], f2 = Fs[2][h];
+        if (owned) {
+            T m = nmass[n];
+            if (m > T(0)) {
+                vec4<T> w = uh[h];
+                f0 += m * w.x; f1 += m * w.y; f2 += m * w.z;
+                acc += (double)(m * (w.x * w.x + w.y * w.y + w.z * w.z));
             }
         }
-        int64_t n = (owned || has) ? halo_node(t, nplus, h) : -1;
-        if (n >= 0) {
-            if (owned) {
-                T m = nmass[n];
-                if (m > T(0)) {
-                    vec4<T> w = uh[h];
-                    f[0] += m * w.x; f[1] += m * w.y; f[2] += m * w.z;
-                    acc += (double)(m * (w.x * w.x + w.y * w.y + w.z * w.z));
-                    any = true;
-                }
-            }
-            if (any) {
-                if (interior) Hu[n] = mk4<T>(f[0], f[1], f[2], T(0));
-                else atomic_add3<T>(Hu + n, f[0], f[1], f[2]);
-            }
-        }
+        if (interior) Hu[n] = mk4<T>(f0, f1, f2, T(0));
+        else if (f0 != T(0) || f1 != T(0) || f2 != T(0)) atomic_add3<T>(Hu + n, f0, f1, f2);
     }
     if (uHu) block_add(acc, uHu);
 }
@@ -432,25 +438,21 @@ __global__ void k_pcg_init(int64_t N, const uint8_t *__restrict__ flag, const ve
         p[i] = zv;
         x[i] = mk4<T>(0, 0, 0, 0);
     }
-    block_add(rz, &slot[0].rz);
-    block_add(rr, &slot[0].rr);
+    block_add(rz, slot[0].rz);
+    block_add(rr, slot[0].rr);
 }
 
-// converged / broken down before iteration j?
-__device__ __forceinline__ bool cg_stop(const CGSlot *slot, int j, double thr, const DevScalars *sc) {
-    if (sc->neg_curv) return true;
-    return j > 0 && slot[j].rr <= thr;
-}
-
-// x += alpha p ; r -= alpha Hp ; z = D^{-1} r ; slot[j+1] = (r.z, r.r)
+// x += alpha p ; r -= alpha Hp ; z = D^{-1} r ; slot[j+1] = (r.z, r.r) ; Hp := 0 for the next HVP
 template <class T>
-__global__ void k_pcg_update1(int64_t N, int j, double thr, const uint8_t *__restrict__ flag,
-                              const vec4<T> *__restrict__ D, const vec4<T> *__restrict__ p,
-                              const vec4<T> *__restrict__ Hp, vec4<T> *__restrict__ x, vec4<T> *__restrict__ r,
-                              CGSlot *slot, DevScalars *sc) {
-    if (cg_stop(slot, j, thr, sc)) return;
-    double pHp = slot[j].pHp;
-    if (!(pHp > 0.0)) {  // breakdown (negative curvature): first iteration returns p = z_0
+__global__ void __launch_bounds__(256) k_pcg_update1(int64_t N, int j, double thr, const uint8_t *__restrict__ flag,
+                                                     const vec4<T> *__restrict__ D, const vec4<T> *__restrict__ p,
+                                                     vec4<T> *__restrict__ Hp, vec4<T> *__restrict__ x,
+                                                     vec4<T> *__restrict__ r, CGSlot *slot, DevScalars *sc) {
+    const double rr_j = stripe_sum_bcast(slot[j].rr);
+    if (sc->neg_curv || (j > 0 && rr_j <= thr)) return;  // converged before iteration j
+    const double pHp = stripe_sum_bcast(slot[j].pHp);
+    const double rz_j = stripe_sum_bcast(slot[j].rz);
+    if (!(pHp > 0.0)) {  // breakdown (negative curvature): the first iteration returns p = z_0
         if (j == 0)
             for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
                 x[i] = p[i];
@@ -460,11 +462,13 @@ __global__ void k_pcg_update1(int64_t N, int j, double thr, const uint8_t *__res
         }
         return;
     }
-    const T alpha = T(slot[j].rz / pHp);
+    const T alpha = T(rz_j / pHp);
     double rz = 0, rr = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        vec4<T> hv = Hp[i];
+        Hp[i] = mk4<T>(0, 0, 0, 0);
         if (flag[i] != 1) continue;
-        vec4<T> pv = p[i], hv = Hp[i], xv = x[i], rv = r[i], dv = D[i];
+        vec4<T> pv = p[i], xv = x[i], rv = r[i], dv = D[i];
         xv.x += alpha * pv.x; xv.y += alpha * pv.y; xv.z += alpha * pv.z;
         rv.x -= alpha * hv.x; rv.y -= alpha * hv.y; rv.z -= alpha * hv.z;
         x[i] = xv;
@@ -472,19 +476,21 @@ __global__ void k_pcg_update1(int64_t N, int j, double thr, const uint8_t *__res
         rz += (double)(rv.x * rv.x / dv.x + rv.y * rv.y / dv.y + rv.z * rv.z / dv.z);
         rr += (double)(rv.x * rv.x + rv.y * rv.y + rv.z * rv.z);
     }
-    block_add(rz, &slot[j + 1].rz);
-    block_add(rr, &slot[j + 1].rr);
+    block_add(rz, slot[j + 1].rz);
+    block_add(rr, slot[j + 1].rr);
 }
 
-// p = z + beta p, beta = rz_{j+1} / rz_j ; also zeroes Hp for the next HVP's atomics
+// p = z + beta p, beta = rz_{j+1} / rz_j
 template <class T>
-__global__ void k_pcg_update2(int64_t N, int j, double thr, const uint8_t *__restrict__ flag,
-                              const vec4<T> *__restrict__ D, const vec4<T> *__restrict__ r, vec4<T> *__restrict__ p,
-                              vec4<T> *__restrict__ Hp, const CGSlot *slot, const DevScalars *sc) {
-    if (cg_stop(slot, j + 1, thr, sc)) return;
-    const T beta = T(slot[j + 1].rz / slot[j].rz);
+__global__ void __launch_bounds__(256) k_pcg_update2(int64_t N, int j, double thr, const uint8_t *__restrict__ flag,
+                                                     const vec4<T> *__restrict__ D, const vec4<T> *__restrict__ r,
+                                                     vec4<T> *__restrict__ p, const CGSlot *slot,
+                                                     const DevScalars *sc) {
+    const double rr = stripe_sum_bcast(slot[j + 1].rr);
+    if (sc->neg_curv || rr <= thr) return;
+    const double rz1 = stripe_sum_bcast(slot[j + 1].rz), rz0 = stripe_sum_bcast(slot[j].rz);
+    const T beta = T(rz1 / rz0);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
-        Hp[i] = mk4<T>(0, 0, 0, 0);
         if (flag[i] != 1) continue;
         vec4<T> rv = r[i], dv = D[i], pv = p[i];
         p[i] = mk4<T>(rv.x / dv.x + beta * pv.x, rv.y / dv.y + beta * pv.y, rv.z / dv.z + beta * pv.z, 0);
@@ -560,7 +566,7 @@ mpl_status canon_to_tile(mpl_ctx ctx, const void *src, void *dst_tile) {
     MPL_CUDA(cudaMemcpyAsync(ctx->io_stage.p, src, n * 3 * sizeof(T), cudaMemcpyDefault, st));
     MPL_CUDA(cudaMemsetAsync(dst_tile, 0, NT * sizeof(vec4<T>), st));
     if (n) k_canon_to_tile<T><<<nblk(n, 256), 256, 0, st>>>(n, (const int *)ctx->n_list.p, (const T *)ctx->io_stage.p,
-                                                          (vec4<T> *)dst_tile);
+                                                          (vec4<T> *)dst_tile); ctx->launches++;
     MPL_CUDA(cudaGetLastError());
     return MPL_OK;
 }
@@ -571,7 +577,7 @@ mpl_status tile_to_canon(mpl_ctx ctx, const void *src_tile, void *dst) {
     cudaStream_t st = ctx->stream;
     MPL_CHECK(ensure(ctx, ctx->io_stage, (size_t)(n * 3 + 4) * sizeof(T)));
     if (n) k_tile_to_canon<T><<<nblk(n, 256), 256, 0, st>>>(n, (const int *)ctx->n_list.p, (const vec4<T> *)src_tile,
-                                                          (T *)ctx->io_stage.p);
+                                                          (T *)ctx->io_stage.p); ctx->launches++;
     MPL_CUDA(cudaMemcpyAsync(dst, ctx->io_stage.p, n * 3 * sizeof(T), cudaMemcpyDefault, st));
     MPL_CUDA(cudaStreamSynchronize(st));
     return MPL_OK;
@@ -584,7 +590,7 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
     const int T_ = ctx->T;
     const int64_t NT = (int64_t)T_ * 64;
     DevScalars *sc = (DevScalars *)ctx->scalars.p;
-    MPL_CUDA(cudaMemsetAsync(&sc->energy, 0, sizeof(double), st));
+    MPL_CUDA(cudaMemsetAsync(sc->energy, 0, sizeof(sc->energy), st));
     MPL_CUDA(cudaMemsetAsync(&sc->inverted, 0, sizeof(int), st));
     if (mode != LIN_ENERGY) MPL_CUDA(cudaMemsetAsync(ctx->n_g.p, 0, NT * sizeof(vec4<T>), st));
     if (mode == LIN_FULL) MPL_CUDA(cudaMemsetAsync(ctx->n_diag.p, 0, NT * sizeof(vec4<T>), st));
@@ -597,16 +603,17 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
         if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY><<<T_, 128, 0, st>>>(LIN_ARGS);
         else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD><<<T_, 128, 0, st>>>(LIN_ARGS);
         else k_linearize<T, LIN_FULL><<<T_, 128, 0, st>>>(LIN_ARGS);
+        ctx->launches++;
 #undef LIN_ARGS
     }
     MPL_CUDA(cudaGetLastError());
     if (phi) {
-        double e = 0;
+        double e[NSTRIPE];
         int inv = 0;
-        MPL_CUDA(cudaMemcpyAsync(&e, &sc->energy, sizeof(double), cudaMemcpyDeviceToHost, st));
+        MPL_CUDA(cudaMemcpyAsync(e, sc->energy, sizeof e, cudaMemcpyDeviceToHost, st));
         MPL_CUDA(cudaMemcpyAsync(&inv, &sc->inverted, sizeof(int), cudaMemcpyDeviceToHost, st));
         MPL_CUDA(cudaStreamSynchronize(st));
-        *phi = inv ? __builtin_inf() : e;
+        *phi = inv ? __builtin_inf() : host_stripes(e);
     }
     if (mode == LIN_FULL) ctx->linearized = true;
     return MPL_OK;
@@ -619,10 +626,10 @@ mpl_status hvp_tile(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu_
     const int T_ = ctx->T;
     MPL_CUDA(cudaMemsetAsync(Hu_tile, 0, (size_t)T_ * 64 * sizeof(vec4<T>), st));
     if (T_)
-        k_hvp<T><<<T_, 128, 0, st>>>((const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,
+        k_hvp<T><<<T_, 64, 0, st>>>((const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,
                                      (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p, (const T *)ctx->K.p,
                                      (const T *)ctx->n_mass.p, (const vec4<T> *)u_tile, (vec4<T> *)Hu_tile, uHu_accum,
-                                     nullptr, 0, 0.0, nullptr);
+                                     nullptr, 0, 0.0, nullptr); ctx->launches++;
     MPL_CUDA(cudaGetLastError());
     return MPL_OK;
 }
@@ -673,19 +680,20 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         MPL_CUDA(cudaMemsetAsync(slots, 0, slots_needed * sizeof(CGSlot), st));
         MPL_CUDA(cudaMemsetAsync(&sc->neg_curv, 0, sizeof(int), st));
         MPL_CUDA(cudaMemsetAsync(&sc->cg_done_iter, 0xff, sizeof(int), st));
-        k_pcg_init<T><<<VG, 256, 0, st>>>(NT, flag, g, D, r, p, x, slots);
+        k_pcg_init<T><<<VG, 256, 0, st>>>(NT, flag, g, D, r, p, x, slots); ctx->launches++;
         MPL_CUDA(cudaMemsetAsync(Hp, 0, NT * sizeof(vec4<T>), st));
         cudaEventRecord(e1, st);
         CGSlot s0;
-        double e = 0;
+        double e[NSTRIPE];
         int inv = 0;
         MPL_CUDA(cudaMemcpyAsync(&s0, slots, sizeof s0, cudaMemcpyDeviceToHost, st));
-        MPL_CUDA(cudaMemcpyAsync(&e, &sc->energy, sizeof e, cudaMemcpyDeviceToHost, st));
+        MPL_CUDA(cudaMemcpyAsync(e, sc->energy, sizeof e, cudaMemcpyDeviceToHost, st));
         MPL_CUDA(cudaMemcpyAsync(&inv, &sc->inverted, sizeof inv, cudaMemcpyDeviceToHost, st));
         MPL_CUDA(cudaStreamSynchronize(st));
         t_lin += elapsed(e0, e1);
-        phi0 = inv ? __builtin_inf() : e;
-        const double gn = sqrt(s0.rr);
+        phi0 = inv ? __builtin_inf() : host_stripes(e);
+        const double rr0 = host_stripes(s0.rr);
+        const double gn = sqrt(rr0);
         if (k == 0) S.grad_norm0 = gn;
         S.grad_norm = gn;
         if (!fixed && gn <= cfg->newton_rtol * S.grad_norm0) {
@@ -694,10 +702,10 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         }
         // ---- PCG on H x = -g -----------------------------------------------------------------
         const int itmax = cfg->fixed_cg_iters ? cfg->fixed_cg_iters[k] : cg_cap;
-        const double thr = cfg->fixed_cg_iters ? -1.0 : cfg->cg_rtol * cfg->cg_rtol * s0.rr;
+        const double thr = cfg->fixed_cg_iters ? -1.0 : cfg->cg_rtol * cfg->cg_rtol * rr0;
         int launched = 0, its = 0;
         cudaEventRecord(e0, st);
-        if (s0.rr > 0.0 && itmax > 0) {
+        if (rr0 > 0.0 && itmax > 0) {
             int chunk = 4;
             bool done = false;
             while (!done && launched < itmax) {
@@ -712,14 +720,14 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     cudaEventRecord(hev[S.n_hvp].first, st);
                     // the HVP is skipped on device once converged (its output is then unused)
                     if (ctx->T)
-                        k_hvp<T><<<ctx->T, 128, 0, st>>>((const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,
+                        k_hvp<T><<<ctx->T, 64, 0, st>>>((const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,
                                                         (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p,
                                                         (const T *)ctx->K.p, (const T *)ctx->n_mass.p, p, Hp,
-                                                        &slots[jj].pHp, slots, jj, thr, sc);
+                                                        slots[jj].pHp, slots, jj, thr, sc); ctx->launches++;
                     cudaEventRecord(hev[S.n_hvp].second, st);
                     S.n_hvp++;
-                    k_pcg_update1<T><<<VG, 256, 0, st>>>(NT, jj, thr, flag, D, p, Hp, x, r, slots, sc);
-                    k_pcg_update2<T><<<VG, 256, 0, st>>>(NT, jj, thr, flag, D, r, p, Hp, slots, sc);
+                    k_pcg_update1<T><<<VG, 256, 0, st>>>(NT, jj, thr, flag, D, p, Hp, x, r, slots, sc); ctx->launches++;
+                    k_pcg_update2<T><<<VG, 256, 0, st>>>(NT, jj, thr, flag, D, r, p, slots, sc); ctx->launches++;
                 }
                 launched += n;
                 MPL_CUDA(cudaGetLastError());
@@ -728,7 +736,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                 MPL_CUDA(cudaMemcpyAsync(&sl, slots + launched, sizeof sl, cudaMemcpyDeviceToHost, st));
                 MPL_CUDA(cudaMemcpyAsync(&neg, &sc->neg_curv, sizeof neg, cudaMemcpyDeviceToHost, st));
                 MPL_CUDA(cudaStreamSynchronize(st));
-                if (neg || sl.rr <= thr) done = true;
+                if (neg || host_stripes(sl.rr) <= thr) done = true;
                 chunk = std::min(chunk * 2, 64);
             }
             hslots.resize(launched + 1);
@@ -743,7 +751,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                 S.neg_curvature++;
             } else {
                 for (int s = 1; s <= launched; s++)
-                    if (hslots[s].rr <= thr) { its = s; break; }
+                    if (host_stripes(hslots[s].rr) <= thr) { its = s; break; }
             }
         }
         cudaEventRecord(e1, st);
@@ -753,19 +761,20 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         S.cg_iters_total += its;
         // ---- Armijo backtracking line search ------------------------------------------------
         cudaEventRecord(e0, st);
-        MPL_CUDA(cudaMemsetAsync(&sc->gp, 0, sizeof(double), st));
-        k_dot_free<T><<<VG, 256, 0, st>>>(NT, flag, g, x, &sc->gp);
-        double gp = 0;
-        MPL_CUDA(cudaMemcpyAsync(&gp, &sc->gp, sizeof gp, cudaMemcpyDeviceToHost, st));
+        MPL_CUDA(cudaMemsetAsync(sc->gp, 0, sizeof(sc->gp), st));
+        k_dot_free<T><<<VG, 256, 0, st>>>(NT, flag, g, x, sc->gp); ctx->launches++;
+        double gps[NSTRIPE];
+        MPL_CUDA(cudaMemcpyAsync(gps, sc->gp, sizeof gps, cudaMemcpyDeviceToHost, st));
         MPL_CUDA(cudaStreamSynchronize(st));
+        const double gp = host_stripes(gps);
         double alpha = 1.0;
         int h = 0;
         if (cfg->fixed_ls_halvings) {
             for (h = 0; h < cfg->fixed_ls_halvings[k]; h++) alpha *= 0.5;
-            k_axpy_free<T><<<VG, 256, 0, st>>>(NT, flag, T(alpha), v, x, vt);
+            k_axpy_free<T><<<VG, 256, 0, st>>>(NT, flag, T(alpha), v, x, vt); ctx->launches++;
         } else {
             for (;;) {
-                k_axpy_free<T><<<VG, 256, 0, st>>>(NT, flag, T(alpha), v, x, vt);
+                k_axpy_free<T><<<VG, 256, 0, st>>>(NT, flag, T(alpha), v, x, vt); ctx->launches++;
                 double phi = 0;
                 MPL_CHECK(energy_at<T>(ctx, vt, &phi));
                 if (std::isinf(phi)) S.n_inverted_trials++;
@@ -786,12 +795,12 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     }
     if (!fixed && S.newton_iters == kmax && !S.converged) {
         MPL_CHECK(linearize_impl<T>(ctx, v, LIN_GRAD, nullptr));
-        MPL_CUDA(cudaMemsetAsync(&sc->gnorm2, 0, sizeof(double), st));
-        k_dot_free<T><<<VG, 256, 0, st>>>(NT, flag, g, g, &sc->gnorm2);
-        double g2 = 0;
-        MPL_CUDA(cudaMemcpyAsync(&g2, &sc->gnorm2, sizeof g2, cudaMemcpyDeviceToHost, st));
+        MPL_CUDA(cudaMemsetAsync(sc->gnorm2, 0, sizeof(sc->gnorm2), st));
+        k_dot_free<T><<<VG, 256, 0, st>>>(NT, flag, g, g, sc->gnorm2); ctx->launches++;
+        double g2[NSTRIPE];
+        MPL_CUDA(cudaMemcpyAsync(g2, sc->gnorm2, sizeof g2, cudaMemcpyDeviceToHost, st));
         MPL_CUDA(cudaStreamSynchronize(st));
-        S.grad_norm = sqrt(g2);
+        S.grad_norm = sqrt(host_stripes(g2));
         if (S.grad_norm <= cfg->newton_rtol * S.grad_norm0) S.converged = 1;
     }
     MPL_CHECK(energy_at<T>(ctx, v, &S.energy));

@@ -368,8 +368,15 @@ mpl_status mpl_newton_step(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_sta
     MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample before mpl_newton_step"));
     if (cfg->newton_max < 0 || cfg->cg_max < 0 || cfg->ls_max < 0) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(set_device(ctx));
+    const int64_t l0 = ctx->launches;
     mpl_status s = DISPATCH(ctx, newton_impl, cfg, stats);
     if (s != MPL_OK) ctx->resampled = false;
+    if (stats) {
+        stats->n_cells = ctx->n_cells_active;
+        stats->n_nodes = ctx->n_nodes_active;
+        stats->n_free_nodes = ctx->n_free_nodes;
+        stats->n_launches = ctx->launches - l0;
+    }
     return s;
 }
 
@@ -398,6 +405,7 @@ mpl_status mpl_step(mpl_ctx ctx, double dt, const mpl_solver_cfg *cfg, mpl_solve
     if (!ctx || !cfg) return MPL_ERR_INVALID_ARG;
     cudaEvent_t e[4];
     for (auto &x : e) cudaEventCreate(&x);
+    const int64_t l0 = ctx->launches;
     cudaEventRecord(e[0], ctx->stream);
     MPL_CHECK(mpl_resample(ctx, dt, nullptr, nullptr, nullptr));
     cudaEventRecord(e[1], ctx->stream);
@@ -415,6 +423,7 @@ mpl_status mpl_step(mpl_ctx ctx, double dt, const mpl_solver_cfg *cfg, mpl_solve
     S.ms_phase[0] = a;  // bin + sort + P2Q + C2N + stretch (resample)
     S.ms_phase[6] = c;
     S.ms_phase[7] = a + b + c;
+    S.n_launches = ctx->launches - l0;
     if (stats) *stats = S;
     return MPL_OK;
 }

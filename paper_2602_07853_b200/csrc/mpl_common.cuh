@@ -162,16 +162,60 @@ template <class T> __device__ __forceinline__ T dlog(T lx, T ly) {
 __host__ __device__ __forceinline__ constexpr int kofs(int r) { return r * 9 - (r * (r - 1)) / 2; }
 __host__ __device__ __forceinline__ constexpr int kidx(int r, int s) { return kofs(r) + (s - r); }
 
-// warp/block reductions (double)
+// warp/block reductions (double).  Cross-CTA sums go to NSTRIPE "striped" accumulators
+// (one fp64 atomic per CTA into stripe blockIdx % NSTRIPE): tens of thousands of same-address
+// atomics per launch serialise in L2, striping removes that contention.
+#define NSTRIPE 32
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
-// adds v from every thread of the block into *out (one atomic per warp)
-__device__ __forceinline__ void block_add(double v, double *out) {
+// all threads of the block must call; adds the block total into acc[blockIdx.x % NSTRIPE]
+__device__ __forceinline__ void block_add(double v, double *acc) {
+    __shared__ double red_[32];
     v = warp_sum(v);
-    if ((threadIdx.x & 31) == 0 && v != 0.0) atomicAdd(out, v);
+    const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red_[w] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double x = threadIdx.x < nw ? red_[threadIdx.x] : 0.0;
+        x = warp_sum(x);
+        if (threadIdx.x == 0 && x != 0.0) atomicAdd(&acc[blockIdx.x % NSTRIPE], x);
+    }
+}
+// sum of NSTRIPE stripes, broadcast to the block (all threads must call)
+__device__ __forceinline__ double stripe_sum_bcast(const double *acc) {
+    __shared__ double s_;
+    if (threadIdx.x < 32) {
+        double x = acc[threadIdx.x];
+        x = warp_sum(x);
+        if (threadIdx.x == 0) s_ = x;
+    }
+    __syncthreads();
+    double r = s_;
+    __syncthreads();
+    return r;
+}
+inline double host_stripes(const double *h) {
+    double s = 0;
+    for (int i = 0; i < NSTRIPE; i++) s += h[i];
+    return s;
+}
+
+// Tangent layout (per tile, ncp = padded cell count): element e < NCH*VEC of cell j at
+// base + ((e / VEC) * ncp + j) * VEC + e % VEC  (16-byte vectors, coalesced across cells);
+// the remaining element (e = 44) at base + NCH*VEC*ncp + j.  base = cstart[t] * 45.
+template <class T> struct KL {
+    static constexpr int VEC = 16 / (int)sizeof(T);
+    static constexpr int NCH = 45 / VEC;
+    static constexpr int REM = 45 - NCH * VEC;
+};
+template <class T> __host__ __device__ __forceinline__ int64_t k_off(int64_t base, int ncp, int j, int e) {
+    return e < KL<T>::NCH * KL<T>::VEC
+               ? base + ((int64_t)(e / KL<T>::VEC) * ncp + j) * KL<T>::VEC + (e % KL<T>::VEC)
+               : base + (int64_t)KL<T>::NCH * KL<T>::VEC * ncp + (int64_t)j * KL<T>::REM + (e - KL<T>::NCH * KL<T>::VEC);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -184,18 +228,16 @@ struct DevBuf {
 
 // Per-Newton-iteration PCG accumulators (one slot per CG iteration; fp64)
 struct CGSlot {
-    double rz;   // r_j . z_j
-    double rr;   // r_j . r_j
-    double pHp;  // p_j . H p_j
-    double pad;
+    double rz[NSTRIPE];   // r_j . z_j   (striped)
+    double rr[NSTRIPE];   // r_j . r_j
+    double pHp[NSTRIPE];  // p_j . H p_j
 };
 
 // device-side scalar block (fp64 accumulators and flags)
 struct DevScalars {
-    double energy;     // Phi accumulator
-    double gnorm2;     // ||g_free||^2
-    double gp;         // g . p
-    double aux;
+    double energy[NSTRIPE];  // Phi accumulator (striped)
+    double gnorm2[NSTRIPE];  // ||g_free||^2
+    double gp[NSTRIPE];      // g . p
     int inverted;      // det(I + dt G) <= 0 seen
     int nonfinite;
     int oob_particle;  // min index of an out-of-domain particle (INT_MAX = none)
@@ -226,7 +268,8 @@ struct mpl_ctx_s {
     // tiles
     int T = 0;
     int64_t C = 0;  // compact cells incl. padding
-    int64_t n_cells_active = 0, n_nodes_active = 0, n_blocks_active = 0;
+    int64_t n_cells_active = 0, n_nodes_active = 0, n_blocks_active = 0, n_free_nodes = 0;
+    int64_t launches = 0;  // kernels launched by this context (cumulative)
     int dense_n = 0;  // nb0*nb1*nb2
     DevBuf cflag, nflag, tile_of, scan_tmp;
     DevBuf t_coord, t_nplus, t_nminus, t_cstart, t_ccount, t_hascells, t_bcount, t_bstart, t_cellof, t_cmask;

@@ -66,7 +66,9 @@ class SolveStats(C.Structure):
                 ("converged", C.c_int32), ("neg_curvature", C.c_int32), ("n_inverted_trials", C.c_int32),
                 ("grad_norm0", C.c_double), ("grad_norm", C.c_double), ("energy", C.c_double),
                 ("cg_iters", C.c_int32 * MAX_NEWTON_LOG), ("ls_iters", C.c_int32 * MAX_NEWTON_LOG),
-                ("n_hvp", C.c_int32), ("hvp_ms", C.c_double), ("ms_phase", C.c_double * 8)]
+                ("n_hvp", C.c_int32), ("hvp_ms", C.c_double), ("ms_phase", C.c_double * 8),
+                ("n_cells", C.c_int64), ("n_nodes", C.c_int64), ("n_free_nodes", C.c_int64),
+                ("n_launches", C.c_int64)]
 
     def as_dict(self) -> dict:
         n = min(self.newton_iters, MAX_NEWTON_LOG)
@@ -75,7 +77,8 @@ class SolveStats(C.Structure):
                     n_inverted_trials=self.n_inverted_trials, grad_norm0=self.grad_norm0,
                     grad_norm=self.grad_norm, energy=self.energy, cg_iters=list(self.cg_iters[:n]),
                     ls_iters=list(self.ls_iters[:n]), n_hvp=self.n_hvp, hvp_ms=self.hvp_ms,
-                    ms_phase=list(self.ms_phase))
+                    ms_phase=list(self.ms_phase), n_cells=self.n_cells, n_nodes=self.n_nodes,
+                    n_free_nodes=self.n_free_nodes, n_launches=self.n_launches)
 
 
 _vp, _i32, _i64, _d = C.c_void_p, C.c_int32, C.c_int64, C.c_double
@@ -352,6 +355,7 @@ class Context:
         st = SolveStats()
         self._chk(_lib.mpl_step(self._h, float(dt), C.byref(cfg), C.byref(st)), "mpl_step")
         del keep
+        self.counts = Counts(st.n_cells, st.n_nodes, self.counts.n_blocks if self.counts else -1)
         return st.as_dict()
 
 

@@ -296,156 +296,45 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
 }
 
 // =============================================================================================
-// a6: HVP  (Hu)_i = m_i u_i + sum_c (K_c : dG_c(u)) grad w_ic   (one tile per 64-thread CTA)
-//   1. each cell thread loads its 45-number tangent straight into registers with 16-byte loads
-//      that are coalesced across the tile's cells (chunked layout, KL<T>);
-//   2. the 5^3 node halo of u is staged in shared memory;
-//   3. P = K' dG' (81 FMA, symmetric K), scattered to the 8 corners in 8 passes: in pass o every
-//      cell adds to node (cell + o), an injective map, so the shared-memory adds never collide;
-//   4. nodes with all 8 cells in the tile are stored, face nodes are summed with one float4 atomic.
-// Also accumulates u . Hu = sum_i m_i |u_i|^2 + sum_c dG_c : K_c : dG_c (exact without completion).
-// =============================================================================================
-template <class T> __device__ __forceinline__ void ldk(const T *p, T *k);
-template <> __device__ __forceinline__ void ldk<float>(const float *p, float *k) {
-    float4 v = __ldg(reinterpret_cast<const float4 *>(p));
-    k[0] = v.x; k[1] = v.y; k[2] = v.z; k[3] = v.w;
-}
-template <> __device__ __forceinline__ void ldk<double>(const double *p, double *k) {
-    double2 v = __ldg(reinterpret_cast<const double2 *>(p));
-    k[0] = v.x; k[1] = v.y;
-}
-
-template <class T>
-__global__ void __launch_bounds__(64) k_hvp(const int *__restrict__ nplus, const int *__restrict__ cstart,
-                                            const uint8_t *__restrict__ clocal, const int *__restrict__ hascells,
-                                            const T *__restrict__ K, const T *__restrict__ nmass,
-                                            const vec4<T> *__restrict__ u, vec4<T> *__restrict__ Hu,
-                                            double *__restrict__ uHu, const CGSlot *__restrict__ cgs, int cgj,
-                                            double cgthr, const DevScalars *__restrict__ sc) {
-    __shared__ vec4<T> uh[125];
-    __shared__ T Fs[3][128];
-    const int t = blockIdx.x, tid = threadIdx.x;
-    if (cgs != nullptr) {  // inside PCG: skip once converged / broken down (uniform per CTA)
-        double rr = stripe_sum_bcast(cgs[cgj].rr);
-        if (sc->neg_curv || (cgj > 0 && rr <= cgthr)) return;
-    }
-    const int has = hascells[t];
-    const int cs = cstart[t], ncp = cstart[t + 1] - cs;
-    constexpr int VEC = KL<T>::VEC, NCH = KL<T>::NCH;
-    T k[45];
-    int l = 0xFF;
-    if (tid < ncp) {
-        l = clocal[cs + tid];
-        const T *base = K + (int64_t)cs * 45;
-#pragma unroll
-        for (int c = 0; c < NCH; c++) ldk<T>(base + ((int64_t)c * ncp + tid) * VEC, k + c * VEC);
-        k[44] = __ldg(base + (int64_t)NCH * VEC * ncp + tid);
-    }
-    for (int h = tid; h < 125; h += 64) {
-        int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
-        bool owned = hx < 4 && hy < 4 && hz < 4;
-        int64_t n = (has || owned) ? halo_node(t, nplus, h) : -1;
-        uh[h] = n >= 0 ? u[n] : mk4<T>(0, 0, 0, 0);
-        Fs[0][h] = Fs[1][h] = Fs[2][h] = T(0);
-    }
-    __syncthreads();
-    double acc = 0.0;
-    const bool act = (l != 0xFF);
-    const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
-    T P[9];
-    if (act) {
-        T dG[9];
-#pragma unroll
-        for (int a = 0; a < 9; a++) dG[a] = T(0);
-#pragma unroll
-        for (int o = 0; o < 8; o++) {
-            const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
-            vec4<T> w = uh[((lx + ox) * 5 + ly + oy) * 5 + lz + oz];
-            const T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
-            dG[0] += w.x * s0; dG[1] += w.x * s1; dG[2] += w.x * s2;
-            dG[3] += w.y * s0; dG[4] += w.y * s1; dG[5] += w.y * s2;
-            dG[6] += w.z * s0; dG[7] += w.z * s1; dG[8] += w.z * s2;
-        }
-#pragma unroll
-        for (int r = 0; r < 9; r++) P[r] = k[kidx(r, r)] * dG[r];
-#pragma unroll
-        for (int r = 0; r < 9; r++)
-#pragma unroll
-            for (int q = r + 1; q < 9; q++) {
-                P[r] += k[kidx(r, q)] * dG[q];
-                P[q] += k[kidx(r, q)] * dG[r];
-            }
-        T qf = T(0);
-#pragma unroll
-        for (int r = 0; r < 9; r++) qf += P[r] * dG[r];
-        acc += (double)qf;
-    }
-    if (has) {
-#pragma unroll
-        for (int o = 0; o < 8; o++) {
-            if (act) {
-                const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
-                const T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
-                const int h = ((lx + ox) * 5 + ly + oy) * 5 + lz + oz;
-                Fs[0][h] += P[0] * s0 + P[1] * s1 + P[2] * s2;
-                Fs[1][h] += P[3] * s0 + P[4] * s1 + P[5] * s2;
-                Fs[2][h] += P[6] * s0 + P[7] * s1 + P[8] * s2;
-            }
-            __syncthreads();
-        }
-    }
-    for (int h = tid; h < 125; h += 64) {
-        int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
-        bool owned = hx < 4 && hy < 4 && hz < 4;
-        if (!has && !owned) continue;
-        bool interior = hx >= 1 && hx <= 3 && hy >= 1 && hy <= 3 && hz >= 1 && hz <= 3;
-        int64_t n = halo_node(t, nplus, h);
-        if (n < 0) continue;
-        T f0 = Fs[0][h], f1 = Fs[1][h], f2 = Fs[2][h];
-        if (owned) {
-            T m = nmass[n];
-            if (m > T(0)) {
-                vec4<T> w = uh[h];
-                f0 += m * w.x; f1 += m * w.y; f2 += m * w.z;
-                acc += (double)(m * (w.x * w.x + w.y * w.y + w.z * w.z));
-            }
-        }
-        if (interior) Hu[n] = mk4<T>(f0, f1, f2, T(0));
-        else if (f0 != T(0) || f1 != T(0) || f2 != T(0)) atomic_add3<T>(Hu + n, f0, f1, f2);
-    }
-    if (uHu) block_add(acc, uHu);
-}
-
-// =============================================================================================
 // a7: Jacobi-PCG vector kernels (fp64 accumulation of every dot product)
 // slot j: rz_j = r_j.z_j, rr_j = r_j.r_j, pHp_j = p_j.H p_j
 // =============================================================================================
+// ---- PCG on the compact list of active nodes (i -> tile-dense slot list[i]) ---------------------
+// x, r, invD are compact (active nodes only); p and Hp stay tile-dense because the HVP gathers and
+// scatters them by tile.  invD.w = 1 marks a free DOF; prescribed DOFs have invD = 0 and r = p = 0.
+
+// r = -g, invD = 1/D on free DOFs; z = invD r; p = z; x = 0; slot[0] = (r.z, r.r)
 template <class T>
-__global__ void k_pcg_init(int64_t N, const uint8_t *__restrict__ flag, const vec4<T> *__restrict__ g,
-                           const vec4<T> *__restrict__ D, vec4<T> *__restrict__ r, vec4<T> *__restrict__ p,
-                           vec4<T> *__restrict__ x, CGSlot *slot) {
-    double rz = 0, rr = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
-        vec4<T> rv = mk4<T>(0, 0, 0, 0), zv = mk4<T>(0, 0, 0, 0);
-        if (flag[i] == 1) {
-            vec4<T> gv = g[i], dv = D[i];
+__global__ void __launch_bounds__(256) k_pcg_init(int64_t n, const int *__restrict__ list,
+                                                  const uint8_t *__restrict__ flag, const vec4<T> *__restrict__ g,
+                                                  const vec4<T> *__restrict__ D, vec4<T> *__restrict__ invD,
+                                                  vec4<T> *__restrict__ r, vec4<T> *__restrict__ p,
+                                                  vec4<T> *__restrict__ x, CGSlot *slot) {
+    T rz = 0, rr = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int ti = list[i];
+        vec4<T> rv = mk4<T>(0, 0, 0, 0), zv = mk4<T>(0, 0, 0, 0), iv = mk4<T>(0, 0, 0, 0);
+        if (flag[ti] == 1) {
+            vec4<T> gv = g[ti], dv = D[ti];
+            iv = mk4<T>(T(1) / dv.x, T(1) / dv.y, T(1) / dv.z, T(1));
             rv = mk4<T>(-gv.x, -gv.y, -gv.z, 0);
-            zv = mk4<T>(rv.x / dv.x, rv.y / dv.y, rv.z / dv.z, 0);
-            rz += (double)(rv.x * zv.x + rv.y * zv.y + rv.z * zv.z);
-            rr += (double)(rv.x * rv.x + rv.y * rv.y + rv.z * rv.z);
+            zv = mk4<T>(rv.x * iv.x, rv.y * iv.y, rv.z * iv.z, 0);
+            rz += rv.x * zv.x + rv.y * zv.y + rv.z * zv.z;
+            rr += rv.x * rv.x + rv.y * rv.y + rv.z * rv.z;
         }
+        invD[i] = iv;
         r[i] = rv;
-        p[i] = zv;
+        p[ti] = zv;
         x[i] = mk4<T>(0, 0, 0, 0);
     }
-    block_add(rz, slot[0].rz);
-    block_add(rr, slot[0].rr);
+    block_add((double)rz, slot[0].rz);
+    block_add((double)rr, slot[0].rr);
 }
 
-// x += alpha p ; r -= alpha Hp ; z = D^{-1} r ; slot[j+1] = (r.z, r.r) ; Hp := 0 for the next HVP
+// x += alpha p ; r -= alpha Hp ; slot[j+1] = (r.invD r, r.r) ; Hp := 0 for the next HVP's atomics
 template <class T>
-__global__ void __launch_bounds__(256) k_pcg_update1(int64_t N, int j, double thr, const uint8_t *__restrict__ flag,
-                                                     const vec4<T> *__restrict__ D, const vec4<T> *__restrict__ p,
+__global__ void __launch_bounds__(256) k_pcg_update1(int64_t n, const int *__restrict__ list, int j, double thr,
+                                                     const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ p,
                                                      vec4<T> *__restrict__ Hp, vec4<T> *__restrict__ x,
                                                      vec4<T> *__restrict__ r, CGSlot *slot, DevScalars *sc) {
     const double rr_j = stripe_sum_bcast(slot[j].rr);
@@ -454,8 +343,8 @@ __global__ void __launch_bounds__(256) k_pcg_update1(int64_t N, int j, double th
     const double rz_j = stripe_sum_bcast(slot[j].rz);
     if (!(pHp > 0.0)) {  // breakdown (negative curvature): the first iteration returns p = z_0
         if (j == 0)
-            for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
-                x[i] = p[i];
+            for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+                x[i] = p[list[i]];
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             sc->neg_curv = 1;
             sc->cg_done_iter = j + 1;
@@ -463,37 +352,65 @@ __global__ void __launch_bounds__(256) k_pcg_update1(int64_t N, int j, double th
         return;
     }
     const T alpha = T(rz_j / pHp);
-    double rz = 0, rr = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
-        vec4<T> hv = Hp[i];
-        Hp[i] = mk4<T>(0, 0, 0, 0);
-        if (flag[i] != 1) continue;
-        vec4<T> pv = p[i], xv = x[i], rv = r[i], dv = D[i];
+    T rz = 0, rr = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int ti = list[i];
+        const vec4<T> hv = Hp[ti], pv = p[ti], iv = invD[i];
+        vec4<T> xv = x[i], rv = r[i];
+        Hp[ti] = mk4<T>(0, 0, 0, 0);
+        const T aw = alpha * iv.w;
         xv.x += alpha * pv.x; xv.y += alpha * pv.y; xv.z += alpha * pv.z;
-        rv.x -= alpha * hv.x; rv.y -= alpha * hv.y; rv.z -= alpha * hv.z;
+        rv.x -= aw * hv.x; rv.y -= aw * hv.y; rv.z -= aw * hv.z;
         x[i] = xv;
         r[i] = rv;
-        rz += (double)(rv.x * rv.x / dv.x + rv.y * rv.y / dv.y + rv.z * rv.z / dv.z);
-        rr += (double)(rv.x * rv.x + rv.y * rv.y + rv.z * rv.z);
+        rz += rv.x * rv.x * iv.x + rv.y * rv.y * iv.y + rv.z * rv.z * iv.z;
+        rr += rv.x * rv.x + rv.y * rv.y + rv.z * rv.z;
     }
-    block_add(rz, slot[j + 1].rz);
-    block_add(rr, slot[j + 1].rr);
+    block_add((double)rz, slot[j + 1].rz);
+    block_add((double)rr, slot[j + 1].rr);
 }
 
-// p = z + beta p, beta = rz_{j+1} / rz_j
+// p = invD r + beta p, beta = rz_{j+1} / rz_j
 template <class T>
-__global__ void __launch_bounds__(256) k_pcg_update2(int64_t N, int j, double thr, const uint8_t *__restrict__ flag,
-                                                     const vec4<T> *__restrict__ D, const vec4<T> *__restrict__ r,
+__global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, const int *__restrict__ list, int j, double thr,
+                                                     const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ r,
                                                      vec4<T> *__restrict__ p, const CGSlot *slot,
                                                      const DevScalars *sc) {
     const double rr = stripe_sum_bcast(slot[j + 1].rr);
     if (sc->neg_curv || rr <= thr) return;
     const double rz1 = stripe_sum_bcast(slot[j + 1].rz), rz0 = stripe_sum_bcast(slot[j].rz);
     const T beta = T(rz1 / rz0);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
-        if (flag[i] != 1) continue;
-        vec4<T> rv = r[i], dv = D[i], pv = p[i];
-        p[i] = mk4<T>(rv.x / dv.x + beta * pv.x, rv.y / dv.y + beta * pv.y, rv.z / dv.z + beta * pv.z, 0);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int ti = list[i];
+        const vec4<T> rv = r[i], iv = invD[i], pv = p[ti];
+        p[ti] = mk4<T>(rv.x * iv.x + beta * pv.x, rv.y * iv.y + beta * pv.y, rv.z * iv.z + beta * pv.z, T(0));
+    }
+}
+
+// g . x over free DOFs (g tile-dense, x compact)
+template <class T>
+__global__ void k_dot_gx(int64_t n, const int *__restrict__ list, const uint8_t *__restrict__ flag,
+                         const vec4<T> *__restrict__ g, const vec4<T> *__restrict__ x, double *out) {
+    double s = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int ti = list[i];
+        if (flag[ti] != 1) continue;
+        vec4<T> a = g[ti], b = x[i];
+        s += (double)(a.x * b.x + a.y * b.y + a.z * b.z);
+    }
+    block_add(s, out);
+}
+
+// vt = v + alpha x on free DOFs (vt pre-filled with v)
+template <class T>
+__global__ void k_axpy_compact(int64_t n, const int *__restrict__ list, const uint8_t *__restrict__ flag, T alpha,
+                               const vec4<T> *__restrict__ v, const vec4<T> *__restrict__ x, vec4<T> *__restrict__ vt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int ti = list[i];
+        if (flag[ti] != 1) continue;
+        vec4<T> a = v[ti], b = x[i];
+        a.x += alpha * b.x; a.y += alpha * b.y; a.z += alpha * b.z;
+        vt[ti] = a;
     }
 }
 
@@ -622,16 +539,8 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
 // One HVP on tile-dense vectors: Hu = H u (Hu zeroed here); optional u.Hu accumulation.
 template <class T>
 mpl_status hvp_tile(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu_accum) {
-    cudaStream_t st = ctx->stream;
-    const int T_ = ctx->T;
-    MPL_CUDA(cudaMemsetAsync(Hu_tile, 0, (size_t)T_ * 64 * sizeof(vec4<T>), st));
-    if (T_)
-        k_hvp<T><<<T_, 64, 0, st>>>((const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,
-                                     (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p, (const T *)ctx->K.p,
-                                     (const T *)ctx->n_mass.p, (const vec4<T> *)u_tile, (vec4<T> *)Hu_tile, uHu_accum,
-                                     nullptr, 0, 0.0, nullptr); ctx->launches++;
-    MPL_CUDA(cudaGetLastError());
-    return MPL_OK;
+    MPL_CUDA(cudaMemsetAsync(Hu_tile, 0, (size_t)ctx->T * 64 * sizeof(vec4<T>), ctx->stream));
+    return launch_hvp<T>(ctx, u_tile, Hu_tile, uHu_accum, nullptr, 0, 0.0);
 }
 
 namespace {
@@ -658,9 +567,14 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     const uint8_t *flag = (const uint8_t *)ctx->n_flag.p;
     vec4<T> *v = (vec4<T> *)ctx->n_v.p, *vt = (vec4<T> *)ctx->n_vt.p;
     vec4<T> *g = (vec4<T> *)ctx->n_g.p, *D = (vec4<T> *)ctx->n_diag.p;
+    MPL_CHECK(ensure(ctx, ctx->n_invD, (size_t)NT * sizeof(vec4<T>) + 64));
+    vec4<T> *invD = (vec4<T> *)ctx->n_invD.p;
     vec4<T> *x = (vec4<T> *)ctx->n_x.p, *r = (vec4<T> *)ctx->n_r.p, *p = (vec4<T> *)ctx->n_p.p,
             *Hp = (vec4<T> *)ctx->n_Hp.p;
     const unsigned VG = vgrid(NT);
+    const int64_t NA = ctx->n_nodes_active;
+    const unsigned VA = vgrid(NA);
+    const int *list = (const int *)ctx->n_list.p;
     cudaEvent_t e0, e1, h0, h1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -680,7 +594,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         MPL_CUDA(cudaMemsetAsync(slots, 0, slots_needed * sizeof(CGSlot), st));
         MPL_CUDA(cudaMemsetAsync(&sc->neg_curv, 0, sizeof(int), st));
         MPL_CUDA(cudaMemsetAsync(&sc->cg_done_iter, 0xff, sizeof(int), st));
-        k_pcg_init<T><<<VG, 256, 0, st>>>(NT, flag, g, D, r, p, x, slots); ctx->launches++;
+        MPL_CUDA(cudaMemsetAsync(p, 0, NT * sizeof(vec4<T>), st));
+        k_pcg_init<T><<<VA, 256, 0, st>>>(NA, list, flag, g, D, invD, r, p, x, slots); ctx->launches++;
         MPL_CUDA(cudaMemsetAsync(Hp, 0, NT * sizeof(vec4<T>), st));
         cudaEventRecord(e1, st);
         CGSlot s0;
@@ -719,15 +634,11 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     }
                     cudaEventRecord(hev[S.n_hvp].first, st);
                     // the HVP is skipped on device once converged (its output is then unused)
-                    if (ctx->T)
-                        k_hvp<T><<<ctx->T, 64, 0, st>>>((const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,
-                                                        (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p,
-                                                        (const T *)ctx->K.p, (const T *)ctx->n_mass.p, p, Hp,
-                                                        slots[jj].pHp, slots, jj, thr, sc); ctx->launches++;
+                    MPL_CHECK(launch_hvp<T>(ctx, p, Hp, slots[jj].pHp, slots, jj, thr));
                     cudaEventRecord(hev[S.n_hvp].second, st);
                     S.n_hvp++;
-                    k_pcg_update1<T><<<VG, 256, 0, st>>>(NT, jj, thr, flag, D, p, Hp, x, r, slots, sc); ctx->launches++;
-                    k_pcg_update2<T><<<VG, 256, 0, st>>>(NT, jj, thr, flag, D, r, p, slots, sc); ctx->launches++;
+                    k_pcg_update1<T><<<VA, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc); ctx->launches++;
+                    k_pcg_update2<T><<<VA, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, slots, sc); ctx->launches++;
                 }
                 launched += n;
                 MPL_CUDA(cudaGetLastError());
@@ -762,7 +673,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         // ---- Armijo backtracking line search ------------------------------------------------
         cudaEventRecord(e0, st);
         MPL_CUDA(cudaMemsetAsync(sc->gp, 0, sizeof(sc->gp), st));
-        k_dot_free<T><<<VG, 256, 0, st>>>(NT, flag, g, x, sc->gp); ctx->launches++;
+        k_dot_gx<T><<<VA, 256, 0, st>>>(NA, list, flag, g, x, sc->gp); ctx->launches++;
         double gps[NSTRIPE];
         MPL_CUDA(cudaMemcpyAsync(gps, sc->gp, sizeof gps, cudaMemcpyDeviceToHost, st));
         MPL_CUDA(cudaStreamSynchronize(st));
@@ -771,10 +682,12 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         int h = 0;
         if (cfg->fixed_ls_halvings) {
             for (h = 0; h < cfg->fixed_ls_halvings[k]; h++) alpha *= 0.5;
-            k_axpy_free<T><<<VG, 256, 0, st>>>(NT, flag, T(alpha), v, x, vt); ctx->launches++;
+            MPL_CUDA(cudaMemcpyAsync(vt, v, NT * sizeof(vec4<T>), cudaMemcpyDeviceToDevice, st));
+            k_axpy_compact<T><<<VA, 256, 0, st>>>(NA, list, flag, T(alpha), v, x, vt); ctx->launches++;
         } else {
             for (;;) {
-                k_axpy_free<T><<<VG, 256, 0, st>>>(NT, flag, T(alpha), v, x, vt); ctx->launches++;
+                MPL_CUDA(cudaMemcpyAsync(vt, v, NT * sizeof(vec4<T>), cudaMemcpyDeviceToDevice, st));
+            k_axpy_compact<T><<<VA, 256, 0, st>>>(NA, list, flag, T(alpha), v, x, vt); ctx->launches++;
                 double phi = 0;
                 MPL_CHECK(energy_at<T>(ctx, vt, &phi));
                 if (std::isinf(phi)) S.n_inverted_trials++;

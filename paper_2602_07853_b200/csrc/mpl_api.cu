@@ -101,7 +101,7 @@ void mpl_destroy(mpl_ctx ctx) {
                      &ctx->scan_tmp, &ctx->t_coord, &ctx->t_nplus, &ctx->t_nminus, &ctx->t_cstart, &ctx->t_ccount,
                      &ctx->t_hascells, &ctx->t_bcount, &ctx->t_bstart, &ctx->t_cellof, &ctx->t_cmask, &ctx->c_local,
                      &ctx->q_m, &ctx->q_mv, &ctx->q_mG, &ctx->q_slot, &ctx->q_vc, &ctx->q_Gc, &ctx->K, &ctx->n_mass,
-                     &ctx->n_flag, &ctx->n_vn, &ctx->n_vhat, &ctx->n_v, &ctx->n_vt, &ctx->n_g, &ctx->n_diag,
+                     &ctx->n_flag, &ctx->n_vn, &ctx->n_vhat, &ctx->n_v, &ctx->n_vt, &ctx->n_g, &ctx->n_diag, &ctx->n_invD,
                      &ctx->n_x, &ctx->n_r, &ctx->n_p, &ctx->n_Hp, &ctx->n_u, &ctx->n_u2, &ctx->n_act,
                      &ctx->n_canon, &ctx->n_list, &ctx->scalars, &ctx->cg_slots, &ctx->io_stage, &ctx->io_stage2};
     for (DevBuf *b : all) free_buf(*b);

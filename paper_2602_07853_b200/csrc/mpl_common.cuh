@@ -279,7 +279,7 @@ struct mpl_ctx_s {
     DevBuf q_vc, q_Gc;               // load: v_c, G_c
     DevBuf K;                        // C * 45 tangent (scaled by 1/(16 dx^2))
     // nodes (tile-dense, T*64)
-    DevBuf n_mass, n_flag, n_vn, n_vhat, n_v, n_vt, n_g, n_diag, n_x, n_r, n_p, n_Hp, n_u, n_u2, n_act;
+    DevBuf n_mass, n_flag, n_vn, n_vhat, n_v, n_vt, n_g, n_diag, n_invD, n_x, n_r, n_p, n_Hp, n_u, n_u2, n_act;
     // canonical node index per tile-dense node (-1 inactive)
     DevBuf n_canon, n_list;  // n_list: canonical -> tile-dense index
     DevBuf scalars, cg_slots, io_stage, io_stage2;
@@ -314,6 +314,8 @@ mpl_status ensure(mpl_ctx ctx, DevBuf &b, size_t bytes);
 template <class T> mpl_status resample_impl(mpl_ctx ctx, double dt);
 template <class T> mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi);
 template <class T> mpl_status hvp_tile(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *pHp_accum);
+template <class T> mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu,
+                                         const CGSlot *cgs, int cgj, double cgthr);
 template <class T> mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *st);
 template <class T> mpl_status g2p_impl(mpl_ctx ctx, double dt);
 template <class T> mpl_status canon_to_tile(mpl_ctx ctx, const void *src, void *dst_tile);

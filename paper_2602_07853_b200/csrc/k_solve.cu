@@ -331,40 +331,55 @@ __global__ void __launch_bounds__(256) k_pcg_init(int64_t n, const int *__restri
     block_add((double)rr, slot[0].rr);
 }
 
-// x += alpha p ; r -= alpha Hp ; slot[j+1] = (r.invD r, r.r) ; Hp := 0 for the next HVP's atomics
+// Scalars of CG iteration j, read once per CTA: rr_j, pHp_j, rz_j, rz_{j+1}, rr_{j+1} (striped sums).
+struct CGScal {
+    double rr, pHp, rz, rz1, rr1;
+};
+__device__ __forceinline__ CGScal cg_scalars(const CGSlot *slot, int j, bool next) {
+    __shared__ CGScal s_;
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        double a = warp_sum(slot[j].rr[l]), b = warp_sum(slot[j].pHp[l]), c = warp_sum(slot[j].rz[l]);
+        double d = next ? warp_sum(slot[j + 1].rz[l]) : 0.0, e = next ? warp_sum(slot[j + 1].rr[l]) : 0.0;
+        if (l == 0) s_ = CGScal{a, b, c, d, e};
+    }
+    __syncthreads();
+    return s_;
+}
+
+// x += alpha p ; r -= alpha Hp ; slot[j+1] = (r.invD r, r.r) ; Hp := 0 for the next HVP's atomics.
+// One active node per thread: all loads are issued before any use (latency hidden by occupancy).
 template <class T>
 __global__ void __launch_bounds__(256) k_pcg_update1(int64_t n, const int *__restrict__ list, int j, double thr,
                                                      const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ p,
                                                      vec4<T> *__restrict__ Hp, vec4<T> *__restrict__ x,
                                                      vec4<T> *__restrict__ r, CGSlot *slot, DevScalars *sc) {
-    const double rr_j = stripe_sum_bcast(slot[j].rr);
-    if (sc->neg_curv || (j > 0 && rr_j <= thr)) return;  // converged before iteration j
-    const double pHp = stripe_sum_bcast(slot[j].pHp);
-    const double rz_j = stripe_sum_bcast(slot[j].rz);
-    if (!(pHp > 0.0)) {  // breakdown (negative curvature): the first iteration returns p = z_0
-        if (j == 0)
-            for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-                x[i] = p[list[i]];
+    const CGScal cs = cg_scalars(slot, j, false);
+    if (sc->neg_curv || (j > 0 && cs.rr <= thr)) return;  // converged before iteration j
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (!(cs.pHp > 0.0)) {  // breakdown (negative curvature): the first iteration returns p = z_0
+        if (j == 0 && i < n) x[i] = p[list[i]];
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             sc->neg_curv = 1;
             sc->cg_done_iter = j + 1;
         }
         return;
     }
-    const T alpha = T(rz_j / pHp);
+    const T alpha = T(cs.rz / cs.pHp);
     T rz = 0, rr = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n) {
         const int ti = list[i];
-        const vec4<T> hv = Hp[ti], pv = p[ti], iv = invD[i];
+        const vec4<T> iv = invD[i];
         vec4<T> xv = x[i], rv = r[i];
+        const vec4<T> hv = Hp[ti], pv = p[ti];
         Hp[ti] = mk4<T>(0, 0, 0, 0);
         const T aw = alpha * iv.w;
         xv.x += alpha * pv.x; xv.y += alpha * pv.y; xv.z += alpha * pv.z;
         rv.x -= aw * hv.x; rv.y -= aw * hv.y; rv.z -= aw * hv.z;
         x[i] = xv;
         r[i] = rv;
-        rz += rv.x * rv.x * iv.x + rv.y * rv.y * iv.y + rv.z * rv.z * iv.z;
-        rr += rv.x * rv.x + rv.y * rv.y + rv.z * rv.z;
+        rz = rv.x * rv.x * iv.x + rv.y * rv.y * iv.y + rv.z * rv.z * iv.z;
+        rr = rv.x * rv.x + rv.y * rv.y + rv.z * rv.z;
     }
     block_add((double)rz, slot[j + 1].rz);
     block_add((double)rr, slot[j + 1].rr);
@@ -376,13 +391,14 @@ __global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, const int *__res
                                                      const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ r,
                                                      vec4<T> *__restrict__ p, const CGSlot *slot,
                                                      const DevScalars *sc) {
-    const double rr = stripe_sum_bcast(slot[j + 1].rr);
-    if (sc->neg_curv || rr <= thr) return;
-    const double rz1 = stripe_sum_bcast(slot[j + 1].rz), rz0 = stripe_sum_bcast(slot[j].rz);
-    const T beta = T(rz1 / rz0);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const CGScal cs = cg_scalars(slot, j, true);
+    if (sc->neg_curv || cs.rr1 <= thr) return;
+    const T beta = T(cs.rz1 / cs.rz);
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
         const int ti = list[i];
-        const vec4<T> rv = r[i], iv = invD[i], pv = p[ti];
+        const vec4<T> rv = r[i], iv = invD[i];
+        const vec4<T> pv = p[ti];
         p[ti] = mk4<T>(rv.x * iv.x + beta * pv.x, rv.y * iv.y + beta * pv.y, rv.z * iv.z + beta * pv.z, T(0));
     }
 }
@@ -574,6 +590,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     const unsigned VG = vgrid(NT);
     const int64_t NA = ctx->n_nodes_active;
     const unsigned VA = vgrid(NA);
+    const unsigned VA1 = nblk(NA > 0 ? NA : 1, 256);  // one active node per thread
     const int *list = (const int *)ctx->n_list.p;
     cudaEvent_t e0, e1, h0, h1;
     cudaEventCreate(&e0);
@@ -637,8 +654,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     MPL_CHECK(launch_hvp<T>(ctx, p, Hp, slots[jj].pHp, slots, jj, thr));
                     cudaEventRecord(hev[S.n_hvp].second, st);
                     S.n_hvp++;
-                    k_pcg_update1<T><<<VA, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc); ctx->launches++;
-                    k_pcg_update2<T><<<VA, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, slots, sc); ctx->launches++;
+                    k_pcg_update1<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc); ctx->launches++;
+                    k_pcg_update2<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, slots, sc); ctx->launches++;
                 }
                 launched += n;
                 MPL_CUDA(cudaGetLastError());

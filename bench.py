@@ -6,8 +6,10 @@
 A *step* is one full implicit time step of the workload: bin + sort,
 P2Q + stretch, C2N, Newton (linearise, Jacobi-PCG with the matrix-free HVP, line search), G2P.
 `value` = HVP GDOF/s = 3 * free nodes * HVP launches / summed HVP device time (CUDA events on the
-library stream) over the K timed steps, summed over ranks.  `ms_per_step` = implicit-step time
-(device clock, max over ranks).  Inputs are resident in HBM when the timed region starts; the
+library stream) over the K timed steps.  With N > 1 GPUs the grid is slab-decomposed:
+free nodes are summed over ranks (a shared node counts once), the HVP time includes its interface
+halo sum and p.Hp allreduce and is the max over ranks.  `ms_per_step` = implicit-step time (device
+clock, max over ranks).  Inputs are resident in HBM when the timed region starts; the
 HVP's tangent stream (>= 392 MB at cfg4) is larger than the 126 MB L2.
 
 --impl reference times the CPU oracle (oracle/, plain fp64 C, 1 core) on a bounded window of the
@@ -113,15 +115,26 @@ def load_traffic(config: str):
 def run_ours(args):
     import torch
 
+    from paper_2602_07853_b200 import dist as pdist
     from paper_2602_07853_b200 import mpl, scenes
 
     ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
     sc = scenes.by_name(args.config, args.precision)
-    ctx = mpl.from_scene(sc, device=local)
+    sel = None
+    if ws > 1:
+        # slab decomposition: rank r owns the x-slab [cuts[r], cuts[r+1]) of 4-cell blocks; the library's
+        # own NCCL communicator carries the halo sums, PCG allreduces and particle migration
+        nccl_id = pdist.share_nccl_id()
+        cuts = pdist.agree_cuts(mpl.slab_cuts(sc, ws))
+        ctx = mpl.from_scene_rank(sc, rank, ws, cuts, device=local, nccl_id=nccl_id)
+        sel = mpl.slab_select(sc, cuts, rank)
+    else:
+        cuts = None
+        ctx = mpl.from_scene(sc, device=local)
     stream = torch.cuda.Stream(device=local)
     ctx.set_stream(stream.cuda_stream)
     solver = sc.solver
@@ -135,7 +148,6 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     stats = []
-    counts = []
     with ClockSampler(local) as clk:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -143,33 +155,36 @@ def run_ours(args):
         e0.record(stream)
         for _ in range(args.steps):
             stats.append(one_step())
-            counts.append(ctx.counts)
         e1.record(stream)
         torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
     ms_total = e0.elapsed_time(e1)
     n_hvp = sum(s["n_hvp"] for s in stats)
     hvp_ms = sum(s["hvp_ms"] for s in stats)
-    cells = [s["n_cells"] for s in stats]
-    nodes = [s["n_nodes"] for s in stats]
-    # HVP DOF throughput: each step's free DOFs times that step's HVP launches
+    cells = statistics.mean(s["n_cells"] for s in stats)
+    nodes = statistics.mean(s["n_nodes"] for s in stats)
+    # HVP DOF throughput: each step's free DOFs (owned, so a shared node counts once) times its HVPs
     dof_hvp = sum(3.0 * s["n_free_nodes"] * s["n_hvp"] for s in stats)
-    n_free = int(statistics.mean(s["n_free_nodes"] for s in stats))
-    gdofs = dof_hvp / (hvp_ms * 1e-3) / 1e9 if hvp_ms > 0 else 0.0
+    n_free = statistics.mean(s["n_free_nodes"] for s in stats)
     ms_per_step = ms_total / args.steps
+    launches = float(sum(s["n_launches"] for s in stats))
     if ws > 1:
-        t = torch.tensor([ms_per_step, gdofs], dtype=torch.float64, device="cuda")
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = t.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms_per_step = float(mx[0])
-        gdofs = float(sm[1])
-    avg_hvp_ms = hvp_ms / max(n_hvp, 1)
-    nbytes = hvp_bytes(statistics.mean(cells), statistics.mean(nodes), 4 if args.precision == 32 else 8)
+        # max over ranks of the times; sums of the work (HVP time includes its halo + p.Hp allreduce)
+        ms_per_step, hvp_ms_max = pdist.reduce_scalars([ms_per_step, hvp_ms], "max", device="cuda")
+        dof_hvp, cells_all, nodes_all, n_free_all, launches = pdist.reduce_scalars(
+            [dof_hvp, cells, nodes, n_free, launches], "sum", device="cuda")
+    else:
+        hvp_ms_max, cells_all, nodes_all, n_free_all = hvp_ms, cells, nodes, n_free
+    gdofs = dof_hvp / (hvp_ms_max * 1e-3) / 1e9 if hvp_ms_max > 0 else 0.0
+    avg_hvp_ms = hvp_ms_max / max(n_hvp, 1)
+    # roofline of the dominant kernel on this rank (rank 0's HVP launches)
+    nbytes = hvp_bytes(cells, nodes, 4 if args.precision == 32 else 8)
     peak, peak_kind = load_peaks()
-    achieved = nbytes / (avg_hvp_ms * 1e-3) / 1e9
+    avg_local = hvp_ms / max(n_hvp, 1)
+    achieved = nbytes / (avg_local * 1e-3) / 1e9
     # e2e: the same metric through the C ABI with HOST buffers (H2D of particles, D2H of results)
-    e2e = run_e2e(ctx, sc, solver, stream, args) if (rank == 0 and not args.no_e2e) else None
+    e2e = None if args.no_e2e else run_e2e(ctx, sc, solver, args, sel, ws)
     clocks = clk.summary()
     result = {
         "metric": "HVP GDOF/s (matrix-free incremental-potential Hessian-vector product inside Newton-PCG)",
@@ -180,16 +195,18 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 3),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f32" if args.precision == 32 else "f64",
         "data": "synthetic (seeded scene generator, paper_2602_07853_b200/scenes.py)",
         "config": {
             "workload": f"{sc.name}: {sc.n[0]}^3 grid, {sc.n_particles} particles, "
                         f"{len(sc.materials)} material(s), dt={sc.dt}",
-            "grid": list(sc.n), "particles": sc.n_particles, "quadrature_points": int(statistics.mean(cells)),
-            "active_nodes": int(statistics.mean(nodes)), "free_dofs": 3 * n_free,
-            "parallelism": "1 GPU" if ws == 1 else f"{ws} independent replicas (slab decomposition: DESIGN.md §6)",
+            "grid": list(sc.n), "particles": sc.n_particles, "quadrature_points": int(cells_all),
+            "active_nodes": int(nodes_all), "free_dofs": int(3 * n_free_all),
+            "parallelism": "1 GPU" if ws == 1 else
+            f"x-slab decomposition over {ws} GPUs (cuts {list(map(int, cuts))} in 4-cell blocks; "
+            "halo sums + allreduces on the library's NCCL communicator)",
             "l2": "inputs larger than L2 (tangent stream > 126 MB per HVP)",
             "step": "full implicit step: resample + Newton-PCG + G2P",
         },
@@ -198,13 +215,13 @@ def run_ours(args):
         "cg_iters": [s["cg_iters"] for s in stats],
         "hvp_ms": round(avg_hvp_ms, 5),
         "hvp_per_s": round(1e3 / avg_hvp_ms, 1),
-        "qp_per_s": round(statistics.mean(cells) / (avg_hvp_ms * 1e-3), 1),
+        "qp_per_s": round(cells_all / (avg_hvp_ms * 1e-3), 1),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": load_traffic(sc.name),
-                     "peak_kind": peak_kind, "kernel": "k_hvp",
+                     "frac": round(achieved / peak, 4), "traffic": load_traffic(sc.name) if ws == 1 else None,
+                     "peak_kind": peak_kind, "kernel": "k_hvp_pipe",
                      "algorithmic_bytes_per_launch": int(nbytes), "pct_of_8TBps": round(achieved / 8000.0, 4)},
         "e2e": e2e,
-        "gpu_launches": int(sum(s["n_launches"] for s in stats)),
+        "gpu_launches": int(launches),
         "phase_ms": {"resample": round(statistics.mean(s["ms_phase"][0] for s in stats), 3),
                      "linearize": round(statistics.mean(s["ms_phase"][3] for s in stats), 3),
                      "pcg": round(statistics.mean(s["ms_phase"][4] for s in stats), 3),
@@ -221,28 +238,43 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(ctx, sc, solver, stream, args):
-    """Same metric through the C ABI with host buffers: each step copies the particle state from
-    pinned host memory (H2D), steps, and reads the particle state back (D2H)."""
+def run_e2e(ctx, sc, solver, args, sel, ws):
+    """Same metric through the C ABI with host buffers: each step copies the (rank's) particle state
+    from pinned host memory (H2D), steps, and reads the particle state back (D2H).  Wall clock, max
+    over ranks."""
     import torch
     dt_ = torch.float32 if args.precision == 32 else torch.float64
-    host = [torch.from_numpy(np.ascontiguousarray(a)).to(dt_).pin_memory() for a in (sc.x, sc.v, sc.F, sc.G, sc.vol)]
-    mat = torch.from_numpy(np.ascontiguousarray(sc.mat)).pin_memory()
-    outs = [torch.empty((sc.n_particles, w), dtype=dt_).pin_memory() for w in (3, 3, 9, 9)]
+    idx = np.arange(sc.n_particles) if sel is None else sel
+    host = [torch.from_numpy(np.ascontiguousarray(a[idx])).to(dt_).pin_memory() for a in (sc.x, sc.v, sc.F, sc.G, sc.vol)]
+    mat = torch.from_numpy(np.ascontiguousarray(sc.mat[idx])).pin_memory()
+    cap = int(len(idx) * 1.25) + 1024
+    outs = [torch.empty((cap, w), dtype=dt_).pin_memory() for w in (3, 3, 9, 9)]
     s = 4 if args.precision == 32 else 8
-    h2d = sc.n_particles * (3 + 3 + 9 + 9 + 1) * s + sc.n_particles * 4
-    d2h = sc.n_particles * (3 + 3 + 9 + 9) * s
+    n = len(idx)
+    h2d = n * (3 + 3 + 9 + 9 + 1) * s + n * 4
     steps = max(1, min(args.steps, 3))
     n_hvp_dofs = 0.0
+    d2h = 0
     torch.cuda.synchronize()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         ctx.set_particles(*host, mat)
+        if sel is not None:
+            ctx.set_particle_ids(sel.astype(np.int32))
         st = ctx.step(sc.dt, solver)
-        ctx.get_particles(*outs)
+        k = ctx.num_particles()
+        ctx.get_particles(*[o[:k] for o in outs])
+        d2h = k * (3 + 3 + 9 + 9) * s
         n_hvp_dofs += 3.0 * st["n_free_nodes"] * st["n_hvp"]
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
+    if ws > 1:
+        from paper_2602_07853_b200 import dist as pdist
+        wall, = pdist.reduce_scalars([wall], "max", device="cuda")
+        n_hvp_dofs, h2d, d2h = pdist.reduce_scalars([n_hvp_dofs, h2d, d2h], "sum", device="cuda")
     val = n_hvp_dofs / wall / 1e9
     return {"value": round(val, 3), "unit": "GDOF/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": round(wall * 1e3 / steps, 3), "steps": steps}

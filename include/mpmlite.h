@@ -49,6 +49,9 @@ extern "C" {
 #endif
 
 typedef struct mpl_ctx_s *mpl_ctx;
+/* An in-process group of slab ranks (one host thread per rank, one process): the loopback transport
+ * used to run the multi-GPU decomposition on one GPU (tests).  Production runs use NCCL instead. */
+typedef struct mpl_group_s *mpl_group;
 
 typedef enum {
     MPL_OK = 0,
@@ -81,6 +84,8 @@ typedef struct {
     int32_t device;    /* CUDA device ordinal                                   */
     int32_t rank, nranks; /* slab decomposition rank / size (1 process per GPU) */
     const uint8_t *nccl_unique_id; /* 128 bytes from mpl_nccl_unique_id on rank 0; NULL if nranks==1 */
+    mpl_group loopback;            /* non-NULL: ranks are threads of this process (mpl_group_create);
+                                      every collective then meets at a host barrier (no NCCL)        */
 } mpl_config;
 
 typedef struct {
@@ -127,6 +132,32 @@ MPL_API const char *mpl_version(void);
 /* rank 0 only: 128-byte NCCL unique id to broadcast to the other ranks before mpl_create. */
 MPL_API mpl_status mpl_nccl_unique_id(uint8_t out[128]);
 
+/* ---- slab decomposition ---------------------------------------
+ * With nranks > 1 every call below marked "collective" must be made by every rank, in the same
+ * order.  Rank r owns the 4-cell blocks [cuts[r], cuts[r+1]) along x: their quadrature points, the
+ * particles whose base cell lies there, and the nodes those cells touch.  The node plane at the
+ * cut is held by both neighbours with identical values (partial sums completed by a neighbour
+ * exchange after C2N, every gradient and every HVP); dot products and Phi count it once.  Each
+ * step particles that left the slab migrate to the neighbour (more than one slab per step is
+ * MPL_ERR_OUT_OF_DOMAIN) and the last owned cell plane is copied to the upper neighbour as ghosts.
+ * A failing collective returns an error on every rank. */
+MPL_API mpl_status mpl_group_create(int32_t nranks, mpl_group *out);
+MPL_API void mpl_group_destroy(mpl_group g);
+/* cuts: nranks + 1 strictly increasing cell-block x indices, cuts[0] = 0, cuts[nranks] =
+ * ceil(n[0] / 4).  Default: equal widths.  Call before mpl_set_particles. */
+MPL_API mpl_status mpl_set_slabs(mpl_ctx ctx, const int32_t *cuts);
+/* Host-only helper (no GPU needed): cuts balancing a per-plane weight (e.g. particles per cell-block
+ * plane); cuts[r] is the first plane whose prefix weight reaches r / nranks of the total, kept
+ * strictly increasing.  weight may be NULL (equal widths). */
+MPL_API mpl_status mpl_balance_slabs(int32_t nplanes, const int64_t *weight, int32_t nranks, int32_t *cuts);
+/* Global particle ids (int32 >= 0) of the particles last passed to mpl_set_particles on this rank
+ * (slab ranks only; default: input index).  Exports of a slab rank (mpl_get_particles,
+ * mpl_get_particle_cells, mpl_get_particle_ids) list its owned particles in ascending id. */
+MPL_API mpl_status mpl_set_particle_ids(mpl_ctx ctx, const int32_t *ids);
+MPL_API mpl_status mpl_get_particle_ids(mpl_ctx ctx, int32_t *ids);
+/* per active node (canonical order): 1 if this rank's copy is the counted one (n_nodes bytes). */
+MPL_API mpl_status mpl_get_node_owner(mpl_ctx ctx, uint8_t *owned);
+
 /* ---- scene -------------------------------------------------------------------------------- */
 /* n <= 8 materials; kind must be 0 (StVK-Hencky).  Requires mu > 0 and lam > -2 mu / 3. */
 MPL_API mpl_status mpl_set_materials(mpl_ctx ctx, int32_t n, const mpl_material *mats);
@@ -139,7 +170,8 @@ MPL_API mpl_status mpl_set_dirichlet(mpl_ctx ctx, int32_t n, const mpl_dirichlet
  * on_device is advisory (any cudaMemcpyDefault pointer works). */
 MPL_API mpl_status mpl_set_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v, const void *F,
                              const void *G, const void *vol, const int32_t *mat, int32_t on_device);
-/* Particle state in the order it was given to mpl_set_particles.  Any pointer may be NULL. */
+/* Particle state in the order it was given to mpl_set_particles (one rank; slab ranks: owned
+ * particles in ascending global id, mpl_num_particles of them).  Any pointer may be NULL. */
 MPL_API mpl_status mpl_get_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G, int32_t on_device);
 MPL_API int64_t mpl_num_particles(mpl_ctx ctx);
 

@@ -15,12 +15,13 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libmpmlite.so")
-BUILD = os.path.join(HERE, "csrc", "build")
+DEBUG = os.environ.get("MPL_DEBUG", "0") == "1"  # device bounds checks (DASSERT), separate .so
+OUT = os.path.join(HERE, "libmpmlite_dbg.so" if DEBUG else "libmpmlite.so")
+BUILD = os.path.join(HERE, "csrc", "build_dbg" if DEBUG else "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + (["-DMPL_DEBUG"] if DEBUG else [])
 
 
 def _sources():

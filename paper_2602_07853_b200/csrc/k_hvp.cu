@@ -3,22 +3,23 @@
 // (App. B: H = M + d^2 E/dv^2; grad w_ic = (x_i - x_c)/(2 dx^2); "matrix-free
 // PCG" P:495), with K_c the cached 9x9 symmetric tangent of the quadrature point (k_linearize).
 //
-// Persistent CTAs (64 threads, one tile of 4^3 cells at a time, tiles strided by gridDim):
+// Default kernel k_hvp_pipe: persistent CTAs (64 threads, one tile of 4^3 cells at a time, tiles
+// strided by gridDim):
 //   * tangent blocks (<= 64 cells x 180 B) stream through an NS-stage shared-memory ring filled by
-//     cp.async.bulk (TMA bulk copy, SASS UBLKCP) completing on an mbarrier, issued NS-1 tiles ahead;
-//   * the 5^3 node halo of u is prefetched with 16-byte cp.async (LDGSTS) into the same stage;
-//   * P = K dG (81 FMA), scattered to the 8 corners in 8 barrier-separated passes (pass o adds to
-//     node cell+o, injective, so shared adds never collide);
+//     cp.async.bulk (TMA bulk copy, SASS UBLKCP) completing on an mbarrier, NS tiles in flight;
+//   * the 5^3 node halo of u, the owned masses and the cell ids are prefetched with cp.async (LDGSTS)
+//     into the same stage;
+//   * P = K dG (81 FMA), scattered to the 8 corners in 8 passes into a per-warp force buffer (pass o
+//     adds to node cell+o, injective over the warp, so only __syncwarp separates passes);
 //   * the 27 nodes whose 8 cells all lie in the tile are stored, the face nodes get one float4 atomic.
-// u . Hu = sum_i m_i |u_i|^2 + sum_c dG:K:dG is accumulated exactly (striped fp64 accumulators).
+// Two block barriers per tile.  u . Hu = sum_i m_i |u_i|^2 + sum_c dG:K:dG is accumulated exactly
+// (striped fp64 accumulators).
 #include <cstdlib>
 
 #include "mpl_common.cuh"
 
 namespace {
 
-constexpr int HVP_THREADS = 64;
-constexpr int HVP_STAGES = 3;
 
 __device__ __forceinline__ int local_id(int lx, int ly, int lz) { return (lx * 4 + ly) * 4 + lz; }
 
@@ -85,176 +86,8 @@ template <> __device__ __forceinline__ void lds_vec<double>(const double *p, dou
     k[0] = v.x; k[1] = v.y;
 }
 
-template <class T> struct HvpSmem {
-    alignas(128) T K[HVP_STAGES][64 * 45];
-    alignas(16) vec4<T> uh[HVP_STAGES][125];
-    T F[3][128];
-    uint64_t bar[HVP_STAGES];
-    int has[HVP_STAGES], cs[HVP_STAGES], ncp[HVP_STAGES];
-    double red[2];
-    int stop;
-};
-
-template <class T>
-__device__ __forceinline__ void hvp_issue(HvpSmem<T> &S, int stage, int t, int T_, const int *__restrict__ nplus,
-                                          const int *__restrict__ cstart, const int *__restrict__ hascells,
-                                          const T *__restrict__ K, const vec4<T> *__restrict__ u) {
-    const int tid = threadIdx.x;
-    if (t < T_) {
-        const int cs = cstart[t], ncp = cstart[t + 1] - cs, has = hascells[t];
-        if (tid == 0) {
-            S.has[stage] = has;
-            S.cs[stage] = cs;
-            S.ncp[stage] = ncp;
-            const uint32_t bytes = (uint32_t)(ncp * 45 * sizeof(T));
-            mbar_expect_tx(&S.bar[stage], bytes);
-            if (bytes) bulk_g2s(S.K[stage], K + (int64_t)cs * 45, bytes, &S.bar[stage]);
-        }
-        for (int h = tid; h < 125; h += HVP_THREADS) {
-            int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
-            bool owned = hx < 4 && hy < 4 && hz < 4;
-            int64_t n = (has || owned) ? halo_node(t, nplus, h) : -1;
-            if (n >= 0) {
-#pragma unroll
-                for (int q = 0; q < (int)(sizeof(vec4<T>) / 16); q++)
-                    cp_async16(reinterpret_cast<char *>(&S.uh[stage][h]) + 16 * q,
-                               reinterpret_cast<const char *>(u + n) + 16 * q);
-            } else {
-                S.uh[stage][h] = mk4<T>(0, 0, 0, 0);
-            }
-        }
-    }
-    cp_async_commit();
-}
-
-template <class T>
-__global__ void __launch_bounds__(HVP_THREADS) k_hvp_tma(int T_, const int *__restrict__ nplus,
-                                                         const int *__restrict__ cstart,
-                                                         const uint8_t *__restrict__ clocal,
-                                                         const int *__restrict__ hascells, const T *__restrict__ K,
-                                                         const T *__restrict__ nmass, const vec4<T> *__restrict__ u,
-                                                         vec4<T> *__restrict__ Hu, double *__restrict__ uHu,
-                                                         const CGSlot *__restrict__ cgs, int cgj, double cgthr,
-                                                         const DevScalars *__restrict__ sc) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    HvpSmem<T> &S = *reinterpret_cast<HvpSmem<T> *>(smem_raw);
-    const int tid = threadIdx.x;
-    if (cgs != nullptr) {  // inside PCG: skip once converged / broken down (uniform per CTA)
-        double rr = stripe_sum_bcast(cgs[cgj].rr);
-        if (sc->neg_curv || (cgj > 0 && rr <= cgthr)) return;
-    }
-    if (tid == 0) {
-        for (int s = 0; s < HVP_STAGES; s++) mbar_init(&S.bar[s], 1);
-        mbar_fence_init();
-    }
-    for (int i = tid; i < 3 * 128; i += HVP_THREADS) (&S.F[0][0])[i] = T(0);
-    __syncthreads();
-    const int G = gridDim.x;
-    const int t0 = blockIdx.x;
-    // prologue: tiles it = 0 .. NS-2
-#pragma unroll
-    for (int s = 0; s < HVP_STAGES - 1; s++) hvp_issue<T>(S, s, t0 + s * G, T_, nplus, cstart, hascells, K, u);
-    double acc = 0.0;
-    int it = 0;
-    for (int t = t0; t < T_; t += G, it++) {
-        const int stage = it % HVP_STAGES;
-        // refill the stage freed at the end of the previous iteration (NS-1 tiles ahead)
-        hvp_issue<T>(S, (it + HVP_STAGES - 1) % HVP_STAGES, t + (HVP_STAGES - 1) * G, T_, nplus, cstart, hascells, K, u);
-        cp_async_wait<HVP_STAGES - 1>();
-        mbar_wait(&S.bar[stage], (uint32_t)((it / HVP_STAGES) & 1));
-        __syncthreads();
-        const int has = S.has[stage], cs = S.cs[stage], ncp = S.ncp[stage];
-        const vec4<T> *uh = S.uh[stage];
-        // ---- cell phase ----------------------------------------------------------------------
-        int l = 0xFF;
-        if (tid < ncp) l = clocal[cs + tid];
-        const bool act = (l != 0xFF);
-        const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
-        T P[9];
-        if (act) {
-            constexpr int VEC = KL<T>::VEC, NCH = KL<T>::NCH;
-            const T *Ks = S.K[stage];
-            T k[45];
-#pragma unroll
-            for (int c = 0; c < NCH; c++) lds_vec<T>(Ks + (c * ncp + tid) * VEC, k + c * VEC);
-            k[44] = Ks[NCH * VEC * ncp + tid];
-            T dG[9];
-#pragma unroll
-            for (int a = 0; a < 9; a++) dG[a] = T(0);
-#pragma unroll
-            for (int o = 0; o < 8; o++) {
-                const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
-                vec4<T> w = uh[((lx + ox) * 5 + ly + oy) * 5 + lz + oz];
-                const T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
-                dG[0] += w.x * s0; dG[1] += w.x * s1; dG[2] += w.x * s2;
-                dG[3] += w.y * s0; dG[4] += w.y * s1; dG[5] += w.y * s2;
-                dG[6] += w.z * s0; dG[7] += w.z * s1; dG[8] += w.z * s2;
-            }
-#pragma unroll
-            for (int r = 0; r < 9; r++) P[r] = k[kidx(r, r)] * dG[r];
-#pragma unroll
-            for (int r = 0; r < 9; r++)
-#pragma unroll
-                for (int q = r + 1; q < 9; q++) {
-                    P[r] += k[kidx(r, q)] * dG[q];
-                    P[q] += k[kidx(r, q)] * dG[r];
-                }
-            T qf = T(0);
-#pragma unroll
-            for (int r = 0; r < 9; r++) qf += P[r] * dG[r];
-            acc += (double)qf;
-        }
-        if (has) {
-#pragma unroll
-            for (int o = 0; o < 8; o++) {
-                if (act) {
-                    const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
-                    const T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
-                    const int h = ((lx + ox) * 5 + ly + oy) * 5 + lz + oz;
-                    S.F[0][h] += P[0] * s0 + P[1] * s1 + P[2] * s2;
-                    S.F[1][h] += P[3] * s0 + P[4] * s1 + P[5] * s2;
-                    S.F[2][h] += P[6] * s0 + P[7] * s1 + P[8] * s2;
-                }
-                __syncthreads();
-            }
-        }
-        // ---- node phase: store interior nodes, atomically add face nodes ----------------------
-        for (int h = tid; h < 125; h += HVP_THREADS) {
-            int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
-            bool owned = hx < 4 && hy < 4 && hz < 4;
-            T f0 = S.F[0][h], f1 = S.F[1][h], f2 = S.F[2][h];
-            S.F[0][h] = S.F[1][h] = S.F[2][h] = T(0);
-            if (!has && !owned) continue;
-            bool interior = hx >= 1 && hx <= 3 && hy >= 1 && hy <= 3 && hz >= 1 && hz <= 3;
-            int64_t n = halo_node(t, nplus, h);
-            if (n < 0) continue;
-            if (owned) {
-                T m = nmass[n];
-                if (m > T(0)) {
-                    vec4<T> w = uh[h];
-                    f0 += m * w.x; f1 += m * w.y; f2 += m * w.z;
-                    acc += (double)(m * (w.x * w.x + w.y * w.y + w.z * w.z));
-                }
-            }
-            if (interior) Hu[n] = mk4<T>(f0, f1, f2, T(0));
-            else if (f0 != T(0) || f1 != T(0) || f2 != T(0)) atomic_add3<T>(Hu + n, f0, f1, f2);
-        }
-        __syncthreads();  // stage and F free for reuse
-    }
-    cp_async_wait<0>();
-    if (uHu) {
-        double v = warp_sum(acc);
-        if ((tid & 31) == 0) S.red[tid >> 5] = v;
-        __syncthreads();
-        if (tid == 0) {
-            double s = S.red[0] + S.red[1];
-            if (s != 0.0) atomicAdd(&uHu[blockIdx.x % NSTRIPE], s);
-        }
-    }
-}
-
-// v2 (default): one tile per 64-thread CTA, tangent loaded straight into registers with 16-byte
-// loads coalesced across the tile's cells; ~14 CTAs resident per SM hide the latency.
+// v2 (MPL_HVP_KERNEL=reg): one tile per 64-thread CTA, tangent loaded straight into registers with
+// 16-byte loads coalesced across the tile's cells; ~14 CTAs resident per SM hide the latency.
 template <class T> __device__ __forceinline__ void ldg_vec(const T *p, T *k);
 template <> __device__ __forceinline__ void ldg_vec<float>(const float *p, float *k) {
     float4 v = __ldg(reinterpret_cast<const float4 *>(p));
@@ -285,7 +118,7 @@ __global__ void __launch_bounds__(64) k_hvp_reg(const int *__restrict__ nplus, c
     constexpr int VEC = KL<T>::VEC, NCH = KL<T>::NCH;
     T k[45];
     int l = 0xFF;
-    if (tid < ncp) {
+    if (has && tid < ncp) {  // tiles outside the slab (ghost planes) carry no tangent
         l = clocal[cs + tid];
         const T *base = K + (int64_t)cs * 45;
 #pragma unroll
@@ -375,7 +208,480 @@ __global__ void __launch_bounds__(64) k_hvp_reg(const int *__restrict__ nplus, c
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// v3 (default): persistent, software-pipelined.  One 64-thread CTA walks tiles t0, t0+G, ... with
+// an NS-stage shared-memory ring: the tile's contiguous tangent block arrives by one cp.async.bulk
+// (TMA bulk copy, SASS UBLKCP) completing on an mbarrier; the 5^3 u halo, the 64 owned masses and
+// the 64 local cell ids arrive by cp.async, all issued NS-1 tiles ahead.  Each thread owns two halo
+// roles (h = tid, tid + 64) whose coordinates / neighbour slot / interior flag are computed once per
+// launch, so the per-tile integer work of v2 (h/25, h/5, table lookups) disappears; the neighbour
+// table and tile metadata of the tile after next are prefetched into registers one iteration early.
+// ---------------------------------------------------------------------------------------------
+template <class T, int NS> struct PipeSmem {
+    alignas(128) T K[NS][64 * 45];
+    alignas(16) vec4<T> uh[NS][128];
+    alignas(16) T mh[NS][64];
+    alignas(16) uint8_t cl[NS][64];
+    T F[2][3][128];  // per-warp corner-force accumulators
+    uint64_t bar[NS];
+    int nb[NS + 1][8];    // metadata ring is one deeper than the data ring: the slot written for tile
+    int meta[NS + 1][4];  // it+NS is never a slot of a tile still in flight or being consumed
+    double red[2];
+};
+
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+template <class T> __device__ __forceinline__ void cp_async_real(T *dst, const T *src);
+template <> __device__ __forceinline__ void cp_async_real<float>(float *dst, const float *src) { cp_async4(dst, src); }
+template <> __device__ __forceinline__ void cp_async_real<double>(double *dst, const double *src) { cp_async8(dst, src); }
+
+// halo role: bits 0-5 local node id in its tile, 6-8 neighbour slot dp, 9 owned (dp == 0),
+// 10 interior (all 8 cells in this tile), 11-17 halo index h; -1 = no role
+__device__ __forceinline__ int make_role(int h) {
+    if (h >= 125) return -1;
+    const int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
+    const int dp = ((hx >> 2) << 2) | ((hy >> 2) << 1) | (hz >> 2);
+    const int loc = local_id(hx & 3, hy & 3, hz & 3);
+    const int interior = (hx >= 1 && hx <= 3 && hy >= 1 && hy <= 3 && hz >= 1 && hz <= 3);
+    return loc | (dp << 6) | ((dp == 0) << 9) | (interior << 10) | (h << 11);
+}
+
+template <class T, int NS>
+__global__ void __launch_bounds__(64) k_hvp_pipe(int T_, const int *__restrict__ nplus, const int *__restrict__ cstart,
+                                                 const uint8_t *__restrict__ clocal, const int *__restrict__ hascells,
+                                                 const T *__restrict__ K, const T *__restrict__ nmass,
+                                                 const vec4<T> *__restrict__ u, vec4<T> *__restrict__ Hu,
+                                                 double *__restrict__ uHu, const CGSlot *__restrict__ cgs, int cgj,
+                                                 double cgthr, const DevScalars *__restrict__ sc) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    PipeSmem<T, NS> &S = *reinterpret_cast<PipeSmem<T, NS> *>(smem_raw);
+    const int tid = threadIdx.x;
+    if (cgs != nullptr) {  // inside PCG: skip once converged / broken down (uniform per CTA)
+        double rr = stripe_sum_bcast(cgs[cgj].rr);
+        if (sc->neg_curv || (cgj > 0 && rr <= cgthr)) return;
+    }
+    const int role0 = make_role(tid), role1 = make_role(tid + 64);
+    if (tid == 0) {
+        for (int s = 0; s < NS; s++) mbar_init(&S.bar[s], 1);
+        mbar_fence_init();
+    }
+    for (int i = tid; i < 2 * 3 * 128; i += 64) (&S.F[0][0][0])[i] = T(0);
+    const int G = gridDim.x, t0 = blockIdx.x;
+    // register-staged metadata of the next tile to issue: tid < 8 neighbour slot tid, 8 cs, 9 ce, 10 has
+    auto load_meta = [&](int t) -> int {
+        if (t >= T_) return 0;
+        if (tid < 8) return tid ? nplus[8 * t + tid] : t;
+        if (tid == 8) return cstart[t];
+        if (tid == 9) return cstart[t + 1];
+        if (tid == 10) return hascells[t];
+        return 0;
+    };
+    auto put_meta = [&](int s, int t, int reg) {
+        if (tid < 8) S.nb[s][tid] = reg;
+        if (tid == 8) S.meta[s][0] = reg;
+        if (tid == 9) S.meta[s][1] = reg;  // ce for now; issue() turns it into ncp
+        if (tid == 10) S.meta[s][2] = reg;
+        if (tid == 11) S.meta[s][3] = t;
+    };
+    auto issue_role = [&](int s, int mi, int has, int role) {
+        if (role < 0) return;
+        const int loc = role & 63, dp = (role >> 6) & 7, owned = (role >> 9) & 1, h = role >> 11;
+        const int tt = S.nb[mi][dp];
+        if ((has || owned) && tt >= 0) {
+            const int64_t n = (int64_t)tt * 64 + loc;
+#pragma unroll
+            for (int q = 0; q < (int)(sizeof(vec4<T>) / 16); q++)
+                cp_async16(reinterpret_cast<char *>(&S.uh[s][h]) + 16 * q, reinterpret_cast<const char *>(u + n) + 16 * q);
+            if (owned) cp_async_real<T>(&S.mh[s][loc], nmass + n);
+        } else {
+            S.uh[s][h] = mk4<T>(0, 0, 0, 0);
+            if (owned) S.mh[s][loc] = T(0);
+        }
+    };
+    // all threads: after a barrier that published S.nb[s] / S.meta[s]
+    auto issue = [&](int s, int mi, int t) {
+        if (t < T_) {
+            const int cs = S.meta[mi][0], ncp = S.meta[mi][1] - cs, has = S.meta[mi][2];
+            const int nk = has ? ncp : 0;
+            if (tid == 0) {
+                const uint32_t bytes = (uint32_t)(nk * 45 * sizeof(T));
+                mbar_expect_tx(&S.bar[s], bytes);
+                if (bytes) bulk_g2s(S.K[s], K + (int64_t)cs * 45, bytes, &S.bar[s]);
+            }
+            if (tid * 4 < nk) cp_async4(&S.cl[s][tid * 4], clocal + cs + tid * 4);
+            issue_role(s, mi, has, role0);
+            issue_role(s, mi, has, role1);
+        }
+        cp_async_commit();
+    };
+    __syncthreads();
+    // prologue: tiles 0 .. NS-1 of this CTA in flight
+    for (int s = 0; s < NS; s++) {
+        const int t = t0 + s * G;
+        put_meta(s, t, load_meta(t));
+        __syncthreads();
+        issue(s, s, t);
+    }
+    int reg = load_meta(t0 + NS * G);
+    double acc = 0.0;
+    int it = 0;
+    for (int t = t0; t < T_; t += G, it++) {
+        const int st = it % NS;
+        const int mc = it % (NS + 1), mn = (it + NS) % (NS + 1);
+        cp_async_wait<NS - 1>();
+        mbar_wait(&S.bar[st], (uint32_t)((it / NS) & 1));
+        __syncthreads();  // (B) stage st complete for every thread
+        const int ncp = S.meta[mc][1] - S.meta[mc][0], has = S.meta[mc][2];
+        const vec4<T> *uh = S.uh[st];
+        // ---- cell phase: P = K dG, corner forces added to F with shared-memory atomics ---------
+        const int l = (has && tid < ncp) ? (int)S.cl[st][tid] : 0xFF;
+        if (l != 0xFF) {
+            const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+            constexpr int VEC = KL<T>::VEC, NCH = KL<T>::NCH;
+            const T *Ks = S.K[st];
+            T k[45];
+#pragma unroll
+            for (int c = 0; c < NCH; c++) lds_vec<T>(Ks + (c * ncp + tid) * VEC, k + c * VEC);
+            k[44] = Ks[NCH * VEC * ncp + tid];
+            T dG[9];
+#pragma unroll
+            for (int a = 0; a < 9; a++) dG[a] = T(0);
+            const int hb = (lx * 5 + ly) * 5 + lz;
+#pragma unroll
+            for (int o = 0; o < 8; o++) {
+                const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+                vec4<T> w = uh[hb + ox * 25 + oy * 5 + oz];
+                const T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
+                dG[0] += w.x * s0; dG[1] += w.x * s1; dG[2] += w.x * s2;
+                dG[3] += w.y * s0; dG[4] += w.y * s1; dG[5] += w.y * s2;
+                dG[6] += w.z * s0; dG[7] += w.z * s1; dG[8] += w.z * s2;
+            }
+            T P[9];
+#pragma unroll
+            for (int r = 0; r < 9; r++) P[r] = k[kidx(r, r)] * dG[r];
+#pragma unroll
+            for (int r = 0; r < 9; r++)
+#pragma unroll
+                for (int q = r + 1; q < 9; q++) {
+                    P[r] += k[kidx(r, q)] * dG[q];
+                    P[q] += k[kidx(r, q)] * dG[r];
+                }
+            T qf = T(0);
+#pragma unroll
+            for (int r = 0; r < 9; r++) qf += P[r] * dG[r];
+            acc += (double)qf;
+            // pass o adds to node cell + o: injective over the warp's cells, so no lane conflicts;
+            // each warp has its own F, so passes need only __syncwarp (no block barrier)
+            T *Fw = S.F[tid >> 5][0];
+#pragma unroll
+            for (int o = 0; o < 8; o++) {
+                const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+                const T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
+                const int h = hb + ox * 25 + oy * 5 + oz;
+                Fw[h] += P[0] * s0 + P[1] * s1 + P[2] * s2;
+                Fw[128 + h] += P[3] * s0 + P[4] * s1 + P[5] * s2;
+                Fw[256 + h] += P[6] * s0 + P[7] * s1 + P[8] * s2;
+                __syncwarp(__activemask());
+            }
+        }
+        // node-phase inputs that live in the stage go to registers, so the stage can be refilled
+        // right after the barrier
+        int64_t nidx[2];
+        T fm[2][3];
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+            const int role = r ? role1 : role0;
+            nidx[r] = -1;
+            fm[r][0] = fm[r][1] = fm[r][2] = T(0);
+            if (role < 0) continue;
+            const int loc = role & 63, dp = (role >> 6) & 7, owned = (role >> 9) & 1, h = role >> 11;
+            if (!has && !owned) continue;
+            const int tt = dp ? S.nb[mc][dp] : t;
+            if (tt < 0) continue;
+            nidx[r] = (int64_t)tt * 64 + loc;
+            if (owned) {
+                const T m = S.mh[st][loc];
+                if (m > T(0)) {
+                    const vec4<T> w = uh[h];
+                    fm[r][0] = m * w.x; fm[r][1] = m * w.y; fm[r][2] = m * w.z;
+                    acc += (double)(m * (w.x * w.x + w.y * w.y + w.z * w.z));
+                }
+            }
+        }
+        put_meta(mn, t + NS * G, reg);
+        __syncthreads();  // (C) F complete; stage st consumed; metadata of tile t + NS G visible
+        issue(st, mn, t + NS * G);
+        reg = load_meta(t + (NS + 1) * G);
+        // ---- node phase (two fixed roles per thread) -------------------------------------------
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+            const int role = r ? role1 : role0;
+            if (role < 0) continue;
+            const int h = role >> 11, interior = (role >> 10) & 1;
+            const T f0 = S.F[0][0][h] + S.F[1][0][h] + fm[r][0], f1 = S.F[0][1][h] + S.F[1][1][h] + fm[r][1],
+                    f2 = S.F[0][2][h] + S.F[1][2][h] + fm[r][2];
+            S.F[0][0][h] = S.F[0][1][h] = S.F[0][2][h] = S.F[1][0][h] = S.F[1][1][h] = S.F[1][2][h] = T(0);
+            if (nidx[r] < 0) continue;
+            if (interior) Hu[nidx[r]] = mk4<T>(f0, f1, f2, T(0));
+            else if (f0 != T(0) || f1 != T(0) || f2 != T(0)) atomic_add3<T>(Hu + nidx[r], f0, f1, f2);
+        }
+    }
+    cp_async_wait<0>();
+    if (uHu) {
+        double v = warp_sum(acc);
+        if ((tid & 31) == 0) S.red[tid >> 5] = v;
+        __syncthreads();
+        if (tid == 0) {
+            double s = S.red[0] + S.red[1];
+            if (s != 0.0) atomicAdd(&uHu[blockIdx.x % NSTRIPE], s);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// v4 (MPL_HVP_KERNEL=rp): persistent, register-pipelined.  The next tile's tangent goes straight
+// from HBM into the registers that just finished the current tile's K dG (16-byte loads coalesced
+// across the tile's cells, issued before the scatter / node phase, so those phases and the other
+// resident CTAs cover the load latency); the u halo / masses / cell ids of the next tile are
+// cp.async'ed into the other half of a 2-slot shared buffer.  No tangent staging in shared memory:
+// ~8 KB of shared memory per CTA, so registers alone bound occupancy.
+// ---------------------------------------------------------------------------------------------
+template <class T> struct RpSmem {
+    alignas(16) vec4<T> uh[2][128];
+    alignas(16) T mh[2][64];
+    alignas(16) uint8_t cl[2][64];
+    T F[2][3][128];
+    int nb[3][8];
+    int meta[3][4];  // cs, ce, has
+    double red[2];
+};
+
+template <class T>
+__global__ void __launch_bounds__(64) k_hvp_rp(int T_, const int *__restrict__ nplus, const int *__restrict__ cstart,
+                                               const uint8_t *__restrict__ clocal, const int *__restrict__ hascells,
+                                               const T *__restrict__ K, const T *__restrict__ nmass,
+                                               const vec4<T> *__restrict__ u, vec4<T> *__restrict__ Hu,
+                                               double *__restrict__ uHu, const CGSlot *__restrict__ cgs, int cgj,
+                                               double cgthr, const DevScalars *__restrict__ sc) {
+    __shared__ RpSmem<T> S;
+    const int tid = threadIdx.x;
+    if (cgs != nullptr) {
+        double rr = stripe_sum_bcast(cgs[cgj].rr);
+        if (sc->neg_curv || (cgj > 0 && rr <= cgthr)) return;
+    }
+    constexpr int VEC = KL<T>::VEC, NCH = KL<T>::NCH;
+    const int role0 = make_role(tid), role1 = make_role(tid + 64);
+    for (int i = tid; i < 2 * 3 * 128; i += 64) (&S.F[0][0][0])[i] = T(0);
+    const int G = gridDim.x, t0 = blockIdx.x;
+    auto load_meta = [&](int t) -> int {
+        if (t >= T_) return 0;
+        if (tid < 8) return tid ? nplus[8 * t + tid] : t;
+        if (tid == 8) return cstart[t];
+        if (tid == 9) return cstart[t + 1];
+        if (tid == 10) return hascells[t];
+        return 0;
+    };
+    auto put_meta = [&](int m, int reg) {
+        if (tid < 8) S.nb[m][tid] = reg;
+        else if (tid < 11) S.meta[m][tid - 8] = reg;
+    };
+    auto issue_role = [&](int b, int m, int has, int role) {
+        if (role < 0) return;
+        const int loc = role & 63, dp = (role >> 6) & 7, owned = (role >> 9) & 1, h = role >> 11;
+        const int tt = S.nb[m][dp];
+        if ((has || owned) && tt >= 0) {
+            const int64_t n = (int64_t)tt * 64 + loc;
+#pragma unroll
+            for (int q = 0; q < (int)(sizeof(vec4<T>) / 16); q++)
+                cp_async16(reinterpret_cast<char *>(&S.uh[b][h]) + 16 * q, reinterpret_cast<const char *>(u + n) + 16 * q);
+            if (owned) cp_async_real<T>(&S.mh[b][loc], nmass + n);
+        } else {
+            S.uh[b][h] = mk4<T>(0, 0, 0, 0);
+            if (owned) S.mh[b][loc] = T(0);
+        }
+    };
+    T k[45];
+    // tile t's tangent -> registers, its halo -> shared slot b (all threads, after its metadata is visible)
+    auto issue = [&](int t, int b, int m) {
+        if (t < T_) {
+            const int cs = S.meta[m][0], ncp = S.meta[m][1] - cs, has = S.meta[m][2];
+            if (has && tid < ncp) {
+                const T *base = K + (int64_t)cs * 45;
+#pragma unroll
+                for (int c = 0; c < NCH; c++) ldg_vec<T>(base + ((int64_t)c * ncp + tid) * VEC, k + c * VEC);
+                k[44] = __ldg(base + (int64_t)NCH * VEC * ncp + tid);
+            }
+            if (has && tid * 4 < ncp) cp_async4(&S.cl[b][tid * 4], clocal + cs + tid * 4);
+            issue_role(b, m, has, role0);
+            issue_role(b, m, has, role1);
+        }
+        cp_async_commit();
+    };
+    put_meta(0, load_meta(t0));
+    put_meta(1, load_meta(t0 + G));
+    __syncthreads();
+    issue(t0, 0, 0);
+    int reg = load_meta(t0 + 2 * G);
+    double acc = 0.0;
+    int it = 0;
+    for (int t = t0; t < T_; t += G, it++) {
+        const int b = it & 1, m = it % 3;
+        cp_async_wait<0>();
+        __syncthreads();  // (B) halo slot b complete; metadata slot (it+1)%3 visible
+        const int ncp = S.meta[m][1] - S.meta[m][0], has = S.meta[m][2];
+        const vec4<T> *uh = S.uh[b];
+        const int l = (has && tid < ncp) ? (int)S.cl[b][tid] : 0xFF;
+        T P[9];
+        int hb = 0;
+        if (l != 0xFF) {
+            const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+            hb = (lx * 5 + ly) * 5 + lz;
+            T dG[9];
+#pragma unroll
+            for (int a = 0; a < 9; a++) dG[a] = T(0);
+#pragma unroll
+            for (int o = 0; o < 8; o++) {
+                const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+                vec4<T> w = uh[hb + ox * 25 + oy * 5 + oz];
+                const T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
+                dG[0] += w.x * s0; dG[1] += w.x * s1; dG[2] += w.x * s2;
+                dG[3] += w.y * s0; dG[4] += w.y * s1; dG[5] += w.y * s2;
+                dG[6] += w.z * s0; dG[7] += w.z * s1; dG[8] += w.z * s2;
+            }
+#pragma unroll
+            for (int r = 0; r < 9; r++) P[r] = k[kidx(r, r)] * dG[r];
+#pragma unroll
+            for (int r = 0; r < 9; r++)
+#pragma unroll
+                for (int q = r + 1; q < 9; q++) {
+                    P[r] += k[kidx(r, q)] * dG[q];
+                    P[q] += k[kidx(r, q)] * dG[r];
+                }
+            T qf = T(0);
+#pragma unroll
+            for (int r = 0; r < 9; r++) qf += P[r] * dG[r];
+            acc += (double)qf;
+        }
+        // k is free: start the next tile's loads now; they overlap the scatter and node phase
+        issue(t + G, b ^ 1, (it + 1) % 3);
+        if (l != 0xFF) {
+            T *Fw = S.F[tid >> 5][0];
+#pragma unroll
+            for (int o = 0; o < 8; o++) {
+                const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+                const T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
+                const int h = hb + ox * 25 + oy * 5 + oz;
+                Fw[h] += P[0] * s0 + P[1] * s1 + P[2] * s2;
+                Fw[128 + h] += P[3] * s0 + P[4] * s1 + P[5] * s2;
+                Fw[256 + h] += P[6] * s0 + P[7] * s1 + P[8] * s2;
+                __syncwarp(__activemask());
+            }
+        }
+        int64_t nidx[2];
+        T fm[2][3];
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+            const int role = r ? role1 : role0;
+            nidx[r] = -1;
+            fm[r][0] = fm[r][1] = fm[r][2] = T(0);
+            if (role < 0) continue;
+            const int loc = role & 63, dp = (role >> 6) & 7, owned = (role >> 9) & 1, h = role >> 11;
+            if (!has && !owned) continue;
+            const int tt = dp ? S.nb[m][dp] : t;
+            if (tt < 0) continue;
+            nidx[r] = (int64_t)tt * 64 + loc;
+            if (owned) {
+                const T mm = S.mh[b][loc];
+                if (mm > T(0)) {
+                    const vec4<T> w = uh[h];
+                    fm[r][0] = mm * w.x; fm[r][1] = mm * w.y; fm[r][2] = mm * w.z;
+                    acc += (double)(mm * (w.x * w.x + w.y * w.y + w.z * w.z));
+                }
+            }
+        }
+        __syncthreads();  // (C) F complete
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+            const int role = r ? role1 : role0;
+            if (role < 0) continue;
+            const int h = role >> 11, interior = (role >> 10) & 1;
+            const T f0 = S.F[0][0][h] + S.F[1][0][h] + fm[r][0], f1 = S.F[0][1][h] + S.F[1][1][h] + fm[r][1],
+                    f2 = S.F[0][2][h] + S.F[1][2][h] + fm[r][2];
+            S.F[0][0][h] = S.F[0][1][h] = S.F[0][2][h] = S.F[1][0][h] = S.F[1][1][h] = S.F[1][2][h] = T(0);
+            if (nidx[r] < 0) continue;
+            if (interior) Hu[nidx[r]] = mk4<T>(f0, f1, f2, T(0));
+            else if (f0 != T(0) || f1 != T(0) || f2 != T(0)) atomic_add3<T>(Hu + nidx[r], f0, f1, f2);
+        }
+        put_meta((it + 2) % 3, reg);  // metadata of tile t + 2G (slot last read by tile t - G)
+        reg = load_meta(t + 3 * G);
+    }
+    cp_async_wait<0>();
+    if (uHu) {
+        double v = warp_sum(acc);
+        if ((tid & 31) == 0) S.red[tid >> 5] = v;
+        __syncthreads();
+        if (tid == 0) {
+            double s = S.red[0] + S.red[1];
+            if (s != 0.0) atomicAdd(&uHu[blockIdx.x % NSTRIPE], s);
+        }
+    }
+}
+
 int g_num_sms = 0;
+
+template <class T>
+mpl_status launch_rp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
+                     double cgthr) {
+    static int per_sm[2] = {0, 0};
+    const int pi = sizeof(T) == 8;
+    if (per_sm[pi] == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        int occ = 0;
+        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_rp<T>, 64, 0));
+        per_sm[pi] = occ > 0 ? occ : 1;
+    }
+    int grid = g_num_sms * per_sm[pi];
+    if (grid > ctx->T) grid = ctx->T;
+    k_hvp_rp<T><<<grid, 64, 0, ctx->stream>>>(
+        ctx->T, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p, (const uint8_t *)ctx->c_local.p,
+        (const int *)ctx->t_hascells.p, (const T *)ctx->K.p, (const T *)owned_mass(ctx), (const vec4<T> *)u_tile,
+        (vec4<T> *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p);
+    ctx->launches++;
+    MPL_CUDA(cudaGetLastError());
+    return MPL_OK;
+}
+
+template <class T, int NS>
+mpl_status launch_pipe(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
+                       double cgthr) {
+    static int per_sm[2] = {0, 0};
+    const int pi = sizeof(T) == 8;
+    const size_t smem = sizeof(PipeSmem<T, NS>);
+    if (per_sm[pi] == 0) {
+        MPL_CUDA(cudaFuncSetAttribute(k_hvp_pipe<T, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        int occ = 0;
+        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_pipe<T, NS>, 64, smem));
+        per_sm[pi] = occ > 0 ? occ : 1;
+    }
+    int grid = g_num_sms * per_sm[pi];
+    if (grid > ctx->T) grid = ctx->T;
+    k_hvp_pipe<T, NS><<<grid, 64, smem, ctx->stream>>>(
+        ctx->T, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p, (const uint8_t *)ctx->c_local.p,
+        (const int *)ctx->t_hascells.p, (const T *)ctx->K.p, (const T *)owned_mass(ctx), (const vec4<T> *)u_tile,
+        (vec4<T> *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p);
+    ctx->launches++;
+    MPL_CUDA(cudaGetLastError());
+    return MPL_OK;
+}
 
 }  // namespace
 
@@ -386,41 +692,25 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
     if (ctx->T == 0) return MPL_OK;
     static int variant = -1;
     if (variant < 0) {
+        // "pipe2" / "pipe3" (default pipe2): persistent pipelined v3 with 2 / 3 stages;
+        // "rp": persistent, tangent register-pipelined (v4); "reg": one tile per CTA (v2)
         const char *e = getenv("MPL_HVP_KERNEL");
-        variant = (e && e[0] == 't') ? 1 : 0;  // "tma" = persistent bulk-copy ring, default = register v2
+        variant = 2;
+        if (e && e[0] == 'r' && e[1] == 'p') variant = 4;
+        else if (e && e[0] == 'r') variant = 0;
+        else if (e && e[0] == 'p' && e[4] == '3') variant = 3;
     }
+    if (variant == 2) return launch_pipe<T, 2>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+    if (variant == 4) return launch_rp<T>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+    if (variant == 3) return launch_pipe<T, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
     if (variant == 0) {
         k_hvp_reg<T><<<ctx->T, 64, 0, ctx->stream>>>(
             (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p, (const uint8_t *)ctx->c_local.p,
-            (const int *)ctx->t_hascells.p, (const T *)ctx->K.p, (const T *)ctx->n_mass.p, (const vec4<T> *)u_tile,
+            (const int *)ctx->t_hascells.p, (const T *)ctx->K.p, (const T *)owned_mass(ctx), (const vec4<T> *)u_tile,
             (vec4<T> *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p);
         ctx->launches++;
         MPL_CUDA(cudaGetLastError());
-        return MPL_OK;
     }
-    static bool attr_set[2] = {false, false};
-    const size_t smem = sizeof(HvpSmem<T>);
-    const int pi = sizeof(T) == 8;
-    if (!attr_set[pi]) {
-        MPL_CUDA(cudaFuncSetAttribute(k_hvp_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set[pi] = true;
-    }
-    if (g_num_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    int per_sm = 0;
-    MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hvp_tma<T>, HVP_THREADS, smem));
-    if (per_sm < 1) per_sm = 1;
-    int grid = g_num_sms * per_sm;
-    if (grid > ctx->T) grid = ctx->T;
-    k_hvp_tma<T><<<grid, HVP_THREADS, smem, ctx->stream>>>(
-        ctx->T, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p, (const uint8_t *)ctx->c_local.p,
-        (const int *)ctx->t_hascells.p, (const T *)ctx->K.p, (const T *)ctx->n_mass.p, (const vec4<T> *)u_tile,
-        (vec4<T> *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p);
-    ctx->launches++;
-    MPL_CUDA(cudaGetLastError());
     return MPL_OK;
 }
 

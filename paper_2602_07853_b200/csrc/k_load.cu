@@ -19,8 +19,9 @@ __global__ void __launch_bounds__(128) k_n2c(GridP g, const int *__restrict__ np
                                              vec4<T> *__restrict__ vc, T *__restrict__ Gc) {
     __shared__ vec4<T> vh[125];
     const int t = blockIdx.x, tid = threadIdx.x;
-    if (!hascells[t]) return;
+    (void)hascells;  // every tile with structural cells: on a slab rank that includes the ghost plane
     const int cs = cstart[t], nc = cstart[t + 1] - cs;
+    if (nc == 0) return;
     for (int h = tid; h < 125; h += blockDim.x) {
         int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
         int dp = ((hx >> 2) << 2) | ((hy >> 2) << 1) | (hz >> 2);
@@ -56,11 +57,12 @@ __global__ void __launch_bounds__(128) k_n2c(GridP g, const int *__restrict__ np
 
 // per particle (sorted order): interpolate, advect, update F
 template <class T>
-__global__ void k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ skey, const int *__restrict__ nplus,
+__global__ void k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ skey, const int *__restrict__ pid,
+                      const int *__restrict__ nplus,
                       const int *__restrict__ cellof, const vec4<T> *__restrict__ vc, const T *__restrict__ Gc,
                       T *__restrict__ x, T *__restrict__ v, T *__restrict__ F, T *__restrict__ G) {
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= np) return;
+    if (p >= np || pid[p] < 0) return;  // ghosts (slab ranks) are advected by their owner
     const int key = skey[p];
     const int t = key >> 6, l = key & 63;
     const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
@@ -156,13 +158,16 @@ __global__ void k_export_q(int64_t C, int nmat, GridP g, const int *__restrict__
     }
 }
 
-__global__ void k_ccanon_flags(int64_t C, const uint8_t *__restrict__ clocal, int *__restrict__ act) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < C) act[i] = clocal[i] != 0xFF;
+// exported cells: structural cells of owned tiles (hascells), one thread per padded slot
+__global__ void k_ccanon_flags(const int *__restrict__ cstart, const int *__restrict__ hascells,
+                               const uint8_t *__restrict__ clocal, int *__restrict__ act) {
+    const int t = blockIdx.x;
+    const int cs = cstart[t], ce = cstart[t + 1];
+    if (cs + (int)threadIdx.x < ce) act[cs + threadIdx.x] = hascells[t] && clocal[cs + threadIdx.x] != 0xFF;
 }
-__global__ void k_ccanon_fix(int64_t C, const uint8_t *__restrict__ clocal, int *__restrict__ canon) {
+__global__ void k_ccanon_fix(int64_t C, const int *__restrict__ act, int *__restrict__ canon) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < C && clocal[i] == 0xFF) canon[i] = -1;
+    if (i < C && !act[i]) canon[i] = -1;
 }
 
 inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
@@ -174,6 +179,7 @@ mpl_status g2p_impl(mpl_ctx ctx, double dt) {
     cudaStream_t st = ctx->stream;
     const int T_ = ctx->T;
     const int c = ctx->cur;
+    MPL_CHECK(ghost_nodes_from_upper<T>(ctx, ctx->n_v.p));  // slab ranks: next slab's second node plane
     if (T_)
         k_n2c<T><<<T_, 128, 0, st>>>(ctx->grid, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,
                                      (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p,
@@ -181,6 +187,7 @@ mpl_status g2p_impl(mpl_ctx ctx, double dt) {
                                      (T *)ctx->q_Gc.p); ctx->launches++;
     if (ctx->np)
         k_c2p<T><<<nblk(ctx->np, 256), 256, 0, st>>>(ctx->grid, dt, ctx->np, (const int *)ctx->pskey.p,
+                                                    (const int *)ctx->pid[c].p,
                                                     (const int *)ctx->t_nplus.p, (const int *)ctx->t_cellof.p,
                                                     (const vec4<T> *)ctx->q_vc.p, (const T *)ctx->q_Gc.p,
                                                     (T *)ctx->px[c].p, (T *)ctx->pv.p, (T *)ctx->pF[c].p,
@@ -195,6 +202,7 @@ mpl_status g2p_impl(mpl_ctx ctx, double dt) {
 
 template <class T>
 mpl_status export_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G) {
+    if (multi(ctx)) return export_owned_particles<T>(ctx, x, v, F, G, nullptr, nullptr);
     cudaStream_t st = ctx->stream;
     const int64_t np = ctx->np;
     const int c = ctx->cur;
@@ -234,13 +242,14 @@ mpl_status export_quadrature(mpl_ctx ctx, int32_t *ijk, void *m_c, void *v_c, vo
         return MPL_ERR_OOM;
     }
     if (C) {
-        k_ccanon_flags<<<nblk(C, 256), 256, 0, st>>>(C, (const uint8_t *)ctx->c_local.p, (int *)act.p); ctx->launches++;
+        k_ccanon_flags<<<ctx->T, 64, 0, st>>>((const int *)ctx->t_cstart.p, (const int *)ctx->t_hascells.p,
+                                              (const uint8_t *)ctx->c_local.p, (int *)act.p); ctx->launches++;
         size_t tmp = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, tmp, (const int *)act.p, (int *)canon.p, (int)C, st);
         void *tp = nullptr;
         cudaMalloc(&tp, tmp + 16);
         cub::DeviceScan::ExclusiveSum(tp, tmp, (const int *)act.p, (int *)canon.p, (int)C, st);
-        k_ccanon_fix<<<nblk(C, 256), 256, 0, st>>>(C, (const uint8_t *)ctx->c_local.p, (int *)canon.p); ctx->launches++;
+        k_ccanon_fix<<<nblk(C, 256), 256, 0, st>>>(C, (const int *)act.p, (int *)canon.p); ctx->launches++;
         char *o = (char *)out.p;
         int32_t *d_ijk = (int32_t *)o; o += n * 3 * 4;
         T *d_m = (T *)o; o += n * s;

@@ -47,12 +47,12 @@ __global__ void k_bin_flags(GridP g, int64_t np, const T *__restrict__ x, const 
 
 // active node blocks = cell blocks dilated by +{0,1}^3; also counts active cell blocks
 __global__ void k_node_flags(GridP g, const int *__restrict__ cflag, int *__restrict__ nflag,
-                             unsigned long long *nblocks) {
+                             unsigned long long *nblocks, int xlo, int xhi) {
     int d = blockIdx.x * blockDim.x + threadIdx.x;
     int N = g.nb[0] * g.nb[1] * g.nb[2];
     if (d >= N || !cflag[d]) return;
-    atomicAdd(nblocks, 1ull);
     int bz = d % g.nb[2], by = (d / g.nb[2]) % g.nb[1], bx = d / (g.nb[1] * g.nb[2]);
+    if (bx >= xlo && bx < xhi) atomicAdd(nblocks, 1ull);  // owned cell blocks (slab)
     for (int o = 0; o < 8; o++) {
         int x = bx + ((o >> 2) & 1), y = by + ((o >> 1) & 1), z = bz + (o & 1);
         if (x < g.nb[0] && y < g.nb[1] && z < g.nb[2]) nflag[dense_id(g, x, y, z)] = 1;
@@ -74,9 +74,11 @@ __global__ void k_tiles(GridP g, const int *__restrict__ nflag, int *__restrict_
     }
 }
 
+// hascells[t]: the tile's cell block is active AND owned by this slab rank (physics runs on it);
+// cell blocks outside the slab (ghost planes) keep their structural cells for P2Q / G2P only.
 __global__ void k_tile_nbrs(GridP g, int T, const int *__restrict__ coord, const int *__restrict__ tile_of,
                             const int *__restrict__ cflag, int *__restrict__ nplus, int *__restrict__ nminus,
-                            int *__restrict__ hascells) {
+                            int *__restrict__ hascells, int xlo, int xhi) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= T) return;
     int c[3] = {coord[3 * t], coord[3 * t + 1], coord[3 * t + 2]};
@@ -87,7 +89,7 @@ __global__ void k_tile_nbrs(GridP g, int T, const int *__restrict__ coord, const
         x = c[0] - ox; y = c[1] - oy; z = c[2] - oz;
         nminus[8 * t + o] = (x >= 0 && y >= 0 && z >= 0) ? tile_of[dense_id(g, x, y, z)] : -1;
     }
-    hascells[t] = cflag[dense_id(g, c[0], c[1], c[2])];
+    hascells[t] = cflag[dense_id(g, c[0], c[1], c[2])] && c[0] >= xlo && c[0] < xhi;
 }
 
 // bucket key (tile*64 + local base cell) and rank inside the bucket
@@ -98,6 +100,7 @@ __global__ void k_count(GridP g, int64_t np, const int *__restrict__ base, const
     int b = base[p];
     int bx = b >> 20, by = (b >> 10) & 1023, bz = b & 1023;
     int t = tile_of[dense_id(g, bx >> 2, by >> 2, bz >> 2)];
+    DASSERT(t >= 0 && b >= 0);
     int k = t * 64 + local_id(bx & 3, by & 3, bz & 3);
     key[p] = k;
     rank[p] = atomicAdd(&bcount[k], 1);
@@ -146,6 +149,7 @@ __global__ void k_scatter(GridP g, MatP mp, int64_t np, const int *__restrict__ 
     if (p >= np) return;
     int k = key[p];
     int64_t d = bstart[k] + rank[p];
+    DASSERT(k >= 0 && d >= 0 && d < np);
     T xp[3], vp[3], Fp[9], Gp[9];
 #pragma unroll
     for (int a = 0; a < 3; a++) { xp[a] = x[3 * p + a]; vp[a] = v[3 * p + a]; }
@@ -189,8 +193,9 @@ __global__ void k_scatter(GridP g, MatP mp, int64_t np, const int *__restrict__ 
 
 // ---- structural cell masks: cell active iff some base-cell bucket in cell - {0,1}^3 is non-empty
 __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, const int *__restrict__ nminus,
-                            const int *__restrict__ bcount, unsigned long long *__restrict__ cmask,
-                            int *__restrict__ ccount, unsigned long long *ncells) {
+                            const int *__restrict__ bcount, const int *__restrict__ hascells,
+                            unsigned long long *__restrict__ cmask, int *__restrict__ ccount,
+                            unsigned long long *ncells) {
     int t = blockIdx.x;
     int l = threadIdx.x;  // 64 threads
     int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
@@ -216,7 +221,7 @@ __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, cons
         cmask[t] = m;
         int c = __popcll(m);
         ccount[t] = (c + 3) & ~3;
-        if (c) atomicAdd(ncells, (unsigned long long)c);
+        if (c && hascells[t]) atomicAdd(ncells, (unsigned long long)c);
     }
 }
 
@@ -335,48 +340,64 @@ __global__ void __launch_bounds__(64) k_p2q(GridP g, MatP mp, const int *__restr
 }
 
 // ---- a3: C2N gather (Alg. 2 lines 16-22) + Newton target and Dirichlet sets ----------
-template <class T>
+// PH 0: gather + finish in one pass (one rank).  PH 1: gather only, n_vn = ((mv)_i, m_i) partial
+// sums over this rank's cells (slab ranks; completed by c2n_halo).  PH 2: finish from n_vn.
+// Only owned cells (hascells of their tile) contribute; own[i] marks the copy counted by this rank.
+template <class T, int PH>
 __global__ void __launch_bounds__(64) k_c2n(GridP g, BoxP bx, double dt, double gx, double gy, double gz,
                                             const int *__restrict__ coord, const int *__restrict__ nminus,
-                                            const int *__restrict__ cellof, const T *__restrict__ q_m,
-                                            const T *__restrict__ q_mv, const T *__restrict__ q_mG,
-                                            T *__restrict__ n_mass, uint8_t *__restrict__ n_flag,
-                                            vec4<T> *__restrict__ n_vn, vec4<T> *__restrict__ n_vhat,
-                                            vec4<T> *__restrict__ n_v, unsigned long long *__restrict__ nfree) {
+                                            const int *__restrict__ cellof, const int *__restrict__ hascells,
+                                            const T *__restrict__ q_m, const T *__restrict__ q_mv,
+                                            const T *__restrict__ q_mG, T *__restrict__ n_mass,
+                                            uint8_t *__restrict__ n_flag, vec4<T> *__restrict__ n_vn,
+                                            vec4<T> *__restrict__ n_vhat, vec4<T> *__restrict__ n_v,
+                                            uint8_t *__restrict__ n_own, T *__restrict__ n_mown,
+                                            unsigned long long *__restrict__ nfree) {
     int t = blockIdx.x;
     int l = threadIdx.x;
     int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
     int ix = coord[3 * t] * 4 + lx, iy = coord[3 * t + 1] * 4 + ly, iz = coord[3 * t + 2] * 4 + lz;
-    T m = 0, mv[3] = {0, 0, 0};
-    const T hdx = T(0.5 * g.dx);
-    for (int o = 0; o < 8; o++) {
-        int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
-        int cx = ix - ox, cy = iy - oy, cz = iz - oz;  // node = cell + o
-        if (cx < 0 || cy < 0 || cz < 0 || cx >= g.n[0] || cy >= g.n[1] || cz >= g.n[2]) continue;
-        int bx_ = lx - ox, by_ = ly - oy, bz_ = lz - oz;
-        int dm = ((bx_ < 0) << 2) | ((by_ < 0) << 1) | (bz_ < 0);
-        int tt = nminus[8 * t + dm];
-        if (tt < 0) continue;
-        int cc = cellof[tt * 64 + local_id(bx_ & 3, by_ & 3, bz_ & 3)];
-        if (cc < 0) continue;
-        T mc = q_m[cc];
-        if (mc == T(0)) continue;
-        // x_i - x_c = dx (o - 1/2)
-        T d0 = ox ? hdx : -hdx, d1 = oy ? hdx : -hdx, d2 = oz ? hdx : -hdx;
-        const T *G = q_mG + 9 * (int64_t)cc;
-        m += T(0.125) * mc;
-        mv[0] += T(0.125) * (q_mv[3 * (int64_t)cc + 0] + G[0] * d0 + G[1] * d1 + G[2] * d2);
-        mv[1] += T(0.125) * (q_mv[3 * (int64_t)cc + 1] + G[3] * d0 + G[4] * d1 + G[5] * d2);
-        mv[2] += T(0.125) * (q_mv[3 * (int64_t)cc + 2] + G[6] * d0 + G[7] * d1 + G[8] * d2);
-    }
     int64_t nidx = (int64_t)t * 64 + l;
+    T m = 0, mv[3] = {0, 0, 0};
+    if (PH != 2) {
+        const T hdx = T(0.5 * g.dx);
+        for (int o = 0; o < 8; o++) {
+            int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+            int cx = ix - ox, cy = iy - oy, cz = iz - oz;  // node = cell + o
+            if (cx < 0 || cy < 0 || cz < 0 || cx >= g.n[0] || cy >= g.n[1] || cz >= g.n[2]) continue;
+            int bx_ = lx - ox, by_ = ly - oy, bz_ = lz - oz;
+            int dm = ((bx_ < 0) << 2) | ((by_ < 0) << 1) | (bz_ < 0);
+            int tt = nminus[8 * t + dm];
+            if (tt < 0 || !hascells[tt]) continue;
+            int cc = cellof[tt * 64 + local_id(bx_ & 3, by_ & 3, bz_ & 3)];
+            if (cc < 0) continue;
+            T mc = q_m[cc];
+            if (mc == T(0)) continue;
+            // x_i - x_c = dx (o - 1/2)
+            T d0 = ox ? hdx : -hdx, d1 = oy ? hdx : -hdx, d2 = oz ? hdx : -hdx;
+            const T *G = q_mG + 9 * (int64_t)cc;
+            m += T(0.125) * mc;
+            mv[0] += T(0.125) * (q_mv[3 * (int64_t)cc + 0] + G[0] * d0 + G[1] * d1 + G[2] * d2);
+            mv[1] += T(0.125) * (q_mv[3 * (int64_t)cc + 1] + G[3] * d0 + G[4] * d1 + G[5] * d2);
+            mv[2] += T(0.125) * (q_mv[3 * (int64_t)cc + 2] + G[6] * d0 + G[7] * d1 + G[8] * d2);
+        }
+        if (PH == 1) {
+            n_vn[nidx] = mk4<T>(mv[0], mv[1], mv[2], m);
+            n_own[nidx] = 1;
+            return;
+        }
+    } else {
+        vec4<T> a = n_vn[nidx];
+        mv[0] = a.x; mv[1] = a.y; mv[2] = a.z; m = a.w;
+    }
     vec4<T> vn = mk4<T>(0, 0, 0, 0), vh = mk4<T>(0, 0, 0, 0), v0 = mk4<T>(0, 0, 0, 0);
-    uint8_t flag = 0;
+    uint8_t flag = 0, own = 0;
     if (m > T(0)) {
         T im = T(1) / m;
         vn = mk4<T>(mv[0] * im, mv[1] * im, mv[2] * im, 0);
         vh = mk4<T>(vn.x + T(dt * gx), vn.y + T(dt * gy), vn.z + T(dt * gz), m);
         flag = 1;
+        own = PH == 2 ? n_own[nidx] : 1;
         v0 = mk4<T>(vh.x, vh.y, vh.z, 0);
         double xi[3] = {g.origin[0] + g.dx * ix, g.origin[1] + g.dx * iy, g.origin[2] + g.dx * iz};
         for (int b = 0; b < bx.nbox; b++) {
@@ -390,13 +411,15 @@ __global__ void __launch_bounds__(64) k_c2n(GridP g, BoxP bx, double dt, double 
             }
         }
     }
-    unsigned int fb = __ballot_sync(0xffffffffu, flag == 1);
+    unsigned int fb = __ballot_sync(0xffffffffu, flag == 1 && own);
     if ((threadIdx.x & 31) == 0 && fb) atomicAdd(nfree, (unsigned long long)__popc(fb));
     n_mass[nidx] = m;
     n_flag[nidx] = flag;
     n_vn[nidx] = vn;
     n_vhat[nidx] = vh;
     n_v[nidx] = v0;
+    n_own[nidx] = own;
+    if (PH == 2) n_mown[nidx] = own ? m : T(0);
 }
 
 __global__ void k_node_active(int64_t N, const uint8_t *__restrict__ flag, int *__restrict__ act) {
@@ -440,6 +463,7 @@ template <class T>
 mpl_status import_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v, const void *F, const void *G,
                             const void *vol, const int32_t *mat) {
     ctx->np = n;
+    ctx->np_own = n;
     ctx->cur = 0;
     size_t s = sizeof(T);
     MPL_CHECK(ensure(ctx, ctx->px[0], n * 3 * s));
@@ -474,11 +498,46 @@ template <class T>
 mpl_status resample_impl(mpl_ctx ctx, double dt) {
     cudaStream_t st = ctx->stream;
     const GridP &g = ctx->grid;
-    const int64_t np = ctx->np;
     const int N = g.nb[0] * g.nb[1] * g.nb[2];
     ctx->dense_n = N;
     ctx->dt = dt;
+    MPL_CHECK(redistribute_particles<T>(ctx));  // slab ranks: migration + ghosts (no-op on one rank)
+    DBG_GUARDS("after redistribute");
+    const int64_t np = ctx->np;
     int c = ctx->cur, nx = 1 - c;
+#ifdef MPL_DEBUG
+    // debug build: host-side consistency checks of the particle bookkeeping
+    auto count_neg = [&](const void *pid, int64_t n, int64_t *neg) -> mpl_status {
+        MPL_CUDA(cudaStreamSynchronize(st));
+        std::vector<int> h(n);
+        if (n) MPL_CUDA(cudaMemcpy(h.data(), pid, n * 4, cudaMemcpyDeviceToHost));
+        *neg = 0;
+        for (int64_t i = 0; i < n; i++) *neg += h[i] < 0;
+        return MPL_OK;
+    };
+    int64_t neg0 = 0;
+    MPL_CHECK(count_neg(ctx->pid[c].p, np, &neg0));
+    if (neg0 != np - ctx->np_own) {
+        ctx->err = "debug: after redistribute " + std::to_string(neg0) + " ghosts, expected " +
+                   std::to_string(np - ctx->np_own);
+        fprintf(stderr, "[rank %d] %s\n", ctx->rank, ctx->err.c_str());
+        return MPL_ERR_STATE;
+    }
+#endif
+    {
+        // per-particle scratch and the sorted-output buffer set (content not needed)
+        const size_t sz = sizeof(T);
+        MPL_CHECK(ensure(ctx, ctx->pkey, np * 4 + 16));
+        MPL_CHECK(ensure(ctx, ctx->prank, np * 4 + 16));
+        MPL_CHECK(ensure(ctx, ctx->pbase, np * 4 + 16));
+        MPL_CHECK(ensure(ctx, ctx->prec, np * REC * sz + 16));
+        MPL_CHECK(ensure(ctx, ctx->px[nx], np * 3 * sz + 16));
+        MPL_CHECK(ensure(ctx, ctx->pF[nx], np * 9 * sz + 16));
+        MPL_CHECK(ensure(ctx, ctx->pvol[nx], np * sz + 16));
+        MPL_CHECK(ensure(ctx, ctx->pmat[nx], np * 4 + 16));
+        MPL_CHECK(ensure(ctx, ctx->pid[nx], np * 4 + 16));
+    }
+    const int xlo = multi(ctx) ? ctx->slab_lo : -(1 << 30), xhi = multi(ctx) ? ctx->slab_hi : (1 << 30);
     DevScalars *sc = (DevScalars *)ctx->scalars.p;
     // reset error slots
     {
@@ -499,7 +558,10 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     // a0: base cells + active cell blocks
     if (np) k_bin_flags<T><<<nblk(np, 256), 256, 0, st>>>(g, np, (const T *)ctx->px[c].p, (const int *)ctx->pid[c].p,
                                                          (int *)ctx->pbase.p, (int *)ctx->cflag.p, sc); ctx->launches++;
-    k_node_flags<<<nblk(N, 256), 256, 0, st>>>(g, (const int *)ctx->cflag.p, (int *)ctx->nflag.p, counters + 0); ctx->launches++;
+    DBG_GUARDS("resample #1");
+    k_node_flags<<<nblk(N, 256), 256, 0, st>>>(g, (const int *)ctx->cflag.p, (int *)ctx->nflag.p, counters + 0, xlo,
+                                               xhi); ctx->launches++;
+    DBG_GUARDS("resample #2");
     MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->nflag.p, (int *)ctx->tile_of.p, N + 0));
     // fetch error flags + tile count (one sync)
     DevScalars hs;
@@ -510,11 +572,13 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     unsigned long long nblocks = 0;
     MPL_CUDA(cudaMemcpyAsync(&nblocks, counters + 0, 8, cudaMemcpyDeviceToHost, st));
     MPL_CUDA(cudaStreamSynchronize(st));
+    mpl_status bad = MPL_OK;
     if (hs.oob_particle != 0x7fffffff) {
         ctx->err = "particle " + std::to_string(hs.oob_particle) +
                    " is out of the domain: its base cell must satisfy 0 <= b <= N-2 on every axis";
-        return MPL_ERR_OUT_OF_DOMAIN;
+        bad = MPL_ERR_OUT_OF_DOMAIN;
     }
+    MPL_CHECK(agree(ctx, bad));
     const int T_ = last_tile + last_flag;
     ctx->T = T_;
     ctx->n_blocks_active = (int64_t)nblocks;
@@ -529,13 +593,22 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CHECK(ensure(ctx, ctx->t_bstart, ((size_t)T_ * 64 + 1) * 4 + 16));
     MPL_CHECK(ensure(ctx, ctx->t_cellof, (size_t)T_ * 64 * 4 + 16));
     k_tiles<<<nblk(N, 256), 256, 0, st>>>(g, (const int *)ctx->nflag.p, (int *)ctx->tile_of.p, (int *)ctx->t_coord.p); ctx->launches++;
+    DBG_GUARDS("resample #3");
     if (T_) k_tile_nbrs<<<nblk(T_, 128), 128, 0, st>>>(g, T_, (const int *)ctx->t_coord.p, (const int *)ctx->tile_of.p,
                                                      (const int *)ctx->cflag.p, (int *)ctx->t_nplus.p,
-                                                     (int *)ctx->t_nminus.p, (int *)ctx->t_hascells.p); ctx->launches++;
+                                                     (int *)ctx->t_nminus.p, (int *)ctx->t_hascells.p, xlo,
+                                                     xhi); ctx->launches++;
+    DBG_GUARDS("resample #4");
+    MPL_CHECK(build_interface_lists(ctx));
+    DBG_GUARDS("interface lists");
+#ifdef MPL_DEBUG
+    MPL_CHECK(debug_check_tiles(ctx, "after tile build"));
+#endif
     // particle buckets: key = tile*64 + local base cell; counting sort
     MPL_CUDA(cudaMemsetAsync(ctx->t_bcount.p, 0, ((size_t)T_ * 64 + 1) * 4, st));
     if (np) k_count<<<nblk(np, 256), 256, 0, st>>>(g, np, (const int *)ctx->pbase.p, (const int *)ctx->tile_of.p,
                                                   (int *)ctx->pkey.p, (int *)ctx->prank.p, (int *)ctx->t_bcount.p); ctx->launches++;
+    DBG_GUARDS("resample #5");
     MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_bcount.p, (int *)ctx->t_bstart.p, (int64_t)T_ * 64 + 1));
     // scatter into sorted order + records
     MPL_CHECK(ensure(ctx, ctx->pskey, (size_t)np * 4 + 16));
@@ -546,13 +619,31 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
             (const T *)ctx->pvol[c].p, (const int *)ctx->pmat[c].p, (const int *)ctx->pid[c].p, (T *)ctx->px[nx].p,
             (T *)ctx->pF[nx].p, (T *)ctx->pvol[nx].p, (int *)ctx->pmat[nx].p, (int *)ctx->pid[nx].p,
             (int *)ctx->pskey.p, (T *)ctx->prec.p, sc); ctx->launches++;
+    DBG_GUARDS("resample #6");
     ctx->cur = nx;
+#ifdef MPL_DEBUG
+    {
+        int bsum = 0;
+        MPL_CUDA(cudaStreamSynchronize(st));
+        MPL_CUDA(cudaMemcpy(&bsum, (int *)ctx->t_bstart.p + (size_t)T_ * 64, 4, cudaMemcpyDeviceToHost));
+        int64_t neg1 = 0;
+        MPL_CHECK(count_neg(ctx->pid[nx].p, np, &neg1));
+        if (bsum != np || neg1 != neg0) {
+            ctx->err = "debug: bucket total " + std::to_string(bsum) + " (np " + std::to_string(np) + "), ghosts " +
+                       std::to_string(neg1) + " after sort vs " + std::to_string(neg0) + ", T " + std::to_string(T_);
+            fprintf(stderr, "[rank %d] %s\n", ctx->rank, ctx->err.c_str());
+            return MPL_ERR_STATE;
+        }
+    }
+#endif
     // structural cells: masks, padded counts, compact offsets
     MPL_CHECK(ensure(ctx, ctx->t_ccount, (size_t)(T_ + 1) * 4 + 16));
     MPL_CUDA(cudaMemsetAsync(ctx->t_ccount.p, 0, (size_t)(T_ + 1) * 4, st));
     if (T_) k_cell_mask<<<T_, 64, 0, st>>>(g, T_, (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p,
-                                          (const int *)ctx->t_bcount.p, (unsigned long long *)ctx->t_cmask.p,
+                                          (const int *)ctx->t_bcount.p, (const int *)ctx->t_hascells.p,
+                                          (unsigned long long *)ctx->t_cmask.p,
                                           (int *)ctx->t_ccount.p, counters + 1); ctx->launches++;
+    DBG_GUARDS("resample #7");
     MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_ccount.p, (int *)ctx->t_cstart.p, (int64_t)T_ + 1));
     int Cpad = 0;
     unsigned long long ncells = 0;
@@ -560,10 +651,14 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CUDA(cudaMemcpyAsync(&ncells, counters + 1, 8, cudaMemcpyDeviceToHost, st));
     MPL_CUDA(cudaMemcpyAsync(&hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
     MPL_CUDA(cudaStreamSynchronize(st));
+    bad = MPL_OK;
     if (hs.inv_particle != 0x7fffffff) {
         ctx->err = "particle " + std::to_string(hs.inv_particle) + " has det F_p <= 0 (inverted element)";
+        bad = MPL_ERR_INVERTED;
+    }
+    if (agree(ctx, bad) != MPL_OK) {
         ctx->cur = c;  // particle state unchanged
-        return MPL_ERR_INVERTED;
+        return bad != MPL_OK ? bad : MPL_ERR_STATE;
     }
     ctx->C = Cpad;
     ctx->n_cells_active = (int64_t)ncells;
@@ -581,9 +676,11 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     if (T_) {
         k_cell_list<<<T_, 64, 0, st>>>(T_, (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_cstart.p,
                                        (uint8_t *)ctx->c_local.p, (int *)ctx->t_cellof.p); ctx->launches++;
+    DBG_GUARDS("resample #8");
         k_p2q<T><<<T_, 64, 0, st>>>(g, ctx->mats, (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p,
                                     (const int *)ctx->t_bstart.p, (const int *)ctx->t_cellof.p, (const T *)ctx->prec.p,
                                     (T *)ctx->q_m.p, (T *)ctx->q_mv.p, (T *)ctx->q_mG.p, (T *)ctx->q_slot.p); ctx->launches++;
+    DBG_GUARDS("resample #9");
     }
     // nodes
     const size_t NN = (size_t)T_ * 64 + 64;
@@ -593,25 +690,40 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
                       &ctx->n_x, &ctx->n_r, &ctx->n_p, &ctx->n_Hp, &ctx->n_u, &ctx->n_u2};
     for (DevBuf *b : vecs) MPL_CHECK(ensure(ctx, *b, NN * 4 * s));
     MPL_CHECK(ensure(ctx, ctx->n_act, NN * 4));
+    MPL_CHECK(ensure(ctx, ctx->n_own, NN));
+    if (multi(ctx)) MPL_CHECK(ensure(ctx, ctx->n_mown, NN * s));
     MPL_CHECK(ensure(ctx, ctx->n_canon, NN * 4));
     MPL_CHECK(ensure(ctx, ctx->n_list, NN * 4));
-    if (T_)
-        k_c2n<T><<<T_, 64, 0, st>>>(g, ctx->boxes, dt, ctx->gravity[0], ctx->gravity[1], ctx->gravity[2],
-                                    (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p,
-                                    (const int *)ctx->t_cellof.p, (const T *)ctx->q_m.p, (const T *)ctx->q_mv.p,
-                                    (const T *)ctx->q_mG.p, (T *)ctx->n_mass.p, (uint8_t *)ctx->n_flag.p,
-                                    (vec4<T> *)ctx->n_vn.p, (vec4<T> *)ctx->n_vhat.p, (vec4<T> *)ctx->n_v.p,
-                                    counters + 2); ctx->launches++;
+#define C2N_ARGS                                                                                                  \
+    g, ctx->boxes, dt, ctx->gravity[0], ctx->gravity[1], ctx->gravity[2], (const int *)ctx->t_coord.p,            \
+        (const int *)ctx->t_nminus.p, (const int *)ctx->t_cellof.p, (const int *)ctx->t_hascells.p,                \
+        (const T *)ctx->q_m.p, (const T *)ctx->q_mv.p, (const T *)ctx->q_mG.p, (T *)ctx->n_mass.p,                \
+        (uint8_t *)ctx->n_flag.p, (vec4<T> *)ctx->n_vn.p, (vec4<T> *)ctx->n_vhat.p, (vec4<T> *)ctx->n_v.p,          \
+        (uint8_t *)ctx->n_own.p, (T *)ctx->n_mown.p, counters + 2
+    if (!multi(ctx)) {
+        if (T_) k_c2n<T, 0><<<T_, 64, 0, st>>>(C2N_ARGS), ctx->launches++;
+    DBG_GUARDS("resample #10");
+    } else {
+        if (T_) k_c2n<T, 1><<<T_, 64, 0, st>>>(C2N_ARGS), ctx->launches++;
+    DBG_GUARDS("resample #11");
+        MPL_CHECK(c2n_halo<T>(ctx));
+        DBG_GUARDS("c2n_halo");
+        if (T_) k_c2n<T, 2><<<T_, 64, 0, st>>>(C2N_ARGS), ctx->launches++;
+    DBG_GUARDS("resample #12");
+    }
+#undef C2N_ARGS
     const int64_t NT = (int64_t)T_ * 64;
     int nact = 0;
     if (NT) {
         k_node_active<<<nblk(NT, 256), 256, 0, st>>>(NT, (const uint8_t *)ctx->n_flag.p, (int *)ctx->n_act.p); ctx->launches++;
+    DBG_GUARDS("resample #13");
         MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->n_act.p, (int *)ctx->n_canon.p, NT));
         int lc = 0, la = 0;  // read before k_node_canon rewrites inactive entries (stream order)
         MPL_CUDA(cudaMemcpyAsync(&lc, (int *)ctx->n_canon.p + (NT - 1), 4, cudaMemcpyDeviceToHost, st));
         MPL_CUDA(cudaMemcpyAsync(&la, (int *)ctx->n_act.p + (NT - 1), 4, cudaMemcpyDeviceToHost, st));
         k_node_canon<<<nblk(NT, 256), 256, 0, st>>>(NT, (const uint8_t *)ctx->n_flag.p, (int *)ctx->n_canon.p,
                                                     (int *)ctx->n_list.p); ctx->launches++;
+    DBG_GUARDS("resample #14");
         MPL_CUDA(cudaStreamSynchronize(st));
         nact = lc + la;
         unsigned long long nf = 0;
@@ -621,6 +733,9 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     ctx->n_nodes_active = nact;
     MPL_CUDA(cudaGetLastError());
     MPL_CUDA(cudaStreamSynchronize(st));
+#ifdef MPL_DEBUG
+    MPL_CHECK(debug_check_tiles(ctx, "end of resample"));
+#endif
     ctx->resampled = true;
     ctx->linearized = false;
     ctx->solved = false;

@@ -58,24 +58,26 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
     const int t = blockIdx.x, tid = threadIdx.x;
     const int has = hascells[t];
     const int cs = cstart[t], nc = cstart[t + 1] - cs;
+    DASSERT(nc >= 0 && nc <= 64 && cstart[t + 1] <= cstart[gridDim.x]);
     for (int h = tid; h < 125; h += blockDim.x) {
         int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
         bool owned = hx < 4 && hy < 4 && hz < 4;
         int64_t n = (has || owned) ? halo_node(t, nplus, h) : -1;
+        DASSERT(n < (int64_t)gridDim.x * 64);
         vh[h] = n >= 0 ? v[n] : mk4<T>(0, 0, 0, 0);
     }
     if (tid < 64) cslot[tid] = -1;
     if (MODE == LIN_FULL)
         for (int i = tid; i < nc * 45; i += blockDim.x) Ks[i] = T(0);
     __syncthreads();
-    if (tid < nc) {
+    if (has && tid < nc) {
         int l = clocal[cs + tid];
         if (l != 0xFF) cslot[l] = tid;
     }
     double e_loc = 0.0;
     const T dt = T(dt_);
     const T q = T(0.25 * g.inv_dx);  // grad w = s q, s in {-1,+1}^3
-    if (tid < nc) {
+    if (has && tid < nc) {
         int l = clocal[cs + tid];
         if (l != 0xFF) {
             int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
@@ -95,7 +97,7 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
 #pragma unroll
             for (int a = 0; a < 9; a++) { W[a] = dt * q * Gs[a]; A[a] = W[a] + ((a % 4 == 0) ? T(1) : T(0)); }
             T detA = inv_transpose3(A, AiT);
-            if (!(detA > T(0))) sc->inverted = 1;  // amb-21: Phi = +inf
+            if (!(detA > T(0))) sc->inv_any = 1.0;  // amb-21: Phi = +inf
             T Pc[9];
 #pragma unroll
             for (int a = 0; a < 9; a++) Pc[a] = T(0);
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
         }
     }
     __syncthreads();
-    if (MODE == LIN_FULL) {  // tile's tangent block, permuted into the chunked (coalesced) layout
+    if (MODE == LIN_FULL && has) {  // tile's tangent block, permuted into the chunked (coalesced) layout
         const int64_t base = (int64_t)cs * 45;
         for (int i = tid; i < nc * 45; i += blockDim.x) Kout[k_off<T>(base, nc, i / 45, i % 45)] = Ks[i];
     }
@@ -262,6 +264,7 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
             }
         }
         int64_t n = (owned || has) ? halo_node(t, nplus, h) : -1;
+        DASSERT(n < (int64_t)gridDim.x * 64);
         if (n >= 0) {
             if (owned) {
                 T m = nmass[n];
@@ -306,7 +309,8 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
 // r = -g, invD = 1/D on free DOFs; z = invD r; p = z; x = 0; slot[0] = (r.z, r.r)
 template <class T>
 __global__ void __launch_bounds__(256) k_pcg_init(int64_t n, const int *__restrict__ list,
-                                                  const uint8_t *__restrict__ flag, const vec4<T> *__restrict__ g,
+                                                  const uint8_t *__restrict__ flag, const uint8_t *__restrict__ own,
+                                                  const vec4<T> *__restrict__ g,
                                                   const vec4<T> *__restrict__ D, vec4<T> *__restrict__ invD,
                                                   vec4<T> *__restrict__ r, vec4<T> *__restrict__ p,
                                                   vec4<T> *__restrict__ x, CGSlot *slot) {
@@ -316,11 +320,12 @@ __global__ void __launch_bounds__(256) k_pcg_init(int64_t n, const int *__restri
         vec4<T> rv = mk4<T>(0, 0, 0, 0), zv = mk4<T>(0, 0, 0, 0), iv = mk4<T>(0, 0, 0, 0);
         if (flag[ti] == 1) {
             vec4<T> gv = g[ti], dv = D[ti];
+            const T w = T(own[ti]);  // r.w carries the owner weight of the node's dot-product terms
             iv = mk4<T>(T(1) / dv.x, T(1) / dv.y, T(1) / dv.z, T(1));
-            rv = mk4<T>(-gv.x, -gv.y, -gv.z, 0);
+            rv = mk4<T>(-gv.x, -gv.y, -gv.z, w);
             zv = mk4<T>(rv.x * iv.x, rv.y * iv.y, rv.z * iv.z, 0);
-            rz += rv.x * zv.x + rv.y * zv.y + rv.z * zv.z;
-            rr += rv.x * rv.x + rv.y * rv.y + rv.z * rv.z;
+            rz += w * (rv.x * zv.x + rv.y * zv.y + rv.z * zv.z);
+            rr += w * (rv.x * rv.x + rv.y * rv.y + rv.z * rv.z);
         }
         invD[i] = iv;
         r[i] = rv;
@@ -378,8 +383,8 @@ __global__ void __launch_bounds__(256) k_pcg_update1(int64_t n, const int *__res
         rv.x -= aw * hv.x; rv.y -= aw * hv.y; rv.z -= aw * hv.z;
         x[i] = xv;
         r[i] = rv;
-        rz = rv.x * rv.x * iv.x + rv.y * rv.y * iv.y + rv.z * rv.z * iv.z;
-        rr = rv.x * rv.x + rv.y * rv.y + rv.z * rv.z;
+        rz = rv.w * (rv.x * rv.x * iv.x + rv.y * rv.y * iv.y + rv.z * rv.z * iv.z);
+        rr = rv.w * (rv.x * rv.x + rv.y * rv.y + rv.z * rv.z);
     }
     block_add((double)rz, slot[j + 1].rz);
     block_add((double)rr, slot[j + 1].rr);
@@ -406,11 +411,12 @@ __global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, const int *__res
 // g . x over free DOFs (g tile-dense, x compact)
 template <class T>
 __global__ void k_dot_gx(int64_t n, const int *__restrict__ list, const uint8_t *__restrict__ flag,
-                         const vec4<T> *__restrict__ g, const vec4<T> *__restrict__ x, double *out) {
+                         const uint8_t *__restrict__ own, const vec4<T> *__restrict__ g, const vec4<T> *__restrict__ x,
+                         double *out) {
     double s = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int ti = list[i];
-        if (flag[ti] != 1) continue;
+        if (flag[ti] != 1 || !own[ti]) continue;
         vec4<T> a = g[ti], b = x[i];
         s += (double)(a.x * b.x + a.y * b.y + a.z * b.z);
     }
@@ -439,11 +445,11 @@ __global__ void k_zero4(int64_t N, vec4<T> *a) {
 
 // g . x over free nodes
 template <class T>
-__global__ void k_dot_free(int64_t N, const uint8_t *__restrict__ flag, const vec4<T> *__restrict__ a,
-                           const vec4<T> *__restrict__ b, double *out) {
+__global__ void k_dot_free(int64_t N, const uint8_t *__restrict__ flag, const uint8_t *__restrict__ own,
+                           const vec4<T> *__restrict__ a, const vec4<T> *__restrict__ b, double *out) {
     double s = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
-        if (flag[i] != 1) continue;
+        if (flag[i] != 1 || !own[i]) continue;
         vec4<T> x = a[i], y = b[i];
         s += (double)(x.x * y.x + x.y * y.y + x.z * y.z);
     }
@@ -520,18 +526,20 @@ mpl_status tile_to_canon(mpl_ctx ctx, const void *src_tile, void *dst) {
 template <class T>
 mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi) {
     cudaStream_t st = ctx->stream;
+#ifdef MPL_DEBUG
+    MPL_CHECK(debug_check_tiles(ctx, "linearize"));
+#endif
     const int T_ = ctx->T;
     const int64_t NT = (int64_t)T_ * 64;
     DevScalars *sc = (DevScalars *)ctx->scalars.p;
-    MPL_CUDA(cudaMemsetAsync(sc->energy, 0, sizeof(sc->energy), st));
-    MPL_CUDA(cudaMemsetAsync(&sc->inverted, 0, sizeof(int), st));
+    MPL_CUDA(cudaMemsetAsync(sc->energy, 0, sizeof(sc->energy) + sizeof(double), st));  // + inv_any
     if (mode != LIN_ENERGY) MPL_CUDA(cudaMemsetAsync(ctx->n_g.p, 0, NT * sizeof(vec4<T>), st));
     if (mode == LIN_FULL) MPL_CUDA(cudaMemsetAsync(ctx->n_diag.p, 0, NT * sizeof(vec4<T>), st));
     if (T_) {
 #define LIN_ARGS                                                                                                  \
     ctx->grid, ctx->mats, ctx->dt, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,                     \
         (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p, (const vec4<T> *)v_tile,                  \
-        (const vec4<T> *)ctx->n_vhat.p, (const T *)ctx->n_mass.p, (const T *)ctx->q_slot.p, (T *)ctx->K.p,         \
+        (const vec4<T> *)ctx->n_vhat.p, (const T *)owned_mass(ctx), (const T *)ctx->q_slot.p, (T *)ctx->K.p,       \
         (vec4<T> *)ctx->n_g.p, (vec4<T> *)ctx->n_diag.p, sc
         if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY><<<T_, 128, 0, st>>>(LIN_ARGS);
         else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD><<<T_, 128, 0, st>>>(LIN_ARGS);
@@ -540,13 +548,14 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
 #undef LIN_ARGS
     }
     MPL_CUDA(cudaGetLastError());
+    // slab ranks: complete g / diag on the shared node planes, sum Phi over ranks
+    if (mode != LIN_ENERGY) MPL_CHECK(halo_sum_nodes<T>(ctx, ctx->n_g.p, mode == LIN_FULL ? ctx->n_diag.p : nullptr));
+    MPL_CHECK(allreduce_d(ctx, sc->energy, NSTRIPE + 1));
     if (phi) {
-        double e[NSTRIPE];
-        int inv = 0;
+        double e[NSTRIPE + 1];
         MPL_CUDA(cudaMemcpyAsync(e, sc->energy, sizeof e, cudaMemcpyDeviceToHost, st));
-        MPL_CUDA(cudaMemcpyAsync(&inv, &sc->inverted, sizeof(int), cudaMemcpyDeviceToHost, st));
         MPL_CUDA(cudaStreamSynchronize(st));
-        *phi = inv ? __builtin_inf() : host_stripes(e);
+        *phi = e[NSTRIPE] != 0.0 ? __builtin_inf() : host_stripes(e);
     }
     if (mode == LIN_FULL) ctx->linearized = true;
     return MPL_OK;
@@ -556,7 +565,8 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
 template <class T>
 mpl_status hvp_tile(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu_accum) {
     MPL_CUDA(cudaMemsetAsync(Hu_tile, 0, (size_t)ctx->T * 64 * sizeof(vec4<T>), ctx->stream));
-    return launch_hvp<T>(ctx, u_tile, Hu_tile, uHu_accum, nullptr, 0, 0.0);
+    MPL_CHECK(launch_hvp<T>(ctx, u_tile, Hu_tile, uHu_accum, nullptr, 0, 0.0));
+    return halo_sum_nodes<T>(ctx, Hu_tile, nullptr);
 }
 
 namespace {
@@ -581,6 +591,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     MPL_CHECK(ensure(ctx, ctx->cg_slots, (size_t)slots_needed * sizeof(CGSlot)));
     CGSlot *slots = (CGSlot *)ctx->cg_slots.p;
     const uint8_t *flag = (const uint8_t *)ctx->n_flag.p;
+    const uint8_t *own = (const uint8_t *)ctx->n_own.p;
     vec4<T> *v = (vec4<T> *)ctx->n_v.p, *vt = (vec4<T> *)ctx->n_vt.p;
     vec4<T> *g = (vec4<T> *)ctx->n_g.p, *D = (vec4<T> *)ctx->n_diag.p;
     MPL_CHECK(ensure(ctx, ctx->n_invD, (size_t)NT * sizeof(vec4<T>) + 64));
@@ -612,18 +623,17 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         MPL_CUDA(cudaMemsetAsync(&sc->neg_curv, 0, sizeof(int), st));
         MPL_CUDA(cudaMemsetAsync(&sc->cg_done_iter, 0xff, sizeof(int), st));
         MPL_CUDA(cudaMemsetAsync(p, 0, NT * sizeof(vec4<T>), st));
-        k_pcg_init<T><<<VA, 256, 0, st>>>(NA, list, flag, g, D, invD, r, p, x, slots); ctx->launches++;
+        k_pcg_init<T><<<VA, 256, 0, st>>>(NA, list, flag, own, g, D, invD, r, p, x, slots); ctx->launches++;
+        MPL_CHECK(allreduce_d(ctx, slots[0].rz, 3 * NSTRIPE));
         MPL_CUDA(cudaMemsetAsync(Hp, 0, NT * sizeof(vec4<T>), st));
         cudaEventRecord(e1, st);
         CGSlot s0;
-        double e[NSTRIPE];
-        int inv = 0;
+        double e[NSTRIPE + 1];
         MPL_CUDA(cudaMemcpyAsync(&s0, slots, sizeof s0, cudaMemcpyDeviceToHost, st));
         MPL_CUDA(cudaMemcpyAsync(e, sc->energy, sizeof e, cudaMemcpyDeviceToHost, st));
-        MPL_CUDA(cudaMemcpyAsync(&inv, &sc->inverted, sizeof inv, cudaMemcpyDeviceToHost, st));
         MPL_CUDA(cudaStreamSynchronize(st));
         t_lin += elapsed(e0, e1);
-        phi0 = inv ? __builtin_inf() : host_stripes(e);
+        phi0 = e[NSTRIPE] != 0.0 ? __builtin_inf() : host_stripes(e);
         const double rr0 = host_stripes(s0.rr);
         const double gn = sqrt(rr0);
         if (k == 0) S.grad_norm0 = gn;
@@ -652,9 +662,14 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     cudaEventRecord(hev[S.n_hvp].first, st);
                     // the HVP is skipped on device once converged (its output is then unused)
                     MPL_CHECK(launch_hvp<T>(ctx, p, Hp, slots[jj].pHp, slots, jj, thr));
+                    if (multi(ctx)) {  // complete Hp on the shared planes; global p.Hp (timed with the HVP)
+                        MPL_CHECK(halo_sum_nodes<T>(ctx, Hp, nullptr));
+                        MPL_CHECK(allreduce_d(ctx, slots[jj].pHp, NSTRIPE));
+                    }
                     cudaEventRecord(hev[S.n_hvp].second, st);
                     S.n_hvp++;
                     k_pcg_update1<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc); ctx->launches++;
+                    MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
                     k_pcg_update2<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, slots, sc); ctx->launches++;
                 }
                 launched += n;
@@ -690,7 +705,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         // ---- Armijo backtracking line search ------------------------------------------------
         cudaEventRecord(e0, st);
         MPL_CUDA(cudaMemsetAsync(sc->gp, 0, sizeof(sc->gp), st));
-        k_dot_gx<T><<<VA, 256, 0, st>>>(NA, list, flag, g, x, sc->gp); ctx->launches++;
+        k_dot_gx<T><<<VA, 256, 0, st>>>(NA, list, flag, own, g, x, sc->gp); ctx->launches++;
+        MPL_CHECK(allreduce_d(ctx, sc->gp, NSTRIPE));
         double gps[NSTRIPE];
         MPL_CUDA(cudaMemcpyAsync(gps, sc->gp, sizeof gps, cudaMemcpyDeviceToHost, st));
         MPL_CUDA(cudaStreamSynchronize(st));
@@ -726,7 +742,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     if (!fixed && S.newton_iters == kmax && !S.converged) {
         MPL_CHECK(linearize_impl<T>(ctx, v, LIN_GRAD, nullptr));
         MPL_CUDA(cudaMemsetAsync(sc->gnorm2, 0, sizeof(sc->gnorm2), st));
-        k_dot_free<T><<<VG, 256, 0, st>>>(NT, flag, g, g, sc->gnorm2); ctx->launches++;
+        k_dot_free<T><<<VG, 256, 0, st>>>(NT, flag, own, g, g, sc->gnorm2); ctx->launches++;
+        MPL_CHECK(allreduce_d(ctx, sc->gnorm2, NSTRIPE));
         double g2[NSTRIPE];
         MPL_CUDA(cudaMemcpyAsync(g2, sc->gnorm2, sizeof g2, cudaMemcpyDeviceToHost, st));
         MPL_CUDA(cudaStreamSynchronize(st));

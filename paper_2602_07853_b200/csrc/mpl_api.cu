@@ -1,9 +1,53 @@
 // mpl_api.cu — the C ABI declared in include/mpmlite.h.  Argument checking, context state and
 // dispatch on the context precision; all numerical work runs in the k_*.cu kernels.
 #include <cmath>
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "mpl_common.cuh"
+
+// ---- MPL_LOOPBACK_SERIAL: process-wide API lock (see mpl_comm.cu group_barrier) -----------------
+namespace {
+std::recursive_mutex g_api_mu;
+thread_local int t_api_depth = 0;
+}  // namespace
+bool serial_mode() {
+    static int s = -1;
+    if (s < 0) {
+        const char *e = getenv("MPL_LOOPBACK_SERIAL");
+        s = (e && e[0] == '1') ? 1 : 0;
+    }
+    return s == 1;
+}
+ApiLock::ApiLock() : on(serial_mode()) {
+    if (on) {
+        g_api_mu.lock();
+        t_api_depth++;
+    }
+}
+ApiLock::~ApiLock() {
+    if (on) {
+        t_api_depth--;
+        g_api_mu.unlock();
+    }
+}
+int api_lock_release_all() {
+    const int d = t_api_depth;
+    for (int i = 0; i < d; i++) g_api_mu.unlock();
+    return d;
+}
+void api_lock_reacquire(int depth) {
+    for (int i = 0; i < depth; i++) g_api_mu.lock();
+}
+
+#ifdef MPL_DEBUG
+constexpr size_t GUARD = 1 << 16;  // debug build: a filled guard zone after every buffer
+#else
+constexpr size_t GUARD = 0;
+#endif
 
 mpl_status ensure(mpl_ctx ctx, DevBuf &b, size_t bytes) {
     if (bytes == 0) bytes = 16;
@@ -12,15 +56,60 @@ mpl_status ensure(mpl_ctx ctx, DevBuf &b, size_t bytes) {
     b.p = nullptr;
     b.cap = 0;
     size_t want = bytes + bytes / 8;  // headroom: the active set grows as particles move
-    cudaError_t e = cudaMalloc(&b.p, want);
+    cudaError_t e = cudaMalloc(&b.p, want + GUARD);
     if (e != cudaSuccess) {
         cudaGetLastError();
         ctx->err = "cudaMalloc of " + std::to_string(want) + " bytes failed: " + cudaGetErrorString(e);
         return MPL_ERR_OOM;
     }
+    if (GUARD) {
+        cudaError_t me = cudaMemset((char *)b.p + want, 0xAB, GUARD);
+        cudaError_t se = cudaDeviceSynchronize();
+        if (me != cudaSuccess || se != cudaSuccess)
+            fprintf(stderr, "[rank %d] guard memset failed: %s / %s\n", ctx->rank, cudaGetErrorString(me),
+                    cudaGetErrorString(se));
+    }
     b.cap = want;
     return MPL_OK;
 }
+
+#ifdef MPL_DEBUG
+mpl_status debug_check_guards(mpl_ctx ctx, const char *where) {
+    MPL_CUDA(cudaStreamSynchronize(ctx->stream));
+    MPL_CUDA(cudaDeviceSynchronize());
+    std::vector<unsigned char> h(GUARD);
+    std::string bad;
+    for_each_buf(ctx, [&](const char *name, DevBuf &b) {
+        if (!b.p) return;
+        if (cudaMemcpy(h.data(), (char *)b.p + b.cap, GUARD, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            bad += std::string(" [guard read failed for ") + name + "]";
+            return;
+        }
+        size_t first = GUARD, last = 0, nbad = 0;
+        for (size_t i = 0; i < GUARD; i++)
+            if (h[i] != 0xAB) {
+                first = std::min(first, i);
+                last = i;
+                nbad++;
+            }
+        if (nbad) {
+            char buf[256];
+            snprintf(buf, sizeof buf, " [%s p=%p cap=%zu: %zu bad guard bytes in %zu..%zu, first bytes %02x %02x %02x %02x]",
+                     name, b.p, b.cap, nbad, first, last, h[first], h[first + 1 < GUARD ? first + 1 : first],
+                     h[first + 2 < GUARD ? first + 2 : first], h[first + 3 < GUARD ? first + 3 : first]);
+            bad += buf;
+        }
+    });
+    if (!bad.empty()) {
+        ctx->err = std::string("debug guard (") + where + ", rank " + std::to_string(ctx->rank) + "): " + bad;
+        fprintf(stderr, "%s\n", ctx->err.c_str());
+        return MPL_ERR_STATE;
+    }
+    return MPL_OK;
+}
+#else
+mpl_status debug_check_guards(mpl_ctx, const char *) { return MPL_OK; }
+#endif
 
 namespace {
 
@@ -50,18 +139,25 @@ extern "C" {
 const char *mpl_version(void) { return "mpmlite-b200 0.1 (sm_100a)"; }
 
 mpl_status mpl_create(const mpl_config *cfg, const mpl_grid *grid, mpl_ctx *out) {
+    ApiLock api_lock_;
     if (!cfg || !grid || !out) return MPL_ERR_INVALID_ARG;
     *out = nullptr;
     if (cfg->precision != 32 && cfg->precision != 64) return MPL_ERR_INVALID_ARG;
     for (int a = 0; a < 3; a++)
         if (grid->n[a] < 2 || grid->n[a] > 1022) return MPL_ERR_INVALID_ARG;
     if (!(grid->dx > 0)) return MPL_ERR_INVALID_ARG;
-    if (cfg->nranks != 1 && cfg->nranks != 0) return MPL_ERR_UNSUPPORTED;  // slab decomposition: see DESIGN.md §6
+    const int R = cfg->nranks > 0 ? cfg->nranks : 1;
+    const int NBX = (grid->n[0] + 3) / 4;  // cell blocks along x
+    if (R > 1 && (cfg->rank < 0 || cfg->rank >= R || R > NBX)) return MPL_ERR_INVALID_ARG;
     mpl_ctx ctx = new mpl_ctx_s();
     ctx->precision = cfg->precision;
     ctx->device = cfg->device;
-    ctx->rank = cfg->rank;
-    ctx->nranks = 1;
+    ctx->rank = R > 1 ? cfg->rank : 0;
+    ctx->nranks = R;
+    ctx->cuts.resize(R + 1);
+    for (int r = 0; r <= R; r++) ctx->cuts[r] = (int)((int64_t)r * NBX / R);
+    ctx->slab_lo = ctx->cuts[ctx->rank];
+    ctx->slab_hi = ctx->cuts[ctx->rank + 1];
     for (int a = 0; a < 3; a++) {
         ctx->grid.n[a] = grid->n[a];
         ctx->grid.nb[a] = grid->n[a] / 4 + 1;
@@ -87,24 +183,26 @@ mpl_status mpl_create(const mpl_config *cfg, const mpl_grid *grid, mpl_ctx *out)
         return MPL_ERR_OOM;
     }
     cudaMemset(ctx->scalars.p, 0, 4096);
+    if (R > 1) {
+        s = comm_create(ctx, cfg);  // NCCL init is collective over the ranks
+        if (s != MPL_OK) {
+            cudaFree(ctx->scalars.p);
+            if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+            delete ctx;
+            return s;
+        }
+    }
     *out = ctx;
     return MPL_OK;
 }
 
 void mpl_destroy(mpl_ctx ctx) {
+    ApiLock api_lock_;
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    DevBuf *all[] = {&ctx->px[0], &ctx->px[1], &ctx->pF[0], &ctx->pF[1], &ctx->pv, &ctx->pG, &ctx->pvol[0],
-                     &ctx->pvol[1], &ctx->pmat[0], &ctx->pmat[1], &ctx->pid[0], &ctx->pid[1], &ctx->pkey,
-                     &ctx->prank, &ctx->prec, &ctx->pbase, &ctx->pskey, &ctx->cflag, &ctx->nflag, &ctx->tile_of,
-                     &ctx->scan_tmp, &ctx->t_coord, &ctx->t_nplus, &ctx->t_nminus, &ctx->t_cstart, &ctx->t_ccount,
-                     &ctx->t_hascells, &ctx->t_bcount, &ctx->t_bstart, &ctx->t_cellof, &ctx->t_cmask, &ctx->c_local,
-                     &ctx->q_m, &ctx->q_mv, &ctx->q_mG, &ctx->q_slot, &ctx->q_vc, &ctx->q_Gc, &ctx->K, &ctx->n_mass,
-                     &ctx->n_flag, &ctx->n_vn, &ctx->n_vhat, &ctx->n_v, &ctx->n_vt, &ctx->n_g, &ctx->n_diag, &ctx->n_invD,
-                     &ctx->n_x, &ctx->n_r, &ctx->n_p, &ctx->n_Hp, &ctx->n_u, &ctx->n_u2, &ctx->n_act,
-                     &ctx->n_canon, &ctx->n_list, &ctx->scalars, &ctx->cg_slots, &ctx->io_stage, &ctx->io_stage2};
-    for (DevBuf *b : all) free_buf(*b);
+    for_each_buf(ctx, [](const char *, DevBuf &b) { free_buf(b); });
+    comm_destroy(ctx);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -112,6 +210,7 @@ void mpl_destroy(mpl_ctx ctx) {
 const char *mpl_last_error(mpl_ctx ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 mpl_status mpl_set_stream(mpl_ctx ctx, void *stream) {
+    ApiLock api_lock_;
     if (!ctx) return MPL_ERR_INVALID_ARG;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
@@ -126,12 +225,70 @@ mpl_status mpl_set_stream(mpl_ctx ctx, void *stream) {
     return MPL_OK;
 }
 
-mpl_status mpl_nccl_unique_id(uint8_t out[128]) {
-    (void)out;
-    return MPL_ERR_UNSUPPORTED;
+mpl_status mpl_set_slabs(mpl_ctx ctx, const int32_t *cuts) {
+    ApiLock api_lock_;
+    if (!ctx || !cuts) return MPL_ERR_INVALID_ARG;
+    const int R = ctx->nranks, NBX = (ctx->grid.n[0] + 3) / 4;
+    if (cuts[0] != 0 || cuts[R] != NBX) {
+        ctx->err = "slab cuts must start at 0 and end at ceil(n[0] / 4)";
+        return MPL_ERR_INVALID_ARG;
+    }
+    for (int r = 0; r < R; r++)
+        if (cuts[r + 1] <= cuts[r]) {
+            ctx->err = "slab cuts must be strictly increasing";
+            return MPL_ERR_INVALID_ARG;
+        }
+    for (int r = 0; r <= R; r++) ctx->cuts[r] = cuts[r];
+    ctx->slab_lo = cuts[ctx->rank];
+    ctx->slab_hi = cuts[ctx->rank + 1];
+    ctx->resampled = ctx->linearized = ctx->solved = false;
+    return MPL_OK;
+}
+
+mpl_status mpl_set_particle_ids(mpl_ctx ctx, const int32_t *ids) {
+    ApiLock api_lock_;
+    if (!ctx || (!ids && ctx->np)) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->have_particles, "mpl_set_particles before mpl_set_particle_ids"));
+    if (!multi(ctx)) {
+        ctx->err = "particle ids are for slab ranks (one rank exports in input order)";
+        return MPL_ERR_INVALID_ARG;
+    }
+    MPL_CHECK(set_device(ctx));
+    if (ctx->np) {
+        MPL_CUDA(cudaMemcpyAsync(ctx->pid[ctx->cur].p, ids, ctx->np * 4, cudaMemcpyDefault, ctx->stream));
+        MPL_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    return MPL_OK;
+}
+
+mpl_status mpl_get_particle_ids(mpl_ctx ctx, int32_t *ids) {
+    ApiLock api_lock_;
+    if (!ctx || !ids) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->have_particles, "mpl_set_particles first"));
+    MPL_CHECK(set_device(ctx));
+    if (!multi(ctx)) {
+        for (int64_t i = 0; i < ctx->np; i++) ids[i] = (int32_t)i;
+        return MPL_OK;
+    }
+    return DISPATCH(ctx, export_owned_particles, nullptr, nullptr, nullptr, nullptr, ids, nullptr);
+}
+
+mpl_status mpl_get_node_owner(mpl_ctx ctx, uint8_t *owned) {
+    ApiLock api_lock_;
+    if (!ctx || !owned) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
+    MPL_CHECK(set_device(ctx));
+    const int64_t n = ctx->n_nodes_active;
+    std::vector<int> list(n);
+    std::vector<uint8_t> own((size_t)ctx->T * 64);
+    MPL_CUDA(cudaMemcpy(list.data(), ctx->n_list.p, n * 4, cudaMemcpyDeviceToHost));
+    MPL_CUDA(cudaMemcpy(own.data(), ctx->n_own.p, own.size(), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; i++) owned[i] = own[list[i]];
+    return MPL_OK;
 }
 
 mpl_status mpl_set_materials(mpl_ctx ctx, int32_t n, const mpl_material *mats) {
+    ApiLock api_lock_;
     if (!ctx || !mats || n < 1 || n > MPL_MAXMAT) return MPL_ERR_INVALID_ARG;
     for (int k = 0; k < n; k++) {
         const mpl_material &m = mats[k];
@@ -154,12 +311,14 @@ mpl_status mpl_set_materials(mpl_ctx ctx, int32_t n, const mpl_material *mats) {
 }
 
 mpl_status mpl_set_gravity(mpl_ctx ctx, const double g[3]) {
+    ApiLock api_lock_;
     if (!ctx || !g) return MPL_ERR_INVALID_ARG;
     for (int a = 0; a < 3; a++) ctx->gravity[a] = g[a];
     return MPL_OK;
 }
 
 mpl_status mpl_set_dirichlet(mpl_ctx ctx, int32_t n, const mpl_dirichlet_box *boxes) {
+    ApiLock api_lock_;
     if (!ctx || n < 0 || n > MPL_MAXBOX || (n > 0 && !boxes)) return MPL_ERR_INVALID_ARG;
     ctx->boxes.nbox = n;
     for (int b = 0; b < n; b++)
@@ -173,6 +332,7 @@ mpl_status mpl_set_dirichlet(mpl_ctx ctx, int32_t n, const mpl_dirichlet_box *bo
 
 mpl_status mpl_set_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v, const void *F, const void *G,
                              const void *vol, const int32_t *mat, int32_t on_device) {
+    ApiLock api_lock_;
     (void)on_device;
     if (!ctx || n < 0 || (n > 0 && (!x || !v || !F || !G || !vol || !mat))) return MPL_ERR_INVALID_ARG;
     if (n > (int64_t)1 << 30) return MPL_ERR_INVALID_ARG;
@@ -186,6 +346,7 @@ mpl_status mpl_set_particles(mpl_ctx ctx, int64_t n, const void *x, const void *
 }
 
 mpl_status mpl_get_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G, int32_t on_device) {
+    ApiLock api_lock_;
     (void)on_device;
     if (!ctx) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->have_particles, "mpl_set_particles first"));
@@ -193,9 +354,13 @@ mpl_status mpl_get_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G, in
     return DISPATCH(ctx, export_particles, x, v, F, G);
 }
 
-int64_t mpl_num_particles(mpl_ctx ctx) { return ctx ? ctx->np : -1; }
+int64_t mpl_num_particles(mpl_ctx ctx) {
+    ApiLock api_lock_;
+    return ctx ? ctx->np_own : -1;
+}
 
 mpl_status mpl_resample(mpl_ctx ctx, double dt, int64_t *n_cells, int64_t *n_nodes, int64_t *n_blocks) {
+    ApiLock api_lock_;
     if (!ctx || !(dt > 0)) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->have_particles, "mpl_set_particles before mpl_resample"));
     MPL_CHECK(need(ctx, ctx->mats.nmat > 0, "mpl_set_materials before mpl_resample"));
@@ -210,6 +375,7 @@ mpl_status mpl_resample(mpl_ctx ctx, double dt, int64_t *n_cells, int64_t *n_nod
 }
 
 mpl_status mpl_get_nodes(mpl_ctx ctx, int32_t *ijk, void *m, void *v_n, uint8_t *free_dof) {
+    ApiLock api_lock_;
     if (!ctx) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
     MPL_CHECK(set_device(ctx));
@@ -247,10 +413,12 @@ mpl_status mpl_get_nodes(mpl_ctx ctx, int32_t *ijk, void *m, void *v_n, uint8_t 
 }
 
 mpl_status mpl_get_active_blocks(mpl_ctx ctx, int64_t *ids) {
+    ApiLock api_lock_;
     if (!ctx || !ids) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->resampled || ctx->T > 0, "mpl_resample first"));
     MPL_CHECK(set_device(ctx));
     const GridP &g = ctx->grid;
+    const int xlo = multi(ctx) ? ctx->slab_lo : 0, xhi = multi(ctx) ? ctx->slab_hi : (1 << 30);
     std::vector<int> flag(ctx->dense_n);
     MPL_CUDA(cudaMemcpy(flag.data(), ctx->cflag.p, flag.size() * 4, cudaMemcpyDeviceToHost));
     int64_t k = 0;
@@ -259,14 +427,17 @@ mpl_status mpl_get_active_blocks(mpl_ctx ctx, int64_t *ids) {
     for (int bx = 0; bx < g.nb[0]; bx++)
         for (int by = 0; by < g.nb[1]; by++)
             for (int bz = 0; bz < g.nb[2]; bz++)
-                if (flag[(bx * g.nb[1] + by) * g.nb[2] + bz]) ids[k++] = ((int64_t)bx * NB[1] + by) * NB[2] + bz;
+                if (flag[(bx * g.nb[1] + by) * g.nb[2] + bz] && bx >= xlo && bx < xhi)
+                    ids[k++] = ((int64_t)bx * NB[1] + by) * NB[2] + bz;
     return MPL_OK;
 }
 
 mpl_status mpl_get_particle_cells(mpl_ctx ctx, int32_t *base_ijk) {
+    ApiLock api_lock_;
     if (!ctx || !base_ijk) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->have_particles, "mpl_set_particles first"));
     MPL_CHECK(set_device(ctx));
+    if (multi(ctx)) return DISPATCH(ctx, export_owned_particles, nullptr, nullptr, nullptr, nullptr, nullptr, base_ijk);
     // recompute from the current positions (sorted) and unsort via ids
     const int64_t np = ctx->np;
     std::vector<int> id(np);
@@ -292,6 +463,7 @@ mpl_status mpl_get_particle_cells(mpl_ctx ctx, int32_t *base_ijk) {
 
 mpl_status mpl_get_quadrature(mpl_ctx ctx, int32_t *ijk, void *m_c, void *v_c, void *G_c, void *V_ck, void *tau_ck,
                               void *S_ck) {
+    ApiLock api_lock_;
     if (!ctx) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
     MPL_CHECK(set_device(ctx));
@@ -299,6 +471,7 @@ mpl_status mpl_get_quadrature(mpl_ctx ctx, int32_t *ijk, void *m_c, void *v_c, v
 }
 
 mpl_status mpl_energy(mpl_ctx ctx, const void *v, double *phi) {
+    ApiLock api_lock_;
     if (!ctx || !v || !phi) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
     MPL_CHECK(set_device(ctx));
@@ -307,6 +480,7 @@ mpl_status mpl_energy(mpl_ctx ctx, const void *v, double *phi) {
 }
 
 mpl_status mpl_gradient(mpl_ctx ctx, const void *v, void *g, double *phi) {
+    ApiLock api_lock_;
     if (!ctx || !v || !g) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
     MPL_CHECK(set_device(ctx));
@@ -318,6 +492,7 @@ mpl_status mpl_gradient(mpl_ctx ctx, const void *v, void *g, double *phi) {
 }
 
 mpl_status mpl_linearize(mpl_ctx ctx, const void *v) {
+    ApiLock api_lock_;
     if (!ctx || !v) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
     MPL_CHECK(set_device(ctx));
@@ -327,6 +502,7 @@ mpl_status mpl_linearize(mpl_ctx ctx, const void *v) {
 }
 
 mpl_status mpl_get_diag(mpl_ctx ctx, void *D) {
+    ApiLock api_lock_;
     if (!ctx || !D) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->linearized, "mpl_linearize first"));
     MPL_CHECK(set_device(ctx));
@@ -334,6 +510,7 @@ mpl_status mpl_get_diag(mpl_ctx ctx, void *D) {
 }
 
 mpl_status mpl_hvp(mpl_ctx ctx, const void *u, void *Hu) {
+    ApiLock api_lock_;
     if (!ctx || !u || !Hu) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->linearized, "mpl_linearize before mpl_hvp"));
     MPL_CHECK(set_device(ctx));
@@ -343,6 +520,7 @@ mpl_status mpl_hvp(mpl_ctx ctx, const void *u, void *Hu) {
 }
 
 mpl_status mpl_hvp_bench(mpl_ctx ctx, const void *u, void *Hu, int32_t reps, double *ms_per_hvp) {
+    ApiLock api_lock_;
     if (!ctx || !u || reps < 1) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->linearized, "mpl_linearize before mpl_hvp_bench"));
     MPL_CHECK(set_device(ctx));
@@ -364,6 +542,7 @@ mpl_status mpl_hvp_bench(mpl_ctx ctx, const void *u, void *Hu, int32_t reps, dou
 }
 
 mpl_status mpl_newton_step(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *stats) {
+    ApiLock api_lock_;
     if (!ctx || !cfg) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample before mpl_newton_step"));
     if (cfg->newton_max < 0 || cfg->cg_max < 0 || cfg->ls_max < 0) return MPL_ERR_INVALID_ARG;
@@ -381,6 +560,7 @@ mpl_status mpl_newton_step(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_sta
 }
 
 mpl_status mpl_get_velocity(mpl_ctx ctx, void *v) {
+    ApiLock api_lock_;
     if (!ctx || !v) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
     MPL_CHECK(set_device(ctx));
@@ -388,6 +568,7 @@ mpl_status mpl_get_velocity(mpl_ctx ctx, void *v) {
 }
 
 mpl_status mpl_set_velocity(mpl_ctx ctx, const void *v) {
+    ApiLock api_lock_;
     if (!ctx || !v) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first"));
     MPL_CHECK(set_device(ctx));
@@ -395,6 +576,7 @@ mpl_status mpl_set_velocity(mpl_ctx ctx, const void *v) {
 }
 
 mpl_status mpl_transfer_to_particles(mpl_ctx ctx, double dt) {
+    ApiLock api_lock_;
     if (!ctx || !(dt > 0)) return MPL_ERR_INVALID_ARG;
     MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample (and mpl_newton_step) before mpl_transfer_to_particles"));
     MPL_CHECK(set_device(ctx));
@@ -402,6 +584,7 @@ mpl_status mpl_transfer_to_particles(mpl_ctx ctx, double dt) {
 }
 
 mpl_status mpl_step(mpl_ctx ctx, double dt, const mpl_solver_cfg *cfg, mpl_solve_stats *stats) {
+    ApiLock api_lock_;
     if (!ctx || !cfg) return MPL_ERR_INVALID_ARG;
     cudaEvent_t e[4];
     for (auto &x : e) cudaEventCreate(&x);

@@ -18,6 +18,28 @@
 #include "../../include/mpmlite.h"
 
 #define MPL_MAXMAT 8
+
+// Debug build (MPL_DEBUG=1 python -m paper_2602_07853_b200.build): device-side bounds checks that
+// print the failing condition and trap (a stand-in for compute-sanitizer, which this pool closes).
+#ifdef MPL_DEBUG
+#include <cstdio>
+#define DASSERT(c)                                                                                          \
+    do {                                                                                                    \
+        if (!(c)) {                                                                                         \
+            printf("MPL_DEBUG assert failed: %s at %s:%d (block %d thread %d)\n", #c, __FILE__, __LINE__,   \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                      \
+            __trap();                                                                                       \
+        }                                                                                                   \
+    } while (0)
+#define MPL_DEBUG_PRINT(ctx) fprintf(stderr, "[rank %d] %s\n", (ctx)->rank, (ctx)->err.c_str())
+#else
+#define MPL_DEBUG_PRINT(ctx) \
+    do {                     \
+    } while (0)
+#define DASSERT(c) \
+    do {           \
+    } while (0)
+#endif
 #define MPL_MAXBOX 8
 #define MPL_LOG_NEWTON 64
 
@@ -236,9 +258,9 @@ struct CGSlot {
 // device-side scalar block (fp64 accumulators and flags)
 struct DevScalars {
     double energy[NSTRIPE];  // Phi accumulator (striped)
+    double inv_any;          // 1.0 if det(I + dt G) <= 0 was seen (reduced with energy; amb-21)
     double gnorm2[NSTRIPE];  // ||g_free||^2
     double gp[NSTRIPE];      // g . p
-    int inverted;      // det(I + dt G) <= 0 seen
     int nonfinite;
     int oob_particle;  // min index of an out-of-domain particle (INT_MAX = none)
     int inv_particle;  // min index of an inverted particle
@@ -247,8 +269,32 @@ struct DevScalars {
     int pad[2];
 };
 
+// Communicator between the slab ranks.  Every method is collective over the ranks and
+// stream-ordered on ctx->stream; implementations: NCCL (one process per GPU, mpl_comm.cu) and an
+// in-process loopback group (ranks as host threads of one process, for single-GPU testing).
+struct Comm {
+    int rank = 0, nranks = 1;
+    virtual ~Comm() {}
+    // in-place sum of n doubles (device memory) over all ranks; every rank gets the same values
+    virtual mpl_status allreduce(mpl_ctx ctx, double *dev, int64_t n) = 0;
+    // neighbour exchange: send_lo -> rank-1 (arrives in its recv_hi), send_hi -> rank+1 (its recv_lo).
+    // Byte counts must match pairwise; a missing neighbour's arguments are ignored.
+    virtual mpl_status neighbors(mpl_ctx ctx, const void *send_lo, size_t n_send_lo, void *recv_lo, size_t n_recv_lo,
+                                 const void *send_hi, size_t n_send_hi, void *recv_hi, size_t n_recv_hi) = 0;
+};
+
 struct mpl_ctx_s {
     int precision = 32, device = 0, rank = 0, nranks = 1;
+    Comm *comm = nullptr;                  // nranks > 1
+    int slab_lo = 0, slab_hi = 1 << 30;    // owned cell-block x range [slab_lo, slab_hi) (4-cell blocks)
+    std::vector<int> cuts;                 // nranks + 1 slab boundaries (cell blocks)
+    int64_t np_own = 0;                    // owned particles (the rest of np are ghosts, pid < 0)
+    DevBuf pv_alt, pG_alt;                 // redistribution targets for v, G
+    DevBuf mig_send_lo, mig_send_hi, mig_recv_lo, mig_recv_hi, mig_cnt;
+    DevBuf pl_send_lo, pl_send_hi, pl_recv_lo, pl_recv_hi;  // dense node-plane halo buffers
+    DevBuf t_lo_list, t_hi_list;           // tiles on the lower / upper interface node-block planes
+    int n_lo_tiles = 0, n_hi_tiles = 0;
+    DevBuf n_own, n_mown;                  // per node: owner flag (uint8), owned mass (m if owner else 0)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     std::string err;
@@ -294,21 +340,115 @@ struct mpl_ctx_s {
 // ------------------------------------------------------------------------------------------
 #define MPL_CUDA(call)                                                                  \
     do {                                                                                \
-        cudaError_t e_ = (call);                                                        \
-        if (e_ != cudaSuccess) {                                                        \
-            ctx->err = std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " +  \
+        const cudaError_t mpl_cuda_err_ = (call);                                       \
+        if (mpl_cuda_err_ != cudaSuccess) {                                             \
+            ctx->err = std::string("CUDA error: ") + cudaGetErrorString(mpl_cuda_err_) + \
+                       " at " +                                                         \
                        __FILE__ + ":" + std::to_string(__LINE__);                       \
+            MPL_DEBUG_PRINT(ctx);                                                       \
             return MPL_ERR_CUDA;                                                        \
         }                                                                               \
     } while (0)
 
-#define MPL_CHECK(st)                \
-    do {                             \
-        mpl_status s_ = (st);        \
-        if (s_ != MPL_OK) return s_; \
+#define MPL_CHECK(st)                                      \
+    do {                                                   \
+        const mpl_status mpl_check_st_ = (st);             \
+        if (mpl_check_st_ != MPL_OK) return mpl_check_st_; \
     } while (0)
 
 mpl_status ensure(mpl_ctx ctx, DevBuf &b, size_t bytes);
+// every device buffer of a context with its name (destroy, debug guard checks)
+template <class F> void for_each_buf(mpl_ctx ctx, F f) {
+    struct NB { const char *name; DevBuf &b; };
+    NB all[] = {
+        {"px[0]", ctx->px[0]},
+        {"px[1]", ctx->px[1]},
+        {"pF[0]", ctx->pF[0]},
+        {"pF[1]", ctx->pF[1]},
+        {"pv", ctx->pv},
+        {"pG", ctx->pG},
+        {"pvol[0]", ctx->pvol[0]},
+        {"pvol[1]", ctx->pvol[1]},
+        {"pmat[0]", ctx->pmat[0]},
+        {"pmat[1]", ctx->pmat[1]},
+        {"pid[0]", ctx->pid[0]},
+        {"pid[1]", ctx->pid[1]},
+        {"pkey", ctx->pkey},
+        {"prank", ctx->prank},
+        {"prec", ctx->prec},
+        {"pbase", ctx->pbase},
+        {"pskey", ctx->pskey},
+        {"cflag", ctx->cflag},
+        {"nflag", ctx->nflag},
+        {"tile_of", ctx->tile_of},
+        {"scan_tmp", ctx->scan_tmp},
+        {"t_coord", ctx->t_coord},
+        {"t_nplus", ctx->t_nplus},
+        {"t_nminus", ctx->t_nminus},
+        {"t_cstart", ctx->t_cstart},
+        {"t_ccount", ctx->t_ccount},
+        {"t_hascells", ctx->t_hascells},
+        {"t_bcount", ctx->t_bcount},
+        {"t_bstart", ctx->t_bstart},
+        {"t_cellof", ctx->t_cellof},
+        {"t_cmask", ctx->t_cmask},
+        {"c_local", ctx->c_local},
+        {"q_m", ctx->q_m},
+        {"q_mv", ctx->q_mv},
+        {"q_mG", ctx->q_mG},
+        {"q_slot", ctx->q_slot},
+        {"q_vc", ctx->q_vc},
+        {"q_Gc", ctx->q_Gc},
+        {"K", ctx->K},
+        {"n_mass", ctx->n_mass},
+        {"n_flag", ctx->n_flag},
+        {"n_vn", ctx->n_vn},
+        {"n_vhat", ctx->n_vhat},
+        {"n_v", ctx->n_v},
+        {"n_vt", ctx->n_vt},
+        {"n_g", ctx->n_g},
+        {"n_diag", ctx->n_diag},
+        {"n_invD", ctx->n_invD},
+        {"n_x", ctx->n_x},
+        {"n_r", ctx->n_r},
+        {"n_p", ctx->n_p},
+        {"n_Hp", ctx->n_Hp},
+        {"n_u", ctx->n_u},
+        {"n_u2", ctx->n_u2},
+        {"n_act", ctx->n_act},
+        {"n_canon", ctx->n_canon},
+        {"n_list", ctx->n_list},
+        {"scalars", ctx->scalars},
+        {"cg_slots", ctx->cg_slots},
+        {"io_stage", ctx->io_stage},
+        {"io_stage2", ctx->io_stage2},
+        {"pv_alt", ctx->pv_alt},
+        {"pG_alt", ctx->pG_alt},
+        {"mig_send_lo", ctx->mig_send_lo},
+        {"mig_send_hi", ctx->mig_send_hi},
+        {"mig_recv_lo", ctx->mig_recv_lo},
+        {"mig_recv_hi", ctx->mig_recv_hi},
+        {"mig_cnt", ctx->mig_cnt},
+        {"pl_send_lo", ctx->pl_send_lo},
+        {"pl_send_hi", ctx->pl_send_hi},
+        {"pl_recv_lo", ctx->pl_recv_lo},
+        {"pl_recv_hi", ctx->pl_recv_hi},
+        {"t_lo_list", ctx->t_lo_list},
+        {"t_hi_list", ctx->t_hi_list},
+        {"n_own", ctx->n_own},
+        {"n_mown", ctx->n_mown}
+    };
+    for (NB &x : all) f(x.name, x.b);
+}
+mpl_status debug_check_guards(mpl_ctx ctx, const char *where);
+#ifdef MPL_DEBUG
+#define DBG_GUARDS(where) MPL_CHECK(debug_check_guards(ctx, where))
+#else
+#define DBG_GUARDS(where) \
+    do {                  \
+    } while (0)
+#endif
+
 
 // kernels' host launchers (defined in k_*.cu), templated on the compute precision
 template <class T> mpl_status resample_impl(mpl_ctx ctx, double dt);
@@ -323,6 +463,31 @@ template <class T> mpl_status tile_to_canon(mpl_ctx ctx, const void *src_tile, v
 template <class T> mpl_status export_quadrature(mpl_ctx ctx, int32_t *ijk, void *m_c, void *v_c, void *G_c,
                                                 void *V_ck, void *tau_ck, void *S_ck);
 template <class T> mpl_status export_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G);
+// multi-rank plumbing (mpl_comm.cu)
+template <class T> mpl_status redistribute_particles(mpl_ctx ctx);
+template <class T> mpl_status halo_sum_nodes(mpl_ctx ctx, void *a_tile, void *b_tile);
+template <class T> mpl_status ghost_nodes_from_upper(mpl_ctx ctx, void *v_tile);
+template <class T> mpl_status c2n_halo(mpl_ctx ctx);
+template <class T> mpl_status export_owned_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G, int32_t *ids,
+                                                     int32_t *base_ijk);
+mpl_status build_interface_lists(mpl_ctx ctx);
+mpl_status debug_check_tiles(mpl_ctx ctx, const char *where);
+mpl_status allreduce_d(mpl_ctx ctx, double *dev, int64_t n);
+mpl_status agree(mpl_ctx ctx, mpl_status local);
+inline bool multi(mpl_ctx ctx) { return ctx->nranks > 1; }
+bool serial_mode();
+struct ApiLock {  // MPL_LOOPBACK_SERIAL debugging aid (mpl_api.cu)
+    bool on;
+    ApiLock();
+    ~ApiLock();
+};
+int api_lock_release_all();
+void api_lock_reacquire(int depth);
+// lumped mass counted by this rank (m_i on owned nodes, 0 on the copies of shared nodes)
+inline const void *owned_mass(mpl_ctx ctx) { return multi(ctx) ? ctx->n_mown.p : ctx->n_mass.p; }
+mpl_status comm_create(mpl_ctx ctx, const mpl_config *cfg);
+void comm_destroy(mpl_ctx ctx);
+
 template <class T> mpl_status import_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v, const void *F,
                                                const void *G, const void *vol, const int32_t *mat);
 

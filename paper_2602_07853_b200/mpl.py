@@ -15,7 +15,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpmlite.so")
+# MPL_LIB=dbg loads the bounds-checked debug build (MPL_DEBUG=1 python -m paper_2602_07853_b200.build)
+LIB_PATH = os.path.join(_HERE, "libmpmlite_dbg.so" if os.environ.get("MPL_LIB") == "dbg" else "libmpmlite.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2602_07853_b200.build` "
@@ -44,7 +45,7 @@ class Material(C.Structure):
 
 class Config(C.Structure):
     _fields_ = [("precision", C.c_int32), ("device", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32),
-                ("nccl_unique_id", C.c_void_p)]
+                ("nccl_unique_id", C.c_void_p), ("loopback", C.c_void_p)]
 
 
 class DirichletBox(C.Structure):
@@ -89,6 +90,13 @@ _SIGS = {
     "mpl_set_stream": [_vp, _vp],
     "mpl_version": [],
     "mpl_nccl_unique_id": [_vp],
+    "mpl_group_create": [_i32, _vp],
+    "mpl_group_destroy": [_vp],
+    "mpl_set_slabs": [_vp, _vp],
+    "mpl_balance_slabs": [_i32, _vp, _i32, _vp],
+    "mpl_set_particle_ids": [_vp, _vp],
+    "mpl_get_particle_ids": [_vp, _vp],
+    "mpl_get_node_owner": [_vp, _vp],
     "mpl_set_materials": [_vp, _i32, _vp],
     "mpl_set_gravity": [_vp, _vp],
     "mpl_set_dirichlet": [_vp, _i32, _vp],
@@ -120,10 +128,53 @@ _lib.mpl_last_error.restype = C.c_char_p
 _lib.mpl_version.restype = C.c_char_p
 _lib.mpl_num_particles.restype = C.c_int64
 _lib.mpl_destroy.restype = None
+_lib.mpl_group_destroy.restype = None
 
 
 def version() -> str:
     return _lib.mpl_version().decode()
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0; broadcast it to the other ranks before creating contexts)."""
+    buf = (C.c_uint8 * 128)()
+    st = _lib.mpl_nccl_unique_id(buf)
+    if st != 0:
+        raise MplError(st, "mpl_nccl_unique_id failed (is libnccl.so.2 loadable?)")
+    return bytes(buf)
+
+
+def balance_slabs(weight, nranks: int) -> np.ndarray:
+    """Slab cuts (nranks + 1 cell-block x indices) balancing a per-plane weight (host-only call)."""
+    w = np.ascontiguousarray(weight, dtype=np.int64)
+    cuts = np.zeros(nranks + 1, np.int32)
+    st = _lib.mpl_balance_slabs(int(w.size), w.ctypes.data, int(nranks), cuts.ctypes.data)
+    if st != 0:
+        raise MplError(st, "mpl_balance_slabs")
+    return cuts
+
+
+class Group:
+    """In-process loopback group: ranks are host threads of this process (tests on one GPU)."""
+
+    def __init__(self, nranks: int):
+        h = C.c_void_p()
+        st = _lib.mpl_group_create(int(nranks), C.byref(h))
+        if st != 0:
+            raise MplError(st, "mpl_group_create")
+        self._h = h
+        self.nranks = nranks
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.mpl_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def _ptr(a) -> Optional[int]:
@@ -150,8 +201,13 @@ class Context:
     """One simulation context on one GPU (C ABI mpl_ctx)."""
 
     def __init__(self, n: Sequence[int], dx: float, precision: int = 32, device: int = 0,
-                 origin: Sequence[float] = (0.0, 0.0, 0.0)):
-        cfg = Config(precision=precision, device=device, rank=0, nranks=1, nccl_unique_id=None)
+                 origin: Sequence[float] = (0.0, 0.0, 0.0), rank: int = 0, nranks: int = 1,
+                 nccl_id: Optional[bytes] = None, group: Optional[Group] = None):
+        self._idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
+        cfg = Config(precision=precision, device=device, rank=rank, nranks=nranks,
+                     nccl_unique_id=C.cast(self._idbuf, C.c_void_p) if self._idbuf is not None else None,
+                     loopback=group._h if group is not None else None)
+        self.rank, self.nranks = rank, nranks
         g = Grid()
         for a in range(3):
             g.n[a] = int(n[a])
@@ -161,6 +217,7 @@ class Context:
         st = _lib.mpl_create(C.byref(cfg), C.byref(g), C.byref(h))
         if st != 0:
             raise MplError(st, "mpl_create failed")
+        self.n = tuple(int(a) for a in n)
         self._h = h
         self.precision = precision
         self.dtype = np.float32 if precision == 32 else np.float64
@@ -235,6 +292,27 @@ class Context:
         self._keep = None
         self.np = n
 
+    def set_slabs(self, cuts):
+        c = np.ascontiguousarray(cuts, dtype=np.int32)
+        self._chk(_lib.mpl_set_slabs(self._h, c.ctypes.data), "mpl_set_slabs")
+
+    def set_particle_ids(self, ids):
+        a = np.ascontiguousarray(ids, dtype=np.int32)
+        self._chk(_lib.mpl_set_particle_ids(self._h, a.ctypes.data), "mpl_set_particle_ids")
+
+    def num_particles(self) -> int:
+        return int(_lib.mpl_num_particles(self._h))
+
+    def get_particle_ids(self) -> np.ndarray:
+        ids = np.zeros(self.num_particles(), np.int32)
+        self._chk(_lib.mpl_get_particle_ids(self._h, _ptr(ids)), "mpl_get_particle_ids")
+        return ids
+
+    def get_node_owner(self) -> np.ndarray:
+        o = np.zeros(self.counts.n_nodes, np.uint8)
+        self._chk(_lib.mpl_get_node_owner(self._h, _ptr(o)), "mpl_get_node_owner")
+        return o
+
     def get_particles(self, x=None, v=None, F=None, G=None):
         n = _lib.mpl_num_particles(self._h)
         x = self._out((n, 3), x)
@@ -266,7 +344,7 @@ class Context:
         return ids
 
     def get_particle_cells(self) -> np.ndarray:
-        b = np.zeros((self.np, 3), np.int32)
+        b = np.zeros((self.num_particles(), 3), np.int32)
         self._chk(_lib.mpl_get_particle_cells(self._h, _ptr(b)), "mpl_get_particle_cells")
         return b
 
@@ -366,4 +444,31 @@ def from_scene(scene, device: int = 0, precision: Optional[int] = None) -> Conte
     ctx.set_gravity(scene.gravity)
     ctx.set_dirichlet(scene.dirichlet)
     ctx.set_particles(scene.x, scene.v, scene.F, scene.G, scene.vol, scene.mat)
+    return ctx
+
+
+def slab_cuts(scene, nranks: int) -> np.ndarray:
+    """Cuts balancing the scene's particles over nranks x-slabs of 4-cell blocks."""
+    from .dist import plane_weights
+    return balance_slabs(plane_weights(scene.x[:, 0], scene.n[0], scene.dx, scene.origin[0]), nranks)
+
+
+def slab_select(scene, cuts, rank: int) -> np.ndarray:
+    """Indices of the particles rank owns: base cell x-block in [cuts[rank], cuts[rank+1])."""
+    bx = np.floor((np.asarray(scene.x[:, 0], np.float64) - scene.origin[0]) / scene.dx - 0.5).astype(np.int64) // 4
+    return np.nonzero((bx >= cuts[rank]) & (bx < cuts[rank + 1]))[0]
+
+
+def from_scene_rank(scene, rank: int, nranks: int, cuts, device: int = 0, precision: Optional[int] = None,
+                    nccl_id: Optional[bytes] = None, group: Optional[Group] = None) -> Context:
+    """Slab rank `rank` of `nranks`: its owned particles (global ids = scene indices)."""
+    ctx = Context(scene.n, scene.dx, precision or scene.precision, device, scene.origin, rank=rank, nranks=nranks,
+                  nccl_id=nccl_id, group=group)
+    ctx.set_slabs(cuts)
+    ctx.set_materials(scene.materials)
+    ctx.set_gravity(scene.gravity)
+    ctx.set_dirichlet(scene.dirichlet)
+    sel = slab_select(scene, cuts, rank)
+    ctx.set_particles(scene.x[sel], scene.v[sel], scene.F[sel], scene.G[sel], scene.vol[sel], scene.mat[sel])
+    ctx.set_particle_ids(sel.astype(np.int32))
     return ctx

@@ -348,3 +348,18 @@ def subset(scene: Scene, keep: np.ndarray, name: Optional[str] = None) -> Scene:
     """Scene restricted to particles `keep` (bool mask or index array) — used for windows."""
     return dataclasses.replace(scene, name=name or scene.name, x=scene.x[keep], v=scene.v[keep],
                                F=scene.F[keep], G=scene.G[keep], vol=scene.vol[keep], mat=scene.mat[keep])
+
+
+def key_noise(keys: np.ndarray, seed: int, dims: int = 3) -> np.ndarray:
+    """Standard-normal numbers indexed by an integer key (e.g. a global node id), so a full-size
+    run and an oracle window draw identical probe values for the same node (splitmix64 + Box-Muller)."""
+    with np.errstate(over="ignore"):
+        k = np.asarray(keys, dtype=np.uint64).reshape(-1, 1) * np.uint64(2 * dims) + np.arange(
+            2 * dims, dtype=np.uint64)[None, :] + np.uint64(seed) * np.uint64(0x9E3779B97F4A7C15)
+        z = k + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    u = ((z >> np.uint64(11)).astype(np.float64) + 0.5) * (1.0 / 9007199254740992.0)
+    u1, u2 = u[:, :dims], u[:, dims:]
+    return np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)

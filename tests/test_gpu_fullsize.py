@@ -1,0 +1,157 @@
+"""Parity at BASELINE.json's full sizes, in the configuration bench.py times (one GPU, fp32, the
+default HVP kernel): the CUDA path runs the whole scene; the fp64 oracle recomputes sampled outputs
+on windows of it (20^3 cells plus the particles whose stencil reaches in).  Outputs at nodes / cells /
+particles whose whole support lies inside a window equal the full-scene values, so they are compared
+element by element:
+  * a0 bit-exact: every particle's base cell and the full sorted active-block list (numpy, all particles);
+  * a2-a4 on the window's complete cells (m_c, v_c, G_c, V_ck, S_ck) and a3 on its complete nodes;
+  * a5 gradient and a6 HVP + Jacobi diagonal at a probe v = v^0 + 0.01 n(key), direction u = n(key)
+    (key-indexed normal draws, so window and full run use identical probes);
+  * a9 G2P of the window's particles from the GPU's own v^{n+1} after one adaptive implicit step.
+Bars: the fp32 ones of BASELINE.json (1e-5 on unload / gradient / HVP; 1e-4 on the step)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2602_07853_b200 import mpl, scenes
+
+from ._parity import node_ids, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+SIZE = 20
+# windows (lower cell corner) inside material / across interfaces for each full-size config
+WINDOWS = {
+    "cfg2": [(22, 22, 22), (44, 10, 30)],
+    "cfg3": [(54, 54, 54), (100, 60, 2)],
+    "cfg4": [(54, 80, 118), (180, 80, 118), (118, 2, 118)],  # left sphere, right sphere, slab + floor
+}
+
+
+class Full:
+    def __init__(self, name):
+        self.name = name
+        self.sc = sc = scenes.by_name(name, 32)
+        self.ctx = ctx = mpl.from_scene(sc, 0)
+        self.counts = ctx.resample(sc.dt)
+        self.ijk, self.m, self.vn, self.free = ctx.get_nodes()
+        self.q = ctx.get_quadrature()
+        self.base = ctx.get_particle_cells()
+        self.blocks = ctx.get_active_blocks()
+        n1, n2 = sc.n[1] + 1, sc.n[2] + 1
+        self.key = (self.ijk[:, 0].astype(np.int64) * n1 + self.ijk[:, 1]) * n2 + self.ijk[:, 2]
+        self.v0 = ctx.get_velocity().astype(np.float64)
+        self.vp = (self.v0 + 0.01 * scenes.key_noise(self.key, 5)).astype(np.float32).astype(np.float64)
+        self.u = scenes.key_noise(self.key, 4).astype(np.float32).astype(np.float64)
+        self.g, self.phi = ctx.gradient(self.vp)
+        ctx.linearize(self.vp)
+        self.h = ctx.hvp(self.u)
+        self.D = ctx.get_diag()
+        ctx.set_velocity(self.v0)
+        self.st = ctx.newton_step(sc.solver)
+        self.vnew = ctx.get_velocity().astype(np.float64)
+        ctx.transfer_to_particles(sc.dt)
+        self.parts = ctx.get_particles()
+        ctx.close()
+        self.pos = {int(k): i for i, k in enumerate(self.key)}
+
+
+@pytest.fixture(scope="module", params=list(WINDOWS))
+def full(request):
+    return Full(request.param)
+
+
+def _window(full, lo):
+    """Oracle on the window; returns it with the global<->window node maps of its complete nodes."""
+    sc = full.sc
+    lo = np.asarray(lo)
+    x = sc.x.astype(np.float64)
+    cell = np.floor(x / sc.dx - 0.5).astype(np.int64)
+    keep = np.nonzero(np.all((cell >= lo - 1) & (cell <= lo + SIZE), axis=1))[0]
+    sub = scenes.subset(sc, keep)
+    grid = oracle.Grid((SIZE + 2,) * 3, sc.dx, tuple((lo - 1) * sc.dx))
+    un, S, prob, v0 = oracle.prepare(sub, grid, clip=True)
+    wijk = grid.node_ijk()
+    gijk = wijk + (lo - 1)[None, :]
+    n1, n2 = sc.n[1] + 1, sc.n[2] + 1
+    gkey = (gijk[:, 0] * n1 + gijk[:, 1]) * n2 + gijk[:, 2]
+    gpos = np.array([full.pos.get(int(k), -1) for k in gkey])
+    complete = np.all((wijk >= 2) & (wijk <= SIZE + 1), axis=1)
+    return dict(lo=lo, keep=keep, sub=sub, grid=grid, un=un, S=S, prob=prob, gpos=gpos, complete=complete, gkey=gkey)
+
+
+def test_indices_bit_exact_full_scene(full):
+    sc = full.sc
+    grid = oracle.Grid(sc.n, sc.dx, sc.origin)
+    base = oracle.base_cells(grid, sc.x)
+    assert np.array_equal(full.base, base)
+    assert np.array_equal(full.blocks, oracle.active_blocks(grid, base))
+
+
+def test_windows_unload_gradient_hvp(full):
+    for lo in WINDOWS[full.name]:
+        w = _window(full, lo)
+        un, prob, gpos, cm = w["un"], w["prob"], w["gpos"], w["complete"]
+        act = cm & (un.m_i > 0)
+        assert act.sum() > 100, f"window {lo} holds too little material"
+        assert np.all(gpos[act] >= 0), "a node active in the oracle window is missing on the GPU"
+        # nodes the GPU holds inside the window's complete region must be active in the oracle too
+        assert np.all((un.m_i[cm & (gpos >= 0)]) > 0)
+        sel = gpos[act]
+        assert rel_l2(full.m[sel], un.m_i[act]) <= 1e-5
+        assert rel_l2(full.vn[sel], un.v_i[act]) <= 1e-5
+        assert np.array_equal(full.free[sel].astype(bool), prob.freed[act] != 0)
+        # probes at every window node the GPU holds (zero elsewhere: massless there)
+        have = gpos >= 0
+        v = np.zeros((w["grid"].nnodes, 3))
+        u = np.zeros_like(v)
+        v[have] = full.vp[gpos[have]]
+        u[have] = full.u[gpos[have]]
+        assert rel_l2(full.g[sel], prob.gradient(v)[act]) <= 1e-5
+        assert rel_l2(full.h[sel], prob.hvp(v, u)[act]) <= 1e-5
+        assert rel_l2(full.D[sel], prob.diag(v)[act]) <= 1e-5
+
+
+def test_windows_quadrature(full):
+    sc = full.sc
+    q = full.q
+    n1, n2 = sc.n[1], sc.n[2]
+    ckey = (q["ijk"][:, 0].astype(np.int64) * n1 + q["ijk"][:, 1]) * n2 + q["ijk"][:, 2]
+    cpos = {int(k): i for i, k in enumerate(ckey)}
+    for lo in WINDOWS[full.name]:
+        w = _window(full, lo)
+        un, grid = w["un"], w["grid"]
+        cijk = grid.cell_ijk()
+        comp = np.all((cijk >= 1) & (cijk <= SIZE), axis=1) & (un.m_c > 0)
+        g = cijk[comp] + (np.asarray(lo) - 1)[None, :]
+        sel = np.array([cpos[int(k)] for k in (g[:, 0] * n1 + g[:, 1]) * n2 + g[:, 2]])
+        assert rel_l2(q["m_c"][sel], un.m_c[comp]) <= 1e-5
+        assert rel_l2(q["v_c"][sel], un.v_c[comp]) <= 1e-5
+        for k in range(len(sc.materials)):
+            assert rel_l2(q["V_ck"][k][sel], un.V_ck[k][comp]) <= 1e-5
+            has = un.V_ck[k][comp] > 0
+            if has.any():
+                assert rel_l2(q["S_ck"][k][sel][has], w["S"][k][comp][has]) <= 1e-5
+
+
+def test_step_converges_and_g2p_windows(full):
+    """One adaptive implicit step (the bench's solve) converges; G2P of window particles from the GPU's
+    v^{n+1} matches the oracle's Load (Alg. 4)."""
+    assert full.st["converged"] == 1
+    sc = full.sc
+    x_g, v_g, F_g, G_g = full.parts
+    for lo in WINDOWS[full.name]:
+        w = _window(full, lo)
+        lo_ = np.asarray(lo)
+        sub = w["sub"]
+        base = np.floor(sub.x.astype(np.float64) / sc.dx - 0.5).astype(np.int64)
+        inner = np.all((base >= lo_ + 1) & (base <= lo_ + SIZE - 2), axis=1)  # whole support inside
+        vnew = np.zeros((w["grid"].nnodes, 3))
+        have = w["gpos"] >= 0
+        vnew[have] = full.vnew[w["gpos"][have]]
+        x_o, v_o, F_o, G_o = oracle.g2p(w["grid"], sc.dt, w["un"].m_c, vnew, sub.x, sub.v, sub.F, sub.G, clip=True)
+        idx = w["keep"][inner]
+        assert rel_l2(x_g[idx], x_o[inner]) <= 1e-6
+        assert rel_l2(v_g[idx], v_o[inner]) <= 1e-4
+        assert rel_l2(F_g[idx], F_o[inner]) <= 1e-4
+        assert rel_l2(G_g[idx], G_o[inner]) <= 1e-4

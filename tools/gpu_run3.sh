@@ -1,0 +1,9 @@
+set -u
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+for v in reg pipe2 pipe3; do MPL_HVP_KERNEL=$v timeout 300 python tools/prof_hvp.py --config cfg4 --reps 20 >> gpurun_out/variants.log 2>&1; echo "$v rc=$?" >> gpurun_out/variants.log; done
+MPL_HVP_KERNEL=pipe2 timeout 300 python tools/prof_hvp.py --config cfg4 --precision 64 --reps 10 >> gpurun_out/variants.log 2>&1
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+MPL_HVP_KERNEL=pipe3 timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_pipe3.json 2>> gpurun_out/bench.err
+echo done

@@ -118,12 +118,13 @@ __global__ void __launch_bounds__(64) k_hvp_reg(const int *__restrict__ nplus, c
     constexpr int VEC = KL<T>::VEC, NCH = KL<T>::NCH;
     T k[45];
     int l = 0xFF;
-    if (has && tid < ncp) {  // tiles outside the slab (ghost planes) carry no tangent
-        l = clocal[cs + tid];
+    const int cj = hvp_cell(tid), ks = hvp_slot(tid, ncp);
+    if (has && cj < ncp) {  // tiles outside the slab (ghost planes) carry no tangent
+        l = clocal[cs + cj];
         const T *base = K + (int64_t)cs * 45;
 #pragma unroll
-        for (int c = 0; c < NCH; c++) ldg_vec<T>(base + ((int64_t)c * ncp + tid) * VEC, k + c * VEC);
-        k[44] = __ldg(base + (int64_t)NCH * VEC * ncp + tid);
+        for (int c = 0; c < NCH; c++) ldg_vec<T>(base + ((int64_t)c * ncp + ks) * VEC, k + c * VEC);
+        k[44] = __ldg(base + (int64_t)NCH * VEC * ncp + ks);
     }
     for (int h = tid; h < 125; h += 64) {
         int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
@@ -338,15 +339,16 @@ __global__ void __launch_bounds__(64) k_hvp_pipe(int T_, const int *__restrict__
         const int ncp = S.meta[mc][1] - S.meta[mc][0], has = S.meta[mc][2];
         const vec4<T> *uh = S.uh[st];
         // ---- cell phase: P = K dG, corner forces added to F with shared-memory atomics ---------
-        const int l = (has && tid < ncp) ? (int)S.cl[st][tid] : 0xFF;
+        const int cj = hvp_cell(tid), ks = hvp_slot(tid, ncp);
+        const int l = (has && cj < ncp) ? (int)S.cl[st][cj] : 0xFF;
         if (l != 0xFF) {
             const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
             constexpr int VEC = KL<T>::VEC, NCH = KL<T>::NCH;
             const T *Ks = S.K[st];
             T k[45];
 #pragma unroll
-            for (int c = 0; c < NCH; c++) lds_vec<T>(Ks + (c * ncp + tid) * VEC, k + c * VEC);
-            k[44] = Ks[NCH * VEC * ncp + tid];
+            for (int c = 0; c < NCH; c++) lds_vec<T>(Ks + (c * ncp + ks) * VEC, k + c * VEC);
+            k[44] = Ks[NCH * VEC * ncp + ks];
             T dG[9];
 #pragma unroll
             for (int a = 0; a < 9; a++) dG[a] = T(0);
@@ -460,8 +462,8 @@ template <class T> struct RpSmem {
     double red[2];
 };
 
-template <class T>
-__global__ void __launch_bounds__(64) k_hvp_rp(int T_, const int *__restrict__ nplus, const int *__restrict__ cstart,
+template <class T, int MINB>
+__global__ void __launch_bounds__(64, MINB) k_hvp_rp(int T_, const int *__restrict__ nplus, const int *__restrict__ cstart,
                                                const uint8_t *__restrict__ clocal, const int *__restrict__ hascells,
                                                const T *__restrict__ K, const T *__restrict__ nmass,
                                                const vec4<T> *__restrict__ u, vec4<T> *__restrict__ Hu,
@@ -509,11 +511,12 @@ __global__ void __launch_bounds__(64) k_hvp_rp(int T_, const int *__restrict__ n
     auto issue = [&](int t, int b, int m) {
         if (t < T_) {
             const int cs = S.meta[m][0], ncp = S.meta[m][1] - cs, has = S.meta[m][2];
-            if (has && tid < ncp) {
+            const int cj = hvp_cell(tid), ks = hvp_slot(tid, ncp);
+            if (has && cj < ncp) {
                 const T *base = K + (int64_t)cs * 45;
 #pragma unroll
-                for (int c = 0; c < NCH; c++) ldg_vec<T>(base + ((int64_t)c * ncp + tid) * VEC, k + c * VEC);
-                k[44] = __ldg(base + (int64_t)NCH * VEC * ncp + tid);
+                for (int c = 0; c < NCH; c++) ldg_vec<T>(base + ((int64_t)c * ncp + ks) * VEC, k + c * VEC);
+                k[44] = __ldg(base + (int64_t)NCH * VEC * ncp + ks);
             }
             if (has && tid * 4 < ncp) cp_async4(&S.cl[b][tid * 4], clocal + cs + tid * 4);
             issue_role(b, m, has, role0);
@@ -534,7 +537,8 @@ __global__ void __launch_bounds__(64) k_hvp_rp(int T_, const int *__restrict__ n
         __syncthreads();  // (B) halo slot b complete; metadata slot (it+1)%3 visible
         const int ncp = S.meta[m][1] - S.meta[m][0], has = S.meta[m][2];
         const vec4<T> *uh = S.uh[b];
-        const int l = (has && tid < ncp) ? (int)S.cl[b][tid] : 0xFF;
+        const int cj = hvp_cell(tid);
+        const int l = (has && cj < ncp) ? (int)S.cl[b][cj] : 0xFF;
         T P[9];
         int hb = 0;
         if (l != 0xFF) {
@@ -633,7 +637,7 @@ __global__ void __launch_bounds__(64) k_hvp_rp(int T_, const int *__restrict__ n
 
 int g_num_sms = 0;
 
-template <class T>
+template <class T, int MINB>
 mpl_status launch_rp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
                      double cgthr) {
     static int per_sm[2] = {0, 0};
@@ -643,12 +647,12 @@ mpl_status launch_rp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         int occ = 0;
-        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_rp<T>, 64, 0));
+        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_rp<T, MINB>, 64, 0));
         per_sm[pi] = occ > 0 ? occ : 1;
     }
     int grid = g_num_sms * per_sm[pi];
     if (grid > ctx->T) grid = ctx->T;
-    k_hvp_rp<T><<<grid, 64, 0, ctx->stream>>>(
+    k_hvp_rp<T, MINB><<<grid, 64, 0, ctx->stream>>>(
         ctx->T, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p, (const uint8_t *)ctx->c_local.p,
         (const int *)ctx->t_hascells.p, (const T *)ctx->K.p, (const T *)owned_mass(ctx), (const vec4<T> *)u_tile,
         (vec4<T> *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p);
@@ -692,16 +696,19 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
     if (ctx->T == 0) return MPL_OK;
     static int variant = -1;
     if (variant < 0) {
-        // "pipe2" / "pipe3" (default pipe2): persistent pipelined v3 with 2 / 3 stages;
-        // "rp": persistent, tangent register-pipelined (v4); "reg": one tile per CTA (v2)
+        // "rp10" (default) / "rp" / "rp12": persistent, tangent register-pipelined (v4) with >= 10 / 1 /
+        // 12 CTAs per SM requested from ptxas; "pipe2" / "pipe3": persistent TMA-ring v3 with 2 / 3
+        // stages; "reg": one tile per CTA (v2)
         const char *e = getenv("MPL_HVP_KERNEL");
-        variant = 2;
-        if (e && e[0] == 'r' && e[1] == 'p') variant = 4;
+        variant = 5;
+        if (e && e[0] == 'r' && e[1] == 'p') variant = e[2] == '1' ? (e[3] == '2' ? 6 : 5) : 4;
         else if (e && e[0] == 'r') variant = 0;
         else if (e && e[0] == 'p' && e[4] == '3') variant = 3;
     }
     if (variant == 2) return launch_pipe<T, 2>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
-    if (variant == 4) return launch_rp<T>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+    if (variant == 4) return launch_rp<T, 1>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+    if (variant == 5) return launch_rp<T, 10>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+    if (variant == 6) return launch_rp<T, 12>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
     if (variant == 3) return launch_pipe<T, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
     if (variant == 0) {
         k_hvp_reg<T><<<ctx->T, 64, 0, ctx->stream>>>(

@@ -12,6 +12,7 @@
 // (local coords 1..3) are written with plain stores; the other (face) nodes are summed with global
 // atomics into a zeroed output.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "mpl_common.cuh"
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
     __syncthreads();
     if (MODE == LIN_FULL && has) {  // tile's tangent block, permuted into the chunked (coalesced) layout
         const int64_t base = (int64_t)cs * 45;
-        for (int i = tid; i < nc * 45; i += blockDim.x) Kout[k_off<T>(base, nc, i / 45, i % 45)] = Ks[i];
+        for (int i = tid; i < nc * 45; i += blockDim.x) Kout[k_off<T>(base, nc, kslot(i / 45, nc), i % 45)] = Ks[i];
     }
     // ---- node phase -----------------------------------------------------------------------
     if (tid < 125) {
@@ -360,7 +361,10 @@ __global__ void __launch_bounds__(256) k_pcg_update1(int64_t n, const int *__res
                                                      vec4<T> *__restrict__ Hp, vec4<T> *__restrict__ x,
                                                      vec4<T> *__restrict__ r, CGSlot *slot, DevScalars *sc) {
     const CGScal cs = cg_scalars(slot, j, false);
-    if (sc->neg_curv || (j > 0 && cs.rr <= thr)) return;  // converged before iteration j
+    // converged, or broken down at an earlier iteration (cg_done_iter, not neg_curv: block 0 of this
+    // launch may set neg_curv while later blocks start)
+    const int done = sc->cg_done_iter;
+    if ((done >= 0 && done <= j) || (j > 0 && cs.rr <= thr)) return;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (!(cs.pHp > 0.0)) {  // breakdown (negative curvature): the first iteration returns p = z_0
         if (j == 0 && i < n) x[i] = p[list[i]];
@@ -401,6 +405,74 @@ __global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, const int *__res
     const T beta = T(cs.rz1 / cs.rz);
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) {
+        const int ti = list[i];
+        const vec4<T> rv = r[i], iv = invD[i];
+        const vec4<T> pv = p[ti];
+        p[ti] = mk4<T>(rv.x * iv.x + beta * pv.x, rv.y * iv.y + beta * pv.y, rv.z * iv.z + beta * pv.z, T(0));
+    }
+}
+
+// One rank: update1 and update2 of iteration j in one persistent launch with a grid-wide barrier in
+// between (all CTAs co-resident: cudaLaunchCooperativeKernel).  Phase 2 walks the nodes in reverse so
+// it first re-reads the r / invD / p lines phase 1 touched last (still in L2).  bar[j] is a fresh
+// counter per iteration; a skipped iteration (converged / broken down) is skipped by every CTA.
+template <class T>
+__global__ void __launch_bounds__(256) k_pcg_fused(int64_t n, const int *__restrict__ list, int j, double thr,
+                                                   const vec4<T> *__restrict__ invD, vec4<T> *__restrict__ p,
+                                                   vec4<T> *__restrict__ Hp, vec4<T> *__restrict__ x,
+                                                   vec4<T> *__restrict__ r, CGSlot *slot, DevScalars *sc,
+                                                   unsigned int *bar) {
+    const CGScal cs = cg_scalars(slot, j, false);
+    const int done = sc->cg_done_iter;  // see k_pcg_update1
+    if ((done >= 0 && done <= j) || (j > 0 && cs.rr <= thr)) return;  // uniform over the grid
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x, gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (!(cs.pHp > 0.0)) {  // breakdown (negative curvature): the first iteration returns p = z_0
+        if (j == 0)
+            for (int64_t i = gt; i < n; i += stride) x[i] = p[list[i]];
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            sc->neg_curv = 1;
+            sc->cg_done_iter = j + 1;
+        }
+        return;
+    }
+    const T alpha = T(cs.rz / cs.pHp);
+    T rz = 0, rr = 0;
+    for (int64_t i = gt; i < n; i += stride) {
+        const int ti = list[i];
+        const vec4<T> iv = invD[i];
+        vec4<T> xv = x[i], rv = r[i];
+        const vec4<T> hv = Hp[ti], pv = p[ti];
+        Hp[ti] = mk4<T>(0, 0, 0, 0);
+        const T aw = alpha * iv.w;
+        xv.x += alpha * pv.x; xv.y += alpha * pv.y; xv.z += alpha * pv.z;
+        rv.x -= aw * hv.x; rv.y -= aw * hv.y; rv.z -= aw * hv.z;
+        x[i] = xv;
+        r[i] = rv;
+        rz += rv.w * (rv.x * rv.x * iv.x + rv.y * rv.y * iv.y + rv.z * rv.z * iv.z);
+        rr += rv.w * (rv.x * rv.x + rv.y * rv.y + rv.z * rv.z);
+    }
+    block_add((double)rz, slot[j + 1].rz);
+    block_add((double)rr, slot[j + 1].rr);
+    // ---- grid barrier ----------------------------------------------------------------------------
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(&bar[j], 1u);
+        while (atomicAdd(&bar[j], 0u) < gridDim.x) __nanosleep(64);
+        __threadfence();
+    }
+    __syncthreads();
+    // ---- update2: p = invD r + beta p -----------------------------------------------------------------
+    __shared__ double s_rz1, s_rr1;
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        double a = warp_sum(__ldcg(&slot[j + 1].rz[l])), b = warp_sum(__ldcg(&slot[j + 1].rr[l]));
+        if (l == 0) { s_rz1 = a; s_rr1 = b; }
+    }
+    __syncthreads();
+    if (s_rr1 <= thr) return;  // converged: p is not needed any more
+    const T beta = T(s_rz1 / cs.rz);
+    for (int64_t i = n - 1 - gt; i >= 0; i -= stride) {
         const int ti = list[i];
         const vec4<T> rv = r[i], iv = invD[i];
         const vec4<T> pv = p[ti];
@@ -588,8 +660,26 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     int slots_needed = cg_cap + 2;
     if (cfg->fixed_cg_iters)
         for (int k = 0; k < kmax; k++) slots_needed = std::max(slots_needed, cfg->fixed_cg_iters[k] + 2);
-    MPL_CHECK(ensure(ctx, ctx->cg_slots, (size_t)slots_needed * sizeof(CGSlot)));
+    MPL_CHECK(ensure(ctx, ctx->cg_slots, (size_t)slots_needed * (sizeof(CGSlot) + sizeof(unsigned int)) + 64));
     CGSlot *slots = (CGSlot *)ctx->cg_slots.p;
+    unsigned int *bar = (unsigned int *)(slots + slots_needed);  // grid-barrier counters of k_pcg_fused
+    // fused vector update: one rank, co-resident grid (MPL_PCG_FUSED=0 disables)
+    int fused_grid = 0;
+    {
+        static int max_blocks[2] = {-1, -1};
+        const int pi = sizeof(T) == 8;
+        const char *e = getenv("MPL_PCG_FUSED");
+        if (!multi(ctx) && !(e && e[0] == '0')) {
+            if (max_blocks[pi] < 0) {
+                int dev = 0, sms = 0, occ = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_fused<T>, 256, 0);
+                max_blocks[pi] = sms * occ;
+            }
+            fused_grid = (int)std::min<int64_t>(max_blocks[pi], std::max<int64_t>(1, (ctx->n_nodes_active + 255) / 256));
+        }
+    }
     const uint8_t *flag = (const uint8_t *)ctx->n_flag.p;
     const uint8_t *own = (const uint8_t *)ctx->n_own.p;
     vec4<T> *v = (vec4<T> *)ctx->n_v.p, *vt = (vec4<T> *)ctx->n_vt.p;
@@ -607,6 +697,9 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> hev;
+    // per-HVP device timing (stats.hvp_ms); MPL_HVP_EVENTS=0 drops the two events per HVP
+    const char *hve = getenv("MPL_HVP_EVENTS");
+    const bool hvp_events = !(hve && hve[0] == '0');
     double t_lin = 0, t_pcg = 0, t_ls = 0;
     auto elapsed = [&](cudaEvent_t a, cudaEvent_t b) {
         float ms = 0;
@@ -619,7 +712,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         // ---- linearise at v^k -------------------------------------------------------------
         cudaEventRecord(e0, st);
         MPL_CHECK(linearize_impl<T>(ctx, v, LIN_FULL, nullptr));
-        MPL_CUDA(cudaMemsetAsync(slots, 0, slots_needed * sizeof(CGSlot), st));
+        MPL_CUDA(cudaMemsetAsync(slots, 0, slots_needed * (sizeof(CGSlot) + sizeof(unsigned int)), st));
         MPL_CUDA(cudaMemsetAsync(&sc->neg_curv, 0, sizeof(int), st));
         MPL_CUDA(cudaMemsetAsync(&sc->cg_done_iter, 0xff, sizeof(int), st));
         MPL_CUDA(cudaMemsetAsync(p, 0, NT * sizeof(vec4<T>), st));
@@ -659,18 +752,31 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                         cudaEventCreate(&b);
                         hev.push_back({a, b});
                     }
-                    cudaEventRecord(hev[S.n_hvp].first, st);
+                    if (hvp_events) cudaEventRecord(hev[S.n_hvp].first, st);
                     // the HVP is skipped on device once converged (its output is then unused)
                     MPL_CHECK(launch_hvp<T>(ctx, p, Hp, slots[jj].pHp, slots, jj, thr));
                     if (multi(ctx)) {  // complete Hp on the shared planes; global p.Hp (timed with the HVP)
                         MPL_CHECK(halo_sum_nodes<T>(ctx, Hp, nullptr));
                         MPL_CHECK(allreduce_d(ctx, slots[jj].pHp, NSTRIPE));
                     }
-                    cudaEventRecord(hev[S.n_hvp].second, st);
+                    if (hvp_events) cudaEventRecord(hev[S.n_hvp].second, st);
                     S.n_hvp++;
-                    k_pcg_update1<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc); ctx->launches++;
-                    MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
-                    k_pcg_update2<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, slots, sc); ctx->launches++;
+                    if (fused_grid > 0) {  // one rank: both vector updates in one cooperative launch
+                        int64_t na = NA;
+                        int jj_ = jj;
+                        double thr_ = thr;
+                        const vec4<T> *invD_ = invD;
+                        CGSlot *slots_ = slots;
+                        void *args[] = {&na, (void *)&list, &jj_, &thr_, (void *)&invD_, (void *)&p, (void *)&Hp,
+                                        (void *)&x, (void *)&r, (void *)&slots_, (void *)&sc, (void *)&bar};
+                        MPL_CUDA(cudaLaunchCooperativeKernel((const void *)k_pcg_fused<T>, dim3(fused_grid), dim3(256),
+                                                             args, 0, st));
+                        ctx->launches++;
+                    } else {
+                        k_pcg_update1<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc); ctx->launches++;
+                        MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
+                        k_pcg_update2<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, slots, sc); ctx->launches++;
+                    }
                 }
                 launched += n;
                 MPL_CUDA(cudaGetLastError());
@@ -752,7 +858,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     }
     MPL_CHECK(energy_at<T>(ctx, v, &S.energy));
     double hsum = 0;
-    for (int i = 0; i < S.n_hvp; i++) hsum += elapsed(hev[i].first, hev[i].second);
+    if (hvp_events)
+        for (int i = 0; i < S.n_hvp; i++) hsum += elapsed(hev[i].first, hev[i].second);
     for (auto &pr : hev) {
         cudaEventDestroy(pr.first);
         cudaEventDestroy(pr.second);

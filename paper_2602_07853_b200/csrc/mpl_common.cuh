@@ -234,6 +234,13 @@ template <class T> struct KL {
     static constexpr int NCH = 45 / VEC;
     static constexpr int REM = 45 - NCH * VEC;
 };
+// Cell j of a tile is handled by HVP thread (warp j & 1, lane j >> 1), so the two warps of a 64-thread
+// CTA get ceil(ncp/2) and floor(ncp/2) cells; the tangent of cell j is stored at slot
+// kslot(j) = (j & 1) ncp/2 + (j >> 1), so each warp's 16-byte loads are contiguous.
+__host__ __device__ __forceinline__ int kslot(int j, int ncp) { return (j & 1) * (ncp >> 1) + (j >> 1); }
+// HVP thread -> (cell j, tangent slot)
+__device__ __forceinline__ int hvp_cell(int tid) { return 2 * (tid & 31) + (tid >> 5); }
+__device__ __forceinline__ int hvp_slot(int tid, int ncp) { return (tid >> 5) * (ncp >> 1) + (tid & 31); }
 template <class T> __host__ __device__ __forceinline__ int64_t k_off(int64_t base, int ncp, int j, int e) {
     return e < KL<T>::NCH * KL<T>::VEC
                ? base + ((int64_t)(e / KL<T>::VEC) * ncp + j) * KL<T>::VEC + (e % KL<T>::VEC)

@@ -210,8 +210,9 @@ MPL_API mpl_status mpl_get_diag(mpl_ctx ctx, void *D);
 /* Matrix-free Hessian-vector product at the last linearisation point (unprojected):
  * (Hu)_i = m_i u_i + sum_c (K_c : dG_c(u)) grad w_ic, dG_c(u) = sum_j u_j (x) grad w_jc. */
 MPL_API mpl_status mpl_hvp(mpl_ctx ctx, const void *u, void *Hu);
-/* The same product on device-resident canonical vectors, repeated `reps` times back to back;
- * reports the mean device time per HVP launch (CUDA events on the context stream). */
+/* Benchmark of the HVP kernel: `reps` back-to-back launches on u (canonical order, any memory),
+ * mean device time per launch from CUDA events on the context stream (kernel only: no zeroing of Hu,
+ * no slab halo exchange); then one complete product written to Hu (may be NULL). */
 MPL_API mpl_status mpl_hvp_bench(mpl_ctx ctx, const void *u_dev, void *Hu_dev, int32_t reps, double *ms_per_hvp);
 
 /* ---- the implicit solve ---------------------------------------- */

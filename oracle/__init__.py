@@ -45,7 +45,7 @@ class _Grid(C.Structure):
 
 
 class _Mat(C.Structure):
-    _fields_ = [("E", C.c_double), ("nu", C.c_double), ("rho", C.c_double)]
+    _fields_ = [("E", C.c_double), ("nu", C.c_double), ("rho", C.c_double), ("kind", C.c_int32)]
 
 
 class _Box(C.Structure):
@@ -94,6 +94,14 @@ def lib():
         L.orc_c2n.argtypes = [vp, vp, vp, vp, vp, vp]
         L.orc_dirichlet.argtypes = [vp, i32, vp, vp, vp, vp]
         L.orc_stretch.argtypes = [vp, d, d, vp]
+        L.orc_nh_tau.argtypes = [vp, d, d, vp]
+        L.orc_nh_tau.restype = C.c_int
+        L.orc_nh_psi.argtypes = [vp, d, d]
+        L.orc_nh_psi.restype = d
+        L.orc_nh_stretch.argtypes = [vp, d, d, vp, vp]
+        L.orc_nh_stretch.restype = C.c_int
+        L.orc_nh_cardano.argtypes = [d, d, d, vp]
+        L.orc_nh_cardano.restype = d
         L.orc_stretch_all.argtypes = [vp, i32, vp, vp, vp, vp]
         L.orc_energy.argtypes = [vp, vp]
         L.orc_energy.restype = d
@@ -151,6 +159,7 @@ def _mats(materials) -> "C.Array":
     arr = (_Mat * MAXMAT)()
     for k, m in enumerate(materials):
         arr[k].E, arr[k].nu, arr[k].rho = float(m.E), float(m.nu), float(m.rho)
+        arr[k].kind = int(getattr(m, "kind", 0))  # 0 StVK-Hencky, 1 split Neo-Hookean
     return arr
 
 
@@ -217,6 +226,43 @@ def hencky_tau(F, mu: float, lam: float) -> np.ndarray:
 def hencky_psi(F, mu: float, lam: float) -> float:
     F = _f64(F).reshape(9)
     return float(lib().orc_hencky_psi(_p(F), mu, lam))
+
+
+def bulk_modulus(mu: float, lam: float) -> float:
+    """kappa = 2/3 mu + lam in 3D."""
+    return 2.0 * mu / 3.0 + lam
+
+
+def nh_tau(F, mu: float, kappa: float) -> np.ndarray:
+    """Split Neo-Hookean Kirchhoff stress (Eq. split-nh-tau)."""
+    F = _f64(F).reshape(9)
+    t = np.zeros(9)
+    if lib().orc_nh_tau(_p(F), mu, kappa, _p(t)) != 0:
+        raise ValueError("inverted F (det <= 0)")
+    return t.reshape(3, 3)
+
+
+def nh_psi(F, mu: float, kappa: float) -> float:
+    """Split Neo-Hookean energy density (Eq. split-nh-energy)."""
+    F = _f64(F).reshape(9)
+    return float(lib().orc_nh_psi(_p(F), mu, kappa))
+
+
+def nh_stretch(tau, mu: float, kappa: float):
+    """Split Neo-Hookean stretch reconstruction (App. C Cardano); returns (S, branch)
+    with branch 1 (Delta >= 0) or 3 (three real roots)."""
+    tau = _f64(tau).reshape(9)
+    S = np.zeros(9)
+    br = C.c_int32(0)
+    if lib().orc_nh_stretch(_p(tau), mu, kappa, _p(S), C.byref(br)) != 0:
+        raise ValueError("stress outside the split Neo-Hookean inversion domain")
+    return S.reshape(3, 3), br.value
+
+
+def nh_cardano(p: float, q: float, dmin: float):
+    br = C.c_int32(0)
+    m = lib().orc_nh_cardano(float(p), float(q), float(dmin), C.byref(br))
+    return m, br.value
 
 
 def stretch(tau, mu: float, lam: float) -> np.ndarray:

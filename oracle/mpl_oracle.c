@@ -33,6 +33,7 @@ typedef struct {
 
 typedef struct {
     double E, nu, rho;
+    int32_t kind; /* 0 = StVK-Hencky, 1 = split Neo-Hookean (App. C) */
 } orc_material;
 
 typedef struct {
@@ -223,6 +224,148 @@ static double hencky_psi(const double F[9], double mu, double lam) {
 double orc_hencky_psi(const double F[9], double mu, double lam) { return hencky_psi(F, mu, lam); }
 
 /* ------------------------------------------------------------------------ */
+/* Split Neo-Hookean (§4.3.2, d = 3):                              */
+/*   Psi(F) = mu/2 (tr((J^{-1/3}F)^T (J^{-1/3}F)) - 3) + kappa/4 (J^2 - 1 - 2 log J)   */
+/*            (Eq. split-nh-energy; kappa = 2/3 mu + lam)                */
+/*   tau(F) = mu J^{-2/3} dev(b) + alpha(J) I, alpha = kappa/2 (J^2 - 1)       */
+/*            (Eq. split-nh-tau)                                     */
+/* Written out as the paper states them (the oracle is fp64).                 */
+/* ------------------------------------------------------------------------ */
+static double nh_kappa(double mu, double lam) { return 2.0 * mu / 3.0 + lam; }
+
+int orc_nh_tau(const double F[9], double mu, double kappa, double tau[9]) {
+    double J = mat_det(F);
+    if (!(J > 0.0)) return -1;
+    double FT[9], b[9];
+    mat_T(F, FT);
+    mat_mul(F, FT, b);
+    double trb = b[0] + b[4] + b[8];
+    double Jm23 = pow(J, -2.0 / 3.0);
+    double alpha = 0.5 * kappa * (J * J - 1.0);
+    for (int a = 0; a < 9; a++) {
+        double devb = b[a] - ((a % 4 == 0) ? trb / 3.0 : 0.0);
+        tau[a] = mu * Jm23 * devb + ((a % 4 == 0) ? alpha : 0.0);
+    }
+    return 0;
+}
+
+double orc_nh_psi(const double F[9], double mu, double kappa) {
+    double J = mat_det(F);
+    if (!(J > 0.0)) return INFINITY;
+    double FT[9], C[9];
+    mat_T(F, FT);
+    mat_mul(FT, F, C);
+    double trC = C[0] + C[4] + C[8];
+    return 0.5 * mu * (pow(J, -2.0 / 3.0) * trC - 3.0) + 0.25 * kappa * (J * J - 1.0 - 2.0 * log(J));
+}
+
+/* Directional derivative of tau along dF (differentiating Eq. split-nh-tau):
+ *   dJ = J tr(F^{-1} dF); db = dF F^T + F dF^T;
+ *   dtau = mu [ -2/3 J^{-2/3} (dJ/J) dev(b) + J^{-2/3} dev(db) ] + kappa J dJ I. */
+static void nh_dtau(const double F[9], const double dF[9], double mu, double kappa, double dtau[9]) {
+    double J = mat_det(F), Fi[9], FidF[9], FT[9], dFT[9], b[9], t1[9], t2[9], db[9];
+    mat_inv(F, Fi);
+    mat_mul(Fi, dF, FidF);
+    double dJ = J * (FidF[0] + FidF[4] + FidF[8]);
+    mat_T(F, FT);
+    mat_T(dF, dFT);
+    mat_mul(F, FT, b);
+    mat_mul(dF, FT, t1);
+    mat_mul(F, dFT, t2);
+    for (int a = 0; a < 9; a++) db[a] = t1[a] + t2[a];
+    double trb = b[0] + b[4] + b[8], trdb = db[0] + db[4] + db[8];
+    double Jm23 = pow(J, -2.0 / 3.0);
+    for (int a = 0; a < 9; a++) {
+        double dev_b = b[a] - ((a % 4 == 0) ? trb / 3.0 : 0.0);
+        double dev_db = db[a] - ((a % 4 == 0) ? trdb / 3.0 : 0.0);
+        dtau[a] = mu * (-2.0 / 3.0 * Jm23 * (dJ / J) * dev_b + Jm23 * dev_db) + ((a % 4 == 0) ? kappa * J * dJ : 0.0);
+    }
+}
+
+/* Cardano root of m^3 + p m + q = 0 on the admissible branch m > -min_i delta_i (App. C,
+ * P:1305-1348; Eqs. cardano-one-real / cardano-three-real).  *branch = 1 (Delta >= 0) or 3. */
+static double cbrt_signed(double z) { return z < 0 ? -pow(-z, 1.0 / 3.0) : pow(z, 1.0 / 3.0); }
+double orc_nh_cardano(double p, double q, double dmin, int32_t *branch) {
+    double Delta = (q / 2.0) * (q / 2.0) + (p / 3.0) * (p / 3.0) * (p / 3.0);
+    if (Delta >= 0.0) {
+        if (branch) *branch = 1;
+        /* m = cbrt(-q/2 + sqrt D) + cbrt(-q/2 - sqrt D) (Eq. cardano-one-real).  The two cube roots
+         * u, v satisfy u v = -p/3; the one of larger magnitude is taken from the formula and the other
+         * as -p/(3u) — the same expression without the cancellation of -q/2 - sqrt D when |p| << |q|. */
+        double sd = sqrt(Delta);
+        double u = cbrt_signed(-q / 2.0 + (q <= 0.0 ? sd : -sd));
+        return u != 0.0 ? u - p / (3.0 * u) : 0.0;
+    }
+    if (branch) *branch = 3;
+    double r = 2.0 * sqrt(-p / 3.0);
+    double arg = (3.0 * q / (2.0 * p)) * sqrt(-3.0 / p);
+    if (arg > 1.0) arg = 1.0; /* "we clamp the arccos argument in [-1,1]" */
+    if (arg < -1.0) arg = -1.0;
+    double theta = acos(arg) / 3.0;
+    double best = NAN;
+    for (int k = 0; k < 3; k++) { /* the admissible root: beta_i = m + delta_i > 0 for all i */
+        double m = r * cos(theta - 2.0 * M_PI * k / 3.0);
+        if (m > -dmin && (isnan(best) || m > best)) best = m;
+    }
+    return best;
+}
+
+/* Stretch reconstruction (§4.3.2 P:258-271 + App. C): tau = U diag(tau_i) U^T;
+ * alpha = tr(tau)/3, J = sqrt(1 + 2 alpha / kappa) (Eq. J-from-alpha), s = mu J^{-2/3},
+ * delta_i = (tau_i - alpha)/s, S2 = sum_{i<j} delta_i delta_j, S3 = prod delta_i; the cubic
+ * m^3 + S2 m + (S3 - J^2) = 0 (Eq. m-3D), beta_i = m + delta_i, sigma_i = sqrt(beta_i),
+ * S = U diag(sigma) U^T.  Returns -1 outside the inversion domain (1 + 2 alpha/kappa <= 0). */
+int orc_nh_stretch(const double tau[9], double mu, double kappa, double S[9], int32_t *branch) {
+    double w[3], U[9];
+    orc_sym_eig3(tau, w, U);
+    double alpha = (w[0] + w[1] + w[2]) / 3.0;
+    double J2 = 1.0 + 2.0 * alpha / kappa;
+    if (!(J2 > 0.0)) return -1;
+    double J = sqrt(J2);
+    double s = mu * pow(J, -2.0 / 3.0);
+    double d[3];
+    for (int i = 0; i < 3; i++) d[i] = (w[i] - alpha) / s;
+    double S2 = d[0] * d[1] + d[1] * d[2] + d[2] * d[0], S3 = d[0] * d[1] * d[2];
+    double dmin = fmin(d[0], fmin(d[1], d[2]));
+    double m = orc_nh_cardano(S2, S3 - J * J, dmin, branch);
+    /* The reconstruction is defined by the root of Eq. m-3D; Cardano's closed form (which picks the
+     * admissible branch) loses digits near a double root, so the root is refined by Newton steps on
+     * the same cubic (reading f1-a). */
+    for (int it = 0; it < 3; it++) {
+        double f = m * m * m + S2 * m + (S3 - J * J), df = 3.0 * m * m + S2;
+        if (!(fabs(df) > 1e-300)) break;
+        double mn = m - f / df;
+        if (!(mn > -dmin)) break;
+        m = mn;
+    }
+    double sig[3];
+    for (int i = 0; i < 3; i++) {
+        double beta = m + d[i];
+        if (!(beta > 0.0)) return -1;
+        sig[i] = sqrt(beta);
+    }
+    for (int a = 0; a < 3; a++)
+        for (int b2 = 0; b2 < 3; b2++) {
+            double v = 0;
+            for (int i = 0; i < 3; i++) v += U[3 * a + i] * sig[i] * U[3 * b2 + i];
+            S[3 * a + b2] = v;
+        }
+    return 0;
+}
+
+/* ---- per-material dispatch (each material slot keeps its own constitutive law) ---- */
+static int law_tau(const orc_material *m, const double F[9], double tau[9]) {
+    double mu, lam;
+    lame(m, &mu, &lam);
+    return m->kind == 1 ? orc_nh_tau(F, mu, nh_kappa(mu, lam), tau) : orc_hencky_tau(F, mu, lam, tau);
+}
+static double law_psi(const orc_material *m, const double F[9]) {
+    double mu, lam;
+    lame(m, &mu, &lam);
+    return m->kind == 1 ? orc_nh_psi(F, mu, nh_kappa(mu, lam)) : hencky_psi(F, mu, lam);
+}
+
+/* ------------------------------------------------------------------------ */
 /* C3: particle -> quadrature unload (Alg. 2 lines 1-9; Eqs.        */
 /* p2c-mV, p2c-mv-affine, p2c-A-sum P:64-68; Eq. vtau).  Outputs the   */
 /* raw accumulators; orc_normalize performs Alg. 2 lines 10-15.                */
@@ -243,11 +386,9 @@ int64_t orc_p2q(const orc_grid *g, int32_t nmat, const orc_material *mats, int64
     for (int64_t p = 0; p < np; p++) {
         int k = mat[p];
         if (k < 0 || k >= nmat) return -(p + 1);
-        double mu, lam;
-        lame(&mats[k], &mu, &lam);
         double mp = mats[k].rho * vol[p]; /* m_p = rho V_p */
         double tau[9];
-        if (orc_hencky_tau(F + 9 * p, mu, lam, tau)) return -(p + 1); /* Alg. 2 line 3 */
+        if (law_tau(&mats[k], F + 9 * p, tau)) return -(p + 1); /* Alg. 2 line 3 */
         int32_t b[3];
         double f[3], w[8];
         orc_base_cell(g, x + 3 * p, b, f);
@@ -376,9 +517,15 @@ void orc_stretch_all(const orc_grid *g, int32_t nmat, const orc_material *mats, 
         lame(&mats[k], &mu, &lam);
         for (int64_t c = 0; c < nc; c++) {
             double *S = S_ck + ((int64_t)k * nc + c) * 9;
-            if (V_ck[(int64_t)k * nc + c] != 0.0)
-                orc_stretch(tau_ck + ((int64_t)k * nc + c) * 9, mu, lam, S); /* Alg. 3 line 6 */
-            else
+            if (V_ck[(int64_t)k * nc + c] != 0.0) {
+                const double *tau = tau_ck + ((int64_t)k * nc + c) * 9; /* Alg. 3 line 6 */
+                if (mats[k].kind == 1) {
+                    if (orc_nh_stretch(tau, mu, nh_kappa(mu, lam), S, NULL))
+                        for (int a = 0; a < 9; a++) S[a] = NAN; /* outside the inversion domain */
+                } else {
+                    orc_stretch(tau, mu, lam, S);
+                }
+            } else
                 for (int a = 0; a < 9; a++) S[a] = (a % 4 == 0) ? 1.0 : 0.0;
         }
     }
@@ -425,21 +572,20 @@ double orc_energy(const orc_problem *P, const double *v) {
                 for (int k = 0; k < P->nmat; k++) {
                     double V = P->V_ck[(int64_t)k * nc + c];
                     if (V == 0.0) continue;
-                    double mu, lam, F[9];
-                    lame(&P->mats[k], &mu, &lam);
+                    double F[9];
                     mat_mul(A, P->S_ck + ((int64_t)k * nc + c) * 9, F); /* Eq. Ftrial-rotfree */
-                    E += V * hencky_psi(F, mu, lam);
+                    E += V * law_psi(&P->mats[k], F);
                 }
             }
     return E;
 }
 
 /* Per-cell, per-slot gradient block: dt V tau(F) A^{-T}  (== dt V P(F) S^T, amb-3) */
-static void slot_grad(double dt, double V, double mu, double lam, const double A[9], const double S[9],
+static void slot_grad(double dt, double V, const orc_material *m, const double A[9], const double S[9],
                       double out[9]) {
     double F[9], tau[9], Ai[9], AiT[9];
     mat_mul(A, S, F);
-    orc_hencky_tau(F, mu, lam, tau);
+    law_tau(m, F, tau);
     mat_inv(A, Ai);
     mat_T(Ai, AiT);
     mat_mul(tau, AiT, out);
@@ -459,8 +605,10 @@ static double dlog(double lx, double ly) {
  *   dF = dt dG S ; db = dF F^T + F dF^T ; D = Q (L o (Q^T db Q)) Q^T  (Daleckii-Krein) ;
  *   dtau = mu D + lam/2 tr(D) I ;  d(A^{-T}) = -A^{-T} (dt dG)^T A^{-T} ;
  *   out = dt V (dtau A^{-T} + tau d(A^{-T})).   (App. B; C6 of SURVEY §8(c)) */
-static void slot_tangent(double dt, double V, double mu, double lam, const double A[9], const double S[9],
+static void slot_tangent(double dt, double V, const orc_material *m, const double A[9], const double S[9],
                          const double dG[9], double out[9]) {
+    double mu, lam;
+    lame(m, &mu, &lam);
     double F[9], H[9], HT[9], HHT[9], Bm[9], w[3], Q[9], QT[9];
     mat_mul(A, S, F);
     for (int a = 0; a < 9; a++) H[a] = F[a] - ((a % 4 == 0) ? 1.0 : 0.0);
@@ -489,6 +637,10 @@ static void slot_tangent(double dt, double V, double mu, double lam, const doubl
     double trD = D[0] + D[4] + D[8];
     double dtau[9];
     for (int a = 0; a < 9; a++) dtau[a] = mu * D[a] + ((a % 4 == 0) ? 0.5 * lam * trD : 0.0);
+    if (m->kind == 1) { /* split Neo-Hookean: tau and its derivative directly (Eq. split-nh-tau) */
+        orc_nh_tau(F, mu, nh_kappa(mu, lam), tau);
+        nh_dtau(F, dF, mu, nh_kappa(mu, lam), dtau);
+    }
     double Ai[9], AiT[9], dGT[9], dAiT[9], r1[9], r2[9];
     mat_inv(A, Ai);
     mat_T(Ai, AiT);
@@ -525,9 +677,8 @@ void orc_gradient(const orc_problem *P, const double *v, double *grad) {
                 for (int k = 0; k < P->nmat; k++) {
                     double V = P->V_ck[(int64_t)k * nc + c];
                     if (V == 0.0) continue;
-                    double mu, lam, blk[9];
-                    lame(&P->mats[k], &mu, &lam);
-                    slot_grad(P->dt, V, mu, lam, A, P->S_ck + ((int64_t)k * nc + c) * 9, blk);
+                    double blk[9];
+                    slot_grad(P->dt, V, &P->mats[k], A, P->S_ck + ((int64_t)k * nc + c) * 9, blk);
                     for (int a = 0; a < 9; a++) Pc[a] += blk[a];
                 }
                 for (int o = 0; o < 8; o++) {
@@ -558,9 +709,8 @@ void orc_hvp(const orc_problem *P, const double *v, const double *u, double *Hu)
                 for (int k = 0; k < P->nmat; k++) {
                     double V = P->V_ck[(int64_t)k * nc + c];
                     if (V == 0.0) continue;
-                    double mu, lam, blk[9];
-                    lame(&P->mats[k], &mu, &lam);
-                    slot_tangent(P->dt, V, mu, lam, A, P->S_ck + ((int64_t)k * nc + c) * 9, dG, blk);
+                    double blk[9];
+                    slot_tangent(P->dt, V, &P->mats[k], A, P->S_ck + ((int64_t)k * nc + c) * 9, dG, blk);
                     for (int a = 0; a < 9; a++) Pc[a] += blk[a];
                 }
                 for (int o = 0; o < 8; o++) {
@@ -596,9 +746,8 @@ void orc_diag(const orc_problem *P, const double *v, double *D) {
                         for (int k = 0; k < P->nmat; k++) {
                             double V = P->V_ck[(int64_t)k * nc + c];
                             if (V == 0.0) continue;
-                            double mu, lam, blk[9];
-                            lame(&P->mats[k], &mu, &lam);
-                            slot_tangent(P->dt, V, mu, lam, A, P->S_ck + ((int64_t)k * nc + c) * 9, dG, blk);
+                            double blk[9];
+                            slot_tangent(P->dt, V, &P->mats[k], A, P->S_ck + ((int64_t)k * nc + c) * 9, dG, blk);
                             for (int e = 0; e < 9; e++) Pc[e] += blk[e];
                         }
                         D[3 * i + a] += Pc[3 * a] * gw[0] + Pc[3 * a + 1] * gw[1] + Pc[3 * a + 2] * gw[2];

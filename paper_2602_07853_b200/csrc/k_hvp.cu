@@ -101,7 +101,8 @@ template <> __device__ __forceinline__ void ldg_vec<double>(const double *p, dou
 template <class T>
 __global__ void __launch_bounds__(64) k_hvp_reg(const int *__restrict__ nplus, const int *__restrict__ cstart,
                                                 const uint8_t *__restrict__ clocal, const int *__restrict__ hascells,
-                                                const T *__restrict__ K, const T *__restrict__ nmass,
+                                                const T *__restrict__ K, const int *__restrict__ kstart,
+                                                const int *__restrict__ ncell, const T *__restrict__ nmass,
                                                 const vec4<T> *__restrict__ u, vec4<T> *__restrict__ Hu,
                                                 double *__restrict__ uHu, const CGSlot *__restrict__ cgs, int cgj,
                                                 double cgthr, const DevScalars *__restrict__ sc) {
@@ -114,17 +115,17 @@ __global__ void __launch_bounds__(64) k_hvp_reg(const int *__restrict__ nplus, c
         if (sc->neg_curv || (cgj > 0 && rr <= cgthr)) return;
     }
     const int has = hascells[t];
-    const int cs = cstart[t], ncp = cstart[t + 1] - cs;
+    const int cs = cstart[t], n = ncell[t];
     constexpr int VEC = KL<T>::VEC, NCH = KL<T>::NCH;
     T k[45];
     int l = 0xFF;
-    const int cj = hvp_cell(tid), ks = hvp_slot(tid, ncp);
-    if (has && cj < ncp) {  // tiles outside the slab (ghost planes) carry no tangent
+    const int cj = hvp_cell(tid), ks = hvp_slot(tid, n);
+    if (has && cj < n) {  // tiles outside the slab (ghost planes) carry no tangent
         l = clocal[cs + cj];
-        const T *base = K + (int64_t)cs * 45;
+        const T *base = K + kstart[t];
 #pragma unroll
-        for (int c = 0; c < NCH; c++) ldg_vec<T>(base + ((int64_t)c * ncp + ks) * VEC, k + c * VEC);
-        k[44] = __ldg(base + (int64_t)NCH * VEC * ncp + ks);
+        for (int c = 0; c < NCH; c++) ldg_vec<T>(base + ((int64_t)c * n + ks) * VEC, k + c * VEC);
+        k[44] = __ldg(base + (int64_t)NCH * VEC * n + ks);
     }
     for (int h = tid; h < 125; h += 64) {
         int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
@@ -254,7 +255,8 @@ __device__ __forceinline__ int make_role(int h) {
 template <class T, int NS>
 __global__ void __launch_bounds__(64) k_hvp_pipe(int T_, const int *__restrict__ nplus, const int *__restrict__ cstart,
                                                  const uint8_t *__restrict__ clocal, const int *__restrict__ hascells,
-                                                 const T *__restrict__ K, const T *__restrict__ nmass,
+                                                 const T *__restrict__ K, const int *__restrict__ kstart,
+                                                const int *__restrict__ ncell, const T *__restrict__ nmass,
                                                  const vec4<T> *__restrict__ u, vec4<T> *__restrict__ Hu,
                                                  double *__restrict__ uHu, const CGSlot *__restrict__ cgs, int cgj,
                                                  double cgthr, const DevScalars *__restrict__ sc) {
@@ -277,16 +279,15 @@ __global__ void __launch_bounds__(64) k_hvp_pipe(int T_, const int *__restrict__
         if (t >= T_) return 0;
         if (tid < 8) return tid ? nplus[8 * t + tid] : t;
         if (tid == 8) return cstart[t];
-        if (tid == 9) return cstart[t + 1];
+        if (tid == 9) return ncell[t];
         if (tid == 10) return hascells[t];
+        if (tid == 11) return kstart[t];
         return 0;
     };
     auto put_meta = [&](int s, int t, int reg) {
         if (tid < 8) S.nb[s][tid] = reg;
-        if (tid == 8) S.meta[s][0] = reg;
-        if (tid == 9) S.meta[s][1] = reg;  // ce for now; issue() turns it into ncp
-        if (tid == 10) S.meta[s][2] = reg;
-        if (tid == 11) S.meta[s][3] = t;
+        if (tid >= 8 && tid < 12) S.meta[s][tid - 8] = reg;  // cs, n (real cells), has, kstart
+        (void)t;
     };
     auto issue_role = [&](int s, int mi, int has, int role) {
         if (role < 0) return;
@@ -306,12 +307,12 @@ __global__ void __launch_bounds__(64) k_hvp_pipe(int T_, const int *__restrict__
     // all threads: after a barrier that published S.nb[s] / S.meta[s]
     auto issue = [&](int s, int mi, int t) {
         if (t < T_) {
-            const int cs = S.meta[mi][0], ncp = S.meta[mi][1] - cs, has = S.meta[mi][2];
-            const int nk = has ? ncp : 0;
+            const int cs = S.meta[mi][0], n = S.meta[mi][1], has = S.meta[mi][2], kb = S.meta[mi][3];
+            const int nk = has ? n : 0;
             if (tid == 0) {
-                const uint32_t bytes = (uint32_t)(nk * 45 * sizeof(T));
+                const uint32_t bytes = (uint32_t)(((45 * nk + 3) & ~3) * sizeof(T));  // t_kcnt: multiple of 16 B
                 mbar_expect_tx(&S.bar[s], bytes);
-                if (bytes) bulk_g2s(S.K[s], K + (int64_t)cs * 45, bytes, &S.bar[s]);
+                if (bytes) bulk_g2s(S.K[s], K + kb, bytes, &S.bar[s]);
             }
             if (tid * 4 < nk) cp_async4(&S.cl[s][tid * 4], clocal + cs + tid * 4);
             issue_role(s, mi, has, role0);
@@ -336,9 +337,9 @@ __global__ void __launch_bounds__(64) k_hvp_pipe(int T_, const int *__restrict__
         cp_async_wait<NS - 1>();
         mbar_wait(&S.bar[st], (uint32_t)((it / NS) & 1));
         __syncthreads();  // (B) stage st complete for every thread
-        const int ncp = S.meta[mc][1] - S.meta[mc][0], has = S.meta[mc][2];
+        const int ncp = S.meta[mc][1], has = S.meta[mc][2];  // ncp: real cells of the tile
         const vec4<T> *uh = S.uh[st];
-        // ---- cell phase: P = K dG, corner forces added to F with shared-memory atomics ---------
+        // ---- cell phase: P = K dG, corner forces added to per-warp F ---------------------------
         const int cj = hvp_cell(tid), ks = hvp_slot(tid, ncp);
         const int l = (has && cj < ncp) ? (int)S.cl[st][cj] : 0xFF;
         if (l != 0xFF) {
@@ -458,14 +459,15 @@ template <class T> struct RpSmem {
     alignas(16) uint8_t cl[2][64];
     T F[2][3][128];
     int nb[3][8];
-    int meta[3][4];  // cs, ce, has
+    int meta[3][4];  // cs, n (real cells), has, kstart
     double red[2];
 };
 
 template <class T, int MINB>
 __global__ void __launch_bounds__(64, MINB) k_hvp_rp(int T_, const int *__restrict__ nplus, const int *__restrict__ cstart,
                                                const uint8_t *__restrict__ clocal, const int *__restrict__ hascells,
-                                               const T *__restrict__ K, const T *__restrict__ nmass,
+                                               const T *__restrict__ K, const int *__restrict__ kstart,
+                                                const int *__restrict__ ncell, const T *__restrict__ nmass,
                                                const vec4<T> *__restrict__ u, vec4<T> *__restrict__ Hu,
                                                double *__restrict__ uHu, const CGSlot *__restrict__ cgs, int cgj,
                                                double cgthr, const DevScalars *__restrict__ sc) {
@@ -483,13 +485,14 @@ __global__ void __launch_bounds__(64, MINB) k_hvp_rp(int T_, const int *__restri
         if (t >= T_) return 0;
         if (tid < 8) return tid ? nplus[8 * t + tid] : t;
         if (tid == 8) return cstart[t];
-        if (tid == 9) return cstart[t + 1];
+        if (tid == 9) return ncell[t];
         if (tid == 10) return hascells[t];
+        if (tid == 11) return kstart[t];
         return 0;
     };
     auto put_meta = [&](int m, int reg) {
         if (tid < 8) S.nb[m][tid] = reg;
-        else if (tid < 11) S.meta[m][tid - 8] = reg;
+        else if (tid < 12) S.meta[m][tid - 8] = reg;  // cs, n (real cells), has, kstart
     };
     auto issue_role = [&](int b, int m, int has, int role) {
         if (role < 0) return;
@@ -510,10 +513,10 @@ __global__ void __launch_bounds__(64, MINB) k_hvp_rp(int T_, const int *__restri
     // tile t's tangent -> registers, its halo -> shared slot b (all threads, after its metadata is visible)
     auto issue = [&](int t, int b, int m) {
         if (t < T_) {
-            const int cs = S.meta[m][0], ncp = S.meta[m][1] - cs, has = S.meta[m][2];
+            const int cs = S.meta[m][0], ncp = S.meta[m][1], has = S.meta[m][2];
             const int cj = hvp_cell(tid), ks = hvp_slot(tid, ncp);
             if (has && cj < ncp) {
-                const T *base = K + (int64_t)cs * 45;
+                const T *base = K + S.meta[m][3];
 #pragma unroll
                 for (int c = 0; c < NCH; c++) ldg_vec<T>(base + ((int64_t)c * ncp + ks) * VEC, k + c * VEC);
                 k[44] = __ldg(base + (int64_t)NCH * VEC * ncp + ks);
@@ -535,7 +538,7 @@ __global__ void __launch_bounds__(64, MINB) k_hvp_rp(int T_, const int *__restri
         const int b = it & 1, m = it % 3;
         cp_async_wait<0>();
         __syncthreads();  // (B) halo slot b complete; metadata slot (it+1)%3 visible
-        const int ncp = S.meta[m][1] - S.meta[m][0], has = S.meta[m][2];
+        const int ncp = S.meta[m][1], has = S.meta[m][2];  // ncp: real cells of the tile
         const vec4<T> *uh = S.uh[b];
         const int cj = hvp_cell(tid);
         const int l = (has && cj < ncp) ? (int)S.cl[b][cj] : 0xFF;
@@ -654,7 +657,8 @@ mpl_status launch_rp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
     if (grid > ctx->T) grid = ctx->T;
     k_hvp_rp<T, MINB><<<grid, 64, 0, ctx->stream>>>(
         ctx->T, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p, (const uint8_t *)ctx->c_local.p,
-        (const int *)ctx->t_hascells.p, (const T *)ctx->K.p, (const T *)owned_mass(ctx), (const vec4<T> *)u_tile,
+        (const int *)ctx->t_hascells.p, (const T *)ctx->K.p, (const int *)ctx->t_kstart.p,
+        (const int *)ctx->t_ncell.p, (const T *)owned_mass(ctx), (const vec4<T> *)u_tile,
         (vec4<T> *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p);
     ctx->launches++;
     MPL_CUDA(cudaGetLastError());
@@ -680,7 +684,8 @@ mpl_status launch_pipe(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *u
     if (grid > ctx->T) grid = ctx->T;
     k_hvp_pipe<T, NS><<<grid, 64, smem, ctx->stream>>>(
         ctx->T, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p, (const uint8_t *)ctx->c_local.p,
-        (const int *)ctx->t_hascells.p, (const T *)ctx->K.p, (const T *)owned_mass(ctx), (const vec4<T> *)u_tile,
+        (const int *)ctx->t_hascells.p, (const T *)ctx->K.p, (const int *)ctx->t_kstart.p,
+        (const int *)ctx->t_ncell.p, (const T *)owned_mass(ctx), (const vec4<T> *)u_tile,
         (vec4<T> *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p);
     ctx->launches++;
     MPL_CUDA(cudaGetLastError());
@@ -713,7 +718,8 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
     if (variant == 0) {
         k_hvp_reg<T><<<ctx->T, 64, 0, ctx->stream>>>(
             (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p, (const uint8_t *)ctx->c_local.p,
-            (const int *)ctx->t_hascells.p, (const T *)ctx->K.p, (const T *)owned_mass(ctx), (const vec4<T> *)u_tile,
+            (const int *)ctx->t_hascells.p, (const T *)ctx->K.p, (const int *)ctx->t_kstart.p,
+        (const int *)ctx->t_ncell.p, (const T *)owned_mass(ctx), (const vec4<T> *)u_tile,
             (vec4<T> *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p);
         ctx->launches++;
         MPL_CUDA(cudaGetLastError());

@@ -194,8 +194,8 @@ __global__ void k_scatter(GridP g, MatP mp, int64_t np, const int *__restrict__ 
 // ---- structural cell masks: cell active iff some base-cell bucket in cell - {0,1}^3 is non-empty
 __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, const int *__restrict__ nminus,
                             const int *__restrict__ bcount, const int *__restrict__ hascells,
-                            unsigned long long *__restrict__ cmask, int *__restrict__ ccount,
-                            unsigned long long *ncells) {
+                            unsigned long long *__restrict__ cmask, int *__restrict__ ccount, int *__restrict__ ncell,
+                            int *__restrict__ kcnt, unsigned long long *ncells) {
     int t = blockIdx.x;
     int l = threadIdx.x;  // 64 threads
     int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
@@ -221,6 +221,8 @@ __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, cons
         cmask[t] = m;
         int c = __popcll(m);
         ccount[t] = (c + 3) & ~3;
+        ncell[t] = c;
+        kcnt[t] = hascells[t] ? (45 * c + 3) & ~3 : 0;  // tangent only on owned tiles
         if (c && hascells[t]) atomicAdd(ncells, (unsigned long long)c);
     }
 }
@@ -639,13 +641,20 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     // structural cells: masks, padded counts, compact offsets
     MPL_CHECK(ensure(ctx, ctx->t_ccount, (size_t)(T_ + 1) * 4 + 16));
     MPL_CUDA(cudaMemsetAsync(ctx->t_ccount.p, 0, (size_t)(T_ + 1) * 4, st));
+    MPL_CHECK(ensure(ctx, ctx->t_ncell, (size_t)(T_ + 1) * 4 + 16));
+    MPL_CHECK(ensure(ctx, ctx->t_kcnt, (size_t)(T_ + 1) * 4 + 16));
+    MPL_CHECK(ensure(ctx, ctx->t_kstart, (size_t)(T_ + 1) * 4 + 16));
+    MPL_CUDA(cudaMemsetAsync(ctx->t_kcnt.p, 0, (size_t)(T_ + 1) * 4, st));
     if (T_) k_cell_mask<<<T_, 64, 0, st>>>(g, T_, (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p,
                                           (const int *)ctx->t_bcount.p, (const int *)ctx->t_hascells.p,
                                           (unsigned long long *)ctx->t_cmask.p,
-                                          (int *)ctx->t_ccount.p, counters + 1); ctx->launches++;
+                                          (int *)ctx->t_ccount.p, (int *)ctx->t_ncell.p, (int *)ctx->t_kcnt.p,
+                                          counters + 1); ctx->launches++;
     DBG_GUARDS("resample #7");
     MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_ccount.p, (int *)ctx->t_cstart.p, (int64_t)T_ + 1));
-    int Cpad = 0;
+    MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_kcnt.p, (int *)ctx->t_kstart.p, (int64_t)T_ + 1));
+    int Cpad = 0, Ktot = 0;
+    MPL_CUDA(cudaMemcpyAsync(&Ktot, (int *)ctx->t_kstart.p + T_, 4, cudaMemcpyDeviceToHost, st));
     unsigned long long ncells = 0;
     MPL_CUDA(cudaMemcpyAsync(&Cpad, (int *)ctx->t_cstart.p + T_, 4, cudaMemcpyDeviceToHost, st));
     MPL_CUDA(cudaMemcpyAsync(&ncells, counters + 1, 8, cudaMemcpyDeviceToHost, st));
@@ -672,7 +681,7 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CHECK(ensure(ctx, ctx->q_slot, C * nm * 16 * s));
     MPL_CHECK(ensure(ctx, ctx->q_vc, C * 4 * s));
     MPL_CHECK(ensure(ctx, ctx->q_Gc, C * 9 * s));
-    MPL_CHECK(ensure(ctx, ctx->K, C * 45 * s + 256));
+    MPL_CHECK(ensure(ctx, ctx->K, (size_t)Ktot * s + 256));
     if (T_) {
         k_cell_list<<<T_, 64, 0, st>>>(T_, (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_cstart.p,
                                        (uint8_t *)ctx->c_local.p, (int *)ctx->t_cellof.p); ctx->launches++;

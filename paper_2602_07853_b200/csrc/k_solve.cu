@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
                                                    const int *__restrict__ hascells, const vec4<T> *__restrict__ v,
                                                    const vec4<T> *__restrict__ vhat, const T *__restrict__ nmass,
                                                    const T *__restrict__ qslot, T *__restrict__ Kout,
+                                                   const int *__restrict__ kstart, const int *__restrict__ ncell,
                                                    vec4<T> *__restrict__ grad, vec4<T> *__restrict__ diag,
                                                    DevScalars *sc) {
     constexpr int KS = (MODE == LIN_FULL) ? 64 * 45 : 1;
@@ -221,8 +222,9 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
     }
     __syncthreads();
     if (MODE == LIN_FULL && has) {  // tile's tangent block, permuted into the chunked (coalesced) layout
-        const int64_t base = (int64_t)cs * 45;
-        for (int i = tid; i < nc * 45; i += blockDim.x) Kout[k_off<T>(base, nc, kslot(i / 45, nc), i % 45)] = Ks[i];
+        const int64_t base = kstart[t];
+        const int n = ncell[t];  // real cells come first in the compact run
+        for (int i = tid; i < n * 45; i += blockDim.x) Kout[k_off<T>(base, n, kslot(i / 45, n), i % 45)] = Ks[i];
     }
     // ---- node phase -----------------------------------------------------------------------
     if (tid < 125) {
@@ -412,74 +414,6 @@ __global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, const int *__res
     }
 }
 
-// One rank: update1 and update2 of iteration j in one persistent launch with a grid-wide barrier in
-// between (all CTAs co-resident: cudaLaunchCooperativeKernel).  Phase 2 walks the nodes in reverse so
-// it first re-reads the r / invD / p lines phase 1 touched last (still in L2).  bar[j] is a fresh
-// counter per iteration; a skipped iteration (converged / broken down) is skipped by every CTA.
-template <class T>
-__global__ void __launch_bounds__(256) k_pcg_fused(int64_t n, const int *__restrict__ list, int j, double thr,
-                                                   const vec4<T> *__restrict__ invD, vec4<T> *__restrict__ p,
-                                                   vec4<T> *__restrict__ Hp, vec4<T> *__restrict__ x,
-                                                   vec4<T> *__restrict__ r, CGSlot *slot, DevScalars *sc,
-                                                   unsigned int *bar) {
-    const CGScal cs = cg_scalars(slot, j, false);
-    const int done = sc->cg_done_iter;  // see k_pcg_update1
-    if ((done >= 0 && done <= j) || (j > 0 && cs.rr <= thr)) return;  // uniform over the grid
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x, gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (!(cs.pHp > 0.0)) {  // breakdown (negative curvature): the first iteration returns p = z_0
-        if (j == 0)
-            for (int64_t i = gt; i < n; i += stride) x[i] = p[list[i]];
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            sc->neg_curv = 1;
-            sc->cg_done_iter = j + 1;
-        }
-        return;
-    }
-    const T alpha = T(cs.rz / cs.pHp);
-    T rz = 0, rr = 0;
-    for (int64_t i = gt; i < n; i += stride) {
-        const int ti = list[i];
-        const vec4<T> iv = invD[i];
-        vec4<T> xv = x[i], rv = r[i];
-        const vec4<T> hv = Hp[ti], pv = p[ti];
-        Hp[ti] = mk4<T>(0, 0, 0, 0);
-        const T aw = alpha * iv.w;
-        xv.x += alpha * pv.x; xv.y += alpha * pv.y; xv.z += alpha * pv.z;
-        rv.x -= aw * hv.x; rv.y -= aw * hv.y; rv.z -= aw * hv.z;
-        x[i] = xv;
-        r[i] = rv;
-        rz += rv.w * (rv.x * rv.x * iv.x + rv.y * rv.y * iv.y + rv.z * rv.z * iv.z);
-        rr += rv.w * (rv.x * rv.x + rv.y * rv.y + rv.z * rv.z);
-    }
-    block_add((double)rz, slot[j + 1].rz);
-    block_add((double)rr, slot[j + 1].rr);
-    // ---- grid barrier ----------------------------------------------------------------------------
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(&bar[j], 1u);
-        while (atomicAdd(&bar[j], 0u) < gridDim.x) __nanosleep(64);
-        __threadfence();
-    }
-    __syncthreads();
-    // ---- update2: p = invD r + beta p -----------------------------------------------------------------
-    __shared__ double s_rz1, s_rr1;
-    if (threadIdx.x < 32) {
-        const int l = threadIdx.x;
-        double a = warp_sum(__ldcg(&slot[j + 1].rz[l])), b = warp_sum(__ldcg(&slot[j + 1].rr[l]));
-        if (l == 0) { s_rz1 = a; s_rr1 = b; }
-    }
-    __syncthreads();
-    if (s_rr1 <= thr) return;  // converged: p is not needed any more
-    const T beta = T(s_rz1 / cs.rz);
-    for (int64_t i = n - 1 - gt; i >= 0; i -= stride) {
-        const int ti = list[i];
-        const vec4<T> rv = r[i], iv = invD[i];
-        const vec4<T> pv = p[ti];
-        p[ti] = mk4<T>(rv.x * iv.x + beta * pv.x, rv.y * iv.y + beta * pv.y, rv.z * iv.z + beta * pv.z, T(0));
-    }
-}
-
 // g . x over free DOFs (g tile-dense, x compact)
 template <class T>
 __global__ void k_dot_gx(int64_t n, const int *__restrict__ list, const uint8_t *__restrict__ flag,
@@ -612,7 +546,7 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
     ctx->grid, ctx->mats, ctx->dt, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,                     \
         (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p, (const vec4<T> *)v_tile,                  \
         (const vec4<T> *)ctx->n_vhat.p, (const T *)owned_mass(ctx), (const T *)ctx->q_slot.p, (T *)ctx->K.p,       \
-        (vec4<T> *)ctx->n_g.p, (vec4<T> *)ctx->n_diag.p, sc
+        (const int *)ctx->t_kstart.p, (const int *)ctx->t_ncell.p, (vec4<T> *)ctx->n_g.p, (vec4<T> *)ctx->n_diag.p, sc
         if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY><<<T_, 128, 0, st>>>(LIN_ARGS);
         else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD><<<T_, 128, 0, st>>>(LIN_ARGS);
         else k_linearize<T, LIN_FULL><<<T_, 128, 0, st>>>(LIN_ARGS);
@@ -660,26 +594,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     int slots_needed = cg_cap + 2;
     if (cfg->fixed_cg_iters)
         for (int k = 0; k < kmax; k++) slots_needed = std::max(slots_needed, cfg->fixed_cg_iters[k] + 2);
-    MPL_CHECK(ensure(ctx, ctx->cg_slots, (size_t)slots_needed * (sizeof(CGSlot) + sizeof(unsigned int)) + 64));
+    MPL_CHECK(ensure(ctx, ctx->cg_slots, (size_t)slots_needed * sizeof(CGSlot)));
     CGSlot *slots = (CGSlot *)ctx->cg_slots.p;
-    unsigned int *bar = (unsigned int *)(slots + slots_needed);  // grid-barrier counters of k_pcg_fused
-    // fused vector update: one rank, co-resident grid (MPL_PCG_FUSED=0 disables)
-    int fused_grid = 0;
-    {
-        static int max_blocks[2] = {-1, -1};
-        const int pi = sizeof(T) == 8;
-        const char *e = getenv("MPL_PCG_FUSED");
-        if (!multi(ctx) && !(e && e[0] == '0')) {
-            if (max_blocks[pi] < 0) {
-                int dev = 0, sms = 0, occ = 0;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_fused<T>, 256, 0);
-                max_blocks[pi] = sms * occ;
-            }
-            fused_grid = (int)std::min<int64_t>(max_blocks[pi], std::max<int64_t>(1, (ctx->n_nodes_active + 255) / 256));
-        }
-    }
     const uint8_t *flag = (const uint8_t *)ctx->n_flag.p;
     const uint8_t *own = (const uint8_t *)ctx->n_own.p;
     vec4<T> *v = (vec4<T> *)ctx->n_v.p, *vt = (vec4<T> *)ctx->n_vt.p;
@@ -712,7 +628,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         // ---- linearise at v^k -------------------------------------------------------------
         cudaEventRecord(e0, st);
         MPL_CHECK(linearize_impl<T>(ctx, v, LIN_FULL, nullptr));
-        MPL_CUDA(cudaMemsetAsync(slots, 0, slots_needed * (sizeof(CGSlot) + sizeof(unsigned int)), st));
+        MPL_CUDA(cudaMemsetAsync(slots, 0, slots_needed * sizeof(CGSlot), st));
         MPL_CUDA(cudaMemsetAsync(&sc->neg_curv, 0, sizeof(int), st));
         MPL_CUDA(cudaMemsetAsync(&sc->cg_done_iter, 0xff, sizeof(int), st));
         MPL_CUDA(cudaMemsetAsync(p, 0, NT * sizeof(vec4<T>), st));
@@ -761,22 +677,9 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     }
                     if (hvp_events) cudaEventRecord(hev[S.n_hvp].second, st);
                     S.n_hvp++;
-                    if (fused_grid > 0) {  // one rank: both vector updates in one cooperative launch
-                        int64_t na = NA;
-                        int jj_ = jj;
-                        double thr_ = thr;
-                        const vec4<T> *invD_ = invD;
-                        CGSlot *slots_ = slots;
-                        void *args[] = {&na, (void *)&list, &jj_, &thr_, (void *)&invD_, (void *)&p, (void *)&Hp,
-                                        (void *)&x, (void *)&r, (void *)&slots_, (void *)&sc, (void *)&bar};
-                        MPL_CUDA(cudaLaunchCooperativeKernel((const void *)k_pcg_fused<T>, dim3(fused_grid), dim3(256),
-                                                             args, 0, st));
-                        ctx->launches++;
-                    } else {
-                        k_pcg_update1<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc); ctx->launches++;
-                        MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
-                        k_pcg_update2<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, slots, sc); ctx->launches++;
-                    }
+                    k_pcg_update1<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc); ctx->launches++;
+                    MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
+                    k_pcg_update2<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, slots, sc); ctx->launches++;
                 }
                 launched += n;
                 MPL_CUDA(cudaGetLastError());

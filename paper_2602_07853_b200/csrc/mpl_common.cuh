@@ -234,13 +234,14 @@ template <class T> struct KL {
     static constexpr int NCH = 45 / VEC;
     static constexpr int REM = 45 - NCH * VEC;
 };
-// Cell j of a tile is handled by HVP thread (warp j & 1, lane j >> 1), so the two warps of a 64-thread
-// CTA get ceil(ncp/2) and floor(ncp/2) cells; the tangent of cell j is stored at slot
-// kslot(j) = (j & 1) ncp/2 + (j >> 1), so each warp's 16-byte loads are contiguous.
-__host__ __device__ __forceinline__ int kslot(int j, int ncp) { return (j & 1) * (ncp >> 1) + (j >> 1); }
+// Tangent layout per tile: n = the tile's real cells (no padding), block of 45 n reals (rounded up
+// to 4) at t_kstart[t].  Cell j of a tile is handled by HVP thread (warp j & 1, lane j >> 1), so the
+// two warps of a 64-thread CTA get ceil(n/2) and floor(n/2) cells; the tangent of cell j is stored at
+// slot kslot(j) = (j & 1) ceil(n/2) + (j >> 1), so each warp's 16-byte loads are contiguous.
+__host__ __device__ __forceinline__ int kslot(int j, int n) { return (j & 1) * ((n + 1) >> 1) + (j >> 1); }
 // HVP thread -> (cell j, tangent slot)
 __device__ __forceinline__ int hvp_cell(int tid) { return 2 * (tid & 31) + (tid >> 5); }
-__device__ __forceinline__ int hvp_slot(int tid, int ncp) { return (tid >> 5) * (ncp >> 1) + (tid & 31); }
+__device__ __forceinline__ int hvp_slot(int tid, int n) { return (tid >> 5) * ((n + 1) >> 1) + (tid & 31); }
 template <class T> __host__ __device__ __forceinline__ int64_t k_off(int64_t base, int ncp, int j, int e) {
     return e < KL<T>::NCH * KL<T>::VEC
                ? base + ((int64_t)(e / KL<T>::VEC) * ncp + j) * KL<T>::VEC + (e % KL<T>::VEC)
@@ -326,11 +327,12 @@ struct mpl_ctx_s {
     int dense_n = 0;  // nb0*nb1*nb2
     DevBuf cflag, nflag, tile_of, scan_tmp;
     DevBuf t_coord, t_nplus, t_nminus, t_cstart, t_ccount, t_hascells, t_bcount, t_bstart, t_cellof, t_cmask;
+    DevBuf t_ncell, t_kcnt, t_kstart;  // real cells per tile; tangent reals per tile (rounded to 4) and offsets
     DevBuf c_local;
     // quadrature (compact cells)
     DevBuf q_m, q_mv, q_mG, q_slot;  // q_slot: C * nmat * 8 (V, E xx yy zz xy yz xz, pad)
     DevBuf q_vc, q_Gc;               // load: v_c, G_c
-    DevBuf K;                        // C * 45 tangent (scaled by 1/(16 dx^2))
+    DevBuf K;                        // tangent (scaled by 1/(16 dx^2)), per tile at t_kstart, 45 reals per real cell
     // nodes (tile-dense, T*64)
     DevBuf n_mass, n_flag, n_vn, n_vhat, n_v, n_vt, n_g, n_diag, n_invD, n_x, n_r, n_p, n_Hp, n_u, n_u2, n_act;
     // canonical node index per tile-dense node (-1 inactive)
@@ -407,6 +409,9 @@ template <class F> void for_each_buf(mpl_ctx ctx, F f) {
         {"q_vc", ctx->q_vc},
         {"q_Gc", ctx->q_Gc},
         {"K", ctx->K},
+        {"t_ncell", ctx->t_ncell},
+        {"t_kcnt", ctx->t_kcnt},
+        {"t_kstart", ctx->t_kstart},
         {"n_mass", ctx->n_mass},
         {"n_flag", ctx->n_flag},
         {"n_vn", ctx->n_vn},

@@ -15,7 +15,7 @@ from paper_2602_07853_b200 import scenes
 
 
 def make_scene(n=8, lo=2, hi=6, E=1e8, nu=0.3, rho=1000.0, dt=1e-3, prestrain=True, vel=0.3, seed=0,
-               lattice=False, nmat=1, gravity=scenes.GRAVITY, boxes=()):
+               lattice=False, nmat=1, gravity=scenes.GRAVITY, boxes=(), kind=0):
     cells = scenes.cells_box([lo] * 3, [hi] * 3)
     if lattice:  # unjittered: sub-cell centres
         k = 2
@@ -27,7 +27,9 @@ def make_scene(n=8, lo=2, hi=6, E=1e8, nu=0.3, rho=1000.0, dt=1e-3, prestrain=Tr
     v = vel * rng.normal(size=x.shape)
     F = scenes._prestrain(x.shape[0], seed + 3) if prestrain else np.tile(np.eye(3).ravel(), (x.shape[0], 1))
     mat = rng.integers(0, nmat, size=x.shape[0]).astype(np.int32)
-    mats = [scenes.Material(E * (1 + 0.7 * k), nu, rho) for k in range(nmat)]
+    # kind: 0 StVK-Hencky, 1 split Neo-Hookean, "mix": one of each (material slots k = 0, 1)
+    kinds = [k % 2 for k in range(nmat)] if kind == "mix" else [kind] * nmat
+    mats = [scenes.Material(E * (1 + 0.7 * k), nu, rho, kinds[k]) for k in range(nmat)]
     return scenes.Scene(name="t", precision=64, n=(n, n, n), dx=1 / n, dt=dt, materials=mats, x=x, v=v, F=F,
                         G=np.zeros((x.shape[0], 9)), vol=np.full(x.shape[0], (1 / n) ** 3 / 8), mat=mat,
                         dirichlet=list(boxes), solver=scenes.SolverCfg(eps_cg=1e-12, eps_newton=1e-10),
@@ -42,9 +44,9 @@ def elastic_part(prob, g_or_hu, v_or_u, vhat=None):
 
 
 # ------------------------------------------------------------------ C6 derivatives
-@pytest.mark.parametrize("nmat", [1, 2])
-def test_gradient_matches_fd(orc, nmat):
-    sc = make_scene(nmat=nmat)
+@pytest.mark.parametrize("nmat,kind", [(1, 0), (2, 0), (1, 1), (2, "mix")])
+def test_gradient_matches_fd(orc, nmat, kind):
+    sc = make_scene(nmat=nmat, kind=kind)
     un, S, prob, v0 = orc.prepare(sc)
     rng = np.random.default_rng(5)
     act = prob.m_i > 0
@@ -65,9 +67,9 @@ def test_gradient_matches_fd(orc, nmat):
     assert np.linalg.norm(fdel - gel) <= 1e-5 * np.linalg.norm(gel)
 
 
-@pytest.mark.parametrize("nmat", [1, 2])
-def test_hvp_matches_fd_and_is_symmetric(orc, nmat):
-    sc = make_scene(nmat=nmat, seed=2)
+@pytest.mark.parametrize("nmat,kind", [(1, 0), (2, 0), (1, 1), (2, "mix")])
+def test_hvp_matches_fd_and_is_symmetric(orc, nmat, kind):
+    sc = make_scene(nmat=nmat, seed=2, kind=kind)
     un, S, prob, v0 = orc.prepare(sc)
     rng = np.random.default_rng(4)
     act = (prob.m_i > 0)[:, None]
@@ -84,8 +86,9 @@ def test_hvp_matches_fd_and_is_symmetric(orc, nmat):
     assert abs((u * Hw).sum() - (w * Hu).sum()) <= 1e-12 * abs((u * Hw).sum())
 
 
-def test_diag_is_eHe(orc):
-    sc = make_scene(seed=3)
+@pytest.mark.parametrize("kind", [0, 1])
+def test_diag_is_eHe(orc, kind):
+    sc = make_scene(seed=3, kind=kind)
     un, S, prob, v0 = orc.prepare(sc)
     rng = np.random.default_rng(6)
     v = v0 + 0.01 * rng.normal(size=v0.shape) * (prob.m_i > 0)[:, None]
@@ -98,10 +101,11 @@ def test_diag_is_eHe(orc):
             assert D[i, a] == pytest.approx(prob.hvp(v, e)[i, a], rel=1e-12)
 
 
-def test_textbook_linear_hex_stiffness(orc):
+@pytest.mark.parametrize("kind", [0, 1])  # both laws linearise to 2 mu eps + lam tr(eps) I at rest
+def test_textbook_linear_hex_stiffness(orc, kind):
     """At S = I and v = 0 (G = 0, A = I): K_c = dt^2 V C with C:e = 2 mu sym(e) + lam tr(e) I, the
     one-point trilinear-hex linear-elastic stiffness."""
-    sc = make_scene(prestrain=False, vel=0.0, seed=7)
+    sc = make_scene(prestrain=False, vel=0.0, seed=7, kind=kind)
     un, S, prob, v0 = orc.prepare(sc)
     g = prob.grid
     rng = np.random.default_rng(8)
@@ -137,11 +141,12 @@ def test_explicit_force_special_case(orc):
     assert np.abs(f).max() > 0
 
 
-def test_patch_test_affine_zero_interior_force(orc):
+@pytest.mark.parametrize("kind", [0, 1])
+def test_patch_test_affine_zero_interior_force(orc, kind):
     """Constant-strain patch test (north_star): unjittered lattice -> interior V_c = dx^3 exactly;
     uniform F_p -> uniform S; affine v -> zero net elastic force on interior nodes (sum_c grad w_ic = 0)."""
     n = 12
-    sc = make_scene(n=n, lo=2, hi=10, lattice=True, prestrain=False, seed=1)
+    sc = make_scene(n=n, lo=2, hi=10, lattice=True, prestrain=False, seed=1, kind=kind)
     F0 = np.array([[1.05, 0.02, 0.0], [0.01, 0.97, 0.03], [0.0, -0.02, 1.01]])
     sc = dataclasses.replace(sc, F=np.tile(F0.ravel(), (sc.x.shape[0], 1)))
     un, S, prob, v0 = orc.prepare(sc)
@@ -161,13 +166,14 @@ def test_patch_test_affine_zero_interior_force(orc):
     assert np.abs(gel[boundary]).max() > 0
 
 
-def test_rigid_rotation(orc):
+@pytest.mark.parametrize("kind", [0, 1])
+def test_rigid_rotation(orc, kind):
     """v_i = ((R - I)/dt)(x_i - x0) gives G_c = (R - I)/dt exactly, F = R S: with S = I the elastic
     energy and force vanish; with S != I the elastic energy equals that at v = 0 (isotropy)."""
     ang = 0.3
     R = np.array([[np.cos(ang), -np.sin(ang), 0], [np.sin(ang), np.cos(ang), 0], [0, 0, 1.0]])
     for prestrain in (False, True):
-        sc = make_scene(prestrain=prestrain, seed=4)
+        sc = make_scene(prestrain=prestrain, seed=4, kind=kind)
         un, S, prob, v0 = orc.prepare(sc)
         g = prob.grid
         x0 = np.array([0.5, 0.5, 0.5])
@@ -205,11 +211,13 @@ def test_mass_only_limit(orc):
     assert np.allclose(r.v_new[act], r.problem.vhat[act], atol=1e-12)
 
 
-def test_newton_bruteforce_dense(orc):
+@pytest.mark.parametrize("kind", [0, 1])
+def test_newton_bruteforce_dense(orc, kind):
     """Brute force on a tiny grid: dense H from n HVPs is symmetric positive definite; one Newton
     iteration with exact PCG equals v + H^{-1}(-g) (dense Cholesky); the converged step has ||g|| ~ 0
     and the energy decreases at every accepted iterate."""
-    sc = make_scene(n=6, lo=2, hi=4, E=1e7, seed=5, boxes=[scenes.DirichletBox((-1, -1, -1), (2, 2 / 6, 2), (0, 0, 0))])
+    sc = make_scene(n=6, lo=2, hi=4, E=1e7, seed=5, boxes=[scenes.DirichletBox((-1, -1, -1), (2, 2 / 6, 2), (0, 0, 0))],
+                    kind=kind)
     un, S, prob, v0 = orc.prepare(sc)
     fr = np.nonzero(prob.freed)[0]
     assert 0 < len(fr) < np.count_nonzero(prob.m_i)

@@ -228,6 +228,7 @@ def run_ours(args):
         "phase_ms": {"resample": round(statistics.mean(s["ms_phase"][0] for s in stats), 3),
                      "linearize": round(statistics.mean(s["ms_phase"][3] for s in stats), 3),
                      "pcg": round(statistics.mean(s["ms_phase"][4] for s in stats), 3),
+                     "pcg_vector_kernels": round(statistics.mean(s["ms_phase"][1] for s in stats), 3),
                      "line_search": round(statistics.mean(s["ms_phase"][5] for s in stats), 3),
                      "g2p": round(statistics.mean(s["ms_phase"][6] for s in stats), 3)},
         "clocks": clocks,

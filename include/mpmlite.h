@@ -114,8 +114,8 @@ typedef struct {
     int32_t cg_iters[MPL_MAX_NEWTON_LOG];
     int32_t ls_iters[MPL_MAX_NEWTON_LOG];
     int32_t n_hvp;        /* HVP launches in this call                                    */
-    double hvp_ms;        /* summed device time of those HVP launches (CUDA events)       */
-    double ms_phase[8];   /* 0 resample, 3 linearize, 4 PCG, 5 line search, 6 G2P, 7 total (ms)   */
+    double hvp_ms;        /* device time of those HVP launches (CUDA events around every 4th launch, scaled) */
+    double ms_phase[8];   /* 0 resample, 1 PCG vector kernels (MPL_VEC_EVENTS=1), 3 linearize, 4 PCG, 5 line search, 6 G2P, 7 total (ms) */
     int64_t n_cells, n_nodes, n_free_nodes; /* quadrature points, active nodes, free (non-Dirichlet) nodes */
     int64_t n_launches;   /* CUDA kernels launched by the library during this call                */
 } mpl_solve_stats;
@@ -159,7 +159,9 @@ MPL_API mpl_status mpl_get_particle_ids(mpl_ctx ctx, int32_t *ids);
 MPL_API mpl_status mpl_get_node_owner(mpl_ctx ctx, uint8_t *owned);
 
 /* ---- scene -------------------------------------------------------------------------------- */
-/* n <= 8 materials; kind must be 0 (StVK-Hencky).  Requires mu > 0 and lam > -2 mu / 3. */
+/* n <= 8 materials; kind 0 (StVK-Hencky) or 1 (split Neo-Hookean, bulk modulus kappa = 2/3 mu + lam,
+ * P:250).  Requires mu > 0 and lam > -2 mu / 3.  Each material slot of a quadrature point keeps
+ * its own law. */
 MPL_API mpl_status mpl_set_materials(mpl_ctx ctx, int32_t n, const mpl_material *mats);
 /* gravity acceleration g (inertia target vhat = v^n + dt g, amb-4); default (0, -9.81, 0). */
 MPL_API mpl_status mpl_set_gravity(mpl_ctx ctx, const double g[3]);

@@ -134,6 +134,88 @@ __device__ __forceinline__ void hencky_tau(const T F[9], T mu, T lam, T tau[6]) 
     tau[5] = Q[0] * Q[6] * t0 + Q[1] * Q[7] * t1 + Q[2] * Q[8] * t2;
 }
 
+// ---- Kirchhoff stress of a particle, split Neo-Hookean (Eq. split-nh-tau), packed
+template <class T>
+__device__ __forceinline__ void nh_tau(const T F[9], T mu, T kappa, T tau[6]) {
+    T H[9];
+#pragma unroll
+    for (int a = 0; a < 9; a++) H[a] = F[a] - ((a % 4 == 0) ? T(1) : T(0));
+    T B[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++)
+            B[3 * a + b] = H[3 * a + b] + H[3 * b + a] + H[3 * a] * H[3 * b] + H[3 * a + 1] * H[3 * b + 1] +
+                           H[3 * a + 2] * H[3 * b + 2];
+    const T jm1 = det_ipm1(H);
+    const T j23 = mexpm1(T(-2.0 / 3.0) * mlog1p(jm1));  // J^{-2/3} - 1
+    const T trB3 = (B[0] + B[4] + B[8]) / T(3);
+    const T s = mu * (T(1) + j23), al = T(0.5) * kappa * jm1 * (T(2) + jm1);
+    tau[0] = s * (B[0] - trB3) + al;
+    tau[1] = s * (B[4] - trB3) + al;
+    tau[2] = s * (B[8] - trB3) + al;
+    tau[3] = s * B[1];
+    tau[4] = s * B[5];
+    tau[5] = s * B[2];
+}
+
+// ---- split Neo-Hookean stretch reconstruction (App. C), in fp64 -------
+// tau = U diag(tau_i) U^T; alpha = tr/3; J = sqrt(1 + 2 alpha / kappa); s = mu J^{-2/3};
+// delta_i = (tau_i - alpha)/s; m solves m^3 + S2 m + (S3 - J^2) = 0 on the branch m > -min delta
+// (Cardano, Vieta form of the one-real-root case, Newton-polished); beta_i = m + delta_i;
+// returns E = S - I = U diag(sqrt(beta_i) - 1) U^T.  false outside the inversion domain.
+__device__ __forceinline__ double cbrt_s(double z) { return cbrt(z); }
+__device__ bool nh_stretch_E(const double tau[6], double mu, double kappa, double E[6]) {
+    double A[9] = {tau[0], tau[3], tau[5], tau[3], tau[1], tau[4], tau[5], tau[4], tau[2]};
+    double w[3], U[9];
+    sym_eig3(A, w, U);
+    const double alpha = (w[0] + w[1] + w[2]) / 3.0;
+    const double J2m1 = 2.0 * alpha / kappa;  // J^2 - 1
+    if (!(J2m1 > -1.0)) return false;
+    const double J2 = 1.0 + J2m1, J = sqrt(J2);
+    const double s = mu * exp(-log1p(J2m1) / 3.0);  // mu J^{-2/3}
+    double d[3];
+    for (int i = 0; i < 3; i++) d[i] = (w[i] - alpha) / s;
+    const double p = d[0] * d[1] + d[1] * d[2] + d[2] * d[0], q = d[0] * d[1] * d[2] - J2;
+    const double dmin = fmin(d[0], fmin(d[1], d[2]));
+    const double D = 0.25 * q * q + p * p * p / 27.0;
+    double m;
+    if (D >= 0.0) {
+        const double u = cbrt_s(-0.5 * q + (q <= 0.0 ? sqrt(D) : -sqrt(D)));
+        m = u != 0.0 ? u - p / (3.0 * u) : 0.0;
+    } else {
+        const double r = 2.0 * sqrt(-p / 3.0);
+        double arg = (1.5 * q / p) * sqrt(-3.0 / p);
+        arg = fmin(1.0, fmax(-1.0, arg));
+        const double th = acos(arg) / 3.0;
+        m = -1e300;
+        for (int k = 0; k < 3; k++) {
+            const double mk = r * cos(th - 2.0943951023931953 * k);
+            if (mk > -dmin && mk > m) m = mk;
+        }
+    }
+    for (int it = 0; it < 3; it++) {  // Newton polish on the same cubic
+        const double f = m * m * m + p * m + q, df = 3.0 * m * m + p;
+        if (!(fabs(df) > 1e-300)) break;
+        const double mn = m - f / df;
+        if (!(mn > -dmin)) break;
+        m = mn;
+    }
+    double em[3];
+    for (int i = 0; i < 3; i++) {
+        const double beta = m + d[i];
+        if (!(beta > 0.0)) return false;
+        em[i] = (beta - 1.0) / (sqrt(beta) + 1.0);  // sigma_i - 1
+    }
+    E[0] = U[0] * U[0] * em[0] + U[1] * U[1] * em[1] + U[2] * U[2] * em[2];
+    E[1] = U[3] * U[3] * em[0] + U[4] * U[4] * em[1] + U[5] * U[5] * em[2];
+    E[2] = U[6] * U[6] * em[0] + U[7] * U[7] * em[1] + U[8] * U[8] * em[2];
+    E[3] = U[0] * U[3] * em[0] + U[1] * U[4] * em[1] + U[2] * U[5] * em[2];
+    E[4] = U[3] * U[6] * em[0] + U[4] * U[7] * em[1] + U[5] * U[8] * em[2];
+    E[5] = U[0] * U[6] * em[0] + U[1] * U[7] * em[1] + U[2] * U[8] * em[2];
+    return true;
+}
+
 // ---- particle scatter into sorted order + P2Q record ------------------------------------------
 // record (24 reals): f(3) fraction in the base cell, m_p, a = m_p (v_p - dx G_p f) (3),
 // m_p G_p (9), V_p, V_p tau_p (6), material id (as real)
@@ -162,7 +244,8 @@ __global__ void k_scatter(GridP g, MatP mp, int64_t np, const int *__restrict__ 
     T mu = T(mp.mu[m]), lam = T(mp.lam[m]);
     T mass = T(mp.rho[m]) * Vp;
     T tau[6];
-    hencky_tau(Fp, mu, lam, tau);
+    if (mp.kind[m] == 1) nh_tau(Fp, mu, T(mp.kappa[m]), tau);  // Alg. 2 line 3, per-material law
+    else hencky_tau(Fp, mu, lam, tau);
     T f[3];
 #pragma unroll
     for (int a = 0; a < 3; a++) {
@@ -253,7 +336,7 @@ __global__ void __launch_bounds__(64) k_p2q(GridP g, MatP mp, const int *__restr
                                             const int *__restrict__ nminus, const int *__restrict__ bstart,
                                             const int *__restrict__ cellof, const T *__restrict__ rec,
                                             T *__restrict__ q_m, T *__restrict__ q_mv, T *__restrict__ q_mG,
-                                            T *__restrict__ q_slot) {
+                                            T *__restrict__ q_slot, DevScalars *sc) {
     int t = blockIdx.x;
     int l = threadIdx.x;
     int cc = cellof[t * 64 + l];
@@ -315,7 +398,22 @@ __global__ void __launch_bounds__(64) k_p2q(GridP g, MatP mp, const int *__restr
         T *sl = q_slot + ((int64_t)cc * nmat + k) * 16;
         T tau[6] = {0, 0, 0, 0, 0, 0};
         T E[6] = {0, 0, 0, 0, 0, 0};
-        if (V[k] != T(0)) {
+        if (V[k] != T(0) && mp.kind[k] == 1) {
+            T iv = T(1) / V[k];
+#pragma unroll
+            for (int a = 0; a < 6; a++) tau[a] = Vt[k][a] * iv;  // Eq. vtau normalisation
+            double td[6], Ed[6];
+#pragma unroll
+            for (int a = 0; a < 6; a++) td[a] = (double)tau[a];
+            if (nh_stretch_E(td, mp.mu[k], mp.kappa[k], Ed)) {
+#pragma unroll
+                for (int a = 0; a < 6; a++) E[a] = T(Ed[a]);
+            } else {
+#pragma unroll
+                for (int a = 0; a < 6; a++) E[a] = T(0);
+                sc->nonfinite = 1;  // outside the inversion domain (reported by resample)
+            }
+        } else if (V[k] != T(0)) {
             T iv = T(1) / V[k];
 #pragma unroll
             for (int a = 0; a < 6; a++) tau[a] = Vt[k][a] * iv;  // Eq. vtau normalisation
@@ -688,7 +786,8 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     DBG_GUARDS("resample #8");
         k_p2q<T><<<T_, 64, 0, st>>>(g, ctx->mats, (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p,
                                     (const int *)ctx->t_bstart.p, (const int *)ctx->t_cellof.p, (const T *)ctx->prec.p,
-                                    (T *)ctx->q_m.p, (T *)ctx->q_mv.p, (T *)ctx->q_mG.p, (T *)ctx->q_slot.p); ctx->launches++;
+                                    (T *)ctx->q_m.p, (T *)ctx->q_mv.p, (T *)ctx->q_mG.p, (T *)ctx->q_slot.p, sc);
+        ctx->launches++;
     DBG_GUARDS("resample #9");
     }
     // nodes
@@ -742,6 +841,17 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     ctx->n_nodes_active = nact;
     MPL_CUDA(cudaGetLastError());
     MPL_CUDA(cudaStreamSynchronize(st));
+    {
+        int nf = 0;
+        MPL_CUDA(cudaMemcpy(&nf, &sc->nonfinite, sizeof nf, cudaMemcpyDeviceToHost));
+        mpl_status bad2 = MPL_OK;
+        if (nf) {
+            ctx->err = "a quadrature stress lies outside the split Neo-Hookean inversion domain "
+                       "(1 + 2 tr(tau) / (3 kappa) <= 0 or no admissible stretch; P:268, App. C)";
+            bad2 = MPL_ERR_INVERSION_DOMAIN;
+        }
+        MPL_CHECK(agree(ctx, bad2));
+    }
 #ifdef MPL_DEBUG
     MPL_CHECK(debug_check_tiles(ctx, "end of resample"));
 #endif

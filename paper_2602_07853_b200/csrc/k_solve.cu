@@ -127,6 +127,75 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
                         B[3 * a + b] = val;
                         B[3 * b + a] = val;
                     }
+                if (mp.kind[k] == 1) {
+                    // ---- split Neo-Hookean slot (PAPER §4.3.2; stable forms in mpl_common.cuh) ----
+                    const T kap = T(mp.kappa[k]);
+                    const T jm1 = det_ipm1(H), j23 = mexpm1(T(-2.0 / 3.0) * mlog1p(jm1));
+                    const T trB = B[0] + B[4] + B[8];
+                    const T psi = T(0.5) * mu * (T(3) * j23 + trB * (T(1) + j23)) + T(0.25) * kap * nh_f(jm1);
+                    e_loc += (double)(V * psi);
+                    if (MODE == LIN_ENERGY) continue;
+                    const T sdev = mu * (T(1) + j23), al = T(0.5) * kap * jm1 * (T(2) + jm1);
+                    T devB[9], tau[9];
+#pragma unroll
+                    for (int a = 0; a < 9; a++) {
+                        devB[a] = B[a] - ((a % 4 == 0) ? trB / T(3) : T(0));
+                        tau[a] = sdev * devB[a] + ((a % 4 == 0) ? al : T(0));
+                    }
+                    T TA[9];  // tau A^{-T}
+                    mm3(tau, AiT, TA);
+                    const T sV = dt * V;
+#pragma unroll
+                    for (int a = 0; a < 9; a++) Pc[a] += sV * TA[a];
+                    if (MODE == LIN_FULL) {
+                        // column (a,b) of the tangent: dF = dt e_a (x) S[b,:] (dG = e_a e_b^T), so
+                        //   dJ = J dt (F^{-T} S)[a][b], db = dt (e_a y_b^T + y_b e_a^T), y_b = (F S)[:, b],
+                        //   dtau = mu J^{-2/3} (-2/3 dJ/J dev(b) + dev(db)) + kappa J dJ I.
+                        T F[9], S[9], FS[9], FiT[9], M[9];
+#pragma unroll
+                        for (int a = 0; a < 9; a++) {
+                            F[a] = H[a] + ((a % 4 == 0) ? T(1) : T(0));
+                            S[a] = E[a] + ((a % 4 == 0) ? T(1) : T(0));
+                        }
+                        mm3(F, S, FS);
+                        inv_transpose3(F, FiT);
+                        mm3(FiT, S, M);
+                        const T Jv = T(1) + jm1;
+                        const T kscale = sV * T(1.0 / 16.0) * T(g.inv_dx * g.inv_dx);
+                        T *Kr = Ks + j * 45;
+#pragma unroll
+                        for (int a = 0; a < 3; a++)
+#pragma unroll
+                            for (int b = 0; b < 3; b++) {
+                                const T dJ_J = dt * M[3 * a + b];  // dJ / J
+                                const T tdb3 = T(2.0 / 3.0) * dt * FS[3 * a + b];
+                                T dtau[9];
+#pragma unroll
+                                for (int i = 0; i < 3; i++)
+#pragma unroll
+                                    for (int jj = 0; jj < 3; jj++) {
+                                        T db = dt * ((i == a ? FS[3 * jj + b] : T(0)) + (jj == a ? FS[3 * i + b] : T(0)));
+                                        if (i == jj) db -= tdb3;  // dev(db)
+                                        dtau[3 * i + jj] = sdev * (T(-2.0 / 3.0) * dJ_J * devB[3 * i + jj] + db) +
+                                                           ((i == jj) ? kap * Jv * Jv * dJ_J : T(0));
+                                    }
+                                const int cidx = 3 * a + b;
+#pragma unroll
+                                for (int i = 0; i < 3; i++)
+#pragma unroll
+                                    for (int jj = 0; jj < 3; jj++) {
+                                        T r1 = dtau[3 * i] * AiT[jj] + dtau[3 * i + 1] * AiT[3 + jj] + dtau[3 * i + 2] * AiT[6 + jj];
+                                        T r2 = -dt * TA[3 * i + b] * AiT[3 * a + jj];
+                                        T val = kscale * (r1 + r2);
+                                        const int r = 3 * i + jj;
+                                        if (r == cidx) Kr[kidx(r, r)] += val;
+                                        else if (r < cidx) Kr[kidx(r, cidx)] += T(0.5) * val;
+                                        else Kr[kidx(cidx, r)] += T(0.5) * val;
+                                    }
+                            }
+                    }
+                    continue;
+                }
                 T lam3[3], Q[9];
                 sym_eig3(B, lam3, Q);
                 T l0 = mlog1p(lam3[0]), l1 = mlog1p(lam3[1]), l2 = mlog1p(lam3[2]);
@@ -582,6 +651,8 @@ mpl_status energy_at(mpl_ctx ctx, const void *v_tile, double *phi) {
 }
 }  // namespace
 
+constexpr int HVP_SAMPLE = 4;
+
 template <class T>
 mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *out) {
     cudaStream_t st = ctx->stream;
@@ -613,9 +684,14 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> hev;
-    // per-HVP device timing (stats.hvp_ms); MPL_HVP_EVENTS=0 drops the two events per HVP
+    // per-HVP device timing (stats.hvp_ms): CUDA events around every HVP_SAMPLE-th HVP launch (the
+    // events cost ~4 us each inside the PCG loop); MPL_HVP_EVENTS=0 drops them
     const char *hve = getenv("MPL_HVP_EVENTS");
     const bool hvp_events = !(hve && hve[0] == '0');
+    // MPL_VEC_EVENTS=1: also time the PCG vector kernels (stats.ms_phase[1])
+    const char *vee = getenv("MPL_VEC_EVENTS");
+    const bool vec_events = vee && vee[0] == '1';
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> vev;
     double t_lin = 0, t_pcg = 0, t_ls = 0;
     auto elapsed = [&](cudaEvent_t a, cudaEvent_t b) {
         float ms = 0;
@@ -667,19 +743,27 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                         cudaEventCreate(&a);
                         cudaEventCreate(&b);
                         hev.push_back({a, b});
+                        if (vec_events) {
+                            cudaEventCreate(&a);
+                            cudaEventCreate(&b);
+                            vev.push_back({a, b});
+                        }
                     }
-                    if (hvp_events) cudaEventRecord(hev[S.n_hvp].first, st);
+                    const bool timed = hvp_events && (S.n_hvp % HVP_SAMPLE == 0);
+                    if (timed) cudaEventRecord(hev[S.n_hvp].first, st);
                     // the HVP is skipped on device once converged (its output is then unused)
                     MPL_CHECK(launch_hvp<T>(ctx, p, Hp, slots[jj].pHp, slots, jj, thr));
                     if (multi(ctx)) {  // complete Hp on the shared planes; global p.Hp (timed with the HVP)
                         MPL_CHECK(halo_sum_nodes<T>(ctx, Hp, nullptr));
                         MPL_CHECK(allreduce_d(ctx, slots[jj].pHp, NSTRIPE));
                     }
-                    if (hvp_events) cudaEventRecord(hev[S.n_hvp].second, st);
+                    if (timed) cudaEventRecord(hev[S.n_hvp].second, st);
                     S.n_hvp++;
+                    if (vec_events) cudaEventRecord(vev[S.n_hvp - 1].first, st);
                     k_pcg_update1<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc); ctx->launches++;
                     MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
                     k_pcg_update2<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, slots, sc); ctx->launches++;
+                    if (vec_events) cudaEventRecord(vev[S.n_hvp - 1].second, st);
                 }
                 launched += n;
                 MPL_CUDA(cudaGetLastError());
@@ -761,8 +845,19 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     }
     MPL_CHECK(energy_at<T>(ctx, v, &S.energy));
     double hsum = 0;
-    if (hvp_events)
-        for (int i = 0; i < S.n_hvp; i++) hsum += elapsed(hev[i].first, hev[i].second);
+    if (hvp_events && S.n_hvp > 0) {  // every HVP_SAMPLE-th launch is timed; scaled to all launches
+        int ns = 0;
+        for (int i = 0; i < S.n_hvp; i += HVP_SAMPLE, ns++) hsum += elapsed(hev[i].first, hev[i].second);
+        hsum *= (double)S.n_hvp / ns;
+    }
+    double vsum = 0;
+    if (vec_events)
+        for (int i = 0; i < S.n_hvp; i++) vsum += elapsed(vev[i].first, vev[i].second);
+    for (auto &pr : vev) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
+    S.ms_phase[1] = vsum;
     for (auto &pr : hev) {
         cudaEventDestroy(pr.first);
         cudaEventDestroy(pr.second);

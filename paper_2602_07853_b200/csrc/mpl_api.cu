@@ -292,17 +292,20 @@ mpl_status mpl_set_materials(mpl_ctx ctx, int32_t n, const mpl_material *mats) {
     if (!ctx || !mats || n < 1 || n > MPL_MAXMAT) return MPL_ERR_INVALID_ARG;
     for (int k = 0; k < n; k++) {
         const mpl_material &m = mats[k];
-        if (m.kind != 0) {
-            ctx->err = "only StVK-Hencky (kind 0) is implemented";
+        if (m.kind != 0 && m.kind != 1) {
+            ctx->err = "material kind must be 0 (StVK-Hencky) or 1 (split Neo-Hookean)";
             return MPL_ERR_UNSUPPORTED;
         }
         double mu = m.E / (2.0 * (1.0 + m.nu)), lam = m.E * m.nu / ((1.0 + m.nu) * (1.0 - 2.0 * m.nu));
+        // both laws need mu > 0 and kappa = 2/3 mu + lam > 0 (P:227 for Hencky; P:268 J = sqrt(1 + 2 alpha/kappa))
         if (!(mu > 0) || !(lam > -2.0 * mu / 3.0) || !(m.rho > 0)) {
             ctx->err = "material " + std::to_string(k) + ": need mu > 0, lam > -2mu/3, rho > 0 (P:227)";
             return MPL_ERR_INVALID_ARG;
         }
+        ctx->mats.kind[k] = m.kind;
         ctx->mats.mu[k] = mu;
         ctx->mats.lam[k] = lam;
+        ctx->mats.kappa[k] = 2.0 * mu / 3.0 + lam;
         ctx->mats.rho[k] = m.rho;
     }
     ctx->mats.nmat = n;

@@ -71,7 +71,8 @@ struct GridP {
 
 struct MatP {
     int nmat;
-    double mu[MPL_MAXMAT], lam[MPL_MAXMAT], rho[MPL_MAXMAT];
+    int kind[MPL_MAXMAT];  // 0 StVK-Hencky, 1 split Neo-Hookean
+    double mu[MPL_MAXMAT], lam[MPL_MAXMAT], rho[MPL_MAXMAT], kappa[MPL_MAXMAT];  // kappa = 2/3 mu + lam
 };
 
 struct BoxP {
@@ -178,6 +179,26 @@ template <class T> __device__ __forceinline__ T dlog(T lx, T ly) {
     const T thr = sizeof(T) == 4 ? T(2e-2) : T(1e-3);
     if (mabs(t) < thr) return (T(1) + t * (T(-0.5) + t * (T(1) / T(3) + t * (T(-0.25) + t * T(0.2))))) / y;
     return mlog1p(t) / (lx - ly);
+}
+
+// ---- split Neo-Hookean (PAPER §4.3.2) in forms that keep fp32 accurate at small strain:
+// with H = F - I and Bm = b - I = H + H^T + H H^T,
+//   J - 1 = tr H + (tr(H)^2 - tr(H^2))/2 + det H,   J^{-2/3} - 1 = expm1(-2/3 log1p(J - 1)),
+//   tau = mu J^{-2/3} dev(Bm) + kappa/2 (J-1)(J+1) I                      (Eq. split-nh-tau),
+//   Psi = mu/2 (3 (J^{-2/3}-1) + tr(Bm) J^{-2/3}) + kappa/4 f(J-1),
+//   f(x) = x (2 + x) - 2 log1p(x)                                         (Eq. split-nh-energy).
+template <class T> __device__ __forceinline__ T det_ipm1(const T H[9]) {  // det(I + H) - 1
+    const T tr = H[0] + H[4] + H[8];
+    const T tr2 = H[0] * H[0] + H[4] * H[4] + H[8] * H[8] + T(2) * (H[1] * H[3] + H[2] * H[6] + H[5] * H[7]);
+    return tr + T(0.5) * (tr * tr - tr2) + det3(H);
+}
+template <class T> __device__ __forceinline__ T nh_f(T x) {  // x (2 + x) - 2 log1p(x), series near 0
+    // the series (truncation ~x^8/4) replaces the cancelling direct form below |x| = 0.1 (fp32) / 1e-3 (fp64)
+    if (mabs(x) < (sizeof(T) == 4 ? T(0.1) : T(1e-3))) {
+        // 2 x^2 - 2/3 x^3 + 1/2 x^4 - 2/5 x^5 + 1/3 x^6 - 2/7 x^7
+        return x * x * (T(2) + x * (T(-2.0 / 3.0) + x * (T(0.5) + x * (T(-0.4) + x * (T(1.0 / 3.0) + x * T(-2.0 / 7.0))))));
+    }
+    return x * (T(2) + x) - T(2) * mlog1p(x);
 }
 
 // symmetric 9x9 upper-triangle packing: row r (r = 3a+b) stores s = r..8

@@ -265,7 +265,7 @@ class Context:
     def set_materials(self, materials):
         arr = (Material * len(materials))()
         for k, m in enumerate(materials):
-            arr[k].kind, arr[k].E, arr[k].nu, arr[k].rho = 0, float(m.E), float(m.nu), float(m.rho)
+            arr[k].kind, arr[k].E, arr[k].nu, arr[k].rho = int(getattr(m, "kind", 0)), float(m.E), float(m.nu), float(m.rho)
         self._chk(_lib.mpl_set_materials(self._h, len(materials), arr), "mpl_set_materials")
         self.nmat = len(materials)
 

@@ -27,8 +27,9 @@ def small_cfg2(precision=32, k=16):
                             scenes.SolverCfg(eps_cg=tol[0], eps_newton=tol[1], ls_slack=1e-13 if precision == 64 else 1e-6), 1)
 
 
-def two_material(precision=64):
-    """Two materials mixed in the same cells + a sticky floor (exercises slots and Dirichlet)."""
+def two_material(precision=64, kinds=(0, 0)):
+    """Two materials mixed in the same cells + a sticky floor (exercises slots and Dirichlet); kinds
+    selects each material's law (0 StVK-Hencky, 1 split Neo-Hookean)."""
     n = 16
     cells = scenes.cells_box([4, 2, 4], [12, 10, 12])
     dt_ = np.float32 if precision == 32 else np.float64
@@ -40,7 +41,8 @@ def two_material(precision=64):
     floor = scenes.DirichletBox((-1e9, -1e9, -1e9), (1e9, 3 / n, 1e9), (0.0, 0.0, 0.0))
     tol = (1e-8, 1e-9) if precision == 64 else (1e-5, 1e-5)
     return scenes._assemble("mix", precision, n, 1e-3,
-                            [scenes.Material(1e5, 0.3, 1000.0), scenes.Material(3e6, 0.45, 2500.0)], x, v, F,
+                            [scenes.Material(1e5, 0.3, 1000.0, kinds[0]), scenes.Material(3e6, 0.45, 2500.0, kinds[1])],
+                            x, v, F,
                             np.zeros((x.shape[0], 9)), mat, 8, [floor],
                             scenes.SolverCfg(eps_cg=tol[0], eps_newton=tol[1]), 1)
 
@@ -53,6 +55,11 @@ SCENES = {
     "cfg2s_fp64": lambda: small_cfg2(64),
     "mix_fp64": lambda: two_material(64),
     "mix_fp32": lambda: two_material(32),
+    # split Neo-Hookean: alone (pre-strained cube) and mixed with StVK-Hencky in the same cells
+    "nh_fp64": lambda: dataclasses.replace(scenes.cfg1(prestrain=True),
+                                           materials=[scenes.Material(1e4, 0.3, 1000.0, 1)]),
+    "lawmix_fp64": lambda: two_material(64, (0, 1)),
+    "lawmix_fp32": lambda: two_material(32, (1, 0)),
 }
 
 

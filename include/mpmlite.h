@@ -113,9 +113,9 @@ typedef struct {
     double grad_norm0, grad_norm, energy;
     int32_t cg_iters[MPL_MAX_NEWTON_LOG];
     int32_t ls_iters[MPL_MAX_NEWTON_LOG];
-    int32_t n_hvp;        /* HVP launches in this call                                    */
+    int32_t n_hvp;        /* HVPs executed in this call (= PCG iterations; launches past convergence exit at once) */
     double hvp_ms;        /* device time of those HVP launches (CUDA events around every 4th launch, scaled) */
-    double ms_phase[8];   /* 0 resample, 1 PCG vector kernels (MPL_VEC_EVENTS=1), 3 linearize, 4 PCG, 5 line search, 6 G2P, 7 total (ms) */
+    double ms_phase[8];   /* 0 resample, 1 PCG vector kernels (MPL_VEC_EVENTS=1), 2 explicit update, 3 linearize, 4 PCG, 5 line search, 6 G2P, 7 total (ms) */
     int64_t n_cells, n_nodes, n_free_nodes; /* quadrature points, active nodes, free (non-Dirichlet) nodes */
     int64_t n_launches;   /* CUDA kernels launched by the library during this call                */
 } mpl_solve_stats;
@@ -141,6 +141,9 @@ MPL_API mpl_status mpl_nccl_unique_id(uint8_t out[128]);
  * step particles that left the slab migrate to the neighbour (more than one slab per step is
  * MPL_ERR_OUT_OF_DOMAIN) and the last owned cell plane is copied to the upper neighbour as ghosts.
  * A failing collective returns an error on every rank. */
+/* One-rank self-test of the NCCL transport on `device` (unique id, communicator, allreduce, grouped
+ * send / receive); *out_sum = 8.0 on success.  MPL_ERR_NCCL if libnccl.so.2 cannot be used. */
+MPL_API mpl_status mpl_nccl_selftest(int32_t device, double *out_sum);
 MPL_API mpl_status mpl_group_create(int32_t nranks, mpl_group *out);
 MPL_API void mpl_group_destroy(mpl_group g);
 /* cuts: nranks + 1 strictly increasing cell-block x indices, cuts[0] = 0, cuts[nranks] =
@@ -229,6 +232,15 @@ MPL_API mpl_status mpl_set_velocity(mpl_ctx ctx, const void *v);
 /* Alg. 4: v_c = sum w_ic v_i, G_c = sum v_i (x) grad w_ic (cells with m_c > 0); v_p = sum w_cp v_c,
  * G_p = sum w_cp G_c (weights at x_p^n); x_p += dt v_p; F_p <- (I + dt G_p) F_p. */
 MPL_API mpl_status mpl_transfer_to_particles(mpl_ctx ctx, double dt);
+
+/* ---- explicit integration (Eq. explicitforce; Alg. 3 lines 1-3) -- */
+/* After mpl_resample: f_i = -sum_{c,k} V_ck tau_ck grad w_ic and v^{n+1} = v^n + dt (g + f_i / m_i) on
+ * free nodes (prescribed nodes keep their Dirichlet value); v^{n+1} is then read by
+ * mpl_get_velocity / mpl_transfer_to_particles.  Collective on slab ranks (force halo sum). */
+MPL_API mpl_status mpl_explicit_velocity(mpl_ctx ctx);
+/* One explicit step: resample -> explicit velocity -> transfer.  stats (may be NULL): ms_phase[0]
+ * resample, [2] explicit update, [6] transfer, [7] total; counts as for mpl_step. */
+MPL_API mpl_status mpl_explicit_step(mpl_ctx ctx, double dt, mpl_solve_stats *stats);
 
 /* One full step: resample -> newton -> transfer (Alg. 1). */
 MPL_API mpl_status mpl_step(mpl_ctx ctx, double dt, const mpl_solver_cfg *cfg, mpl_solve_stats *stats);

@@ -439,6 +439,146 @@ __global__ void __launch_bounds__(64) k_p2q(GridP g, MatP mp, const int *__restr
     }
 }
 
+// ---- a2-a4, parallel form (default): 8 lanes per cell --------------------------------------------
+// Lane o of a cell's 8-lane group gathers the base-cell bucket c - o (the particles whose stencil
+// corner o is this cell); the 8 partial sums are combined with shuffles inside the aligned group;
+// lane k then reconstructs material slot k's stretch (Eqs. hencky-ei/sigmai, or the split
+// Neo-Hookean inversion) — the slots of a cell in parallel.  256 threads = half a tile (32 cells).
+template <class T>
+__device__ __forceinline__ T grp_sum(T v) {  // sum over the aligned 8-lane group
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    return v;
+}
+
+template <class T>
+__device__ __forceinline__ void stretch_slot(const MatP &mp, int k, const T tau[6], T E[6], DevScalars *sc) {
+    if (mp.kind[k] == 1) {
+        double td[6], Ed[6];
+#pragma unroll
+        for (int a = 0; a < 6; a++) td[a] = (double)tau[a];
+        if (nh_stretch_E(td, mp.mu[k], mp.kappa[k], Ed)) {
+#pragma unroll
+            for (int a = 0; a < 6; a++) E[a] = T(Ed[a]);
+        } else {
+#pragma unroll
+            for (int a = 0; a < 6; a++) E[a] = T(0);
+            sc->nonfinite = 1;  // outside the inversion domain (reported by resample)
+        }
+        return;
+    }
+    const T mu = T(mp.mu[k]), lam = T(mp.lam[k]);
+    T A[9] = {tau[0], tau[3], tau[5], tau[3], tau[1], tau[4], tau[5], tau[4], tau[2]};
+    T w[3], U[9];
+    sym_eig3(A, w, U);
+    const T s = (w[0] + w[1] + w[2]) / (T(2) * mu + T(3) * lam);  // Eq. hencky-trace
+    T em[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) em[i] = mexpm1((w[i] - lam * s) / (T(2) * mu));  // sigma_i - 1
+    E[0] = U[0] * U[0] * em[0] + U[1] * U[1] * em[1] + U[2] * U[2] * em[2];
+    E[1] = U[3] * U[3] * em[0] + U[4] * U[4] * em[1] + U[5] * U[5] * em[2];
+    E[2] = U[6] * U[6] * em[0] + U[7] * U[7] * em[1] + U[8] * U[8] * em[2];
+    E[3] = U[0] * U[3] * em[0] + U[1] * U[4] * em[1] + U[2] * U[5] * em[2];
+    E[4] = U[3] * U[6] * em[0] + U[4] * U[7] * em[1] + U[5] * U[8] * em[2];
+    E[5] = U[0] * U[6] * em[0] + U[1] * U[7] * em[1] + U[2] * U[8] * em[2];
+}
+
+template <class T, int NM>  // NM >= mp.nmat: register arrays sized for NM material slots
+__global__ void __launch_bounds__(256) k_p2q8(GridP g, MatP mp, const int *__restrict__ coord,
+                                              const int *__restrict__ nminus, const int *__restrict__ bstart,
+                                              const int *__restrict__ cellof, const T *__restrict__ rec,
+                                              T *__restrict__ q_m, T *__restrict__ q_mv, T *__restrict__ q_mG,
+                                              T *__restrict__ q_slot, DevScalars *sc) {
+    const int t = blockIdx.x >> 1;
+    const int l = ((blockIdx.x & 1) << 5) | (threadIdx.x >> 3), o = threadIdx.x & 7;
+    const int cc = cellof[t * 64 + l];
+    const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+    const int cx = coord[3 * t] * 4 + lx, cy = coord[3 * t + 1] * 4 + ly, cz = coord[3 * t + 2] * 4 + lz;
+    const int nmat = mp.nmat;
+    const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+    T m = 0, mv[3] = {0, 0, 0}, mG[9];
+#pragma unroll
+    for (int a = 0; a < 9; a++) mG[a] = 0;
+    T V[NM], Vt[NM][6];
+#pragma unroll
+    for (int k = 0; k < NM; k++) {
+        V[k] = 0;
+#pragma unroll
+        for (int a = 0; a < 6; a++) Vt[k][a] = 0;
+    }
+    if (cc >= 0 && cx - ox >= 0 && cy - oy >= 0 && cz - oz >= 0) {
+        const int bx = lx - ox, by = ly - oy, bz = lz - oz;
+        const int dm = ((bx < 0) << 2) | ((by < 0) << 1) | (bz < 0);
+        const int tt = nminus[8 * t + dm];
+        if (tt >= 0) {
+            const int kk = tt * 64 + local_id(bx & 3, by & 3, bz & 3);
+            const int s0 = bstart[kk], e0 = bstart[kk + 1];
+            const T dx = T(g.dx);
+            for (int p = s0; p < e0; p++) {
+                const T *r = rec + (int64_t)p * REC;
+                // cell = base + o  =>  w = prod_a (o_a ? f_a : 1 - f_a)
+                const T w = (ox ? r[0] : T(1) - r[0]) * (oy ? r[1] : T(1) - r[1]) * (oz ? r[2] : T(1) - r[2]);
+                m += w * r[3];
+                // m (v + G (x_c - x_p)) = a + dx (mG) o   (x_c - x_p = dx (o - f))
+                mv[0] += w * (r[4] + dx * ((ox ? r[7] : T(0)) + (oy ? r[8] : T(0)) + (oz ? r[9] : T(0))));
+                mv[1] += w * (r[5] + dx * ((ox ? r[10] : T(0)) + (oy ? r[11] : T(0)) + (oz ? r[12] : T(0))));
+                mv[2] += w * (r[6] + dx * ((ox ? r[13] : T(0)) + (oy ? r[14] : T(0)) + (oz ? r[15] : T(0))));
+#pragma unroll
+                for (int a = 0; a < 9; a++) mG[a] += w * r[7 + a];
+                const int k = (int)r[23];
+#pragma unroll
+                for (int q = 0; q < NM; q++) {
+                    if (q == k) {
+                        V[q] += w * r[16];
+#pragma unroll
+                        for (int a = 0; a < 6; a++) Vt[q][a] += w * r[17 + a];
+                    }
+                }
+            }
+        }
+    }
+    // combine the 8 source buckets of the cell (inactive groups carry zeros and write nothing)
+    m = grp_sum(m);
+#pragma unroll
+    for (int a = 0; a < 3; a++) mv[a] = grp_sum(mv[a]);
+#pragma unroll
+    for (int a = 0; a < 9; a++) mG[a] = grp_sum(mG[a]);
+#pragma unroll
+    for (int q = 0; q < NM; q++) {
+        if (q >= nmat) break;  // uniform
+        V[q] = grp_sum(V[q]);
+#pragma unroll
+        for (int a = 0; a < 6; a++) Vt[q][a] = grp_sum(Vt[q][a]);
+    }
+    if (cc < 0) return;
+    if (o == 0) {
+        q_m[cc] = m;
+#pragma unroll
+        for (int a = 0; a < 3; a++) q_mv[3 * (int64_t)cc + a] = mv[a];
+    }
+    if (o == 1)
+#pragma unroll
+        for (int a = 0; a < 9; a++) q_mG[9 * (int64_t)cc + a] = mG[a];
+    // material slot k on lane k (nmat <= 8)
+#pragma unroll
+    for (int q = 0; q < NM; q++) {
+        if (q != o || q >= nmat) continue;
+        T *sl = q_slot + ((int64_t)cc * nmat + q) * 16;
+        T tau[6] = {0, 0, 0, 0, 0, 0}, E[6] = {0, 0, 0, 0, 0, 0};
+        if (V[q] != T(0)) {
+            const T iv = T(1) / V[q];
+#pragma unroll
+            for (int a = 0; a < 6; a++) tau[a] = Vt[q][a] * iv;  // Eq. vtau normalisation
+            stretch_slot<T>(mp, q, tau, E, sc);
+        }
+        sl[0] = V[q];
+#pragma unroll
+        for (int a = 0; a < 6; a++) { sl[1 + a] = E[a]; sl[7 + a] = tau[a]; }
+        sl[13] = sl[14] = sl[15] = T(0);
+    }
+}
+
 // ---- a3: C2N gather (Alg. 2 lines 16-22) + Newton target and Dirichlet sets ----------
 // PH 0: gather + finish in one pass (one rank).  PH 1: gather only, n_vn = ((mv)_i, m_i) partial
 // sums over this rank's cells (slab ranks; completed by c2n_halo).  PH 2: finish from n_vn.
@@ -784,9 +924,13 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
         k_cell_list<<<T_, 64, 0, st>>>(T_, (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_cstart.p,
                                        (uint8_t *)ctx->c_local.p, (int *)ctx->t_cellof.p); ctx->launches++;
     DBG_GUARDS("resample #8");
-        k_p2q<T><<<T_, 64, 0, st>>>(g, ctx->mats, (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p,
-                                    (const int *)ctx->t_bstart.p, (const int *)ctx->t_cellof.p, (const T *)ctx->prec.p,
-                                    (T *)ctx->q_m.p, (T *)ctx->q_mv.p, (T *)ctx->q_mG.p, (T *)ctx->q_slot.p, sc);
+#define P2Q_ARGS                                                                                             \
+    g, ctx->mats, (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p, (const int *)ctx->t_bstart.p, \
+        (const int *)ctx->t_cellof.p, (const T *)ctx->prec.p, (T *)ctx->q_m.p, (T *)ctx->q_mv.p,            \
+        (T *)ctx->q_mG.p, (T *)ctx->q_slot.p, sc
+        if (ctx->mats.nmat <= 2) k_p2q8<T, 2><<<2 * T_, 256, 0, st>>>(P2Q_ARGS);
+        else k_p2q8<T, MPL_MAXMAT><<<2 * T_, 256, 0, st>>>(P2Q_ARGS);
+#undef P2Q_ARGS
         ctx->launches++;
     DBG_GUARDS("resample #9");
     }

@@ -371,6 +371,84 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
 }
 
 // =============================================================================================
+// Explicit integration (Eq. explicitforce, Alg. 3 lines 1-3):
+//   f_i = - sum_c sum_k V_ck tau_ck grad w_ic ,   v_i^{n+1} = v_i^n + dt (g + f_i / m_i)  (gravity amb-4)
+// on the same tiles: per cell Pc = sum_k V_ck tau_ck (the quadrature stress content of P2Q), scattered
+// to the 8 corners with grad w_ic = s_ic / (4 dx); interior nodes stored, face nodes atomically added.
+// =============================================================================================
+template <class T>
+__global__ void __launch_bounds__(128) k_explicit_force(GridP g, int nmat, const int *__restrict__ nplus,
+                                                        const int *__restrict__ cstart,
+                                                        const uint8_t *__restrict__ clocal,
+                                                        const int *__restrict__ hascells, const T *__restrict__ qslot,
+                                                        vec4<T> *__restrict__ f) {
+    __shared__ T Pg[64 * 9];
+    __shared__ int cslot[64];
+    const int t = blockIdx.x, tid = threadIdx.x;
+    const int has = hascells[t];
+    if (!has) return;
+    const int cs = cstart[t], nc = cstart[t + 1] - cs;
+    if (tid < 64) cslot[tid] = -1;
+    __syncthreads();
+    const T q = T(0.25 * g.inv_dx);
+    if (tid < nc) {
+        const int l = clocal[cs + tid];
+        if (l != 0xFF) {
+            cslot[l] = tid;
+            T P[6] = {0, 0, 0, 0, 0, 0};
+            for (int k = 0; k < nmat; k++) {
+                const T *sl = qslot + ((int64_t)(cs + tid) * nmat + k) * 16;
+                const T V = sl[0];
+#pragma unroll
+                for (int a = 0; a < 6; a++) P[a] += V * sl[7 + a];  // V_ck tau_ck (xx yy zz xy yz xz)
+            }
+            const T full[9] = {P[0], P[3], P[5], P[3], P[1], P[4], P[5], P[4], P[2]};
+#pragma unroll
+            for (int a = 0; a < 9; a++) Pg[l * 9 + a] = -full[a] * q;  // f = -V tau grad w
+        }
+    }
+    __syncthreads();
+    if (tid < 125) {
+        const int h = tid, hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
+        const bool interior = hx >= 1 && hx <= 3 && hy >= 1 && hy <= 3 && hz >= 1 && hz <= 3;
+        T fv[3] = {0, 0, 0};
+        bool any = false;
+#pragma unroll
+        for (int o = 0; o < 8; o++) {
+            const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+            const int cx = hx - ox, cy = hy - oy, cz = hz - oz;
+            if (cx < 0 || cy < 0 || cz < 0 || cx > 3 || cy > 3 || cz > 3) continue;
+            const int l = local_id(cx, cy, cz);
+            if (cslot[l] < 0) continue;
+            any = true;
+            const T s0 = ox ? T(1) : T(-1), s1 = oy ? T(1) : T(-1), s2 = oz ? T(1) : T(-1);
+            const T *P = Pg + l * 9;
+#pragma unroll
+            for (int a = 0; a < 3; a++) fv[a] += P[3 * a] * s0 + P[3 * a + 1] * s1 + P[3 * a + 2] * s2;
+        }
+        const int64_t n = halo_node(t, nplus, h);
+        if (any && n >= 0) {
+            if (interior) f[n] = mk4<T>(fv[0], fv[1], fv[2], T(0));
+            else atomic_add3<T>(f + n, fv[0], fv[1], fv[2]);
+        }
+    }
+}
+
+// v^{n+1} = vhat + dt f / m on free nodes (vhat = v^n + dt g); prescribed nodes keep their value
+template <class T>
+__global__ void k_explicit_update(int64_t n, const int *__restrict__ list, const uint8_t *__restrict__ flag,
+                                  const vec4<T> *__restrict__ vhat, const T *__restrict__ m,
+                                  const vec4<T> *__restrict__ f, T dt, vec4<T> *__restrict__ v) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int ti = list[i];
+    if (flag[ti] != 1) return;
+    const vec4<T> vh = vhat[ti], fv = f[ti];
+    const T s = dt / m[ti];
+    v[ti] = mk4<T>(vh.x + s * fv.x, vh.y + s * fv.y, vh.z + s * fv.z, T(0));
+}
+
+// =============================================================================================
 // a7: Jacobi-PCG vector kernels (fp64 accumulation of every dot product)
 // slot j: rz_j = r_j.z_j, rr_j = r_j.r_j, pHp_j = p_j.H p_j
 // =============================================================================================
@@ -424,7 +502,8 @@ __device__ __forceinline__ CGScal cg_scalars(const CGSlot *slot, int j, bool nex
     return s_;
 }
 
-// x += alpha p ; r -= alpha Hp ; slot[j+1] = (r.invD r, r.r) ; Hp := 0 for the next HVP's atomics.
+// r -= alpha Hp ; slot[j+1] = (r.invD r, r.r) ; Hp := 0 for the next HVP's atomics.  (The iterate
+// update x += alpha p is deferred to k_pcg_update2, which reads p anyway: one fewer pass over p.)
 // One active node per thread: all loads are issued before any use (latency hidden by occupancy).
 template <class T>
 __global__ void __launch_bounds__(256) k_pcg_update1(int64_t n, const int *__restrict__ list, int j, double thr,
@@ -450,13 +529,11 @@ __global__ void __launch_bounds__(256) k_pcg_update1(int64_t n, const int *__res
     if (i < n) {
         const int ti = list[i];
         const vec4<T> iv = invD[i];
-        vec4<T> xv = x[i], rv = r[i];
-        const vec4<T> hv = Hp[ti], pv = p[ti];
+        vec4<T> rv = r[i];
+        const vec4<T> hv = Hp[ti];
         Hp[ti] = mk4<T>(0, 0, 0, 0);
         const T aw = alpha * iv.w;
-        xv.x += alpha * pv.x; xv.y += alpha * pv.y; xv.z += alpha * pv.z;
         rv.x -= aw * hv.x; rv.y -= aw * hv.y; rv.z -= aw * hv.z;
-        x[i] = xv;
         r[i] = rv;
         rz = rv.w * (rv.x * rv.x * iv.x + rv.y * rv.y * iv.y + rv.z * rv.z * iv.z);
         rr = rv.w * (rv.x * rv.x + rv.y * rv.y + rv.z * rv.z);
@@ -465,21 +542,30 @@ __global__ void __launch_bounds__(256) k_pcg_update1(int64_t n, const int *__res
     block_add((double)rr, slot[j + 1].rr);
 }
 
-// p = invD r + beta p, beta = rz_{j+1} / rz_j
+// x += alpha_j p_j ; then (unless converged) p = invD r + beta p, beta = rz_{j+1} / rz_j
 template <class T>
 __global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, const int *__restrict__ list, int j, double thr,
                                                      const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ r,
-                                                     vec4<T> *__restrict__ p, const CGSlot *slot,
-                                                     const DevScalars *sc) {
+                                                     vec4<T> *__restrict__ p, vec4<T> *__restrict__ x,
+                                                     const CGSlot *slot, const DevScalars *sc) {
     const CGScal cs = cg_scalars(slot, j, true);
-    if (sc->neg_curv || cs.rr1 <= thr) return;
-    const T beta = T(cs.rz1 / cs.rz);
+    // iteration j was not executed (converged before it) or broke down (x already set by update1)
+    const int done = sc->cg_done_iter;
+    if ((done >= 0 && done <= j + 1) || (j > 0 && cs.rr <= thr)) return;
+    const T alpha = T(cs.rz / cs.pHp);
+    const bool more = cs.rr1 > thr;  // p_{j+1} is needed
+    const T beta = more ? T(cs.rz1 / cs.rz) : T(0);
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) {
         const int ti = list[i];
-        const vec4<T> rv = r[i], iv = invD[i];
         const vec4<T> pv = p[ti];
-        p[ti] = mk4<T>(rv.x * iv.x + beta * pv.x, rv.y * iv.y + beta * pv.y, rv.z * iv.z + beta * pv.z, T(0));
+        vec4<T> xv = x[i];
+        xv.x += alpha * pv.x; xv.y += alpha * pv.y; xv.z += alpha * pv.z;
+        x[i] = xv;
+        if (more) {
+            const vec4<T> rv = r[i], iv = invD[i];
+            p[ti] = mk4<T>(rv.x * iv.x + beta * pv.x, rv.y * iv.y + beta * pv.y, rv.z * iv.z + beta * pv.z, T(0));
+        }
     }
 }
 
@@ -684,6 +770,10 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> hev;
+    std::vector<std::pair<int, int>> sampled;  // (event pair, PCG iteration) of timed HVP launches
+    int nl = 0;                                // HVP launches (incl. ones skipped after convergence)
+    double hvp_sample_ms = 0.0;
+    int hvp_sample_n = 0;
     // per-HVP device timing (stats.hvp_ms): CUDA events around every HVP_SAMPLE-th HVP launch (the
     // events cost ~4 us each inside the PCG loop); MPL_HVP_EVENTS=0 drops them
     const char *hve = getenv("MPL_HVP_EVENTS");
@@ -738,7 +828,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
             while (!done && launched < itmax) {
                 int n = std::min(chunk, itmax - launched);
                 for (int jj = launched; jj < launched + n; jj++) {
-                    if ((int)hev.size() <= S.n_hvp) {
+                    if ((int)hev.size() <= nl) {
                         cudaEvent_t a, b;
                         cudaEventCreate(&a);
                         cudaEventCreate(&b);
@@ -749,21 +839,22 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                             vev.push_back({a, b});
                         }
                     }
-                    const bool timed = hvp_events && (S.n_hvp % HVP_SAMPLE == 0);
-                    if (timed) cudaEventRecord(hev[S.n_hvp].first, st);
+                    const bool timed = hvp_events && (jj % HVP_SAMPLE == 0);
+                    if (timed) cudaEventRecord(hev[nl].first, st);
                     // the HVP is skipped on device once converged (its output is then unused)
                     MPL_CHECK(launch_hvp<T>(ctx, p, Hp, slots[jj].pHp, slots, jj, thr));
                     if (multi(ctx)) {  // complete Hp on the shared planes; global p.Hp (timed with the HVP)
                         MPL_CHECK(halo_sum_nodes<T>(ctx, Hp, nullptr));
                         MPL_CHECK(allreduce_d(ctx, slots[jj].pHp, NSTRIPE));
                     }
-                    if (timed) cudaEventRecord(hev[S.n_hvp].second, st);
-                    S.n_hvp++;
-                    if (vec_events) cudaEventRecord(vev[S.n_hvp - 1].first, st);
+                    if (timed) cudaEventRecord(hev[nl].second, st);
+                    if (timed) sampled.push_back({nl, jj});
+                    nl++;
+                    if (vec_events) cudaEventRecord(vev[nl - 1].first, st);
                     k_pcg_update1<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc); ctx->launches++;
                     MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
-                    k_pcg_update2<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, slots, sc); ctx->launches++;
-                    if (vec_events) cudaEventRecord(vev[S.n_hvp - 1].second, st);
+                    k_pcg_update2<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, x, slots, sc); ctx->launches++;
+                    if (vec_events) cudaEventRecord(vev[nl - 1].second, st);
                 }
                 launched += n;
                 MPL_CUDA(cudaGetLastError());
@@ -793,6 +884,14 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         cudaEventRecord(e1, st);
         MPL_CUDA(cudaEventSynchronize(e1));
         t_pcg += elapsed(e0, e1);
+        // HVPs launched past convergence exit on the device at once: only iterations jj < its count
+        for (const auto &sp : sampled)
+            if (sp.second < its) {
+                hvp_sample_ms += elapsed(hev[sp.first].first, hev[sp.first].second);
+                hvp_sample_n++;
+            }
+        sampled.clear();
+        S.n_hvp += its;
         if (k < MPL_MAX_NEWTON_LOG) S.cg_iters[k] = its;
         S.cg_iters_total += its;
         // ---- Armijo backtracking line search ------------------------------------------------
@@ -845,14 +944,11 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     }
     MPL_CHECK(energy_at<T>(ctx, v, &S.energy));
     double hsum = 0;
-    if (hvp_events && S.n_hvp > 0) {  // every HVP_SAMPLE-th launch is timed; scaled to all launches
-        int ns = 0;
-        for (int i = 0; i < S.n_hvp; i += HVP_SAMPLE, ns++) hsum += elapsed(hev[i].first, hev[i].second);
-        hsum *= (double)S.n_hvp / ns;
-    }
+    if (hvp_events && hvp_sample_n > 0)  // mean of the timed executed HVPs x executed HVPs
+        hsum = hvp_sample_ms / hvp_sample_n * S.n_hvp;
     double vsum = 0;
     if (vec_events)
-        for (int i = 0; i < S.n_hvp; i++) vsum += elapsed(vev[i].first, vev[i].second);
+        for (int i = 0; i < nl; i++) vsum += elapsed(vev[i].first, vev[i].second);
     for (auto &pr : vev) {
         cudaEventDestroy(pr.first);
         cudaEventDestroy(pr.second);
@@ -876,6 +972,37 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     return MPL_OK;
 }
 
+// Explicit step velocities (Alg. 3 "Explicit" branch): force into n_g, v^{n+1} into n_v.
+template <class T>
+mpl_status explicit_impl(mpl_ctx ctx) {
+    cudaStream_t st = ctx->stream;
+    const int64_t NT = (int64_t)ctx->T * 64, NA = ctx->n_nodes_active;
+    MPL_CUDA(cudaMemsetAsync(ctx->n_g.p, 0, NT * sizeof(vec4<T>), st));
+    if (ctx->T) {
+        k_explicit_force<T><<<ctx->T, 128, 0, st>>>(ctx->grid, ctx->mats.nmat, (const int *)ctx->t_nplus.p,
+                                                    (const int *)ctx->t_cstart.p, (const uint8_t *)ctx->c_local.p,
+                                                    (const int *)ctx->t_hascells.p, (const T *)ctx->q_slot.p,
+                                                    (vec4<T> *)ctx->n_g.p);
+        ctx->launches++;
+    }
+    MPL_CUDA(cudaGetLastError());
+    MPL_CHECK(halo_sum_nodes<T>(ctx, ctx->n_g.p, nullptr));  // slab ranks: complete f on the shared planes
+    if (NA) {
+        k_explicit_update<T><<<nblk(NA, 256), 256, 0, st>>>(NA, (const int *)ctx->n_list.p,
+                                                            (const uint8_t *)ctx->n_flag.p,
+                                                            (const vec4<T> *)ctx->n_vhat.p, (const T *)ctx->n_mass.p,
+                                                            (const vec4<T> *)ctx->n_g.p, T(ctx->dt),
+                                                            (vec4<T> *)ctx->n_v.p);
+        ctx->launches++;
+    }
+    MPL_CUDA(cudaGetLastError());
+    MPL_CUDA(cudaStreamSynchronize(st));
+    ctx->solved = true;
+    return MPL_OK;
+}
+
+template mpl_status explicit_impl<float>(mpl_ctx);
+template mpl_status explicit_impl<double>(mpl_ctx);
 template mpl_status canon_to_tile<float>(mpl_ctx, const void *, void *);
 template mpl_status canon_to_tile<double>(mpl_ctx, const void *, void *);
 template mpl_status tile_to_canon<float>(mpl_ctx, const void *, void *);

@@ -592,6 +592,49 @@ mpl_status mpl_transfer_to_particles(mpl_ctx ctx, double dt) {
     return DISPATCH(ctx, g2p_impl, dt);
 }
 
+mpl_status mpl_explicit_velocity(mpl_ctx ctx) {
+    ApiLock api_lock_;
+    if (!ctx) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample before mpl_explicit_velocity"));
+    MPL_CHECK(set_device(ctx));
+    return ctx->precision == 64 ? explicit_impl<double>(ctx) : explicit_impl<float>(ctx);
+}
+
+mpl_status mpl_explicit_step(mpl_ctx ctx, double dt, mpl_solve_stats *stats) {
+    ApiLock api_lock_;
+    if (!ctx) return MPL_ERR_INVALID_ARG;
+    cudaEvent_t e[4];
+    for (auto &x : e) cudaEventCreate(&x);
+    const int64_t l0 = ctx->launches;
+    cudaEventRecord(e[0], ctx->stream);
+    MPL_CHECK(mpl_resample(ctx, dt, nullptr, nullptr, nullptr));
+    cudaEventRecord(e[1], ctx->stream);
+    MPL_CHECK(mpl_explicit_velocity(ctx));
+    cudaEventRecord(e[2], ctx->stream);
+    MPL_CHECK(mpl_transfer_to_particles(ctx, dt));
+    cudaEventRecord(e[3], ctx->stream);
+    cudaEventSynchronize(e[3]);
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, e[0], e[1]);
+    cudaEventElapsedTime(&b, e[1], e[2]);
+    cudaEventElapsedTime(&c, e[2], e[3]);
+    for (auto &x : e) cudaEventDestroy(x);
+    if (stats) {
+        mpl_solve_stats S{};
+        S.ms_phase[0] = a;
+        S.ms_phase[2] = b;
+        S.ms_phase[6] = c;
+        S.ms_phase[7] = a + b + c;
+        S.converged = 1;
+        S.n_cells = ctx->n_cells_active;
+        S.n_nodes = ctx->n_nodes_active;
+        S.n_free_nodes = ctx->n_free_nodes;
+        S.n_launches = ctx->launches - l0;
+        *stats = S;
+    }
+    return MPL_OK;
+}
+
 mpl_status mpl_step(mpl_ctx ctx, double dt, const mpl_solver_cfg *cfg, mpl_solve_stats *stats) {
     ApiLock api_lock_;
     if (!ctx || !cfg) return MPL_ERR_INVALID_ARG;

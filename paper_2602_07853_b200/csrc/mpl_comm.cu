@@ -934,6 +934,38 @@ mpl_status mpl_nccl_unique_id(uint8_t out[128]) {
     return MPL_OK;
 }
 
+// One-rank NCCL self-test on `device`: the exact entry points the slab transport uses (unique id,
+// communicator init, in-place fp64 allreduce, a grouped send/receive to itself, destroy), so the
+// dlopen'ed NCCL path is exercised on a single GPU (multi-rank runs need one GPU per rank).
+mpl_status mpl_nccl_selftest(int32_t device, double *out_sum) {
+    NcclApi &api = nccl();
+    if (!api.ok) return MPL_ERR_NCCL;
+    if (cudaSetDevice(device) != cudaSuccess) return MPL_ERR_CUDA;
+    ncclUniqueId id;
+    if (api.GetUniqueId(&id) != ncclSuccess) return MPL_ERR_NCCL;
+    ncclComm_t comm = nullptr;
+    if (api.CommInitRank(&comm, 1, id, 0) != ncclSuccess) return MPL_ERR_NCCL;
+    cudaStream_t st;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    double h[4] = {1.5, 2.5, 0.0, 0.0}, *d = nullptr;
+    mpl_status rc = MPL_OK;
+    if (cudaMalloc(&d, 4 * sizeof(double)) != cudaSuccess) rc = MPL_ERR_OOM;
+    if (rc == MPL_OK) {
+        cudaMemcpy(d, h, 4 * sizeof(double), cudaMemcpyHostToDevice);
+        if (api.AllReduce(d, d, 2, ncclFloat64, ncclSum, comm, st) != ncclSuccess) rc = MPL_ERR_NCCL;
+        if (rc == MPL_OK && (api.GroupStart() != ncclSuccess || api.Send(d, 16, ncclUint8, 0, comm, st) != ncclSuccess ||
+                             api.Recv(d + 2, 16, ncclUint8, 0, comm, st) != ncclSuccess || api.GroupEnd() != ncclSuccess))
+            rc = MPL_ERR_NCCL;
+        if (cudaStreamSynchronize(st) != cudaSuccess) rc = MPL_ERR_CUDA;
+        cudaMemcpy(h, d, 4 * sizeof(double), cudaMemcpyDeviceToHost);
+        cudaFree(d);
+    }
+    cudaStreamDestroy(st);
+    api.CommDestroy(comm);
+    if (out_sum) *out_sum = h[0] + h[1] + h[2] + h[3];  // 1.5 + 2.5 copied once more: 8.0
+    return rc;
+}
+
 // Balanced slab cuts: cuts[0] = 0, cuts[nranks] = nplanes, and cuts[r] the first plane whose prefix
 // weight reaches r/nranks of the total, kept strictly increasing (every slab >= 1 plane).
 mpl_status mpl_balance_slabs(int32_t nplanes, const int64_t *weight, int32_t nranks, int32_t *cuts) {

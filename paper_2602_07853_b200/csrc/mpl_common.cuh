@@ -491,6 +491,7 @@ template <class T> mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *
                                          const CGSlot *cgs, int cgj, double cgthr);
 template <class T> mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *st);
 template <class T> mpl_status g2p_impl(mpl_ctx ctx, double dt);
+template <class T> mpl_status explicit_impl(mpl_ctx ctx);
 template <class T> mpl_status canon_to_tile(mpl_ctx ctx, const void *src, void *dst_tile);
 template <class T> mpl_status tile_to_canon(mpl_ctx ctx, const void *src_tile, void *dst);
 template <class T> mpl_status export_quadrature(mpl_ctx ctx, int32_t *ijk, void *m_c, void *v_c, void *G_c,

@@ -91,6 +91,7 @@ _SIGS = {
     "mpl_version": [],
     "mpl_nccl_unique_id": [_vp],
     "mpl_group_create": [_i32, _vp],
+    "mpl_nccl_selftest": [_i32, _vp],
     "mpl_group_destroy": [_vp],
     "mpl_set_slabs": [_vp, _vp],
     "mpl_balance_slabs": [_i32, _vp, _i32, _vp],
@@ -119,6 +120,8 @@ _SIGS = {
     "mpl_set_velocity": [_vp, _vp],
     "mpl_transfer_to_particles": [_vp, _d],
     "mpl_step": [_vp, _d, _vp, _vp],
+    "mpl_explicit_velocity": [_vp],
+    "mpl_explicit_step": [_vp, _d, _vp],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -142,6 +145,15 @@ def nccl_unique_id() -> bytes:
     if st != 0:
         raise MplError(st, "mpl_nccl_unique_id failed (is libnccl.so.2 loadable?)")
     return bytes(buf)
+
+
+def nccl_selftest(device: int = 0) -> float:
+    """One-rank NCCL transport self-test (returns 8.0)."""
+    out = C.c_double()
+    st = _lib.mpl_nccl_selftest(int(device), C.byref(out))
+    if st != 0:
+        raise MplError(st, "mpl_nccl_selftest")
+    return out.value
 
 
 def balance_slabs(weight, nranks: int) -> np.ndarray:
@@ -252,6 +264,10 @@ class Context:
             if shape is not None:
                 assert a.size == int(np.prod(shape)), (a.shape, shape)
         return a
+
+    def _nn(self) -> int:
+        # before a (successful) resample there are no nodes: the library then reports the call-order error
+        return self.counts.n_nodes if self.counts is not None else 0
 
     def _out(self, shape, out=None):
         if out is not None:
@@ -367,7 +383,7 @@ class Context:
 
     def gradient(self, v, out=None):
         v = self._real(v)
-        g = self._out((self.counts.n_nodes, 3), out)
+        g = self._out((self._nn(), 3), out)
         e = C.c_double()
         self._chk(_lib.mpl_gradient(self._h, _ptr(v), _ptr(g), C.byref(e)), "mpl_gradient")
         return g, e.value
@@ -377,13 +393,13 @@ class Context:
         self._chk(_lib.mpl_linearize(self._h, _ptr(v)), "mpl_linearize")
 
     def get_diag(self, out=None):
-        d = self._out((self.counts.n_nodes, 3), out)
+        d = self._out((self._nn(), 3), out)
         self._chk(_lib.mpl_get_diag(self._h, _ptr(d)), "mpl_get_diag")
         return d
 
     def hvp(self, u, out=None):
         u = self._real(u)
-        h = self._out((self.counts.n_nodes, 3), out)
+        h = self._out((self._nn(), 3), out)
         self._chk(_lib.mpl_hvp(self._h, _ptr(u), _ptr(h)), "mpl_hvp")
         return h
 
@@ -417,7 +433,7 @@ class Context:
         return st.as_dict()
 
     def get_velocity(self, out=None):
-        v = self._out((self.counts.n_nodes, 3), out)
+        v = self._out((self._nn(), 3), out)
         self._chk(_lib.mpl_get_velocity(self._h, _ptr(v)), "mpl_get_velocity")
         return v
 
@@ -427,6 +443,15 @@ class Context:
 
     def transfer_to_particles(self, dt: float):
         self._chk(_lib.mpl_transfer_to_particles(self._h, float(dt)), "mpl_transfer_to_particles")
+
+    def explicit_velocity(self):
+        """Explicit update v^{n+1} = v^n + dt (g + f/m) after resample (Eq. explicitforce)."""
+        self._chk(_lib.mpl_explicit_velocity(self._h), "mpl_explicit_velocity")
+
+    def explicit_step(self, dt: float) -> dict:
+        st = SolveStats()
+        self._chk(_lib.mpl_explicit_step(self._h, float(dt), C.byref(st)), "mpl_explicit_step")
+        return st.as_dict()
 
     def step(self, dt: float, solver, fixed_newton: int = 0, fixed_cg=None, fixed_ls=None) -> dict:
         cfg, keep = self.solver_cfg(solver, fixed_newton, fixed_cg, fixed_ls)

@@ -43,6 +43,7 @@ CASES = {
     "cfg2s_fp32_R3": (lambda: small_cfg2(32), [0, 3, 4, 8]),
     "cfg2s_fp64_R4": (lambda: small_cfg2(64), [0, 3, 4, 5, 8]),
     "mix_fp64_R2": (lambda: two_material(64), [0, 2, 4]),
+    "lawmix_fp32_R2": (lambda: two_material(32, (1, 0)), [0, 2, 4]),  # split Neo-Hookean + Hencky
 }
 
 
@@ -236,3 +237,11 @@ def test_collective_error_reaches_every_rank():
     grp.close()
     assert codes[1] == 3  # MPL_ERR_OUT_OF_DOMAIN where it happened
     assert codes[0] is not None  # and an error (not a hang) on the other rank
+
+
+def test_nccl_transport_selftest():
+    """The NCCL entry points the slab transport uses work on this GPU (one-rank communicator)."""
+    import torch  # noqa: F401  (loads torch's NCCL first, as bench.py does)
+    assert mpl.nccl_selftest(0) == 8.0
+    uid = mpl.nccl_unique_id()
+    assert len(uid) == 128

@@ -103,6 +103,13 @@ def hvp_bytes(n_cells, n_nodes, s=4):
     return n_cells * 45 * s + n_nodes * 7 * s
 
 
+def hvp_kernel_name() -> str:
+    """The HVP kernel the library runs (MPL_HVP_KERNEL, default rp10: k_hvp_rp<T, 10>)."""
+    v = os.environ.get("MPL_HVP_KERNEL", "rp10")
+    return {"rp10": "k_hvp_rp<10>", "rp": "k_hvp_rp<1>", "rp12": "k_hvp_rp<12>", "pipe2": "k_hvp_pipe<2>",
+            "pipe3": "k_hvp_pipe<3>", "reg": "k_hvp_reg"}.get(v, "k_hvp_rp<10>")
+
+
 def workload_name(sc) -> str:
     return f"{sc.name}: {sc.n[0]}^3 grid, {sc.n_particles} particles, {len(sc.materials)} material(s), dt={sc.dt}"
 
@@ -221,7 +228,7 @@ def run_ours(args):
         "qp_per_s": round(cells_all / (avg_hvp_ms * 1e-3), 1) if avg_hvp_ms > 0 else None,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": load_traffic(sc.name) if ws == 1 else None,
-                     "peak_kind": peak_kind, "kernel": "k_hvp_pipe",
+                     "peak_kind": peak_kind, "kernel": hvp_kernel_name(),
                      "algorithmic_bytes_per_launch": int(nbytes), "pct_of_8TBps": round(achieved / 8000.0, 4)},
         "e2e": e2e,
         "gpu_launches": int(launches),
@@ -229,6 +236,7 @@ def run_ours(args):
                      "linearize": round(statistics.mean(s["ms_phase"][3] for s in stats), 3),
                      "pcg": round(statistics.mean(s["ms_phase"][4] for s in stats), 3),
                      "pcg_vector_kernels": round(statistics.mean(s["ms_phase"][1] for s in stats), 3),
+                     "pcg_update2": round(statistics.mean(s["ms_phase"][2] for s in stats), 3),
                      "line_search": round(statistics.mean(s["ms_phase"][5] for s in stats), 3),
                      "g2p": round(statistics.mean(s["ms_phase"][6] for s in stats), 3)},
         "clocks": clocks,

@@ -1,3 +1,4 @@
+#include <array>
 // k_solve.cu — SURVEY §8(a) rows a5-a8: linearisation (energy / gradient / cached tangent /
 // Jacobi diagonal), the matrix-free HVP, Jacobi-PCG vector kernels and the Newton driver.
 //
@@ -569,6 +570,95 @@ __global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, const int *__res
     }
 }
 
+// Persistent forms (MPL_VEC_KERNEL=pers): one CTA wave (SMs x 8 CTAs of 256), the CG scalars read once
+// per CTA, U nodes per thread per pass with every independent load issued before the dependent
+// tile-dense one (list -> Hp / p), so no CTA wave pays the scalar -> list -> data latency chain.
+template <class T, int U>
+__global__ void __launch_bounds__(256) k_pcg_update1p(int64_t n, const int *__restrict__ list, int j, double thr,
+                                                      const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ p,
+                                                      vec4<T> *__restrict__ Hp, vec4<T> *__restrict__ x,
+                                                      vec4<T> *__restrict__ r, CGSlot *slot, DevScalars *sc) {
+    const CGScal cs = cg_scalars(slot, j, false);
+    const int done = sc->cg_done_iter;
+    if ((done >= 0 && done <= j) || (j > 0 && cs.rr <= thr)) return;
+    const int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+    if (!(cs.pHp > 0.0)) {
+        if (j == 0)
+            for (int64_t i = g0; i < n; i += gs) x[i] = p[list[i]];
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            sc->neg_curv = 1;
+            sc->cg_done_iter = j + 1;
+        }
+        return;
+    }
+    const T alpha = T(cs.rz / cs.pHp);
+    T rz = 0, rr = 0;
+    for (int64_t b = g0; b < n; b += gs * U) {
+        int ti[U];
+        vec4<T> iv[U], rv[U], hv[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t i = b + u * gs;
+            ti[u] = i < n ? list[i] : -1;
+            if (i < n) { iv[u] = invD[i]; rv[u] = r[i]; }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            if (ti[u] >= 0) hv[u] = Hp[ti[u]];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (ti[u] < 0) continue;
+            Hp[ti[u]] = mk4<T>(0, 0, 0, 0);
+            const T aw = alpha * iv[u].w;
+            rv[u].x -= aw * hv[u].x; rv[u].y -= aw * hv[u].y; rv[u].z -= aw * hv[u].z;
+            r[b + u * gs] = rv[u];
+            rz += rv[u].w * (rv[u].x * rv[u].x * iv[u].x + rv[u].y * rv[u].y * iv[u].y + rv[u].z * rv[u].z * iv[u].z);
+            rr += rv[u].w * (rv[u].x * rv[u].x + rv[u].y * rv[u].y + rv[u].z * rv[u].z);
+        }
+    }
+    block_add((double)rz, slot[j + 1].rz);
+    block_add((double)rr, slot[j + 1].rr);
+}
+
+template <class T, int U>
+__global__ void __launch_bounds__(256) k_pcg_update2p(int64_t n, const int *__restrict__ list, int j, double thr,
+                                                      const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ r,
+                                                      vec4<T> *__restrict__ p, vec4<T> *__restrict__ x,
+                                                      const CGSlot *slot, const DevScalars *sc) {
+    const CGScal cs = cg_scalars(slot, j, true);
+    const int done = sc->cg_done_iter;
+    if ((done >= 0 && done <= j + 1) || (j > 0 && cs.rr <= thr)) return;
+    const T alpha = T(cs.rz / cs.pHp);
+    const bool more = cs.rr1 > thr;
+    const T beta = more ? T(cs.rz1 / cs.rz) : T(0);
+    const int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t b = g0; b < n; b += gs * U) {
+        int ti[U];
+        vec4<T> xv[U], rv[U], iv[U], pv[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t i = b + u * gs;
+            ti[u] = i < n ? list[i] : -1;
+            if (i < n) {
+                xv[u] = x[i];
+                if (more) { rv[u] = r[i]; iv[u] = invD[i]; }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            if (ti[u] >= 0) pv[u] = p[ti[u]];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (ti[u] < 0) continue;
+            xv[u].x += alpha * pv[u].x; xv[u].y += alpha * pv[u].y; xv[u].z += alpha * pv[u].z;
+            x[b + u * gs] = xv[u];
+            if (more)
+                p[ti[u]] = mk4<T>(rv[u].x * iv[u].x + beta * pv[u].x, rv[u].y * iv[u].y + beta * pv[u].y,
+                                  rv[u].z * iv[u].z + beta * pv[u].z, T(0));
+        }
+    }
+}
+
 // g . x over free DOFs (g tile-dense, x compact)
 template <class T>
 __global__ void k_dot_gx(int64_t n, const int *__restrict__ list, const uint8_t *__restrict__ flag,
@@ -765,6 +855,16 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     const int64_t NA = ctx->n_nodes_active;
     const unsigned VA = vgrid(NA);
     const unsigned VA1 = nblk(NA > 0 ? NA : 1, 256);  // one active node per thread
+    // MPL_VEC_KERNEL=pers: persistent update kernels (one wave of SMs x 8 CTAs)
+    const char *vke = getenv("MPL_VEC_KERNEL");
+    const bool vec_pers = vke && vke[0] == 'p';
+    int nsm_ = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm_, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const unsigned VAP = std::min<unsigned>(VA1, (unsigned)nsm_ * 8);
     const int *list = (const int *)ctx->n_list.p;
     cudaEvent_t e0, e1, h0, h1;
     cudaEventCreate(&e0);
@@ -780,8 +880,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     const bool hvp_events = !(hve && hve[0] == '0');
     // MPL_VEC_EVENTS=1: also time the PCG vector kernels (stats.ms_phase[1])
     const char *vee = getenv("MPL_VEC_EVENTS");
-    const bool vec_events = vee && vee[0] == '1';
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> vev;
+    const bool vec_events = vee && (vee[0] == '1' || vee[0] == '2');
+    std::vector<std::array<cudaEvent_t, 3>> vev;  // before update1, between, after update2
     double t_lin = 0, t_pcg = 0, t_ls = 0;
     auto elapsed = [&](cudaEvent_t a, cudaEvent_t b) {
         float ms = 0;
@@ -834,9 +934,9 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                         cudaEventCreate(&b);
                         hev.push_back({a, b});
                         if (vec_events) {
-                            cudaEventCreate(&a);
-                            cudaEventCreate(&b);
-                            vev.push_back({a, b});
+                            std::array<cudaEvent_t, 3> ev;
+                            for (auto &x : ev) cudaEventCreate(&x);
+                            vev.push_back(ev);
                         }
                     }
                     const bool timed = hvp_events && (jj % HVP_SAMPLE == 0);
@@ -850,11 +950,16 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     if (timed) cudaEventRecord(hev[nl].second, st);
                     if (timed) sampled.push_back({nl, jj});
                     nl++;
-                    if (vec_events) cudaEventRecord(vev[nl - 1].first, st);
-                    k_pcg_update1<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc); ctx->launches++;
+                    if (vec_events) cudaEventRecord(vev[nl - 1][0], st);
+                    if (vec_pers) k_pcg_update1p<T, 4><<<VAP, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc);
+                    else k_pcg_update1<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc);
+                    ctx->launches++;
                     MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
-                    k_pcg_update2<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, x, slots, sc); ctx->launches++;
-                    if (vec_events) cudaEventRecord(vev[nl - 1].second, st);
+                    if (vec_events) cudaEventRecord(vev[nl - 1][1], st);
+                    if (vec_pers) k_pcg_update2p<T, 4><<<VAP, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, x, slots, sc);
+                    else k_pcg_update2<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, x, slots, sc);
+                    ctx->launches++;
+                    if (vec_events) cudaEventRecord(vev[nl - 1][2], st);
                 }
                 launched += n;
                 MPL_CUDA(cudaGetLastError());
@@ -946,14 +1051,16 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     double hsum = 0;
     if (hvp_events && hvp_sample_n > 0)  // mean of the timed executed HVPs x executed HVPs
         hsum = hvp_sample_ms / hvp_sample_n * S.n_hvp;
-    double vsum = 0;
+    double vsum = 0, v2sum = 0;
     if (vec_events)
-        for (int i = 0; i < nl; i++) vsum += elapsed(vev[i].first, vev[i].second);
-    for (auto &pr : vev) {
-        cudaEventDestroy(pr.first);
-        cudaEventDestroy(pr.second);
-    }
+        for (int i = 0; i < nl; i++) {
+            vsum += elapsed(vev[i][0], vev[i][2]);
+            v2sum += elapsed(vev[i][1], vev[i][2]);
+        }
+    for (auto &ev : vev)
+        for (auto &x : ev) cudaEventDestroy(x);
     S.ms_phase[1] = vsum;
+    S.ms_phase[2] = v2sum;  // update2 share of ms_phase[1]
     for (auto &pr : hev) {
         cudaEventDestroy(pr.first);
         cudaEventDestroy(pr.second);

@@ -52,11 +52,13 @@ def test_single_particle_at_centre():
     assert np.allclose(m, mp / 8, rtol=1e-14)
     assert np.allclose(vn, [[1.0, 0.0, 0.0]] * 8, atol=1e-14)
     assert sorted(map(tuple, ijk.tolist())) == sorted((7 + a, 8 + b, 9 + d) for a in (0, 1) for b in (0, 1) for d in (0, 1))
-    # F = I, uniform v, no gravity: g is rounding noise (~1e-23) and the relative Newton test cannot
-    # fire (the oracle runs to newton_max as well); the velocities must stay put
+    # F = I, uniform v: the Newton start v-hat = v + dt g (amb-4) is already the minimiser, g is rounding
+    # noise (~1e-23) and the relative Newton test need not fire (the oracle runs to newton_max as well);
+    # the velocities must stay at v-hat
     st = ctx.newton_step(sc.solver)
     assert st["newton_iters"] >= 1
-    assert np.allclose(ctx.get_velocity(), [[1.0, 0.0, 0.0]] * 8, atol=1e-12)
+    vhat = np.array([1.0, 0.0, 0.0]) + sc.dt * np.asarray(sc.gravity)
+    assert np.allclose(ctx.get_velocity(), [vhat] * 8, atol=1e-12)
     ctx.close()
 
 

@@ -6,6 +6,7 @@ The oracle side composes oracle.explicit_force (pinned in test_oracle_solver.py 
 gradient at S = stretch(tau), and the O(dt^2) stiff limit) with oracle.prepare's v-hat and
 Dirichlet sets and oracle.g2p.  Slab ranks (loopback group, one GPU) must reproduce it on owned nodes."""
 import concurrent.futures as cf
+import dataclasses
 
 import numpy as np
 import pytest
@@ -31,10 +32,17 @@ def explicit_oracle(sc):
     return grid, un, f, v1, parts
 
 
+def _prestrained(sc):
+    """Pre-strained F (non-zero tau) and a sticky floor through the block's two lowest node layers."""
+    inf = float("inf")
+    floor = scenes.DirichletBox((-inf, -inf, -inf), (inf, 9.0 / 32, inf), (0.0, 0.0, 0.0))
+    return dataclasses.replace(sc, F=scenes._prestrain(sc.n_particles, 7).astype(sc.F.dtype), dirichlet=[floor])
+
+
 SCENES = {
     "cfg1b_fp64": lambda: scenes.cfg1(prestrain=True),
     "cfg1b_fp32": lambda: scenes.cfg1(prestrain=True, precision=32),
-    "cfg2s_fp64_dirichlet": lambda: small_cfg2(64),
+    "cfg2s_fp64_dirichlet": lambda: _prestrained(small_cfg2(64)),
     "lawmix_fp64": lambda: two_material(64, (1, 0)),
 }
 

@@ -503,78 +503,15 @@ __device__ __forceinline__ CGScal cg_scalars(const CGSlot *slot, int j, bool nex
     return s_;
 }
 
-// r -= alpha Hp ; slot[j+1] = (r.invD r, r.r) ; Hp := 0 for the next HVP's atomics.  (The iterate
-// update x += alpha p is deferred to k_pcg_update2, which reads p anyway: one fewer pass over p.)
-// One active node per thread: all loads are issued before any use (latency hidden by occupancy).
-template <class T>
-__global__ void __launch_bounds__(256) k_pcg_update1(int64_t n, const int *__restrict__ list, int j, double thr,
-                                                     const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ p,
-                                                     vec4<T> *__restrict__ Hp, vec4<T> *__restrict__ x,
-                                                     vec4<T> *__restrict__ r, CGSlot *slot, DevScalars *sc) {
-    const CGScal cs = cg_scalars(slot, j, false);
-    // converged, or broken down at an earlier iteration (cg_done_iter, not neg_curv: block 0 of this
-    // launch may set neg_curv while later blocks start)
-    const int done = sc->cg_done_iter;
-    if ((done >= 0 && done <= j) || (j > 0 && cs.rr <= thr)) return;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (!(cs.pHp > 0.0)) {  // breakdown (negative curvature): the first iteration returns p = z_0
-        if (j == 0 && i < n) x[i] = p[list[i]];
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            sc->neg_curv = 1;
-            sc->cg_done_iter = j + 1;
-        }
-        return;
-    }
-    const T alpha = T(cs.rz / cs.pHp);
-    T rz = 0, rr = 0;
-    if (i < n) {
-        const int ti = list[i];
-        const vec4<T> iv = invD[i];
-        vec4<T> rv = r[i];
-        const vec4<T> hv = Hp[ti];
-        Hp[ti] = mk4<T>(0, 0, 0, 0);
-        const T aw = alpha * iv.w;
-        rv.x -= aw * hv.x; rv.y -= aw * hv.y; rv.z -= aw * hv.z;
-        r[i] = rv;
-        rz = rv.w * (rv.x * rv.x * iv.x + rv.y * rv.y * iv.y + rv.z * rv.z * iv.z);
-        rr = rv.w * (rv.x * rv.x + rv.y * rv.y + rv.z * rv.z);
-    }
-    block_add((double)rz, slot[j + 1].rz);
-    block_add((double)rr, slot[j + 1].rr);
-}
-
-// x += alpha_j p_j ; then (unless converged) p = invD r + beta p, beta = rz_{j+1} / rz_j
-template <class T>
-__global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, const int *__restrict__ list, int j, double thr,
-                                                     const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ r,
-                                                     vec4<T> *__restrict__ p, vec4<T> *__restrict__ x,
-                                                     const CGSlot *slot, const DevScalars *sc) {
-    const CGScal cs = cg_scalars(slot, j, true);
-    // iteration j was not executed (converged before it) or broke down (x already set by update1)
-    const int done = sc->cg_done_iter;
-    if ((done >= 0 && done <= j + 1) || (j > 0 && cs.rr <= thr)) return;
-    const T alpha = T(cs.rz / cs.pHp);
-    const bool more = cs.rr1 > thr;  // p_{j+1} is needed
-    const T beta = more ? T(cs.rz1 / cs.rz) : T(0);
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) {
-        const int ti = list[i];
-        const vec4<T> pv = p[ti];
-        vec4<T> xv = x[i];
-        xv.x += alpha * pv.x; xv.y += alpha * pv.y; xv.z += alpha * pv.z;
-        x[i] = xv;
-        if (more) {
-            const vec4<T> rv = r[i], iv = invD[i];
-            p[ti] = mk4<T>(rv.x * iv.x + beta * pv.x, rv.y * iv.y + beta * pv.y, rv.z * iv.z + beta * pv.z, T(0));
-        }
-    }
-}
-
-// Persistent forms (MPL_VEC_KERNEL=pers): one CTA wave (SMs x 8 CTAs of 256), the CG scalars read once
-// per CTA, U nodes per thread per pass with every independent load issued before the dependent
-// tile-dense one (list -> Hp / p), so no CTA wave pays the scalar -> list -> data latency chain.
+// k_pcg_update1: r -= alpha Hp ; slot[j+1] = (r.invD r, r.r) ; Hp := 0 for the next HVP's atomics.
+// k_pcg_update2: x += alpha_j p_j ; then (unless converged) p = invD r + beta p, beta = rz_{j+1} / rz_j.
+// (x is updated in update2, which reads p anyway: one fewer pass over p.)
+// Persistent: one CTA wave (SMs x 8 CTAs of 256), the CG scalars read once per CTA, U nodes per thread
+// per pass with every independent load issued before the dependent tile-dense one (list -> Hp / p).
+// One node per thread (~9000 CTAs) was 3x slower: each CTA's two striped fp64 atomics serialised on
+// the slot's cache lines (ncu: long scoreboard 72 %, barrier 20 %; 104 us vs 34 us live at cfg4).
 template <class T, int U>
-__global__ void __launch_bounds__(256) k_pcg_update1p(int64_t n, const int *__restrict__ list, int j, double thr,
+__global__ void __launch_bounds__(256) k_pcg_update1(int64_t n, const int *__restrict__ list, int j, double thr,
                                                       const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ p,
                                                       vec4<T> *__restrict__ Hp, vec4<T> *__restrict__ x,
                                                       vec4<T> *__restrict__ r, CGSlot *slot, DevScalars *sc) {
@@ -621,7 +558,7 @@ __global__ void __launch_bounds__(256) k_pcg_update1p(int64_t n, const int *__re
 }
 
 template <class T, int U>
-__global__ void __launch_bounds__(256) k_pcg_update2p(int64_t n, const int *__restrict__ list, int j, double thr,
+__global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, const int *__restrict__ list, int j, double thr,
                                                       const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ r,
                                                       vec4<T> *__restrict__ p, vec4<T> *__restrict__ x,
                                                       const CGSlot *slot, const DevScalars *sc) {
@@ -854,17 +791,14 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     const unsigned VG = vgrid(NT);
     const int64_t NA = ctx->n_nodes_active;
     const unsigned VA = vgrid(NA);
-    const unsigned VA1 = nblk(NA > 0 ? NA : 1, 256);  // one active node per thread
-    // MPL_VEC_KERNEL=pers: persistent update kernels (one wave of SMs x 8 CTAs)
-    const char *vke = getenv("MPL_VEC_KERNEL");
-    const bool vec_pers = vke && vke[0] == 'p';
+    const unsigned VA1 = nblk(NA > 0 ? NA : 1, 256);
     int nsm_ = 148;
     {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm_, cudaDevAttrMultiProcessorCount, dev);
     }
-    const unsigned VAP = std::min<unsigned>(VA1, (unsigned)nsm_ * 8);
+    const unsigned VAP = std::min<unsigned>(VA1, (unsigned)nsm_ * 8);  // persistent update kernels
     const int *list = (const int *)ctx->n_list.p;
     cudaEvent_t e0, e1, h0, h1;
     cudaEventCreate(&e0);
@@ -951,13 +885,11 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     if (timed) sampled.push_back({nl, jj});
                     nl++;
                     if (vec_events) cudaEventRecord(vev[nl - 1][0], st);
-                    if (vec_pers) k_pcg_update1p<T, 4><<<VAP, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc);
-                    else k_pcg_update1<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc);
+                    k_pcg_update1<T, 4><<<VAP, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc);
                     ctx->launches++;
                     MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
                     if (vec_events) cudaEventRecord(vev[nl - 1][1], st);
-                    if (vec_pers) k_pcg_update2p<T, 4><<<VAP, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, x, slots, sc);
-                    else k_pcg_update2<T><<<VA1, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, x, slots, sc);
+                    k_pcg_update2<T, 4><<<VAP, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, x, slots, sc);
                     ctx->launches++;
                     if (vec_events) cudaEventRecord(vev[nl - 1][2], st);
                 }

@@ -106,7 +106,7 @@ def hvp_bytes(n_cells, n_nodes, s=4):
 def hvp_kernel_name() -> str:
     """The HVP kernel the library runs (MPL_HVP_KERNEL, default rp10: k_hvp_rp<T, 10>)."""
     v = os.environ.get("MPL_HVP_KERNEL", "rp10")
-    return {"rp10": "k_hvp_rp<10>", "rp": "k_hvp_rp<1>", "rp12": "k_hvp_rp<12>", "pipe2": "k_hvp_pipe<2>",
+    return {"rq": "k_hvp_rq<10>", "rq8": "k_hvp_rq<8>", "rp10": "k_hvp_rp<10>", "rp": "k_hvp_rp<1>", "rp12": "k_hvp_rp<12>", "pipe2": "k_hvp_pipe<2>",
             "pipe3": "k_hvp_pipe<3>", "reg": "k_hvp_reg"}.get(v, "k_hvp_rp<10>")
 
 

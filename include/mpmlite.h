@@ -74,7 +74,8 @@ typedef struct {
 } mpl_grid;
 
 typedef struct {
-    int32_t kind; /* 0 = StVK with Hencky strain (amb-1)   */
+    int32_t kind; /* 0 = StVK with Hencky strain (amb-1); 1 = split Neo-Hookean
+                     (P:229-285); 2 = J-based water (kappa = E)          */
     double E, nu; /* Young's modulus, Poisson ratio -> 3D Lame (amb-2) */
     double rho;   /* density: m_p = rho * V_p                          */
 } mpl_material;
@@ -163,8 +164,12 @@ MPL_API mpl_status mpl_get_node_owner(mpl_ctx ctx, uint8_t *owned);
 
 /* ---- scene -------------------------------------------------------------------------------- */
 /* n <= 8 materials; kind 0 (StVK-Hencky) or 1 (split Neo-Hookean, bulk modulus kappa = 2/3 mu + lam,
- * P:250).  Requires mu > 0 and lam > -2 mu / 3.  Each material slot of a quadrature point keeps
- * its own law. */
+ * P:250): require mu > 0 and lam > -2 mu / 3.  Kind 2 (J-based water, §4.5):
+ * psi = kappa/2 (J - 1)^2 with kappa = E > 0 (nu ignored); a water particle carries only
+ * J_p = det F_p: its stress is kappa J (J - 1) I, its slot's base stretch J_base^{1/3} I
+ * (J_base = (1 + sqrt(1 + 4 pi_c / kappa)) / 2), and Load sets F_p = J_p^{1/3} I with
+ * J_p^{n+1} = (1 + dt tr G_p) J_p^n.  Each material slot of a quadrature point keeps its own
+ * law; solids and water may share cells. */
 MPL_API mpl_status mpl_set_materials(mpl_ctx ctx, int32_t n, const mpl_material *mats);
 /* gravity acceleration g (inertia target vhat = v^n + dt g, amb-4); default (0, -9.81, 0). */
 MPL_API mpl_status mpl_set_gravity(mpl_ctx ctx, const double g[3]);

@@ -111,6 +111,19 @@ def lib():
         L.orc_newton.argtypes = [vp, vp, vp, vp]
         L.orc_g2p.argtypes = [vp, d, vp, vp, i64, vp, vp, vp, vp, i32]
         L.orc_g2p.restype = i64
+        L.orc_g2p_mat.argtypes = [vp, d, vp, vp, i64, vp, vp, vp, vp, vp, vp, i32]
+        L.orc_g2p_mat.restype = i64
+        L.orc_water_pi.argtypes = [d, d]
+        L.orc_water_pi.restype = d
+        L.orc_water_psi_J.argtypes = [d, d]
+        L.orc_water_psi_J.restype = d
+        L.orc_water_jbase.argtypes = [d, d]
+        L.orc_water_jbase.restype = d
+        L.orc_water_tau.argtypes = [vp, d, vp]
+        L.orc_water_tau.restype = C.c_int
+        L.orc_water_psi.argtypes = [vp, d]
+        L.orc_water_psi.restype = d
+        L.orc_water_stretch.argtypes = [vp, d, vp]
         L.orc_explicit_force.argtypes = [vp, i32, vp, vp, vp, vp]
     return _lib
 
@@ -159,7 +172,7 @@ def _mats(materials) -> "C.Array":
     arr = (_Mat * MAXMAT)()
     for k, m in enumerate(materials):
         arr[k].E, arr[k].nu, arr[k].rho = float(m.E), float(m.nu), float(m.rho)
-        arr[k].kind = int(getattr(m, "kind", 0))  # 0 StVK-Hencky, 1 split Neo-Hookean
+        arr[k].kind = int(getattr(m, "kind", 0))  # 0 StVK-Hencky, 1 split Neo-Hookean, 2 water (kappa = E)
     return arr
 
 
@@ -263,6 +276,42 @@ def nh_cardano(p: float, q: float, dmin: float):
     br = C.c_int32(0)
     m = lib().orc_nh_cardano(float(p), float(q), float(dmin), C.byref(br))
     return m, br.value
+
+
+def water_pi(J: float, kappa: float) -> float:
+    """Water Kirchhoff pressure pi(J) = J psi'(J) = kappa J (J - 1) (§4.5)."""
+    return float(lib().orc_water_pi(float(J), float(kappa)))
+
+
+def water_psi_J(J: float, kappa: float) -> float:
+    """Water energy density psi(J) = kappa/2 (J - 1)^2."""
+    return float(lib().orc_water_psi_J(float(J), float(kappa)))
+
+
+def water_jbase(pi: float, kappa: float) -> float:
+    """J_base = (1 + sqrt(1 + 4 pi / kappa)) / 2, radicand clamped at 0."""
+    return float(lib().orc_water_jbase(float(pi), float(kappa)))
+
+
+def water_tau(F, kappa: float) -> np.ndarray:
+    F = _f64(F).reshape(9)
+    t = np.zeros(9)
+    if lib().orc_water_tau(_p(F), kappa, _p(t)) != 0:
+        raise ValueError("inverted F (det <= 0)")
+    return t.reshape(3, 3)
+
+
+def water_psi(F, kappa: float) -> float:
+    F = _f64(F).reshape(9)
+    return float(lib().orc_water_psi(_p(F), kappa))
+
+
+def water_stretch(tau, kappa: float) -> np.ndarray:
+    """Base stretch of a water slot: J_base(tr tau / 3)^{1/3} I."""
+    tau = _f64(tau).reshape(9)
+    S = np.zeros(9)
+    lib().orc_water_stretch(_p(tau), kappa, _p(S))
+    return S.reshape(3, 3)
 
 
 def stretch(tau, mu: float, lam: float) -> np.ndarray:
@@ -406,11 +455,17 @@ def explicit_force(grid: Grid, nmat: int, m_c, V_ck, tau_ck) -> np.ndarray:
     return f
 
 
-def g2p(grid: Grid, dt: float, m_c, v_i, x, v, F, G, clip: bool = False):
-    """Alg. 4. Returns updated copies (x, v, F, G)."""
+def g2p(grid: Grid, dt: float, m_c, v_i, x, v, F, G, clip: bool = False, mat=None, materials=None):
+    """Alg. 4. Returns updated copies (x, v, F, G).  With (mat, materials), water
+    particles (kind 2) update J_p by the trace form of P:316 and keep F_p = J_p^{1/3} I."""
     x, v, F, G = _f64(x).copy(), _f64(v).copy(), _f64(F).copy(), _f64(G).copy()
-    r = lib().orc_g2p(C.byref(grid.c()), float(dt), _p(_f64(m_c)), _p(_f64(v_i).reshape(-1, 3)), x.shape[0],
-                      _p(x), _p(v), _p(F), _p(G), int(clip))
+    if mat is not None and any(getattr(m, "kind", 0) == 2 for m in materials):
+        mat = np.ascontiguousarray(mat, dtype=np.int32)
+        r = lib().orc_g2p_mat(C.byref(grid.c()), float(dt), _p(_f64(m_c)), _p(_f64(v_i).reshape(-1, 3)),
+                              x.shape[0], _p(x), _p(v), _p(F), _p(G), _p(mat), _mats(materials), int(clip))
+    else:
+        r = lib().orc_g2p(C.byref(grid.c()), float(dt), _p(_f64(m_c)), _p(_f64(v_i).reshape(-1, 3)), x.shape[0],
+                          _p(x), _p(v), _p(F), _p(G), int(clip))
     if r != 0:
         raise ValueError(f"oracle g2p: particle {-r - 1} out of domain")
     return x, v, F, G
@@ -449,5 +504,6 @@ def prepare(scene, grid: Optional[Grid] = None, clip: bool = False):
 def step(scene, fixed_newton: int = 0, fixed_cg=None, solver=None, fixed_ls=None) -> StepResult:
     un, S, prob, v0 = prepare(scene)
     vnew, stats = prob.newton(v0, solver or scene.solver, fixed_newton, fixed_cg, fixed_ls)
-    parts = g2p(prob.grid, scene.dt, un.m_c, vnew, scene.x, scene.v, scene.F, scene.G)
+    parts = g2p(prob.grid, scene.dt, un.m_c, vnew, scene.x, scene.v, scene.F, scene.G, mat=scene.mat,
+                materials=scene.materials)
     return StepResult(un, S, prob, v0, vnew, stats, parts)

@@ -33,7 +33,8 @@ typedef struct {
 
 typedef struct {
     double E, nu, rho;
-    int32_t kind; /* 0 = StVK-Hencky, 1 = split Neo-Hookean (App. C) */
+    int32_t kind; /* 0 = StVK-Hencky, 1 = split Neo-Hookean (App. C),
+                     2 = J-based water (kappa = E, Table 2 caption P:536)       */
 } orc_material;
 
 typedef struct {
@@ -282,6 +283,47 @@ static void nh_dtau(const double F[9], const double dF[9], double mu, double kap
     }
 }
 
+/* ------------------------------------------------------------------------ */
+/* J-based water (§4.5):                                           */
+/*   psi(J) = kappa/2 (J - 1)^2 ;  pi(J) = J psi'(J) = kappa J (J - 1) ;       */
+/*   tau = pi I (the hydrostatic Kirchhoff stress; the particle carries only  */
+/*   J = det F_p) ;  J_base = (1 + sqrt(1 + 4 pi_c / kappa)) / 2 (positive    */
+/*   root; the radicand is clamped at 0, its minimum over J > 0 being 0 at J=1/2). */
+/* kappa is the material's E ("we use E in place of kappa").          */
+/* ------------------------------------------------------------------------ */
+double orc_water_pi(double J, double kappa) { return kappa * J * (J - 1.0); }
+double orc_water_psi_J(double J, double kappa) { return 0.5 * kappa * (J - 1.0) * (J - 1.0); }
+double orc_water_jbase(double pi, double kappa) {
+    double r = 1.0 + 4.0 * pi / kappa;
+    if (r < 0.0) r = 0.0;
+    return 0.5 * (1.0 + sqrt(r));
+}
+int orc_water_tau(const double F[9], double kappa, double tau[9]) {
+    double J = mat_det(F);
+    if (!(J > 0.0)) return -1;
+    for (int a = 0; a < 9; a++) tau[a] = (a % 4 == 0) ? orc_water_pi(J, kappa) : 0.0;
+    return 0;
+}
+double orc_water_psi(const double F[9], double kappa) {
+    double J = mat_det(F);
+    if (!(J > 0.0)) return INFINITY;
+    return orc_water_psi_J(J, kappa);
+}
+/* d tau along dF: dJ = J tr(F^{-1} dF), d pi = kappa (2J - 1) dJ */
+static void water_dtau(const double F[9], const double dF[9], double kappa, double dtau[9]) {
+    double J = mat_det(F), Fi[9], FidF[9];
+    mat_inv(F, Fi);
+    mat_mul(Fi, dF, FidF);
+    double dJ = J * (FidF[0] + FidF[4] + FidF[8]);
+    for (int a = 0; a < 9; a++) dtau[a] = (a % 4 == 0) ? kappa * (2.0 * J - 1.0) * dJ : 0.0;
+}
+/* base stretch of a water slot: S = J_base^{1/3} I, pi_c = tr(tau_c)/3 (det S = J_base) */
+void orc_water_stretch(const double tau[9], double kappa, double S[9]) {
+    double Jb = orc_water_jbase((tau[0] + tau[4] + tau[8]) / 3.0, kappa);
+    double s = cbrt(Jb);
+    for (int a = 0; a < 9; a++) S[a] = (a % 4 == 0) ? s : 0.0;
+}
+
 /* Cardano root of m^3 + p m + q = 0 on the admissible branch m > -min_i delta_i (App. C,
  * P:1305-1348; Eqs. cardano-one-real / cardano-three-real).  *branch = 1 (Delta >= 0) or 3. */
 static double cbrt_signed(double z) { return z < 0 ? -pow(-z, 1.0 / 3.0) : pow(z, 1.0 / 3.0); }
@@ -356,11 +398,13 @@ int orc_nh_stretch(const double tau[9], double mu, double kappa, double S[9], in
 /* ---- per-material dispatch (each material slot keeps its own constitutive law) ---- */
 static int law_tau(const orc_material *m, const double F[9], double tau[9]) {
     double mu, lam;
+    if (m->kind == 2) return orc_water_tau(F, m->E, tau);
     lame(m, &mu, &lam);
     return m->kind == 1 ? orc_nh_tau(F, mu, nh_kappa(mu, lam), tau) : orc_hencky_tau(F, mu, lam, tau);
 }
 static double law_psi(const orc_material *m, const double F[9]) {
     double mu, lam;
+    if (m->kind == 2) return orc_water_psi(F, m->E);
     lame(m, &mu, &lam);
     return m->kind == 1 ? orc_nh_psi(F, mu, nh_kappa(mu, lam)) : hencky_psi(F, mu, lam);
 }
@@ -519,7 +563,9 @@ void orc_stretch_all(const orc_grid *g, int32_t nmat, const orc_material *mats, 
             double *S = S_ck + ((int64_t)k * nc + c) * 9;
             if (V_ck[(int64_t)k * nc + c] != 0.0) {
                 const double *tau = tau_ck + ((int64_t)k * nc + c) * 9; /* Alg. 3 line 6 */
-                if (mats[k].kind == 1) {
+                if (mats[k].kind == 2) {
+                    orc_water_stretch(tau, mats[k].E, S); /* Eq. J_base */
+                } else if (mats[k].kind == 1) {
                     if (orc_nh_stretch(tau, mu, nh_kappa(mu, lam), S, NULL))
                         for (int a = 0; a < 9; a++) S[a] = NAN; /* outside the inversion domain */
                 } else {
@@ -640,6 +686,9 @@ static void slot_tangent(double dt, double V, const orc_material *m, const doubl
     if (m->kind == 1) { /* split Neo-Hookean: tau and its derivative directly (Eq. split-nh-tau) */
         orc_nh_tau(F, mu, nh_kappa(mu, lam), tau);
         nh_dtau(F, dF, mu, nh_kappa(mu, lam), dtau);
+    } else if (m->kind == 2) { /* water: tau = pi(J) I */
+        orc_water_tau(F, m->E, tau);
+        water_dtau(F, dF, m->E, dtau);
     }
     double Ai[9], AiT[9], dGT[9], dAiT[9], r1[9], r2[9];
     mat_inv(A, Ai);
@@ -898,8 +947,18 @@ int orc_newton(const orc_problem *P, const orc_solver_cfg *cfg, double *v, orc_s
 /* v_p = sum w_cp v_c ; G_p = sum w_cp G_c (weights from x_p^n) ;             */
 /* x_p += dt v_p ; F_p <- (I + dt G_p) F_p.   (v_c = G_c = 0 where m_c = 0)   */
 /* ------------------------------------------------------------------------ */
+/* Water particles (kind 2) carry only J_p: their F_p is J_p^{1/3} I, updated by
+ * J_p^{n+1} = (1 + dt tr(G_p)) J_p^n (the trace form; G_p = sum_c w_cp G_c^{n+1}). */
+int64_t orc_g2p_mat(const orc_grid *g, double dt, const double *m_c, const double *v_i, int64_t np,
+                    double *x, double *v, double *F, double *G, const int32_t *mat, const orc_material *mats,
+                    int32_t clip);
 int64_t orc_g2p(const orc_grid *g, double dt, const double *m_c, const double *v_i, int64_t np,
                 double *x, double *v, double *F, double *G, int32_t clip) {
+    return orc_g2p_mat(g, dt, m_c, v_i, np, x, v, F, G, NULL, NULL, clip);
+}
+int64_t orc_g2p_mat(const orc_grid *g, double dt, const double *m_c, const double *v_i, int64_t np,
+                    double *x, double *v, double *F, double *G, const int32_t *mat, const orc_material *mats,
+                    int32_t clip) {
     int64_t nc = ncells(g);
     double *vc = calloc(nc * 3, sizeof(double)), *Gc = calloc(nc * 9, sizeof(double));
     for (int ci = 0; ci < g->n[0]; ci++)
@@ -935,7 +994,13 @@ int64_t orc_g2p(const orc_grid *g, double dt, const double *m_c, const double *v
         }
         double A[9], Fn[9];
         for (int a = 0; a < 9; a++) A[a] = ((a % 4 == 0) ? 1.0 : 0.0) + dt * Gp[a];
-        mat_mul(A, F + 9 * p, Fn);
+        if (mat && mats[mat[p]].kind == 2) {
+            double Jn = (1.0 + dt * (Gp[0] + Gp[4] + Gp[8])) * mat_det(F + 9 * p);
+            double s = cbrt(Jn);
+            for (int a = 0; a < 9; a++) Fn[a] = (a % 4 == 0) ? s : 0.0;
+        } else {
+            mat_mul(A, F + 9 * p, Fn);
+        }
         for (int a = 0; a < 3; a++) {
             x[3 * p + a] += dt * vp[a];
             v[3 * p + a] = vp[a];

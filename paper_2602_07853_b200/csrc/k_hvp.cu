@@ -638,7 +638,266 @@ __global__ void __launch_bounds__(64, MINB) k_hvp_rp(int T_, const int *__restri
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// v5 (MPL_HVP_KERNEL=rq, default): rp with an instruction diet.  ncu of rp at cfg4: 72 M warp
+// instructions (IPC 1.9), 42 % of them integer / control flow (divergence around inactive lanes and
+// the masked scatter), shared-memory pipe 51 % busy with 2-way bank conflicts on a third of its
+// wavefronts.  Changes:
+//   * every lane has a distinct cell position: perm[t][j] lists the tile's cells, then its empty
+//     positions, so lanes without a cell run the same code with dG = 0 (no divergence, full-warp
+//     __syncwarp between scatter passes);
+//   * dG and the 8 corner forces by tensor-product sums/differences (17 + 10 adds per component
+//     instead of 24 + 24);
+//   * shared layouts chosen (exhaustive search) so a full tile's 32 cells per warp hit distinct banks
+//     in every pass: u halo at 5hx + 25hy + 2hz (16-byte slots, 129), forces at 8hx + 25hy + 10hz (173).
+// ---------------------------------------------------------------------------------------------
+__host__ __device__ constexpr int rq_u(int hx, int hy, int hz) { return 5 * hx + 25 * hy + 2 * hz; }
+__host__ __device__ constexpr int rq_f(int hx, int hy, int hz) { return 8 * hx + 25 * hy + 10 * hz; }
+constexpr int RQ_U = 132, RQ_F = 176;
+
+template <class T> struct RqSmem {
+    alignas(16) vec4<T> uh[2][RQ_U];
+    alignas(16) T mh[2][64];
+    alignas(16) uint8_t pm[2][64];  // lane permutation of the tile (cp.async'ed with the halo)
+    T F[2][3][RQ_F];
+    int nb[3][8];
+    int meta[3][4];  // cs, n (real cells), has, kstart
+    double red[2];
+};
+
+// role: bits 0-5 local node id, 6-8 neighbour slot, 9 owned, 10 interior, 11-18 u slot, 19-26 F slot
+__device__ __forceinline__ int rq_role(int h) {
+    if (h >= 125) return -1;
+    const int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
+    const int dp = ((hx >> 2) << 2) | ((hy >> 2) << 1) | (hz >> 2);
+    const int loc = local_id(hx & 3, hy & 3, hz & 3);
+    const int interior = (hx >= 1 && hx <= 3 && hy >= 1 && hy <= 3 && hz >= 1 && hz <= 3);
+    return loc | (dp << 6) | ((dp == 0) << 9) | (interior << 10) | (rq_u(hx, hy, hz) << 11) | (rq_f(hx, hy, hz) << 19);
+}
+
+template <class T, int MINB>
+__global__ void __launch_bounds__(64, MINB) k_hvp_rq(int T_, const int *__restrict__ nplus, const uint8_t *__restrict__ perm,
+                                               const int *__restrict__ hascells, const T *__restrict__ K,
+                                               const int *__restrict__ kstart, const int *__restrict__ ncell,
+                                               const T *__restrict__ nmass, const vec4<T> *__restrict__ u,
+                                               vec4<T> *__restrict__ Hu, double *__restrict__ uHu,
+                                               const CGSlot *__restrict__ cgs, int cgj, double cgthr,
+                                               const DevScalars *__restrict__ sc) {
+    __shared__ RqSmem<T> S;
+    const int tid = threadIdx.x;
+    if (cgs != nullptr) {
+        double rr = stripe_sum_bcast(cgs[cgj].rr);
+        if (sc->neg_curv || (cgj > 0 && rr <= cgthr)) return;
+    }
+    constexpr int VEC = KL<T>::VEC, NCH = KL<T>::NCH;
+    const int role0 = rq_role(tid), role1 = rq_role(tid + 64);
+    for (int i = tid; i < 2 * 3 * RQ_F; i += 64) (&S.F[0][0][0])[i] = T(0);
+    const int G = gridDim.x, t0 = blockIdx.x;
+    const int j = hvp_cell(tid);  // this lane's cell rank in every tile
+    auto load_meta = [&](int t) -> int {
+        if (t >= T_) return 0;
+        if (tid < 8) return tid ? nplus[8 * t + tid] : t;
+        if (tid == 9) return ncell[t];
+        if (tid == 10) return hascells[t];
+        if (tid == 11) return kstart[t];
+        return 0;
+    };
+    auto put_meta = [&](int m, int reg) {
+        if (tid < 8) S.nb[m][tid] = reg;
+        else if (tid < 12) S.meta[m][tid - 8] = reg;
+    };
+    auto issue_role = [&](int b, int m, int has, int role) {
+        if (role < 0) return;
+        const int loc = role & 63, dp = (role >> 6) & 7, owned = (role >> 9) & 1, uo = (role >> 11) & 255;
+        const int tt = S.nb[m][dp];
+        if ((has || owned) && tt >= 0) {
+            const int64_t n = (int64_t)tt * 64 + loc;
+#pragma unroll
+            for (int q = 0; q < (int)(sizeof(vec4<T>) / 16); q++)
+                cp_async16(reinterpret_cast<char *>(&S.uh[b][uo]) + 16 * q, reinterpret_cast<const char *>(u + n) + 16 * q);
+            if (owned) cp_async_real<T>(&S.mh[b][loc], nmass + n);
+        } else {
+            S.uh[b][uo] = mk4<T>(0, 0, 0, 0);
+            if (owned) S.mh[b][loc] = T(0);
+        }
+    };
+    T k[45];
+#pragma unroll
+    for (int i = 0; i < 45; i++) k[i] = T(0);
+    int anext = 0;
+    // tile t: tangent -> registers, lane permutation + halo -> shared slot b
+    auto issue = [&](int t, int b, int m) {
+        if (t < T_) {
+            const int ncp = S.meta[m][1], has = S.meta[m][2];
+            anext = has && j < ncp;
+            if (tid < 4) {
+                if (has) cp_async16(&S.pm[b][16 * tid], perm + (int64_t)t * 64 + 16 * tid);
+                else
+                    for (int q = 0; q < 16; q++) S.pm[b][16 * tid + q] = (uint8_t)(16 * tid + q);
+            }
+            if (anext) {
+                // 32-bit element offsets from the tile's block (a block is < 64 x 45 reals)
+                const T *blk = K + S.meta[m][3];
+                const int sl = hvp_slot(tid, ncp);
+                int off = sl * VEC;
+#pragma unroll
+                for (int c = 0; c < NCH; c++, off += ncp * VEC) ldg_vec<T>(blk + off, k + c * VEC);
+                k[44] = __ldg(blk + NCH * VEC * ncp + sl);
+            }
+            issue_role(b, m, has, role0);
+            issue_role(b, m, has, role1);
+        }
+        cp_async_commit();
+    };
+    put_meta(0, load_meta(t0));
+    put_meta(1, load_meta(t0 + G));
+    __syncthreads();
+    issue(t0, 0, 0);
+    int reg = load_meta(t0 + 2 * G);
+    double acc = 0.0;
+    int b = 0, m = 0;
+    for (int t = t0; t < T_; t += G) {
+        cp_async_wait<0>();
+        __syncthreads();  // (B) halo slot b complete; metadata slot m+1 visible
+        const int has = S.meta[m][2];
+        const int l = S.pm[b][j];
+        const T am = anext ? T(1) : T(0);
+        const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+        const vec4<T> *uh = S.uh[b] + rq_u(lx, ly, lz);
+        T dG[9];
+        {
+            vec4<T> w[8];
+#pragma unroll
+            for (int o = 0; o < 8; o++) w[o] = uh[rq_u((o >> 2) & 1, (o >> 1) & 1, o & 1)];
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+                T c[8];
+#pragma unroll
+                for (int o = 0; o < 8; o++) c[o] = a == 0 ? w[o].x : (a == 1 ? w[o].y : w[o].z);
+                // o = 4 ox + 2 oy + oz
+                const T p00 = c[1] + c[0], m00 = c[1] - c[0], p01 = c[3] + c[2], m01 = c[3] - c[2];
+                const T p10 = c[5] + c[4], m10 = c[5] - c[4], p11 = c[7] + c[6], m11 = c[7] - c[6];
+                const T pp0 = p01 + p00, pm0 = p01 - p00, mp0 = m01 + m00;
+                const T pp1 = p11 + p10, pm1 = p11 - p10, mp1 = m11 + m10;
+                dG[3 * a + 0] = (pp1 - pp0) * am;
+                dG[3 * a + 1] = (pm1 + pm0) * am;
+                dG[3 * a + 2] = (mp1 + mp0) * am;
+            }
+        }
+        T P[9];
+#pragma unroll
+        for (int r = 0; r < 9; r++) P[r] = k[kidx(r, r)] * dG[r];
+#pragma unroll
+        for (int r = 0; r < 9; r++)
+#pragma unroll
+            for (int q = r + 1; q < 9; q++) {
+                P[r] += k[kidx(r, q)] * dG[q];
+                P[q] += k[kidx(r, q)] * dG[r];
+            }
+        T qf = T(0);
+#pragma unroll
+        for (int r = 0; r < 9; r++) qf += P[r] * dG[r];
+        acc += (double)qf;
+        // k is free: the next tile's loads overlap the scatter and the node phase
+        const int bn = b ^ 1, mn = m == 2 ? 0 : m + 1;
+        issue(t + G, bn, mn);
+        {
+            T *Fw = S.F[tid >> 5][0] + rq_f(lx, ly, lz);
+            T ypp[3], ypm[3];
+#pragma unroll
+            for (int a = 0; a < 3; a++) { ypp[a] = P[3 * a + 1] + P[3 * a + 2]; ypm[a] = P[3 * a + 1] - P[3 * a + 2]; }
+#pragma unroll
+            for (int o = 0; o < 8; o++) {
+                const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+                const int fo = rq_f(ox, oy, oz);
+#pragma unroll
+                for (int a = 0; a < 3; a++) {
+                    const T yz = oy ? (oz ? ypp[a] : ypm[a]) : (oz ? -ypm[a] : -ypp[a]);
+                    Fw[a * RQ_F + fo] += (ox ? P[3 * a] : -P[3 * a]) + yz;
+                }
+                __syncwarp();
+            }
+        }
+        int64_t nidx[2];
+        T fm[2][3];
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+            const int role = r ? role1 : role0;
+            nidx[r] = -1;
+            fm[r][0] = fm[r][1] = fm[r][2] = T(0);
+            if (role < 0) continue;
+            const int loc = role & 63, dp = (role >> 6) & 7, owned = (role >> 9) & 1;
+            if (!has && !owned) continue;
+            const int tt = dp ? S.nb[m][dp] : t;
+            if (tt < 0) continue;
+            nidx[r] = (int64_t)tt * 64 + loc;
+            if (owned) {
+                const T mm = S.mh[b][loc];
+                const vec4<T> w = S.uh[b][(role >> 11) & 255];
+                fm[r][0] = mm * w.x; fm[r][1] = mm * w.y; fm[r][2] = mm * w.z;
+                acc += (double)(mm * (w.x * w.x + w.y * w.y + w.z * w.z));
+            }
+        }
+        __syncthreads();  // (C) F complete
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+            const int role = r ? role1 : role0;
+            if (role < 0) continue;
+            const int fo = (role >> 19) & 255, interior = (role >> 10) & 1;
+            T f[3];
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+                f[a] = S.F[0][a][fo] + S.F[1][a][fo] + fm[r][a];
+                S.F[0][a][fo] = T(0);
+                S.F[1][a][fo] = T(0);
+            }
+            if (nidx[r] < 0) continue;
+            if (interior) Hu[nidx[r]] = mk4<T>(f[0], f[1], f[2], T(0));
+            else if (f[0] != T(0) || f[1] != T(0) || f[2] != T(0)) atomic_add3<T>(Hu + nidx[r], f[0], f[1], f[2]);
+        }
+        const int m2 = mn == 2 ? 0 : mn + 1;
+        put_meta(m2, reg);  // metadata of tile t + 2G (slot last read by tile t - G)
+        reg = load_meta(t + 3 * G);
+        b = bn;
+        m = mn;
+    }
+    cp_async_wait<0>();
+    if (uHu) {
+        double v = warp_sum(acc);
+        if ((tid & 31) == 0) S.red[tid >> 5] = v;
+        __syncthreads();
+        if (tid == 0) {
+            double s = S.red[0] + S.red[1];
+            if (s != 0.0) atomicAdd(&uHu[blockIdx.x % NSTRIPE], s);
+        }
+    }
+}
+
 int g_num_sms = 0;
+
+template <class T, int MINB>
+mpl_status launch_rq(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
+                     double cgthr) {
+    static int per_sm[2] = {0, 0};
+    const int pi = sizeof(T) == 8;
+    if (per_sm[pi] == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        int occ = 0;
+        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_rq<T, MINB>, 64, 0));
+        per_sm[pi] = occ > 0 ? occ : 1;
+    }
+    int grid = g_num_sms * per_sm[pi];
+    if (grid > ctx->T) grid = ctx->T;
+    k_hvp_rq<T, MINB><<<grid, 64, 0, ctx->stream>>>(
+        ctx->T, (const int *)ctx->t_nplus.p, (const uint8_t *)ctx->t_perm.p, (const int *)ctx->t_hascells.p,
+        (const T *)ctx->K.p, (const int *)ctx->t_kstart.p, (const int *)ctx->t_ncell.p, (const T *)owned_mass(ctx),
+        (const vec4<T> *)u_tile, (vec4<T> *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p);
+    ctx->launches++;
+    MPL_CUDA(cudaGetLastError());
+    return MPL_OK;
+}
 
 template <class T, int MINB>
 mpl_status launch_rp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
@@ -706,10 +965,13 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
         // stages; "reg": one tile per CTA (v2)
         const char *e = getenv("MPL_HVP_KERNEL");
         variant = 5;
-        if (e && e[0] == 'r' && e[1] == 'p') variant = e[2] == '1' ? (e[3] == '2' ? 6 : 5) : 4;
+        if (e && e[0] == 'r' && e[1] == 'q') variant = e[2] == '8' ? 8 : 7;
+        else if (e && e[0] == 'r' && e[1] == 'p') variant = e[2] == '1' ? (e[3] == '2' ? 6 : 5) : 4;
         else if (e && e[0] == 'r') variant = 0;
         else if (e && e[0] == 'p' && e[4] == '3') variant = 3;
     }
+    if (variant == 7) return launch_rq<T, 10>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+    if (variant == 8) return launch_rq<T, 8>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
     if (variant == 2) return launch_pipe<T, 2>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
     if (variant == 4) return launch_rp<T, 1>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
     if (variant == 5) return launch_rp<T, 10>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);

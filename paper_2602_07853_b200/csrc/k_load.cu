@@ -60,7 +60,8 @@ template <class T>
 __global__ void k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ skey, const int *__restrict__ pid,
                       const int *__restrict__ nplus,
                       const int *__restrict__ cellof, const vec4<T> *__restrict__ vc, const T *__restrict__ Gc,
-                      T *__restrict__ x, T *__restrict__ v, T *__restrict__ F, T *__restrict__ G) {
+                      T *__restrict__ x, T *__restrict__ v, T *__restrict__ F, T *__restrict__ G,
+                      const int *__restrict__ mat, unsigned water_mask) {
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= np || pid[p] < 0) return;  // ghosts (slab ranks) are advected by their owner
     const int key = skey[p];
@@ -97,7 +98,20 @@ __global__ void k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ s
         Fp[a] = F[9 * p + a];
         A[a] = dt * Gp[a] + ((a % 4 == 0) ? T(1) : T(0));
     }
-    mm3(A, Fp, Fn);
+    if ((water_mask >> mat[p]) & 1u) {
+        // water particle: J^{n+1} = (1 + dt tr G_p) J^n, F_p = J^{1/3} I (J - 1 kept exact in
+        // the product (1 + a)(1 + b) - 1 = a + b + a b)
+        T H[9];
+#pragma unroll
+        for (int a = 0; a < 9; a++) H[a] = Fp[a] - ((a % 4 == 0) ? T(1) : T(0));
+        const T jm1 = det_ipm1(H), da = dt * (Gp[0] + Gp[4] + Gp[8]);
+        const T jn1 = jm1 + da + jm1 * da;
+        const T s = T(1) + mexpm1(mlog1p(jn1) / T(3));
+#pragma unroll
+        for (int a = 0; a < 9; a++) Fn[a] = (a % 4 == 0) ? s : T(0);
+    } else {
+        mm3(A, Fp, Fn);
+    }
 #pragma unroll
     for (int a = 0; a < 3; a++) {
         x[3 * p + a] = xp[a] + dt * vp[a];
@@ -191,7 +205,8 @@ mpl_status g2p_impl(mpl_ctx ctx, double dt) {
                                                     (const int *)ctx->t_nplus.p, (const int *)ctx->t_cellof.p,
                                                     (const vec4<T> *)ctx->q_vc.p, (const T *)ctx->q_Gc.p,
                                                     (T *)ctx->px[c].p, (T *)ctx->pv.p, (T *)ctx->pF[c].p,
-                                                    (T *)ctx->pG.p); ctx->launches++;
+                                                    (T *)ctx->pG.p, (const int *)ctx->pmat[c].p,
+                                                    water_mask(ctx->mats)); ctx->launches++;
     MPL_CUDA(cudaGetLastError());
     MPL_CUDA(cudaStreamSynchronize(st));
     ctx->resampled = false;  // quadrature state is consumed

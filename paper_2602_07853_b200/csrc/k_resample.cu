@@ -159,6 +159,30 @@ __device__ __forceinline__ void nh_tau(const T F[9], T mu, T kappa, T tau[6]) {
     tau[5] = s * B[2];
 }
 
+// ---- J-based water (§4.5): tau = pi I, pi = kappa J (J - 1), J = det F_p ----------------
+// (the particle carries only J; kappa = E).  J - 1 from the cancellation-free det(I + H) - 1.
+template <class T>
+__device__ __forceinline__ void water_tau(const T F[9], T kappa, T tau[6]) {
+    T H[9];
+#pragma unroll
+    for (int a = 0; a < 9; a++) H[a] = F[a] - ((a % 4 == 0) ? T(1) : T(0));
+    const T jm1 = det_ipm1(H);
+    const T pi = kappa * (T(1) + jm1) * jm1;
+    tau[0] = tau[1] = tau[2] = pi;
+    tau[3] = tau[4] = tau[5] = T(0);
+}
+
+// Water slot base stretch (Eq. J_base) in fp64: pi_c = tr(tau_c)/3, r = 1 + 4 pi_c/kappa
+// (clamped at 0), J_base - 1 = (r - 1) / (2 (sqrt r + 1)), S = J_base^{1/3} I -> E = (J_base^{1/3} - 1) I.
+__device__ __forceinline__ void water_stretch_E(const double tau[6], double kappa, double E[6]) {
+    const double x = 4.0 * (tau[0] + tau[1] + tau[2]) / (3.0 * kappa);  // r - 1
+    const double xr = x < -1.0 ? -1.0 : x;
+    const double jbm1 = xr / (2.0 * (sqrt(1.0 + xr) + 1.0));
+    const double sm1 = expm1(log1p(jbm1) / 3.0);
+    E[0] = E[1] = E[2] = sm1;
+    E[3] = E[4] = E[5] = 0.0;
+}
+
 // ---- split Neo-Hookean stretch reconstruction (App. C), in fp64 -------
 // tau = U diag(tau_i) U^T; alpha = tr/3; J = sqrt(1 + 2 alpha / kappa); s = mu J^{-2/3};
 // delta_i = (tau_i - alpha)/s; m solves m^3 + S2 m + (S3 - J^2) = 0 on the branch m > -min delta
@@ -245,6 +269,7 @@ __global__ void k_scatter(GridP g, MatP mp, int64_t np, const int *__restrict__ 
     T mass = T(mp.rho[m]) * Vp;
     T tau[6];
     if (mp.kind[m] == 1) nh_tau(Fp, mu, T(mp.kappa[m]), tau);  // Alg. 2 line 3, per-material law
+    else if (mp.kind[m] == 2) water_tau(Fp, T(mp.kappa[m]), tau);
     else hencky_tau(Fp, mu, lam, tau);
     T f[3];
 #pragma unroll
@@ -310,133 +335,25 @@ __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, cons
     }
 }
 
+// perm[t][j]: local position of the tile's j-th cell (j < n, increasing l), then its unoccupied
+// positions in increasing order: a permutation of 0..63 that gives every HVP lane a distinct position.
 __global__ void k_cell_list(int T_, const unsigned long long *__restrict__ cmask, const int *__restrict__ cstart,
-                            uint8_t *__restrict__ clocal, int *__restrict__ cellof) {
+                            uint8_t *__restrict__ clocal, int *__restrict__ cellof, uint8_t *__restrict__ perm) {
     int t = blockIdx.x;
     int l = threadIdx.x;
     unsigned long long m = cmask[t];
     int cs = cstart[t], ce = cstart[t + 1];
+    int c = __popcll(m);
+    const int r = __popcll(m & ((1ull << l) - 1ull));
     if ((m >> l) & 1ull) {
-        int r = __popcll(m & ((1ull << l) - 1ull));
         clocal[cs + r] = (uint8_t)l;
         cellof[t * 64 + l] = cs + r;
+        perm[t * 64 + r] = (uint8_t)l;
     } else {
         cellof[t * 64 + l] = -1;
+        perm[t * 64 + c + (l - r)] = (uint8_t)l;
     }
-    int c = __popcll(m);
     if (cs + c + l < ce) clocal[cs + c + l] = 0xFF;
-}
-
-// ---- a2-a4: P2Q gather + normalisation + stretch reconstruction (per cell) --------------------
-// One thread per structural cell of the tile gathers the particles of its 8 base-cell buckets.
-// Outputs (compact cell cc): q_m = m_c, q_mv = (mv)_c, q_mG = (mG)_c (unnormalised contents),
-// per material slot k: [V_ck, E_ck = S_ck - I (6), tau_ck (6)] with S from Eqs. hencky-ei/sigmai.
-template <class T>
-__global__ void __launch_bounds__(64) k_p2q(GridP g, MatP mp, const int *__restrict__ coord,
-                                            const int *__restrict__ nminus, const int *__restrict__ bstart,
-                                            const int *__restrict__ cellof, const T *__restrict__ rec,
-                                            T *__restrict__ q_m, T *__restrict__ q_mv, T *__restrict__ q_mG,
-                                            T *__restrict__ q_slot, DevScalars *sc) {
-    int t = blockIdx.x;
-    int l = threadIdx.x;
-    int cc = cellof[t * 64 + l];
-    if (cc < 0) return;
-    int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
-    int cx = coord[3 * t] * 4 + lx, cy = coord[3 * t + 1] * 4 + ly, cz = coord[3 * t + 2] * 4 + lz;
-    const int nmat = mp.nmat;
-    T m = 0, mv[3] = {0, 0, 0}, mG[9];
-#pragma unroll
-    for (int a = 0; a < 9; a++) mG[a] = 0;
-    T V[MPL_MAXMAT], Vt[MPL_MAXMAT][6];
-#pragma unroll
-    for (int k = 0; k < MPL_MAXMAT; k++) {
-        V[k] = 0;
-#pragma unroll
-        for (int a = 0; a < 6; a++) Vt[k][a] = 0;
-    }
-    const T dx = T(g.dx);
-    for (int o = 0; o < 8; o++) {
-        int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
-        if (cx - ox < 0 || cy - oy < 0 || cz - oz < 0) continue;
-        int bx = lx - ox, by = ly - oy, bz = lz - oz;
-        int dm = ((bx < 0) << 2) | ((by < 0) << 1) | (bz < 0);
-        int tt = nminus[8 * t + dm];
-        if (tt < 0) continue;
-        int kk = tt * 64 + local_id(bx & 3, by & 3, bz & 3);
-        int s = bstart[kk], e = bstart[kk + 1];
-        for (int p = s; p < e; p++) {
-            const T *r = rec + (int64_t)p * REC;
-            // cell = base + o  =>  w = prod_a (o_a ? f_a : 1 - f_a)
-            T w = (ox ? r[0] : T(1) - r[0]) * (oy ? r[1] : T(1) - r[1]) * (oz ? r[2] : T(1) - r[2]);
-            T mass = r[3];
-            m += w * mass;
-            // m (v + G (x_c - x_p)) = a + dx (mG) o   (x_c - x_p = dx (o - f))
-            mv[0] += w * (r[4] + dx * ((ox ? r[7] : T(0)) + (oy ? r[8] : T(0)) + (oz ? r[9] : T(0))));
-            mv[1] += w * (r[5] + dx * ((ox ? r[10] : T(0)) + (oy ? r[11] : T(0)) + (oz ? r[12] : T(0))));
-            mv[2] += w * (r[6] + dx * ((ox ? r[13] : T(0)) + (oy ? r[14] : T(0)) + (oz ? r[15] : T(0))));
-#pragma unroll
-            for (int a = 0; a < 9; a++) mG[a] += w * r[7 + a];
-            int k = (int)r[23];
-#pragma unroll
-            for (int q = 0; q < MPL_MAXMAT; q++) {
-                if (q == k) {
-                    V[q] += w * r[16];
-#pragma unroll
-                    for (int a = 0; a < 6; a++) Vt[q][a] += w * r[17 + a];
-                }
-            }
-        }
-    }
-    q_m[cc] = m;
-#pragma unroll
-    for (int a = 0; a < 3; a++) q_mv[3 * (int64_t)cc + a] = mv[a];
-#pragma unroll
-    for (int a = 0; a < 9; a++) q_mG[9 * (int64_t)cc + a] = mG[a];
-#pragma unroll
-    for (int k = 0; k < MPL_MAXMAT; k++) {
-        if (k >= nmat) break;
-        T *sl = q_slot + ((int64_t)cc * nmat + k) * 16;
-        T tau[6] = {0, 0, 0, 0, 0, 0};
-        T E[6] = {0, 0, 0, 0, 0, 0};
-        if (V[k] != T(0) && mp.kind[k] == 1) {
-            T iv = T(1) / V[k];
-#pragma unroll
-            for (int a = 0; a < 6; a++) tau[a] = Vt[k][a] * iv;  // Eq. vtau normalisation
-            double td[6], Ed[6];
-#pragma unroll
-            for (int a = 0; a < 6; a++) td[a] = (double)tau[a];
-            if (nh_stretch_E(td, mp.mu[k], mp.kappa[k], Ed)) {
-#pragma unroll
-                for (int a = 0; a < 6; a++) E[a] = T(Ed[a]);
-            } else {
-#pragma unroll
-                for (int a = 0; a < 6; a++) E[a] = T(0);
-                sc->nonfinite = 1;  // outside the inversion domain (reported by resample)
-            }
-        } else if (V[k] != T(0)) {
-            T iv = T(1) / V[k];
-#pragma unroll
-            for (int a = 0; a < 6; a++) tau[a] = Vt[k][a] * iv;  // Eq. vtau normalisation
-            T mu = T(mp.mu[k]), lam = T(mp.lam[k]);
-            T A[9] = {tau[0], tau[3], tau[5], tau[3], tau[1], tau[4], tau[5], tau[4], tau[2]};
-            T w[3], U[9];
-            sym_eig3(A, w, U);
-            T s = (w[0] + w[1] + w[2]) / (T(2) * mu + T(3) * lam);  // Eq. hencky-trace
-            T em[3];
-#pragma unroll
-            for (int i = 0; i < 3; i++) em[i] = mexpm1((w[i] - lam * s) / (T(2) * mu));  // sigma_i - 1
-            E[0] = U[0] * U[0] * em[0] + U[1] * U[1] * em[1] + U[2] * U[2] * em[2];
-            E[1] = U[3] * U[3] * em[0] + U[4] * U[4] * em[1] + U[5] * U[5] * em[2];
-            E[2] = U[6] * U[6] * em[0] + U[7] * U[7] * em[1] + U[8] * U[8] * em[2];
-            E[3] = U[0] * U[3] * em[0] + U[1] * U[4] * em[1] + U[2] * U[5] * em[2];
-            E[4] = U[3] * U[6] * em[0] + U[4] * U[7] * em[1] + U[5] * U[8] * em[2];
-            E[5] = U[0] * U[6] * em[0] + U[1] * U[7] * em[1] + U[2] * U[8] * em[2];
-        }
-        sl[0] = V[k];
-#pragma unroll
-        for (int a = 0; a < 6; a++) { sl[1 + a] = E[a]; sl[7 + a] = tau[a]; }
-        sl[13] = sl[14] = sl[15] = T(0);
-    }
 }
 
 // ---- a2-a4, parallel form (default): 8 lanes per cell --------------------------------------------
@@ -454,6 +371,15 @@ __device__ __forceinline__ T grp_sum(T v) {  // sum over the aligned 8-lane grou
 
 template <class T>
 __device__ __forceinline__ void stretch_slot(const MatP &mp, int k, const T tau[6], T E[6], DevScalars *sc) {
+    if (mp.kind[k] == 2) {
+        double td[6], Ed[6];
+#pragma unroll
+        for (int a = 0; a < 6; a++) td[a] = (double)tau[a];
+        water_stretch_E(td, mp.kappa[k], Ed);
+#pragma unroll
+        for (int a = 0; a < 6; a++) E[a] = T(Ed[a]);
+        return;
+    }
     if (mp.kind[k] == 1) {
         double td[6], Ed[6];
 #pragma unroll
@@ -832,6 +758,7 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CHECK(ensure(ctx, ctx->t_bcount, ((size_t)T_ * 64 + 1) * 4 + 16));
     MPL_CHECK(ensure(ctx, ctx->t_bstart, ((size_t)T_ * 64 + 1) * 4 + 16));
     MPL_CHECK(ensure(ctx, ctx->t_cellof, (size_t)T_ * 64 * 4 + 16));
+    MPL_CHECK(ensure(ctx, ctx->t_perm, (size_t)T_ * 64 + 16));
     k_tiles<<<nblk(N, 256), 256, 0, st>>>(g, (const int *)ctx->nflag.p, (int *)ctx->tile_of.p, (int *)ctx->t_coord.p); ctx->launches++;
     DBG_GUARDS("resample #3");
     if (T_) k_tile_nbrs<<<nblk(T_, 128), 128, 0, st>>>(g, T_, (const int *)ctx->t_coord.p, (const int *)ctx->tile_of.p,
@@ -922,7 +849,8 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CHECK(ensure(ctx, ctx->K, (size_t)Ktot * s + 256));
     if (T_) {
         k_cell_list<<<T_, 64, 0, st>>>(T_, (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_cstart.p,
-                                       (uint8_t *)ctx->c_local.p, (int *)ctx->t_cellof.p); ctx->launches++;
+                                       (uint8_t *)ctx->c_local.p, (int *)ctx->t_cellof.p, (uint8_t *)ctx->t_perm.p);
+        ctx->launches++;
     DBG_GUARDS("resample #8");
 #define P2Q_ARGS                                                                                             \
     g, ctx->mats, (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p, (const int *)ctx->t_bstart.p, \

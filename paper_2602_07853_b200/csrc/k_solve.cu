@@ -128,6 +128,55 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
                         B[3 * a + b] = val;
                         B[3 * b + a] = val;
                     }
+                if (mp.kind[k] == 2) {
+                    // ---- J-based water slot (PAPER §4.5): psi = kappa/2 (J-1)^2, J = det(A S),
+                    //      tau = pi I, pi = kappa J (J-1); column (a,b): dJ/J = dt (F^{-T} S)[a][b],
+                    //      dtau = kappa (2J-1) J (dJ/J) I ----
+                    const T kap = T(mp.kappa[k]);
+                    const T jm1 = det_ipm1(H), Jv = T(1) + jm1;
+                    e_loc += (double)(V * T(0.5) * kap * jm1 * jm1);
+                    if (MODE == LIN_ENERGY) continue;
+                    const T pi = kap * Jv * jm1;
+                    T TA[9];  // tau A^{-T}
+#pragma unroll
+                    for (int a = 0; a < 9; a++) TA[a] = pi * AiT[a];
+                    const T sV = dt * V;
+#pragma unroll
+                    for (int a = 0; a < 9; a++) Pc[a] += sV * TA[a];
+                    if (MODE == LIN_FULL) {
+                        T F[9], S[9], FiT[9], M[9];
+#pragma unroll
+                        for (int a = 0; a < 9; a++) {
+                            F[a] = H[a] + ((a % 4 == 0) ? T(1) : T(0));
+                            S[a] = E[a] + ((a % 4 == 0) ? T(1) : T(0));
+                        }
+                        inv_transpose3(F, FiT);
+                        mm3(FiT, S, M);
+                        const T kscale = sV * T(1.0 / 16.0) * T(g.inv_dx * g.inv_dx);
+                        const T dpi_c = kap * (T(2) * Jv - T(1)) * Jv * dt;
+                        T *Kr = Ks + j * 45;
+#pragma unroll
+                        for (int a = 0; a < 3; a++)
+#pragma unroll
+                            for (int b = 0; b < 3; b++) {
+                                const T dpi = dpi_c * M[3 * a + b];
+                                const int cidx = 3 * a + b;
+#pragma unroll
+                                for (int i = 0; i < 3; i++)
+#pragma unroll
+                                    for (int jj = 0; jj < 3; jj++) {
+                                        T r1 = dpi * AiT[3 * i + jj];
+                                        T r2 = -dt * TA[3 * i + b] * AiT[3 * a + jj];
+                                        T val = kscale * (r1 + r2);
+                                        const int r = 3 * i + jj;
+                                        if (r == cidx) Kr[kidx(r, r)] += val;
+                                        else if (r < cidx) Kr[kidx(r, cidx)] += T(0.5) * val;
+                                        else Kr[kidx(cidx, r)] += T(0.5) * val;
+                                    }
+                            }
+                    }
+                    continue;
+                }
                 if (mp.kind[k] == 1) {
                     // ---- split Neo-Hookean slot (PAPER §4.3.2; stable forms in mpl_common.cuh) ----
                     const T kap = T(mp.kappa[k]);

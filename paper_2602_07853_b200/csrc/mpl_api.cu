@@ -292,9 +292,21 @@ mpl_status mpl_set_materials(mpl_ctx ctx, int32_t n, const mpl_material *mats) {
     if (!ctx || !mats || n < 1 || n > MPL_MAXMAT) return MPL_ERR_INVALID_ARG;
     for (int k = 0; k < n; k++) {
         const mpl_material &m = mats[k];
-        if (m.kind != 0 && m.kind != 1) {
-            ctx->err = "material kind must be 0 (StVK-Hencky) or 1 (split Neo-Hookean)";
+        if (m.kind != 0 && m.kind != 1 && m.kind != 2) {
+            ctx->err = "material kind must be 0 (StVK-Hencky), 1 (split Neo-Hookean) or 2 (water)";
             return MPL_ERR_UNSUPPORTED;
+        }
+        if (m.kind == 2) {  // J-based water: kappa = E; no shear modulus
+            if (!(m.E > 0) || !(m.rho > 0)) {
+                ctx->err = "material " + std::to_string(k) + ": water needs kappa = E > 0 and rho > 0 (P:297)";
+                return MPL_ERR_INVALID_ARG;
+            }
+            ctx->mats.kind[k] = 2;
+            ctx->mats.mu[k] = 0.0;
+            ctx->mats.lam[k] = m.E;
+            ctx->mats.kappa[k] = m.E;
+            ctx->mats.rho[k] = m.rho;
+            continue;
         }
         double mu = m.E / (2.0 * (1.0 + m.nu)), lam = m.E * m.nu / ((1.0 + m.nu) * (1.0 - 2.0 * m.nu));
         // both laws need mu > 0 and kappa = 2/3 mu + lam > 0 (P:227 for Hencky; P:268 J = sqrt(1 + 2 alpha/kappa))
@@ -533,6 +545,9 @@ mpl_status mpl_hvp_bench(mpl_ctx ctx, const void *u, void *Hu, int32_t reps, dou
     cudaEventCreate(&b);
     // timed: the HVP kernel alone, back to back (Hu accumulates; zeroed once), then one clean product
     MPL_CUDA(cudaMemsetAsync(ctx->n_u2.p, 0, (size_t)ctx->T * 64 * (ctx->precision == 64 ? 32 : 16), ctx->stream));
+    // one untimed launch first (first-call occupancy query and module load stay out of the timing)
+    MPL_CHECK(ctx->precision == 64 ? launch_hvp<double>(ctx, ctx->n_u.p, ctx->n_u2.p, nullptr, nullptr, 0, 0.0)
+                                   : launch_hvp<float>(ctx, ctx->n_u.p, ctx->n_u2.p, nullptr, nullptr, 0, 0.0));
     cudaEventRecord(a, ctx->stream);
     for (int i = 0; i < reps; i++)
         MPL_CHECK(ctx->precision == 64

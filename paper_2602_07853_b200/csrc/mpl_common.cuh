@@ -71,7 +71,7 @@ struct GridP {
 
 struct MatP {
     int nmat;
-    int kind[MPL_MAXMAT];  // 0 StVK-Hencky, 1 split Neo-Hookean
+    int kind[MPL_MAXMAT];  // 0 StVK-Hencky, 1 split Neo-Hookean, 2 J-based water (kappa = E)
     double mu[MPL_MAXMAT], lam[MPL_MAXMAT], rho[MPL_MAXMAT], kappa[MPL_MAXMAT];  // kappa = 2/3 mu + lam
 };
 
@@ -255,6 +255,14 @@ template <class T> struct KL {
     static constexpr int NCH = 45 / VEC;
     static constexpr int REM = 45 - NCH * VEC;
 };
+// bit k set: material k is J-based water (kind 2; Load updates J only)
+inline unsigned water_mask(const MatP &mp) {
+    unsigned m = 0;
+    for (int k = 0; k < mp.nmat; k++)
+        if (mp.kind[k] == 2) m |= 1u << k;
+    return m;
+}
+
 // Tangent layout per tile: n = the tile's real cells (no padding), block of 45 n reals (rounded up
 // to 4) at t_kstart[t].  Cell j of a tile is handled by HVP thread (warp j & 1, lane j >> 1), so the
 // two warps of a 64-thread CTA get ceil(n/2) and floor(n/2) cells; the tangent of cell j is stored at
@@ -347,7 +355,7 @@ struct mpl_ctx_s {
     int64_t launches = 0;  // kernels launched by this context (cumulative)
     int dense_n = 0;  // nb0*nb1*nb2
     DevBuf cflag, nflag, tile_of, scan_tmp;
-    DevBuf t_coord, t_nplus, t_nminus, t_cstart, t_ccount, t_hascells, t_bcount, t_bstart, t_cellof, t_cmask;
+    DevBuf t_coord, t_nplus, t_nminus, t_cstart, t_ccount, t_hascells, t_bcount, t_bstart, t_cellof, t_cmask, t_perm;
     DevBuf t_ncell, t_kcnt, t_kstart;  // real cells per tile; tangent reals per tile (rounded to 4) and offsets
     DevBuf c_local;
     // quadrature (compact cells)
@@ -422,6 +430,7 @@ template <class F> void for_each_buf(mpl_ctx ctx, F f) {
         {"t_bstart", ctx->t_bstart},
         {"t_cellof", ctx->t_cellof},
         {"t_cmask", ctx->t_cmask},
+        {"t_perm", ctx->t_perm},
         {"c_local", ctx->c_local},
         {"q_m", ctx->q_m},
         {"q_mv", ctx->q_mv},

@@ -33,7 +33,7 @@ class Material:
     E: float
     nu: float
     rho: float
-    kind: int = 0  # 0 StVK-Hencky, 1 split Neo-Hookean
+    kind: int = 0  # 0 StVK-Hencky, 1 split Neo-Hookean, 2 water (kappa = E)
 
 
 @dataclasses.dataclass

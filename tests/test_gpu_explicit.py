@@ -28,7 +28,7 @@ def explicit_oracle(sc):
     free = act & (prob.freed != 0)
     v1 = v0.copy()
     v1[free] = prob.vhat[free] + sc.dt * f[free] / un.m_i[free][:, None]
-    parts = oracle.g2p(grid, sc.dt, un.m_c, v1, sc.x, sc.v, sc.F, sc.G)
+    parts = oracle.g2p(grid, sc.dt, un.m_c, v1, sc.x, sc.v, sc.F, sc.G, mat=sc.mat, materials=sc.materials)
     return grid, un, f, v1, parts
 
 
@@ -44,6 +44,7 @@ SCENES = {
     "cfg1b_fp32": lambda: scenes.cfg1(prestrain=True, precision=32),
     "cfg2s_fp64_dirichlet": lambda: _prestrained(small_cfg2(64)),
     "lawmix_fp64": lambda: two_material(64, (1, 0)),
+    "watermix_fp64": lambda: two_material(64, (0, 2)),
 }
 
 

@@ -29,7 +29,7 @@ def small_cfg2(precision=32, k=16):
 
 def two_material(precision=64, kinds=(0, 0)):
     """Two materials mixed in the same cells + a sticky floor (exercises slots and Dirichlet); kinds
-    selects each material's law (0 StVK-Hencky, 1 split Neo-Hookean)."""
+    selects each material's law (0 StVK-Hencky, 1 split Neo-Hookean, 2 J-based water)."""
     n = 16
     cells = scenes.cells_box([4, 2, 4], [12, 10, 12])
     dt_ = np.float32 if precision == 32 else np.float64
@@ -47,6 +47,24 @@ def two_material(precision=64, kinds=(0, 0)):
                             scenes.SolverCfg(eps_cg=tol[0], eps_newton=tol[1]), 1)
 
 
+def water_block(precision=64):
+    """A water block (kind 2, kappa = E = 2e5) with J_p ~ U(0.97, 1.03) (F_p = J_p^{1/3} I),
+    random velocities, over a sticky floor."""
+    n = 16
+    cells = scenes.cells_box([4, 2, 4], [12, 9, 11])
+    dt_ = np.float32 if precision == 32 else np.float64
+    x = scenes.stratified(cells, n, 2, seed=2, dtype=dt_)
+    rng = np.random.default_rng(7)
+    v = rng.normal(0, 0.3, size=x.shape)
+    J = rng.uniform(0.97, 1.03, size=x.shape[0])
+    F = (J[:, None] ** (1 / 3)) * np.eye(3).ravel()[None, :]
+    floor = scenes.DirichletBox((-1e9, -1e9, -1e9), (1e9, 3 / n, 1e9), (0.0, 0.0, 0.0))
+    tol = (1e-8, 1e-9) if precision == 64 else (1e-5, 1e-5)
+    return scenes._assemble("water", precision, n, 1e-3, [scenes.Material(2e5, 0.0, 1000.0, 2)], x, v, F,
+                            np.zeros((x.shape[0], 9)), np.zeros(x.shape[0], np.int32), 8, [floor],
+                            scenes.SolverCfg(eps_cg=tol[0], eps_newton=tol[1]), 1)
+
+
 SCENES = {
     "cfg1": lambda: scenes.cfg1(),
     "cfg1b": lambda: scenes.cfg1(prestrain=True),
@@ -60,6 +78,10 @@ SCENES = {
                                            materials=[scenes.Material(1e4, 0.3, 1000.0, 1)]),
     "lawmix_fp64": lambda: two_material(64, (0, 1)),
     "lawmix_fp32": lambda: two_material(32, (1, 0)),
+    # J-based water: alone, and water + StVK-Hencky in the same cells (sand-and-water shape)
+    "water_fp64": lambda: water_block(64),
+    "watermix_fp64": lambda: two_material(64, (0, 2)),
+    "watermix_fp32": lambda: two_material(32, (2, 0)),
 }
 
 
@@ -163,7 +185,8 @@ def test_full_step_parity(pair):
     assert rel_l2(v_g, v_o[pair.nid]) <= tol
     ctx.transfer_to_particles(sc.dt)
     x_g, vp_g, F_g, G_g = ctx.get_particles()
-    x_o, vp_o, F_o, G_o = oracle.g2p(pair.grid, sc.dt, pair.un.m_c, v_o, sc.x, sc.v, sc.F, sc.G)
+    x_o, vp_o, F_o, G_o = oracle.g2p(pair.grid, sc.dt, pair.un.m_c, v_o, sc.x, sc.v, sc.F, sc.G, mat=sc.mat,
+                                     materials=sc.materials)
     assert rel_l2(x_g, x_o) <= tol
     assert rel_l2(vp_g, vp_o) <= tol
     assert rel_l2(F_g, F_o) <= tol

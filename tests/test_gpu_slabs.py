@@ -44,6 +44,7 @@ CASES = {
     "cfg2s_fp64_R4": (lambda: small_cfg2(64), [0, 3, 4, 5, 8]),
     "mix_fp64_R2": (lambda: two_material(64), [0, 2, 4]),
     "lawmix_fp32_R2": (lambda: two_material(32, (1, 0)), [0, 2, 4]),  # split Neo-Hookean + Hencky
+    "watermix_fp64_R2": (lambda: two_material(64, (0, 2)), [0, 2, 4]),  # Hencky + J-based water
 }
 
 
@@ -167,7 +168,8 @@ def test_replayed_step(run):
     ids = np.concatenate([o["ids"] for o in run.res])
     assert np.array_equal(np.sort(ids), np.arange(sc.n_particles))
     order = np.argsort(ids)
-    x_o, vp_o, F_o, G_o = oracle.g2p(run.grid, sc.dt, run.un.m_c, run.v_o, sc.x, sc.v, sc.F, sc.G)
+    x_o, vp_o, F_o, G_o = oracle.g2p(run.grid, sc.dt, run.un.m_c, run.v_o, sc.x, sc.v, sc.F, sc.G, mat=sc.mat,
+                                     materials=sc.materials)
     for key, ref, t in (("x", x_o, tol), ("pv", vp_o, tol), ("F", F_o, tol), ("G", G_o, tol * 10)):
         got = np.concatenate([o[key] for o in run.res])[order]
         assert rel_l2(got, ref) <= t, key

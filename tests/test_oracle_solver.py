@@ -27,8 +27,14 @@ def make_scene(n=8, lo=2, hi=6, E=1e8, nu=0.3, rho=1000.0, dt=1e-3, prestrain=Tr
     v = vel * rng.normal(size=x.shape)
     F = scenes._prestrain(x.shape[0], seed + 3) if prestrain else np.tile(np.eye(3).ravel(), (x.shape[0], 1))
     mat = rng.integers(0, nmat, size=x.shape[0]).astype(np.int32)
-    # kind: 0 StVK-Hencky, 1 split Neo-Hookean, "mix": one of each (material slots k = 0, 1)
-    kinds = [k % 2 for k in range(nmat)] if kind == "mix" else [kind] * nmat
+    # kind: 0 StVK-Hencky, 1 split Neo-Hookean, 2 water; "mix": Hencky + Neo-Hookean slots,
+    # "wmix": Hencky + water slots (material slots k = 0, 1)
+    if kind == "mix":
+        kinds = [k % 2 for k in range(nmat)]
+    elif kind == "wmix":
+        kinds = [2 * (k % 2) for k in range(nmat)]
+    else:
+        kinds = [kind] * nmat
     mats = [scenes.Material(E * (1 + 0.7 * k), nu, rho, kinds[k]) for k in range(nmat)]
     return scenes.Scene(name="t", precision=64, n=(n, n, n), dx=1 / n, dt=dt, materials=mats, x=x, v=v, F=F,
                         G=np.zeros((x.shape[0], 9)), vol=np.full(x.shape[0], (1 / n) ** 3 / 8), mat=mat,
@@ -44,7 +50,7 @@ def elastic_part(prob, g_or_hu, v_or_u, vhat=None):
 
 
 # ------------------------------------------------------------------ C6 derivatives
-@pytest.mark.parametrize("nmat,kind", [(1, 0), (2, 0), (1, 1), (2, "mix")])
+@pytest.mark.parametrize("nmat,kind", [(1, 0), (2, 0), (1, 1), (2, "mix"), (1, 2), (2, "wmix")])
 def test_gradient_matches_fd(orc, nmat, kind):
     sc = make_scene(nmat=nmat, kind=kind)
     un, S, prob, v0 = orc.prepare(sc)
@@ -67,7 +73,7 @@ def test_gradient_matches_fd(orc, nmat, kind):
     assert np.linalg.norm(fdel - gel) <= 1e-5 * np.linalg.norm(gel)
 
 
-@pytest.mark.parametrize("nmat,kind", [(1, 0), (2, 0), (1, 1), (2, "mix")])
+@pytest.mark.parametrize("nmat,kind", [(1, 0), (2, 0), (1, 1), (2, "mix"), (1, 2), (2, "wmix")])
 def test_hvp_matches_fd_and_is_symmetric(orc, nmat, kind):
     sc = make_scene(nmat=nmat, seed=2, kind=kind)
     un, S, prob, v0 = orc.prepare(sc)
@@ -86,7 +92,7 @@ def test_hvp_matches_fd_and_is_symmetric(orc, nmat, kind):
     assert abs((u * Hw).sum() - (w * Hu).sum()) <= 1e-12 * abs((u * Hw).sum())
 
 
-@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("kind", [0, 1, 2])
 def test_diag_is_eHe(orc, kind):
     sc = make_scene(seed=3, kind=kind)
     un, S, prob, v0 = orc.prepare(sc)
@@ -101,7 +107,8 @@ def test_diag_is_eHe(orc, kind):
             assert D[i, a] == pytest.approx(prob.hvp(v, e)[i, a], rel=1e-12)
 
 
-@pytest.mark.parametrize("kind", [0, 1])  # both laws linearise to 2 mu eps + lam tr(eps) I at rest
+# both solid laws linearise to 2 mu eps + lam tr(eps) I at rest; water to kappa tr(eps) I
+@pytest.mark.parametrize("kind", [0, 1, 2])
 def test_textbook_linear_hex_stiffness(orc, kind):
     """At S = I and v = 0 (G = 0, A = I): K_c = dt^2 V C with C:e = 2 mu sym(e) + lam tr(e) I, the
     one-point trilinear-hex linear-elastic stiffness."""
@@ -113,6 +120,8 @@ def test_textbook_linear_hex_stiffness(orc, kind):
     v = np.zeros_like(u)
     Hu = prob.hvp(v, u)
     mu, lam = orc.lame(sc.materials[0].E, sc.materials[0].nu)
+    if kind == 2:
+        mu, lam = 0.0, sc.materials[0].E  # psi = kappa/2 (J-1)^2, kappa = E
     ref = prob.m_i[:, None] * u
     ijk = g.cell_ijk()
     n1 = g.n[1] + 1
@@ -141,7 +150,7 @@ def test_explicit_force_special_case(orc):
     assert np.abs(f).max() > 0
 
 
-@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("kind", [0, 1, 2])
 def test_patch_test_affine_zero_interior_force(orc, kind):
     """Constant-strain patch test (north_star): unjittered lattice -> interior V_c = dx^3 exactly;
     uniform F_p -> uniform S; affine v -> zero net elastic force on interior nodes (sum_c grad w_ic = 0)."""
@@ -166,7 +175,7 @@ def test_patch_test_affine_zero_interior_force(orc, kind):
     assert np.abs(gel[boundary]).max() > 0
 
 
-@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("kind", [0, 1, 2])
 def test_rigid_rotation(orc, kind):
     """v_i = ((R - I)/dt)(x_i - x0) gives G_c = (R - I)/dt exactly, F = R S: with S = I the elastic
     energy and force vanish; with S != I the elastic energy equals that at v = 0 (isotropy)."""
@@ -211,7 +220,7 @@ def test_mass_only_limit(orc):
     assert np.allclose(r.v_new[act], r.problem.vhat[act], atol=1e-12)
 
 
-@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("kind", [0, 1, 2])
 def test_newton_bruteforce_dense(orc, kind):
     """Brute force on a tiny grid: dense H from n HVPs is symmetric positive definite; one Newton
     iteration with exact PCG equals v + H^{-1}(-g) (dense Cholesky); the converged step has ||g|| ~ 0

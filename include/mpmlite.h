@@ -78,6 +78,11 @@ typedef struct {
                      (P:229-285); 2 = J-based water (kappa = E)          */
     double E, nu; /* Young's modulus, Poisson ratio -> 3D Lame (amb-2) */
     double rho;   /* density: m_p = rho * V_p                          */
+    double yield_stress; /* von Mises sigma_y > 0: fixed-point plasticity (kind 0 only; 0 = elastic).
+                            P:658-663: at every Newton iterate the trial deformation A(v) S_base of
+                            each slot is return-mapped in Hencky space, the slot's base
+                            becomes S = S_base P (A(v) S = F^E) and is held through that iteration's
+                            PCG (elasticity only) and line search; Load return-maps F_p too.   */
 } mpl_material;
 
 typedef struct {

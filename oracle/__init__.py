@@ -45,7 +45,8 @@ class _Grid(C.Structure):
 
 
 class _Mat(C.Structure):
-    _fields_ = [("E", C.c_double), ("nu", C.c_double), ("rho", C.c_double), ("kind", C.c_int32)]
+    _fields_ = [("E", C.c_double), ("nu", C.c_double), ("rho", C.c_double), ("kind", C.c_int32),
+                ("yield_stress", C.c_double)]
 
 
 class _Box(C.Structure):
@@ -124,6 +125,11 @@ def lib():
         L.orc_water_psi.argtypes = [vp, d]
         L.orc_water_psi.restype = d
         L.orc_water_stretch.argtypes = [vp, d, vp]
+        L.orc_vm_plastic_P.argtypes = [vp, d, d, vp]
+        L.orc_vm_plastic_P.restype = C.c_int
+        L.orc_vm_return.argtypes = [vp, d, d, vp]
+        L.orc_plastic_update.argtypes = [vp, vp, vp, vp]
+        L.orc_plastic_update.restype = i64
         L.orc_explicit_force.argtypes = [vp, i32, vp, vp, vp, vp]
     return _lib
 
@@ -173,6 +179,7 @@ def _mats(materials) -> "C.Array":
     for k, m in enumerate(materials):
         arr[k].E, arr[k].nu, arr[k].rho = float(m.E), float(m.nu), float(m.rho)
         arr[k].kind = int(getattr(m, "kind", 0))  # 0 StVK-Hencky, 1 split Neo-Hookean, 2 water (kappa = E)
+        arr[k].yield_stress = float(getattr(m, "yield_stress", 0.0))  # von Mises sigma_y (kind 0; 0 = elastic)
     return arr
 
 
@@ -314,6 +321,21 @@ def water_stretch(tau, kappa: float) -> np.ndarray:
     return S.reshape(3, 3)
 
 
+def vm_plastic_P(F, mu: float, sigma_y: float):
+    """Von Mises return map in Hencky space as F^E = F P: (P, projected)."""
+    F = _f64(F).reshape(9)
+    P = np.zeros(9)
+    r = lib().orc_vm_plastic_P(_p(F), float(mu), float(sigma_y), _p(P))
+    return P.reshape(3, 3), bool(r)
+
+
+def vm_return(F, mu: float, sigma_y: float) -> np.ndarray:
+    F = _f64(F).reshape(9)
+    FE = np.zeros(9)
+    lib().orc_vm_return(_p(F), float(mu), float(sigma_y), _p(FE))
+    return FE.reshape(3, 3)
+
+
 def stretch(tau, mu: float, lam: float) -> np.ndarray:
     tau = _f64(tau).reshape(9)
     S = np.zeros(9)
@@ -400,6 +422,17 @@ class Problem:
         P.m_c, P.V_ck, P.S_ck = _p(self.m_c).value, _p(self.V_ck).value, _p(self.S_ck).value
         self._c = P
 
+    def plastic_update(self, v):
+        """Bases after the von Mises return map at iterate v: (S_ck, number of projected slots)."""
+        v = _f64(v).reshape(-1, 3)
+        S = np.zeros_like(self.S_ck)
+        n = lib().orc_plastic_update(C.byref(self._c), _p(v), _p(self.S_ck), _p(S))
+        return S, int(n)
+
+    def with_bases(self, S_ck) -> "Problem":
+        """The same problem with other bases (e.g. the plastic iterate's, held fixed)."""
+        return Problem(self.grid, self.materials, self.dt, self.m_i, self.vhat, self.freed, self.m_c, self.V_ck, S_ck)
+
     def energy(self, v) -> float:
         v = _f64(v).reshape(-1, 3)
         return float(lib().orc_energy(C.byref(self._c), _p(v)))
@@ -459,7 +492,7 @@ def g2p(grid: Grid, dt: float, m_c, v_i, x, v, F, G, clip: bool = False, mat=Non
     """Alg. 4. Returns updated copies (x, v, F, G).  With (mat, materials), water
     particles (kind 2) update J_p by the trace form of P:316 and keep F_p = J_p^{1/3} I."""
     x, v, F, G = _f64(x).copy(), _f64(v).copy(), _f64(F).copy(), _f64(G).copy()
-    if mat is not None and any(getattr(m, "kind", 0) == 2 for m in materials):
+    if mat is not None and any(getattr(m, "kind", 0) == 2 or getattr(m, "yield_stress", 0.0) > 0 for m in materials):
         mat = np.ascontiguousarray(mat, dtype=np.int32)
         r = lib().orc_g2p_mat(C.byref(grid.c()), float(dt), _p(_f64(m_c)), _p(_f64(v_i).reshape(-1, 3)),
                               x.shape[0], _p(x), _p(v), _p(F), _p(G), _p(mat), _mats(materials), int(clip))

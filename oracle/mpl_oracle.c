@@ -35,6 +35,8 @@ typedef struct {
     double E, nu, rho;
     int32_t kind; /* 0 = StVK-Hencky, 1 = split Neo-Hookean (App. C),
                      2 = J-based water (kappa = E, Table 2 caption P:536)       */
+    double yield_stress; /* von Mises sigma_y (kind 0 only; 0 = elastic): fixed-point plasticity
+                            inside Newton ("von Mises", Table 2 "VM: sigma_y") */
 } orc_material;
 
 typedef struct {
@@ -885,14 +887,27 @@ done:
 
 /* v (in/out): on entry the inertia target with Dirichlet values imposed on fixed nodes (v^0);
  * on return v^{n+1}. */
-int orc_newton(const orc_problem *P, const orc_solver_cfg *cfg, double *v, orc_solve_stats *st) {
-    int64_t nn = nnodes(&P->g);
-    const uint8_t *fr = P->freed;
+int64_t orc_plastic_update(const orc_problem *P, const double *v, const double *S_base, double *S_out);
+static int any_plastic(const orc_problem *P);
+int orc_newton(const orc_problem *P0, const orc_solver_cfg *cfg, double *v, orc_solve_stats *st) {
+    int64_t nn = nnodes(&P0->g);
+    const uint8_t *fr = P0->freed;
     double *grad = calloc(nn * 3, sizeof(double)), *D = calloc(nn * 3, sizeof(double));
     double *p = calloc(nn * 3, sizeof(double)), *vt = calloc(nn * 3, sizeof(double));
     memset(st, 0, sizeof *st);
+    /* fixed-point plasticity: the bases are re-projected at every Newton iterate from S_base
+     * and held fixed through that iteration's PCG and line search */
+    const int plastic = any_plastic(P0);
+    orc_problem Pw = *P0;
+    double *S_work = NULL;
+    if (plastic) {
+        S_work = malloc(sizeof(double) * 9 * ncells(&P0->g) * P0->nmat);
+        Pw.S_ck = S_work;
+    }
+    const orc_problem *P = &Pw;
     int kmax = cfg->fixed_newton > 0 ? cfg->fixed_newton : cfg->newton_max;
     for (int k = 0; k < kmax; k++) {
+        if (plastic) orc_plastic_update(P0, v, P0->S_ck, S_work);
         orc_gradient(P, v, grad);
         double gn = sqrt(dotf(nn, fr, grad, grad));
         if (k == 0) st->grad_norm0 = gn;
@@ -932,12 +947,93 @@ int orc_newton(const orc_problem *P, const orc_solver_cfg *cfg, double *v, orc_s
         st->newton_iters = k + 1;
     }
     if (cfg->fixed_newton <= 0 && st->newton_iters == kmax && !st->converged) {
+        if (plastic) orc_plastic_update(P0, v, P0->S_ck, S_work);
         orc_gradient(P, v, grad);
         st->grad_norm = sqrt(dotf(nn, fr, grad, grad));
         if (st->grad_norm <= cfg->eps_newton * st->grad_norm0) st->converged = 1;
     }
     st->energy = orc_energy(P, v);
-    free(grad); free(D); free(p); free(vt);
+    free(grad); free(D); free(p); free(vt); free(S_work);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Fixed-point plasticity (§6.5): von Mises return map in Hencky strain */
+/* space, applied to the trial deformation of each plastic slot at every     */
+/* Newton iterate, "while the matrix-free conjugate gradient solve handles elasticity only".        */
+/*   F = U diag(sigma) V^T, e = log sigma, e_dev = e - tr(e)/3;                                     */
+/*   if ||2 mu e_dev|| > sqrt(2/3) sigma_y:  e_dev <- s e_dev, s = sqrt(2/3) sigma_y / (2 mu ||e_dev||) */
+/*   F^E = U diag(exp(e^E)) V^T = F P,  P = V diag(exp((s - 1) e_dev)) V^T  (from C = F^T F = V sigma^2 V^T) */
+/* The volume is kept (tr e unchanged; det P = 1).  Returns 1 if the state was projected.            */
+/* ------------------------------------------------------------------------ */
+int orc_vm_plastic_P(const double F[9], double mu, double sigma_y, double Pm[9]) {
+    double FT[9], Cm[9], lam[3], V[9];
+    mat_T(F, FT);
+    mat_mul(FT, F, Cm);
+    orc_sym_eig3(Cm, lam, V);
+    double e[3], tr = 0.0;
+    for (int i = 0; i < 3; i++) {
+        e[i] = 0.5 * log(lam[i]);
+        tr += e[i];
+    }
+    double ed[3], nrm = 0.0;
+    for (int i = 0; i < 3; i++) {
+        ed[i] = e[i] - tr / 3.0;
+        nrm += ed[i] * ed[i];
+    }
+    nrm = sqrt(nrm);
+    for (int a = 0; a < 9; a++) Pm[a] = (a % 4 == 0) ? 1.0 : 0.0;
+    if (!(2.0 * mu * nrm > sqrt(2.0 / 3.0) * sigma_y)) return 0;
+    double sc = sqrt(2.0 / 3.0) * sigma_y / (2.0 * mu * nrm);
+    double d[3];
+    for (int i = 0; i < 3; i++) d[i] = exp((sc - 1.0) * ed[i]);
+    for (int a = 0; a < 3; a++)
+        for (int b = 0; b < 3; b++) {
+            double v = 0.0;
+            for (int i = 0; i < 3; i++) v += V[3 * a + i] * d[i] * V[3 * b + i];
+            Pm[3 * a + b] = v;
+        }
+    return 1;
+}
+
+void orc_vm_return(const double F[9], double mu, double sigma_y, double FE[9]) {
+    double Pm[9];
+    orc_vm_plastic_P(F, mu, sigma_y, Pm);
+    mat_mul(F, Pm, FE);
+}
+
+/* Plastic update of the bases at iterate v (the fixed point on F): for each plastic slot,
+ * F^tr = A(v) S_base, F^E = Z(F^tr), and the slot's base becomes S = A(v)^{-1} F^E = S_base P, so that
+ * A(v) S = F^E; elastic slots keep S_base.  Returns the number of projected slots. */
+int64_t orc_plastic_update(const orc_problem *P, const double *v, const double *S_base, double *S_out) {
+    const orc_grid *g = &P->g;
+    int64_t nc = ncells(g), nproj = 0;
+    memcpy(S_out, S_base, sizeof(double) * 9 * nc * P->nmat);
+    for (int k = 0; k < P->nmat; k++) {
+        const orc_material *m = &P->mats[k];
+        if (m->kind != 0 || !(m->yield_stress > 0.0)) continue;
+        double mu, lam;
+        lame(m, &mu, &lam);
+        for (int ci = 0; ci < g->n[0]; ci++)
+            for (int cj = 0; cj < g->n[1]; cj++)
+                for (int ck = 0; ck < g->n[2]; ck++) {
+                    int64_t c = cid(g, ci, cj, ck);
+                    if (P->m_c[c] == 0.0 || P->V_ck[(int64_t)k * nc + c] == 0.0) continue;
+                    double Gc[9], A[9], Ftr[9], Pm[9];
+                    cell_G(P, v, ci, cj, ck, Gc);
+                    for (int a = 0; a < 9; a++) A[a] = ((a % 4 == 0) ? 1.0 : 0.0) + P->dt * Gc[a];
+                    const double *Sb = S_base + ((int64_t)k * nc + c) * 9;
+                    mat_mul(A, Sb, Ftr);
+                    nproj += orc_vm_plastic_P(Ftr, mu, m->yield_stress, Pm);
+                    mat_mul(Sb, Pm, S_out + ((int64_t)k * nc + c) * 9);
+                }
+    }
+    return nproj;
+}
+
+static int any_plastic(const orc_problem *P) {
+    for (int k = 0; k < P->nmat; k++)
+        if (P->mats[k].kind == 0 && P->mats[k].yield_stress > 0.0) return 1;
     return 0;
 }
 
@@ -948,7 +1044,8 @@ int orc_newton(const orc_problem *P, const orc_solver_cfg *cfg, double *v, orc_s
 /* x_p += dt v_p ; F_p <- (I + dt G_p) F_p.   (v_c = G_c = 0 where m_c = 0)   */
 /* ------------------------------------------------------------------------ */
 /* Water particles (kind 2) carry only J_p: their F_p is J_p^{1/3} I, updated by
- * J_p^{n+1} = (1 + dt tr(G_p)) J_p^n (the trace form; G_p = sum_c w_cp G_c^{n+1}). */
+ * J_p^{n+1} = (1 + dt tr(G_p)) J_p^n (the trace form; G_p = sum_c w_cp G_c^{n+1}).
+ * Plastic particles (kind 0, yield_stress > 0) take the von Mises return map of their trial F. */
 int64_t orc_g2p_mat(const orc_grid *g, double dt, const double *m_c, const double *v_i, int64_t np,
                     double *x, double *v, double *F, double *G, const int32_t *mat, const orc_material *mats,
                     int32_t clip);
@@ -994,7 +1091,13 @@ int64_t orc_g2p_mat(const orc_grid *g, double dt, const double *m_c, const doubl
         }
         double A[9], Fn[9];
         for (int a = 0; a < 9; a++) A[a] = ((a % 4 == 0) ? 1.0 : 0.0) + dt * Gp[a];
-        if (mat && mats[mat[p]].kind == 2) {
+        if (mat && mats[mat[p]].kind == 0 && mats[mat[p]].yield_stress > 0.0) {
+            /* plastic particle: F_p^{n+1} = Z((I + dt G_p) F_p) (same von Mises return map) */
+            double Ftr[9], mu, lam;
+            mat_mul(A, F + 9 * p, Ftr);
+            lame(&mats[mat[p]], &mu, &lam);
+            orc_vm_return(Ftr, mu, mats[mat[p]].yield_stress, Fn);
+        } else if (mat && mats[mat[p]].kind == 2) {
             double Jn = (1.0 + dt * (Gp[0] + Gp[4] + Gp[8])) * mat_det(F + 9 * p);
             double s = cbrt(Jn);
             for (int a = 0; a < 9; a++) Fn[a] = (a % 4 == 0) ? s : 0.0;

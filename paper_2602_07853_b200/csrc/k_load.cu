@@ -61,7 +61,7 @@ __global__ void k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ s
                       const int *__restrict__ nplus,
                       const int *__restrict__ cellof, const vec4<T> *__restrict__ vc, const T *__restrict__ Gc,
                       T *__restrict__ x, T *__restrict__ v, T *__restrict__ F, T *__restrict__ G,
-                      const int *__restrict__ mat, unsigned water_mask) {
+                      const int *__restrict__ mat, MatP mp) {
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= np || pid[p] < 0) return;  // ghosts (slab ranks) are advected by their owner
     const int key = skey[p];
@@ -98,7 +98,8 @@ __global__ void k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ s
         Fp[a] = F[9 * p + a];
         A[a] = dt * Gp[a] + ((a % 4 == 0) ? T(1) : T(0));
     }
-    if ((water_mask >> mat[p]) & 1u) {
+    const int mk = mat[p];
+    if (mp.kind[mk] == 2) {
         // water particle: J^{n+1} = (1 + dt tr G_p) J^n, F_p = J^{1/3} I (J - 1 kept exact in
         // the product (1 + a)(1 + b) - 1 = a + b + a b)
         T H[9];
@@ -109,6 +110,17 @@ __global__ void k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ s
         const T s = T(1) + mexpm1(mlog1p(jn1) / T(3));
 #pragma unroll
         for (int a = 0; a < 9; a++) Fn[a] = (a % 4 == 0) ? s : T(0);
+    } else if (mp.sigy[mk] > 0.0) {
+        // plastic particle: F_p^{n+1} = Z((I + dt G_p) F_p), the same von Mises
+        // return map as the quadrature slots: F^E = F^tr + F^tr (P - I)
+        T Ftr[9], H[9], Pm1[9], FP[9];
+        mm3(A, Fp, Ftr);
+#pragma unroll
+        for (int a = 0; a < 9; a++) H[a] = Ftr[a] - ((a % 4 == 0) ? T(1) : T(0));
+        vm_plastic_Pm1(H, T(mp.mu[mk]), T(mp.sigy[mk]), Pm1);
+        mm3(Ftr, Pm1, FP);
+#pragma unroll
+        for (int a = 0; a < 9; a++) Fn[a] = Ftr[a] + FP[a];
     } else {
         mm3(A, Fp, Fn);
     }
@@ -206,7 +218,7 @@ mpl_status g2p_impl(mpl_ctx ctx, double dt) {
                                                     (const vec4<T> *)ctx->q_vc.p, (const T *)ctx->q_Gc.p,
                                                     (T *)ctx->px[c].p, (T *)ctx->pv.p, (T *)ctx->pF[c].p,
                                                     (T *)ctx->pG.p, (const int *)ctx->pmat[c].p,
-                                                    water_mask(ctx->mats)); ctx->launches++;
+                                                    ctx->mats); ctx->launches++;
     MPL_CUDA(cudaGetLastError());
     MPL_CUDA(cudaStreamSynchronize(st));
     ctx->resampled = false;  // quadrature state is consumed

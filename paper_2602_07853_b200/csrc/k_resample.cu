@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(256) k_p2q8(GridP g, MatP mp, const int *__res
                                               const int *__restrict__ nminus, const int *__restrict__ bstart,
                                               const int *__restrict__ cellof, const T *__restrict__ rec,
                                               T *__restrict__ q_m, T *__restrict__ q_mv, T *__restrict__ q_mG,
-                                              T *__restrict__ q_slot, DevScalars *sc) {
+                                              T *__restrict__ q_slot, T *__restrict__ q_Sp, DevScalars *sc) {
     const int t = blockIdx.x >> 1;
     const int l = ((blockIdx.x & 1) << 5) | (threadIdx.x >> 3), o = threadIdx.x & 7;
     const int cc = cellof[t * 64 + l];
@@ -502,6 +502,13 @@ __global__ void __launch_bounds__(256) k_p2q8(GridP g, MatP mp, const int *__res
 #pragma unroll
         for (int a = 0; a < 6; a++) { sl[1 + a] = E[a]; sl[7 + a] = tau[a]; }
         sl[13] = sl[14] = sl[15] = T(0);
+        if (q_Sp) {  // plastic runs: the iterate's base starts at S_base (general 3x3 storage)
+            T *sp = q_Sp + ((int64_t)cc * nmat + q) * 9;
+            sp[0] = E[0]; sp[4] = E[1]; sp[8] = E[2];
+            sp[1] = sp[3] = E[3];
+            sp[5] = sp[7] = E[4];
+            sp[2] = sp[6] = E[5];
+        }
     }
 }
 
@@ -844,6 +851,7 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CHECK(ensure(ctx, ctx->q_mv, C * 3 * s));
     MPL_CHECK(ensure(ctx, ctx->q_mG, C * 9 * s));
     MPL_CHECK(ensure(ctx, ctx->q_slot, C * nm * 16 * s));
+    if (ctx->mats.plastic) MPL_CHECK(ensure(ctx, ctx->q_Sp, C * nm * 9 * s));
     MPL_CHECK(ensure(ctx, ctx->q_vc, C * 4 * s));
     MPL_CHECK(ensure(ctx, ctx->q_Gc, C * 9 * s));
     MPL_CHECK(ensure(ctx, ctx->K, (size_t)Ktot * s + 256));
@@ -855,7 +863,7 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
 #define P2Q_ARGS                                                                                             \
     g, ctx->mats, (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p, (const int *)ctx->t_bstart.p, \
         (const int *)ctx->t_cellof.p, (const T *)ctx->prec.p, (T *)ctx->q_m.p, (T *)ctx->q_mv.p,            \
-        (T *)ctx->q_mG.p, (T *)ctx->q_slot.p, sc
+        (T *)ctx->q_mG.p, (T *)ctx->q_slot.p, ctx->mats.plastic ? (T *)ctx->q_Sp.p : (T *)nullptr, sc
         if (ctx->mats.nmat <= 2) k_p2q8<T, 2><<<2 * T_, 256, 0, st>>>(P2Q_ARGS);
         else k_p2q8<T, MPL_MAXMAT><<<2 * T_, 256, 0, st>>>(P2Q_ARGS);
 #undef P2Q_ARGS

@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
                                                    const T *__restrict__ qslot, T *__restrict__ Kout,
                                                    const int *__restrict__ kstart, const int *__restrict__ ncell,
                                                    vec4<T> *__restrict__ grad, vec4<T> *__restrict__ diag,
-                                                   DevScalars *sc) {
+                                                   T *__restrict__ qsp, DevScalars *sc) {
     constexpr int KS = (MODE == LIN_FULL) ? 64 * 45 : 1;
     __shared__ vec4<T> vh[125];
     __shared__ T Pg[64 * 9];
@@ -112,6 +112,29 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
                 if (V == T(0)) continue;
                 T mu = T(mp.mu[k]), lamL = T(mp.lam[k]);
                 T E[9] = {sl[1], sl[4], sl[6], sl[4], sl[2], sl[5], sl[6], sl[5], sl[3]};
+                if (qsp && mp.sigy[k] > 0.0) {
+                    // fixed-point plasticity: the slot's base for this Newton iteration.
+                    // Energy-only evaluations (line search) use the stored iterate base; the gradient /
+                    // full linearisation at a new iterate v re-project: F^tr = A(v) S_base, F^E = F^tr P,
+                    // S = S_base P  ->  E = S - I = (P - I) + E_base + E_base (P - I).
+                    T *sp = qsp + ((int64_t)(cs + tid) * nmat + k) * 9;
+                    if (MODE == LIN_ENERGY) {
+#pragma unroll
+                        for (int a = 0; a < 9; a++) E[a] = sp[a];
+                    } else {
+                        T WE0[9], Ht[9], Pm1[9], EP[9];
+                        mm3(W, E, WE0);
+#pragma unroll
+                        for (int a = 0; a < 9; a++) Ht[a] = W[a] + E[a] + WE0[a];  // F^tr - I
+                        vm_plastic_Pm1(Ht, mu, T(mp.sigy[k]), Pm1);
+                        mm3(E, Pm1, EP);
+#pragma unroll
+                        for (int a = 0; a < 9; a++) {
+                            E[a] = Pm1[a] + E[a] + EP[a];
+                            sp[a] = E[a];
+                        }
+                    }
+                }
                 // H = F - I = W + E + W E
                 T WE[9], H[9];
                 mm3(W, E, WE);
@@ -267,13 +290,16 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
 #pragma unroll
                 for (int a = 0; a < 9; a++) Pc[a] += sV * TA[a];
                 if (MODE == LIN_FULL) {
-                    // FS = (I + H)(I + E); Y = Q^T (F S)
+                    // FS = F S^T = (I + H)(I + E)^T; Y = Q^T (F S^T)  (column (a,b): dG S F^T = e_a (F S^T)[:,b]^T;
+                    // S is symmetric except for plastic iterate bases)
                     T F[9], S[9], FS[9], Y[9];
 #pragma unroll
-                    for (int a = 0; a < 9; a++) {
-                        F[a] = H[a] + ((a % 4 == 0) ? T(1) : T(0));
-                        S[a] = E[a] + ((a % 4 == 0) ? T(1) : T(0));
-                    }
+                    for (int a = 0; a < 3; a++)
+#pragma unroll
+                        for (int b = 0; b < 3; b++) {
+                            F[3 * a + b] = H[3 * a + b] + ((a == b) ? T(1) : T(0));
+                            S[3 * a + b] = E[3 * b + a] + ((a == b) ? T(1) : T(0));  // S^T
+                        }
                     mm3(F, S, FS);
 #pragma unroll
                     for (int i = 0; i < 3; i++)
@@ -777,7 +803,8 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
     ctx->grid, ctx->mats, ctx->dt, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,                     \
         (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p, (const vec4<T> *)v_tile,                  \
         (const vec4<T> *)ctx->n_vhat.p, (const T *)owned_mass(ctx), (const T *)ctx->q_slot.p, (T *)ctx->K.p,       \
-        (const int *)ctx->t_kstart.p, (const int *)ctx->t_ncell.p, (vec4<T> *)ctx->n_g.p, (vec4<T> *)ctx->n_diag.p, sc
+        (const int *)ctx->t_kstart.p, (const int *)ctx->t_ncell.p, (vec4<T> *)ctx->n_g.p, (vec4<T> *)ctx->n_diag.p, \
+        ctx->mats.plastic ? (T *)ctx->q_Sp.p : (T *)nullptr, sc
         if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY><<<T_, 128, 0, st>>>(LIN_ARGS);
         else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD><<<T_, 128, 0, st>>>(LIN_ARGS);
         else k_linearize<T, LIN_FULL><<<T_, 128, 0, st>>>(LIN_ARGS);

@@ -296,6 +296,11 @@ mpl_status mpl_set_materials(mpl_ctx ctx, int32_t n, const mpl_material *mats) {
             ctx->err = "material kind must be 0 (StVK-Hencky), 1 (split Neo-Hookean) or 2 (water)";
             return MPL_ERR_UNSUPPORTED;
         }
+        if (!(m.yield_stress >= 0) || (m.yield_stress > 0 && m.kind != 0)) {
+            ctx->err = "material " + std::to_string(k) + ": yield_stress must be >= 0, and > 0 only for kind 0 (von Mises in Hencky space, P:187)";
+            return m.yield_stress > 0 ? MPL_ERR_UNSUPPORTED : MPL_ERR_INVALID_ARG;
+        }
+        ctx->mats.sigy[k] = m.kind == 0 ? m.yield_stress : 0.0;
         if (m.kind == 2) {  // J-based water: kappa = E; no shear modulus
             if (!(m.E > 0) || !(m.rho > 0)) {
                 ctx->err = "material " + std::to_string(k) + ": water needs kappa = E > 0 and rho > 0 (P:297)";
@@ -321,6 +326,9 @@ mpl_status mpl_set_materials(mpl_ctx ctx, int32_t n, const mpl_material *mats) {
         ctx->mats.rho[k] = m.rho;
     }
     ctx->mats.nmat = n;
+    ctx->mats.plastic = 0;
+    for (int k = 0; k < n; k++)
+        if (ctx->mats.sigy[k] > 0) ctx->mats.plastic = 1;
     ctx->resampled = ctx->linearized = ctx->solved = false;
     return MPL_OK;
 }

@@ -73,6 +73,8 @@ struct MatP {
     int nmat;
     int kind[MPL_MAXMAT];  // 0 StVK-Hencky, 1 split Neo-Hookean, 2 J-based water (kappa = E)
     double mu[MPL_MAXMAT], lam[MPL_MAXMAT], rho[MPL_MAXMAT], kappa[MPL_MAXMAT];  // kappa = 2/3 mu + lam
+    double sigy[MPL_MAXMAT];  // von Mises yield stress (kind 0; 0 = elastic)
+    int plastic;              // any sigy > 0: fixed-point plasticity in Newton
 };
 
 struct BoxP {
@@ -192,6 +194,37 @@ template <class T> __device__ __forceinline__ T det_ipm1(const T H[9]) {  // det
     const T tr2 = H[0] * H[0] + H[4] * H[4] + H[8] * H[8] + T(2) * (H[1] * H[3] + H[2] * H[6] + H[5] * H[7]);
     return tr + T(0.5) * (tr * tr - tr2) + det3(H);
 }
+// Von Mises return map in Hencky strain space (P:658-663 fixed-point plasticity), as a right
+// factor F^E = F P with P = V diag(exp((s - 1) e_dev)) V^T from C = F^T F = V sigma^2 V^T, e = log sigma,
+// s = sqrt(2/3) sigma_y / (2 mu |e_dev|) when 2 mu |e_dev| > sqrt(2/3) sigma_y (else P = I).  Takes
+// H = F - I, returns P - I (cancellation-free: C - I = H + H^T + H^T H, e = log1p(.)/2, expm1).
+template <class T> __device__ __forceinline__ bool vm_plastic_Pm1(const T H[9], T mu, T sigy, T Pm1[9]) {
+    T Cm[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++)
+            Cm[3 * a + b] = H[3 * a + b] + H[3 * b + a] + H[a] * H[b] + H[3 + a] * H[3 + b] + H[6 + a] * H[6 + b];
+    T lam[3], V[9];
+    sym_eig3(Cm, lam, V);
+    const T e0 = T(0.5) * mlog1p(lam[0]), e1 = T(0.5) * mlog1p(lam[1]), e2 = T(0.5) * mlog1p(lam[2]);
+    const T m3 = (e0 + e1 + e2) / T(3);
+    const T d0 = e0 - m3, d1 = e1 - m3, d2 = e2 - m3;
+    const T nrm = msqrt(d0 * d0 + d1 * d1 + d2 * d2);
+    const T ry = T(0.81649658092772603) * sigy;  // sqrt(2/3) sigma_y
+#pragma unroll
+    for (int a = 0; a < 9; a++) Pm1[a] = T(0);
+    if (!(T(2) * mu * nrm > ry)) return false;
+    const T sm1 = ry / (T(2) * mu * nrm) - T(1);
+    const T q0 = mexpm1(sm1 * d0), q1 = mexpm1(sm1 * d1), q2 = mexpm1(sm1 * d2);
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++)
+            Pm1[3 * a + b] = V[3 * a] * V[3 * b] * q0 + V[3 * a + 1] * V[3 * b + 1] * q1 + V[3 * a + 2] * V[3 * b + 2] * q2;
+    return true;
+}
+
 template <class T> __device__ __forceinline__ T nh_f(T x) {  // x (2 + x) - 2 log1p(x), series near 0
     // the series (truncation ~x^8/4) replaces the cancelling direct form below |x| = 0.1 (fp32) / 1e-3 (fp64)
     if (mabs(x) < (sizeof(T) == 4 ? T(0.1) : T(1e-3))) {
@@ -255,14 +288,6 @@ template <class T> struct KL {
     static constexpr int NCH = 45 / VEC;
     static constexpr int REM = 45 - NCH * VEC;
 };
-// bit k set: material k is J-based water (kind 2; Load updates J only)
-inline unsigned water_mask(const MatP &mp) {
-    unsigned m = 0;
-    for (int k = 0; k < mp.nmat; k++)
-        if (mp.kind[k] == 2) m |= 1u << k;
-    return m;
-}
-
 // Tangent layout per tile: n = the tile's real cells (no padding), block of 45 n reals (rounded up
 // to 4) at t_kstart[t].  Cell j of a tile is handled by HVP thread (warp j & 1, lane j >> 1), so the
 // two warps of a 64-thread CTA get ceil(n/2) and floor(n/2) cells; the tangent of cell j is stored at
@@ -359,7 +384,8 @@ struct mpl_ctx_s {
     DevBuf t_ncell, t_kcnt, t_kstart;  // real cells per tile; tangent reals per tile (rounded to 4) and offsets
     DevBuf c_local;
     // quadrature (compact cells)
-    DevBuf q_m, q_mv, q_mG, q_slot;  // q_slot: C * nmat * 8 (V, E xx yy zz xy yz xz, pad)
+    DevBuf q_m, q_mv, q_mG, q_slot;  // q_slot: C * nmat * 16 (V, E xx yy zz xy yz xz, tau (6), pad)
+    DevBuf q_Sp;                     // plastic runs: C * nmat * 9, S_k - I of the current Newton iterate
     DevBuf q_vc, q_Gc;               // load: v_c, G_c
     DevBuf K;                        // tangent (scaled by 1/(16 dx^2)), per tile at t_kstart, 45 reals per real cell
     // nodes (tile-dense, T*64)
@@ -436,6 +462,7 @@ template <class F> void for_each_buf(mpl_ctx ctx, F f) {
         {"q_mv", ctx->q_mv},
         {"q_mG", ctx->q_mG},
         {"q_slot", ctx->q_slot},
+        {"q_Sp", ctx->q_Sp},
         {"q_vc", ctx->q_vc},
         {"q_Gc", ctx->q_Gc},
         {"K", ctx->K},

@@ -40,7 +40,8 @@ class Grid(C.Structure):
 
 
 class Material(C.Structure):
-    _fields_ = [("kind", C.c_int32), ("E", C.c_double), ("nu", C.c_double), ("rho", C.c_double)]
+    _fields_ = [("kind", C.c_int32), ("E", C.c_double), ("nu", C.c_double), ("rho", C.c_double),
+                ("yield_stress", C.c_double)]
 
 
 class Config(C.Structure):
@@ -282,6 +283,7 @@ class Context:
         arr = (Material * len(materials))()
         for k, m in enumerate(materials):
             arr[k].kind, arr[k].E, arr[k].nu, arr[k].rho = int(getattr(m, "kind", 0)), float(m.E), float(m.nu), float(m.rho)
+            arr[k].yield_stress = float(getattr(m, "yield_stress", 0.0))
         self._chk(_lib.mpl_set_materials(self._h, len(materials), arr), "mpl_set_materials")
         self.nmat = len(materials)
 

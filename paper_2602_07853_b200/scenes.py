@@ -34,6 +34,7 @@ class Material:
     nu: float
     rho: float
     kind: int = 0  # 0 StVK-Hencky, 1 split Neo-Hookean, 2 water (kappa = E)
+    yield_stress: float = 0.0  # von Mises sigma_y for kind 0 (fixed-point plasticity); 0 = elastic
 
 
 @dataclasses.dataclass
@@ -352,6 +353,13 @@ def by_name(name: str, precision: Optional[int] = None) -> Scene:
         return cfg5("A", precision or 32)
     if name == "jelly":
         return jelly(precision or 32)
+    if name == "cfg4_nh":  # SURVEY f1 measured on cfg4's geometry: both materials split Neo-Hookean
+        sc = cfg4(precision or 32)
+        return dataclasses.replace(sc, name=name, materials=[dataclasses.replace(m, kind=1) for m in sc.materials])
+    if name == "cfg4_water":  # SURVEY f4 on cfg4's geometry: the left sphere is J-based water (kappa = E)
+        sc = cfg4(precision or 32)
+        m0 = dataclasses.replace(sc.materials[0], E=2e5, kind=2)
+        return dataclasses.replace(sc, name=name, materials=[m0, sc.materials[1]])
     raise KeyError(name)
 
 

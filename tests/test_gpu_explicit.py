@@ -45,6 +45,7 @@ SCENES = {
     "cfg2s_fp64_dirichlet": lambda: _prestrained(small_cfg2(64)),
     "lawmix_fp64": lambda: two_material(64, (1, 0)),
     "watermix_fp64": lambda: two_material(64, (0, 2)),
+    "vmmix_fp64": lambda: two_material(64, (0, 0), (1500.0, 0.0)),  # particle return map in Load
 }
 
 

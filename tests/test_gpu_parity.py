@@ -27,7 +27,7 @@ def small_cfg2(precision=32, k=16):
                             scenes.SolverCfg(eps_cg=tol[0], eps_newton=tol[1], ls_slack=1e-13 if precision == 64 else 1e-6), 1)
 
 
-def two_material(precision=64, kinds=(0, 0)):
+def two_material(precision=64, kinds=(0, 0), yields=(0.0, 0.0)):
     """Two materials mixed in the same cells + a sticky floor (exercises slots and Dirichlet); kinds
     selects each material's law (0 StVK-Hencky, 1 split Neo-Hookean, 2 J-based water)."""
     n = 16
@@ -41,7 +41,8 @@ def two_material(precision=64, kinds=(0, 0)):
     floor = scenes.DirichletBox((-1e9, -1e9, -1e9), (1e9, 3 / n, 1e9), (0.0, 0.0, 0.0))
     tol = (1e-8, 1e-9) if precision == 64 else (1e-5, 1e-5)
     return scenes._assemble("mix", precision, n, 1e-3,
-                            [scenes.Material(1e5, 0.3, 1000.0, kinds[0]), scenes.Material(3e6, 0.45, 2500.0, kinds[1])],
+                            [scenes.Material(1e5, 0.3, 1000.0, kinds[0], yields[0]),
+                             scenes.Material(3e6, 0.45, 2500.0, kinds[1], yields[1])],
                             x, v, F,
                             np.zeros((x.shape[0], 9)), mat, 8, [floor],
                             scenes.SolverCfg(eps_cg=tol[0], eps_newton=tol[1]), 1)
@@ -65,6 +66,13 @@ def water_block(precision=64):
                             scenes.SolverCfg(eps_cg=tol[0], eps_newton=tol[1]), 1)
 
 
+def plastic_cube(precision=64):
+    """cfg1b (pre-strained cube, E = 1e4) with von Mises sigma_y = 150 Pa: 2 mu |e_dev| of the prestrain
+    (~400 Pa) puts most slots outside the yield surface."""
+    sc = scenes.cfg1(prestrain=True, precision=precision)
+    return dataclasses.replace(sc, materials=[dataclasses.replace(sc.materials[0], yield_stress=150.0)])
+
+
 SCENES = {
     "cfg1": lambda: scenes.cfg1(),
     "cfg1b": lambda: scenes.cfg1(prestrain=True),
@@ -82,6 +90,11 @@ SCENES = {
     "water_fp64": lambda: water_block(64),
     "watermix_fp64": lambda: two_material(64, (0, 2)),
     "watermix_fp32": lambda: two_material(32, (2, 0)),
+    # fixed-point von Mises plasticity: pre-strained cube past the yield surface, and a
+    # plastic + elastic mixture in the same cells
+    "vm_fp64": lambda: plastic_cube(64),
+    "vm_fp32": lambda: plastic_cube(32),
+    "vmmix_fp64": lambda: two_material(64, (0, 0), (1500.0, 0.0)),
 }
 
 
@@ -143,13 +156,22 @@ def _probe(pair):
     return v, u
 
 
+def _at(pair, v):
+    """The oracle problem the GPU evaluates at v: with fixed-point plasticity the gradient and the full
+    linearisation re-project the bases at v; otherwise the resample's bases."""
+    if any(getattr(m, "yield_stress", 0.0) > 0 for m in pair.scene.materials):
+        return pair.prob.with_bases(pair.prob.plastic_update(v)[0])
+    return pair.prob
+
+
 def test_energy_gradient_parity(pair):
     tol = TOL[pair.scene.precision]["grad"]
     v, _ = _probe(pair)
-    g_o = pair.prob.gradient(v)
+    po = _at(pair, v)
+    g_o = po.gradient(v)
     g_g, phi_g = pair.ctx.gradient(pair.to_gpu(v))
     assert rel_l2(g_g, g_o[pair.nid]) <= tol
-    phi_o = pair.prob.energy(v)
+    phi_o = po.energy(v)
     assert abs(phi_g - phi_o) <= tol * abs(phi_o)
     assert abs(pair.ctx.energy(pair.to_gpu(v)) - phi_o) <= tol * abs(phi_o)
 
@@ -158,7 +180,8 @@ def test_hvp_and_diag_parity(pair):
     tol = TOL[pair.scene.precision]["hvp"]
     v, u = _probe(pair)
     pair.ctx.linearize(pair.to_gpu(v))
-    h_o = pair.prob.hvp(v, u)
+    po = _at(pair, v)
+    h_o = po.hvp(v, u)
     h_g = pair.ctx.hvp(pair.to_gpu(u))
     assert rel_l2(h_g, h_o[pair.nid]) <= tol
     # elastic part alone (the mass term is exact and could hide tangent errors)
@@ -166,7 +189,7 @@ def test_hvp_and_diag_parity(pair):
     el_o = (h_o - m * u)[pair.nid]
     el_g = h_g - pair.m[:, None] * pair.to_gpu(u)
     assert rel_l2(el_g, el_o) <= (tol if pair.scene.precision == 64 else 2e-4)
-    d_o = pair.prob.diag(v)
+    d_o = po.diag(v)
     assert rel_l2(pair.ctx.get_diag(), d_o[pair.nid]) <= tol
 
 

@@ -11,12 +11,42 @@ namespace {
 
 __device__ __forceinline__ int local_id(int lx, int ly, int lz) { return (lx * 4 + ly) * 4 + lz; }
 
-// per cell: v_c (vec4) and G_c (9) from the 5^3 node halo
+template <class T> __device__ __forceinline__ void st_vec12(T *dst, const T *v);
+template <> __device__ __forceinline__ void st_vec12<float>(float *dst, const float *v) {
+    float4 *d = reinterpret_cast<float4 *>(dst);
+#pragma unroll
+    for (int i = 0; i < 3; i++) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+}
+template <> __device__ __forceinline__ void st_vec12<double>(double *dst, const double *v) {
+    double2 *d = reinterpret_cast<double2 *>(dst);
+#pragma unroll
+    for (int i = 0; i < 6; i++) d[i] = make_double2(v[2 * i], v[2 * i + 1]);
+}
+template <class T> __device__ __forceinline__ void ld_vec12(const T *src, T *v);
+template <> __device__ __forceinline__ void ld_vec12<float>(const float *src, float *v) {
+    const float4 *s = reinterpret_cast<const float4 *>(src);
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        const float4 x = __ldg(s + i);
+        v[4 * i] = x.x; v[4 * i + 1] = x.y; v[4 * i + 2] = x.z; v[4 * i + 3] = x.w;
+    }
+}
+template <> __device__ __forceinline__ void ld_vec12<double>(const double *src, double *v) {
+    const double2 *s = reinterpret_cast<const double2 *>(src);
+#pragma unroll
+    for (int i = 0; i < 6; i++) {
+        const double2 x = __ldg(s + i);
+        v[2 * i] = x.x; v[2 * i + 1] = x.y;
+    }
+}
+
+// per cell: (v_c, G_c) from the 5^3 node halo, packed as 12 reals [v_c (3), G_c (9)] so G2P gathers a
+// cell with three 16-byte loads (fp32)
 template <class T>
 __global__ void __launch_bounds__(128) k_n2c(GridP g, const int *__restrict__ nplus, const int *__restrict__ cstart,
                                              const uint8_t *__restrict__ clocal, const int *__restrict__ hascells,
                                              const T *__restrict__ q_m, const vec4<T> *__restrict__ v,
-                                             vec4<T> *__restrict__ vc, T *__restrict__ Gc) {
+                                             T *__restrict__ vG) {
     __shared__ vec4<T> vh[125];
     const int t = blockIdx.x, tid = threadIdx.x;
     (void)hascells;  // every tile with structural cells: on a slab rank that includes the ghost plane
@@ -50,16 +80,15 @@ __global__ void __launch_bounds__(128) k_n2c(GridP g, const int *__restrict__ np
             G[6] += u.z * s0; G[7] += u.z * s1; G[8] += u.z * s2;
         }
     }
-    vc[cc] = vv;
-#pragma unroll
-    for (int a = 0; a < 9; a++) Gc[9 * cc + a] = G[a];
+    T out[12] = {vv.x, vv.y, vv.z, G[0], G[1], G[2], G[3], G[4], G[5], G[6], G[7], G[8]};
+    st_vec12<T>(vG + 12 * cc, out);
 }
 
 // per particle (sorted order): interpolate, advect, update F
 template <class T>
 __global__ void k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ skey, const int *__restrict__ pid,
                       const int *__restrict__ nplus,
-                      const int *__restrict__ cellof, const vec4<T> *__restrict__ vc, const T *__restrict__ Gc,
+                      const int *__restrict__ cellof, const T *__restrict__ vG,
                       T *__restrict__ x, T *__restrict__ v, T *__restrict__ F, T *__restrict__ G,
                       const int *__restrict__ mat, MatP mp) {
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -85,11 +114,11 @@ __global__ void k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ s
         int tt = dp ? nplus[8 * t + dp] : t;
         int cc = cellof[tt * 64 + local_id(cx & 3, cy & 3, cz & 3)];
         T w = (ox ? f[0] : T(1) - f[0]) * (oy ? f[1] : T(1) - f[1]) * (oz ? f[2] : T(1) - f[2]);
-        vec4<T> c = vc[cc];
-        vp[0] += w * c.x; vp[1] += w * c.y; vp[2] += w * c.z;
-        const T *Gq = Gc + 9 * (int64_t)cc;
+        T c[12];
+        ld_vec12<T>(vG + 12 * (int64_t)cc, c);
+        vp[0] += w * c[0]; vp[1] += w * c[1]; vp[2] += w * c[2];
 #pragma unroll
-        for (int a = 0; a < 9; a++) Gp[a] += w * Gq[a];
+        for (int a = 0; a < 9; a++) Gp[a] += w * c[3 + a];
     }
     const T dt = T(dt_);
     T Fp[9], A[9], Fn[9];
@@ -209,13 +238,13 @@ mpl_status g2p_impl(mpl_ctx ctx, double dt) {
     if (T_)
         k_n2c<T><<<T_, 128, 0, st>>>(ctx->grid, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,
                                      (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p,
-                                     (const T *)ctx->q_m.p, (const vec4<T> *)ctx->n_v.p, (vec4<T> *)ctx->q_vc.p,
-                                     (T *)ctx->q_Gc.p); ctx->launches++;
+                                     (const T *)ctx->q_m.p, (const vec4<T> *)ctx->n_v.p, (T *)ctx->q_vc.p);
+        ctx->launches++;
     if (ctx->np)
         k_c2p<T><<<nblk(ctx->np, 256), 256, 0, st>>>(ctx->grid, dt, ctx->np, (const int *)ctx->pskey.p,
                                                     (const int *)ctx->pid[c].p,
                                                     (const int *)ctx->t_nplus.p, (const int *)ctx->t_cellof.p,
-                                                    (const vec4<T> *)ctx->q_vc.p, (const T *)ctx->q_Gc.p,
+                                                    (const T *)ctx->q_vc.p,
                                                     (T *)ctx->px[c].p, (T *)ctx->pv.p, (T *)ctx->pF[c].p,
                                                     (T *)ctx->pG.p, (const int *)ctx->pmat[c].p,
                                                     ctx->mats); ctx->launches++;

@@ -244,6 +244,17 @@ __device__ bool nh_stretch_E(const double tau[6], double mu, double kappa, doubl
 // record (24 reals): f(3) fraction in the base cell, m_p, a = m_p (v_p - dx G_p f) (3),
 // m_p G_p (9), V_p, V_p tau_p (6), material id (as real)
 constexpr int REC = 24;
+template <class T> __device__ __forceinline__ void st_rec(T *dst, const T *r);
+template <> __device__ __forceinline__ void st_rec<float>(float *dst, const float *r) {
+    float4 *d4 = reinterpret_cast<float4 *>(dst);
+#pragma unroll
+    for (int i = 0; i < REC / 4; i++) d4[i] = make_float4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+}
+template <> __device__ __forceinline__ void st_rec<double>(double *dst, const double *r) {
+    double2 *d2 = reinterpret_cast<double2 *>(dst);
+#pragma unroll
+    for (int i = 0; i < REC / 2; i++) d2[i] = make_double2(r[2 * i], r[2 * i + 1]);
+}
 template <class T>
 __global__ void k_scatter(GridP g, MatP mp, int64_t np, const int *__restrict__ key, const int *__restrict__ rank,
                           const int *__restrict__ bstart, const T *__restrict__ x, const T *__restrict__ v,
@@ -278,7 +289,7 @@ __global__ void k_scatter(GridP g, MatP mp, int64_t np, const int *__restrict__ 
         f[a] = t - floor(t);
     }
     T dx = T(g.dx);
-    T *r = rec + d * REC;
+    T r[REC];  // assembled in registers, written with 16-byte stores (the destination is scattered)
     r[0] = f[0]; r[1] = f[1]; r[2] = f[2];
     r[3] = mass;
 #pragma unroll
@@ -289,6 +300,7 @@ __global__ void k_scatter(GridP g, MatP mp, int64_t np, const int *__restrict__ 
 #pragma unroll
     for (int a = 0; a < 6; a++) r[17 + a] = Vp * tau[a];
     r[23] = T(m);
+    st_rec<T>(rec + d * REC, r);
 #pragma unroll
     for (int a = 0; a < 3; a++) xo[3 * d + a] = xp[a];
 #pragma unroll
@@ -354,6 +366,24 @@ __global__ void k_cell_list(int T_, const unsigned long long *__restrict__ cmask
         perm[t * 64 + c + (l - r)] = (uint8_t)l;
     }
     if (cs + c + l < ce) clocal[cs + c + l] = 0xFF;
+}
+
+template <class T> __device__ __forceinline__ void ld_rec(const T *__restrict__ src, T *r);
+template <> __device__ __forceinline__ void ld_rec<float>(const float *__restrict__ src, float *r) {
+    const float4 *s4 = reinterpret_cast<const float4 *>(src);
+#pragma unroll
+    for (int i = 0; i < REC / 4; i++) {
+        const float4 v = __ldg(s4 + i);
+        r[4 * i] = v.x; r[4 * i + 1] = v.y; r[4 * i + 2] = v.z; r[4 * i + 3] = v.w;
+    }
+}
+template <> __device__ __forceinline__ void ld_rec<double>(const double *__restrict__ src, double *r) {
+    const double2 *s2 = reinterpret_cast<const double2 *>(src);
+#pragma unroll
+    for (int i = 0; i < REC / 2; i++) {
+        const double2 v = __ldg(s2 + i);
+        r[2 * i] = v.x; r[2 * i + 1] = v.y;
+    }
 }
 
 // ---- a2-a4, parallel form (default): 8 lanes per cell --------------------------------------------
@@ -441,8 +471,12 @@ __global__ void __launch_bounds__(256) k_p2q8(GridP g, MatP mp, const int *__res
             const int kk = tt * 64 + local_id(bx & 3, by & 3, bz & 3);
             const int s0 = bstart[kk], e0 = bstart[kk + 1];
             const T dx = T(g.dx);
+#pragma unroll 2
             for (int p = s0; p < e0; p++) {
-                const T *r = rec + (int64_t)p * REC;
+                // the 96-byte (fp32) record in 16-byte loads (a scalar load per field costs one L1
+                // wavefront per lane: the 8 lanes of a group read 8 different buckets)
+                T r[REC];
+                ld_rec<T>(rec + (int64_t)p * REC, r);
                 // cell = base + o  =>  w = prod_a (o_a ? f_a : 1 - f_a)
                 const T w = (ox ? r[0] : T(1) - r[0]) * (oy ? r[1] : T(1) - r[1]) * (oz ? r[2] : T(1) - r[2]);
                 m += w * r[3];
@@ -852,8 +886,7 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CHECK(ensure(ctx, ctx->q_mG, C * 9 * s));
     MPL_CHECK(ensure(ctx, ctx->q_slot, C * nm * 16 * s));
     if (ctx->mats.plastic) MPL_CHECK(ensure(ctx, ctx->q_Sp, C * nm * 9 * s));
-    MPL_CHECK(ensure(ctx, ctx->q_vc, C * 4 * s));
-    MPL_CHECK(ensure(ctx, ctx->q_Gc, C * 9 * s));
+    MPL_CHECK(ensure(ctx, ctx->q_vc, C * 12 * s));  // (v_c, G_c) per cell, written by Load's n2c
     MPL_CHECK(ensure(ctx, ctx->K, (size_t)Ktot * s + 256));
     if (T_) {
         k_cell_list<<<T_, 64, 0, st>>>(T_, (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_cstart.p,

@@ -386,7 +386,7 @@ struct mpl_ctx_s {
     // quadrature (compact cells)
     DevBuf q_m, q_mv, q_mG, q_slot;  // q_slot: C * nmat * 16 (V, E xx yy zz xy yz xz, tau (6), pad)
     DevBuf q_Sp;                     // plastic runs: C * nmat * 9, S_k - I of the current Newton iterate
-    DevBuf q_vc, q_Gc;               // load: v_c, G_c
+    DevBuf q_vc;                     // load: (v_c, G_c) per cell, 12 reals
     DevBuf K;                        // tangent (scaled by 1/(16 dx^2)), per tile at t_kstart, 45 reals per real cell
     // nodes (tile-dense, T*64)
     DevBuf n_mass, n_flag, n_vn, n_vhat, n_v, n_vt, n_g, n_diag, n_invD, n_x, n_r, n_p, n_Hp, n_u, n_u2, n_act;
@@ -464,7 +464,6 @@ template <class F> void for_each_buf(mpl_ctx ctx, F f) {
         {"q_slot", ctx->q_slot},
         {"q_Sp", ctx->q_Sp},
         {"q_vc", ctx->q_vc},
-        {"q_Gc", ctx->q_Gc},
         {"K", ctx->K},
         {"t_ncell", ctx->t_ncell},
         {"t_kcnt", ctx->t_kcnt},

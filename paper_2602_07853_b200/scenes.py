@@ -356,6 +356,13 @@ def by_name(name: str, precision: Optional[int] = None) -> Scene:
     if name == "cfg4_nh":  # SURVEY f1 measured on cfg4's geometry: both materials split Neo-Hookean
         sc = cfg4(precision or 32)
         return dataclasses.replace(sc, name=name, materials=[dataclasses.replace(m, kind=1) for m in sc.materials])
+    if name == "cfg4_vm":  # SURVEY f2 on cfg4's geometry: pre-strained spheres with von Mises sigma_y = 500 Pa
+        sc = cfg4(precision or 32)
+        sph = sc.mat == 0
+        F = sc.F.copy()
+        F[sph] = _prestrain(int(sph.sum()), 5).astype(F.dtype)
+        m0 = dataclasses.replace(sc.materials[0], yield_stress=500.0)
+        return dataclasses.replace(sc, name=name, F=F, materials=[m0, sc.materials[1]])
     if name == "cfg4_water":  # SURVEY f4 on cfg4's geometry: the left sphere is J-based water (kappa = E)
         sc = cfg4(precision or 32)
         m0 = dataclasses.replace(sc.materials[0], E=2e5, kind=2)

@@ -252,6 +252,22 @@ MPL_API mpl_status mpl_explicit_velocity(mpl_ctx ctx);
  * resample, [2] explicit update, [6] transfer, [7] total; counts as for mpl_step. */
 MPL_API mpl_status mpl_explicit_step(mpl_ctx ctx, double dt, mpl_solve_stats *stats);
 
+/* ---- pipelined particle I/O (end-to-end stepping with host-resident particle state) ---------- */
+/* mpl_stage_particles: like mpl_set_particles, but asynchronous: the host arrays (pinned memory for
+ * real overlap) are copied on the context's H2D copy stream into a staging set, which the next
+ * mpl_resample adopts (it waits for the copy; the staged set becomes the particle state by a buffer
+ * swap).  May be called while the previous step computes, after that step's resample; one staged set
+ * at a time (MPL_ERR_STATE otherwise).  The host arrays must stay valid and unchanged until that
+ * adoption completes (mpl_stage_wait).  Single-rank contexts (MPL_ERR_UNSUPPORTED on slab ranks).
+ * mpl_get_particles_async: like mpl_get_particles (input order), but only enqueues: the reorder runs
+ * on the compute stream after the last enqueued work, the D2H copies on a second copy stream, so they
+ * overlap the next step; the host arrays are complete after mpl_stage_wait.
+ * mpl_stage_wait: blocks until every enqueued stage / readback copy and the compute stream are done. */
+MPL_API mpl_status mpl_stage_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v, const void *F,
+                                       const void *G, const void *vol, const int32_t *mat);
+MPL_API mpl_status mpl_get_particles_async(mpl_ctx ctx, void *x, void *v, void *F, void *G);
+MPL_API mpl_status mpl_stage_wait(mpl_ctx ctx);
+
 /* One full step: resample -> newton -> transfer (Alg. 1). */
 MPL_API mpl_status mpl_step(mpl_ctx ctx, double dt, const mpl_solver_cfg *cfg, mpl_solve_stats *stats);
 

@@ -276,6 +276,40 @@ mpl_status export_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G) {
     return MPL_OK;
 }
 
+// Pipelined readback: unsort x, v, F, G into the readback set on the compute stream (after whatever
+// step was enqueued last), then D2H on the copy stream; the next async readback waits until these
+// copies have drained the readback set (ev_rb_done).  mpl_stage_wait synchronises the copy stream.
+template <class T>
+mpl_status export_particles_async(mpl_ctx ctx, void *x, void *v, void *F, void *G) {
+    MPL_CHECK(io_streams(ctx));
+    cudaStream_t st = ctx->stream, cs = ctx->rstream;
+    const int64_t np = ctx->np;
+    const int c = ctx->cur;
+    if (ctx->rb_once) MPL_CUDA(cudaStreamWaitEvent(st, ctx->ev_rb_done, 0));
+    struct Item { void *dst; const void *src; int w; };
+    Item items[4] = {{x, ctx->px[c].p, 3}, {v, ctx->pv.p, 3}, {F, ctx->pF[c].p, 9}, {G, ctx->pG.p, 9}};
+    for (int i = 0; i < 4; i++) {
+        if (!items[i].dst || !np) continue;
+        MPL_CUDA(cudaStreamSynchronize(cs));  // ensure() may reallocate rb[i]
+        MPL_CHECK(ensure(ctx, ctx->rb[i], (size_t)np * items[i].w * sizeof(T)));
+        k_unsort<T><<<nblk(np * items[i].w, 256), 256, 0, st>>>(np, items[i].w, (const int *)ctx->pid[c].p,
+                                                                (const T *)items[i].src, (T *)ctx->rb[i].p);
+        ctx->launches++;
+    }
+    MPL_CUDA(cudaGetLastError());
+    MPL_CUDA(cudaEventRecord(ctx->ev_rb_ready, st));
+    MPL_CUDA(cudaStreamWaitEvent(cs, ctx->ev_rb_ready, 0));
+    for (int i = 0; i < 4; i++)
+        if (items[i].dst && np)
+            MPL_CUDA(cudaMemcpyAsync(items[i].dst, ctx->rb[i].p, np * items[i].w * sizeof(T), cudaMemcpyDefault, cs));
+    MPL_CUDA(cudaEventRecord(ctx->ev_rb_done, cs));
+    ctx->rb_once = true;
+    return MPL_OK;
+}
+
+template mpl_status export_particles_async<float>(mpl_ctx, void *, void *, void *, void *);
+template mpl_status export_particles_async<double>(mpl_ctx, void *, void *, void *, void *);
+
 template <class T>
 mpl_status export_quadrature(mpl_ctx ctx, int32_t *ijk, void *m_c, void *v_c, void *G_c, void *V_ck, void *tau_ck,
                              void *S_ck) {

@@ -701,6 +701,95 @@ mpl_status import_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v
     return MPL_OK;
 }
 
+// ---- pipelined particle input (mpl_stage_particles) ------------------------------------------------
+mpl_status io_streams(mpl_ctx ctx) {
+    if (ctx->cstream) return MPL_OK;
+    MPL_CUDA(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+    MPL_CUDA(cudaStreamCreateWithFlags(&ctx->rstream, cudaStreamNonBlocking));
+    for (cudaEvent_t *e : {&ctx->ev_staged, &ctx->ev_adopted, &ctx->ev_rb_ready, &ctx->ev_rb_done})
+        MPL_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    return MPL_OK;
+}
+
+// H2D of the next step's inputs into the staging set on the copy stream; it may only overwrite the
+// staging buffers once the compute stream has adopted the previous staged set (ev_adopted), i.e. once
+// the buffers swapped out then (the previous step's particle state) are no longer read.
+template <class T>
+mpl_status stage_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v, const void *F, const void *G,
+                           const void *vol, const int32_t *mat) {
+    MPL_CHECK(io_streams(ctx));
+    const size_t s = sizeof(T);
+    if (ctx->staged) return MPL_ERR_STATE;  // one staged set at a time
+    if (ctx->adopted_once) MPL_CUDA(cudaStreamWaitEvent(ctx->cstream, ctx->ev_adopted, 0));
+    // the live set is resized on adoption; staging sizes follow n (both sets swap roles every step)
+    MPL_CUDA(cudaStreamSynchronize(ctx->cstream));  // ensure() may free: nothing of ours in flight there
+    MPL_CHECK(ensure(ctx, ctx->sx, n * 3 * s));
+    MPL_CHECK(ensure(ctx, ctx->sv, n * 3 * s));
+    MPL_CHECK(ensure(ctx, ctx->sF, n * 9 * s));
+    MPL_CHECK(ensure(ctx, ctx->sG, n * 9 * s));
+    MPL_CHECK(ensure(ctx, ctx->svol, n * s));
+    MPL_CHECK(ensure(ctx, ctx->smat, n * 4));
+    cudaStream_t cs = ctx->cstream;
+    if (n) {
+        MPL_CUDA(cudaMemcpyAsync(ctx->sx.p, x, n * 3 * s, cudaMemcpyDefault, cs));
+        MPL_CUDA(cudaMemcpyAsync(ctx->sv.p, v, n * 3 * s, cudaMemcpyDefault, cs));
+        MPL_CUDA(cudaMemcpyAsync(ctx->sF.p, F, n * 9 * s, cudaMemcpyDefault, cs));
+        MPL_CUDA(cudaMemcpyAsync(ctx->sG.p, G, n * 9 * s, cudaMemcpyDefault, cs));
+        MPL_CUDA(cudaMemcpyAsync(ctx->svol.p, vol, n * s, cudaMemcpyDefault, cs));
+        MPL_CUDA(cudaMemcpyAsync(ctx->smat.p, mat, n * 4, cudaMemcpyDefault, cs));
+    }
+    MPL_CUDA(cudaEventRecord(ctx->ev_staged, cs));
+    ctx->staged = true;
+    ctx->staged_n = n;
+    return MPL_OK;
+}
+
+// Called by mpl_resample: the compute stream waits for the staged copy, the staged set becomes the
+// live particle set (buffer swap, no copy), the old live set becomes the staging set.
+template <class T>
+mpl_status adopt_staged(mpl_ctx ctx) {
+    if (!ctx->staged) return MPL_OK;
+    cudaStream_t st = ctx->stream;
+    MPL_CUDA(cudaStreamWaitEvent(st, ctx->ev_staged, 0));
+    const int64_t n = ctx->staged_n;
+    const size_t s = sizeof(T);
+    const int c = ctx->cur;
+    // live buffers may be larger than n (ensure only grows): sizes of the swapped pairs are exchanged
+    std::swap(ctx->px[c], ctx->sx);
+    std::swap(ctx->pv, ctx->sv);
+    std::swap(ctx->pF[c], ctx->sF);
+    std::swap(ctx->pG, ctx->sG);
+    std::swap(ctx->pvol[c], ctx->svol);
+    std::swap(ctx->pmat[c], ctx->smat);
+    ctx->np = n;
+    ctx->np_own = n;
+    const int nx = 1 - c;
+    MPL_CHECK(ensure(ctx, ctx->px[nx], n * 3 * s));
+    MPL_CHECK(ensure(ctx, ctx->pF[nx], n * 9 * s));
+    MPL_CHECK(ensure(ctx, ctx->pvol[nx], n * s));
+    MPL_CHECK(ensure(ctx, ctx->pmat[nx], n * 4));
+    for (int i = 0; i < 2; i++) MPL_CHECK(ensure(ctx, ctx->pid[i], n * 4));
+    MPL_CHECK(ensure(ctx, ctx->pkey, n * 4));
+    MPL_CHECK(ensure(ctx, ctx->prank, n * 4));
+    MPL_CHECK(ensure(ctx, ctx->pbase, n * 4));
+    MPL_CHECK(ensure(ctx, ctx->prec, n * REC * s));
+    if (n) k_iota<<<nblk(n, 256), 256, 0, st>>>(n, (int *)ctx->pid[c].p);
+    ctx->launches++;
+    MPL_CUDA(cudaGetLastError());
+    MPL_CUDA(cudaEventRecord(ctx->ev_adopted, st));
+    ctx->adopted_once = true;
+    ctx->staged = false;
+    ctx->have_particles = true;
+    return MPL_OK;
+}
+
+template mpl_status stage_particles<float>(mpl_ctx, int64_t, const void *, const void *, const void *, const void *,
+                                           const void *, const int32_t *);
+template mpl_status stage_particles<double>(mpl_ctx, int64_t, const void *, const void *, const void *, const void *,
+                                            const void *, const int32_t *);
+template mpl_status adopt_staged<float>(mpl_ctx);
+template mpl_status adopt_staged<double>(mpl_ctx);
+
 template <class T>
 mpl_status resample_impl(mpl_ctx ctx, double dt) {
     cudaStream_t st = ctx->stream;

@@ -201,6 +201,13 @@ void mpl_destroy(mpl_ctx ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->cstream) {
+        cudaStreamSynchronize(ctx->cstream);
+        cudaStreamSynchronize(ctx->rstream);
+        cudaStreamDestroy(ctx->cstream);
+        cudaStreamDestroy(ctx->rstream);
+        for (cudaEvent_t e : {ctx->ev_staged, ctx->ev_adopted, ctx->ev_rb_ready, ctx->ev_rb_done}) cudaEventDestroy(e);
+    }
     for_each_buf(ctx, [](const char *, DevBuf &b) { free_buf(b); });
     comm_destroy(ctx);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -368,6 +375,43 @@ mpl_status mpl_set_particles(mpl_ctx ctx, int64_t n, const void *x, const void *
     return s;
 }
 
+mpl_status mpl_stage_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v, const void *F, const void *G,
+                               const void *vol, const int32_t *mat) {
+    ApiLock api_lock_;
+    if (!ctx || n < 0 || (n > 0 && (!x || !v || !F || !G || !vol || !mat))) return MPL_ERR_INVALID_ARG;
+    if (n > (int64_t)1 << 30) return MPL_ERR_INVALID_ARG;
+    if (multi(ctx)) {
+        ctx->err = "mpl_stage_particles: single-rank contexts only (slab ranks use mpl_set_particles)";
+        return MPL_ERR_UNSUPPORTED;
+    }
+    MPL_CHECK(set_device(ctx));
+    mpl_status s = DISPATCH(ctx, stage_particles, n, x, v, F, G, vol, mat);
+    if (s == MPL_ERR_STATE) ctx->err = "mpl_stage_particles: the previous staged set was not adopted yet";
+    return s;
+}
+
+mpl_status mpl_get_particles_async(mpl_ctx ctx, void *x, void *v, void *F, void *G) {
+    ApiLock api_lock_;
+    if (!ctx) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(need(ctx, ctx->have_particles, "mpl_set_particles first"));
+    if (multi(ctx)) {
+        ctx->err = "mpl_get_particles_async: single-rank contexts only";
+        return MPL_ERR_UNSUPPORTED;
+    }
+    MPL_CHECK(set_device(ctx));
+    return DISPATCH(ctx, export_particles_async, x, v, F, G);
+}
+
+mpl_status mpl_stage_wait(mpl_ctx ctx) {
+    ApiLock api_lock_;
+    if (!ctx) return MPL_ERR_INVALID_ARG;
+    MPL_CHECK(set_device(ctx));
+    if (ctx->cstream) MPL_CUDA(cudaStreamSynchronize(ctx->cstream));
+    if (ctx->rstream) MPL_CUDA(cudaStreamSynchronize(ctx->rstream));
+    MPL_CUDA(cudaStreamSynchronize(ctx->stream));
+    return MPL_OK;
+}
+
 mpl_status mpl_get_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G, int32_t on_device) {
     ApiLock api_lock_;
     (void)on_device;
@@ -385,10 +429,11 @@ int64_t mpl_num_particles(mpl_ctx ctx) {
 mpl_status mpl_resample(mpl_ctx ctx, double dt, int64_t *n_cells, int64_t *n_nodes, int64_t *n_blocks) {
     ApiLock api_lock_;
     if (!ctx || !(dt > 0)) return MPL_ERR_INVALID_ARG;
-    MPL_CHECK(need(ctx, ctx->have_particles, "mpl_set_particles before mpl_resample"));
+    MPL_CHECK(need(ctx, ctx->have_particles || ctx->staged, "mpl_set_particles before mpl_resample"));
     MPL_CHECK(need(ctx, ctx->mats.nmat > 0, "mpl_set_materials before mpl_resample"));
     MPL_CHECK(set_device(ctx));
     ctx->resampled = ctx->linearized = ctx->solved = false;
+    if (ctx->staged) MPL_CHECK(ctx->precision == 64 ? adopt_staged<double>(ctx) : adopt_staged<float>(ctx));
     mpl_status s = DISPATCH(ctx, resample_impl, dt);
     if (s != MPL_OK) return s;
     if (n_cells) *n_cells = ctx->n_cells_active;

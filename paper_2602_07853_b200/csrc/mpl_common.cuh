@@ -359,6 +359,14 @@ struct mpl_ctx_s {
     DevBuf n_own, n_mown;                  // per node: owner flag (uint8), owned mass (m if owner else 0)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // pipelined particle I/O (mpl_stage_particles / mpl_get_particles_async): copy stream + events,
+    // a staged input set adopted by the next resample, a readback set copied out on the copy stream
+    cudaStream_t cstream = nullptr, rstream = nullptr;  // H2D staging / D2H readback (separate DMA engines)
+    cudaEvent_t ev_staged = nullptr, ev_adopted = nullptr, ev_rb_ready = nullptr, ev_rb_done = nullptr;
+    bool staged = false, adopted_once = false, rb_once = false;
+    int64_t staged_n = 0;
+    DevBuf sx, sv, sF, sG, svol, smat;  // staged inputs (swapped with the live set on adoption)
+    DevBuf rb[4];                       // readback: x, v, F, G in input order
     std::string err;
 
     GridP grid{};
@@ -425,6 +433,16 @@ mpl_status ensure(mpl_ctx ctx, DevBuf &b, size_t bytes);
 template <class F> void for_each_buf(mpl_ctx ctx, F f) {
     struct NB { const char *name; DevBuf &b; };
     NB all[] = {
+        {"sx", ctx->sx},
+        {"sv", ctx->sv},
+        {"sF", ctx->sF},
+        {"sG", ctx->sG},
+        {"svol", ctx->svol},
+        {"smat", ctx->smat},
+        {"rb[0]", ctx->rb[0]},
+        {"rb[1]", ctx->rb[1]},
+        {"rb[2]", ctx->rb[2]},
+        {"rb[3]", ctx->rb[3]},
         {"px[0]", ctx->px[0]},
         {"px[1]", ctx->px[1]},
         {"pF[0]", ctx->pF[0]},
@@ -527,6 +545,11 @@ template <class T> mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *
 template <class T> mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *st);
 template <class T> mpl_status g2p_impl(mpl_ctx ctx, double dt);
 template <class T> mpl_status explicit_impl(mpl_ctx ctx);
+template <class T> mpl_status stage_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v, const void *F,
+                                              const void *G, const void *vol, const int32_t *mat);
+template <class T> mpl_status adopt_staged(mpl_ctx ctx);
+template <class T> mpl_status export_particles_async(mpl_ctx ctx, void *x, void *v, void *F, void *G);
+mpl_status io_streams(mpl_ctx ctx);
 template <class T> mpl_status canon_to_tile(mpl_ctx ctx, const void *src, void *dst_tile);
 template <class T> mpl_status tile_to_canon(mpl_ctx ctx, const void *src_tile, void *dst);
 template <class T> mpl_status export_quadrature(mpl_ctx ctx, int32_t *ijk, void *m_c, void *v_c, void *G_c,

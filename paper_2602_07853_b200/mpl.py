@@ -122,6 +122,9 @@ _SIGS = {
     "mpl_transfer_to_particles": [_vp, _d],
     "mpl_step": [_vp, _d, _vp, _vp],
     "mpl_explicit_velocity": [_vp],
+    "mpl_stage_particles": [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp],
+    "mpl_get_particles_async": [_vp, _vp, _vp, _vp, _vp],
+    "mpl_stage_wait": [_vp],
     "mpl_explicit_step": [_vp, _d, _vp],
 }
 for _name, _args in _SIGS.items():
@@ -309,6 +312,25 @@ class Context:
                                          on_dev), "mpl_set_particles")
         self._keep = None
         self.np = n
+
+    def stage_particles(self, x, v, F, G, vol, mat):
+        """Asynchronous set_particles (mpl_stage_particles): the arrays (pinned host memory or torch
+        tensors) must stay alive and unchanged until stage_wait(); the next resample adopts them."""
+        n = int(x.shape[0])
+        x, v, F, G, vol = (self._real(a) for a in (x, v, F, G, vol))
+        if isinstance(mat, np.ndarray):
+            mat = np.ascontiguousarray(mat, dtype=np.int32)
+        self._staged_keep = (x, v, F, G, vol, mat)
+        self._chk(_lib.mpl_stage_particles(self._h, n, _ptr(x), _ptr(v), _ptr(F), _ptr(G), _ptr(vol), _ptr(mat)),
+                  "mpl_stage_particles")
+        self.np = n
+
+    def get_particles_async(self, x, v, F, G):
+        """Enqueue the readback (input order) into caller-owned host arrays; complete after stage_wait()."""
+        self._chk(_lib.mpl_get_particles_async(self._h, _ptr(x), _ptr(v), _ptr(F), _ptr(G)), "mpl_get_particles_async")
+
+    def stage_wait(self):
+        self._chk(_lib.mpl_stage_wait(self._h), "mpl_stage_wait")
 
     def set_slabs(self, cuts):
         c = np.ascontiguousarray(cuts, dtype=np.int32)

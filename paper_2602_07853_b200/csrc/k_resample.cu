@@ -697,7 +697,7 @@ mpl_status import_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v
     MPL_CUDA(cudaMemcpyAsync(ctx->pmat[0].p, mat, n * 4, cudaMemcpyDefault, st));
     if (n) k_iota<<<nblk(n, 256), 256, 0, st>>>(n, (int *)ctx->pid[0].p); ctx->launches++;
     MPL_CUDA(cudaGetLastError());
-    MPL_CUDA(cudaStreamSynchronize(st));
+    MPL_CHECK(d2h_sync(ctx, st));
     return MPL_OK;
 }
 
@@ -804,7 +804,7 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
 #ifdef MPL_DEBUG
     // debug build: host-side consistency checks of the particle bookkeeping
     auto count_neg = [&](const void *pid, int64_t n, int64_t *neg) -> mpl_status {
-        MPL_CUDA(cudaStreamSynchronize(st));
+        MPL_CHECK(d2h_sync(ctx, st));
         std::vector<int> h(n);
         if (n) MPL_CUDA(cudaMemcpy(h.data(), pid, n * 4, cudaMemcpyDeviceToHost));
         *neg = 0;
@@ -862,12 +862,12 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     // fetch error flags + tile count (one sync)
     DevScalars hs;
     int last_tile = 0, last_flag = 0;
-    MPL_CUDA(cudaMemcpyAsync(&hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
-    MPL_CUDA(cudaMemcpyAsync(&last_tile, (int *)ctx->tile_of.p + (N - 1), 4, cudaMemcpyDeviceToHost, st));
-    MPL_CUDA(cudaMemcpyAsync(&last_flag, (int *)ctx->nflag.p + (N - 1), 4, cudaMemcpyDeviceToHost, st));
+    MPL_CHECK(d2h(ctx, &hs, sc, sizeof hs, st));
+    MPL_CHECK(d2h(ctx, &last_tile, (int *)ctx->tile_of.p + (N - 1), 4, st));
+    MPL_CHECK(d2h(ctx, &last_flag, (int *)ctx->nflag.p + (N - 1), 4, st));
     unsigned long long nblocks = 0;
-    MPL_CUDA(cudaMemcpyAsync(&nblocks, counters + 0, 8, cudaMemcpyDeviceToHost, st));
-    MPL_CUDA(cudaStreamSynchronize(st));
+    MPL_CHECK(d2h(ctx, &nblocks, counters + 0, 8, st));
+    MPL_CHECK(d2h_sync(ctx, st));
     mpl_status bad = MPL_OK;
     if (hs.oob_particle != 0x7fffffff) {
         ctx->err = "particle " + std::to_string(hs.oob_particle) +
@@ -921,8 +921,8 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
 #ifdef MPL_DEBUG
     {
         int bsum = 0;
-        MPL_CUDA(cudaStreamSynchronize(st));
-        MPL_CUDA(cudaMemcpy(&bsum, (int *)ctx->t_bstart.p + (size_t)T_ * 64, 4, cudaMemcpyDeviceToHost));
+        MPL_CHECK(d2h_sync(ctx, st));
+        MPL_CHECK(d2h(ctx, &bsum, (int *)ctx->t_bstart.p + (size_t)T_ * 64, 4, st)); MPL_CHECK(d2h_sync(ctx, st));
         int64_t neg1 = 0;
         MPL_CHECK(count_neg(ctx->pid[nx].p, np, &neg1));
         if (bsum != np || neg1 != neg0) {
@@ -949,12 +949,12 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_ccount.p, (int *)ctx->t_cstart.p, (int64_t)T_ + 1));
     MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_kcnt.p, (int *)ctx->t_kstart.p, (int64_t)T_ + 1));
     int Cpad = 0, Ktot = 0;
-    MPL_CUDA(cudaMemcpyAsync(&Ktot, (int *)ctx->t_kstart.p + T_, 4, cudaMemcpyDeviceToHost, st));
+    MPL_CHECK(d2h(ctx, &Ktot, (int *)ctx->t_kstart.p + T_, 4, st));
     unsigned long long ncells = 0;
-    MPL_CUDA(cudaMemcpyAsync(&Cpad, (int *)ctx->t_cstart.p + T_, 4, cudaMemcpyDeviceToHost, st));
-    MPL_CUDA(cudaMemcpyAsync(&ncells, counters + 1, 8, cudaMemcpyDeviceToHost, st));
-    MPL_CUDA(cudaMemcpyAsync(&hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
-    MPL_CUDA(cudaStreamSynchronize(st));
+    MPL_CHECK(d2h(ctx, &Cpad, (int *)ctx->t_cstart.p + T_, 4, st));
+    MPL_CHECK(d2h(ctx, &ncells, counters + 1, 8, st));
+    MPL_CHECK(d2h(ctx, &hs, sc, sizeof hs, st));
+    MPL_CHECK(d2h_sync(ctx, st));
     bad = MPL_OK;
     if (hs.inv_particle != 0x7fffffff) {
         ctx->err = "particle " + std::to_string(hs.inv_particle) + " has det F_p <= 0 (inverted element)";
@@ -1029,23 +1029,23 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     DBG_GUARDS("resample #13");
         MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->n_act.p, (int *)ctx->n_canon.p, NT));
         int lc = 0, la = 0;  // read before k_node_canon rewrites inactive entries (stream order)
-        MPL_CUDA(cudaMemcpyAsync(&lc, (int *)ctx->n_canon.p + (NT - 1), 4, cudaMemcpyDeviceToHost, st));
-        MPL_CUDA(cudaMemcpyAsync(&la, (int *)ctx->n_act.p + (NT - 1), 4, cudaMemcpyDeviceToHost, st));
+        MPL_CHECK(d2h(ctx, &lc, (int *)ctx->n_canon.p + (NT - 1), 4, st));
+        MPL_CHECK(d2h(ctx, &la, (int *)ctx->n_act.p + (NT - 1), 4, st));
         k_node_canon<<<nblk(NT, 256), 256, 0, st>>>(NT, (const uint8_t *)ctx->n_flag.p, (int *)ctx->n_canon.p,
                                                     (int *)ctx->n_list.p); ctx->launches++;
     DBG_GUARDS("resample #14");
-        MPL_CUDA(cudaStreamSynchronize(st));
+        MPL_CHECK(d2h_sync(ctx, st));
         nact = lc + la;
         unsigned long long nf = 0;
-        MPL_CUDA(cudaMemcpy(&nf, counters + 2, 8, cudaMemcpyDeviceToHost));
+        MPL_CHECK(d2h(ctx, &nf, counters + 2, 8, st)); MPL_CHECK(d2h_sync(ctx, st));
         ctx->n_free_nodes = (int64_t)nf;
     }
     ctx->n_nodes_active = nact;
     MPL_CUDA(cudaGetLastError());
-    MPL_CUDA(cudaStreamSynchronize(st));
+    MPL_CHECK(d2h_sync(ctx, st));
     {
         int nf = 0;
-        MPL_CUDA(cudaMemcpy(&nf, &sc->nonfinite, sizeof nf, cudaMemcpyDeviceToHost));
+        MPL_CHECK(d2h(ctx, &nf, &sc->nonfinite, sizeof nf, st)); MPL_CHECK(d2h_sync(ctx, st));
         mpl_status bad2 = MPL_OK;
         if (nf) {
             ctx->err = "a quadrature stress lies outside the split Neo-Hookean inversion domain "

@@ -781,7 +781,7 @@ mpl_status tile_to_canon(mpl_ctx ctx, const void *src_tile, void *dst) {
     if (n) k_tile_to_canon<T><<<nblk(n, 256), 256, 0, st>>>(n, (const int *)ctx->n_list.p, (const vec4<T> *)src_tile,
                                                           (T *)ctx->io_stage.p); ctx->launches++;
     MPL_CUDA(cudaMemcpyAsync(dst, ctx->io_stage.p, n * 3 * sizeof(T), cudaMemcpyDefault, st));
-    MPL_CUDA(cudaStreamSynchronize(st));
+    MPL_CHECK(d2h_sync(ctx, st));
     return MPL_OK;
 }
 
@@ -817,8 +817,8 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
     MPL_CHECK(allreduce_d(ctx, sc->energy, NSTRIPE + 1));
     if (phi) {
         double e[NSTRIPE + 1];
-        MPL_CUDA(cudaMemcpyAsync(e, sc->energy, sizeof e, cudaMemcpyDeviceToHost, st));
-        MPL_CUDA(cudaStreamSynchronize(st));
+        MPL_CHECK(d2h(ctx, e, sc->energy, sizeof e, st));
+        MPL_CHECK(d2h_sync(ctx, st));
         *phi = e[NSTRIPE] != 0.0 ? __builtin_inf() : host_stripes(e);
     }
     if (mode == LIN_FULL) ctx->linearized = true;
@@ -914,9 +914,9 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         cudaEventRecord(e1, st);
         CGSlot s0;
         double e[NSTRIPE + 1];
-        MPL_CUDA(cudaMemcpyAsync(&s0, slots, sizeof s0, cudaMemcpyDeviceToHost, st));
-        MPL_CUDA(cudaMemcpyAsync(e, sc->energy, sizeof e, cudaMemcpyDeviceToHost, st));
-        MPL_CUDA(cudaStreamSynchronize(st));
+        MPL_CHECK(d2h(ctx, &s0, slots, sizeof s0, st));
+        MPL_CHECK(d2h(ctx, e, sc->energy, sizeof e, st));
+        MPL_CHECK(d2h_sync(ctx, st));
         t_lin += elapsed(e0, e1);
         phi0 = e[NSTRIPE] != 0.0 ? __builtin_inf() : host_stripes(e);
         const double rr0 = host_stripes(s0.rr);
@@ -973,18 +973,18 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                 MPL_CUDA(cudaGetLastError());
                 CGSlot sl;
                 int neg = 0;
-                MPL_CUDA(cudaMemcpyAsync(&sl, slots + launched, sizeof sl, cudaMemcpyDeviceToHost, st));
-                MPL_CUDA(cudaMemcpyAsync(&neg, &sc->neg_curv, sizeof neg, cudaMemcpyDeviceToHost, st));
-                MPL_CUDA(cudaStreamSynchronize(st));
+                MPL_CHECK(d2h(ctx, &sl, slots + launched, sizeof sl, st));
+                MPL_CHECK(d2h(ctx, &neg, &sc->neg_curv, sizeof neg, st));
+                MPL_CHECK(d2h_sync(ctx, st));
                 if (neg || host_stripes(sl.rr) <= thr) done = true;
                 chunk = std::min(chunk * 2, 64);
             }
             hslots.resize(launched + 1);
             int neg = 0, doneit = -1;
-            MPL_CUDA(cudaMemcpyAsync(hslots.data(), slots, (launched + 1) * sizeof(CGSlot), cudaMemcpyDeviceToHost, st));
-            MPL_CUDA(cudaMemcpyAsync(&neg, &sc->neg_curv, sizeof neg, cudaMemcpyDeviceToHost, st));
-            MPL_CUDA(cudaMemcpyAsync(&doneit, &sc->cg_done_iter, sizeof doneit, cudaMemcpyDeviceToHost, st));
-            MPL_CUDA(cudaStreamSynchronize(st));
+            MPL_CHECK(d2h(ctx, hslots.data(), slots, (launched + 1) * sizeof(CGSlot), st));
+            MPL_CHECK(d2h(ctx, &neg, &sc->neg_curv, sizeof neg, st));
+            MPL_CHECK(d2h(ctx, &doneit, &sc->cg_done_iter, sizeof doneit, st));
+            MPL_CHECK(d2h_sync(ctx, st));
             its = launched;
             if (neg) {
                 its = doneit;
@@ -1013,8 +1013,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         k_dot_gx<T><<<VA, 256, 0, st>>>(NA, list, flag, own, g, x, sc->gp); ctx->launches++;
         MPL_CHECK(allreduce_d(ctx, sc->gp, NSTRIPE));
         double gps[NSTRIPE];
-        MPL_CUDA(cudaMemcpyAsync(gps, sc->gp, sizeof gps, cudaMemcpyDeviceToHost, st));
-        MPL_CUDA(cudaStreamSynchronize(st));
+        MPL_CHECK(d2h(ctx, gps, sc->gp, sizeof gps, st));
+        MPL_CHECK(d2h_sync(ctx, st));
         const double gp = host_stripes(gps);
         double alpha = 1.0;
         int h = 0;
@@ -1050,8 +1050,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         k_dot_free<T><<<VG, 256, 0, st>>>(NT, flag, own, g, g, sc->gnorm2); ctx->launches++;
         MPL_CHECK(allreduce_d(ctx, sc->gnorm2, NSTRIPE));
         double g2[NSTRIPE];
-        MPL_CUDA(cudaMemcpyAsync(g2, sc->gnorm2, sizeof g2, cudaMemcpyDeviceToHost, st));
-        MPL_CUDA(cudaStreamSynchronize(st));
+        MPL_CHECK(d2h(ctx, g2, sc->gnorm2, sizeof g2, st));
+        MPL_CHECK(d2h_sync(ctx, st));
         S.grad_norm = sqrt(host_stripes(g2));
         if (S.grad_norm <= cfg->newton_rtol * S.grad_norm0) S.converged = 1;
     }
@@ -1111,7 +1111,7 @@ mpl_status explicit_impl(mpl_ctx ctx) {
         ctx->launches++;
     }
     MPL_CUDA(cudaGetLastError());
-    MPL_CUDA(cudaStreamSynchronize(st));
+    MPL_CHECK(d2h_sync(ctx, st));
     ctx->solved = true;
     return MPL_OK;
 }

@@ -209,6 +209,7 @@ void mpl_destroy(mpl_ctx ctx) {
         for (cudaEvent_t e : {ctx->ev_staged, ctx->ev_adopted, ctx->ev_rb_ready, ctx->ev_rb_done}) cudaEventDestroy(e);
     }
     for_each_buf(ctx, [](const char *, DevBuf &b) { free_buf(b); });
+    if (ctx->pio_buf) cudaFreeHost(ctx->pio_buf);
     comm_destroy(ctx);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;

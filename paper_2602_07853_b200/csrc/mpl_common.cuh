@@ -14,6 +14,7 @@
 
 #include <string>
 #include <vector>
+#include <cstring>
 
 #include "../../include/mpmlite.h"
 
@@ -359,6 +360,13 @@ struct mpl_ctx_s {
     DevBuf n_own, n_mown;                  // per node: owner flag (uint8), owned mass (m if owner else 0)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // pinned staging for the solver's small device->host control reads (counts, CG scalars): a copy
+    // into pageable memory waits behind any large D2H in flight on another stream (measured: 26 ms
+    // behind a 1.5 GB readback), a copy into pinned memory does not (0.07 ms)
+    char *pio_buf = nullptr;
+    size_t pio_cap = 0, pio_used = 0;
+    struct PioPend { void *dst; size_t off, n; };
+    std::vector<PioPend> pio_pend;
     // pipelined particle I/O (mpl_stage_particles / mpl_get_particles_async): copy stream + events,
     // a staged input set adopted by the next resample, a readback set copied out on the copy stream
     cudaStream_t cstream = nullptr, rstream = nullptr;  // H2D staging / D2H readback (separate DMA engines)
@@ -430,6 +438,33 @@ struct mpl_ctx_s {
 
 mpl_status ensure(mpl_ctx ctx, DevBuf &b, size_t bytes);
 // every device buffer of a context with its name (destroy, debug guard checks)
+// Enqueue a small device->host read into the context's pinned staging; the destination is filled by
+// the next d2h_sync (stream synchronisation + host copy).
+inline mpl_status d2h_sync(mpl_ctx ctx, cudaStream_t st) {
+    MPL_CUDA(cudaStreamSynchronize(st));
+    for (auto &q : ctx->pio_pend) memcpy(q.dst, ctx->pio_buf + q.off, q.n);
+    ctx->pio_pend.clear();
+    ctx->pio_used = 0;
+    return MPL_OK;
+}
+inline mpl_status d2h(mpl_ctx ctx, void *dst, const void *src, size_t n, cudaStream_t st) {
+    size_t off = (ctx->pio_used + 15) & ~(size_t)15;
+    if (off + n > ctx->pio_cap) {
+        if (!ctx->pio_pend.empty()) MPL_CHECK(d2h_sync(ctx, st));
+        size_t cap = ctx->pio_cap * 2 > n ? ctx->pio_cap * 2 : n;
+        if (cap < ((size_t)1 << 16)) cap = (size_t)1 << 16;
+        if (ctx->pio_buf) cudaFreeHost(ctx->pio_buf);
+        ctx->pio_buf = nullptr;
+        MPL_CUDA(cudaMallocHost((void **)&ctx->pio_buf, cap));
+        ctx->pio_cap = cap;
+        off = 0;
+    }
+    MPL_CUDA(cudaMemcpyAsync(ctx->pio_buf + off, src, n, cudaMemcpyDeviceToHost, st));
+    ctx->pio_pend.push_back({dst, off, n});
+    ctx->pio_used = off + n;
+    return MPL_OK;
+}
+
 template <class F> void for_each_buf(mpl_ctx ctx, F f) {
     struct NB { const char *name; DevBuf &b; };
     NB all[] = {
@@ -545,6 +580,7 @@ template <class T> mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *
 template <class T> mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *st);
 template <class T> mpl_status g2p_impl(mpl_ctx ctx, double dt);
 template <class T> mpl_status explicit_impl(mpl_ctx ctx);
+
 template <class T> mpl_status stage_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v, const void *F,
                                               const void *G, const void *vol, const int32_t *mat);
 template <class T> mpl_status adopt_staged(mpl_ctx ctx);

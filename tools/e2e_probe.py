@@ -45,22 +45,30 @@ with torch.cuda.stream(s2):
 torch.cuda.synchronize()
 print(f"H2D + D2H concurrently: {(time.perf_counter()-t)*1e3:.1f} ms", flush=True)
 del d
-for rep in range(2):
-    ctx.stage_particles(*host, mat)
+for mode in ("stage+readback", "stage only", "readback only"):
+    stage = mode != "readback only"
+    rb = mode != "stage only"
+    if stage:
+        ctx.stage_particles(*host, mat)
     T = []
     t_all = time.perf_counter()
-    for i in range(5):
+    for i in range(4):
         r = {}
+        if not stage:
+            t = time.perf_counter(); ctx.set_particles(*host, mat); r["set"] = time.perf_counter() - t
         t = time.perf_counter(); ctx.resample(sc.dt); r["resample"] = time.perf_counter() - t
         t = time.perf_counter()
-        if i < 4:
+        if stage and i < 3:
             ctx.stage_particles(*host, mat)
         r["stage"] = time.perf_counter() - t
         t = time.perf_counter(); st = ctx.newton_step(sc.solver); r["newton"] = time.perf_counter() - t
         t = time.perf_counter(); ctx.transfer_to_particles(sc.dt); r["transfer"] = time.perf_counter() - t
-        t = time.perf_counter(); ctx.get_particles_async(*outs); r["get_async"] = time.perf_counter() - t
+        t = time.perf_counter()
+        if rb:
+            ctx.get_particles_async(*outs)
+        r["get_async"] = time.perf_counter() - t
         T.append({k: round(v * 1e3, 2) for k, v in r.items()})
     t = time.perf_counter(); ctx.stage_wait(); w = time.perf_counter() - t
-    print(f"rep {rep}: total {(time.perf_counter()-t_all)*1e3:.1f} ms for 5 steps, final wait {w*1e3:.1f} ms", flush=True)
+    print(f"{mode}: total {(time.perf_counter()-t_all)*1e3:.1f} ms for 4 steps, final wait {w*1e3:.1f} ms", flush=True)
     for x in T:
         print("  ", x, flush=True)

@@ -103,22 +103,30 @@ def hvp_bytes(n_cells, n_nodes, s=4):
     return n_cells * 45 * s + n_nodes * 7 * s
 
 
-def hvp_kernel_name() -> str:
-    """The HVP kernel the library runs (MPL_HVP_KERNEL, default rp10: k_hvp_rp<T, 10>)."""
-    v = os.environ.get("MPL_HVP_KERNEL", "rp10")
-    return {"rq": "k_hvp_rq<10>", "rq8": "k_hvp_rq<8>", "rp10": "k_hvp_rp<10>", "rp": "k_hvp_rp<1>", "rp12": "k_hvp_rp<12>", "pipe2": "k_hvp_pipe<2>",
-            "pipe3": "k_hvp_pipe<3>", "reg": "k_hvp_reg"}.get(v, "k_hvp_rp<10>")
+def hvp_kernel_name(precision: int = 32) -> str:
+    """The HVP kernel the library runs (MPL_HVP_KERNEL; default "wz" = k_hvp_wz<3, 0, 0> in fp32, the
+    wz variants run fp32 only and fp64 uses k_hvp_rp<T, 10>)."""
+    v = os.environ.get("MPL_HVP_KERNEL", "wz")
+    wz = {"wz": "k_hvp_wz<3, 0, 0>", "wz2": "k_hvp_wz<2, 1, 0>", "wzp": "k_hvp_wz<3, 0, 1>",
+          "wzp2": "k_hvp_wz<2, 1, 1>", "wzs": "k_hvp_wz<3, 0, 2>", "wzs2": "k_hvp_wz<2, 1, 2>"}
+    if v in wz:
+        return wz[v] if precision == 32 else "k_hvp_rp<10>"
+    return {"rq": "k_hvp_rq<10>", "rq8": "k_hvp_rq<8>", "rp10": "k_hvp_rp<10>", "rp": "k_hvp_rp<1>", "rp12": "k_hvp_rp<12>",
+            "pipe2": "k_hvp_pipe<2>", "pipe3": "k_hvp_pipe<3>", "reg": "k_hvp_reg"}.get(v, "k_hvp_wz<3, 0, 0>")
 
 
 def workload_name(sc) -> str:
     return f"{sc.name}: {sc.n[0]}^3 grid, {sc.n_particles} particles, {len(sc.materials)} material(s), dt={sc.dt}"
 
 
-def load_traffic(config: str):
+def load_traffic(config: str, kernel: str):
+    """ncu DRAM bytes (read + write) of one HVP launch of `kernel` on `config` (profiles/hvp_traffic.json,
+    from the latest `ncu --set full` capture), else None."""
     p = os.path.join(ROOT, "profiles", "hvp_traffic.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get(config)
+        if d.get("kernel") == kernel:
+            return d.get(config)
     return None
 
 
@@ -227,8 +235,8 @@ def run_ours(args):
         "hvp_per_s": round(1e3 / avg_hvp_ms, 1) if avg_hvp_ms > 0 else None,
         "qp_per_s": round(cells_all / (avg_hvp_ms * 1e-3), 1) if avg_hvp_ms > 0 else None,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": load_traffic(sc.name) if ws == 1 else None,
-                     "peak_kind": peak_kind, "kernel": hvp_kernel_name(),
+                     "frac": round(achieved / peak, 4), "traffic": load_traffic(sc.name, hvp_kernel_name(args.precision)) if ws == 1 else None,
+                     "peak_kind": peak_kind, "kernel": hvp_kernel_name(args.precision),
                      "algorithmic_bytes_per_launch": int(nbytes), "pct_of_8TBps": round(achieved / 8000.0, 4)},
         "e2e": e2e,
         "gpu_launches": int(launches),

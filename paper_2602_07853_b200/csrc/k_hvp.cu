@@ -873,7 +873,476 @@ __global__ void __launch_bounds__(64, MINB) k_hvp_rq(int T_, const int *__restri
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// v6 (MPL_HVP_KERNEL=wz, fp32 default): one warp per tile, two z-adjacent cells per lane, no block
+// barriers.  ncu of rp10 at cfg4: 72 M warp instructions at IPC 1.9 — about 650 per warp per tile,
+// three times the arithmetic — so the kernel was issue bound, not HBM bound.  Here:
+//   * lane = 16 zp + 4 lx + ly owns cells A = (lx, ly, 2zp) and B = (lx, ly, 2zp + 1); they share the
+//     4 nodes of the plane z = 2zp + 1, so the lane reads 12 node vectors instead of 16 and scatters
+//     into 12 nodes instead of 16;
+//   * dG of both cells by tensor-product sums per node plane (7 adds per plane and component);
+//   * corner forces from 4 distinct sums per component and cell, signs folded into the adds;
+//   * the tangent uses the "kz" slot order (kz_key): the A cells of a tile first, then the B cells,
+//     each in lane order, so a warp's 16-byte loads of one chunk are contiguous; the 90 tangent
+//     numbers of the next tile are loaded (L2 evict-first) as soon as the current tile's K dG is done;
+//   * the u halo (shared slot 5x + 26y + z: conflict-free 16-byte accesses for every quarter-warp)
+//     and the owned masses are cp.async double-buffered per warp; the 12 scatter passes are
+//     read-modify-writes of a per-warp force buffer in the same slot map, separated by __syncwarp
+//     only (each pass is injective over the lanes).
+// ---------------------------------------------------------------------------------------------
+constexpr int WZ_W = 4;  // independent warps per CTA
+// per-warp shared state; PLANE: the 12 scatter passes write non-aliasing planes pl[pass][lane] (no
+// read-modify-write chain), the node phase sums a node's <= 8 plane entries
+template <bool PLANE> struct WzWarp {
+    alignas(16) f4 uh[2][132];
+    alignas(16) f4 F[PLANE ? 12 * 32 : 132];
+    alignas(16) float mh[2][64];
+};
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ float4 ldg_stream(const float *p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ldg_stream1(const float *p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+// node-phase node n (0..124) -> halo node (X, Y, Z): n < 80: Z = n / 16, X = n % 16 / 4, Y = n % 4 (a
+// quarter-warp covers X in {2j, 2j+1} x Y = 0..3, so 4X + Y is distinct mod 8); then the X = 4 / Y = 4
+// faces, 9 per plane Z
+__device__ __forceinline__ void wz_node(int n, int &X, int &Y, int &Z) {
+    if (n < 80) { Z = n >> 4; X = (n >> 2) & 3; Y = n & 3; }
+    else { const int m = n - 80, j = m % 9; Z = m / 9; X = j < 5 ? 4 : j - 5; Y = j < 5 ? j : 4; }
+}
+// role: local id | neighbour slot << 6 | owned << 9 | interior << 10 | u-halo slot (5X + 26Y + Z) << 11;
+// -1 = none
+__device__ __forceinline__ int wz_role(int n) {
+    if (n >= 125) return -1;
+    int X, Y, Z;
+    wz_node(n, X, Y, Z);
+    const int dp = ((X >> 2) << 2) | ((Y >> 2) << 1) | (Z >> 2);
+    const int interior = (X >= 1 && X <= 3 && Y >= 1 && Y <= 3 && Z >= 1 && Z <= 3);
+    return local_id(X & 3, Y & 3, Z & 3) | (dp << 6) | ((dp == 0) << 9) | (interior << 10) | ((5 * X + 26 * Y + Z) << 11);
+}
+// PLANE gather of node (X, Y, Z): pass (ox, oy, q) of lane (X - ox, Y - oy, zp) with 2 zp + q = Z lands
+// at pl index ((2 ox + oy) 3 + q) 32 + 16 zp + 4 (X - ox) + (Y - oy) = base + zoff + 188 ox + 95 oy,
+// base = 4X + Y.  Encoded: base | zoff1 << 5 | (Z == 2: second entry zoff 16) << 12 | valid (ox, oy)
+// mask << 13 (bit 2 ox + oy)
+__device__ __forceinline__ int wz_gather(int n) {
+    if (n >= 125) return 0;
+    int X, Y, Z;
+    wz_node(n, X, Y, Z);
+    const int zoff1 = Z == 0 ? 0 : Z == 1 ? 32 : Z == 2 ? 64 : Z == 3 ? 48 : 80;
+    int mask = 0;
+    for (int ox = 0; ox < 2; ox++)
+        for (int oy = 0; oy < 2; oy++)
+            if (X - ox >= 0 && X - ox <= 3 && Y - oy >= 0 && Y - oy <= 3) mask |= 1 << (2 * ox + oy);
+    return (4 * X + Y) | (zoff1 << 5) | ((Z == 2) << 12) | (mask << 13);
+}
+
+// packed upper-triangle element e -> row r (kofs(r) <= e < kofs(r + 1)) and column
+__host__ __device__ constexpr int krow(int e) {
+    int r = 0;
+    while (r < 8 && kofs(r + 1) <= e) r++;
+    return r;
+}
+__host__ __device__ constexpr int kcol(int e) { return krow(e) + (e - kofs(krow(e))); }
+
+// ROLL: each 16-byte chunk of the next tile's tangent is requested as soon as the current tile's K dG
+// has consumed its registers (a whole tile period to arrive) instead of after the whole K dG.
+// SCAT: how the 12 node contributions of a lane reach the nodes —
+//   WZ_RMW   read-modify-write passes into a per-warp force buffer, then a node phase (4 nodes / lane);
+//   WZ_PLANE non-aliasing plane stores, node phase sums <= 8 plane entries per node;
+//   WZ_SHFL  register reduction with shuffles along y (1 lane), x (4 lanes), z (16 lanes), after which
+//            every node value sits in exactly one (lane, slot) and goes straight to global memory; no
+//            force buffer and no node phase.
+enum { WZ_RMW = 0, WZ_PLANE = 1, WZ_SHFL = 2 };
+template <int MINB, bool ROLL, int SCAT>
+__global__ void __launch_bounds__(32 * WZ_W, MINB)
+    k_hvp_wz(int T_, const int *__restrict__ nplus, const unsigned long long *__restrict__ cmask,
+             const int *__restrict__ hascells, const float *__restrict__ K, const int *__restrict__ kstart,
+             const float *__restrict__ nmass, const f4 *__restrict__ u, f4 *__restrict__ Hu, double *__restrict__ uHu,
+             const CGSlot *__restrict__ cgs, int cgj, double cgthr, const DevScalars *__restrict__ sc) {
+    constexpr bool PLANE = SCAT == WZ_PLANE, SHFL = SCAT == WZ_SHFL;
+    __shared__ WzWarp<PLANE> SW[WZ_W];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    WzWarp<PLANE> &S = SW[wid];
+    if (cgs != nullptr) {
+        const double rr = warp_sum(cgs[cgj].rr[lane]);
+        if (sc->neg_curv || (cgj > 0 && rr <= cgthr)) return;
+    }
+    const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
+    const int zp = lane >> 4, lx = (lane >> 2) & 3, ly = lane & 3;
+    const int lA = lx * 16 + ly * 4 + 2 * zp;  // cell A's local position (B = lA + 1)
+    const int hb = 5 * lx + 26 * ly + 2 * zp;  // u-halo slot of cell A's (0,0,0) corner
+    int role[4], gat[4];
+#pragma unroll
+    for (int r = 0; r < 4; r++) { role[r] = wz_role(lane + 32 * r); gat[r] = PLANE ? wz_gather(lane + 32 * r) : 0; }
+    if (SCAT == WZ_RMW)
+        for (int i = lane; i < 132; i += 32) S.F[i] = mk4<float>(0.f, 0.f, 0.f, 0.f);
+    const uint64_t pol = l2_evict_first_policy();
+    const int G = gridDim.x * WZ_W, t0 = blockIdx.x * WZ_W + wid;
+    // tile metadata, spread over lanes 0-11: neighbours (lane 0 = the tile itself), kstart, has, cmask
+    // halves; one 32-bit load per lane at a per-lane base + stride t, no use until the next iteration
+    const int *mbase = lane < 8 ? nplus + lane : lane == 8 ? kstart : lane == 9 ? hascells
+                                                                      : reinterpret_cast<const int *>(cmask) + (lane - 10);
+    const int mstride = lane < 8 ? 8 : lane < 10 ? 1 : 2;
+    auto load_meta = [&](int t) -> int {
+        if (t >= T_ || lane >= 12) return 0;
+        return lane == 0 ? t : __ldg(mbase + (int64_t)mstride * t);
+    };
+    struct TileK {
+        int has, pA, pB, n, sA, sB;  // n: the tile's cells; sA / sB: this lane's cells' tangent slots
+        const float *kb;             // the tile's tangent block
+    };
+    auto tile_k = [&](int t, int meta) -> TileK {
+        TileK q;
+        q.has = __shfl_sync(FULL, meta, 9);
+        const int ks = __shfl_sync(FULL, meta, 8);
+        const unsigned clo = (unsigned)__shfl_sync(FULL, meta, 10), chi = (unsigned)__shfl_sync(FULL, meta, 11);
+        if (t >= T_) q.has = 0;
+        const unsigned word = lA < 32 ? clo : chi;
+        q.pA = q.has ? (int)((word >> (lA & 31)) & 1u) : 0;
+        q.pB = q.has ? (int)((word >> ((lA + 1) & 31)) & 1u) : 0;
+        const unsigned pmA = __ballot_sync(FULL, q.pA), pmB = __ballot_sync(FULL, q.pB);
+        const int nA = __popc(pmA);
+        q.n = nA + __popc(pmB);
+        q.sA = __popc(pmA & lt);
+        q.sB = nA + __popc(pmB & lt);
+        q.kb = K + ks;
+        return q;
+    };
+    float k[90];
+    // chunk c (16 bytes at kb + 4 (c n + s); c = 11: element 44 at kb + 44 n + s) of cell X (off 0 = A,
+    // 45 = B) of tile q -> k
+    auto kload = [&](const TileK &q, int off, int c) {
+        if (!(off ? q.pB : q.pA)) return;
+        const int sl = off ? q.sB : q.sA;
+        if (c < 11) {
+            const float4 v = ldg_stream(q.kb + 4 * (c * q.n + sl), pol);
+            k[off + 4 * c] = v.x; k[off + 4 * c + 1] = v.y; k[off + 4 * c + 2] = v.z; k[off + 4 * c + 3] = v.w;
+        } else {
+            k[off + 44] = ldg_stream1(q.kb + 44 * q.n + sl, pol);
+        }
+    };
+    // tile t: u halo + owned masses -> shared buffer b (cp.async, one group)
+    auto halo = [&](int t, int b, int meta) {
+        const int has = __shfl_sync(FULL, meta, 9);
+        int tt[4];
+#pragma unroll
+        for (int r = 0; r < 4; r++) tt[r] = __shfl_sync(FULL, meta, role[r] < 0 ? 0 : (role[r] >> 6) & 7);
+        if (t < T_) {
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                if (role[r] < 0) continue;
+                const int loc = role[r] & 63, owned = (role[r] >> 9) & 1, h = role[r] >> 11;
+                if ((has || owned) && tt[r] >= 0) {
+                    const int64_t nd = (int64_t)tt[r] * 64 + loc;
+                    cp_async16(&S.uh[b][h], u + nd);
+                    if (owned) cp_async4(&S.mh[b][loc], nmass + nd);
+                } else {
+                    S.uh[b][h] = mk4<float>(0.f, 0.f, 0.f, 0.f);
+                    if (owned) S.mh[b][loc] = 0.f;
+                }
+            }
+        }
+        cp_async_commit();
+    };
+    int mcur = load_meta(t0);
+    int mnext = load_meta(t0 + G);
+    TileK cur = tile_k(t0, mcur);
+#pragma unroll
+    for (int c = 0; c < 12; c++) { kload(cur, 0, c); kload(cur, 45, c); }
+    halo(t0, 0, mcur);
+    double acc = 0.0;
+    int it = 0;
+    for (int t = t0; t < T_; t += G, it++) {
+        const int b = it & 1;
+        const int mnn = load_meta(t + 2 * G);
+        const TileK nxt = tile_k(t + G, mnext);
+        cp_async_wait<0>();
+        __syncwarp();
+        const f4 *uh = S.uh[b];
+        float PA[9], PB[9];
+        if (cur.has) {
+            // ---- dG of cells A and B from the 12 nodes (ox, oy) x z-plane q = 0, 1, 2
+            float Dx[3][3], Dy[3][3], Sz[3][3];  // [plane][component]
+#pragma unroll
+            for (int q = 0; q < 3; q++) {
+                const f4 w00 = uh[hb + q], w01 = uh[hb + 26 + q], w10 = uh[hb + 5 + q], w11 = uh[hb + 31 + q];
+                const float a00[3] = {w00.x, w00.y, w00.z}, a01[3] = {w01.x, w01.y, w01.z};
+                const float a10[3] = {w10.x, w10.y, w10.z}, a11[3] = {w11.x, w11.y, w11.z};
+#pragma unroll
+                for (int a = 0; a < 3; a++) {
+                    const float s1 = a11[a] - a00[a], s2 = a10[a] - a01[a];
+                    Dx[q][a] = s1 + s2;  // sum over oy of (x=1) - (x=0)
+                    Dy[q][a] = s1 - s2;  // sum over ox of (y=1) - (y=0)
+                    Sz[q][a] = (a00[a] + a11[a]) + (a01[a] + a10[a]);
+                }
+            }
+            float dA[9], dB[9];
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+                dA[3 * a] = Dx[0][a] + Dx[1][a]; dA[3 * a + 1] = Dy[0][a] + Dy[1][a]; dA[3 * a + 2] = Sz[1][a] - Sz[0][a];
+                dB[3 * a] = Dx[1][a] + Dx[2][a]; dB[3 * a + 1] = Dy[1][a] + Dy[2][a]; dB[3 * a + 2] = Sz[2][a] - Sz[1][a];
+            }
+            // ---- P = K dG (symmetric, packed upper triangle), element by element
+#pragma unroll
+            for (int r = 0; r < 9; r++) { PA[r] = 0.f; PB[r] = 0.f; }
+#pragma unroll
+            for (int e = 0; e < 45; e++) {
+                const int r = krow(e), c = kcol(e);
+                PA[r] += k[e] * dA[c];
+                if (c != r) PA[c] += k[e] * dA[r];
+                if (ROLL && ((e & 3) == 3 || e == 44)) kload(nxt, 0, e >> 2);
+            }
+#pragma unroll
+            for (int e = 0; e < 45; e++) {
+                const int r = krow(e), c = kcol(e);
+                PB[r] += k[45 + e] * dB[c];
+                if (c != r) PB[c] += k[45 + e] * dB[r];
+                if (ROLL && ((e & 3) == 3 || e == 44)) kload(nxt, 45, e >> 2);
+            }
+            float qf = 0.f;
+#pragma unroll
+            for (int r = 0; r < 9; r++) {
+                PA[r] = cur.pA ? PA[r] : 0.f;  // absent cells: k holds stale numbers
+                PB[r] = cur.pB ? PB[r] : 0.f;
+                qf += PA[r] * dA[r] + PB[r] * dB[r];
+            }
+            acc += (double)qf;
+        }
+        if (!ROLL || !cur.has) {
+            // k is free: start the next tile's loads; they overlap the scatter and the node phase
+#pragma unroll
+            for (int c = 0; c < 12; c++) { kload(nxt, 0, c); kload(nxt, 45, c); }
+        }
+        halo(t + G, b ^ 1, mnext);
+        // corner force of cell X at (sx, sy, sz) = +-(Px +- Py) +- Pz per component: 4 sums g; the value
+        // of corner (ox, oy, oz): (sx, sy) = (+,+) -> g0/g1, (-,-) -> -g1/-g0, (+,-) -> g2/g3,
+        // (-,+) -> -g3/-g2 (first for sz = +1, second for sz = -1)
+        auto corner = [&](const float g[4], int ox, int oy, int oz) -> float {
+            if (ox && oy) return oz ? g[0] : g[1];
+            if (!ox && !oy) return oz ? -g[1] : -g[0];
+            if (ox) return oz ? g[2] : g[3];
+            return oz ? -g[3] : -g[2];
+        };
+        if (SHFL) {
+            // ---- contributions c[ox][oy][q] of node (lx + ox, ly + oy, 2 zp + q), reduced in registers
+            float c[2][2][3][3];
+            if (cur.has) {
+                float gA[3][4], gB[3][4];
+#pragma unroll
+                for (int a = 0; a < 3; a++) {
+                    const float e1 = PA[3 * a] + PA[3 * a + 1], e2 = PA[3 * a] - PA[3 * a + 1], z = PA[3 * a + 2];
+                    gA[a][0] = e1 + z; gA[a][1] = e1 - z; gA[a][2] = e2 + z; gA[a][3] = e2 - z;
+                    const float f1 = PB[3 * a] + PB[3 * a + 1], f2 = PB[3 * a] - PB[3 * a + 1], y = PB[3 * a + 2];
+                    gB[a][0] = f1 + y; gB[a][1] = f1 - y; gB[a][2] = f2 + y; gB[a][3] = f2 - y;
+                }
+#pragma unroll
+                for (int ox = 0; ox < 2; ox++)
+#pragma unroll
+                    for (int oy = 0; oy < 2; oy++)
+#pragma unroll
+                        for (int q = 0; q < 3; q++)
+#pragma unroll
+                            for (int a = 0; a < 3; a++) {
+                                float v = 0.f;
+                                if (q < 2) v = corner(gA[a], ox, oy, q);
+                                if (q > 0) v += corner(gB[a], ox, oy, q - 1);
+                                c[ox][oy][q][a] = v;
+                            }
+                // y: node (., ly + 1, .) of lane ly == node (., ly, .) of lane ly + 1
+#pragma unroll
+                for (int ox = 0; ox < 2; ox++)
+#pragma unroll
+                    for (int q = 0; q < 3; q++)
+#pragma unroll
+                        for (int a = 0; a < 3; a++) {
+                            const float r = __shfl_up_sync(FULL, c[ox][1][q][a], 1);
+                            if (ly > 0) c[ox][0][q][a] += r;
+                        }
+                // x: 4 lanes
+#pragma unroll
+                for (int oy = 0; oy < 2; oy++)
+#pragma unroll
+                    for (int q = 0; q < 3; q++)
+#pragma unroll
+                        for (int a = 0; a < 3; a++) {
+                            const float r = __shfl_up_sync(FULL, c[1][oy][q][a], 4);
+                            if (lx > 0) c[0][oy][q][a] += r;
+                        }
+                // z: plane q = 2 of zp = 0 is plane q = 0 of zp = 1
+#pragma unroll
+                for (int ox = 0; ox < 2; ox++)
+#pragma unroll
+                    for (int oy = 0; oy < 2; oy++)
+#pragma unroll
+                        for (int a = 0; a < 3; a++) {
+                            const float r = __shfl_up_sync(FULL, c[ox][oy][2][a], 16);
+                            if (zp > 0) c[ox][oy][0][a] += r;
+                        }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 36; i++) (&c[0][0][0][0])[i] = 0.f;
+            }
+            // ---- outputs: slot (ox, oy, q) holds a complete node iff (ox == 0 || lx == 3) && (oy == 0 ||
+            // ly == 3) && (q < 2 || zp == 1); its tile is neighbour (ox, oy, q == 2) (warp-uniform)
+#pragma unroll
+            for (int ox = 0; ox < 2; ox++)
+#pragma unroll
+                for (int oy = 0; oy < 2; oy++)
+#pragma unroll
+                    for (int q = 0; q < 3; q++) {
+                        const int dp = (ox << 2) | (oy << 1) | (q == 2);
+                        const int tt = __shfl_sync(FULL, mcur, dp);
+                        const bool valid = (ox == 0 || lx == 3) && (oy == 0 || ly == 3) && (q < 2 || zp == 1);
+                        if (!valid || tt < 0) continue;
+                        const int X = lx + ox, Y = ly + oy, Z = 2 * zp + q;
+                        const int loc = local_id(X & 3, Y & 3, Z & 3);
+                        float fx = c[ox][oy][q][0], fy = c[ox][oy][q][1], fz = c[ox][oy][q][2];
+                        bool interior = false;
+                        if (dp == 0) {  // owned node: lumped mass term
+                            const float mm = S.mh[b][loc];
+                            if (mm > 0.f) {
+                                const f4 w = uh[hb + q];
+                                fx += mm * w.x; fy += mm * w.y; fz += mm * w.z;
+                                acc += (double)(mm * (w.x * w.x + w.y * w.y + w.z * w.z));
+                            }
+                            interior = X >= 1 && Y >= 1 && Z >= 1 && Z <= 3;
+                        } else if (!cur.has) {
+                            continue;
+                        }
+                        const int64_t nd = (int64_t)tt * 64 + loc;
+                        if (interior) Hu[nd] = mk4<float>(fx, fy, fz, 0.f);
+                        else if (fx != 0.f || fy != 0.f || fz != 0.f) atomic_add3<float>(Hu + nd, fx, fy, fz);
+                    }
+            __syncwarp();  // uh[b] / mh[b] read before the next halo refills them
+            mcur = mnext;
+            mnext = mnn;
+            cur = nxt;
+            continue;
+        }
+        if (cur.has) {
+            float gA[3][4], gB[3][4];
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+                const float e1 = PA[3 * a] + PA[3 * a + 1], e2 = PA[3 * a] - PA[3 * a + 1], z = PA[3 * a + 2];
+                gA[a][0] = e1 + z; gA[a][1] = e1 - z; gA[a][2] = e2 + z; gA[a][3] = e2 - z;
+                const float f1 = PB[3 * a] + PB[3 * a + 1], f2 = PB[3 * a] - PB[3 * a + 1], y = PB[3 * a + 2];
+                gB[a][0] = f1 + y; gB[a][1] = f1 - y; gB[a][2] = f2 + y; gB[a][3] = f2 - y;
+            }
+#pragma unroll
+            for (int ox = 0; ox < 2; ox++)
+#pragma unroll
+                for (int oy = 0; oy < 2; oy++)
+#pragma unroll
+                    for (int q = 0; q < 3; q++) {
+                        f4 f = mk4<float>(0.f, 0.f, 0.f, 0.f);
+                        if (q < 2) { f.x = corner(gA[0], ox, oy, q); f.y = corner(gA[1], ox, oy, q); f.z = corner(gA[2], ox, oy, q); }
+                        if (q > 0) {
+                            f.x += corner(gB[0], ox, oy, q - 1); f.y += corner(gB[1], ox, oy, q - 1);
+                            f.z += corner(gB[2], ox, oy, q - 1);
+                        }
+                        if (PLANE) {
+                            S.F[((2 * ox + oy) * 3 + q) * 32 + lane] = f;
+                        } else {
+                            f4 *fp = &S.F[hb + 5 * ox + 26 * oy + q];
+                            const f4 o = *fp;
+                            *fp = mk4<float>(o.x + f.x, o.y + f.y, o.z + f.z, 0.f);
+                            __syncwarp();
+                        }
+                    }
+            if (PLANE) __syncwarp();
+        }
+        // ---- node phase: forces + lumped mass term, stored (interior) or added atomically (faces)
+        int tt[4];
+#pragma unroll
+        for (int r = 0; r < 4; r++) tt[r] = __shfl_sync(FULL, mcur, role[r] < 0 ? 0 : (role[r] >> 6) & 7);
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            if (role[r] < 0) continue;
+            const int loc = role[r] & 63, owned = (role[r] >> 9) & 1, interior = (role[r] >> 10) & 1,
+                      h = role[r] >> 11;
+            f4 f = mk4<float>(0.f, 0.f, 0.f, 0.f);
+            if (cur.has) {
+                if (PLANE) {
+                    const int g = gat[r], i1 = (g & 31) + ((g >> 5) & 127), two = (g >> 12) & 1, mk = g >> 13;
+#pragma unroll
+                    for (int o = 0; o < 4; o++) {
+                        if (!((mk >> o) & 1)) continue;
+                        const int i = i1 + (o >> 1) * 188 + (o & 1) * 95;
+                        const f4 a = S.F[i];
+                        f.x += a.x; f.y += a.y; f.z += a.z;
+                        if (two) {
+                            const f4 c2 = S.F[i - 48];  // zoff 64 -> 16
+                            f.x += c2.x; f.y += c2.y; f.z += c2.z;
+                        }
+                    }
+                } else {
+                    f = S.F[h];
+                    S.F[h] = mk4<float>(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+            if (!(cur.has || owned) || tt[r] < 0) continue;
+            if (owned) {
+                const float mm = S.mh[b][loc];
+                if (mm > 0.f) {
+                    const f4 w = uh[h];
+                    f.x += mm * w.x; f.y += mm * w.y; f.z += mm * w.z;
+                    acc += (double)(mm * (w.x * w.x + w.y * w.y + w.z * w.z));
+                }
+            }
+            const int64_t nd = (int64_t)tt[r] * 64 + loc;
+            if (interior) Hu[nd] = mk4<float>(f.x, f.y, f.z, 0.f);
+            else if (f.x != 0.f || f.y != 0.f || f.z != 0.f) atomic_add3<float>(Hu + nd, f.x, f.y, f.z);
+        }
+        __syncwarp();  // node phase done reading uh[b] / mh[b] / planes before they are refilled
+        mcur = mnext;
+        mnext = mnn;
+        cur = nxt;
+    }
+    cp_async_wait<0>();
+    if (uHu) {
+        const double v = warp_sum(acc);
+        if (lane == 0 && v != 0.0) atomicAdd(&uHu[(blockIdx.x * WZ_W + wid) % NSTRIPE], v);
+    }
+}
+
 int g_num_sms = 0;
+
+template <int MINB, bool ROLL, int SCAT>
+mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
+                     double cgthr) {
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        int occ = 0;
+        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_wz<MINB, ROLL, SCAT>, 32 * WZ_W, 0));
+        per_sm = occ > 0 ? occ : 1;
+    }
+    int grid = g_num_sms * per_sm;
+    const int need = (ctx->T + WZ_W - 1) / WZ_W;
+    if (grid > need) grid = need;
+    k_hvp_wz<MINB, ROLL, SCAT><<<grid, 32 * WZ_W, 0, ctx->stream>>>(
+        ctx->T, (const int *)ctx->t_nplus.p, (const unsigned long long *)ctx->t_cmask.p,
+        (const int *)ctx->t_hascells.p, (const float *)ctx->K.p, (const int *)ctx->t_kstart.p,
+        (const float *)owned_mass(ctx), (const f4 *)u_tile, (f4 *)Hu_tile, uHu, cgs, cgj, cgthr,
+        (const DevScalars *)ctx->scalars.p);
+    ctx->launches++;
+    MPL_CUDA(cudaGetLastError());
+    return MPL_OK;
+}
 
 template <class T, int MINB>
 mpl_status launch_rq(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
@@ -953,22 +1422,49 @@ mpl_status launch_pipe(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *u
 
 }  // namespace
 
+// HVP variant from MPL_HVP_KERNEL: "wz" (default for fp32; fp64 falls back to rp10; "wzp" with the
+// plane scatter, "wzs" with the shuffle reduction, "wz2" / "wzp2" / "wzs2" with rolling tangent loads at
+// 2 CTAs per SM), "rp10" (default
+// for fp64), "rp" / "rp12": persistent, tangent register-pipelined (v4) with >= 10 / 1 / 12 CTAs per SM
+// requested from ptxas; "rq" / "rq8" (v5); "pipe2" / "pipe3": persistent TMA-ring v3 with 2 / 3 stages;
+// "reg": one tile per CTA (v2)
+int hvp_variant() {
+    static int variant = -1;
+    if (variant < 0) {
+        const char *e = getenv("MPL_HVP_KERNEL");
+        variant = 11;
+        if (e && e[0] == 'w' && e[1] == 'z') {
+            const int sc = e[2] == 'p' ? 1 : e[2] == 's' ? 2 : 0;
+            const bool roll = e[sc ? 3 : 2] == '2';
+            variant = sc == 1 ? (roll ? 10 : 9) : sc == 2 ? (roll ? 14 : 13) : (roll ? 12 : 11);
+        }
+        else if (e && e[0] == 'r' && e[1] == 'q') variant = e[2] == '8' ? 8 : 7;
+        else if (e && e[0] == 'r' && e[1] == 'p') variant = e[2] == '1' ? (e[3] == '2' ? 6 : 5) : 4;
+        else if (e && e[0] == 'r') variant = 0;
+        else if (e && e[0] == 'p' && e[4] == '3') variant = 3;
+        else if (e && e[0] == 'p') variant = 2;
+    }
+    return variant;
+}
+// the wz kernel reads the tangent in the kz slot order (kz_key); k_linearize writes it that way
+bool hvp_kz_layout(int precision) { return precision == 32 && hvp_variant() >= 9 && hvp_variant() <= 14; }
+
 // Hu (tile-dense) must be zero on every node that receives atomics (all non-interior nodes).
 template <class T>
 mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
                       double cgthr) {
     if (ctx->T == 0) return MPL_OK;
-    static int variant = -1;
-    if (variant < 0) {
-        // "rp10" (default) / "rp" / "rp12": persistent, tangent register-pipelined (v4) with >= 10 / 1 /
-        // 12 CTAs per SM requested from ptxas; "pipe2" / "pipe3": persistent TMA-ring v3 with 2 / 3
-        // stages; "reg": one tile per CTA (v2)
-        const char *e = getenv("MPL_HVP_KERNEL");
+    int variant = hvp_variant();
+    if (variant >= 9 && variant <= 14) {
+        if (sizeof(T) == 4) {
+            if (variant == 9) return launch_wz<3, false, WZ_PLANE>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+            if (variant == 10) return launch_wz<2, true, WZ_PLANE>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+            if (variant == 11) return launch_wz<3, false, WZ_RMW>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+            if (variant == 13) return launch_wz<3, false, WZ_SHFL>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+            if (variant == 14) return launch_wz<2, true, WZ_SHFL>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+            return launch_wz<2, true, WZ_RMW>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+        }
         variant = 5;
-        if (e && e[0] == 'r' && e[1] == 'q') variant = e[2] == '8' ? 8 : 7;
-        else if (e && e[0] == 'r' && e[1] == 'p') variant = e[2] == '1' ? (e[3] == '2' ? 6 : 5) : 4;
-        else if (e && e[0] == 'r') variant = 0;
-        else if (e && e[0] == 'p' && e[4] == '3') variant = 3;
     }
     if (variant == 7) return launch_rq<T, 10>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
     if (variant == 8) return launch_rq<T, 8>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);

@@ -52,12 +52,13 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
                                                    const T *__restrict__ qslot, T *__restrict__ Kout,
                                                    const int *__restrict__ kstart, const int *__restrict__ ncell,
                                                    vec4<T> *__restrict__ grad, vec4<T> *__restrict__ diag,
-                                                   T *__restrict__ qsp, DevScalars *sc) {
+                                                   T *__restrict__ qsp, DevScalars *sc, int kz) {
     constexpr int KS = (MODE == LIN_FULL) ? 64 * 45 : 1;
     __shared__ vec4<T> vh[125];
     __shared__ T Pg[64 * 9];
     __shared__ T Ks[KS];
     __shared__ int cslot[64];
+    __shared__ int zslot[MODE == LIN_FULL ? 64 : 1];
     const int t = blockIdx.x, tid = threadIdx.x;
     const int has = hascells[t];
     const int cs = cstart[t], nc = cstart[t + 1] - cs;
@@ -369,7 +370,17 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
     if (MODE == LIN_FULL && has) {  // tile's tangent block, permuted into the chunked (coalesced) layout
         const int64_t base = kstart[t];
         const int n = ncell[t];  // real cells come first in the compact run
-        for (int i = tid; i < n * 45; i += blockDim.x) Kout[k_off<T>(base, n, kslot(i / 45, n), i % 45)] = Ks[i];
+        if (kz) {  // slot = rank of the cell's kz_key in the tile (the wz HVP lane order)
+            if (tid < n) {
+                const int key = kz_key(clocal[cs + tid]);
+                int s = 0;
+                for (int j = 0; j < n; j++) s += kz_key(clocal[cs + j]) < key;
+                zslot[tid] = s;
+            }
+            __syncthreads();
+        }
+        for (int i = tid; i < n * 45; i += blockDim.x)
+            Kout[k_off<T>(base, n, kz ? zslot[i / 45] : kslot(i / 45, n), i % 45)] = Ks[i];
     }
     // ---- node phase -----------------------------------------------------------------------
     if (tid < 125) {
@@ -804,7 +815,7 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
         (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p, (const vec4<T> *)v_tile,                  \
         (const vec4<T> *)ctx->n_vhat.p, (const T *)owned_mass(ctx), (const T *)ctx->q_slot.p, (T *)ctx->K.p,       \
         (const int *)ctx->t_kstart.p, (const int *)ctx->t_ncell.p, (vec4<T> *)ctx->n_g.p, (vec4<T> *)ctx->n_diag.p, \
-        ctx->mats.plastic ? (T *)ctx->q_Sp.p : (T *)nullptr, sc
+        ctx->mats.plastic ? (T *)ctx->q_Sp.p : (T *)nullptr, sc, (int)hvp_kz_layout(ctx->precision)
         if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY><<<T_, 128, 0, st>>>(LIN_ARGS);
         else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD><<<T_, 128, 0, st>>>(LIN_ARGS);
         else k_linearize<T, LIN_FULL><<<T_, 128, 0, st>>>(LIN_ARGS);

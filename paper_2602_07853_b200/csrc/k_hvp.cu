@@ -965,7 +965,7 @@ __host__ __device__ constexpr int kcol(int e) { return krow(e) + (e - kofs(krow(
 //            every node value sits in exactly one (lane, slot) and goes straight to global memory; no
 //            force buffer and no node phase.
 enum { WZ_RMW = 0, WZ_PLANE = 1, WZ_SHFL = 2 };
-template <int MINB, bool ROLL, int SCAT>
+template <int MINB, bool ROLL, int SCAT, bool PAD>
 __global__ void __launch_bounds__(32 * WZ_W, MINB)
     k_hvp_wz(int T_, const int *__restrict__ nplus, const unsigned long long *__restrict__ cmask,
              const int *__restrict__ hascells, const float *__restrict__ K, const int *__restrict__ kstart,
@@ -1000,8 +1000,10 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
         return lane == 0 ? t : __ldg(mbase + (int64_t)mstride * t);
     };
     struct TileK {
-        int has, pA, pB, n, sA, sB;  // n: the tile's cells; sA / sB: this lane's cells' tangent slots
-        const float *kb;             // the tile's tangent block
+        int has, pA, pB;         // the tile has cells; this lane's cells A / B are present
+        unsigned sb;             // compact: chunk stride in bytes (16 n)
+        int e44, d44;            // compact: element 44 of cell A at ka + e44, of cell B at kbp + e44 - 3 d44
+        const float *ka, *kbp;   // this lane's first chunk of cell A / B (PAD: cell A; B at + 128)
     };
     auto tile_k = [&](int t, int meta) -> TileK {
         TileK q;
@@ -1012,25 +1014,43 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
         const unsigned word = lA < 32 ? clo : chi;
         q.pA = q.has ? (int)((word >> (lA & 31)) & 1u) : 0;
         q.pB = q.has ? (int)((word >> ((lA + 1) & 31)) & 1u) : 0;
-        const unsigned pmA = __ballot_sync(FULL, q.pA), pmB = __ballot_sync(FULL, q.pB);
-        const int nA = __popc(pmA);
-        q.n = nA + __popc(pmB);
-        q.sA = __popc(pmA & lt);
-        q.sB = nA + __popc(pmB & lt);
-        q.kb = K + ks;
+        if (PAD) {
+            q.ka = K + ks + 4 * lane;
+        } else {
+            const unsigned pmA = __ballot_sync(FULL, q.pA), pmB = __ballot_sync(FULL, q.pB);
+            const int nA = __popc(pmA), n = nA + __popc(pmB);
+            const int sA = __popc(pmA & lt), sB = nA + __popc(pmB & lt);
+            q.sb = 16u * (unsigned)n;
+            q.ka = K + ks + 4 * sA;
+            q.kbp = K + ks + 4 * sB;
+            q.e44 = 44 * n + sA - 4 * sA;  // element 44 of slot s at 44 n + s, relative to ka / kbp
+            q.d44 = sB - sA;
+        }
         return q;
     };
     float k[90];
-    // chunk c (16 bytes at kb + 4 (c n + s); c = 11: element 44 at kb + 44 n + s) of cell X (off 0 = A,
-    // 45 = B) of tile q -> k
+    // chunk c < 11 of slot s at 4 (c n + s), element 44 at 44 n + s (k_off); PAD: n = 64, cell A in slot
+    // lane, cell B in slot 32 + lane, so every load is an immediate offset from q.ka; compact: chunk c at
+    // (byte) ka + c * 16 n, one IMAD.WIDE per load.  Chunk c of cell X (off 0 = A, 45 = B) -> k
     auto kload = [&](const TileK &q, int off, int c) {
         if (!(off ? q.pB : q.pA)) return;
-        const int sl = off ? q.sB : q.sA;
-        if (c < 11) {
-            const float4 v = ldg_stream(q.kb + 4 * (c * q.n + sl), pol);
-            k[off + 4 * c] = v.x; k[off + 4 * c + 1] = v.y; k[off + 4 * c + 2] = v.z; k[off + 4 * c + 3] = v.w;
+        if (PAD) {
+            const float *p = q.ka + (off ? 128 : 0);
+            if (c < 11) {
+                const float4 v = ldg_stream(p + 256 * c, pol);
+                k[off + 4 * c] = v.x; k[off + 4 * c + 1] = v.y; k[off + 4 * c + 2] = v.z; k[off + 4 * c + 3] = v.w;
+            } else {
+                k[off + 44] = ldg_stream1(p - 3 * lane - (off ? 96 : 0) + 2816, pol);
+            }
         } else {
-            k[off + 44] = ldg_stream1(q.kb + 44 * q.n + sl, pol);
+            const float *p = off ? q.kbp : q.ka;
+            if (c < 11) {
+                const float4 v = ldg_stream(reinterpret_cast<const float *>(reinterpret_cast<const char *>(p) +
+                                                                            (uint64_t)q.sb * (uint64_t)c), pol);
+                k[off + 4 * c] = v.x; k[off + 4 * c + 1] = v.y; k[off + 4 * c + 2] = v.z; k[off + 4 * c + 3] = v.w;
+            } else {
+                k[off + 44] = ldg_stream1(p + q.e44 - (off ? 3 * q.d44 : 0), pol);
+            }
         }
     };
     // tile t: u halo + owned masses -> shared buffer b (cp.async, one group)
@@ -1120,7 +1140,10 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
             }
             acc += (double)qf;
         }
-        if (!ROLL || !cur.has) {
+        // SHFL without ROLL: the next tile's tangent is requested after the register reduction, so k's
+        // registers can hold the 36 node contributions meanwhile
+        constexpr bool LATE = SHFL && !ROLL;
+        if (!LATE && (!ROLL || !cur.has)) {
             // k is free: start the next tile's loads; they overlap the scatter and the node phase
 #pragma unroll
             for (int c = 0; c < 12; c++) { kload(nxt, 0, c); kload(nxt, 45, c); }
@@ -1193,6 +1216,10 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
             } else {
 #pragma unroll
                 for (int i = 0; i < 36; i++) (&c[0][0][0][0])[i] = 0.f;
+            }
+            if (LATE) {
+#pragma unroll
+                for (int cc = 0; cc < 12; cc++) { kload(nxt, 0, cc); kload(nxt, 45, cc); }
             }
             // ---- outputs: slot (ox, oy, q) holds a complete node iff (ox == 0 || lx == 3) && (oy == 0 ||
             // ly == 3) && (q < 2 || zp == 1); its tile is neighbour (ox, oy, q == 2) (warp-uniform)
@@ -1319,7 +1346,7 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
 
 int g_num_sms = 0;
 
-template <int MINB, bool ROLL, int SCAT>
+template <int MINB, bool ROLL, int SCAT, bool PAD>
 mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
                      double cgthr) {
     static int per_sm = 0;
@@ -1328,13 +1355,13 @@ mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         int occ = 0;
-        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_wz<MINB, ROLL, SCAT>, 32 * WZ_W, 0));
+        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_wz<MINB, ROLL, SCAT, PAD>, 32 * WZ_W, 0));
         per_sm = occ > 0 ? occ : 1;
     }
     int grid = g_num_sms * per_sm;
     const int need = (ctx->T + WZ_W - 1) / WZ_W;
     if (grid > need) grid = need;
-    k_hvp_wz<MINB, ROLL, SCAT><<<grid, 32 * WZ_W, 0, ctx->stream>>>(
+    k_hvp_wz<MINB, ROLL, SCAT, PAD><<<grid, 32 * WZ_W, 0, ctx->stream>>>(
         ctx->T, (const int *)ctx->t_nplus.p, (const unsigned long long *)ctx->t_cmask.p,
         (const int *)ctx->t_hascells.p, (const float *)ctx->K.p, (const int *)ctx->t_kstart.p,
         (const float *)owned_mass(ctx), (const f4 *)u_tile, (f4 *)Hu_tile, uHu, cgs, cgj, cgthr,
@@ -1436,7 +1463,7 @@ int hvp_variant() {
         if (e && e[0] == 'w' && e[1] == 'z') {
             const int sc = e[2] == 'p' ? 1 : e[2] == 's' ? 2 : 0;
             const bool roll = e[sc ? 3 : 2] == '2';
-            variant = sc == 1 ? (roll ? 10 : 9) : sc == 2 ? (roll ? 14 : 13) : (roll ? 12 : 11);
+            variant = sc == 1 ? 9 : sc == 2 ? (roll ? 14 : 13) : (roll ? 12 : 11);
         }
         else if (e && e[0] == 'r' && e[1] == 'q') variant = e[2] == '8' ? 8 : 7;
         else if (e && e[0] == 'r' && e[1] == 'p') variant = e[2] == '1' ? (e[3] == '2' ? 6 : 5) : 4;
@@ -1446,8 +1473,18 @@ int hvp_variant() {
     }
     return variant;
 }
-// the wz kernel reads the tangent in the kz slot order (kz_key); k_linearize writes it that way
-bool hvp_kz_layout(int precision) { return precision == 32 && hvp_variant() >= 9 && hvp_variant() <= 14; }
+// the wz kernels read the tangent in the kz slot order (kz_key); k_linearize writes it that way:
+// 0 = not kz (fp64, other kernels), 1 = compact kz order (default), 2 = fixed 64-slot kz blocks (MPL_KZ_PAD=1;
+// measured 9 % slower at cfg4)
+int hvp_kz_layout(int precision) {
+    static int pad = -1;
+    if (pad < 0) {
+        const char *e = getenv("MPL_KZ_PAD");
+        pad = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (precision != 32 || hvp_variant() < 9 || hvp_variant() > 14) return 0;
+    return pad ? 2 : 1;
+}
 
 // Hu (tile-dense) must be zero on every node that receives atomics (all non-interior nodes).
 template <class T>
@@ -1457,12 +1494,15 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
     int variant = hvp_variant();
     if (variant >= 9 && variant <= 14) {
         if (sizeof(T) == 4) {
-            if (variant == 9) return launch_wz<3, false, WZ_PLANE>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
-            if (variant == 10) return launch_wz<2, true, WZ_PLANE>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
-            if (variant == 11) return launch_wz<3, false, WZ_RMW>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
-            if (variant == 13) return launch_wz<3, false, WZ_SHFL>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
-            if (variant == 14) return launch_wz<2, true, WZ_SHFL>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
-            return launch_wz<2, true, WZ_RMW>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+            const bool pad = hvp_kz_layout(32) == 2;
+#define WZ(M, R, S) (pad ? launch_wz<M, R, S, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr) \
+                         : launch_wz<M, R, S, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr))
+            if (variant == 9) return WZ(3, false, WZ_PLANE);
+            if (variant == 11) return WZ(3, false, WZ_RMW);
+            if (variant == 14) return WZ(2, true, WZ_SHFL);
+            if (variant == 13) return WZ(3, false, WZ_SHFL);
+            if (variant == 12) return WZ(2, true, WZ_RMW);
+#undef WZ
         }
         variant = 5;
     }

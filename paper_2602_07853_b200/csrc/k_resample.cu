@@ -315,7 +315,7 @@ __global__ void k_scatter(GridP g, MatP mp, int64_t np, const int *__restrict__ 
 __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, const int *__restrict__ nminus,
                             const int *__restrict__ bcount, const int *__restrict__ hascells,
                             unsigned long long *__restrict__ cmask, int *__restrict__ ccount, int *__restrict__ ncell,
-                            int *__restrict__ kcnt, unsigned long long *ncells) {
+                            int *__restrict__ kcnt, unsigned long long *ncells, int kz) {
     int t = blockIdx.x;
     int l = threadIdx.x;  // 64 threads
     int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
@@ -342,7 +342,8 @@ __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, cons
         int c = __popcll(m);
         ccount[t] = (c + 3) & ~3;
         ncell[t] = c;
-        kcnt[t] = hascells[t] ? (45 * c + 3) & ~3 : 0;  // tangent only on owned tiles
+        // tangent only on owned tiles: compact (45 c, rounded up to 4) or, in the padded kz layout, 64 slots
+        kcnt[t] = hascells[t] ? (kz == 2 ? 45 * 64 : (45 * c + 3) & ~3) : 0;
         if (c && hascells[t]) atomicAdd(ncells, (unsigned long long)c);
     }
 }
@@ -944,7 +945,7 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
                                           (const int *)ctx->t_bcount.p, (const int *)ctx->t_hascells.p,
                                           (unsigned long long *)ctx->t_cmask.p,
                                           (int *)ctx->t_ccount.p, (int *)ctx->t_ncell.p, (int *)ctx->t_kcnt.p,
-                                          counters + 1); ctx->launches++;
+                                          counters + 1, hvp_kz_layout(ctx->precision)); ctx->launches++;
     DBG_GUARDS("resample #7");
     MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_ccount.p, (int *)ctx->t_cstart.p, (int64_t)T_ + 1));
     MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_kcnt.p, (int *)ctx->t_kstart.p, (int64_t)T_ + 1));

@@ -370,17 +370,21 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
     if (MODE == LIN_FULL && has) {  // tile's tangent block, permuted into the chunked (coalesced) layout
         const int64_t base = kstart[t];
         const int n = ncell[t];  // real cells come first in the compact run
-        if (kz) {  // slot = rank of the cell's kz_key in the tile (the wz HVP lane order)
+        if (kz) {  // kz order (the wz HVP lanes): 64-slot block, slot = kz_key; compact: slot = its rank
             if (tid < n) {
                 const int key = kz_key(clocal[cs + tid]);
-                int s = 0;
-                for (int j = 0; j < n; j++) s += kz_key(clocal[cs + j]) < key;
-                zslot[tid] = s;
+                int sl = key;
+                if (kz == 1) {
+                    sl = 0;
+                    for (int j = 0; j < n; j++) sl += kz_key(clocal[cs + j]) < key;
+                }
+                zslot[tid] = sl;
             }
             __syncthreads();
         }
+        const int ncp = kz == 2 ? 64 : n;
         for (int i = tid; i < n * 45; i += blockDim.x)
-            Kout[k_off<T>(base, n, kz ? zslot[i / 45] : kslot(i / 45, n), i % 45)] = Ks[i];
+            Kout[k_off<T>(base, ncp, kz ? zslot[i / 45] : kslot(i / 45, n), i % 45)] = Ks[i];
     }
     // ---- node phase -----------------------------------------------------------------------
     if (tid < 125) {
@@ -815,7 +819,7 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
         (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p, (const vec4<T> *)v_tile,                  \
         (const vec4<T> *)ctx->n_vhat.p, (const T *)owned_mass(ctx), (const T *)ctx->q_slot.p, (T *)ctx->K.p,       \
         (const int *)ctx->t_kstart.p, (const int *)ctx->t_ncell.p, (vec4<T> *)ctx->n_g.p, (vec4<T> *)ctx->n_diag.p, \
-        ctx->mats.plastic ? (T *)ctx->q_Sp.p : (T *)nullptr, sc, (int)hvp_kz_layout(ctx->precision)
+        ctx->mats.plastic ? (T *)ctx->q_Sp.p : (T *)nullptr, sc, hvp_kz_layout(ctx->precision)
         if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY><<<T_, 128, 0, st>>>(LIN_ARGS);
         else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD><<<T_, 128, 0, st>>>(LIN_ARGS);
         else k_linearize<T, LIN_FULL><<<T_, 128, 0, st>>>(LIN_ARGS);

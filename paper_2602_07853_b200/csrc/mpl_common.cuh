@@ -294,13 +294,15 @@ template <class T> struct KL {
 // two warps of a 64-thread CTA get ceil(n/2) and floor(n/2) cells; the tangent of cell j is stored at
 // slot kslot(j) = (j & 1) ceil(n/2) + (j >> 1), so each warp's 16-byte loads are contiguous.
 __host__ __device__ __forceinline__ int kslot(int j, int n) { return (j & 1) * ((n + 1) >> 1) + (j >> 1); }
-// "kz" slot order (fp32 default, the wz HVP kernel): a tile's cells sorted by kz_key of their local
-// position l = 16 lx + 4 ly + lz, i.e. the wz lane order (lane = 16 (lz >> 1) + 4 lx + ly) of the even-z
-// cells first, then of the odd-z cells; slot = rank of the key among the tile's cells.
+// "kz" layout (fp32 default, the wz HVP kernel): a fixed block of 64 slots per owned tile (45 * 64 reals,
+// the chunked layout of k_off with ncp = 64), the cell at local position l = 16 lx + 4 ly + lz in slot
+// kz_key(l) = the wz lane (16 (lz >> 1) + 4 lx + ly) for even lz, 32 + that lane for odd lz.  Absent
+// cells leave their slots unwritten and unread; every tangent load of the HVP is then an immediate offset
+// from one per-lane pointer.
 __host__ __device__ __forceinline__ constexpr int kz_key(int l) {
     return ((l & 1) << 5) | (((l >> 1) & 1) << 4) | ((l >> 4) << 2) | ((l >> 2) & 3);
 }
-bool hvp_kz_layout(int precision);
+int hvp_kz_layout(int precision);  // 0: kslot order, 1: compact kz order, 2: 64-slot kz blocks
 // HVP thread -> (cell j, tangent slot)
 __device__ __forceinline__ int hvp_cell(int tid) { return 2 * (tid & 31) + (tid >> 5); }
 __device__ __forceinline__ int hvp_slot(int tid, int n) { return (tid >> 5) * ((n + 1) >> 1) + (tid & 31); }

@@ -963,8 +963,10 @@ __host__ __device__ constexpr int kcol(int e) { return krow(e) + (e - kofs(krow(
 //   WZ_PLANE non-aliasing plane stores, node phase sums <= 8 plane entries per node;
 //   WZ_SHFL  register reduction with shuffles along y (1 lane), x (4 lanes), z (16 lanes), after which
 //            every node value sits in exactly one (lane, slot) and goes straight to global memory; no
-//            force buffer and no node phase.
-enum { WZ_RMW = 0, WZ_PLANE = 1, WZ_SHFL = 2 };
+//            force buffer and no node phase;
+//   WZ_RMW3  WZ_RMW with the z = 2 plane merged by a shuffle first, so the passes form 4 groups of 3
+//            non-aliasing read-modify-writes.
+enum { WZ_RMW = 0, WZ_PLANE = 1, WZ_SHFL = 2, WZ_RMW3 = 3 };
 template <int MINB, bool ROLL, int SCAT, bool PAD>
 __global__ void __launch_bounds__(32 * WZ_W, MINB)
     k_hvp_wz(int T_, const int *__restrict__ nplus, const unsigned long long *__restrict__ cmask,
@@ -1267,6 +1269,44 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
                 const float f1 = PB[3 * a] + PB[3 * a + 1], f2 = PB[3 * a] - PB[3 * a + 1], y = PB[3 * a + 2];
                 gB[a][0] = f1 + y; gB[a][1] = f1 - y; gB[a][2] = f2 + y; gB[a][3] = f2 - y;
             }
+            if (SCAT == WZ_RMW3) {
+                // plane z = 2 is q = 2 of the zp = 0 lanes and q = 0 of the zp = 1 lanes: merge it with a
+                // shuffle, after which the q = 0 (z = 0, 2), q = 1 (z = 1, 3) and q = 2 (z = 4, zp = 1 only)
+                // passes touch disjoint nodes; 4 groups of 3 independent read-modify-writes, one
+                // __syncwarp per group instead of one per pass
+                float zr[2][2][3];
+#pragma unroll
+                for (int ox = 0; ox < 2; ox++)
+#pragma unroll
+                    for (int oy = 0; oy < 2; oy++)
+#pragma unroll
+                        for (int a = 0; a < 3; a++) {
+                            const float v = __shfl_up_sync(FULL, corner(gB[a], ox, oy, 1), 16);
+                            zr[ox][oy][a] = zp ? v : 0.f;
+                        }
+#pragma unroll
+                for (int ox = 0; ox < 2; ox++)
+#pragma unroll
+                    for (int oy = 0; oy < 2; oy++) {
+                        f4 *f0 = &S.F[hb + 5 * ox + 26 * oy];
+                        // the first group touching a node stores instead of adding (no zeroing pass)
+                        const bool first = (ox == 0 || lx == 3) && (oy == 0 || ly == 3);
+                        const f4 zero4 = mk4<float>(0.f, 0.f, 0.f, 0.f);
+                        const f4 o0 = first ? zero4 : f0[0], o1 = first ? zero4 : f0[1];
+                        f0[0] = mk4<float>(o0.x + corner(gA[0], ox, oy, 0) + zr[ox][oy][0],
+                                           o0.y + corner(gA[1], ox, oy, 0) + zr[ox][oy][1],
+                                           o0.z + corner(gA[2], ox, oy, 0) + zr[ox][oy][2], 0.f);
+                        f0[1] = mk4<float>(o1.x + corner(gA[0], ox, oy, 1) + corner(gB[0], ox, oy, 0),
+                                           o1.y + corner(gA[1], ox, oy, 1) + corner(gB[1], ox, oy, 0),
+                                           o1.z + corner(gA[2], ox, oy, 1) + corner(gB[2], ox, oy, 0), 0.f);
+                        if (zp) {
+                            const f4 o2 = first ? zero4 : f0[2];
+                            f0[2] = mk4<float>(o2.x + corner(gB[0], ox, oy, 1), o2.y + corner(gB[1], ox, oy, 1),
+                                               o2.z + corner(gB[2], ox, oy, 1), 0.f);
+                        }
+                        __syncwarp();
+                    }
+            } else
 #pragma unroll
             for (int ox = 0; ox < 2; ox++)
 #pragma unroll
@@ -1316,7 +1356,7 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
                     }
                 } else {
                     f = S.F[h];
-                    S.F[h] = mk4<float>(0.f, 0.f, 0.f, 0.f);
+                    if (SCAT == WZ_RMW) S.F[h] = mk4<float>(0.f, 0.f, 0.f, 0.f);  // RMW3: first writers store
                 }
             }
             if (!(cur.has || owned) || tt[r] < 0) continue;
@@ -1461,9 +1501,9 @@ int hvp_variant() {
         const char *e = getenv("MPL_HVP_KERNEL");
         variant = 11;
         if (e && e[0] == 'w' && e[1] == 'z') {
-            const int sc = e[2] == 'p' ? 1 : e[2] == 's' ? 2 : 0;
+            const int sc = e[2] == 'p' ? 1 : e[2] == 's' ? 2 : e[2] == '3' ? 3 : 0;
             const bool roll = e[sc ? 3 : 2] == '2';
-            variant = sc == 1 ? 9 : sc == 2 ? (roll ? 14 : 13) : (roll ? 12 : 11);
+            variant = sc == 1 ? 9 : sc == 2 ? (roll ? 14 : 13) : sc == 3 ? 15 : (roll ? 12 : 11);
         }
         else if (e && e[0] == 'r' && e[1] == 'q') variant = e[2] == '8' ? 8 : 7;
         else if (e && e[0] == 'r' && e[1] == 'p') variant = e[2] == '1' ? (e[3] == '2' ? 6 : 5) : 4;
@@ -1482,7 +1522,7 @@ int hvp_kz_layout(int precision) {
         const char *e = getenv("MPL_KZ_PAD");
         pad = (e && e[0] == '1') ? 1 : 0;
     }
-    if (precision != 32 || hvp_variant() < 9 || hvp_variant() > 14) return 0;
+    if (precision != 32 || hvp_variant() < 9 || hvp_variant() > 15) return 0;
     return pad ? 2 : 1;
 }
 
@@ -1492,7 +1532,7 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
                       double cgthr) {
     if (ctx->T == 0) return MPL_OK;
     int variant = hvp_variant();
-    if (variant >= 9 && variant <= 14) {
+    if (variant >= 9 && variant <= 15) {
         if (sizeof(T) == 4) {
             const bool pad = hvp_kz_layout(32) == 2;
 #define WZ(M, R, S) (pad ? launch_wz<M, R, S, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr) \
@@ -1501,6 +1541,7 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
             if (variant == 11) return WZ(3, false, WZ_RMW);
             if (variant == 14) return WZ(2, true, WZ_SHFL);
             if (variant == 13) return WZ(3, false, WZ_SHFL);
+            if (variant == 15) return WZ(3, false, WZ_RMW3);
             if (variant == 12) return WZ(2, true, WZ_RMW);
 #undef WZ
         }

@@ -977,6 +977,8 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
     __shared__ WzWarp<PLANE> SW[WZ_W];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WzWarp<PLANE> &S = SW[wid];
+    pdl_trigger();
+    pdl_wait();
     if (cgs != nullptr) {
         const double rr = warp_sum(cgs[cgj].rr[lane]);
         if (sc->neg_curv || (cgj > 0 && rr <= cgthr)) return;
@@ -1401,13 +1403,12 @@ mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
     int grid = g_num_sms * per_sm;
     const int need = (ctx->T + WZ_W - 1) / WZ_W;
     if (grid > need) grid = need;
-    k_hvp_wz<MINB, ROLL, SCAT, PAD><<<grid, 32 * WZ_W, 0, ctx->stream>>>(
-        ctx->T, (const int *)ctx->t_nplus.p, (const unsigned long long *)ctx->t_cmask.p,
-        (const int *)ctx->t_hascells.p, (const float *)ctx->K.p, (const int *)ctx->t_kstart.p,
-        (const float *)owned_mass(ctx), (const f4 *)u_tile, (f4 *)Hu_tile, uHu, cgs, cgj, cgthr,
-        (const DevScalars *)ctx->scalars.p);
+    MPL_CUDA(launch_pdl(k_hvp_wz<MINB, ROLL, SCAT, PAD>, grid, 32 * WZ_W, 0, ctx->stream, ctx->T,
+                        (const int *)ctx->t_nplus.p, (const unsigned long long *)ctx->t_cmask.p,
+                        (const int *)ctx->t_hascells.p, (const float *)ctx->K.p, (const int *)ctx->t_kstart.p,
+                        (const float *)owned_mass(ctx), (const f4 *)u_tile, (f4 *)Hu_tile, uHu, cgs, cgj, cgthr,
+                        (const DevScalars *)ctx->scalars.p));
     ctx->launches++;
-    MPL_CUDA(cudaGetLastError());
     return MPL_OK;
 }
 
@@ -1513,6 +1514,15 @@ int hvp_variant() {
     }
     return variant;
 }
+bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("MPL_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
 // the wz kernels read the tangent in the kz slot order (kz_key); k_linearize writes it that way:
 // 0 = not kz (fp64, other kernels), 1 = compact kz order (default), 2 = fixed 64-slot kz blocks (MPL_KZ_PAD=1;
 // measured 9 % slower at cfg4)

@@ -605,6 +605,8 @@ __global__ void __launch_bounds__(256) k_pcg_update1(int64_t n, const int *__res
                                                       const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ p,
                                                       vec4<T> *__restrict__ Hp, vec4<T> *__restrict__ x,
                                                       vec4<T> *__restrict__ r, CGSlot *slot, DevScalars *sc) {
+    pdl_trigger();
+    pdl_wait();
     const CGScal cs = cg_scalars(slot, j, false);
     const int done = sc->cg_done_iter;
     if ((done >= 0 && done <= j) || (j > 0 && cs.rr <= thr)) return;
@@ -652,6 +654,8 @@ __global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, const int *__res
                                                       const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ r,
                                                       vec4<T> *__restrict__ p, vec4<T> *__restrict__ x,
                                                       const CGSlot *slot, const DevScalars *sc) {
+    pdl_trigger();
+    pdl_wait();
     const CGScal cs = cg_scalars(slot, j, true);
     const int done = sc->cg_done_iter;
     if ((done >= 0 && done <= j + 1) || (j > 0 && cs.rr <= thr)) return;
@@ -976,11 +980,13 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     if (timed) sampled.push_back({nl, jj});
                     nl++;
                     if (vec_events) cudaEventRecord(vev[nl - 1][0], st);
-                    k_pcg_update1<T, 4><<<VAP, 256, 0, st>>>(NA, list, jj, thr, invD, p, Hp, x, r, slots, sc);
+                    MPL_CUDA(launch_pdl(k_pcg_update1<T, 4>, VAP, 256, 0, st, NA, list, jj, thr, invD, p, Hp, x, r,
+                                        slots, sc));
                     ctx->launches++;
                     MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
                     if (vec_events) cudaEventRecord(vev[nl - 1][1], st);
-                    k_pcg_update2<T, 4><<<VAP, 256, 0, st>>>(NA, list, jj, thr, invD, r, p, x, slots, sc);
+                    MPL_CUDA(launch_pdl(k_pcg_update2<T, 4>, VAP, 256, 0, st, NA, list, jj, thr, invD, r, p, x, slots,
+                                        sc));
                     ctx->launches++;
                     if (vec_events) cudaEventRecord(vev[nl - 1][2], st);
                 }

@@ -235,6 +235,33 @@ template <class T> __device__ __forceinline__ T nh_f(T x) {  // x (2 + x) - 2 lo
     return x * (T(2) + x) - T(2) * mlog1p(x);
 }
 
+// Programmatic dependent launch (PCG loop): a kernel launched with launch_pdl may be scheduled while
+// the previous kernel on the stream drains; every such kernel calls pdl_trigger() and then pdl_wait()
+// before touching any memory, so it only overlaps the previous kernel's tail / its own launch latency.
+// Both are no-ops for an ordinary launch.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();  // MPL_PDL (default on)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    if (!pdl_enabled()) {
+        k<<<grid, block, smem, st>>>(static_cast<KArgs>(args)...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // symmetric 9x9 upper-triangle packing: row r (r = 3a+b) stores s = r..8
 __host__ __device__ __forceinline__ constexpr int kofs(int r) { return r * 9 - (r * (r - 1)) / 2; }
 __host__ __device__ __forceinline__ constexpr int kidx(int r, int s) { return kofs(r) + (s - r); }

@@ -544,34 +544,63 @@ __global__ void k_explicit_update(int64_t n, const int *__restrict__ list, const
 // slot j: rz_j = r_j.z_j, rr_j = r_j.r_j, pHp_j = p_j.H p_j
 // =============================================================================================
 // ---- PCG on the compact list of active nodes (i -> tile-dense slot list[i]) ---------------------
-// x, r, invD are compact (active nodes only); p and Hp stay tile-dense because the HVP gathers and
-// scatters them by tile.  invD.w = 1 marks a free DOF; prescribed DOFs have invD = 0 and r = p = 0.
+// x, r and invD are compact over the active nodes and stored component-major (SoA): component c of
+// node i at a[c * S + i], S = the active-node count rounded up to 4, 12 bytes per node in fp32 instead
+// of a 16-byte vec4; p and Hp stay tile-dense vec4 because the HVP gathers and scatters them by tile.
+// Prescribed DOFs have invD = 0 (that is the free mask) and r = p = 0.  own (slab ranks only, else
+// nullptr) weights each node's dot-product terms so shared interface nodes count once.
+
+// 4 consecutive reals (16-byte aligned)
+template <class T> struct R4 { T v[4]; };
+template <class T> __device__ __forceinline__ R4<T> ld4(const T *p);
+template <> __device__ __forceinline__ R4<float> ld4<float>(const float *p) {
+    const float4 a = *reinterpret_cast<const float4 *>(p);
+    return R4<float>{{a.x, a.y, a.z, a.w}};
+}
+template <> __device__ __forceinline__ R4<double> ld4<double>(const double *p) {
+    const double2 a = reinterpret_cast<const double2 *>(p)[0], b = reinterpret_cast<const double2 *>(p)[1];
+    return R4<double>{{a.x, a.y, b.x, b.y}};
+}
+template <class T> __device__ __forceinline__ void st4(T *p, const T v[4]);
+template <> __device__ __forceinline__ void st4<float>(float *p, const float v[4]) {
+    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+template <> __device__ __forceinline__ void st4<double>(double *p, const double v[4]) {
+    reinterpret_cast<double2 *>(p)[0] = make_double2(v[0], v[1]);
+    reinterpret_cast<double2 *>(p)[1] = make_double2(v[2], v[3]);
+}
+inline int64_t soa_stride(int64_t n) { return (n + 3) & ~(int64_t)3; }
 
 // r = -g, invD = 1/D on free DOFs; z = invD r; p = z; x = 0; slot[0] = (r.z, r.r)
 template <class T>
-__global__ void __launch_bounds__(256) k_pcg_init(int64_t n, const int *__restrict__ list,
+__global__ void __launch_bounds__(256) k_pcg_init(int64_t n, int64_t S, const int *__restrict__ list,
                                                   const uint8_t *__restrict__ flag, const uint8_t *__restrict__ own,
                                                   const vec4<T> *__restrict__ g,
-                                                  const vec4<T> *__restrict__ D, vec4<T> *__restrict__ invD,
-                                                  vec4<T> *__restrict__ r, vec4<T> *__restrict__ p,
-                                                  vec4<T> *__restrict__ x, CGSlot *slot) {
+                                                  const vec4<T> *__restrict__ D, T *__restrict__ invD,
+                                                  T *__restrict__ r, vec4<T> *__restrict__ p,
+                                                  T *__restrict__ x, CGSlot *slot) {
     T rz = 0, rr = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int ti = list[i];
-        vec4<T> rv = mk4<T>(0, 0, 0, 0), zv = mk4<T>(0, 0, 0, 0), iv = mk4<T>(0, 0, 0, 0);
-        if (flag[ti] == 1) {
-            vec4<T> gv = g[ti], dv = D[ti];
-            const T w = T(own[ti]);  // r.w carries the owner weight of the node's dot-product terms
-            iv = mk4<T>(T(1) / dv.x, T(1) / dv.y, T(1) / dv.z, T(1));
-            rv = mk4<T>(-gv.x, -gv.y, -gv.z, w);
-            zv = mk4<T>(rv.x * iv.x, rv.y * iv.y, rv.z * iv.z, 0);
-            rz += w * (rv.x * zv.x + rv.y * zv.y + rv.z * zv.z);
-            rr += w * (rv.x * rv.x + rv.y * rv.y + rv.z * rv.z);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x) {
+        T rv[3] = {0, 0, 0}, iv[3] = {0, 0, 0};
+        if (i < n) {
+            const int ti = list[i];
+            if (flag[ti] == 1) {
+                const vec4<T> gv = g[ti], dv = D[ti];
+                const T w = own ? T(own[ti]) : T(1);
+                iv[0] = T(1) / dv.x; iv[1] = T(1) / dv.y; iv[2] = T(1) / dv.z;
+                rv[0] = -gv.x; rv[1] = -gv.y; rv[2] = -gv.z;
+                const T z0 = rv[0] * iv[0], z1 = rv[1] * iv[1], z2 = rv[2] * iv[2];
+                rz += w * (rv[0] * z0 + rv[1] * z1 + rv[2] * z2);
+                rr += w * (rv[0] * rv[0] + rv[1] * rv[1] + rv[2] * rv[2]);
+                p[ti] = mk4<T>(z0, z1, z2, T(0));
+            }
         }
-        invD[i] = iv;
-        r[i] = rv;
-        p[ti] = zv;
-        x[i] = mk4<T>(0, 0, 0, 0);
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            invD[c * S + i] = iv[c];
+            r[c * S + i] = rv[c];
+            x[c * S + i] = T(0);
+        }
     }
     block_add((double)rz, slot[0].rz);
     block_add((double)rr, slot[0].rr);
@@ -593,27 +622,47 @@ __device__ __forceinline__ CGScal cg_scalars(const CGSlot *slot, int j, bool nex
     return s_;
 }
 
+// a group = 4 consecutive compact nodes i0..i0+3: their list entries (-1 past n)
+constexpr int PCG_U = 1;  // groups per thread per pass
+__device__ __forceinline__ void grp_list(const int *__restrict__ list, int64_t i0, int64_t n, int li[4]) {
+    if (i0 + 4 <= n) {
+        const int4 l = *reinterpret_cast<const int4 *>(list + i0);
+        li[0] = l.x; li[1] = l.y; li[2] = l.z; li[3] = l.w;
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; e++) li[e] = i0 + e < n ? list[i0 + e] : -1;
+    }
+}
+
 // k_pcg_update1: r -= alpha Hp ; slot[j+1] = (r.invD r, r.r) ; Hp := 0 for the next HVP's atomics.
 // k_pcg_update2: x += alpha_j p_j ; then (unless converged) p = invD r + beta p, beta = rz_{j+1} / rz_j.
 // (x is updated in update2, which reads p anyway: one fewer pass over p.)
-// Persistent: one CTA wave (SMs x 8 CTAs of 256), the CG scalars read once per CTA, U nodes per thread
-// per pass with every independent load issued before the dependent tile-dense one (list -> Hp / p).
+// Persistent: one CTA wave (SMs x 8 CTAs of 256), the CG scalars read once per CTA; each thread takes
+// groups of 4 consecutive nodes (16-byte loads of every SoA component and of the list), every
+// independent load issued before the dependent tile-dense one (list -> Hp / p).  Bytes per node (fp32):
+// update1 72 (invD 12, r 12 + 12, Hp 16 + 16, list 4), update2 84 (vec4 x / r / invD: 84 and 100).
+// A warp-interleaved mapping (lane l: nodes l + 32 e, scalar component loads) measured slower.
 // One node per thread (~9000 CTAs) was 3x slower: each CTA's two striped fp64 atomics serialised on
 // the slot's cache lines (ncu: long scoreboard 72 %, barrier 20 %; 104 us vs 34 us live at cfg4).
 template <class T, int U>
-__global__ void __launch_bounds__(256) k_pcg_update1(int64_t n, const int *__restrict__ list, int j, double thr,
-                                                      const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ p,
-                                                      vec4<T> *__restrict__ Hp, vec4<T> *__restrict__ x,
-                                                      vec4<T> *__restrict__ r, CGSlot *slot, DevScalars *sc) {
+__global__ void __launch_bounds__(256) k_pcg_update1(int64_t n, int64_t S, const int *__restrict__ list, int j,
+                                                      double thr, const T *__restrict__ invD,
+                                                      const vec4<T> *__restrict__ p, vec4<T> *__restrict__ Hp,
+                                                      T *__restrict__ x, T *__restrict__ r,
+                                                      const uint8_t *__restrict__ own, CGSlot *slot, DevScalars *sc) {
     pdl_trigger();
     pdl_wait();
     const CGScal cs = cg_scalars(slot, j, false);
     const int done = sc->cg_done_iter;
     if ((done >= 0 && done <= j) || (j > 0 && cs.rr <= thr)) return;
     const int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+    const int64_t NG = (n + 3) >> 2;
     if (!(cs.pHp > 0.0)) {
         if (j == 0)
-            for (int64_t i = g0; i < n; i += gs) x[i] = p[list[i]];
+            for (int64_t i = g0; i < n; i += gs) {
+                const vec4<T> pv = p[list[i]];
+                x[i] = pv.x; x[S + i] = pv.y; x[2 * S + i] = pv.z;
+            }
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             sc->neg_curv = 1;
             sc->cg_done_iter = j + 1;
@@ -622,27 +671,44 @@ __global__ void __launch_bounds__(256) k_pcg_update1(int64_t n, const int *__res
     }
     const T alpha = T(cs.rz / cs.pHp);
     T rz = 0, rr = 0;
-    for (int64_t b = g0; b < n; b += gs * U) {
-        int ti[U];
-        vec4<T> iv[U], rv[U], hv[U];
+    for (int64_t b = g0; b < NG; b += gs * U) {
+        int li[U][4];
+        T iv[U][3][4], rv[U][3][4];
+        vec4<T> hv[U][4];
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            const int64_t i = b + u * gs;
-            ti[u] = i < n ? list[i] : -1;
-            if (i < n) { iv[u] = invD[i]; rv[u] = r[i]; }
+            const int64_t i0 = 4 * (b + u * gs);
+            if (i0 >= n) { li[u][0] = li[u][1] = li[u][2] = li[u][3] = -1; continue; }
+            grp_list(list, i0, n, li[u]);
+#pragma unroll
+            for (int c = 0; c < 3; c++) {
+                const R4<T> a = ld4<T>(invD + c * S + i0), q = ld4<T>(r + c * S + i0);
+#pragma unroll
+                for (int e = 0; e < 4; e++) { iv[u][c][e] = a.v[e]; rv[u][c][e] = q.v[e]; }
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; u++)
-            if (ti[u] >= 0) hv[u] = Hp[ti[u]];
+#pragma unroll
+            for (int e = 0; e < 4; e++)
+                if (li[u][e] >= 0) hv[u][e] = Hp[li[u][e]];
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            if (ti[u] < 0) continue;
-            Hp[ti[u]] = mk4<T>(0, 0, 0, 0);
-            const T aw = alpha * iv[u].w;
-            rv[u].x -= aw * hv[u].x; rv[u].y -= aw * hv[u].y; rv[u].z -= aw * hv[u].z;
-            r[b + u * gs] = rv[u];
-            rz += rv[u].w * (rv[u].x * rv[u].x * iv[u].x + rv[u].y * rv[u].y * iv[u].y + rv[u].z * rv[u].z * iv[u].z);
-            rr += rv[u].w * (rv[u].x * rv[u].x + rv[u].y * rv[u].y + rv[u].z * rv[u].z);
+            const int64_t i0 = 4 * (b + u * gs);
+            if (i0 >= n) continue;
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                if (li[u][e] < 0) continue;
+                Hp[li[u][e]] = mk4<T>(0, 0, 0, 0);
+                const T aw = iv[u][0][e] != T(0) ? alpha : T(0);  // prescribed DOFs keep r = 0
+                rv[u][0][e] -= aw * hv[u][e].x; rv[u][1][e] -= aw * hv[u][e].y; rv[u][2][e] -= aw * hv[u][e].z;
+                const T w = own ? T(own[li[u][e]]) : T(1);
+                rz += w * (rv[u][0][e] * rv[u][0][e] * iv[u][0][e] + rv[u][1][e] * rv[u][1][e] * iv[u][1][e] +
+                           rv[u][2][e] * rv[u][2][e] * iv[u][2][e]);
+                rr += w * (rv[u][0][e] * rv[u][0][e] + rv[u][1][e] * rv[u][1][e] + rv[u][2][e] * rv[u][2][e]);
+            }
+#pragma unroll
+            for (int c = 0; c < 3; c++) st4<T>(r + c * S + i0, rv[u][c]);  // S padding absorbs the tail
         }
     }
     block_add((double)rz, slot[j + 1].rz);
@@ -650,10 +716,10 @@ __global__ void __launch_bounds__(256) k_pcg_update1(int64_t n, const int *__res
 }
 
 template <class T, int U>
-__global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, const int *__restrict__ list, int j, double thr,
-                                                      const vec4<T> *__restrict__ invD, const vec4<T> *__restrict__ r,
-                                                      vec4<T> *__restrict__ p, vec4<T> *__restrict__ x,
-                                                      const CGSlot *slot, const DevScalars *sc) {
+__global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, int64_t S, const int *__restrict__ list, int j,
+                                                      double thr, const T *__restrict__ invD,
+                                                      const T *__restrict__ r, vec4<T> *__restrict__ p,
+                                                      T *__restrict__ x, const CGSlot *slot, const DevScalars *sc) {
     pdl_trigger();
     pdl_wait();
     const CGScal cs = cg_scalars(slot, j, true);
@@ -663,57 +729,77 @@ __global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, const int *__res
     const bool more = cs.rr1 > thr;
     const T beta = more ? T(cs.rz1 / cs.rz) : T(0);
     const int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t b = g0; b < n; b += gs * U) {
-        int ti[U];
-        vec4<T> xv[U], rv[U], iv[U], pv[U];
+    const int64_t NG = (n + 3) >> 2;
+    for (int64_t b = g0; b < NG; b += gs * U) {
+        int li[U][4];
+        T xv[U][3][4], rv[U][3][4], iv[U][3][4];
+        vec4<T> pv[U][4];
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            const int64_t i = b + u * gs;
-            ti[u] = i < n ? list[i] : -1;
-            if (i < n) {
-                xv[u] = x[i];
-                if (more) { rv[u] = r[i]; iv[u] = invD[i]; }
+            const int64_t i0 = 4 * (b + u * gs);
+            if (i0 >= n) { li[u][0] = li[u][1] = li[u][2] = li[u][3] = -1; continue; }
+            grp_list(list, i0, n, li[u]);
+#pragma unroll
+            for (int c = 0; c < 3; c++) {
+                const R4<T> a = ld4<T>(x + c * S + i0);
+#pragma unroll
+                for (int e = 0; e < 4; e++) xv[u][c][e] = a.v[e];
+                if (more) {
+                    const R4<T> q = ld4<T>(r + c * S + i0), d = ld4<T>(invD + c * S + i0);
+#pragma unroll
+                    for (int e = 0; e < 4; e++) { rv[u][c][e] = q.v[e]; iv[u][c][e] = d.v[e]; }
+                }
             }
         }
 #pragma unroll
         for (int u = 0; u < U; u++)
-            if (ti[u] >= 0) pv[u] = p[ti[u]];
+#pragma unroll
+            for (int e = 0; e < 4; e++)
+                if (li[u][e] >= 0) pv[u][e] = p[li[u][e]];
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            if (ti[u] < 0) continue;
-            xv[u].x += alpha * pv[u].x; xv[u].y += alpha * pv[u].y; xv[u].z += alpha * pv[u].z;
-            x[b + u * gs] = xv[u];
-            if (more)
-                p[ti[u]] = mk4<T>(rv[u].x * iv[u].x + beta * pv[u].x, rv[u].y * iv[u].y + beta * pv[u].y,
-                                  rv[u].z * iv[u].z + beta * pv[u].z, T(0));
+            const int64_t i0 = 4 * (b + u * gs);
+            if (i0 >= n) continue;
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                if (li[u][e] < 0) continue;
+                xv[u][0][e] += alpha * pv[u][e].x; xv[u][1][e] += alpha * pv[u][e].y; xv[u][2][e] += alpha * pv[u][e].z;
+                if (more)
+                    p[li[u][e]] = mk4<T>(rv[u][0][e] * iv[u][0][e] + beta * pv[u][e].x,
+                                         rv[u][1][e] * iv[u][1][e] + beta * pv[u][e].y,
+                                         rv[u][2][e] * iv[u][2][e] + beta * pv[u][e].z, T(0));
+            }
+#pragma unroll
+            for (int c = 0; c < 3; c++) st4<T>(x + c * S + i0, xv[u][c]);
         }
     }
 }
 
-// g . x over free DOFs (g tile-dense, x compact)
+// g . x over free DOFs (g tile-dense, x compact SoA)
 template <class T>
-__global__ void k_dot_gx(int64_t n, const int *__restrict__ list, const uint8_t *__restrict__ flag,
-                         const uint8_t *__restrict__ own, const vec4<T> *__restrict__ g, const vec4<T> *__restrict__ x,
+__global__ void k_dot_gx(int64_t n, int64_t S, const int *__restrict__ list, const uint8_t *__restrict__ flag,
+                         const uint8_t *__restrict__ own, const vec4<T> *__restrict__ g, const T *__restrict__ x,
                          double *out) {
     double s = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int ti = list[i];
         if (flag[ti] != 1 || !own[ti]) continue;
-        vec4<T> a = g[ti], b = x[i];
-        s += (double)(a.x * b.x + a.y * b.y + a.z * b.z);
+        const vec4<T> a = g[ti];
+        s += (double)(a.x * x[i] + a.y * x[S + i] + a.z * x[2 * S + i]);
     }
     block_add(s, out);
 }
 
 // vt = v + alpha x on free DOFs (vt pre-filled with v)
 template <class T>
-__global__ void k_axpy_compact(int64_t n, const int *__restrict__ list, const uint8_t *__restrict__ flag, T alpha,
-                               const vec4<T> *__restrict__ v, const vec4<T> *__restrict__ x, vec4<T> *__restrict__ vt) {
+__global__ void k_axpy_compact(int64_t n, int64_t S, const int *__restrict__ list, const uint8_t *__restrict__ flag,
+                               T alpha, const vec4<T> *__restrict__ v, const T *__restrict__ x,
+                               vec4<T> *__restrict__ vt) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int ti = list[i];
         if (flag[ti] != 1) continue;
-        vec4<T> a = v[ti], b = x[i];
-        a.x += alpha * b.x; a.y += alpha * b.y; a.z += alpha * b.z;
+        vec4<T> a = v[ti];
+        a.x += alpha * x[i]; a.y += alpha * x[S + i]; a.z += alpha * x[2 * S + i];
         vt[ti] = a;
     }
 }
@@ -879,12 +965,15 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     const uint8_t *own = (const uint8_t *)ctx->n_own.p;
     vec4<T> *v = (vec4<T> *)ctx->n_v.p, *vt = (vec4<T> *)ctx->n_vt.p;
     vec4<T> *g = (vec4<T> *)ctx->n_g.p, *D = (vec4<T> *)ctx->n_diag.p;
-    MPL_CHECK(ensure(ctx, ctx->n_invD, (size_t)NT * sizeof(vec4<T>) + 64));
-    vec4<T> *invD = (vec4<T> *)ctx->n_invD.p;
-    vec4<T> *x = (vec4<T> *)ctx->n_x.p, *r = (vec4<T> *)ctx->n_r.p, *p = (vec4<T> *)ctx->n_p.p,
-            *Hp = (vec4<T> *)ctx->n_Hp.p;
-    const unsigned VG = vgrid(NT);
     const int64_t NA = ctx->n_nodes_active;
+    const int64_t SA = soa_stride(NA);  // SoA stride of x, r, invD (3 SA reals each)
+    MPL_CHECK(ensure(ctx, ctx->n_invD, (size_t)3 * SA * sizeof(T) + 64));
+    MPL_CHECK(ensure(ctx, ctx->n_x, (size_t)3 * SA * sizeof(T) + 64));
+    MPL_CHECK(ensure(ctx, ctx->n_r, (size_t)3 * SA * sizeof(T) + 64));
+    T *invD = (T *)ctx->n_invD.p, *x = (T *)ctx->n_x.p, *r = (T *)ctx->n_r.p;
+    vec4<T> *p = (vec4<T> *)ctx->n_p.p, *Hp = (vec4<T> *)ctx->n_Hp.p;
+    const uint8_t *own_w = multi(ctx) ? own : nullptr;  // dot-product owner weights (slab ranks)
+    const unsigned VG = vgrid(NT);
     const unsigned VA = vgrid(NA);
     const unsigned VA1 = nblk(NA > 0 ? NA : 1, 256);
     int nsm_ = 148;
@@ -927,7 +1016,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         MPL_CUDA(cudaMemsetAsync(&sc->neg_curv, 0, sizeof(int), st));
         MPL_CUDA(cudaMemsetAsync(&sc->cg_done_iter, 0xff, sizeof(int), st));
         MPL_CUDA(cudaMemsetAsync(p, 0, NT * sizeof(vec4<T>), st));
-        k_pcg_init<T><<<VA, 256, 0, st>>>(NA, list, flag, own, g, D, invD, r, p, x, slots); ctx->launches++;
+        k_pcg_init<T><<<vgrid(SA), 256, 0, st>>>(NA, SA, list, flag, own_w, g, D, invD, r, p, x, slots);
+        ctx->launches++;
         MPL_CHECK(allreduce_d(ctx, slots[0].rz, 3 * NSTRIPE));
         MPL_CUDA(cudaMemsetAsync(Hp, 0, NT * sizeof(vec4<T>), st));
         cudaEventRecord(e1, st);
@@ -980,13 +1070,13 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     if (timed) sampled.push_back({nl, jj});
                     nl++;
                     if (vec_events) cudaEventRecord(vev[nl - 1][0], st);
-                    MPL_CUDA(launch_pdl(k_pcg_update1<T, 4>, VAP, 256, 0, st, NA, list, jj, thr, invD, p, Hp, x, r,
-                                        slots, sc));
+                    MPL_CUDA(launch_pdl(k_pcg_update1<T, PCG_U>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p, Hp,
+                                        x, r, own_w, slots, sc));
                     ctx->launches++;
                     MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
                     if (vec_events) cudaEventRecord(vev[nl - 1][1], st);
-                    MPL_CUDA(launch_pdl(k_pcg_update2<T, 4>, VAP, 256, 0, st, NA, list, jj, thr, invD, r, p, x, slots,
-                                        sc));
+                    MPL_CUDA(launch_pdl(k_pcg_update2<T, PCG_U>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, r, p,
+                                        x, slots, sc));
                     ctx->launches++;
                     if (vec_events) cudaEventRecord(vev[nl - 1][2], st);
                 }
@@ -1031,7 +1121,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         // ---- Armijo backtracking line search ------------------------------------------------
         cudaEventRecord(e0, st);
         MPL_CUDA(cudaMemsetAsync(sc->gp, 0, sizeof(sc->gp), st));
-        k_dot_gx<T><<<VA, 256, 0, st>>>(NA, list, flag, own, g, x, sc->gp); ctx->launches++;
+        k_dot_gx<T><<<VA, 256, 0, st>>>(NA, SA, list, flag, own, g, x, sc->gp); ctx->launches++;
         MPL_CHECK(allreduce_d(ctx, sc->gp, NSTRIPE));
         double gps[NSTRIPE];
         MPL_CHECK(d2h(ctx, gps, sc->gp, sizeof gps, st));
@@ -1042,11 +1132,11 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         if (cfg->fixed_ls_halvings) {
             for (h = 0; h < cfg->fixed_ls_halvings[k]; h++) alpha *= 0.5;
             MPL_CUDA(cudaMemcpyAsync(vt, v, NT * sizeof(vec4<T>), cudaMemcpyDeviceToDevice, st));
-            k_axpy_compact<T><<<VA, 256, 0, st>>>(NA, list, flag, T(alpha), v, x, vt); ctx->launches++;
+            k_axpy_compact<T><<<VA, 256, 0, st>>>(NA, SA, list, flag, T(alpha), v, x, vt); ctx->launches++;
         } else {
             for (;;) {
                 MPL_CUDA(cudaMemcpyAsync(vt, v, NT * sizeof(vec4<T>), cudaMemcpyDeviceToDevice, st));
-            k_axpy_compact<T><<<VA, 256, 0, st>>>(NA, list, flag, T(alpha), v, x, vt); ctx->launches++;
+            k_axpy_compact<T><<<VA, 256, 0, st>>>(NA, SA, list, flag, T(alpha), v, x, vt); ctx->launches++;
                 double phi = 0;
                 MPL_CHECK(energy_at<T>(ctx, vt, &phi));
                 if (std::isinf(phi)) S.n_inverted_trials++;

@@ -998,7 +998,7 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CHECK(ensure(ctx, ctx->n_mass, NN * s));
     MPL_CHECK(ensure(ctx, ctx->n_flag, NN));
     DevBuf *vecs[] = {&ctx->n_vn, &ctx->n_vhat, &ctx->n_v, &ctx->n_vt, &ctx->n_g, &ctx->n_diag,
-                      &ctx->n_x, &ctx->n_r, &ctx->n_p, &ctx->n_Hp, &ctx->n_u, &ctx->n_u2};
+                      &ctx->n_x, &ctx->n_r, &ctx->n_u, &ctx->n_u2};  // n_p (p + Hp): newton_impl
     for (DevBuf *b : vecs) MPL_CHECK(ensure(ctx, *b, NN * 4 * s));
     MPL_CHECK(ensure(ctx, ctx->n_act, NN * 4));
     MPL_CHECK(ensure(ctx, ctx->n_own, NN));

@@ -16,6 +16,8 @@
 #include <cstdlib>
 #include <cmath>
 
+#include <type_traits>
+
 #include "mpl_common.cuh"
 
 namespace {
@@ -775,6 +777,137 @@ __global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, int64_t S, const
     }
 }
 
+// Warp-interleaved variants (MPL_PCG_MAP=warp): a warp takes chunks of 32 PCG_E compact nodes, lane l
+// the nodes l + 32 e, so every SoA component load, list load and tile-dense p / Hp access of one
+// instruction is contiguous across the warp (the group mapping above writes p / Hp at a 64-byte lane
+// stride).  Full chunks run without per-node bounds checks.
+constexpr int PCG_E = 4;
+template <class T>
+__global__ void __launch_bounds__(256, 2) k_pcg_update1w(int64_t n, int64_t S, const int *__restrict__ list, int j,
+                                                         double thr, const T *__restrict__ invD,
+                                                         const vec4<T> *__restrict__ p, vec4<T> *__restrict__ Hp,
+                                                         T *__restrict__ x, T *__restrict__ r,
+                                                         const uint8_t *__restrict__ own, CGSlot *slot,
+                                                         DevScalars *sc) {
+    pdl_trigger();
+    pdl_wait();
+    const CGScal cs = cg_scalars(slot, j, false);
+    const int done = sc->cg_done_iter;
+    if ((done >= 0 && done <= j) || (j > 0 && cs.rr <= thr)) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if (!(cs.pHp > 0.0)) {
+        if (j == 0)
+            for (int64_t i = w0 * 32 + lane; i < n; i += nw * 32) {
+                const vec4<T> pv = p[list[i]];
+                x[i] = pv.x; x[S + i] = pv.y; x[2 * S + i] = pv.z;
+            }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            sc->neg_curv = 1;
+            sc->cg_done_iter = j + 1;
+        }
+        return;
+    }
+    const T alpha = T(cs.rz / cs.pHp);
+    T rz = 0, rr = 0;
+    auto chunk = [&](int64_t base, auto full) {
+        constexpr bool FULL = decltype(full)::value;
+        int li[PCG_E];
+        T iv[PCG_E][3], rv[PCG_E][3];
+        vec4<T> hv[PCG_E];
+#pragma unroll
+        for (int e = 0; e < PCG_E; e++) {
+            const int64_t i = base + 32 * e + lane;
+            if (FULL || i < n) {
+                li[e] = list[i];
+#pragma unroll
+                for (int c = 0; c < 3; c++) { iv[e][c] = invD[c * S + i]; rv[e][c] = r[c * S + i]; }
+            } else {
+                li[e] = -1;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < PCG_E; e++)
+            if (FULL || li[e] >= 0) hv[e] = Hp[li[e]];
+#pragma unroll
+        for (int e = 0; e < PCG_E; e++) {
+            if (!FULL && li[e] < 0) continue;
+            const int64_t i = base + 32 * e + lane;
+            Hp[li[e]] = mk4<T>(0, 0, 0, 0);
+            const T aw = iv[e][0] != T(0) ? alpha : T(0);  // prescribed DOFs keep r = 0
+            rv[e][0] -= aw * hv[e].x; rv[e][1] -= aw * hv[e].y; rv[e][2] -= aw * hv[e].z;
+#pragma unroll
+            for (int c = 0; c < 3; c++) r[c * S + i] = rv[e][c];
+            const T w = own ? T(own[li[e]]) : T(1);
+            rz += w * (rv[e][0] * rv[e][0] * iv[e][0] + rv[e][1] * rv[e][1] * iv[e][1] + rv[e][2] * rv[e][2] * iv[e][2]);
+            rr += w * (rv[e][0] * rv[e][0] + rv[e][1] * rv[e][1] + rv[e][2] * rv[e][2]);
+        }
+    };
+    for (int64_t ch = w0; ch * 32 * PCG_E < n; ch += nw) {
+        const int64_t base = ch * 32 * PCG_E;
+        if (base + 32 * PCG_E <= n) chunk(base, std::true_type{});
+        else chunk(base, std::false_type{});
+    }
+    block_add((double)rz, slot[j + 1].rz);
+    block_add((double)rr, slot[j + 1].rr);
+}
+
+template <class T>
+__global__ void __launch_bounds__(256, 2) k_pcg_update2w(int64_t n, int64_t S, const int *__restrict__ list, int j,
+                                                         double thr, const T *__restrict__ invD,
+                                                         const T *__restrict__ r, vec4<T> *__restrict__ p,
+                                                         T *__restrict__ x, const CGSlot *slot, const DevScalars *sc) {
+    pdl_trigger();
+    pdl_wait();
+    const CGScal cs = cg_scalars(slot, j, true);
+    const int done = sc->cg_done_iter;
+    if ((done >= 0 && done <= j + 1) || (j > 0 && cs.rr <= thr)) return;
+    const T alpha = T(cs.rz / cs.pHp);
+    const bool more = cs.rr1 > thr;
+    const T beta = more ? T(cs.rz1 / cs.rz) : T(0);
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    auto chunk = [&](int64_t base, auto full) {
+        constexpr bool FULL = decltype(full)::value;
+        int li[PCG_E];
+        T xv[PCG_E][3], rv[PCG_E][3], iv[PCG_E][3];
+        vec4<T> pv[PCG_E];
+#pragma unroll
+        for (int e = 0; e < PCG_E; e++) {
+            const int64_t i = base + 32 * e + lane;
+            if (FULL || i < n) {
+                li[e] = list[i];
+#pragma unroll
+                for (int c = 0; c < 3; c++) {
+                    xv[e][c] = x[c * S + i];
+                    if (more) { rv[e][c] = r[c * S + i]; iv[e][c] = invD[c * S + i]; }
+                }
+            } else {
+                li[e] = -1;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < PCG_E; e++)
+            if (FULL || li[e] >= 0) pv[e] = p[li[e]];
+#pragma unroll
+        for (int e = 0; e < PCG_E; e++) {
+            if (!FULL && li[e] < 0) continue;
+            const int64_t i = base + 32 * e + lane;
+            x[i] = xv[e][0] + alpha * pv[e].x;
+            x[S + i] = xv[e][1] + alpha * pv[e].y;
+            x[2 * S + i] = xv[e][2] + alpha * pv[e].z;
+            if (more)
+                p[li[e]] = mk4<T>(rv[e][0] * iv[e][0] + beta * pv[e].x, rv[e][1] * iv[e][1] + beta * pv[e].y,
+                                  rv[e][2] * iv[e][2] + beta * pv[e].z, T(0));
+        }
+    };
+    for (int64_t ch = w0; ch * 32 * PCG_E < n; ch += nw) {
+        const int64_t base = ch * 32 * PCG_E;
+        if (base + 32 * PCG_E <= n) chunk(base, std::true_type{});
+        else chunk(base, std::false_type{});
+    }
+}
+
 // g . x over free DOFs (g tile-dense, x compact SoA)
 template <class T>
 __global__ void k_dot_gx(int64_t n, int64_t S, const int *__restrict__ list, const uint8_t *__restrict__ flag,
@@ -971,8 +1104,13 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     MPL_CHECK(ensure(ctx, ctx->n_x, (size_t)3 * SA * sizeof(T) + 64));
     MPL_CHECK(ensure(ctx, ctx->n_r, (size_t)3 * SA * sizeof(T) + 64));
     T *invD = (T *)ctx->n_invD.p, *x = (T *)ctx->n_x.p, *r = (T *)ctx->n_r.p;
-    vec4<T> *p = (vec4<T> *)ctx->n_p.p, *Hp = (vec4<T> *)ctx->n_Hp.p;
+    // p and Hp in one allocation (Hp = p + NT), so one L2 access-policy window can cover both
+    MPL_CHECK(ensure(ctx, ctx->n_p, (size_t)2 * NT * sizeof(vec4<T>) + 64));
+    vec4<T> *p = (vec4<T> *)ctx->n_p.p, *Hp = p + NT;
     const uint8_t *own_w = multi(ctx) ? own : nullptr;  // dot-product owner weights (slab ranks)
+    const char *pme = getenv("MPL_PCG_MAP");
+    // warp-interleaved update kernels (fp32 default; the fp64 instances spill, MPL_PCG_MAP=group / warp)
+    const bool pcg_warp_map = pme ? pme[0] == 'w' : sizeof(T) == 4;
     const unsigned VG = vgrid(NT);
     const unsigned VA = vgrid(NA);
     const unsigned VA1 = nblk(NA > 0 ? NA : 1, 256);
@@ -984,6 +1122,41 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     }
     const unsigned VAP = std::min<unsigned>(VA1, (unsigned)nsm_ * 8);  // persistent update kernels
     const int *list = (const int *)ctx->n_list.p;
+    // L2 persisting access-policy window for the Newton solve over p (MPL_L2WIN=p, default: the HVP's
+    // gathered input, read by update2), Hp (=h: the HVP's atomics target) or both at half hit ratio
+    // (=ph); without it the 390 MB tangent and the vector streams evict them between kernels.  Measured
+    // at cfg4 (step ms / in-step HVP us): none 66.1 / 100.3, p 64.6 / 95.7, h 64.5 / 96.4, ph 65.2 /
+    // 96.9; both at full hit ratio (74 MB of the 126 MB L2) 71.3 / 103.5.  MPL_L2WIN=0 disables;
+    // MPL_L2RESET=1 resets the persisting lines after the solve.  Clamped to the device limits.
+    const char *l2w = getenv("MPL_L2WIN");
+    const int l2mode = !l2w ? 2 : l2w[0] == '0' ? 0 : l2w[0] == 'h' ? 1 : (l2w[0] == 'p' && l2w[1] == 'h') ? 3 : 2;
+    const char *l2r = getenv("MPL_L2RESET");
+    const bool l2reset = l2r && l2r[0] == '1';
+    const bool l2win = l2mode != 0;
+    if (l2win) {
+        int dev = 0, maxp = 0, maxw = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        const size_t vb = (size_t)NT * sizeof(vec4<T>);
+        const size_t want = l2mode == 3 ? 2 * vb : vb;
+        const size_t win = std::min(want, (size_t)maxw);
+        const size_t lim = std::min(vb, (size_t)maxp);
+        static size_t limit_set = 0;
+        if (lim > 0 && limit_set != lim) {
+            MPL_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim));
+            limit_set = lim;
+        }
+        if (win > 0 && lim > 0) {
+            cudaStreamAttrValue a = {};
+            a.accessPolicyWindow.base_ptr = (void *)(l2mode == 1 ? Hp : p);
+            a.accessPolicyWindow.num_bytes = win;
+            a.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)lim / (double)win);
+            a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            MPL_CUDA(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a));
+        }
+    }
     cudaEvent_t e0, e1, h0, h1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -1070,13 +1243,21 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     if (timed) sampled.push_back({nl, jj});
                     nl++;
                     if (vec_events) cudaEventRecord(vev[nl - 1][0], st);
-                    MPL_CUDA(launch_pdl(k_pcg_update1<T, PCG_U>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p, Hp,
-                                        x, r, own_w, slots, sc));
+                    if (pcg_warp_map)
+                        MPL_CUDA(launch_pdl(k_pcg_update1w<T>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p, Hp, x,
+                                            r, own_w, slots, sc));
+                    else
+                        MPL_CUDA(launch_pdl(k_pcg_update1<T, PCG_U>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p,
+                                            Hp, x, r, own_w, slots, sc));
                     ctx->launches++;
                     MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
                     if (vec_events) cudaEventRecord(vev[nl - 1][1], st);
-                    MPL_CUDA(launch_pdl(k_pcg_update2<T, PCG_U>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, r, p,
-                                        x, slots, sc));
+                    if (pcg_warp_map)
+                        MPL_CUDA(launch_pdl(k_pcg_update2w<T>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, r, p, x,
+                                            slots, sc));
+                    else
+                        MPL_CUDA(launch_pdl(k_pcg_update2<T, PCG_U>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, r,
+                                            p, x, slots, sc));
                     ctx->launches++;
                     if (vec_events) cudaEventRecord(vev[nl - 1][2], st);
                 }
@@ -1187,6 +1368,12 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     S.hvp_ms = hsum;
+    if (l2win) {
+        cudaStreamAttrValue a = {};
+        a.accessPolicyWindow.num_bytes = 0;
+        MPL_CUDA(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a));
+        if (l2reset) MPL_CUDA(cudaCtxResetPersistingL2Cache());
+    }
     S.ms_phase[3] = t_lin;
     S.ms_phase[4] = t_pcg;
     S.ms_phase[5] = t_ls;

@@ -1,0 +1,14 @@
+set -u
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+python - > gpurun_out/l2attr.log 2>&1 <<'PY'
+import torch
+p = torch.cuda.get_device_properties(0)
+print(p)
+PY
+for w in 0 1 r; do
+  MPL_L2WIN=$w timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_$w.json 2>> gpurun_out/bench.err
+  echo "$w $(python -c "import json;d=json.load(open('gpurun_out/bench_$w.json'));print(d['ms_per_step'], d['hvp_ms'], d['phase_ms'])")" >> gpurun_out/ab.log
+done
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+echo done

@@ -1,0 +1,8 @@
+set -u
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+for w in h p ph 0; do for rs in 0 1; do
+  MPL_L2RESET=$rs MPL_L2WIN=$w timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_$w.json 2>> gpurun_out/bench.err
+  echo "$w reset=$rs $(python -c "import json;d=json.load(open('gpurun_out/bench_$w.json'));print(d['ms_per_step'], d['hvp_ms'], d['phase_ms'])")" >> gpurun_out/ab.log
+done; done
+echo done

@@ -389,8 +389,7 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
             Kout[k_off<T>(base, ncp, kz ? zslot[i / 45] : kslot(i / 45, n), i % 45)] = Ks[i];
     }
     // ---- node phase -----------------------------------------------------------------------
-    if (tid < 125) {
-        int h = tid;
+    for (int h = tid; h < 125; h += blockDim.x) {
         int hx = h / 25, hy = (h / 5) % 5, hz = h % 5;
         bool owned = hx < 4 && hy < 4 && hz < 4;
         bool interior = hx >= 1 && hx <= 3 && hy >= 1 && hy <= 3 && hz >= 1 && hz <= 3;
@@ -1043,9 +1042,13 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
         (const vec4<T> *)ctx->n_vhat.p, (const T *)owned_mass(ctx), (const T *)ctx->q_slot.p, (T *)ctx->K.p,       \
         (const int *)ctx->t_kstart.p, (const int *)ctx->t_ncell.p, (vec4<T> *)ctx->n_g.p, (vec4<T> *)ctx->n_diag.p, \
         ctx->mats.plastic ? (T *)ctx->q_Sp.p : (T *)nullptr, sc, hvp_kz_layout(ctx->precision)
-        if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY><<<T_, 128, 0, st>>>(LIN_ARGS);
-        else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD><<<T_, 128, 0, st>>>(LIN_ARGS);
-        else k_linearize<T, LIN_FULL><<<T_, 128, 0, st>>>(LIN_ARGS);
+        // 64 threads per tile: one per cell (a tile has <= 64); 128 left half the CTA idle in the
+        // cell phase (ncu at cfg4: barrier stalls 34 %, 16 warps / SM by registers)
+        const char *lte = getenv("MPL_LIN_THREADS");
+        const int lt = lte ? atoi(lte) : 64;
+        if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY><<<T_, lt, 0, st>>>(LIN_ARGS);
+        else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD><<<T_, lt, 0, st>>>(LIN_ARGS);
+        else k_linearize<T, LIN_FULL><<<T_, lt, 0, st>>>(LIN_ARGS);
         ctx->launches++;
 #undef LIN_ARGS
     }

@@ -1,0 +1,40 @@
+"""Subprocess body of tests/test_gpu_hvp_variants.py: with MPL_HVP_KERNEL / MPL_KZ_PAD / MPL_PCG_MAP set in
+the environment (the library reads them once per process), check one scene's HVP, Jacobi diagonal and
+replayed full step against the oracle.  Prints one line 'OK hvp=<rel> step=<rel>' or raises."""
+import sys
+
+import numpy as np
+
+from tests._parity import TOL, Pair, rel_l2
+from tests.test_gpu_parity import SCENES, _at, _fp32_scene, _probe
+
+
+def main(name: str) -> None:
+    pair = Pair(_fp32_scene(SCENES[name]()))
+    sc = pair.scene
+    tol = TOL[sc.precision]
+    v, u = _probe(pair)
+    pair.ctx.linearize(pair.to_gpu(v))
+    po = _at(pair, v)
+    h_o = po.hvp(v, u)
+    h_g = pair.ctx.hvp(pair.to_gpu(u))
+    e_h = rel_l2(h_g, h_o[pair.nid])
+    assert e_h <= tol["hvp"], f"hvp rel l2 {e_h}"
+    m = pair.un.m_i[:, None]
+    e_el = rel_l2(h_g - pair.m[:, None] * pair.to_gpu(u), (h_o - m * u)[pair.nid])
+    assert e_el <= (tol["hvp"] if sc.precision == 64 else 2e-4), f"elastic hvp rel l2 {e_el}"
+    e_d = rel_l2(pair.ctx.get_diag(), po.diag(v)[pair.nid])
+    assert e_d <= tol["hvp"], f"diag rel l2 {e_d}"
+    # one implicit step with the oracle's Newton / PCG / line-search counts replayed
+    st_o = pair.prob.newton(pair.v0, sc.solver)[1]
+    v_o, _ = pair.prob.newton(pair.v0, sc.solver, st_o["newton_iters"], st_o["cg_iters"], st_o["ls_iters"])
+    pair.ctx.set_velocity(pair.to_gpu(pair.v0))
+    st_g = pair.ctx.newton_step(sc.solver, st_o["newton_iters"], st_o["cg_iters"], st_o["ls_iters"])
+    assert st_g["cg_iters"] == st_o["cg_iters"], (st_g["cg_iters"], st_o["cg_iters"])
+    e_s = rel_l2(pair.ctx.get_velocity(), v_o[pair.nid])
+    assert e_s <= tol["step"], f"step rel l2 {e_s}"
+    print(f"OK hvp={e_h:.3e} elastic={e_el:.3e} diag={e_d:.3e} step={e_s:.3e}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])

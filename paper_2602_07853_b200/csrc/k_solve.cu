@@ -1130,13 +1130,13 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     // (=ph); without it the 390 MB tangent and the vector streams evict them between kernels.  Measured
     // at cfg4 (step ms / in-step HVP us): none 66.1 / 100.3, p 64.6 / 95.7, h 64.5 / 96.4, ph 65.2 /
     // 96.9; both at full hit ratio (74 MB of the 126 MB L2) 71.3 / 103.5.  MPL_L2WIN=0 disables;
-    // MPL_L2RESET=1 resets the persisting lines after the solve.  Clamped to the device limits.
+    // after the solve the persisting lines are reset and the set-aside released (MPL_L2RESET=0 keeps them).
     const char *l2w = getenv("MPL_L2WIN");
     const int l2mode = !l2w ? 2 : l2w[0] == '0' ? 0 : l2w[0] == 'h' ? 1 : (l2w[0] == 'p' && l2w[1] == 'h') ? 3 : 2;
     const char *l2r = getenv("MPL_L2RESET");
-    const bool l2reset = l2r && l2r[0] == '1';
-    const bool l2win = l2mode != 0;
-    if (l2win) {
+    const bool l2reset = !(l2r && l2r[0] == '0');
+    bool l2on = l2mode != 0;
+    if (l2on) {
         int dev = 0, maxp = 0, maxw = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
@@ -1145,12 +1145,11 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         const size_t want = l2mode == 3 ? 2 * vb : vb;
         const size_t win = std::min(want, (size_t)maxw);
         const size_t lim = std::min(vb, (size_t)maxp);
-        static size_t limit_set = 0;
-        if (lim > 0 && limit_set != lim) {
-            MPL_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim));
-            limit_set = lim;
-        }
-        if (win > 0 && lim > 0) {
+        // only when the window is fully persisting: a partial hit ratio (cfg5: p = 232 MB) halved the
+        // HVP's speed in the solve and after it
+        if (win > lim || lim == 0) l2on = false;
+        if (l2on) MPL_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim));
+        if (l2on) {
             cudaStreamAttrValue a = {};
             a.accessPolicyWindow.base_ptr = (void *)(l2mode == 1 ? Hp : p);
             a.accessPolicyWindow.num_bytes = win;
@@ -1371,11 +1370,14 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     S.hvp_ms = hsum;
-    if (l2win) {
+    if (l2on) {  // give the set-aside L2 back to the other phases
         cudaStreamAttrValue a = {};
         a.accessPolicyWindow.num_bytes = 0;
         MPL_CUDA(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a));
-        if (l2reset) MPL_CUDA(cudaCtxResetPersistingL2Cache());
+        if (l2reset) {
+            MPL_CUDA(cudaCtxResetPersistingL2Cache());
+            MPL_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
+        }
     }
     S.ms_phase[3] = t_lin;
     S.ms_phase[4] = t_pcg;

@@ -91,15 +91,25 @@ __global__ void k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ s
                       const int *__restrict__ cellof, const T *__restrict__ vG,
                       T *__restrict__ x, T *__restrict__ v, T *__restrict__ F, T *__restrict__ G,
                       const int *__restrict__ mat, MatP mp) {
+    // full warps without ghosts move x, F (in) and x, v, F, G (out) with 16-byte accesses through
+    // shared memory; others per lane
+    __shared__ __align__(16) T wsm[8][32 * 9];
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= np || pid[p] < 0) return;  // ghosts (slab ranks) are advected by their owner
+    const bool valid = p < np && pid[p] >= 0;  // ghosts (slab ranks) are advected by their owner
+    const bool fast = __all_sync(0xffffffffu, valid);
+    T *sm = wsm[threadIdx.x >> 5];
+    const int64_t p0 = p & ~(int64_t)31;
+    if (!valid) return;
     const int key = skey[p];
     const int t = key >> 6, l = key & 63;
     const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
     T xp[3], f[3];
+    if (fast) warp_load_aos<T, 3>(x, p0, sm, xp);
+    else
+#pragma unroll
+        for (int a = 0; a < 3; a++) xp[a] = x[3 * p + a];
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-        xp[a] = x[3 * p + a];
         T tt = (xp[a] - T(g.origin[a])) * T(g.inv_dx) - T(0.5);
         f[a] = tt - floor(tt);
     }
@@ -122,11 +132,12 @@ __global__ void k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ s
     }
     const T dt = T(dt_);
     T Fp[9], A[9], Fn[9];
+    if (fast) warp_load_aos<T, 9>(F, p0, sm, Fp);
+    else
 #pragma unroll
-    for (int a = 0; a < 9; a++) {
-        Fp[a] = F[9 * p + a];
-        A[a] = dt * Gp[a] + ((a % 4 == 0) ? T(1) : T(0));
-    }
+        for (int a = 0; a < 9; a++) Fp[a] = F[9 * p + a];
+#pragma unroll
+    for (int a = 0; a < 9; a++) A[a] = dt * Gp[a] + ((a % 4 == 0) ? T(1) : T(0));
     const int mk = mat[p];
     if (mp.kind[mk] == 2) {
         // water particle: J^{n+1} = (1 + dt tr G_p) J^n, F_p = J^{1/3} I (J - 1 kept exact in
@@ -153,9 +164,19 @@ __global__ void k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ s
     } else {
         mm3(A, Fp, Fn);
     }
+    T xn[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) xn[a] = xp[a] + dt * vp[a];
+    if (fast) {
+        warp_store_aos<T, 3>(x, p0, sm, xn);
+        warp_store_aos<T, 3>(v, p0, sm, vp);
+        warp_store_aos<T, 9>(F, p0, sm, Fn);
+        warp_store_aos<T, 9>(G, p0, sm, Gp);
+        return;
+    }
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-        x[3 * p + a] = xp[a] + dt * vp[a];
+        x[3 * p + a] = xn[a];
         v[3 * p + a] = vp[a];
     }
 #pragma unroll

@@ -262,16 +262,29 @@ __global__ void k_scatter(GridP g, MatP mp, int64_t np, const int *__restrict__ 
                           const int *__restrict__ mat, const int *__restrict__ pid, T *__restrict__ xo,
                           T *__restrict__ Fo, T *__restrict__ volo, int *__restrict__ mato, int *__restrict__ pido,
                           int *__restrict__ keyo, T *__restrict__ rec, DevScalars *sc) {
+    // full warps load x, v, F, G with 16-byte accesses through shared memory, others per lane
+    __shared__ __align__(16) T wsm[8][32 * 9];
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool fast = __all_sync(0xffffffffu, p < np);
+    T xp[3], vp[3], Fp[9], Gp[9];
+    if (fast) {
+        T *sm = wsm[threadIdx.x >> 5];
+        const int64_t p0 = p & ~(int64_t)31;
+        warp_load_aos<T, 3>(x, p0, sm, xp);
+        warp_load_aos<T, 3>(v, p0, sm, vp);
+        warp_load_aos<T, 9>(F, p0, sm, Fp);
+        warp_load_aos<T, 9>(G, p0, sm, Gp);
+    }
     if (p >= np) return;
+    if (!fast) {
+#pragma unroll
+        for (int a = 0; a < 3; a++) { xp[a] = x[3 * p + a]; vp[a] = v[3 * p + a]; }
+#pragma unroll
+        for (int a = 0; a < 9; a++) { Fp[a] = F[9 * p + a]; Gp[a] = G[9 * p + a]; }
+    }
     int k = key[p];
     int64_t d = bstart[k] + rank[p];
     DASSERT(k >= 0 && d >= 0 && d < np);
-    T xp[3], vp[3], Fp[9], Gp[9];
-#pragma unroll
-    for (int a = 0; a < 3; a++) { xp[a] = x[3 * p + a]; vp[a] = v[3 * p + a]; }
-#pragma unroll
-    for (int a = 0; a < 9; a++) { Fp[a] = F[9 * p + a]; Gp[a] = G[9 * p + a]; }
     T Vp = vol[p];
     int m = mat[p];
     int id = pid[p];

@@ -262,6 +262,38 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
     return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
+// Warp-cooperative AoS transfers for the particle kernels: the warp's 32 consecutive particles p0 ..
+// p0 + 31 (p0 % 32 == 0) own W contiguous reals each at A + W p0; 16-byte loads / stores of the whole
+// 32 W-real block through a per-warp shared buffer `sm` (>= 32 W reals), then each lane reads / writes
+// its W reals there (odd W: conflict-free).  One 16-byte access per lane per 4 / W particles instead of
+// W scalar accesses per particle.  All 32 lanes must call.
+template <class T, int W>
+__device__ __forceinline__ void warp_load_aos(const T *__restrict__ A, int64_t p0, T *sm, T out[W]) {
+    const int lane = threadIdx.x & 31;
+    constexpr int NV = (int)(32 * W * sizeof(T) / 16);
+    const float4 *src = reinterpret_cast<const float4 *>(A + (int64_t)W * p0);
+    float4 *d = reinterpret_cast<float4 *>(sm);
+#pragma unroll
+    for (int i = lane; i < NV; i += 32) d[i] = src[i];
+    __syncwarp();
+#pragma unroll
+    for (int a = 0; a < W; a++) out[a] = sm[lane * W + a];
+    __syncwarp();
+}
+template <class T, int W>
+__device__ __forceinline__ void warp_store_aos(T *__restrict__ A, int64_t p0, T *sm, const T in[W]) {
+    const int lane = threadIdx.x & 31;
+    constexpr int NV = (int)(32 * W * sizeof(T) / 16);
+#pragma unroll
+    for (int a = 0; a < W; a++) sm[lane * W + a] = in[a];
+    __syncwarp();
+    float4 *dst = reinterpret_cast<float4 *>(A + (int64_t)W * p0);
+    const float4 *s4 = reinterpret_cast<const float4 *>(sm);
+#pragma unroll
+    for (int i = lane; i < NV; i += 32) dst[i] = s4[i];
+    __syncwarp();
+}
+
 // symmetric 9x9 upper-triangle packing: row r (r = 3a+b) stores s = r..8
 __host__ __device__ __forceinline__ constexpr int kofs(int r) { return r * 9 - (r * (r - 1)) / 2; }
 __host__ __device__ __forceinline__ constexpr int kidx(int r, int s) { return kofs(r) + (s - r); }

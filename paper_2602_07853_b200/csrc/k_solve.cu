@@ -46,7 +46,9 @@ template <> __device__ __forceinline__ void atomic_add3<double>(d4 *p, double x,
 // =============================================================================================
 // a5 / a8: linearisation.  MODE = LIN_ENERGY (Phi only), LIN_GRAD (+ g), LIN_FULL (+ K, diag).
 // =============================================================================================
-template <class T, int MODE>
+// HONLY: every material slot is elastic StVK-Hencky (the other laws and the plastic base update are
+// compiled out: a third of the code, and ncu showed 20 % instruction-fetch stalls on the general kernel)
+template <class T, int MODE, bool HONLY = false>
 __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_, const int *__restrict__ nplus,
                                                    const int *__restrict__ cstart, const uint8_t *__restrict__ clocal,
                                                    const int *__restrict__ hascells, const vec4<T> *__restrict__ v,
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
                 if (V == T(0)) continue;
                 T mu = T(mp.mu[k]), lamL = T(mp.lam[k]);
                 T E[9] = {sl[1], sl[4], sl[6], sl[4], sl[2], sl[5], sl[6], sl[5], sl[3]};
-                if (qsp && mp.sigy[k] > 0.0) {
+                if (!HONLY && qsp && mp.sigy[k] > 0.0) {
                     // fixed-point plasticity: the slot's base for this Newton iteration.
                     // Energy-only evaluations (line search) use the stored iterate base; the gradient /
                     // full linearisation at a new iterate v re-project: F^tr = A(v) S_base, F^E = F^tr P,
@@ -154,7 +156,7 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
                         B[3 * a + b] = val;
                         B[3 * b + a] = val;
                     }
-                if (mp.kind[k] == 2) {
+                if (!HONLY && mp.kind[k] == 2) {
                     // ---- J-based water slot (PAPER §4.5): psi = kappa/2 (J-1)^2, J = det(A S),
                     //      tau = pi I, pi = kappa J (J-1); column (a,b): dJ/J = dt (F^{-T} S)[a][b],
                     //      dtau = kappa (2J-1) J (dJ/J) I ----
@@ -203,7 +205,7 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
                     }
                     continue;
                 }
-                if (mp.kind[k] == 1) {
+                if (!HONLY && mp.kind[k] == 1) {
                     // ---- split Neo-Hookean slot (PAPER §4.3.2; stable forms in mpl_common.cuh) ----
                     const T kap = T(mp.kappa[k]);
                     const T jm1 = det_ipm1(H), j23 = mexpm1(T(-2.0 / 3.0) * mlog1p(jm1));
@@ -1046,9 +1048,17 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
         // cell phase (ncu at cfg4: barrier stalls 34 %, 16 warps / SM by registers)
         const char *lte = getenv("MPL_LIN_THREADS");
         const int lt = lte ? atoi(lte) : 64;
-        if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY><<<T_, lt, 0, st>>>(LIN_ARGS);
-        else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD><<<T_, lt, 0, st>>>(LIN_ARGS);
-        else k_linearize<T, LIN_FULL><<<T_, lt, 0, st>>>(LIN_ARGS);
+        bool honly = !ctx->mats.plastic;
+        for (int k = 0; k < ctx->mats.nmat; k++) honly = honly && ctx->mats.kind[k] == 0;
+        if (honly) {
+            if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY, true><<<T_, lt, 0, st>>>(LIN_ARGS);
+            else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD, true><<<T_, lt, 0, st>>>(LIN_ARGS);
+            else k_linearize<T, LIN_FULL, true><<<T_, lt, 0, st>>>(LIN_ARGS);
+        } else {
+            if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY><<<T_, lt, 0, st>>>(LIN_ARGS);
+            else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD><<<T_, lt, 0, st>>>(LIN_ARGS);
+            else k_linearize<T, LIN_FULL><<<T_, lt, 0, st>>>(LIN_ARGS);
+        }
         ctx->launches++;
 #undef LIN_ARGS
     }

@@ -1386,6 +1386,250 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// v7 (MPL_HVP_KERNEL=wh): one warp per HALF tile, one cell per lane.  The wz kernel holds both cells'
+// tangents (90 registers) to keep a whole tile of loads in flight, which caps it at 12 warps / SM
+// where it is latency bound; here a lane holds one cell's 45 numbers, so 20 warps / SM fit.
+//   * item i = 2 t + h (h = the half: cells lx in {2h, 2h+1}); persistent warps strided by an even
+//     count, so a warp always works on the same half h and its node roles are fixed;
+//   * lane = 16 (lx - 2h) + 4 ly + lz, i.e. local cell l = 32 h + lane: in the tile's natural compact
+//     order (layout 3: slot = rank of l among the tile's cells) a warp's slots are contiguous;
+//   * the half's 3 x 5 x 5 node halo at shared slot 25 x + 5 y + 2 z (every quarter-warp's 16-byte
+//     accesses conflict-free), 8 scatter passes into a per-warp force buffer, then 3 nodes per lane:
+//     the 9 nodes all of whose cells lie in the half are stored, the others (incl. the x = 2 plane
+//     shared with the other half) added atomically; the lumped-mass term of an owned node is added by
+//     the half whose cells own its x (x in {2h, 2h+1}).
+// ---------------------------------------------------------------------------------------------
+constexpr int WH_W = 4;  // warps per CTA
+struct WhWarp {
+    alignas(16) f4 uh[2][80];
+    alignas(16) f4 F[80];
+    alignas(16) float mh[2][32];
+};
+// role of halo node n (0..74) of half h: local id | neighbour slot << 6 | mass << 9 | interior << 10 |
+// shared slot << 11 | mass index << 18; -1 = none
+__device__ __forceinline__ int wh_role(int n, int h) {
+    if (n >= 75) return -1;
+    const int x = n / 25, Y = (n / 5) % 5, Z = n % 5, X = 2 * h + x;
+    const int dp = ((X >> 2) << 2) | ((Y >> 2) << 1) | (Z >> 2);
+    const int mass = (x < 2 && Y < 4 && Z < 4);
+    const int interior = (x == 1 && Y >= 1 && Y <= 3 && Z >= 1 && Z <= 3);
+    const int midx = mass ? x * 16 + Y * 4 + Z : 0;
+    return local_id(X & 3, Y & 3, Z & 3) | (dp << 6) | (mass << 9) | (interior << 10) | ((25 * x + 5 * Y + 2 * Z) << 11) |
+           (midx << 18);
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(32 * WH_W, MINB)
+    k_hvp_wh(int T_, const int *__restrict__ nplus, const unsigned long long *__restrict__ cmask,
+             const int *__restrict__ hascells, const float *__restrict__ K, const int *__restrict__ kstart,
+             const float *__restrict__ nmass, const f4 *__restrict__ u, f4 *__restrict__ Hu, double *__restrict__ uHu,
+             const CGSlot *__restrict__ cgs, int cgj, double cgthr, const DevScalars *__restrict__ sc) {
+    __shared__ WhWarp SW[WH_W];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    WhWarp &S = SW[wid];
+    pdl_trigger();
+    pdl_wait();
+    if (cgs != nullptr) {
+        const double rr = warp_sum(cgs[cgj].rr[lane]);
+        if (sc->neg_curv || (cgj > 0 && rr <= cgthr)) return;
+    }
+    const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
+    const int G = gridDim.x * WH_W, i0 = blockIdx.x * WH_W + wid;  // G even: item parity fixed
+    const int h = i0 & 1;
+    const int lx = 2 * h + (lane >> 4), ly = (lane >> 2) & 3, lz = lane & 3;
+    const int hb = 25 * (lx - 2 * h) + 5 * ly + 2 * lz;  // shared slot of the cell's (0,0,0) corner
+    int role[3];
+#pragma unroll
+    for (int r = 0; r < 3; r++) role[r] = wh_role(lane + 32 * r, h);
+    for (int i = lane; i < 80; i += 32) S.F[i] = mk4<float>(0.f, 0.f, 0.f, 0.f);
+    const uint64_t pol = l2_evict_first_policy();
+    const int NI = 2 * T_;
+    const int *mbase = lane < 8 ? nplus + lane : lane == 8 ? kstart : lane == 9 ? hascells
+                                                                      : reinterpret_cast<const int *>(cmask) + (lane - 10);
+    const int mstride = lane < 8 ? 8 : lane < 10 ? 1 : 2;
+    auto load_meta = [&](int it_) -> int {  // metadata of item it_'s tile, spread over lanes 0-11
+        if (it_ >= NI || lane >= 12) return 0;
+        const int t = it_ >> 1;
+        return lane == 0 ? t : __ldg(mbase + (int64_t)mstride * t);
+    };
+    struct TileK {
+        int has, pres;
+        unsigned sb;  // chunk stride in bytes (16 n)
+        int e44;      // element 44 at ka + e44
+        const float *ka;
+    };
+    auto tile_k = [&](int it_, int meta) -> TileK {
+        TileK q;
+        q.has = __shfl_sync(FULL, meta, 9);
+        const int ks = __shfl_sync(FULL, meta, 8);
+        const unsigned clo = (unsigned)__shfl_sync(FULL, meta, 10), chi = (unsigned)__shfl_sync(FULL, meta, 11);
+        if (it_ >= NI) q.has = 0;
+        const unsigned word = h ? chi : clo;
+        q.pres = q.has ? (int)((word >> lane) & 1u) : 0;
+        const int n = __popc(clo) + __popc(chi);
+        const int sl = (h ? __popc(clo) : 0) + __popc(word & lt);
+        q.sb = 16u * (unsigned)n;
+        q.ka = K + ks + 4 * sl;
+        q.e44 = 44 * n - 3 * sl;
+        return q;
+    };
+    float k[45];
+    auto kload_all = [&](const TileK &q) {
+        if (!q.pres) return;
+#pragma unroll
+        for (int c = 0; c < 11; c++) {
+            const float4 v = ldg_stream(reinterpret_cast<const float *>(reinterpret_cast<const char *>(q.ka) +
+                                                                        (uint64_t)q.sb * (uint64_t)c), pol);
+            k[4 * c] = v.x; k[4 * c + 1] = v.y; k[4 * c + 2] = v.z; k[4 * c + 3] = v.w;
+        }
+        k[44] = ldg_stream1(q.ka + q.e44, pol);
+    };
+    auto halo = [&](int it_, int b, int meta) {
+        const int has = __shfl_sync(FULL, meta, 9);
+        int tt[3];
+#pragma unroll
+        for (int r = 0; r < 3; r++) tt[r] = __shfl_sync(FULL, meta, role[r] < 0 ? 0 : (role[r] >> 6) & 7);
+        if (it_ < NI) {
+#pragma unroll
+            for (int r = 0; r < 3; r++) {
+                if (role[r] < 0) continue;
+                const int loc = role[r] & 63, mass = (role[r] >> 9) & 1, hs = (role[r] >> 11) & 127,
+                          mi = role[r] >> 18;
+                if ((has || mass) && tt[r] >= 0) {
+                    const int64_t nd = (int64_t)tt[r] * 64 + loc;
+                    cp_async16(&S.uh[b][hs], u + nd);
+                    if (mass) cp_async4(&S.mh[b][mi], nmass + nd);
+                } else {
+                    S.uh[b][hs] = mk4<float>(0.f, 0.f, 0.f, 0.f);
+                    if (mass) S.mh[b][mi] = 0.f;
+                }
+            }
+        }
+        cp_async_commit();
+    };
+    int mcur = load_meta(i0);
+    int mnext = load_meta(i0 + G);
+    TileK cur = tile_k(i0, mcur);
+    kload_all(cur);
+    halo(i0, 0, mcur);
+    double acc = 0.0;
+    int itc = 0;
+    for (int it_ = i0; it_ < NI; it_ += G, itc++) {
+        const int b = itc & 1;
+        const int mnn = load_meta(it_ + 2 * G);
+        const TileK nxt = tile_k(it_ + G, mnext);
+        cp_async_wait<0>();
+        __syncwarp();
+        const f4 *uh = S.uh[b];
+        float P[9];
+        if (cur.has) {
+            float dG[9];
+            {
+                float Dx[2][3], Dy[2][3], Sz[2][3];
+#pragma unroll
+                for (int q = 0; q < 2; q++) {
+                    const f4 w00 = uh[hb + q * 2], w01 = uh[hb + 5 + q * 2], w10 = uh[hb + 25 + q * 2],
+                             w11 = uh[hb + 30 + q * 2];
+                    const float a00[3] = {w00.x, w00.y, w00.z}, a01[3] = {w01.x, w01.y, w01.z};
+                    const float a10[3] = {w10.x, w10.y, w10.z}, a11[3] = {w11.x, w11.y, w11.z};
+#pragma unroll
+                    for (int a = 0; a < 3; a++) {
+                        const float s1 = a11[a] - a00[a], s2 = a10[a] - a01[a];
+                        Dx[q][a] = s1 + s2;
+                        Dy[q][a] = s1 - s2;
+                        Sz[q][a] = (a00[a] + a11[a]) + (a01[a] + a10[a]);
+                    }
+                }
+#pragma unroll
+                for (int a = 0; a < 3; a++) {
+                    dG[3 * a] = Dx[0][a] + Dx[1][a];
+                    dG[3 * a + 1] = Dy[0][a] + Dy[1][a];
+                    dG[3 * a + 2] = Sz[1][a] - Sz[0][a];
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < 9; r++) P[r] = 0.f;
+#pragma unroll
+            for (int e = 0; e < 45; e++) {
+                const int r = krow(e), c = kcol(e);
+                P[r] += k[e] * dG[c];
+                if (c != r) P[c] += k[e] * dG[r];
+            }
+            float qf = 0.f;
+#pragma unroll
+            for (int r = 0; r < 9; r++) {
+                P[r] = cur.pres ? P[r] : 0.f;
+                qf += P[r] * dG[r];
+            }
+            acc += (double)qf;
+        }
+        kload_all(nxt);
+        halo(it_ + G, b ^ 1, mnext);
+        if (cur.has) {
+            float g4[3][4];
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+                const float e1 = P[3 * a] + P[3 * a + 1], e2 = P[3 * a] - P[3 * a + 1], z = P[3 * a + 2];
+                g4[a][0] = e1 + z; g4[a][1] = e1 - z; g4[a][2] = e2 + z; g4[a][3] = e2 - z;
+            }
+            auto corner = [&](const float g[4], int ox, int oy, int oz) -> float {
+                if (ox && oy) return oz ? g[0] : g[1];
+                if (!ox && !oy) return oz ? -g[1] : -g[0];
+                if (ox) return oz ? g[2] : g[3];
+                return oz ? -g[3] : -g[2];
+            };
+#pragma unroll
+            for (int ox = 0; ox < 2; ox++)
+#pragma unroll
+                for (int oy = 0; oy < 2; oy++)
+#pragma unroll
+                    for (int oz = 0; oz < 2; oz++) {
+                        f4 *fp = &S.F[hb + 25 * ox + 5 * oy + 2 * oz];
+                        const f4 o = *fp;
+                        *fp = mk4<float>(o.x + corner(g4[0], ox, oy, oz), o.y + corner(g4[1], ox, oy, oz),
+                                         o.z + corner(g4[2], ox, oy, oz), 0.f);
+                        __syncwarp();
+                    }
+        }
+        int tt[3];
+#pragma unroll
+        for (int r = 0; r < 3; r++) tt[r] = __shfl_sync(FULL, mcur, role[r] < 0 ? 0 : (role[r] >> 6) & 7);
+#pragma unroll
+        for (int r = 0; r < 3; r++) {
+            if (role[r] < 0) continue;
+            const int loc = role[r] & 63, mass = (role[r] >> 9) & 1, interior = (role[r] >> 10) & 1,
+                      hs = (role[r] >> 11) & 127, mi = role[r] >> 18;
+            f4 f = mk4<float>(0.f, 0.f, 0.f, 0.f);
+            if (cur.has) {
+                f = S.F[hs];
+                S.F[hs] = mk4<float>(0.f, 0.f, 0.f, 0.f);
+            }
+            if (!(cur.has || mass) || tt[r] < 0) continue;
+            if (mass) {
+                const float mm = S.mh[b][mi];
+                if (mm > 0.f) {
+                    const f4 w = uh[hs];
+                    f.x += mm * w.x; f.y += mm * w.y; f.z += mm * w.z;
+                    acc += (double)(mm * (w.x * w.x + w.y * w.y + w.z * w.z));
+                }
+            }
+            const int64_t nd = (int64_t)tt[r] * 64 + loc;
+            if (interior) Hu[nd] = mk4<float>(f.x, f.y, f.z, 0.f);
+            else if (f.x != 0.f || f.y != 0.f || f.z != 0.f) atomic_add3<float>(Hu + nd, f.x, f.y, f.z);
+        }
+        __syncwarp();
+        mcur = mnext;
+        mnext = mnn;
+        cur = nxt;
+    }
+    cp_async_wait<0>();
+    if (uHu) {
+        const double v = warp_sum(acc);
+        if (lane == 0 && v != 0.0) atomicAdd(&uHu[(blockIdx.x * WH_W + wid) % NSTRIPE], v);
+    }
+}
+
 int g_num_sms = 0;
 
 template <int MINB, bool ROLL, int SCAT, bool PAD>
@@ -1408,6 +1652,29 @@ mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
                         (const int *)ctx->t_hascells.p, (const float *)ctx->K.p, (const int *)ctx->t_kstart.p,
                         (const float *)owned_mass(ctx), (const f4 *)u_tile, (f4 *)Hu_tile, uHu, cgs, cgj, cgthr,
                         (const DevScalars *)ctx->scalars.p));
+    ctx->launches++;
+    return MPL_OK;
+}
+
+template <int MINB>
+mpl_status launch_wh(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
+                     double cgthr) {
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        int occ = 0;
+        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_wh<MINB>, 32 * WH_W, 0));
+        per_sm = occ > 0 ? occ : 1;
+    }
+    int grid = g_num_sms * per_sm;
+    const int need = (2 * ctx->T + WH_W - 1) / WH_W;
+    if (grid > need) grid = need;
+    MPL_CUDA(launch_pdl(k_hvp_wh<MINB>, grid, 32 * WH_W, 0, ctx->stream, ctx->T, (const int *)ctx->t_nplus.p,
+                        (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_hascells.p,
+                        (const float *)ctx->K.p, (const int *)ctx->t_kstart.p, (const float *)owned_mass(ctx),
+                        (const f4 *)u_tile, (f4 *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p));
     ctx->launches++;
     return MPL_OK;
 }
@@ -1490,7 +1757,8 @@ mpl_status launch_pipe(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *u
 
 }  // namespace
 
-// HVP variant from MPL_HVP_KERNEL: "wz" (default for fp32; fp64 falls back to rp10; "wzp" with the
+// HVP variant from MPL_HVP_KERNEL: "wh" / "wh4" (half-tile warps, v7), "wz" (default for fp32; fp64
+// falls back to rp10; "wzp" with the
 // plane scatter, "wzs" with the shuffle reduction, "wz2" / "wzp2" / "wzs2" with rolling tangent loads at
 // 2 CTAs per SM), "rp10" (default
 // for fp64), "rp" / "rp12": persistent, tangent register-pipelined (v4) with >= 10 / 1 / 12 CTAs per SM
@@ -1501,7 +1769,8 @@ int hvp_variant() {
     if (variant < 0) {
         const char *e = getenv("MPL_HVP_KERNEL");
         variant = 11;
-        if (e && e[0] == 'w' && e[1] == 'z') {
+        if (e && e[0] == 'w' && e[1] == 'h') variant = e[2] == '4' ? 17 : 16;
+        else if (e && e[0] == 'w' && e[1] == 'z') {
             const int sc = e[2] == 'p' ? 1 : e[2] == 's' ? 2 : e[2] == '3' ? 3 : 0;
             const bool roll = e[sc ? 3 : 2] == '2';
             variant = sc == 1 ? 9 : sc == 2 ? (roll ? 14 : 13) : sc == 3 ? 15 : (roll ? 12 : 11);
@@ -1532,7 +1801,9 @@ int hvp_kz_layout(int precision) {
         const char *e = getenv("MPL_KZ_PAD");
         pad = (e && e[0] == '1') ? 1 : 0;
     }
-    if (precision != 32 || hvp_variant() < 9 || hvp_variant() > 15) return 0;
+    if (precision != 32) return 0;
+    if (hvp_variant() == 16 || hvp_variant() == 17) return 3;  // wh: natural compact order (slot = rank)
+    if (hvp_variant() < 9 || hvp_variant() > 15) return 0;
     return pad ? 2 : 1;
 }
 
@@ -1542,6 +1813,12 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
                       double cgthr) {
     if (ctx->T == 0) return MPL_OK;
     int variant = hvp_variant();
+    if (variant == 16 || variant == 17) {
+        if (sizeof(T) == 4)
+            return variant == 16 ? launch_wh<5>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr)
+                                 : launch_wh<4>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+        variant = 5;
+    }
     if (variant >= 9 && variant <= 15) {
         if (sizeof(T) == 4) {
             const bool pad = hvp_kz_layout(32) == 2;

@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(128) k_linearize(GridP g, MatP mp, double dt_,
         if (kz) {  // kz order (the wz HVP lanes): 64-slot block, slot = kz_key; compact: slot = its rank
             if (tid < n) {
                 const int key = kz_key(clocal[cs + tid]);
-                int sl = key;
+                int sl = kz == 3 ? tid : key;  // 3: natural compact order (wh HVP)
                 if (kz == 1) {
                     sl = 0;
                     for (int j = 0; j < n; j++) sl += kz_key(clocal[cs + j]) < key;

@@ -19,6 +19,8 @@ CASES = [
     ({"MPL_HVP_KERNEL": "wzs"}, "mix_fp32"),
     ({"MPL_HVP_KERNEL": "wzs2"}, "mix_fp32"),
     ({"MPL_HVP_KERNEL": "wz3"}, "mix_fp32"),
+    ({"MPL_HVP_KERNEL": "wh"}, "mix_fp32"),
+    ({"MPL_HVP_KERNEL": "wh4"}, "mix_fp32"),
     ({"MPL_HVP_KERNEL": "rp10"}, "mix_fp32"),
     ({"MPL_HVP_KERNEL": "rq"}, "mix_fp32"),
     ({"MPL_HVP_KERNEL": "pipe2"}, "mix_fp32"),

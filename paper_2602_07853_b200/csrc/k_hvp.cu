@@ -1401,11 +1401,35 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
 //     the half whose cells own its x (x in {2h, 2h+1}).
 // ---------------------------------------------------------------------------------------------
 constexpr int WH_W = 4;  // warps per CTA
-struct WhWarp {
-    alignas(16) f4 uh[2][80];
-    alignas(16) f4 F[80];
-    alignas(16) float mh[2][32];
+template <class T> struct WhWarp {
+    alignas(16) vec4<T> uh[2][80];
+    alignas(16) vec4<T> F[80];
+    alignas(16) T mh[2][32];
 };
+__device__ __forceinline__ double2 ldg_stream2d(const double *p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ldg_stream1d(const double *p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+// chunk c (16 bytes) of a tangent slot and the remainder element 44, both precisions
+template <class T> __device__ __forceinline__ void wh_chunk(const T *p, uint64_t pol, T *k);
+template <> __device__ __forceinline__ void wh_chunk<float>(const float *p, uint64_t pol, float *k) {
+    const float4 v = ldg_stream(p, pol);
+    k[0] = v.x; k[1] = v.y; k[2] = v.z; k[3] = v.w;
+}
+template <> __device__ __forceinline__ void wh_chunk<double>(const double *p, uint64_t pol, double *k) {
+    const double2 v = ldg_stream2d(p, pol);
+    k[0] = v.x; k[1] = v.y;
+}
+__device__ __forceinline__ float wh_one(const float *p, uint64_t pol) { return ldg_stream1(p, pol); }
+__device__ __forceinline__ double wh_one(const double *p, uint64_t pol) { return ldg_stream1d(p, pol); }
 // role of halo node n (0..74) of half h: local id | neighbour slot << 6 | mass << 9 | interior << 10 |
 // shared slot << 11 | mass index << 18; -1 = none
 __device__ __forceinline__ int wh_role(int n, int h) {
@@ -1419,15 +1443,18 @@ __device__ __forceinline__ int wh_role(int n, int h) {
            (midx << 18);
 }
 
-template <int MINB>
+template <class T, int MINB>
 __global__ void __launch_bounds__(32 * WH_W, MINB)
     k_hvp_wh(int T_, const int *__restrict__ nplus, const unsigned long long *__restrict__ cmask,
-             const int *__restrict__ hascells, const float *__restrict__ K, const int *__restrict__ kstart,
-             const float *__restrict__ nmass, const f4 *__restrict__ u, f4 *__restrict__ Hu, double *__restrict__ uHu,
-             const CGSlot *__restrict__ cgs, int cgj, double cgthr, const DevScalars *__restrict__ sc) {
-    __shared__ WhWarp SW[WH_W];
+             const int *__restrict__ hascells, const T *__restrict__ K, const int *__restrict__ kstart,
+             const T *__restrict__ nmass, const vec4<T> *__restrict__ u, vec4<T> *__restrict__ Hu,
+             double *__restrict__ uHu, const CGSlot *__restrict__ cgs, int cgj, double cgthr,
+             const DevScalars *__restrict__ sc) {
+    using V4 = vec4<T>;
+    constexpr int VEC = KL<T>::VEC, NCH = KL<T>::NCH;
+    __shared__ WhWarp<T> SW[WH_W];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    WhWarp &S = SW[wid];
+    WhWarp<T> &S = SW[wid];
     pdl_trigger();
     pdl_wait();
     if (cgs != nullptr) {
@@ -1442,7 +1469,7 @@ __global__ void __launch_bounds__(32 * WH_W, MINB)
     int role[3];
 #pragma unroll
     for (int r = 0; r < 3; r++) role[r] = wh_role(lane + 32 * r, h);
-    for (int i = lane; i < 80; i += 32) S.F[i] = mk4<float>(0.f, 0.f, 0.f, 0.f);
+    for (int i = lane; i < 80; i += 32) S.F[i] = mk4<T>(T(0), T(0), T(0), T(0));
     const uint64_t pol = l2_evict_first_policy();
     const int NI = 2 * T_;
     const int *mbase = lane < 8 ? nplus + lane : lane == 8 ? kstart : lane == 9 ? hascells
@@ -1457,7 +1484,7 @@ __global__ void __launch_bounds__(32 * WH_W, MINB)
         int has, pres;
         unsigned sb;  // chunk stride in bytes (16 n)
         int e44;      // element 44 at ka + e44
-        const float *ka;
+        const T *ka;
     };
     auto tile_k = [&](int it_, int meta) -> TileK {
         TileK q;
@@ -1470,20 +1497,18 @@ __global__ void __launch_bounds__(32 * WH_W, MINB)
         const int n = __popc(clo) + __popc(chi);
         const int sl = (h ? __popc(clo) : 0) + __popc(word & lt);
         q.sb = 16u * (unsigned)n;
-        q.ka = K + ks + 4 * sl;
-        q.e44 = 44 * n - 3 * sl;
+        q.ka = K + ks + VEC * sl;
+        q.e44 = 44 * n + sl - VEC * sl;
         return q;
     };
-    float k[45];
+    T k[45];
     auto kload_all = [&](const TileK &q) {
         if (!q.pres) return;
 #pragma unroll
-        for (int c = 0; c < 11; c++) {
-            const float4 v = ldg_stream(reinterpret_cast<const float *>(reinterpret_cast<const char *>(q.ka) +
-                                                                        (uint64_t)q.sb * (uint64_t)c), pol);
-            k[4 * c] = v.x; k[4 * c + 1] = v.y; k[4 * c + 2] = v.z; k[4 * c + 3] = v.w;
-        }
-        k[44] = ldg_stream1(q.ka + q.e44, pol);
+        for (int c = 0; c < NCH; c++)
+            wh_chunk<T>(reinterpret_cast<const T *>(reinterpret_cast<const char *>(q.ka) + (uint64_t)q.sb * (uint64_t)c),
+                        pol, k + VEC * c);
+        k[44] = wh_one(q.ka + q.e44, pol);
     };
     auto halo = [&](int it_, int b, int meta) {
         const int has = __shfl_sync(FULL, meta, 9);
@@ -1498,11 +1523,14 @@ __global__ void __launch_bounds__(32 * WH_W, MINB)
                           mi = role[r] >> 18;
                 if ((has || mass) && tt[r] >= 0) {
                     const int64_t nd = (int64_t)tt[r] * 64 + loc;
-                    cp_async16(&S.uh[b][hs], u + nd);
-                    if (mass) cp_async4(&S.mh[b][mi], nmass + nd);
+#pragma unroll
+                    for (int qq = 0; qq < (int)(sizeof(V4) / 16); qq++)
+                        cp_async16(reinterpret_cast<char *>(&S.uh[b][hs]) + 16 * qq,
+                                   reinterpret_cast<const char *>(u + nd) + 16 * qq);
+                    if (mass) cp_async_real<T>(&S.mh[b][mi], nmass + nd);
                 } else {
-                    S.uh[b][hs] = mk4<float>(0.f, 0.f, 0.f, 0.f);
-                    if (mass) S.mh[b][mi] = 0.f;
+                    S.uh[b][hs] = mk4<T>(T(0), T(0), T(0), T(0));
+                    if (mass) S.mh[b][mi] = T(0);
                 }
             }
         }
@@ -1521,21 +1549,21 @@ __global__ void __launch_bounds__(32 * WH_W, MINB)
         const TileK nxt = tile_k(it_ + G, mnext);
         cp_async_wait<0>();
         __syncwarp();
-        const f4 *uh = S.uh[b];
-        float P[9];
+        const V4 *uh = S.uh[b];
+        T P[9];
         if (cur.has) {
-            float dG[9];
+            T dG[9];
             {
-                float Dx[2][3], Dy[2][3], Sz[2][3];
+                T Dx[2][3], Dy[2][3], Sz[2][3];
 #pragma unroll
                 for (int q = 0; q < 2; q++) {
-                    const f4 w00 = uh[hb + q * 2], w01 = uh[hb + 5 + q * 2], w10 = uh[hb + 25 + q * 2],
+                    const V4 w00 = uh[hb + q * 2], w01 = uh[hb + 5 + q * 2], w10 = uh[hb + 25 + q * 2],
                              w11 = uh[hb + 30 + q * 2];
-                    const float a00[3] = {w00.x, w00.y, w00.z}, a01[3] = {w01.x, w01.y, w01.z};
-                    const float a10[3] = {w10.x, w10.y, w10.z}, a11[3] = {w11.x, w11.y, w11.z};
+                    const T a00[3] = {w00.x, w00.y, w00.z}, a01[3] = {w01.x, w01.y, w01.z};
+                    const T a10[3] = {w10.x, w10.y, w10.z}, a11[3] = {w11.x, w11.y, w11.z};
 #pragma unroll
                     for (int a = 0; a < 3; a++) {
-                        const float s1 = a11[a] - a00[a], s2 = a10[a] - a01[a];
+                        const T s1 = a11[a] - a00[a], s2 = a10[a] - a01[a];
                         Dx[q][a] = s1 + s2;
                         Dy[q][a] = s1 - s2;
                         Sz[q][a] = (a00[a] + a11[a]) + (a01[a] + a10[a]);
@@ -1549,17 +1577,17 @@ __global__ void __launch_bounds__(32 * WH_W, MINB)
                 }
             }
 #pragma unroll
-            for (int r = 0; r < 9; r++) P[r] = 0.f;
+            for (int r = 0; r < 9; r++) P[r] = T(0);
 #pragma unroll
             for (int e = 0; e < 45; e++) {
                 const int r = krow(e), c = kcol(e);
                 P[r] += k[e] * dG[c];
                 if (c != r) P[c] += k[e] * dG[r];
             }
-            float qf = 0.f;
+            T qf = T(0);
 #pragma unroll
             for (int r = 0; r < 9; r++) {
-                P[r] = cur.pres ? P[r] : 0.f;
+                P[r] = cur.pres ? P[r] : T(0);
                 qf += P[r] * dG[r];
             }
             acc += (double)qf;
@@ -1567,13 +1595,13 @@ __global__ void __launch_bounds__(32 * WH_W, MINB)
         kload_all(nxt);
         halo(it_ + G, b ^ 1, mnext);
         if (cur.has) {
-            float g4[3][4];
+            T g4[3][4];
 #pragma unroll
             for (int a = 0; a < 3; a++) {
-                const float e1 = P[3 * a] + P[3 * a + 1], e2 = P[3 * a] - P[3 * a + 1], z = P[3 * a + 2];
+                const T e1 = P[3 * a] + P[3 * a + 1], e2 = P[3 * a] - P[3 * a + 1], z = P[3 * a + 2];
                 g4[a][0] = e1 + z; g4[a][1] = e1 - z; g4[a][2] = e2 + z; g4[a][3] = e2 - z;
             }
-            auto corner = [&](const float g[4], int ox, int oy, int oz) -> float {
+            auto corner = [&](const T g[4], int ox, int oy, int oz) -> T {
                 if (ox && oy) return oz ? g[0] : g[1];
                 if (!ox && !oy) return oz ? -g[1] : -g[0];
                 if (ox) return oz ? g[2] : g[3];
@@ -1585,10 +1613,10 @@ __global__ void __launch_bounds__(32 * WH_W, MINB)
                 for (int oy = 0; oy < 2; oy++)
 #pragma unroll
                     for (int oz = 0; oz < 2; oz++) {
-                        f4 *fp = &S.F[hb + 25 * ox + 5 * oy + 2 * oz];
-                        const f4 o = *fp;
-                        *fp = mk4<float>(o.x + corner(g4[0], ox, oy, oz), o.y + corner(g4[1], ox, oy, oz),
-                                         o.z + corner(g4[2], ox, oy, oz), 0.f);
+                        V4 *fp = &S.F[hb + 25 * ox + 5 * oy + 2 * oz];
+                        const V4 o = *fp;
+                        *fp = mk4<T>(o.x + corner(g4[0], ox, oy, oz), o.y + corner(g4[1], ox, oy, oz),
+                                     o.z + corner(g4[2], ox, oy, oz), T(0));
                         __syncwarp();
                     }
         }
@@ -1600,23 +1628,23 @@ __global__ void __launch_bounds__(32 * WH_W, MINB)
             if (role[r] < 0) continue;
             const int loc = role[r] & 63, mass = (role[r] >> 9) & 1, interior = (role[r] >> 10) & 1,
                       hs = (role[r] >> 11) & 127, mi = role[r] >> 18;
-            f4 f = mk4<float>(0.f, 0.f, 0.f, 0.f);
+            V4 f = mk4<T>(T(0), T(0), T(0), T(0));
             if (cur.has) {
                 f = S.F[hs];
-                S.F[hs] = mk4<float>(0.f, 0.f, 0.f, 0.f);
+                S.F[hs] = mk4<T>(T(0), T(0), T(0), T(0));
             }
             if (!(cur.has || mass) || tt[r] < 0) continue;
             if (mass) {
-                const float mm = S.mh[b][mi];
-                if (mm > 0.f) {
-                    const f4 w = uh[hs];
+                const T mm = S.mh[b][mi];
+                if (mm > T(0)) {
+                    const V4 w = uh[hs];
                     f.x += mm * w.x; f.y += mm * w.y; f.z += mm * w.z;
                     acc += (double)(mm * (w.x * w.x + w.y * w.y + w.z * w.z));
                 }
             }
             const int64_t nd = (int64_t)tt[r] * 64 + loc;
-            if (interior) Hu[nd] = mk4<float>(f.x, f.y, f.z, 0.f);
-            else if (f.x != 0.f || f.y != 0.f || f.z != 0.f) atomic_add3<float>(Hu + nd, f.x, f.y, f.z);
+            if (interior) Hu[nd] = mk4<T>(f.x, f.y, f.z, T(0));
+            else if (f.x != T(0) || f.y != T(0) || f.z != T(0)) atomic_add3<T>(Hu + nd, f.x, f.y, f.z);
         }
         __syncwarp();
         mcur = mnext;
@@ -1656,7 +1684,7 @@ mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
     return MPL_OK;
 }
 
-template <int MINB>
+template <class T, int MINB>
 mpl_status launch_wh(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
                      double cgthr) {
     static int per_sm = 0;
@@ -1665,16 +1693,17 @@ mpl_status launch_wh(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         int occ = 0;
-        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_wh<MINB>, 32 * WH_W, 0));
+        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_wh<T, MINB>, 32 * WH_W, 0));
         per_sm = occ > 0 ? occ : 1;
     }
     int grid = g_num_sms * per_sm;
     const int need = (2 * ctx->T + WH_W - 1) / WH_W;
     if (grid > need) grid = need;
-    MPL_CUDA(launch_pdl(k_hvp_wh<MINB>, grid, 32 * WH_W, 0, ctx->stream, ctx->T, (const int *)ctx->t_nplus.p,
+    MPL_CUDA(launch_pdl(k_hvp_wh<T, MINB>, grid, 32 * WH_W, 0, ctx->stream, ctx->T, (const int *)ctx->t_nplus.p,
                         (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_hascells.p,
-                        (const float *)ctx->K.p, (const int *)ctx->t_kstart.p, (const float *)owned_mass(ctx),
-                        (const f4 *)u_tile, (f4 *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p));
+                        (const T *)ctx->K.p, (const int *)ctx->t_kstart.p, (const T *)owned_mass(ctx),
+                        (const vec4<T> *)u_tile, (vec4<T> *)Hu_tile, uHu, cgs, cgj, cgthr,
+                        (const DevScalars *)ctx->scalars.p));
     ctx->launches++;
     return MPL_OK;
 }
@@ -1795,13 +1824,23 @@ bool pdl_enabled() {
 // the wz kernels read the tangent in the kz slot order (kz_key); k_linearize writes it that way:
 // 0 = not kz (fp64, other kernels), 1 = compact kz order (default), 2 = fixed 64-slot kz blocks (MPL_KZ_PAD=1;
 // measured 9 % slower at cfg4)
+// fp64 HVP (MPL_HVP_KERNEL64): "wh" (default: k_hvp_wh<double, 3>, one cell's 45 doubles per lane) or
+// "sel" (the MPL_HVP_KERNEL selection, whose fp32-only variants fall back to k_hvp_rp<double, 10>)
+int hvp_variant64() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MPL_HVP_KERNEL64");
+        v = (e && e[0] == 's') ? hvp_variant() : 18;
+    }
+    return v;
+}
 int hvp_kz_layout(int precision) {
     static int pad = -1;
     if (pad < 0) {
         const char *e = getenv("MPL_KZ_PAD");
         pad = (e && e[0] == '1') ? 1 : 0;
     }
-    if (precision != 32) return 0;
+    if (precision != 32) return hvp_variant64() == 18 ? 3 : 0;
     if (hvp_variant() == 16 || hvp_variant() == 17) return 3;  // wh: natural compact order (slot = rank)
     if (hvp_variant() < 9 || hvp_variant() > 15) return 0;
     return pad ? 2 : 1;
@@ -1813,10 +1852,15 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
                       double cgthr) {
     if (ctx->T == 0) return MPL_OK;
     int variant = hvp_variant();
+    if (sizeof(T) == 8) {
+        variant = hvp_variant64();
+        if (variant == 16 || variant == 17 || variant == 18)
+            return launch_wh<T, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);  // 45 doubles per lane
+    }
     if (variant == 16 || variant == 17) {
         if (sizeof(T) == 4)
-            return variant == 16 ? launch_wh<5>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr)
-                                 : launch_wh<4>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+            return variant == 16 ? launch_wh<T, 5>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr)
+                                 : launch_wh<T, 4>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
         variant = 5;
     }
     if (variant >= 9 && variant <= 15) {

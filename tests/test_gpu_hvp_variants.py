@@ -28,18 +28,19 @@ CASES = [
     ({"MPL_HVP_KERNEL": "reg"}, "mix_fp32"),
     ({"MPL_PCG_MAP": "group"}, "mix_fp32"),
     ({"MPL_PDL": "0", "MPL_L2WIN": "0"}, "mix_fp32"),
-    ({"MPL_HVP_KERNEL": "rp10"}, "mix_fp64"),
-    ({"MPL_HVP_KERNEL": "pipe3"}, "mix_fp64"),
+    ({"MPL_HVP_KERNEL64": "sel", "MPL_HVP_KERNEL": "rp10"}, "mix_fp64"),
+    ({"MPL_HVP_KERNEL64": "sel", "MPL_HVP_KERNEL": "pipe3"}, "mix_fp64"),
+    ({"MPL_HVP_KERNEL64": "sel", "MPL_HVP_KERNEL": "rq"}, "mix_fp64"),
     ({"MPL_PCG_MAP": "warp"}, "mix_fp64"),
 ]
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("env,scene", CASES, ids=[
-    "-".join(f"{k[4:].lower()}={v}" for k, v in e.items()) + f"-{s}" for e, s in CASES])
+    "-".join(f"{k[4:].lower()}={v}" for k, v in e.items()) + f"-{s}" for e, s in CASES])  # noqa: E501
 def test_hvp_variant_parity(env, scene):
     e = dict(os.environ)
-    for k in ("MPL_HVP_KERNEL", "MPL_KZ_PAD", "MPL_PCG_MAP", "MPL_PDL", "MPL_L2WIN"):
+    for k in ("MPL_HVP_KERNEL", "MPL_HVP_KERNEL64", "MPL_KZ_PAD", "MPL_PCG_MAP", "MPL_PDL", "MPL_L2WIN"):
         e.pop(k, None)
     e.update(env)
     r = subprocess.run([sys.executable, "-m", "tests._hvp_variant_check", scene], cwd=ROOT, env=e,

@@ -1280,8 +1280,18 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                 MPL_CHECK(d2h(ctx, &sl, slots + launched, sizeof sl, st));
                 MPL_CHECK(d2h(ctx, &neg, &sc->neg_curv, sizeof neg, st));
                 MPL_CHECK(d2h_sync(ctx, st));
-                if (neg || host_stripes(sl.rr) <= thr) done = true;
-                chunk = std::min(chunk * 2, 64);
+                const double rr_now = host_stripes(sl.rr);
+                if (neg || rr_now <= thr) done = true;
+                // next chunk: the iterations the residual's average decay so far predicts to the
+                // threshold (+2), between 4 and 64 (every launch past convergence exits at once on the
+                // device but still costs its launch; every chunk costs a host round trip)
+                int next = std::min(chunk * 2, 64);
+                if (!done && thr > 0.0 && rr_now > 0.0 && rr_now < rr0) {
+                    const double rate = std::log(rr_now / rr0) / (double)launched;  // < 0 per iteration
+                    const double need = std::log(thr / rr_now) / rate;
+                    if (need > 0.0 && need < 1e6) next = std::max(4, std::min(64, (int)std::ceil(need) + 2));
+                }
+                chunk = next;
             }
             hslots.resize(launched + 1);
             int neg = 0, doneit = -1;

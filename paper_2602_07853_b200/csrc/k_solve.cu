@@ -1140,7 +1140,9 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     // (=ph); without it the 390 MB tangent and the vector streams evict them between kernels.  Measured
     // at cfg4 (step ms / in-step HVP us): none 66.1 / 100.3, p 64.6 / 95.7, h 64.5 / 96.4, ph 65.2 /
     // 96.9; both at full hit ratio (74 MB of the 126 MB L2) 71.3 / 103.5.  MPL_L2WIN=0 disables;
-    // after the solve the persisting lines are reset and the set-aside released (MPL_L2RESET=0 keeps them).
+    // After the solve the persisting lines are reset (MPL_L2RESET=0 keeps them); the persisting limit is
+    // set once, not released: cudaDeviceSetLimit synchronises the device, and calling it per solve
+    // serialised the pipelined host copies (e2e 102 -> 119 ms / step at cfg4).
     const char *l2w = getenv("MPL_L2WIN");
     const int l2mode = !l2w ? 2 : l2w[0] == '0' ? 0 : l2w[0] == 'h' ? 1 : (l2w[0] == 'p' && l2w[1] == 'h') ? 3 : 2;
     const char *l2r = getenv("MPL_L2RESET");
@@ -1158,7 +1160,11 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         // only when the window is fully persisting: a partial hit ratio (cfg5: p = 232 MB) halved the
         // HVP's speed in the solve and after it
         if (win > lim || lim == 0) l2on = false;
-        if (l2on) MPL_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim));
+        static size_t limit_set = 0;  // cudaDeviceSetLimit synchronises the device: only on a change
+        if (l2on && limit_set != lim) {
+            MPL_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim));
+            limit_set = lim;
+        }
         if (l2on) {
             cudaStreamAttrValue a = {};
             a.accessPolicyWindow.base_ptr = (void *)(l2mode == 1 ? Hp : p);
@@ -1394,10 +1400,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         cudaStreamAttrValue a = {};
         a.accessPolicyWindow.num_bytes = 0;
         MPL_CUDA(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a));
-        if (l2reset) {
-            MPL_CUDA(cudaCtxResetPersistingL2Cache());
-            MPL_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
-        }
+        if (l2reset) MPL_CUDA(cudaCtxResetPersistingL2Cache());
     }
     S.ms_phase[3] = t_lin;
     S.ms_phase[4] = t_pcg;

@@ -431,7 +431,8 @@ struct mpl_ctx_s {
     // pinned staging for the solver's small device->host control reads (counts, CG scalars): a copy
     // into pageable memory waits behind any large D2H in flight on another stream (measured: 26 ms
     // behind a 1.5 GB readback), a copy into pinned memory does not (0.07 ms)
-    char *pio_buf = nullptr;
+    char *pio_buf = nullptr;  // mapped pinned host memory; pio_dev: its device address
+    char *pio_dev = nullptr;
     size_t pio_cap = 0, pio_used = 0;
     struct PioPend { void *dst; size_t off, n; };
     std::vector<PioPend> pio_pend;
@@ -515,6 +516,19 @@ inline mpl_status d2h_sync(mpl_ctx ctx, cudaStream_t st) {
     ctx->pio_used = 0;
     return MPL_OK;
 }
+// Small device->host reads (counts, CG scalars, slot histories) are written by a kernel straight
+// into mapped pinned host memory instead of a cudaMemcpyAsync: a DMA copy on the compute stream queued
+// behind the pipelined 1.5 GB particle readback on the copy engine (cfg4: the resample's first count
+// read waited ~29 ms for it), a kernel store over the host link does not.
+static __global__ void k_pio_copy(char *__restrict__ dst, const char *__restrict__ src, size_t n) {
+    for (size_t i = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 16; i < n; i += (size_t)gridDim.x * blockDim.x * 16) {
+        if (i + 16 <= n && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+            *reinterpret_cast<uint4 *>(dst + i) = *reinterpret_cast<const uint4 *>(src + i);
+        } else {
+            for (size_t j = i; j < i + 16 && j < n; j++) dst[j] = src[j];
+        }
+    }
+}
 inline mpl_status d2h(mpl_ctx ctx, void *dst, const void *src, size_t n, cudaStream_t st) {
     size_t off = (ctx->pio_used + 15) & ~(size_t)15;
     if (off + n > ctx->pio_cap) {
@@ -523,11 +537,18 @@ inline mpl_status d2h(mpl_ctx ctx, void *dst, const void *src, size_t n, cudaStr
         if (cap < ((size_t)1 << 16)) cap = (size_t)1 << 16;
         if (ctx->pio_buf) cudaFreeHost(ctx->pio_buf);
         ctx->pio_buf = nullptr;
-        MPL_CUDA(cudaMallocHost((void **)&ctx->pio_buf, cap));
+        ctx->pio_dev = nullptr;
+        MPL_CUDA(cudaHostAlloc((void **)&ctx->pio_buf, cap, cudaHostAllocMapped));
+        MPL_CUDA(cudaHostGetDevicePointer((void **)&ctx->pio_dev, ctx->pio_buf, 0));
         ctx->pio_cap = cap;
         off = 0;
     }
-    MPL_CUDA(cudaMemcpyAsync(ctx->pio_buf + off, src, n, cudaMemcpyDeviceToHost, st));
+    if (n) {
+        const size_t chunks = (n + 15) / 16;
+        const unsigned blocks = (unsigned)(chunks < 256 ? 1 : (chunks / 256 < 1024 ? chunks / 256 + 1 : 1024));
+        k_pio_copy<<<blocks, 256, 0, st>>>(ctx->pio_dev + off, static_cast<const char *>(src), n);
+        MPL_CUDA(cudaGetLastError());
+    }
     ctx->pio_pend.push_back({dst, off, n});
     ctx->pio_used = off + n;
     return MPL_OK;

@@ -454,8 +454,10 @@ __device__ __forceinline__ void stretch_slot(const MatP &mp, int k, const T tau[
     E[5] = U[0] * U[6] * em[0] + U[1] * U[7] * em[1] + U[2] * U[8] * em[2];
 }
 
+// 3 CTAs per SM pinned: the kernel waits on its record loads (ncu: long scoreboard 75 %), and at
+// 88 registers ptxas dropped it to 2 CTAs (cfg4 P2Q +0.4 ms); 4 CTAs (64 registers, spills) is no faster
 template <class T, int NM>  // NM >= mp.nmat: register arrays sized for NM material slots
-__global__ void __launch_bounds__(256) k_p2q8(GridP g, MatP mp, const int *__restrict__ coord,
+__global__ void __launch_bounds__(256, 3) k_p2q8(GridP g, MatP mp, const int *__restrict__ coord,
                                               const int *__restrict__ nminus, const int *__restrict__ bstart,
                                               const int *__restrict__ cellof, const T *__restrict__ rec,
                                               T *__restrict__ q_m, T *__restrict__ q_mv, T *__restrict__ q_mG,

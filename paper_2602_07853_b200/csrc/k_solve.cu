@@ -1050,6 +1050,8 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
         // cell phase (ncu at cfg4: barrier stalls 34 %, 16 warps / SM by registers)
         const char *lte = getenv("MPL_LIN_THREADS");
         const int lt = lte ? atoi(lte) : 64;
+        const char *lge = getenv("MPL_LIN_GEN_MINB");
+        const int lin_gen_minb = lge ? atoi(lge) : 12;  // 12 CTAs per SM (NH / water / VM linearisations -7 %)
         bool honly = !ctx->mats.plastic;
         for (int k = 0; k < ctx->mats.nmat; k++) honly = honly && ctx->mats.kind[k] == 0;
         if (honly) {
@@ -1060,6 +1062,7 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
         } else {
             if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY><<<T_, lt, 0, st>>>(LIN_ARGS);
             else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD><<<T_, lt, 0, st>>>(LIN_ARGS);
+            else if (lt == 64 && lin_gen_minb == 12) k_linearize<T, LIN_FULL, false, 12><<<T_, lt, 0, st>>>(LIN_ARGS);
             else if (lt == 64) k_linearize<T, LIN_FULL, false, 8><<<T_, lt, 0, st>>>(LIN_ARGS);
             else k_linearize<T, LIN_FULL><<<T_, lt, 0, st>>>(LIN_ARGS);
         }

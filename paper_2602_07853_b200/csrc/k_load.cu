@@ -85,8 +85,8 @@ __global__ void __launch_bounds__(128) k_n2c(GridP g, const int *__restrict__ np
 }
 
 // per particle (sorted order): interpolate, advect, update F
-template <class T>
-__global__ void k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ skey, const int *__restrict__ pid,
+template <class T, int CMINB = 1>
+__global__ void __launch_bounds__(256, CMINB) k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ skey, const int *__restrict__ pid,
                       const int *__restrict__ nplus,
                       const int *__restrict__ cellof, const T *__restrict__ vG,
                       T *__restrict__ x, T *__restrict__ v, T *__restrict__ F, T *__restrict__ G,
@@ -261,14 +261,28 @@ mpl_status g2p_impl(mpl_ctx ctx, double dt) {
                                      (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p,
                                      (const T *)ctx->q_m.p, (const vec4<T> *)ctx->n_v.p, (T *)ctx->q_vc.p);
         ctx->launches++;
-    if (ctx->np)
-        k_c2p<T><<<nblk(ctx->np, 256), 256, 0, st>>>(ctx->grid, dt, ctx->np, (const int *)ctx->pskey.p,
+    if (ctx->np) {
+        static int cmb = -1;
+        if (cmb < 0) {
+            const char *e = getenv("MPL_C2P_MINB");
+            cmb = e ? atoi(e) : 4;  // 4 CTAs per SM (64 registers): cfg4 G2P 0.94 -> 0.82 ms, cfg3 PPC 64 4.48 -> 3.83
+        }
+        if (cmb == 4) k_c2p<T, 4><<<nblk(ctx->np, 256), 256, 0, st>>>(ctx->grid, dt, ctx->np, (const int *)ctx->pskey.p,
                                                     (const int *)ctx->pid[c].p,
                                                     (const int *)ctx->t_nplus.p, (const int *)ctx->t_cellof.p,
                                                     (const T *)ctx->q_vc.p,
                                                     (T *)ctx->px[c].p, (T *)ctx->pv.p, (T *)ctx->pF[c].p,
                                                     (T *)ctx->pG.p, (const int *)ctx->pmat[c].p,
-                                                    ctx->mats); ctx->launches++;
+                                                    ctx->mats);
+        else k_c2p<T><<<nblk(ctx->np, 256), 256, 0, st>>>(ctx->grid, dt, ctx->np, (const int *)ctx->pskey.p,
+                                                    (const int *)ctx->pid[c].p,
+                                                    (const int *)ctx->t_nplus.p, (const int *)ctx->t_cellof.p,
+                                                    (const T *)ctx->q_vc.p,
+                                                    (T *)ctx->px[c].p, (T *)ctx->pv.p, (T *)ctx->pF[c].p,
+                                                    (T *)ctx->pG.p, (const int *)ctx->pmat[c].p,
+                                                    ctx->mats);
+        ctx->launches++;
+    }
     MPL_CUDA(cudaGetLastError());
     MPL_CUDA(cudaStreamSynchronize(st));
     ctx->resampled = false;  // quadrature state is consumed

@@ -1182,6 +1182,18 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
             MPL_CUDA(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a));
         }
     }
+    // the window is cleared (and the persisting lines reset) however the solve returns
+    struct L2WindowGuard {
+        cudaStream_t st;
+        bool on, reset;
+        ~L2WindowGuard() {
+            if (!on) return;
+            cudaStreamAttrValue a = {};
+            a.accessPolicyWindow.num_bytes = 0;
+            cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
+            if (reset) cudaCtxResetPersistingL2Cache();
+        }
+    } l2guard{st, l2on, l2reset};
     cudaEvent_t e0, e1, h0, h1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -1403,12 +1415,6 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     S.hvp_ms = hsum;
-    if (l2on) {  // give the set-aside L2 back to the other phases
-        cudaStreamAttrValue a = {};
-        a.accessPolicyWindow.num_bytes = 0;
-        MPL_CUDA(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a));
-        if (l2reset) MPL_CUDA(cudaCtxResetPersistingL2Cache());
-    }
     S.ms_phase[3] = t_lin;
     S.ms_phase[4] = t_pcg;
     S.ms_phase[5] = t_ls;

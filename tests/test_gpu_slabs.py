@@ -42,6 +42,8 @@ CASES = {
     "cfg1_R2": (lambda: scenes.cfg1(prestrain=True), [0, 2, 4]),
     "cfg2s_fp32_R3": (lambda: small_cfg2(32), [0, 3, 4, 8]),
     "cfg2s_fp64_R4": (lambda: small_cfg2(64), [0, 3, 4, 5, 8]),
+    # one 4-cell block plane per rank; ranks 0, 1, 6, 7 hold no cells (only ghost / empty slabs)
+    "cfg2s_fp32_R8": (lambda: small_cfg2(32), [0, 1, 2, 3, 4, 5, 6, 7, 8]),
     "mix_fp64_R2": (lambda: two_material(64), [0, 2, 4]),
     "lawmix_fp32_R2": (lambda: two_material(32, (1, 0)), [0, 2, 4]),  # split Neo-Hookean + Hencky
     "watermix_fp64_R2": (lambda: two_material(64, (0, 2)), [0, 2, 4]),  # Hencky + J-based water
@@ -120,6 +122,8 @@ def test_owned_blocks_and_nodes_partition(run):
     # every rank holds only the nodes of its slab (plus the shared plane)
     for r, o in enumerate(run.res):
         ix = o["nid"] // ((run.grid.n[1] + 1) * (run.grid.n[2] + 1))
+        if len(ix) == 0:  # a slab without active nodes (R8: the outer block planes)
+            continue
         assert ix.min() >= 4 * run.cuts[r] and ix.max() <= 4 * run.cuts[r + 1]
 
 
@@ -152,13 +156,16 @@ def test_energy_gradient_hvp_diag(run):
 
 def test_shared_nodes_bitwise_consistent(run):
     """Both copies of an interface node carry identical gradient, HVP and v^{n+1}."""
+    shared = 0
     for r in range(run.R - 1):
         a, b = run.res[r], run.res[r + 1]
+        # neighbours share the active nodes of their cut's node plane (none when a slab is empty)
         common, ia, ib = np.intersect1d(a["nid"], b["nid"], return_indices=True)
-        assert len(common) > 0
+        shared += len(common)
         for key in ("m", "g", "h", "D", "v"):
             assert np.array_equal(a[key][ia], b[key][ib]), key
         assert np.all(a["own"][ia] + b["own"][ib] == 1)
+    assert shared > 0
 
 
 def test_replayed_step(run):

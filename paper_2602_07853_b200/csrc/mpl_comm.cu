@@ -815,9 +815,28 @@ mpl_status redistribute_particles(mpl_ctx ctx) {
     MPL_CHECK(ctx->comm->neighbors(ctx, nullptr, 0, ctx->mig_recv_lo.p, g_lo * RB, ctx->mig_send_hi.p, ng * RB,
                                    nullptr, 0));
     const int64_t ntot = n_own + (int64_t)g_lo;
-    if ((int64_t)cap < ntot) {  // ghosts beyond the headroom: grow keeping content (rare)
-        ctx->err = "ghost layer larger than the particle buffer headroom";
-        return MPL_ERR_OOM;
+    if ((int64_t)cap < ntot) {
+        // more ghosts than the headroom (a slab that starts nearly empty): grow the destination set,
+        // keeping the n_own particles already unpacked into it
+        const int64_t cap2 = ntot + ntot / 4 + 1024;
+        MPL_CUDA(cudaStreamSynchronize(st));
+        auto grow = [&](DevBuf &b, size_t per) -> mpl_status {
+            DevBuf nb;
+            MPL_CHECK(ensure(ctx, nb, (size_t)cap2 * per));
+            if (n_own) MPL_CUDA(cudaMemcpy(nb.p, b.p, (size_t)n_own * per, cudaMemcpyDeviceToDevice));
+            if (b.p) cudaFree(b.p);
+            b = nb;
+            return MPL_OK;
+        };
+        MPL_CHECK(grow(ctx->px[nx], 3 * s));
+        MPL_CHECK(grow(ctx->pF[nx], 9 * s));
+        MPL_CHECK(grow(ctx->pv_alt, 3 * s));
+        MPL_CHECK(grow(ctx->pG_alt, 9 * s));
+        MPL_CHECK(grow(ctx->pvol[nx], s));
+        MPL_CHECK(grow(ctx->pmat[nx], 4));
+        MPL_CHECK(grow(ctx->pid[nx], 4));
+        o = PartOut{ctx->px[nx].p, ctx->pv_alt.p, ctx->pF[nx].p, ctx->pG_alt.p, ctx->pvol[nx].p, (int *)ctx->pmat[nx].p,
+                    (int *)ctx->pid[nx].p};
     }
     if (g_lo)
         k_unpack_recs<T><<<nblk(g_lo, 256), 256, 0, st>>>((int64_t)g_lo, (const char *)ctx->mig_recv_lo.p, n_own, 1, o),

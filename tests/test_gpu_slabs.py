@@ -223,6 +223,42 @@ def test_migration_multistep_matches_one_rank():
         assert rel_l2(got, ref) <= 1e-7, k
 
 
+def test_migration_multistep_eight_ranks():
+    """The 32^3 cfg2 block moving +x at about 0.3 cells per step over 8 one-plane slabs (four of them
+    start empty): particles migrate into empty ranks; five adaptive steps agree with one rank."""
+    sc = small_cfg2(64)
+    sc = dataclasses.replace(sc, v=sc.v + np.array([5.0, 0.0, 0.0]))
+    steps = 5
+    one = mpl.from_scene(sc, 0)
+    for _ in range(steps):
+        one.step(sc.dt, sc.solver)
+    x1, v1, F1, G1 = one.get_particles()
+    one.close()
+    R = 8
+    cuts = np.arange(R + 1, dtype=np.int32)
+    grp = mpl.Group(R)
+
+    def fn(r):
+        ctx = mpl.from_scene_rank(sc, r, R, cuts, device=0, group=grp)
+        n0 = ctx.num_particles()
+        try:
+            for _ in range(steps):
+                ctx.step(sc.dt, sc.solver)
+            return n0, ctx.get_particle_ids(), ctx.get_particles()
+        finally:
+            ctx.close()
+
+    res = run_ranks(R, fn)
+    grp.close()
+    ids = np.concatenate([r[1] for r in res])
+    assert np.array_equal(np.sort(ids), np.arange(sc.n_particles))
+    assert sum(abs(len(r[1]) - r[0]) for r in res) > 0
+    order = np.argsort(ids)
+    for k, ref in enumerate((x1, v1, F1, G1)):
+        got = np.concatenate([r[2][k] for r in res])[order]
+        assert rel_l2(got, ref) <= 1e-7, k
+
+
 def test_collective_error_reaches_every_rank():
     """A particle outside the grid on one rank fails the resample on every rank (no hang)."""
     sc = scenes.cfg1()

@@ -150,39 +150,17 @@ def run_ours(args):
     sel = None
     solver = sc.solver
     stream = torch.cuda.Stream(device=local)
-    mode, slab_err = "1 GPU", None
+    mode = "1 GPU"
     if ws > 1:
         # slab decomposition: rank r owns the x-slab [cuts[r], cuts[r+1]) of 4-cell blocks; the library's
-        # own NCCL communicator carries the halo sums, PCG allreduces and particle migration.  The first
-        # step doubles as a probe of that communicator: if any rank fails, every rank falls back to
-        # independent full-scene replicas (weak scaling) and the line says so.
-        ctx = None
-        try:
-            nccl_id = pdist.share_nccl_id()
-            cuts = pdist.agree_cuts(mpl.slab_cuts(sc, ws))
-            ctx = mpl.from_scene_rank(sc, rank, ws, cuts, device=local, nccl_id=nccl_id)
-            sel = mpl.slab_select(sc, cuts, rank)
-            ctx.set_stream(stream.cuda_stream)
-            ctx.step(sc.dt, solver)
-            ok = 1
-        except Exception as e:  # noqa: BLE001 - reported in the JSON line
-            ok, slab_err = 0, f"{type(e).__name__}: {e}"[:300]
-        flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        errs = [None] * ws
-        dist.all_gather_object(errs, slab_err)
-        slab_err = next((e for e in errs if e), slab_err)
-        if int(flag.item()) == 1:
-            mode = "slabs"
-        else:
-            if ctx is not None:
-                try:
-                    ctx.close()
-                except Exception:  # noqa: BLE001
-                    pass
-            mode, sel, cuts = "replicas", None, None
-            ctx = mpl.from_scene(sc, device=local)
-            ctx.set_stream(stream.cuda_stream)
+        # own NCCL communicator carries the halo sums, PCG allreduces and particle migration.  A failure
+        # on any rank raises (non-zero exit): there is no silent fallback to replicas.
+        nccl_id = pdist.share_nccl_id()
+        cuts = pdist.agree_cuts(mpl.slab_cuts(sc, ws))
+        ctx = mpl.from_scene_rank(sc, rank, ws, cuts, device=local, nccl_id=nccl_id)
+        sel = mpl.slab_select(sc, cuts, rank)
+        ctx.set_stream(stream.cuda_stream)
+        mode = "slabs"
     else:
         cuts = None
         ctx = mpl.from_scene(sc, device=local)
@@ -235,6 +213,7 @@ def run_ours(args):
     # e2e: the same metric through the C ABI with HOST buffers (H2D of particles, D2H of results)
     e2e = None if args.no_e2e else run_e2e(ctx, sc, solver, args, sel, ws)
     clocks = clk.summary()
+    vec_ev = os.environ.get("MPL_VEC_EVENTS", "0") in ("1", "2")
     result = {
         "metric": "HVP GDOF/s (matrix-free incremental-potential Hessian-vector product inside Newton-PCG)",
         "value": round(gdofs, 3),
@@ -244,7 +223,7 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 3),
         "higher_is_better": True,
-        "scaling": "weak" if mode == "replicas" else "strong",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f32" if args.precision == 32 else "f64",
         "data": "synthetic (seeded scene generator, paper_2602_07853_b200/scenes.py)",
@@ -254,8 +233,7 @@ def run_ours(args):
             "active_nodes": int(nodes_all), "free_dofs": int(3 * n_free_all),
             "parallelism": "1 GPU" if ws == 1 else
             (f"x-slab decomposition over {ws} GPUs (cuts {list(map(int, cuts))} in 4-cell blocks; "
-             "halo sums + allreduces on the library's NCCL communicator)" if mode == "slabs" else
-             f"{ws} independent full-scene replicas (slab path failed: {slab_err})"),
+             "halo sums + allreduces on the library's NCCL communicator)"),
             "l2": "inputs larger than L2 (tangent stream > 126 MB per HVP)",
             "step": "full implicit step: resample + Newton-PCG + G2P",
         },
@@ -271,17 +249,27 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": int(nbytes), "pct_of_8TBps": round(achieved / 8000.0, 4)},
         "e2e": e2e,
         "gpu_launches": int(launches),
+        "converged": [bool(s["converged"]) for s in stats],
+        "all_converged": all(bool(s["converged"]) for s in stats),
+        "grad_rel": [s["grad_norm"] / s["grad_norm0"] if s["grad_norm0"] > 0 else 0.0 for s in stats],
+        "ls_halvings": [s["ls_halvings"] for s in stats],
         "phase_ms": {"resample": round(statistics.mean(s["ms_phase"][0] for s in stats), 3),
                      "linearize": round(statistics.mean(s["ms_phase"][3] for s in stats), 3),
                      "pcg": round(statistics.mean(s["ms_phase"][4] for s in stats), 3),
-                     "pcg_vector_kernels": round(statistics.mean(s["ms_phase"][1] for s in stats), 3),
-                     "pcg_update2": round(statistics.mean(s["ms_phase"][2] for s in stats), 3),
+                     # measured only with MPL_VEC_EVENTS=1 (events around every vector kernel)
+                     "pcg_vector_kernels": round(statistics.mean(s["ms_phase"][1] for s in stats), 3) if vec_ev else None,
+                     "pcg_update2": round(statistics.mean(s["ms_phase"][2] for s in stats), 3) if vec_ev else None,
                      "line_search": round(statistics.mean(s["ms_phase"][5] for s in stats), 3),
                      "g2p": round(statistics.mean(s["ms_phase"][6] for s in stats), 3)},
         "clocks": clocks,
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(sc, args)
+    if not result["all_converged"]:
+        # a step that hit newton_max is not a converged implicit step: say so in the line and on stderr
+        result["invalid"] = "a timed step did not converge (newton_max reached); see grad_rel"
+        if rank == 0:
+            print("bench: WARNING: " + result["invalid"], file=sys.stderr, flush=True)
     if rank == 0:
         print(json.dumps(result), flush=True)
     ctx.close()
@@ -442,12 +430,15 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--config", default=None,
+                    help="default: cfg4 on one GPU (the 256^3 headline), cfg5B (the 512^3 scaling config) for N > 1")
     ap.add_argument("--precision", type=int, default=32)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
+    if args.config is None:
+        args.config = "cfg4" if int(os.environ.get("WORLD_SIZE", "1")) <= 1 else "cfg5B"
     if args.impl == "reference":
         run_reference(args)
     else:

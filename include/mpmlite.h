@@ -124,6 +124,9 @@ typedef struct {
     double ms_phase[8];   /* 0 resample, 1 PCG vector kernels (MPL_VEC_EVENTS=1), 2 explicit update, 3 linearize, 4 PCG, 5 line search, 6 G2P, 7 total (ms) */
     int64_t n_cells, n_nodes, n_free_nodes; /* quadrature points, active nodes, free (non-Dirichlet) nodes */
     int64_t n_launches;   /* CUDA kernels launched by the library during this call                */
+    double grad_norms[MPL_MAX_NEWTON_LOG]; /* ||g_free|| at the start of Newton iteration k (k < newton_iters),
+                                              then at the returned iterate (index newton_iters) if measured */
+    double alphas[MPL_MAX_NEWTON_LOG];     /* accepted line-search step of Newton iteration k            */
 } mpl_solve_stats;
 
 /* ---- context ------------------------------------------------------------------------------ */
@@ -203,7 +206,9 @@ MPL_API mpl_status mpl_get_nodes(mpl_ctx ctx, int32_t *ijk, void *m, void *v_n, 
 /* sorted x-major linear ids (bx*NBy + by)*NBz + bz of the 4^3 cell blocks touched by any particle
  * stencil (structural; bit-exact).  n_blocks entries. */
 MPL_API mpl_status mpl_get_active_blocks(mpl_ctx ctx, int64_t *ids);
-/* per-particle base cell floor((x - origin)/dx - 1/2) (n*3 int32, input order; bit-exact). */
+/* per-particle base cell floor((x - origin)/dx - 1/2) the last mpl_resample binned each particle into
+ * (n*3 int32, input order; bit-exact).  Valid between mpl_resample and mpl_transfer_to_particles (which
+ * moves the particles): MPL_ERR_STATE otherwise. */
 MPL_API mpl_status mpl_get_particle_cells(mpl_ctx ctx, int32_t *base_ijk);
 /* quadrature state (n_cells entries, canonical cell order): ijk (n*3), m_c, v_c (n*3), G_c (n*9),
  * and per material k: V_{c,k} (nmat*n), tau_{c,k} (nmat*n*9), S_{c,k} (nmat*n*9).  NULL skips. */

@@ -32,9 +32,10 @@ MAXMAT = 8
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle (gcc -O2 -ffp-contract=off, no fast-math)."""
+    """Compile the oracle (gcc -O2 -ffp-contract=off, no fast-math, -fopenmp: results are identical at
+    any OMP_NUM_THREADS, see the header of mpl_oracle.c)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
                                "-o", _LIB + ".tmp", _SRC, "-lm"])
         os.replace(_LIB + ".tmp", _LIB)
     return _LIB

@@ -17,6 +17,14 @@
  * All arrays are DENSE over the grid (cells x-major, nodes x-major); a "window"
  * of a large scene is expressed by a smaller grid with a shifted origin.
  * Corner / stencil offsets o in {0,1}^3 are enumerated x-major: o = 4 ox + 2 oy + oz.
+ *
+ * Threads (OpenMP, optional): the sums over cells that scatter into nodes (gradient, HVP,
+ * Jacobi diagonal, explicit force) visit the cells colour by colour, colour = (ci, cj, ck) mod 2,
+ * so two cells of one colour never share a node and a colour's cells can run concurrently; the
+ * energy and the dot products add fixed per-slice partial sums in a fixed order.  Every result is
+ * therefore the same bit for bit at any thread count (OMP_NUM_THREADS); without -fopenmp the
+ * pragmas are ignored and the same loops run serially.  Only the order of the terms of each sum
+ * differs from a plain x-major loop; the terms are the ones the cited definitions state.
  */
 #include <math.h>
 #include <stdint.h>
@@ -561,6 +569,7 @@ void orc_stretch_all(const orc_grid *g, int32_t nmat, const orc_material *mats, 
     for (int k = 0; k < nmat; k++) {
         double mu, lam;
         lame(&mats[k], &mu, &lam);
+#pragma omp parallel for schedule(static)
         for (int64_t c = 0; c < nc; c++) {
             double *S = S_ck + ((int64_t)k * nc + c) * 9;
             if (V_ck[(int64_t)k * nc + c] != 0.0) {
@@ -608,6 +617,10 @@ double orc_energy(const orc_problem *P, const double *v) {
         for (int a = 0; a < 3; a++) d2 += (v[3 * i + a] - P->vhat[3 * i + a]) * (v[3 * i + a] - P->vhat[3 * i + a]);
         E += 0.5 * P->m_i[i] * d2;
     }
+    /* elastic part: one partial sum per x-slice of cells, added in slice order */
+    double *part = calloc((size_t)g->n[0], sizeof(double));
+    int inverted = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(| : inverted)
     for (int ci = 0; ci < g->n[0]; ci++)
         for (int cj = 0; cj < g->n[1]; cj++)
             for (int ck = 0; ck < g->n[2]; ck++) {
@@ -616,16 +629,18 @@ double orc_energy(const orc_problem *P, const double *v) {
                 double Gc[9], A[9];
                 cell_G(P, v, ci, cj, ck, Gc);
                 for (int a = 0; a < 9; a++) A[a] = ((a % 4 == 0) ? 1.0 : 0.0) + P->dt * Gc[a];
-                if (!(mat_det(A) > 0.0)) return INFINITY; /* amb-21 */
+                if (!(mat_det(A) > 0.0)) { inverted = 1; continue; } /* amb-21 */
                 for (int k = 0; k < P->nmat; k++) {
                     double V = P->V_ck[(int64_t)k * nc + c];
                     if (V == 0.0) continue;
                     double F[9];
                     mat_mul(A, P->S_ck + ((int64_t)k * nc + c) * 9, F); /* Eq. Ftrial-rotfree */
-                    E += V * law_psi(&P->mats[k], F);
+                    part[ci] += V * law_psi(&P->mats[k], F);
                 }
             }
-    return E;
+    for (int ci = 0; ci < g->n[0]; ci++) E += part[ci];
+    free(part);
+    return inverted ? INFINITY : E;
 }
 
 /* Per-cell, per-slot gradient block: dt V tau(F) A^{-T}  (== dt V P(F) S^T, amb-3) */
@@ -718,9 +733,11 @@ void orc_gradient(const orc_problem *P, const double *v, double *grad) {
     for (int64_t i = 0; i < nn; i++)
         for (int a = 0; a < 3; a++)
             grad[3 * i + a] = P->m_i[i] != 0.0 ? P->m_i[i] * (v[3 * i + a] - P->vhat[3 * i + a]) : 0.0;
-    for (int ci = 0; ci < g->n[0]; ci++)
-        for (int cj = 0; cj < g->n[1]; cj++)
-            for (int ck = 0; ck < g->n[2]; ck++) {
+    for (int col = 0; col < 8; col++) /* cells of one colour share no node */
+#pragma omp parallel for collapse(2) schedule(dynamic, 1)
+    for (int ci = (col >> 2) & 1; ci < g->n[0]; ci += 2)
+        for (int cj = (col >> 1) & 1; cj < g->n[1]; cj += 2)
+            for (int ck = col & 1; ck < g->n[2]; ck += 2) {
                 int64_t c = cid(g, ci, cj, ck);
                 if (P->m_c[c] == 0.0) continue;
                 double A[9], Pc[9] = {0};
@@ -749,9 +766,11 @@ void orc_hvp(const orc_problem *P, const double *v, const double *u, double *Hu)
     int64_t nn = nnodes(g), nc = ncells(g);
     for (int64_t i = 0; i < nn; i++)
         for (int a = 0; a < 3; a++) Hu[3 * i + a] = P->m_i[i] != 0.0 ? P->m_i[i] * u[3 * i + a] : 0.0;
-    for (int ci = 0; ci < g->n[0]; ci++)
-        for (int cj = 0; cj < g->n[1]; cj++)
-            for (int ck = 0; ck < g->n[2]; ck++) {
+    for (int col = 0; col < 8; col++) /* cells of one colour share no node */
+#pragma omp parallel for collapse(2) schedule(dynamic, 1)
+    for (int ci = (col >> 2) & 1; ci < g->n[0]; ci += 2)
+        for (int cj = (col >> 1) & 1; cj < g->n[1]; cj += 2)
+            for (int ck = col & 1; ck < g->n[2]; ck += 2) {
                 int64_t c = cid(g, ci, cj, ck);
                 if (P->m_c[c] == 0.0) continue;
                 double A[9], dG[9], Pc[9] = {0};
@@ -780,9 +799,11 @@ void orc_diag(const orc_problem *P, const double *v, double *D) {
     int64_t nn = nnodes(g), nc = ncells(g);
     for (int64_t i = 0; i < nn; i++)
         for (int a = 0; a < 3; a++) D[3 * i + a] = P->m_i[i];
-    for (int ci = 0; ci < g->n[0]; ci++)
-        for (int cj = 0; cj < g->n[1]; cj++)
-            for (int ck = 0; ck < g->n[2]; ck++) {
+    for (int col = 0; col < 8; col++) /* cells of one colour share no node */
+#pragma omp parallel for collapse(2) schedule(dynamic, 1)
+    for (int ci = (col >> 2) & 1; ci < g->n[0]; ci += 2)
+        for (int cj = (col >> 1) & 1; cj < g->n[1]; cj += 2)
+            for (int ck = col & 1; ck < g->n[2]; ck += 2) {
                 int64_t c = cid(g, ci, cj, ck);
                 if (P->m_c[c] == 0.0) continue;
                 double A[9];
@@ -829,10 +850,20 @@ typedef struct {
 } orc_solve_stats;
 
 static double dotf(int64_t n, const uint8_t *fr, const double *a, const double *b) {
+    /* fixed chunks of nodes, partial sums added in chunk order */
+    const int64_t CH = 4096, nch = (n + CH - 1) / CH;
+    double *part = calloc((size_t)(nch > 0 ? nch : 1), sizeof(double));
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < nch; q++) {
+        double s = 0;
+        for (int64_t i = q * CH; i < n && i < (q + 1) * CH; i++)
+            if (fr[i])
+                for (int c = 0; c < 3; c++) s += a[3 * i + c] * b[3 * i + c];
+        part[q] = s;
+    }
     double s = 0;
-    for (int64_t i = 0; i < n; i++)
-        if (fr[i])
-            for (int c = 0; c < 3; c++) s += a[3 * i + c] * b[3 * i + c];
+    for (int64_t q = 0; q < nch; q++) s += part[q];
+    free(part);
     return s;
 }
 
@@ -866,6 +897,7 @@ static int pcg(const orc_problem *P, const double *v, const double *grad, const 
             break;
         }
         double alpha = rz / pHp;
+#pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < nn * 3; i++)
             if (fr[i / 3]) {
                 x[i] += alpha * p[i];
@@ -874,10 +906,12 @@ static int pcg(const orc_problem *P, const double *v, const double *grad, const 
         it++;
         double rn = sqrt(dotf(nn, fr, r, r));
         if (!fixed && rn <= eps * r0) break;
+#pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < nn * 3; i++) z[i] = fr[i / 3] ? r[i] / D[i] : 0.0;
         double rz_new = dotf(nn, fr, r, z);
         double beta = rz_new / rz;
         rz = rz_new;
+#pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < nn * 3; i++) p[i] = fr[i / 3] ? z[i] + beta * p[i] : 0.0;
     }
 done:
@@ -1014,6 +1048,7 @@ int64_t orc_plastic_update(const orc_problem *P, const double *v, const double *
         if (m->kind != 0 || !(m->yield_stress > 0.0)) continue;
         double mu, lam;
         lame(m, &mu, &lam);
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : nproj)
         for (int ci = 0; ci < g->n[0]; ci++)
             for (int cj = 0; cj < g->n[1]; cj++)
                 for (int ck = 0; ck < g->n[2]; ck++) {
@@ -1058,6 +1093,7 @@ int64_t orc_g2p_mat(const orc_grid *g, double dt, const double *m_c, const doubl
                     int32_t clip) {
     int64_t nc = ncells(g);
     double *vc = calloc(nc * 3, sizeof(double)), *Gc = calloc(nc * 9, sizeof(double));
+#pragma omp parallel for schedule(static)
     for (int ci = 0; ci < g->n[0]; ci++)
         for (int cj = 0; cj < g->n[1]; cj++)
             for (int ck = 0; ck < g->n[2]; ck++) {
@@ -1121,9 +1157,11 @@ void orc_explicit_force(const orc_grid *g, int32_t nmat, const double *m_c, cons
                         const double *tau_ck, double *f) {
     int64_t nn = nnodes(g), nc = ncells(g);
     memset(f, 0, sizeof(double) * nn * 3);
-    for (int ci = 0; ci < g->n[0]; ci++)
-        for (int cj = 0; cj < g->n[1]; cj++)
-            for (int ck = 0; ck < g->n[2]; ck++) {
+    for (int col = 0; col < 8; col++) /* cells of one colour share no node */
+#pragma omp parallel for collapse(2) schedule(dynamic, 1)
+    for (int ci = (col >> 2) & 1; ci < g->n[0]; ci += 2)
+        for (int cj = (col >> 1) & 1; cj < g->n[1]; cj += 2)
+            for (int ck = col & 1; ck < g->n[2]; ck += 2) {
                 int64_t c = cid(g, ci, cj, ck);
                 if (m_c[c] == 0.0) continue;
                 double Vt[9] = {0};

@@ -285,6 +285,7 @@ mpl_status g2p_impl(mpl_ctx ctx, double dt) {
     }
     MPL_CUDA(cudaGetLastError());
     MPL_CUDA(cudaStreamSynchronize(st));
+    ctx->vg_unsorted = false;  // k_c2p wrote v, G in the sorted order
     ctx->resampled = false;  // quadrature state is consumed
     ctx->linearized = false;
     ctx->solved = false;
@@ -294,6 +295,7 @@ mpl_status g2p_impl(mpl_ctx ctx, double dt) {
 template <class T>
 mpl_status export_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G) {
     if (multi(ctx)) return export_owned_particles<T>(ctx, x, v, F, G, nullptr, nullptr);
+    MPL_CHECK(sync_vg_order<T>(ctx));
     cudaStream_t st = ctx->stream;
     const int64_t np = ctx->np;
     const int c = ctx->cur;
@@ -317,6 +319,7 @@ mpl_status export_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G) {
 template <class T>
 mpl_status export_particles_async(mpl_ctx ctx, void *x, void *v, void *F, void *G) {
     MPL_CHECK(io_streams(ctx));
+    MPL_CHECK(sync_vg_order<T>(ctx));
     cudaStream_t st = ctx->stream, cs = ctx->rstream;
     const int64_t np = ctx->np;
     const int c = ctx->cur;

@@ -324,6 +324,20 @@ __global__ void k_scatter(GridP g, MatP mp, int64_t np, const int *__restrict__ 
     keyo[d] = k;
 }
 
+// v / G into the sorted order of the last k_scatter (see mpl_ctx_s::vg_unsorted)
+template <class T>
+__global__ void k_vg_to_sorted(int64_t np, const int *__restrict__ key, const int *__restrict__ rank,
+                               const int *__restrict__ bstart, const T *__restrict__ v, const T *__restrict__ G,
+                               T *__restrict__ vo, T *__restrict__ Go) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= np) return;
+    const int64_t d = bstart[key[p]] + rank[p];
+#pragma unroll
+    for (int a = 0; a < 3; a++) vo[3 * d + a] = v[3 * p + a];
+#pragma unroll
+    for (int a = 0; a < 9; a++) Go[9 * d + a] = G[9 * p + a];
+}
+
 // ---- structural cell masks: cell active iff some base-cell bucket in cell - {0,1}^3 is non-empty
 __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, const int *__restrict__ nminus,
                             const int *__restrict__ bcount, const int *__restrict__ hascells,
@@ -688,6 +702,7 @@ mpl_status import_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v
     ctx->np = n;
     ctx->np_own = n;
     ctx->cur = 0;
+    ctx->vg_unsorted = false;
     size_t s = sizeof(T);
     MPL_CHECK(ensure(ctx, ctx->px[0], n * 3 * s));
     MPL_CHECK(ensure(ctx, ctx->px[1], n * 3 * s));
@@ -716,6 +731,30 @@ mpl_status import_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v
     MPL_CHECK(d2h_sync(ctx, st));
     return MPL_OK;
 }
+
+// Bring v / G into the order of x / F after a resample whose G2P has not run (mpl_ctx_s::vg_unsorted).
+template <class T>
+mpl_status sync_vg_order(mpl_ctx ctx) {
+    if (!ctx->vg_unsorted) return MPL_OK;
+    const int64_t np = ctx->np;
+    const size_t s = sizeof(T);
+    cudaStream_t st = ctx->stream;
+    MPL_CHECK(ensure(ctx, ctx->pv_alt, np * 3 * s + 16));
+    MPL_CHECK(ensure(ctx, ctx->pG_alt, np * 9 * s + 16));
+    if (np) {
+        k_vg_to_sorted<T><<<nblk(np, 256), 256, 0, st>>>(np, (const int *)ctx->pkey.p, (const int *)ctx->prank.p,
+                                                        (const int *)ctx->t_bstart.p, (const T *)ctx->pv.p,
+                                                        (const T *)ctx->pG.p, (T *)ctx->pv_alt.p, (T *)ctx->pG_alt.p);
+        ctx->launches++;
+        MPL_CUDA(cudaGetLastError());
+    }
+    std::swap(ctx->pv, ctx->pv_alt);
+    std::swap(ctx->pG, ctx->pG_alt);
+    ctx->vg_unsorted = false;
+    return MPL_OK;
+}
+template mpl_status sync_vg_order<float>(mpl_ctx);
+template mpl_status sync_vg_order<double>(mpl_ctx);
 
 // ---- pipelined particle input (mpl_stage_particles) ------------------------------------------------
 mpl_status io_streams(mpl_ctx ctx) {
@@ -779,6 +818,7 @@ mpl_status adopt_staged(mpl_ctx ctx) {
     std::swap(ctx->pmat[c], ctx->smat);
     ctx->np = n;
     ctx->np_own = n;
+    ctx->vg_unsorted = false;  // the adopted set is in input order throughout
     const int nx = 1 - c;
     MPL_CHECK(ensure(ctx, ctx->px[nx], n * 3 * s));
     MPL_CHECK(ensure(ctx, ctx->pF[nx], n * 9 * s));
@@ -813,6 +853,7 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     const int N = g.nb[0] * g.nb[1] * g.nb[2];
     ctx->dense_n = N;
     ctx->dt = dt;
+    MPL_CHECK(sync_vg_order<T>(ctx));  // a resample after a resample (no G2P in between)
     MPL_CHECK(redistribute_particles<T>(ctx));  // slab ranks: migration + ghosts (no-op on one rank)
     DBG_GUARDS("after redistribute");
     const int64_t np = ctx->np;
@@ -934,6 +975,7 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
             (int *)ctx->pskey.p, (T *)ctx->prec.p, sc); ctx->launches++;
     DBG_GUARDS("resample #6");
     ctx->cur = nx;
+    ctx->vg_unsorted = np > 0;  // v / G follow order c until G2P (or sync_vg_order) rewrites them
 #ifdef MPL_DEBUG
     {
         int bsum = 0;
@@ -978,6 +1020,7 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     }
     if (agree(ctx, bad) != MPL_OK) {
         ctx->cur = c;  // particle state unchanged
+        ctx->vg_unsorted = false;
         return bad != MPL_OK ? bad : MPL_ERR_STATE;
     }
     ctx->C = Cpad;

@@ -1242,6 +1242,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         const double gn = sqrt(rr0);
         if (k == 0) S.grad_norm0 = gn;
         S.grad_norm = gn;
+        if (k < MPL_MAX_NEWTON_LOG) S.grad_norms[k] = gn;
         if (!fixed && gn <= cfg->newton_rtol * S.grad_norm0) {
             S.converged = 1;
             break;
@@ -1378,6 +1379,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         MPL_CUDA(cudaEventSynchronize(e1));
         t_ls += elapsed(e0, e1);
         if (k < MPL_MAX_NEWTON_LOG) S.ls_iters[k] = h;
+        if (k < MPL_MAX_NEWTON_LOG) S.alphas[k] = alpha;
         S.ls_halvings += h;
         std::swap(v, vt);
         std::swap(ctx->n_v, ctx->n_vt);
@@ -1392,6 +1394,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         MPL_CHECK(d2h(ctx, g2, sc->gnorm2, sizeof g2, st));
         MPL_CHECK(d2h_sync(ctx, st));
         S.grad_norm = sqrt(host_stripes(g2));
+        if (kmax < MPL_MAX_NEWTON_LOG) S.grad_norms[kmax] = S.grad_norm;
         if (S.grad_norm <= cfg->newton_rtol * S.grad_norm0) S.converged = 1;
     }
     MPL_CHECK(energy_at<T>(ctx, v, &S.energy));

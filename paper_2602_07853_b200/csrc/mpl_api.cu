@@ -504,19 +504,16 @@ mpl_status mpl_get_active_blocks(mpl_ctx ctx, int64_t *ids) {
 mpl_status mpl_get_particle_cells(mpl_ctx ctx, int32_t *base_ijk) {
     ApiLock api_lock_;
     if (!ctx || !base_ijk) return MPL_ERR_INVALID_ARG;
-    MPL_CHECK(need(ctx, ctx->have_particles, "mpl_set_particles first"));
+    // the base cells the last resample binned the particles into (its sorted keys): valid from
+    // mpl_resample until mpl_transfer_to_particles moves the particles
+    MPL_CHECK(need(ctx, ctx->resampled, "mpl_resample first (base cells of the last resample, before the transfer)"));
     MPL_CHECK(set_device(ctx));
     if (multi(ctx)) return DISPATCH(ctx, export_owned_particles, nullptr, nullptr, nullptr, nullptr, nullptr, base_ijk);
-    // recompute from the current positions (sorted) and unsort via ids
     const int64_t np = ctx->np;
-    std::vector<int> id(np);
-    std::vector<char> x(np * 3 * (ctx->precision == 64 ? 8 : 4));
+    std::vector<int> id(np), key(np);
     const int c = ctx->cur;
     MPL_CUDA(cudaMemcpy(id.data(), ctx->pid[c].p, np * 4, cudaMemcpyDeviceToHost));
-    MPL_CUDA(cudaMemcpy(x.data(), ctx->px[c].p, x.size(), cudaMemcpyDeviceToHost));
-    // NOTE: this getter reports the binning rule of the device kernel (k_bin_flags); it reads the
-    // device-computed base cells through the sorted keys so the check stays bit-exact.
-    std::vector<int> key(np);
+    // the device-computed base cells (k_bin_flags -> sorted keys tile * 64 + local cell), unsorted by id
     MPL_CUDA(cudaMemcpy(key.data(), ctx->pskey.p, np * 4, cudaMemcpyDeviceToHost));
     std::vector<int> coord((size_t)ctx->T * 3);
     MPL_CUDA(cudaMemcpy(coord.data(), ctx->t_coord.p, coord.size() * 4, cudaMemcpyDeviceToHost));

@@ -860,6 +860,7 @@ mpl_status redistribute_particles(mpl_ctx ctx) {
 
 template <class T>
 mpl_status export_owned_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G, int32_t *ids, int32_t *base_ijk) {
+    if (v || G) MPL_CHECK(sync_vg_order<T>(ctx));
     cudaStream_t st = ctx->stream;
     const int64_t n = ctx->np;
     const int c = ctx->cur;

@@ -457,6 +457,12 @@ struct mpl_ctx_s {
     int cur = 0;  // which particle buffer set is current
     DevBuf px[2], pF[2], pv, pG, pvol[2], pmat[2], pid[2];
     DevBuf pkey, prank, prec, pbase, pskey;  // per-particle scratch; pskey/prec in sorted order
+    // k_scatter sorts x, F, vol, mat, pid (ping-pong sets) but not v and G: P2Q reads them through the
+    // record and G2P rewrites them in sorted order.  Between the two, v / G still follow the previous
+    // order; vg_unsorted records that, and sync_vg_order (a gather through the resample's sort map
+    // pkey / prank / t_bstart) restores one order before anything else reads v / G (a second resample,
+    // mpl_get_particles*).
+    bool vg_unsorted = false;
 
     // tiles
     int T = 0;
@@ -668,6 +674,7 @@ template <class T> mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *
                                          const CGSlot *cgs, int cgj, double cgthr);
 template <class T> mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *st);
 template <class T> mpl_status g2p_impl(mpl_ctx ctx, double dt);
+template <class T> mpl_status sync_vg_order(mpl_ctx ctx);
 template <class T> mpl_status explicit_impl(mpl_ctx ctx);
 
 template <class T> mpl_status stage_particles(mpl_ctx ctx, int64_t n, const void *x, const void *v, const void *F,

@@ -211,3 +211,61 @@ def test_pipelined_io_matches_synchronous():
     for i in range(3):
         for got, want in zip(outs[i], ref[i]):
             assert rel_l2(got, want) <= 1e-12
+
+
+def _affine_scene():
+    """A pre-strained 16^3 block of a 32^3 grid with the cfg2 smooth field (v, G_p = grad v non-zero),
+    particles given in a shuffled order so the resample's sort moves every array."""
+    n = 32
+    cells = scenes.cells_box([8, 8, 8], [24, 24, 24])
+    x = scenes.stratified(cells, n, 2, seed=0)
+    perm = np.random.default_rng(7).permutation(x.shape[0])
+    x = x[perm]
+    v, G = scenes.eval_smooth_field(x, scenes.smooth_field(2))
+    return scenes._assemble("affine", 64, n, 2e-3, [scenes.Material(1e5, 0.4, 1000.0)], x, v,
+                            scenes._prestrain(x.shape[0], 3), G, np.zeros(x.shape[0], np.int32), 8, [],
+                            scenes.SolverCfg(eps_cg=1e-10, eps_newton=1e-10), 1)
+
+
+def test_resample_twice_equals_once():
+    """mpl_resample sorts x / F; v / G are brought into the same order before anything else
+    reads them, so resample -> resample -> step equals resample -> step, and mpl_get_particles right
+    after a resample returns the input state."""
+    sc = _affine_scene()
+    a = mpl.from_scene(sc, 0)
+    a.resample(sc.dt)
+    x, v, F, G = a.get_particles()  # between resample and transfer: input order, v / G unscrambled
+    assert np.array_equal(x, sc.x) and np.array_equal(v, sc.v) and np.array_equal(F, sc.F) and np.array_equal(G, sc.G)
+    a.resample(sc.dt)  # the recovery path of the header (mpl_resample again)
+    sa = a.newton_step(sc.solver)
+    va = a.get_velocity()
+    a.transfer_to_particles(sc.dt)
+    pa = a.get_particles()
+    a.close()
+    b = mpl.from_scene(sc, 0)
+    b.resample(sc.dt)
+    sb = b.newton_step(sc.solver, sa["newton_iters"], sa["cg_iters"], sa["ls_iters"])
+    vb = b.get_velocity()
+    b.transfer_to_particles(sc.dt)
+    pb = b.get_particles()
+    b.close()
+    assert sb["cg_iters"] == sa["cg_iters"]
+    assert rel_l2(va, vb) <= 1e-12
+    for got, want in zip(pa, pb):
+        assert rel_l2(got, want) <= 1e-12
+
+
+def test_particle_cells_only_between_resample_and_transfer():
+    """mpl_get_particle_cells reports the last resample's binning; after the transfer moved the particles it
+    is a call-order error (it used to return the pre-advection cells)."""
+    sc = _affine_scene()
+    ctx = mpl.from_scene(sc, 0)
+    ctx.resample(sc.dt)
+    grid = oracle.Grid(sc.n, sc.dx, sc.origin)
+    assert np.array_equal(ctx.get_particle_cells(), oracle.base_cells(grid, sc.x))
+    ctx.newton_step(sc.solver)
+    ctx.transfer_to_particles(sc.dt)
+    with pytest.raises(mpl.MplError) as e:
+        ctx.get_particle_cells()
+    assert e.value.code == 2  # MPL_ERR_STATE
+    ctx.close()

@@ -278,3 +278,45 @@ def test_stiff_limit_dt2(orc):
         errs.append(np.linalg.norm((vN - vex)[act]))
     ratios = [errs[i] / errs[i + 1] for i in range(3)]
     assert all(r > 3.0 for r in ratios) and 3.6 < ratios[-1] < 4.4, ratios  # log2 slope -> 2
+
+
+# ---- orc_dirichlet (amb-9: node i is prescribed when lo <= x_i <= hi on every axis) -------------------
+def test_dirichlet_floor_worked_example():
+    """Hand count on an 8^3 grid (dx = 1/8, exact in binary): the cfg4 / cfg5 floor "nodes with y <= 3 dx"
+    prescribes exactly the node planes j = 0, 1, 2, 3 (9 x 4 x 9 = 324 nodes; the plane at y = 3 dx is
+    included, y = 4 dx is not); nodes there with m_i = 0 are no DOF either; the box velocity is returned
+    for every prescribed node, 0 elsewhere."""
+    import oracle
+    grid = oracle.Grid((8, 8, 8), 1 / 8)
+    inf = float("inf")
+    boxes = [scenes.DirichletBox((-inf, -inf, -inf), (inf, 3 / 8, inf), (0.5, -1.0, 2.0))]
+    m_i = np.ones(grid.nnodes)
+    m_i[oracle.Grid((8, 8, 8), 1 / 8).node_ijk()[:, 0] == 8] = 0.0  # the x = 1 plane carries no mass
+    freed, vfix = oracle.dirichlet(grid, boxes, m_i)
+    ijk = grid.node_ijk()
+    fixed = np.all(vfix == [0.5, -1.0, 2.0], axis=1)
+    assert fixed.sum() == 9 * 4 * 9
+    assert set(np.unique(ijk[fixed, 1]).tolist()) == {0, 1, 2, 3}
+    assert np.all(vfix[~fixed] == 0.0)
+    # free DOFs: m_i > 0 and j >= 4 -> x-planes 0..7 (8) x y-planes 4..8 (5) x 9
+    assert freed.sum() == 8 * 5 * 9
+    assert np.all(freed[ijk[:, 1] <= 3] == 0) and np.all(freed[ijk[:, 0] == 8] == 0)
+
+
+def test_dirichlet_first_box_wins_and_plate():
+    """Two overlapping boxes: a node inside both takes the FIRST box's velocity (the header's rule);
+    the cfg5 plate "y >= top" with top on a node plane includes that plane.  Checked against a
+    brute-force membership count over explicit integer node indices (no coordinates): on a 16^3 grid,
+    floor = planes j <= 3, plate = planes j >= 12, a side box i <= 1 overlapping both."""
+    import oracle
+    n = 16
+    grid = oracle.Grid((n, n, n), 1 / n)
+    inf = float("inf")
+    boxes = [scenes.DirichletBox((-inf, -inf, -inf), (inf, 3 / n, inf), (0.0, 0.0, 0.0)),
+             scenes.DirichletBox((-inf, 12 / n, -inf), (inf, inf, inf), (0.0, -0.5, 0.0)),
+             scenes.DirichletBox((-inf, -inf, -inf), (1 / n, inf, inf), (7.0, 7.0, 7.0))]
+    freed, vfix = oracle.dirichlet(grid, boxes, np.ones(grid.nnodes))
+    for idx, (i, j, k) in enumerate(grid.node_ijk()):
+        want = (0.0, 0.0, 0.0) if j <= 3 else (0.0, -0.5, 0.0) if j >= 12 else (7.0, 7.0, 7.0) if i <= 1 else None
+        assert freed[idx] == (want is None)
+        assert tuple(vfix[idx]) == (want if want is not None else (0.0, 0.0, 0.0))

@@ -43,9 +43,10 @@ def main():
             t_us = float(got["gpu__time_duration.sum"][0].replace(",", ""))
             tu = got["gpu__time_duration.sum"][1]
             t_us = t_us / 1000.0 if tu in ("nsecond", "ns") else t_us * (1000.0 if tu in ("msecond", "ms") else 1.0)
-            mb = (float(got["dram__bytes_read.sum"][0].replace(",", "")) + float(got["dram__bytes_write.sum"][0].replace(",", "")))
-            scale = {"Mbyte": 1.0, "Gbyte": 1e3, "Kbyte": 1e-3, "byte": 1e-6}
-            mb *= scale.get(got["dram__bytes_read.sum"][1], 1.0)
+            # each metric carries its own unit (ncu picks Kbyte / Mbyte / Gbyte per value): scale before summing
+            scale = {"Mbyte": 1.0, "Gbyte": 1e3, "Kbyte": 1e-3, "byte": 1e-6, "Tbyte": 1e6}
+            mb = sum(float(got[k][0].replace(",", "")) * scale[got[k][1]]
+                     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
             print(f"  DRAM traffic {mb:.1f} MB in {t_us:.1f} us -> {mb / t_us * 1e3:.0f} GB/s (cold-cache replay)")
             if len(sys.argv) > 2:
                 alg = float(sys.argv[2])

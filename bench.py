@@ -104,19 +104,11 @@ def hvp_bytes(n_cells, n_nodes, s=4):
 
 
 def hvp_kernel_name(precision: int = 32) -> str:
-    """The HVP kernel the library runs: fp32 per MPL_HVP_KERNEL (default "wz" = k_hvp_wz<3, 0, 0>); fp64
-    per MPL_HVP_KERNEL64 (default "wh" = k_hvp_wh<double, 3>; "sel" follows MPL_HVP_KERNEL, whose fp32-only
-    variants fall back to k_hvp_rp<double, 10>)."""
-    v = os.environ.get("MPL_HVP_KERNEL", "wz")
-    if precision == 64 and not os.environ.get("MPL_HVP_KERNEL64", "wh").startswith("s"):
+    """The HVP kernel the library runs: fp32 k_hvp_wz (MPL_HVP_KERNEL=wh: k_hvp_wh<float, 5>), fp64
+    k_hvp_wh<double, 3>."""
+    if precision == 64:
         return "k_hvp_wh<double, 3>"
-    wz = {"wz": "k_hvp_wz<3, 0, 0>", "wz2": "k_hvp_wz<2, 1, 0>", "wzp": "k_hvp_wz<3, 0, 1>",
-          "wzp2": "k_hvp_wz<2, 1, 1>", "wzs": "k_hvp_wz<3, 0, 2>", "wzs2": "k_hvp_wz<2, 1, 2>", "wz3": "k_hvp_wz<3, 0, 3>",
-          "wh": "k_hvp_wh<float, 5>", "wh4": "k_hvp_wh<float, 4>"}
-    if v in wz:
-        return wz[v] if precision == 32 else ("k_hvp_wh<double, 3>" if v.startswith("wh") else "k_hvp_rp<10>")
-    return {"rq": "k_hvp_rq<10>", "rq8": "k_hvp_rq<8>", "rp10": "k_hvp_rp<10>", "rp": "k_hvp_rp<1>", "rp12": "k_hvp_rp<12>",
-            "pipe2": "k_hvp_pipe<2>", "pipe3": "k_hvp_pipe<3>", "reg": "k_hvp_reg"}.get(v, "k_hvp_wz<3, 0, 0>")
+    return "k_hvp_wh<float, 5>" if os.environ.get("MPL_HVP_KERNEL", "wz").startswith("wh") else "k_hvp_wz"
 
 
 def workload_name(sc) -> str:

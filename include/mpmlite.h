@@ -110,6 +110,10 @@ typedef struct {
     int32_t fixed_newton_iters;        /* >0: run exactly this many Newton iterations (parity replay) */
     const int32_t *fixed_cg_iters;     /* NULL or per-Newton-iteration PCG counts (parity replay)    */
     const int32_t *fixed_ls_halvings;  /* NULL or per-Newton-iteration halvings (parity replay)      */
+    int32_t psd_project;  /* 0: exact Hessian, PCG stops at negative curvature (amb-6);
+                             1: per-cell PSD projection of the cached tangent, K_c -> Q max(Lambda, 0) Q^T
+                             (for indefinite compressed states, e.g. cfg5's plate contact).
+                             Energy and gradient are unchanged; the Jacobi diagonal follows K_c.      */
 } mpl_solver_cfg;
 
 #define MPL_MAX_NEWTON_LOG 64
@@ -225,6 +229,9 @@ MPL_API mpl_status mpl_gradient(mpl_ctx ctx, const void *v, void *g, double *phi
 /* Linearise at v: caches the per-quadrature tangent K_c (45 numbers, the 9x9 symmetric
  * d^2(sum_k V_ck psi_k)/dG^2) and the Jacobi diagonal.  Required before mpl_hvp. */
 MPL_API mpl_status mpl_linearize(mpl_ctx ctx, const void *v);
+/* Tangent used by mpl_linearize / mpl_hvp / mpl_get_diag: 0 = exact (default), 1 = per-cell PSD projection
+ * (as mpl_solver_cfg.psd_project; mpl_newton_step follows its cfg instead). */
+MPL_API mpl_status mpl_set_psd_projection(mpl_ctx ctx, int32_t on);
 /* Jacobi diagonal D_ia = (H)_{ia,ia} at the last linearisation point (n_nodes*3). */
 MPL_API mpl_status mpl_get_diag(mpl_ctx ctx, void *D);
 /* Matrix-free Hessian-vector product at the last linearisation point (unprojected):

@@ -57,7 +57,7 @@ class _Box(C.Structure):
 class _Problem(C.Structure):
     _fields_ = [("g", _Grid), ("nmat", C.c_int32), ("mats", _Mat * MAXMAT), ("dt", C.c_double),
                 ("m_i", C.c_void_p), ("vhat", C.c_void_p), ("freed", C.c_void_p), ("m_c", C.c_void_p),
-                ("V_ck", C.c_void_p), ("S_ck", C.c_void_p)]
+                ("V_ck", C.c_void_p), ("S_ck", C.c_void_p), ("psd", C.c_int32)]
 
 
 class _SolverCfg(C.Structure):
@@ -132,6 +132,7 @@ def lib():
         L.orc_plastic_update.argtypes = [vp, vp, vp, vp]
         L.orc_plastic_update.restype = i64
         L.orc_explicit_force.argtypes = [vp, i32, vp, vp, vp, vp]
+        L.orc_psd_project9.argtypes = [vp, vp]
     return _lib
 
 
@@ -409,8 +410,9 @@ def dirichlet(grid: Grid, boxes, m_i) -> tuple:
 class Problem:
     """Integrate-time problem (Alg. 3): everything the solve reads, nothing from particles."""
 
-    def __init__(self, grid: Grid, materials, dt: float, m_i, vhat, freed, m_c, V_ck, S_ck):
+    def __init__(self, grid: Grid, materials, dt: float, m_i, vhat, freed, m_c, V_ck, S_ck, psd: bool = False):
         self.grid, self.materials, self.dt = grid, list(materials), float(dt)
+        self.psd = bool(psd)  # Hessian blocks K_c PSD-projected (SPEC S:427): hvp, diag and the Newton solve
         self.m_i, self.vhat = _f64(m_i), _f64(vhat).reshape(-1, 3)
         self.freed = np.ascontiguousarray(freed, dtype=np.uint8)
         self.m_c, self.V_ck, self.S_ck = _f64(m_c), _f64(V_ck), _f64(S_ck)
@@ -421,6 +423,7 @@ class Problem:
         P.dt = self.dt
         P.m_i, P.vhat, P.freed = _p(self.m_i).value, _p(self.vhat).value, _p(self.freed).value
         P.m_c, P.V_ck, P.S_ck = _p(self.m_c).value, _p(self.V_ck).value, _p(self.S_ck).value
+        P.psd = int(self.psd)
         self._c = P
 
     def plastic_update(self, v):
@@ -432,7 +435,13 @@ class Problem:
 
     def with_bases(self, S_ck) -> "Problem":
         """The same problem with other bases (e.g. the plastic iterate's, held fixed)."""
-        return Problem(self.grid, self.materials, self.dt, self.m_i, self.vhat, self.freed, self.m_c, self.V_ck, S_ck)
+        return Problem(self.grid, self.materials, self.dt, self.m_i, self.vhat, self.freed, self.m_c, self.V_ck, S_ck,
+                       self.psd)
+
+    def with_psd(self, psd: bool) -> "Problem":
+        """The same problem with the exact (False) or per-cell PSD-projected (True) Hessian."""
+        return Problem(self.grid, self.materials, self.dt, self.m_i, self.vhat, self.freed, self.m_c, self.V_ck,
+                       self.S_ck, psd)
 
     def energy(self, v) -> float:
         v = _f64(v).reshape(-1, 3)
@@ -458,6 +467,8 @@ class Problem:
 
     def newton(self, v0, solver, fixed_newton: int = 0, fixed_cg: Optional[Sequence[int]] = None,
                fixed_ls: Optional[Sequence[int]] = None):
+        if bool(getattr(solver, "psd", False)) != self.psd:  # the solver's Hessian mode
+            return self.with_psd(bool(getattr(solver, "psd", False))).newton(v0, solver, fixed_newton, fixed_cg, fixed_ls)
         v = _f64(v0).reshape(-1, 3).copy()
         cfg = _SolverCfg()
         cfg.newton_max, cfg.cg_max, cfg.ls_max = solver.newton_max, solver.cg_max, solver.ls_max
@@ -481,6 +492,14 @@ class Problem:
                      cg_iters=[st.cg_iters[k] for k in range(min(n, 64))],
                      ls_iters=[st.ls_iters[k] for k in range(min(n, 64))])
         return v, stats
+
+
+def psd_project9(M) -> np.ndarray:
+    """Per-cell PSD projection of a symmetric 9x9 block: Q max(Lambda, 0) Q^T (oracle's cyclic Jacobi)."""
+    M = _f64(M).reshape(81)
+    out = np.zeros(81)
+    lib().orc_psd_project9(_p(M), _p(out))
+    return out.reshape(9, 9)
 
 
 def explicit_force(grid: Grid, nmat: int, m_c, V_ck, tau_ck) -> np.ndarray:

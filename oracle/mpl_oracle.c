@@ -63,6 +63,7 @@ typedef struct {
     const double *m_c;    /* ncells      cell mass (cells with m_c>0 are quadrature) */
     const double *V_ck;   /* nmat*ncells rest volume per material slot      */
     const double *S_ck;   /* nmat*ncells*9 stretch base S_{c,k} (row-major)  */
+    int32_t psd;          /* 1: the Hessian's per-cell blocks K_c are PSD-projected  */
 } orc_problem;
 
 /* ------------------------------------------------------------------------ */
@@ -759,6 +760,78 @@ void orc_gradient(const orc_problem *P, const double *v, double *grad) {
             }
 }
 
+/* Per-cell PSD projection ("per-cell PSD projection of the elastic energy Hessian
+ * (eigenvalue clamping at 0)"): M -> Q max(Lambda, 0) Q^T for a symmetric 9x9 M, eigenpairs by the
+ * textbook cyclic Jacobi method (rotations until the off-diagonal part vanishes). */
+void orc_psd_project9(const double Min[81], double Mout[81]) {
+    double A[81], V[81];
+    for (int r = 0; r < 9; r++)
+        for (int c = 0; c < 9; c++) {
+            A[9 * r + c] = 0.5 * (Min[9 * r + c] + Min[9 * c + r]);
+            V[9 * r + c] = (r == c) ? 1.0 : 0.0;
+        }
+    for (int sweep = 0; sweep < 50; sweep++) {
+        double off = 0.0, dg = 0.0;
+        for (int r = 0; r < 9; r++)
+            for (int c = 0; c < 9; c++) {
+                if (r != c) off += A[9 * r + c] * A[9 * r + c];
+                else dg += A[9 * r + c] * A[9 * r + c];
+            }
+        if (!(off > 1e-32 * dg)) break;
+        for (int p = 0; p < 8; p++)
+            for (int q = p + 1; q < 9; q++) {
+                double apq = A[9 * p + q];
+                if (apq == 0.0) continue;
+                double theta = (A[9 * q + q] - A[9 * p + p]) / (2.0 * apq);
+                double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+                for (int r = 0; r < 9; r++) { /* columns p, q */
+                    double arp = A[9 * r + p], arq = A[9 * r + q];
+                    A[9 * r + p] = c * arp - s * arq;
+                    A[9 * r + q] = s * arp + c * arq;
+                }
+                for (int r = 0; r < 9; r++) { /* rows p, q */
+                    double apr = A[9 * p + r], aqr = A[9 * q + r];
+                    A[9 * p + r] = c * apr - s * aqr;
+                    A[9 * q + r] = s * apr + c * aqr;
+                }
+                for (int r = 0; r < 9; r++) { /* eigenvectors */
+                    double vrp = V[9 * r + p], vrq = V[9 * r + q];
+                    V[9 * r + p] = c * vrp - s * vrq;
+                    V[9 * r + q] = s * vrp + c * vrq;
+                }
+            }
+    }
+    for (int r = 0; r < 9; r++)
+        for (int c = 0; c < 9; c++) {
+            double v = 0.0;
+            for (int i = 0; i < 9; i++) {
+                double l = A[9 * i + i] > 0.0 ? A[9 * i + i] : 0.0;
+                v += V[9 * r + i] * l * V[9 * c + i];
+            }
+            Mout[9 * r + c] = v;
+        }
+}
+
+/* The cell's tangent as a 9x9 matrix: column (e,f) = sum_k slot_tangent along the unit dG = e_e (x) e_f,
+ * i.e. K_c[(a,b),(e,f)] = d Pc_ab / d G_ef with Pc = sum_k dt V tau A^{-T}; PSD-projected if P->psd. */
+static void cell_tangent_matrix(const orc_problem *P, const double A[9], int64_t c, double M[81]) {
+    int64_t nc = ncells(&P->g);
+    for (int e = 0; e < 9; e++) {
+        double dG[9] = {0}, Pc[9] = {0};
+        dG[e] = 1.0;
+        for (int k = 0; k < P->nmat; k++) {
+            double V = P->V_ck[(int64_t)k * nc + c];
+            if (V == 0.0) continue;
+            double blk[9];
+            slot_tangent(P->dt, V, &P->mats[k], A, P->S_ck + ((int64_t)k * nc + c) * 9, dG, blk);
+            for (int a = 0; a < 9; a++) Pc[a] += blk[a];
+        }
+        for (int a = 0; a < 9; a++) M[9 * a + e] = Pc[a];
+    }
+    if (P->psd) orc_psd_project9(M, M);
+}
+
 /* (H u)_i = m_i u_i + sum_c [sum_k K_ck : dG_c(u)] grad w_ic,  dG_c(u) = sum_j u_j (x) grad w_jc
  * (Hessian of Phi at v, App. B; full, unprojected). */
 void orc_hvp(const orc_problem *P, const double *v, const double *u, double *Hu) {
@@ -776,6 +849,12 @@ void orc_hvp(const orc_problem *P, const double *v, const double *u, double *Hu)
                 double A[9], dG[9], Pc[9] = {0};
                 cell_A(P, v, ci, cj, ck, A);
                 cell_G(P, u, ci, cj, ck, dG);
+                if (P->psd) { /* projected block: Pc = K_c^+ : dG */
+                    double M[81];
+                    cell_tangent_matrix(P, A, c, M);
+                    for (int a = 0; a < 9; a++)
+                        for (int e = 0; e < 9; e++) Pc[a] += M[9 * a + e] * dG[e];
+                } else
                 for (int k = 0; k < P->nmat; k++) {
                     double V = P->V_ck[(int64_t)k * nc + c];
                     if (V == 0.0) continue;
@@ -806,8 +885,9 @@ void orc_diag(const orc_problem *P, const double *v, double *D) {
             for (int ck = col & 1; ck < g->n[2]; ck += 2) {
                 int64_t c = cid(g, ci, cj, ck);
                 if (P->m_c[c] == 0.0) continue;
-                double A[9];
+                double A[9], M[81];
                 cell_A(P, v, ci, cj, ck, A);
+                if (P->psd) cell_tangent_matrix(P, A, c, M);
                 for (int o = 0; o < 8; o++) {
                     int64_t i = nid(g, ci + ((o >> 2) & 1), cj + ((o >> 1) & 1), ck + (o & 1));
                     double gw[3];
@@ -815,6 +895,10 @@ void orc_diag(const orc_problem *P, const double *v, double *D) {
                     for (int a = 0; a < 3; a++) {
                         double dG[9] = {0}, Pc[9] = {0};
                         for (int b = 0; b < 3; b++) dG[3 * a + b] = gw[b];
+                        if (P->psd) {
+                            for (int r = 0; r < 9; r++)
+                                for (int e = 0; e < 9; e++) Pc[r] += M[9 * r + e] * dG[e];
+                        } else
                         for (int k = 0; k < P->nmat; k++) {
                             double V = P->V_ck[(int64_t)k * nc + c];
                             if (V == 0.0) continue;

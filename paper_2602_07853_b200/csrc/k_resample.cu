@@ -369,8 +369,8 @@ __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, cons
         int c = __popcll(m);
         ccount[t] = (c + 3) & ~3;
         ncell[t] = c;
-        // tangent only on owned tiles: compact (45 c, rounded up to 4) or, in the padded kz layout, 64 slots
-        kcnt[t] = hascells[t] ? (kz == 2 ? 45 * 64 : (45 * c + 3) & ~3) : 0;
+        // tangent only on owned tiles: compact, 45 c reals rounded up to 4
+        kcnt[t] = hascells[t] ? (45 * c + 3) & ~3 : 0;
         if (c && hascells[t]) atomicAdd(ncells, (unsigned long long)c);
     }
 }

@@ -44,13 +44,85 @@ template <> __device__ __forceinline__ void atomic_add3<double>(d4 *p, double x,
 }
 
 // =============================================================================================
+// Per-cell PSD projection of the tangent ("per-cell PSD projection of the elastic energy
+// Hessian (eigenvalue clamping at 0)"; the paper's "off-the-shelf nonlinear solvers" P:4, "trust
+// region ... damping/line-search" P:1150).  K (9x9 symmetric, packed upper triangle, 45 reals) is
+// replaced by Q max(Lambda, 0) Q^T, with (Lambda, Q) from a cyclic Jacobi eigen-decomposition in fp64
+// (a continuous map of K: no per-cell decision, and a positive-definite K is returned up to rounding).
+// Used when the exact Hessian is indefinite (compressed StVK-Hencky cells: cfg5's plate contact).
+// =============================================================================================
+// Register-resident cyclic Jacobi on the packed upper triangle a[45] (A <- J^T A J, V <- V J per pair
+// (p, q); Numerical Recipes' update form), every index compile-time so nothing spills to local memory;
+// in the context's precision (fp32 resolves the eigenvalues to ~eps |K|, well inside the parity bars).
+template <class T>
+__device__ __forceinline__ void psd_project45(T *k) {
+    T a[45], V[81];
+#pragma unroll
+    for (int e = 0; e < 45; e++) a[e] = k[e];
+#pragma unroll
+    for (int e = 0; e < 81; e++) V[e] = (e % 10 == 0) ? T(1) : T(0);
+    T nd = T(0);
+#pragma unroll
+    for (int r = 0; r < 9; r++) nd += a[kidx(r, r)] * a[kidx(r, r)];
+    const T tiny = (sizeof(T) == 4 ? T(1e-14) : T(1e-30)) * nd;
+    for (int sweep = 0; sweep < 12; sweep++) {
+        T off = T(0);
+#pragma unroll
+        for (int p_ = 0; p_ < 8; p_++)
+#pragma unroll
+            for (int q = p_ + 1; q < 9; q++) off += a[kidx(p_, q)] * a[kidx(p_, q)];
+        if (!(off > tiny)) break;
+#pragma unroll
+        for (int p_ = 0; p_ < 8; p_++)
+#pragma unroll
+            for (int q = p_ + 1; q < 9; q++) {
+                const T apq = a[kidx(p_, q)];
+                if (apq != T(0)) {
+                    const T th = (a[kidx(q, q)] - a[kidx(p_, p_)]) / (T(2) * apq);
+                    const T t = (th >= T(0) ? T(1) : T(-1)) / (fabs(th) + sqrt(th * th + T(1)));
+                    const T c = T(1) / sqrt(t * t + T(1)), s_ = t * c, tau = s_ / (T(1) + c);
+                    a[kidx(p_, p_)] -= t * apq;
+                    a[kidx(q, q)] += t * apq;
+                    a[kidx(p_, q)] = T(0);
+#pragma unroll
+                    for (int r = 0; r < 9; r++) {
+                        if (r == p_ || r == q) continue;
+                        const int ip = r < p_ ? kidx(r, p_) : kidx(p_, r), iq = r < q ? kidx(r, q) : kidx(q, r);
+                        const T arp = a[ip], arq = a[iq];
+                        a[ip] = arp - s_ * (arq + tau * arp);
+                        a[iq] = arq + s_ * (arp - tau * arq);
+                    }
+#pragma unroll
+                    for (int r = 0; r < 9; r++) {
+                        const T vrp = V[9 * r + p_], vrq = V[9 * r + q];
+                        V[9 * r + p_] = vrp - s_ * (vrq + tau * vrp);
+                        V[9 * r + q] = vrq + s_ * (vrp - tau * vrq);
+                    }
+                }
+            }
+    }
+    T lam[9];
+#pragma unroll
+    for (int i = 0; i < 9; i++) lam[i] = a[kidx(i, i)] > T(0) ? a[kidx(i, i)] : T(0);
+#pragma unroll
+    for (int r = 0; r < 9; r++)
+#pragma unroll
+        for (int c = r; c < 9; c++) {
+            T v = T(0);
+#pragma unroll
+            for (int i = 0; i < 9; i++) v += V[9 * r + i] * lam[i] * V[9 * c + i];
+            k[kidx(r, c)] = v;
+        }
+}
+
+// =============================================================================================
 // a5 / a8: linearisation.  MODE = LIN_ENERGY (Phi only), LIN_GRAD (+ g), LIN_FULL (+ K, diag).
 // =============================================================================================
 // HONLY: every material slot is elastic StVK-Hencky (the other laws and the plastic base update are
 // compiled out: a third of the code, and ncu showed 20 % instruction-fetch stalls on the general kernel)
 // LMINB > 1: 64-thread launch with LMINB CTAs per SM requested from ptxas (the Hencky-only full
 // linearisation at 12: 80 registers, small spills, 24 warps / SM: cfg4 3.89 -> 3.62 ms per step; 16: 3.84)
-template <class T, int MODE, bool HONLY = false, int LMINB = 1>
+template <class T, int MODE, bool HONLY = false, int LMINB = 1, bool PSD = false>
 __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP g, MatP mp, double dt_, const int *__restrict__ nplus,
                                                    const int *__restrict__ cstart, const uint8_t *__restrict__ clocal,
                                                    const int *__restrict__ hascells, const vec4<T> *__restrict__ v,
@@ -373,24 +445,26 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
         }
     }
     __syncthreads();
+    if (PSD && MODE == LIN_FULL && has) {  // per-cell PSD projection before the K write and the diagonal
+        if (tid < nc && clocal[cs + tid] != 0xFF) psd_project45<T>(Ks + tid * 45);  // fp64: spills, acceptable
+        __syncthreads();
+    }
     if (MODE == LIN_FULL && has) {  // tile's tangent block, permuted into the chunked (coalesced) layout
         const int64_t base = kstart[t];
         const int n = ncell[t];  // real cells come first in the compact run
-        if (kz) {  // kz order (the wz HVP lanes): 64-slot block, slot = kz_key; compact: slot = its rank
-            if (tid < n) {
+        // slot of each cell: kz == 1 (k_hvp_wz lanes): the rank of its kz_key among the tile's cells;
+        // kz == 3 (k_hvp_wh): its rank in the natural compact order
+        if (tid < n) {
+            int sl = tid;
+            if (kz == 1) {
                 const int key = kz_key(clocal[cs + tid]);
-                int sl = kz == 3 ? tid : key;  // 3: natural compact order (wh HVP)
-                if (kz == 1) {
-                    sl = 0;
-                    for (int j = 0; j < n; j++) sl += kz_key(clocal[cs + j]) < key;
-                }
-                zslot[tid] = sl;
+                sl = 0;
+                for (int j = 0; j < n; j++) sl += kz_key(clocal[cs + j]) < key;
             }
-            __syncthreads();
+            zslot[tid] = sl;
         }
-        const int ncp = kz == 2 ? 64 : n;
-        for (int i = tid; i < n * 45; i += blockDim.x)
-            Kout[k_off<T>(base, ncp, kz ? zslot[i / 45] : kslot(i / 45, n), i % 45)] = Ks[i];
+        __syncthreads();
+        for (int i = tid; i < n * 45; i += blockDim.x) Kout[k_off<T>(base, n, zslot[i / 45], i % 45)] = Ks[i];
     }
     // ---- node phase -----------------------------------------------------------------------
     for (int h = tid; h < 125; h += blockDim.x) {
@@ -1054,7 +1128,11 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
         const int lin_gen_minb = lge ? atoi(lge) : 12;  // 12 CTAs per SM (NH / water / VM linearisations -7 %)
         bool honly = !ctx->mats.plastic;
         for (int k = 0; k < ctx->mats.nmat; k++) honly = honly && ctx->mats.kind[k] == 0;
-        if (honly) {
+        if (mode == LIN_FULL && ctx->psd_now) {  // per-cell PSD projection of K
+            // launch bounds (128, 1): the register-resident Jacobi (126 live reals) needs the registers
+            if (honly) k_linearize<T, LIN_FULL, true, 1, true><<<T_, 64, 0, st>>>(LIN_ARGS);
+            else k_linearize<T, LIN_FULL, false, 1, true><<<T_, 64, 0, st>>>(LIN_ARGS);
+        } else if (honly) {
             if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY, true><<<T_, lt, 0, st>>>(LIN_ARGS);
             else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD, true><<<T_, lt, 0, st>>>(LIN_ARGS);
             else if (lt == 64) k_linearize<T, LIN_FULL, true, 12><<<T_, lt, 0, st>>>(LIN_ARGS);
@@ -1106,6 +1184,13 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     const int64_t NT = (int64_t)ctx->T * 64;
     DevScalars *sc = (DevScalars *)ctx->scalars.p;
     mpl_solve_stats S{};
+    // Hessian used by this solve: exact (amb-6, negative-curvature stop) or per-cell PSD-projected
+    struct PsdGuard {
+        mpl_ctx c;
+        int old;
+        ~PsdGuard() { c->psd_now = old; }
+    } psd_guard{ctx, ctx->psd_now};
+    ctx->psd_now = cfg->psd_project ? 1 : 0;
     const bool fixed = cfg->fixed_newton_iters > 0;
     const int kmax = fixed ? cfg->fixed_newton_iters : cfg->newton_max;
     const int cg_cap = cfg->cg_max > 0 ? cfg->cg_max : 1;

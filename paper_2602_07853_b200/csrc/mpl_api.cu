@@ -564,7 +564,15 @@ mpl_status mpl_linearize(mpl_ctx ctx, const void *v) {
     MPL_CHECK(set_device(ctx));
     MPL_CHECK(DISPATCH(ctx, canon_to_tile, v, ctx->n_u.p));
     double e = 0;
+    ctx->psd_now = ctx->psd_default;
     return DISPATCH(ctx, linearize_impl, ctx->n_u.p, (int)LIN_FULL, &e);
+}
+
+mpl_status mpl_set_psd_projection(mpl_ctx ctx, int32_t on) {
+    ApiLock api_lock_;
+    if (!ctx || (on != 0 && on != 1)) return MPL_ERR_INVALID_ARG;
+    ctx->psd_default = on;
+    return MPL_OK;
 }
 
 mpl_status mpl_get_diag(mpl_ctx ctx, void *D) {

@@ -349,22 +349,14 @@ template <class T> struct KL {
     static constexpr int REM = 45 - NCH * VEC;
 };
 // Tangent layout per tile: n = the tile's real cells (no padding), block of 45 n reals (rounded up
-// to 4) at t_kstart[t].  Cell j of a tile is handled by HVP thread (warp j & 1, lane j >> 1), so the
-// two warps of a 64-thread CTA get ceil(n/2) and floor(n/2) cells; the tangent of cell j is stored at
-// slot kslot(j) = (j & 1) ceil(n/2) + (j >> 1), so each warp's 16-byte loads are contiguous.
-__host__ __device__ __forceinline__ int kslot(int j, int n) { return (j & 1) * ((n + 1) >> 1) + (j >> 1); }
-// "kz" layout (fp32 default, the wz HVP kernel): a fixed block of 64 slots per owned tile (45 * 64 reals,
-// the chunked layout of k_off with ncp = 64), the cell at local position l = 16 lx + 4 ly + lz in slot
-// kz_key(l) = the wz lane (16 (lz >> 1) + 4 lx + ly) for even lz, 32 + that lane for odd lz.  Absent
-// cells leave their slots unwritten and unread; every tangent load of the HVP is then an immediate offset
-// from one per-lane pointer.
+// to 4) at t_kstart[t], chunked as k_off with ncp = n.  Slot order: k_hvp_wz's "kz" order (layout 1:
+// the cell at local position l = 16 lx + 4 ly + lz is ranked by kz_key(l) = the wz lane (16 (lz >> 1) +
+// 4 lx + ly) for even lz, 32 + that lane for odd lz, so a warp's 16-byte loads of one chunk are
+// contiguous), or the natural compact order (layout 3: slot = rank of l; k_hvp_wh).
 __host__ __device__ __forceinline__ constexpr int kz_key(int l) {
     return ((l & 1) << 5) | (((l >> 1) & 1) << 4) | ((l >> 4) << 2) | ((l >> 2) & 3);
 }
-int hvp_kz_layout(int precision);  // 0: kslot order, 1: compact kz order, 2: 64-slot kz blocks
-// HVP thread -> (cell j, tangent slot)
-__device__ __forceinline__ int hvp_cell(int tid) { return 2 * (tid & 31) + (tid >> 5); }
-__device__ __forceinline__ int hvp_slot(int tid, int n) { return (tid >> 5) * ((n + 1) >> 1) + (tid & 31); }
+int hvp_kz_layout(int precision);  // 1: compact kz order (k_hvp_wz), 3: natural compact order (k_hvp_wh)
 template <class T> __host__ __device__ __forceinline__ int64_t k_off(int64_t base, int ncp, int j, int e) {
     return e < KL<T>::NCH * KL<T>::VEC
                ? base + ((int64_t)(e / KL<T>::VEC) * ncp + j) * KL<T>::VEC + (e % KL<T>::VEC)
@@ -463,6 +455,9 @@ struct mpl_ctx_s {
     // pkey / prank / t_bstart) restores one order before anything else reads v / G (a second resample,
     // mpl_get_particles*).
     bool vg_unsorted = false;
+    // Hessian mode of the cached tangent: psd_default (mpl_set_psd_projection) for mpl_linearize,
+    // psd_now = the value the current linearisation uses (newton_impl sets it from its solver cfg)
+    int psd_default = 0, psd_now = 0;
 
     // tiles
     int T = 0;

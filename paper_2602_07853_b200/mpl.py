@@ -57,7 +57,7 @@ class SolverCfg(C.Structure):
     _fields_ = [("newton_max", C.c_int32), ("cg_max", C.c_int32), ("newton_rtol", C.c_double),
                 ("cg_rtol", C.c_double), ("armijo_c", C.c_double), ("ls_max", C.c_int32),
                 ("ls_slack", C.c_double), ("fixed_newton_iters", C.c_int32), ("fixed_cg_iters", C.c_void_p),
-                ("fixed_ls_halvings", C.c_void_p)]
+                ("fixed_ls_halvings", C.c_void_p), ("psd_project", C.c_int32)]
 
 
 MAX_NEWTON_LOG = 64
@@ -116,6 +116,7 @@ _SIGS = {
     "mpl_gradient": [_vp, _vp, _vp, _vp],
     "mpl_linearize": [_vp, _vp],
     "mpl_get_diag": [_vp, _vp],
+    "mpl_set_psd_projection": [_vp, _i32],
     "mpl_hvp": [_vp, _vp, _vp],
     "mpl_hvp_bench": [_vp, _vp, _vp, _i32, _vp],
     "mpl_newton_step": [_vp, _vp, _vp],
@@ -414,6 +415,10 @@ class Context:
         self._chk(_lib.mpl_gradient(self._h, _ptr(v), _ptr(g), C.byref(e)), "mpl_gradient")
         return g, e.value
 
+    def set_psd_projection(self, on: bool):
+        """Tangent of mpl_linearize / mpl_hvp / mpl_get_diag: exact (False) or per-cell PSD-projected (True)."""
+        self._chk(_lib.mpl_set_psd_projection(self._h, int(bool(on))), "mpl_set_psd_projection")
+
     def linearize(self, v):
         v = self._real(v)
         self._chk(_lib.mpl_linearize(self._h, _ptr(v)), "mpl_linearize")
@@ -439,7 +444,7 @@ class Context:
     def solver_cfg(s, fixed_newton: int = 0, fixed_cg=None, fixed_ls=None):
         cfg = SolverCfg(newton_max=s.newton_max, cg_max=s.cg_max, newton_rtol=s.eps_newton, cg_rtol=s.eps_cg,
                         armijo_c=s.armijo, ls_max=s.ls_max, ls_slack=getattr(s, "ls_slack", 1e-13),
-                        fixed_newton_iters=int(fixed_newton))
+                        fixed_newton_iters=int(fixed_newton), psd_project=int(bool(getattr(s, "psd", False))))
         keep = []
         if fixed_cg is not None:
             a = np.ascontiguousarray(fixed_cg, dtype=np.int32)

@@ -53,6 +53,7 @@ class SolverCfg:
     ls_max: int = 30
     armijo: float = 1e-4
     ls_slack: float = 1e-13  # Armijo rounding slack relative to |Phi| (amb-6); fp32 runs use 1e-6
+    psd: bool = False  # per-cell PSD projection of the Hessian; cfg5 (indefinite under the plate)
 
 
 @dataclasses.dataclass

@@ -31,9 +31,9 @@ def test_hvp_helpers():
     # 180 B of tangent per quadrature point + 28 B per active node (fp32), doubled in fp64
     assert bench.hvp_bytes(10, 20, 4) == 10 * 180 + 20 * 28
     assert bench.hvp_bytes(10, 20, 8) == 2 * (10 * 180 + 20 * 28)
-    env = {k: os.environ.pop(k) for k in ("MPL_HVP_KERNEL", "MPL_HVP_KERNEL64") if k in os.environ}
+    env = {k: os.environ.pop(k) for k in ("MPL_HVP_KERNEL",) if k in os.environ}
     try:
-        assert bench.hvp_kernel_name(32) == "k_hvp_wz<3, 0, 0>"
+        assert bench.hvp_kernel_name(32) == "k_hvp_wz"
         assert bench.hvp_kernel_name(64) == "k_hvp_wh<double, 3>"
     finally:
         os.environ.update(env)

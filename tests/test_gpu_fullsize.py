@@ -8,14 +8,17 @@ element by element:
   * a5 gradient and a6 HVP + Jacobi diagonal at a probe v = v^0 + 0.01 n(key), direction u = n(key)
     (key-indexed normal draws, so window and full run use identical probes);
   * a9 G2P of the window's particles from the GPU's own v^{n+1} after one adaptive implicit step.
-Bars: the fp32 ones of BASELINE.json (1e-5 on unload / gradient / HVP; 1e-4 on the step)."""
+Cases: cfg2, cfg3 (PPC 8), cfg4 and cfg5B (512^3, ~93M particles: wheel rim, wheel-slab contact, the
+plate's Dirichlet layer) in fp32 — the bench's configuration — and cfg4 / cfg5B in fp64 (the fp64 HVP
+kernel; cfg5B's "fp64 check" of BASELINE.json config 5).
+Bars: BASELINE.json's (1e-5 fp32 / 1e-10 fp64 on unload / gradient / HVP; the step bars for G2P)."""
 import numpy as np
 import pytest
 
 import oracle
 from paper_2602_07853_b200 import mpl, scenes
 
-from ._parity import node_ids, rel_l2
+from ._parity import TOL, node_ids, rel_l2
 
 pytestmark = pytest.mark.gpu
 
@@ -25,13 +28,24 @@ WINDOWS = {
     "cfg2": [(22, 22, 22), (44, 10, 30)],
     "cfg3": [(54, 54, 54), (100, 60, 2)],
     "cfg4": [(54, 80, 118), (180, 80, 118), (118, 2, 118)],  # left sphere, right sphere, slab + floor
+    # cfg5B (dx = 1/512; wheel axis z through (256, 182.6, 256) cells, R = 153.6, r = 51.2 cells, z in
+    # [217.6, 294.4); slab y in [3, 29); plate: nodes with y >= 336.2): outer rim, inner rim, wheel-slab
+    # contact + floor, the plate layer at the wheel's top
+    "cfg5B": [(395, 172, 246), (296, 172, 246), (246, 20, 246), (246, 322, 246)],
 }
+CASES = [("cfg2", 32), ("cfg3", 32), ("cfg4", 32), ("cfg5B", 32), ("cfg4", 64), ("cfg5B", 64)]
+
+
+# elastic part of the HVP: the fp32 bar times this slack (DESIGN.md §9 reading r2-a); fp64: none
+ELASTIC_SLACK = {32: 1.0, 64: 1.0}
 
 
 class Full:
-    def __init__(self, name):
+    def __init__(self, name, precision=32):
         self.name = name
-        self.sc = sc = scenes.by_name(name, 32)
+        self.precision = precision
+        self.tol = TOL[precision]
+        self.sc = sc = scenes.by_name(name, precision)
         self.ctx = ctx = mpl.from_scene(sc, 0)
         self.counts = ctx.resample(sc.dt)
         self.ijk, self.m, self.vn, self.free = ctx.get_nodes()
@@ -41,8 +55,9 @@ class Full:
         n1, n2 = sc.n[1] + 1, sc.n[2] + 1
         self.key = (self.ijk[:, 0].astype(np.int64) * n1 + self.ijk[:, 1]) * n2 + self.ijk[:, 2]
         self.v0 = ctx.get_velocity().astype(np.float64)
-        self.vp = (self.v0 + 0.01 * scenes.key_noise(self.key, 5)).astype(np.float32).astype(np.float64)
-        self.u = scenes.key_noise(self.key, 4).astype(np.float32).astype(np.float64)
+        dt_ = np.float32 if precision == 32 else np.float64
+        self.vp = (self.v0 + 0.01 * scenes.key_noise(self.key, 5)).astype(dt_).astype(np.float64)
+        self.u = scenes.key_noise(self.key, 4).astype(dt_).astype(np.float64)
         self.g, self.phi = ctx.gradient(self.vp)
         ctx.linearize(self.vp)
         self.h = ctx.hvp(self.u)
@@ -56,9 +71,9 @@ class Full:
         self.pos = {int(k): i for i, k in enumerate(self.key)}
 
 
-@pytest.fixture(scope="module", params=list(WINDOWS))
+@pytest.fixture(scope="module", params=CASES, ids=[f"{n}_fp{p}" for n, p in CASES])
 def full(request):
-    return Full(request.param)
+    return Full(*request.param)
 
 
 def _window(full, lo):
@@ -98,8 +113,9 @@ def test_windows_unload_gradient_hvp(full):
         # nodes the GPU holds inside the window's complete region must be active in the oracle too
         assert np.all((un.m_i[cm & (gpos >= 0)]) > 0)
         sel = gpos[act]
-        assert rel_l2(full.m[sel], un.m_i[act]) <= 1e-5
-        assert rel_l2(full.vn[sel], un.v_i[act]) <= 1e-5
+        tol = full.tol
+        assert rel_l2(full.m[sel], un.m_i[act]) <= tol["unload"]
+        assert rel_l2(full.vn[sel], un.v_i[act]) <= tol["unload"]
         assert np.array_equal(full.free[sel].astype(bool), prob.freed[act] != 0)
         # probes at every window node the GPU holds (zero elsewhere: massless there)
         have = gpos >= 0
@@ -107,9 +123,14 @@ def test_windows_unload_gradient_hvp(full):
         u = np.zeros_like(v)
         v[have] = full.vp[gpos[have]]
         u[have] = full.u[gpos[have]]
-        assert rel_l2(full.g[sel], prob.gradient(v)[act]) <= 1e-5
-        assert rel_l2(full.h[sel], prob.hvp(v, u)[act]) <= 1e-5
-        assert rel_l2(full.D[sel], prob.diag(v)[act]) <= 1e-5
+        assert rel_l2(full.g[sel], prob.gradient(v)[act]) <= tol["grad"]
+        h_o = prob.hvp(v, u)
+        assert rel_l2(full.h[sel], h_o[act]) <= tol["hvp"]
+        # the elastic part alone (the exact mass term could hide tangent errors; cfg5B's plate layer is
+        # stiffness-dominated, the spheres of cfg4 mass-dominated)
+        mu_ = un.m_i[:, None] * u
+        assert rel_l2(full.h[sel] - full.m[sel][:, None] * full.u[sel], (h_o - mu_)[act]) <= tol["hvp"] * ELASTIC_SLACK[full.precision]
+        assert rel_l2(full.D[sel], prob.diag(v)[act]) <= tol["hvp"]
 
 
 def test_windows_quadrature(full):
@@ -125,13 +146,14 @@ def test_windows_quadrature(full):
         comp = np.all((cijk >= 1) & (cijk <= SIZE), axis=1) & (un.m_c > 0)
         g = cijk[comp] + (np.asarray(lo) - 1)[None, :]
         sel = np.array([cpos[int(k)] for k in (g[:, 0] * n1 + g[:, 1]) * n2 + g[:, 2]])
-        assert rel_l2(q["m_c"][sel], un.m_c[comp]) <= 1e-5
-        assert rel_l2(q["v_c"][sel], un.v_c[comp]) <= 1e-5
+        tol = full.tol["unload"]
+        assert rel_l2(q["m_c"][sel], un.m_c[comp]) <= tol
+        assert rel_l2(q["v_c"][sel], un.v_c[comp]) <= tol
         for k in range(len(sc.materials)):
-            assert rel_l2(q["V_ck"][k][sel], un.V_ck[k][comp]) <= 1e-5
+            assert rel_l2(q["V_ck"][k][sel], un.V_ck[k][comp]) <= tol
             has = un.V_ck[k][comp] > 0
             if has.any():
-                assert rel_l2(q["S_ck"][k][sel][has], w["S"][k][comp][has]) <= 1e-5
+                assert rel_l2(q["S_ck"][k][sel][has], w["S"][k][comp][has]) <= tol
 
 
 def test_step_converges_and_g2p_windows(full):
@@ -151,10 +173,11 @@ def test_step_converges_and_g2p_windows(full):
         vnew[have] = full.vnew[w["gpos"][have]]
         x_o, v_o, F_o, G_o = oracle.g2p(w["grid"], sc.dt, w["un"].m_c, vnew, sub.x, sub.v, sub.F, sub.G, clip=True)
         idx = w["keep"][inner]
-        assert rel_l2(x_g[idx], x_o[inner]) <= 1e-6
-        assert rel_l2(v_g[idx], v_o[inner]) <= 1e-4
-        assert rel_l2(F_g[idx], F_o[inner]) <= 1e-4
+        tol = full.tol["step"]
+        assert rel_l2(x_g[idx], x_o[inner]) <= 1e-2 * tol  # x moves by dt v: far tighter than the step bar
+        assert rel_l2(v_g[idx], v_o[inner]) <= tol
+        assert rel_l2(F_g[idx], F_o[inner]) <= tol
         # G_p = sum_c w G_c is a difference quotient of v^{n+1} (~|v|/dx): where the material barely
-        # deforms (the stiff slab) fp32 rounding of v alone is ~1e-7 |v|/dx, so scale by that too
+        # deforms (the stiff slab) rounding of v alone is ~eps |v|/dx, so scale by that too (reading r2-b)
         scale = max(np.linalg.norm(G_o[inner]), np.linalg.norm(v_o[inner]) / sc.dx)
-        assert np.linalg.norm(G_g[idx] - G_o[inner]) <= 1e-4 * scale
+        assert np.linalg.norm(G_g[idx] - G_o[inner]) <= tol * scale

@@ -73,6 +73,16 @@ def plastic_cube(precision=64):
     return dataclasses.replace(sc, materials=[dataclasses.replace(sc.materials[0], yield_stress=150.0)])
 
 
+def compressed_cube(precision=64):
+    """cfg1's cube uniformly compressed (F_p = 0.93^{1/3} R_p-free, tau < 0: the exact Hessian is indefinite)
+    on a sticky floor, solved with the per-cell PSD-projected Hessian (solver psd)."""
+    sc = scenes.cfg1(prestrain=False, precision=precision)
+    F = np.tile((0.93 ** (1 / 3) * np.eye(3)).ravel(), (sc.x.shape[0], 1))
+    floor = scenes.DirichletBox((-1e9, -1e9, -1e9), (1e9, 4.5 / 16, 1e9), (0.0, 0.0, 0.0))
+    return dataclasses.replace(sc, name="psd", F=F, materials=[scenes.Material(1e6, 0.3, 1000.0)], dirichlet=[floor],
+                               solver=dataclasses.replace(sc.solver, psd=True))
+
+
 SCENES = {
     "cfg1": lambda: scenes.cfg1(),
     "cfg1b": lambda: scenes.cfg1(prestrain=True),
@@ -95,6 +105,9 @@ SCENES = {
     "vm_fp64": lambda: plastic_cube(64),
     "vm_fp32": lambda: plastic_cube(32),
     "vmmix_fp64": lambda: two_material(64, (0, 0), (1500.0, 0.0)),
+    # per-cell PSD-projected Hessian on an indefinite (compressed) state
+    "psd_fp64": lambda: compressed_cube(64),
+    "psd_fp32": lambda: compressed_cube(32),
 }
 
 
@@ -137,7 +150,7 @@ def test_unload_parity(pair):
         assert rel_l2(q["V_ck"][k][act], pair.un.V_ck[k][cid][act]) <= tol
         sel = pair.un.V_ck[k][cid] > 0
         if np.abs(pair.un.tau_ck[k]).max() > 0:
-            assert rel_l2(q["tau_ck"][k][sel], pair.un.tau_ck[k][cid][sel]) <= tol * 10
+            assert rel_l2(q["tau_ck"][k][sel], pair.un.tau_ck[k][cid][sel]) <= tol
         assert rel_l2(q["S_ck"][k][sel], pair.S[k][cid][sel]) <= tol
     assert rel_l2(pair.m, pair.un.m_i[pair.nid]) <= tol
     assert rel_l2(pair.vn, pair.un.v_i[pair.nid]) <= tol
@@ -158,10 +171,13 @@ def _probe(pair):
 
 def _at(pair, v):
     """The oracle problem the GPU evaluates at v: with fixed-point plasticity the gradient and the full
-    linearisation re-project the bases at v; otherwise the resample's bases."""
+    linearisation re-project the bases at v; otherwise the resample's bases.  The Hessian mode
+    (exact / PSD-projected) follows the scene's solver, and the GPU context is set to the same."""
+    psd = bool(getattr(pair.scene.solver, "psd", False))
+    pair.ctx.set_psd_projection(psd)
     if any(getattr(m, "yield_stress", 0.0) > 0 for m in pair.scene.materials):
-        return pair.prob.with_bases(pair.prob.plastic_update(v)[0])
-    return pair.prob
+        return pair.prob.with_bases(pair.prob.plastic_update(v)[0]).with_psd(psd)
+    return pair.prob.with_psd(psd)
 
 
 def test_energy_gradient_parity(pair):
@@ -179,16 +195,20 @@ def test_energy_gradient_parity(pair):
 def test_hvp_and_diag_parity(pair):
     tol = TOL[pair.scene.precision]["hvp"]
     v, u = _probe(pair)
-    pair.ctx.linearize(pair.to_gpu(v))
     po = _at(pair, v)
+    pair.ctx.linearize(pair.to_gpu(v))
     h_o = po.hvp(v, u)
     h_g = pair.ctx.hvp(pair.to_gpu(u))
     assert rel_l2(h_g, h_o[pair.nid]) <= tol
-    # elastic part alone (the mass term is exact and could hide tangent errors)
+    # elastic part alone (the mass term is exact and could hide tangent errors).  The GPU returns Hu
+    # rounded to its precision, so the part recovered by subtracting m u carries that rounding, at most
+    # a few eps |m u| (DESIGN.md §9 reading r2-a): bar = tol |el| + 4 eps |m u|
     m = pair.un.m_i[:, None]
     el_o = (h_o - m * u)[pair.nid]
     el_g = h_g - pair.m[:, None] * pair.to_gpu(u)
-    assert rel_l2(el_g, el_o) <= (tol if pair.scene.precision == 64 else 2e-4)
+    eps = 2.0 ** -24 if pair.scene.precision == 32 else 2.0 ** -53
+    mu_ = np.linalg.norm((m * u)[pair.nid])
+    assert np.linalg.norm(el_g - el_o) <= tol * np.linalg.norm(el_o) + 4 * eps * mu_
     d_o = po.diag(v)
     assert rel_l2(pair.ctx.get_diag(), d_o[pair.nid]) <= tol
 
@@ -213,7 +233,7 @@ def test_full_step_parity(pair):
     assert rel_l2(x_g, x_o) <= tol
     assert rel_l2(vp_g, vp_o) <= tol
     assert rel_l2(F_g, F_o) <= tol
-    assert rel_l2(G_g, G_o) <= tol * 10
+    assert rel_l2(G_g, G_o) <= tol
 
 
 def test_adaptive_solve_converges(pair):
@@ -225,4 +245,6 @@ def test_adaptive_solve_converges(pair):
     st = ctx.newton_step(sc.solver)
     assert st["converged"] == 1
     v_o, st_o = pair.prob.newton(pair.v0, sc.solver)
+    # two independent adaptive solves (own counts), each stopped at ||g|| <= eps_N ||g_0||: they agree to
+    # the solver tolerance, not to rounding (DESIGN.md §9 reading r2-c)
     assert rel_l2(ctx.get_velocity(), v_o[pair.nid]) <= (1e-7 if sc.precision == 64 else 1e-3)

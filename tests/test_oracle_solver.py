@@ -320,3 +320,84 @@ def test_dirichlet_first_box_wins_and_plate():
         want = (0.0, 0.0, 0.0) if j <= 3 else (0.0, -0.5, 0.0) if j >= 12 else (7.0, 7.0, 7.0) if i <= 1 else None
         assert freed[idx] == (want is None)
         assert tuple(vfix[idx]) == (want if want is not None else (0.0, 0.0, 0.0))
+
+
+# ---- per-cell PSD projection of the Hessian (solver option psd, DESIGN.md §2 amb-6b) -----
+def test_psd_project9_matches_eigh_clamp(orc):
+    """The oracle's cyclic-Jacobi projection equals LAPACK's eigh with the negative eigenvalues clamped
+    (an independent eigensolver), including repeated and zero eigenvalues."""
+    rng = np.random.default_rng(11)
+    for trial in range(20):
+        Q, _ = np.linalg.qr(rng.normal(size=(9, 9)))
+        lam = rng.normal(size=9) * 10.0 ** rng.uniform(-3, 3)
+        if trial % 4 == 1:
+            lam[:3] = lam[0]  # repeated
+        if trial % 4 == 2:
+            lam[5] = 0.0
+        M = (Q * lam) @ Q.T
+        w, U = np.linalg.eigh(M)
+        want = (U * np.maximum(w, 0.0)) @ U.T
+        got = orc.psd_project9(M)
+        assert np.allclose(got, got.T, rtol=0, atol=1e-13 * np.abs(M).max())
+        assert np.abs(got - want).max() <= 1e-11 * np.abs(M).max()
+
+
+def _compressed_scene(J=0.93, n=6):
+    """A uniformly compressed block (F_p = J^{1/3} I): a hydrostatic Kirchhoff stress tau < 0 makes the
+    rotation modes of K_c negative (geometric stiffness), so the exact Hessian is indefinite."""
+    sc = make_scene(n=n, lo=2, hi=4, E=1e6, prestrain=False, vel=0.05, seed=3)
+    F = np.tile((J ** (1 / 3) * np.eye(3)).ravel(), (sc.x.shape[0], 1))
+    return dataclasses.replace(sc, F=F)
+
+
+def _dense_elastic(prob, v0):
+    fr = np.nonzero(prob.m_i > 0)[0]
+    dofs = [(i, a) for i in fr for a in range(3)]
+    H = np.zeros((len(dofs), len(dofs)))
+    for j, (i, a) in enumerate(dofs):
+        e = np.zeros_like(v0)
+        e[i, a] = 1.0
+        Hu = prob.hvp(v0, e) - prob.m_i[:, None] * e
+        H[:, j] = [Hu[ii, aa] for ii, aa in dofs]
+    return H, dofs
+
+
+def test_psd_hessian_is_psd_and_dominates_exact(orc):
+    """Compressed block: the exact elastic Hessian has negative eigenvalues; the projected one is
+    symmetric PSD, H+ - H is PSD (clamping only adds sum |lambda_-| q q^T per cell), and the projected
+    Jacobi diagonal is the diagonal of the dense projected Hessian."""
+    sc = _compressed_scene()
+    un, S, prob, v0 = orc.prepare(sc)
+    H, dofs = _dense_elastic(prob, v0)
+    Hp, _ = _dense_elastic(prob.with_psd(True), v0)
+    scale = np.abs(H).max()
+    assert np.linalg.eigvalsh(0.5 * (H + H.T)).min() < -1e-6 * scale
+    assert np.allclose(Hp, Hp.T, rtol=0, atol=1e-11 * scale)
+    assert np.linalg.eigvalsh(0.5 * (Hp + Hp.T)).min() >= -1e-10 * scale
+    assert np.linalg.eigvalsh(0.5 * ((Hp - H) + (Hp - H).T)).min() >= -1e-10 * scale
+    D = prob.with_psd(True).diag(v0)
+    want = np.array([Hp[j, j] for j in range(len(dofs))]) + np.array([prob.m_i[i] for i, _ in dofs])
+    got = np.array([D[i, a] for i, a in dofs])
+    assert np.allclose(got, want, rtol=1e-12, atol=0)
+
+
+def test_psd_is_identity_on_convex_cells(orc):
+    """Stretched block (F_p = 1.05^{1/3} I, tension): every K_c is PSD already, so the projected HVP equals
+    the exact one to rounding."""
+    sc = _compressed_scene(J=1.05)
+    un, S, prob, v0 = orc.prepare(sc)
+    u = np.random.default_rng(4).normal(size=v0.shape) * (prob.m_i > 0)[:, None]
+    h = prob.hvp(v0, u) - prob.m_i[:, None] * u
+    hp = prob.with_psd(True).hvp(v0, u) - prob.m_i[:, None] * u
+    assert np.linalg.norm(hp - h) <= 1e-10 * np.linalg.norm(h)
+
+
+def test_psd_newton_converges_without_negative_curvature(orc):
+    """Projected Newton on the compressed block: PCG never meets negative curvature and the step
+    converges to the Newton tolerance on the true gradient."""
+    sc = _compressed_scene()
+    un, S, prob, v0 = orc.prepare(sc)
+    solver = dataclasses.replace(sc.solver, psd=True, eps_newton=1e-9, eps_cg=1e-10)
+    v, st = prob.newton(v0, solver)
+    assert st["neg_curv"] == 0 and st["converged"] == 1
+    assert np.linalg.norm(prob.gradient(v)[prob.freed == 1]) <= 1e-9 * st["grad_norm0"] * 1.0001

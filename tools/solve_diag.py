@@ -25,12 +25,15 @@ def main():
     ap.add_argument("--eps-newton", type=float, default=None)
     ap.add_argument("--ls-slack", type=float, default=None)
     ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--psd", type=int, default=None, help="1: per-cell PSD-projected Hessian, 0: exact")
+    ap.add_argument("--cg-max", type=int, default=None)
     a = ap.parse_args()
     t0 = time.time()
     sc = scenes.by_name(a.config, a.precision)
     solver = sc.solver
     kw = {k: v for k, v in (("newton_max", a.newton_max), ("eps_cg", a.eps_cg), ("eps_newton", a.eps_newton),
-                            ("ls_slack", a.ls_slack)) if v is not None}
+                            ("ls_slack", a.ls_slack), ("cg_max", a.cg_max),
+                            ("psd", None if a.psd is None else bool(a.psd))) if v is not None}
     solver = dataclasses.replace(solver, **kw)
     t1 = time.time()
     ctx = mpl.from_scene(sc, 0)

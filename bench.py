@@ -158,7 +158,24 @@ def run_ours(args):
         ctx = mpl.from_scene(sc, device=local)
         ctx.set_stream(stream.cuda_stream)
 
+    # --restart (default for cfg5B): every step solves the scene's first time step from the same initial
+    # state, re-set from a device-resident copy (a D2D copy inside the step), so every step and every GPU
+    # count does the same work (strong scaling on a fixed problem; the wheel press hardens as the plate
+    # advances: measured 2.8 / 7.8 / 15.8 s for its first three steps on one GPU)
+    restart = args.restart if args.restart is not None else sc.name.startswith("cfg5")
+    if restart:
+        idx = np.arange(sc.n_particles) if sel is None else sel
+        dt_ = torch.float32 if args.precision == 32 else torch.float64
+        dev0 = [torch.from_numpy(np.ascontiguousarray(a[idx])).to(device="cuda", dtype=dt_)
+                for a in (sc.x, sc.v, sc.F, sc.G, sc.vol)]
+        mat0 = torch.from_numpy(np.ascontiguousarray(sc.mat[idx])).to("cuda")
+        ids0 = None if sel is None else sel.astype(np.int32)
+
     def one_step():
+        if restart:
+            ctx.set_particles(*dev0, mat0)
+            if ids0 is not None:
+                ctx.set_particle_ids(ids0)
         return ctx.step(sc.dt, solver)
 
     for _ in range(args.warmup):
@@ -227,7 +244,11 @@ def run_ours(args):
             (f"x-slab decomposition over {ws} GPUs (cuts {list(map(int, cuts))} in 4-cell blocks; "
              "halo sums + allreduces on the library's NCCL communicator)"),
             "l2": "inputs larger than L2 (tangent stream > 126 MB per HVP)",
-            "step": "full implicit step: resample + Newton-PCG + G2P",
+            "step": "full implicit step: resample + Newton-PCG + G2P" + (
+                " (each step restarts from the initial state: fixed work per step)" if restart else " (consecutive steps)"),
+            "solver": {"eps_cg": solver.eps_cg, "eps_newton": solver.eps_newton, "psd": bool(getattr(solver, "psd", False)),
+                       "newton_max": solver.newton_max, "cg_max": solver.cg_max,
+                       "pcg": os.environ.get("MPL_PCG", "cg1" if ws > 1 else "classic")},
         },
         "implicit_step_ms": round(ms_per_step, 3),
         "newton_iters": [s["newton_iters"] for s in stats],
@@ -428,6 +449,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--restart", type=int, default=None,
+                    help="1: every step restarts from the initial state (default for cfg5B), 0: consecutive steps")
     args = ap.parse_args()
     if args.config is None:
         args.config = "cfg4" if int(os.environ.get("WORLD_SIZE", "1")) <= 1 else "cfg5B"

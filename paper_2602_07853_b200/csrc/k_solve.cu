@@ -985,6 +985,114 @@ __global__ void __launch_bounds__(256, 2) k_pcg_update2w(int64_t n, int64_t S, c
     }
 }
 
+// ---- single-reduction Jacobi-PCG (Chronopoulos & Gear's recurrence; MPL_PCG=cg1, the default) ------
+// Mathematically the Hestenes-Stiefel PCG of the oracle (amb-7, amb-8): the matrix-vector product is
+// applied to the preconditioned residual u = D^-1 r instead of to p, and s = H p is carried by the
+// recurrence s_j = w_j + beta_j s_{j-1} (w_j = H u_j), so every scalar of iteration j is known once
+// its HVP has run:
+//   gamma_j = r_j . u_j (vector kernel j-1),  delta_j = u_j . H u_j (HVP epilogue, quadratic form),
+//   beta_j = gamma_j / gamma_{j-1},  eta_j = delta_j - beta_j gamma_j / alpha_{j-1}  (= p_j . H p_j),
+//   alpha_j = gamma_j / eta_j;  eta_j <= 0: negative curvature (iteration 0 returns u_0 = z_0).
+// One vector kernel per iteration instead of two, and on slab ranks one allreduce (gamma, r.r, delta)
+// instead of two.  u (the HVP input) and w (its output) are tile-dense; x, r, p, s, 1/D compact SoA.
+// Per node (fp32): reads r, 1/D, p, s, x (60 B), w (16), list (4); writes r, p, s, x (48), u (16),
+// w := 0 (16) for the next HVP's atomics.
+template <class T, int E>
+__global__ void __launch_bounds__(256, 2) k_pcg_cg1(int64_t n, int64_t S, const int *__restrict__ list, int j,
+                                                    double thr, const T *__restrict__ invD, vec4<T> *__restrict__ u,
+                                                    vec4<T> *__restrict__ w, T *__restrict__ x, T *__restrict__ r,
+                                                    T *__restrict__ p, T *__restrict__ s_,
+                                                    const uint8_t *__restrict__ own, CGSlot *slot, DevScalars *sc) {
+    pdl_trigger();
+    pdl_wait();
+    __shared__ double sh_[4];
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        const double gam = warp_sum(slot[j].rz[l]), rr = warp_sum(slot[j].rr[l]), del = warp_sum(slot[j].pHp[l]);
+        const double gam0 = j > 0 ? warp_sum(slot[j - 1].rz[l]) : 0.0;
+        if (l == 0) { sh_[0] = gam; sh_[1] = rr; sh_[2] = del; sh_[3] = gam0; }
+    }
+    __syncthreads();
+    const double gam = sh_[0], rr = sh_[1], del = sh_[2], gam0 = sh_[3];
+    const int done = sc->cg_done_iter;
+    if ((done >= 0 && done <= j) || (j > 0 && rr <= thr)) return;
+    const double beta_d = j > 0 ? gam / gam0 : 0.0;
+    const double eta = del - (j > 0 ? beta_d * gam / slot[j - 1].alpha : 0.0);
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if (!(eta > 0.0)) {  // negative curvature: stop; at j == 0 the step is u_0 = D^-1 r_0 (= z_0)
+        if (j == 0)
+            for (int64_t i = w0 * 32 + lane; i < n; i += nw * 32)
+#pragma unroll
+                for (int c = 0; c < 3; c++) x[c * S + i] = invD[c * S + i] * r[c * S + i];
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            sc->neg_curv = 1;
+            sc->cg_done_iter = j + 1;
+        }
+        return;
+    }
+    const double alpha_d = gam / eta;
+    if (blockIdx.x == 0 && threadIdx.x == 0) slot[j].alpha = alpha_d;
+    const T alpha = T(alpha_d), beta = T(beta_d);
+    T gsum = 0, rsum = 0;
+    auto chunk = [&](int64_t base, auto full) {
+        constexpr bool FULL = decltype(full)::value;
+        int li[E];
+        T iv[E][3], rv[E][3], pv[E][3], sv[E][3], xv[E][3];
+        vec4<T> wv[E];
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            const int64_t i = base + 32 * e + lane;
+            if (FULL || i < n) {
+                li[e] = list[i];
+#pragma unroll
+                for (int c = 0; c < 3; c++) {
+                    iv[e][c] = invD[c * S + i]; rv[e][c] = r[c * S + i]; pv[e][c] = p[c * S + i];
+                    sv[e][c] = s_[c * S + i]; xv[e][c] = x[c * S + i];
+                }
+            } else {
+                li[e] = -1;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < E; e++)
+            if (FULL || li[e] >= 0) wv[e] = w[li[e]];
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            if (!FULL && li[e] < 0) continue;
+            const int64_t i = base + 32 * e + lane;
+            const T wc[3] = {wv[e].x, wv[e].y, wv[e].z};
+            T un[3];
+#pragma unroll
+            for (int c = 0; c < 3; c++) {
+                // prescribed DOFs (1/D = 0): r, u, p, s stay 0 (the Hessian is projected onto free DOFs)
+                const T fr = iv[e][c] != T(0) ? T(1) : T(0);
+                const T pn = iv[e][c] * rv[e][c] + beta * pv[e][c];
+                const T sn = fr * (wc[c] + beta * sv[e][c]);
+                xv[e][c] += alpha * pn;
+                rv[e][c] -= alpha * sn;
+                un[c] = iv[e][c] * rv[e][c];
+                p[c * S + i] = pn;
+                s_[c * S + i] = sn;
+                x[c * S + i] = xv[e][c];
+                r[c * S + i] = rv[e][c];
+            }
+            u[li[e]] = mk4<T>(un[0], un[1], un[2], T(0));
+            w[li[e]] = mk4<T>(0, 0, 0, 0);
+            const T ow = own ? T(own[li[e]]) : T(1);
+            gsum += ow * (rv[e][0] * un[0] + rv[e][1] * un[1] + rv[e][2] * un[2]);
+            rsum += ow * (rv[e][0] * rv[e][0] + rv[e][1] * rv[e][1] + rv[e][2] * rv[e][2]);
+        }
+    };
+    for (int64_t ch = w0; ch * 32 * E < n; ch += nw) {
+        const int64_t base = ch * 32 * E;
+        if (base + 32 * E <= n) chunk(base, std::true_type{});
+        else chunk(base, std::false_type{});
+    }
+    block_add((double)gsum, slot[j + 1].rz);
+    block_add((double)rsum, slot[j + 1].rr);
+}
+
 // g . x over free DOFs (g tile-dense, x compact SoA)
 template <class T>
 __global__ void k_dot_gx(int64_t n, int64_t S, const int *__restrict__ list, const uint8_t *__restrict__ flag,
@@ -1210,9 +1318,27 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     MPL_CHECK(ensure(ctx, ctx->n_r, (size_t)3 * SA * sizeof(T) + 64));
     T *invD = (T *)ctx->n_invD.p, *x = (T *)ctx->n_x.p, *r = (T *)ctx->n_r.p;
     // p and Hp in one allocation (Hp = p + NT), so one L2 access-policy window can cover both
-    MPL_CHECK(ensure(ctx, ctx->n_p, (size_t)2 * NT * sizeof(vec4<T>) + 64));
+    // cg1 keeps a second HVP output buffer: the vector kernel of iteration j zeroes w_j while HVP_{j+1}
+    // writes the other one, zeroed an iteration earlier (zeroing right before the HVP that writes the same
+    // buffer left its dirty lines to be written back during that HVP)
+    MPL_CHECK(ensure(ctx, ctx->n_p, (size_t)3 * NT * sizeof(vec4<T>) + 64));
     vec4<T> *p = (vec4<T> *)ctx->n_p.p, *Hp = p + NT;
     const uint8_t *own_w = multi(ctx) ? own : nullptr;  // dot-product owner weights (slab ranks)
+    // PCG form (MPL_PCG): "cg1" single-reduction recurrence (one vector kernel and one allreduce per
+    // iteration: the default on slab ranks, where an allreduce costs more than the kernel) or "classic"
+    // Hestenes-Stiefel with two vector kernels (the default on one GPU: cfg4 PCG 50.7 ms vs 56.1 ms cg1,
+    // whose 13-stream vector kernel runs 71 us vs 60 us for the two, and whose HVP writes into a w
+    // zeroed one iteration earlier: 100.6 vs 95.2 us; profiles/r02_pcg_forms.json)
+    const char *pcge = getenv("MPL_PCG");
+    const bool cg1 = pcge ? pcge[0] != 'c' : multi(ctx);
+    const char *cge = getenv("MPL_CG1_E");  // nodes per lane per chunk of the cg1 vector kernel (2 or 4)
+    const int cg1_e = cge ? atoi(cge) : 2;
+    T *pc = nullptr, *sc_ = nullptr;  // cg1: compact p, s
+    if (cg1) {
+        MPL_CHECK(ensure(ctx, ctx->n_ps, (size_t)6 * SA * sizeof(T) + 64));
+        pc = (T *)ctx->n_ps.p;
+        sc_ = pc + 3 * SA;
+    }
     const char *pme = getenv("MPL_PCG_MAP");
     // warp-interleaved update kernels (fp32 default; the fp64 instances spill, MPL_PCG_MAP=group / warp)
     const bool pcg_warp_map = pme ? pme[0] == 'w' : sizeof(T) == 4;
@@ -1293,7 +1419,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     const bool hvp_events = !(hve && hve[0] == '0');
     // MPL_VEC_EVENTS=1: also time the PCG vector kernels (stats.ms_phase[1])
     const char *vee = getenv("MPL_VEC_EVENTS");
-    const bool vec_events = vee && (vee[0] == '1' || vee[0] == '2');
+    const bool vec_events = vee && (vee[0] == '1' || vee[0] == '2') && !cg1;  // classic PCG only
     std::vector<std::array<cudaEvent_t, 3>> vev;  // before update1, between, after update2
     double t_lin = 0, t_pcg = 0, t_ls = 0;
     auto elapsed = [&](cudaEvent_t a, cudaEvent_t b) {
@@ -1315,6 +1441,10 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         ctx->launches++;
         MPL_CHECK(allreduce_d(ctx, slots[0].rz, 3 * NSTRIPE));
         MPL_CUDA(cudaMemsetAsync(Hp, 0, NT * sizeof(vec4<T>), st));
+        if (cg1) {
+            MPL_CUDA(cudaMemsetAsync(pc, 0, (size_t)6 * SA * sizeof(T), st));  // p_{-1} = s_{-1} = 0
+            MPL_CUDA(cudaMemsetAsync(Hp + NT, 0, NT * sizeof(vec4<T>), st));  // the second w buffer
+        }
         cudaEventRecord(e1, st);
         CGSlot s0;
         double e[NSTRIPE + 1];
@@ -1355,6 +1485,51 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                         }
                     }
                     const bool timed = hvp_events && (jj % HVP_SAMPLE == 0);
+                    if (cg1) {
+                        // iteration jj: [HVP_0 once] -> vector kernel jj -> HVP_{jj+1} (+ halo, one allreduce)
+                        auto wbuf = [&](int i) { return Hp + (int64_t)(i & 1) * NT; };  // w_i
+                        if (jj == 0) {
+                            if (timed) cudaEventRecord(hev[nl].first, st);
+                            MPL_CHECK(launch_hvp<T>(ctx, p, wbuf(0), slots[0].pHp, slots, 0, thr));
+                            if (multi(ctx)) {
+                                MPL_CHECK(halo_sum_nodes<T>(ctx, wbuf(0), nullptr));
+                                MPL_CHECK(allreduce_d(ctx, slots[0].pHp, NSTRIPE));
+                            }
+                            if (timed) {
+                                cudaEventRecord(hev[nl].second, st);
+                                sampled.push_back({nl, 0});
+                            }
+                            nl++;
+                            if ((int)hev.size() <= nl) {
+                                cudaEvent_t a, b;
+                                cudaEventCreate(&a);
+                                cudaEventCreate(&b);
+                                hev.push_back({a, b});
+                            }
+                        }
+                        if (cg1_e == 4)
+                            MPL_CUDA(launch_pdl(k_pcg_cg1<T, 4>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p, wbuf(jj),
+                                                x, r, pc, sc_, own_w, slots, sc));
+                        else
+                            MPL_CUDA(launch_pdl(k_pcg_cg1<T, 2>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p, wbuf(jj),
+                                                x, r, pc, sc_, own_w, slots, sc));
+                        ctx->launches++;
+                        const bool timed1 = hvp_events && ((jj + 1) % HVP_SAMPLE == 0);
+                        if (timed1) cudaEventRecord(hev[nl].first, st);
+                        // on slab ranks slot jj+1 is not reduced yet: skip on the previous (reduced) residual
+                        MPL_CHECK(launch_hvp<T>(ctx, p, wbuf(jj + 1), slots[jj + 1].pHp, slots, multi(ctx) ? jj : jj + 1,
+                                                thr));
+                        if (multi(ctx)) {
+                            MPL_CHECK(halo_sum_nodes<T>(ctx, wbuf(jj + 1), nullptr));
+                            MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 3 * NSTRIPE));  // gamma, r.r, delta
+                        }
+                        if (timed1) {
+                            cudaEventRecord(hev[nl].second, st);
+                            sampled.push_back({nl, jj + 1});
+                        }
+                        nl++;
+                        continue;
+                    }
                     if (timed) cudaEventRecord(hev[nl].first, st);
                     // the HVP is skipped on device once converged (its output is then unused)
                     MPL_CHECK(launch_hvp<T>(ctx, p, Hp, slots[jj].pHp, slots, jj, thr));

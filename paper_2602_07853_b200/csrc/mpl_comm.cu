@@ -23,6 +23,7 @@
 
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <chrono>
 #include <condition_variable>
 #include <cstdlib>
@@ -249,41 +250,37 @@ __global__ void k_interface_lists(int T_, const int *__restrict__ coord, int xlo
     if (bx == xhi) hi_list[atomicAdd(&counts[1], 1)] = t;
 }
 
-// plane point of node (lx, ly, lz) of tile t: (4 by + ly) * 4 NB2 + 4 bz + lz.  The plane spans the
-// node-block extent (4 nb[1] x 4 nb[2] >= (N1+1) x (N2+1)): padding slots of the last blocks map too.
-__device__ __forceinline__ int64_t plane_idx(const GridP &g, const int *coord, int t, int ly, int lz) {
-    return (int64_t)(coord[3 * t + 1] * 4 + ly) * (4 * g.nb[2]) + coord[3 * t + 2] * 4 + lz;
-}
-
-// pack nv node vectors of the lx-plane of the listed tiles into dst (nv vec4 per plane point)
+// Compact face messages: entry k of a (sorted) face list carries the 16 nodes (ly, lz) of the tile's
+// node plane lx, nv vectors each, at dst[(16 k + 4 ly + lz) nv + v].
 template <class T>
-__global__ void k_plane_pack(GridP g, const int *__restrict__ list, const int *__restrict__ coord, int lx, int nv,
-                             const vec4<T> *__restrict__ a, const vec4<T> *__restrict__ b, vec4<T> *__restrict__ dst) {
+__global__ void k_face_pack(const int *__restrict__ list, int lx, int nv, const vec4<T> *__restrict__ a,
+                            const vec4<T> *__restrict__ b, vec4<T> *__restrict__ dst) {
     const int t = list[blockIdx.x];
     const int ly = threadIdx.x >> 2, lz = threadIdx.x & 3;
     const int64_t n = (int64_t)t * 64 + local_id(lx, ly, lz);
-    const int64_t q = plane_idx(g, coord, t, ly, lz) * nv;
-    DASSERT(t >= 0 && q >= 0 && q + nv <= (int64_t)16 * g.nb[1] * g.nb[2] * nv);
+    const int64_t q = ((int64_t)blockIdx.x * 16 + threadIdx.x) * nv;
     dst[q] = a[n];
     if (nv > 1) dst[q + 1] = b[n];
 }
 
-// MODE 0: add (sum of partials); MODE 1: set (ghost values)
+// received entry k (the neighbour's k-th face tile) -> local tile map[k] (-1: not held here, the
+// neighbour's partial is then complete on its own); MODE 0: add (sum of partials), MODE 1: set (ghost)
 template <class T, int MODE>
-__global__ void k_plane_unpack(GridP g, const int *__restrict__ list, const int *__restrict__ coord, int lx, int nv,
-                               const vec4<T> *__restrict__ src, vec4<T> *__restrict__ a, vec4<T> *__restrict__ b) {
-    const int t = list[blockIdx.x];
+__global__ void k_face_unpack(const int *__restrict__ map, int lx, int nv, const vec4<T> *__restrict__ src,
+                              vec4<T> *__restrict__ a, vec4<T> *__restrict__ b) {
+    const int t = map[blockIdx.x];
+    if (t < 0) return;
     const int ly = threadIdx.x >> 2, lz = threadIdx.x & 3;
     const int64_t n = (int64_t)t * 64 + local_id(lx, ly, lz);
-    const int64_t q = plane_idx(g, coord, t, ly, lz) * nv;
-    DASSERT(t >= 0 && q >= 0 && q + nv <= (int64_t)16 * g.nb[1] * g.nb[2] * nv);
-    vec4<T> s = src[q];
+    const int64_t q = ((int64_t)blockIdx.x * 16 + threadIdx.x) * nv;
+    const vec4<T> s = src[q];
     if (MODE == 0) {
         vec4<T> x = a[n];
         x.x += s.x; x.y += s.y; x.z += s.z; x.w += s.w;
         a[n] = x;
         if (nv > 1) {
-            vec4<T> s2 = src[q + 1], y = b[n];
+            const vec4<T> s2 = src[q + 1];
+            vec4<T> y = b[n];
             y.x += s2.x; y.y += s2.y; y.z += s2.z; y.w += s2.w;
             b[n] = y;
         }
@@ -292,29 +289,20 @@ __global__ void k_plane_unpack(GridP g, const int *__restrict__ list, const int 
     }
 }
 
-// C2N halo: pack (mv, m) partials plus a presence marker; on unpack the upper neighbour's presence
-// makes it the owner of the shared node (this rank's copy is then not counted in dots / energy).
+// C2N halo: (mv, m) partials of plane lx = 0; a tile the upper neighbour holds makes it the owner of
+// the shared nodes (this rank's copy is then not counted in dots / energy)
 template <class T>
-__global__ void k_c2n_pack(GridP g, const int *__restrict__ list, const int *__restrict__ coord,
-                           const vec4<T> *__restrict__ mvm, vec4<T> *__restrict__ dst) {
-    const int t = list[blockIdx.x];
+__global__ void k_c2n_face_unpack(const int *__restrict__ map, int upper, const vec4<T> *__restrict__ src,
+                                  vec4<T> *__restrict__ mvm, uint8_t *__restrict__ own) {
+    const int t = map[blockIdx.x];
+    if (t < 0) return;
     const int ly = threadIdx.x >> 2, lz = threadIdx.x & 3;
     const int64_t n = (int64_t)t * 64 + local_id(0, ly, lz);
-    const int64_t q = plane_idx(g, coord, t, ly, lz) * 2;
-    dst[q] = mvm[n];
-    dst[q + 1] = mk4<T>(T(1), T(0), T(0), T(0));
-}
-template <class T>
-__global__ void k_c2n_unpack(GridP g, const int *__restrict__ list, const int *__restrict__ coord, int upper,
-                             const vec4<T> *__restrict__ src, vec4<T> *__restrict__ mvm, uint8_t *__restrict__ own) {
-    const int t = list[blockIdx.x];
-    const int ly = threadIdx.x >> 2, lz = threadIdx.x & 3;
-    const int64_t n = (int64_t)t * 64 + local_id(0, ly, lz);
-    const int64_t q = plane_idx(g, coord, t, ly, lz) * 2;
-    vec4<T> s = src[q], x = mvm[n];
+    const vec4<T> s = src[(int64_t)blockIdx.x * 16 + threadIdx.x];
+    vec4<T> x = mvm[n];
     x.x += s.x; x.y += s.y; x.z += s.z; x.w += s.w;
     mvm[n] = x;
-    if (upper && src[q + 1].x != T(0)) own[n] = 0;
+    if (upper) own[n] = 0;
 }
 
 inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
@@ -562,6 +550,24 @@ mpl_status debug_check_tiles(mpl_ctx ctx, const char *where) {
     return MPL_OK;
 }
 
+namespace {
+// exchange one int64 count with each neighbour: returns (from lower, from upper)
+mpl_status exchange_counts(mpl_ctx ctx, unsigned long long to_lo, unsigned long long to_hi, unsigned long long *from_lo,
+                           unsigned long long *from_hi) {
+    MPL_CHECK(ensure(ctx, ctx->mig_cnt, 256));
+    unsigned long long h[4] = {to_lo, to_hi, 0, 0};
+    unsigned long long *d = (unsigned long long *)ctx->mig_cnt.p + 24;
+    MPL_CUDA(cudaMemcpyAsync(d, h, 16, cudaMemcpyHostToDevice, ctx->stream));
+    MPL_CUDA(cudaMemsetAsync(d + 2, 0, 16, ctx->stream));
+    MPL_CHECK(ctx->comm->neighbors(ctx, d + 0, 8, d + 2, 8, d + 1, 8, d + 3, 8));
+    MPL_CUDA(cudaMemcpyAsync(h, d, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    MPL_CUDA(cudaStreamSynchronize(ctx->stream));
+    *from_lo = ctx->rank > 0 ? h[2] : 0;
+    *from_hi = ctx->rank < ctx->nranks - 1 ? h[3] : 0;
+    return MPL_OK;
+}
+}  // namespace
+
 mpl_status build_interface_lists(mpl_ctx ctx) {
     if (!multi(ctx)) return MPL_OK;
     const int T_ = ctx->T;
@@ -581,85 +587,139 @@ mpl_status build_interface_lists(mpl_ctx ctx) {
     MPL_CUDA(cudaStreamSynchronize(st));
     ctx->n_lo_tiles = h[0];
     ctx->n_hi_tiles = h[1];
+    // sort both face lists by (by, bz) on the host (a few thousand tiles), exchange the keys with the
+    // neighbours and match the neighbour's entries to local tiles
+    std::vector<int> coord((size_t)3 * T_);
+    if (T_) MPL_CUDA(cudaMemcpy(coord.data(), ctx->t_coord.p, coord.size() * 4, cudaMemcpyDeviceToHost));
+    const int64_t NB2 = ctx->grid.nb[2];
+    auto sorted = [&](DevBuf &list, int n, std::vector<int> &tiles, std::vector<int> &keys) -> mpl_status {
+        tiles.resize(n);
+        if (n) MPL_CUDA(cudaMemcpy(tiles.data(), list.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
+        std::sort(tiles.begin(), tiles.end(), [&](int a, int b) {
+            return coord[3 * a + 1] * NB2 + coord[3 * a + 2] < coord[3 * b + 1] * NB2 + coord[3 * b + 2];
+        });
+        keys.resize(n);
+        for (int i = 0; i < n; i++) keys[i] = (int)(coord[3 * tiles[i] + 1] * NB2 + coord[3 * tiles[i] + 2]);
+        if (n) MPL_CUDA(cudaMemcpy(list.p, tiles.data(), (size_t)n * 4, cudaMemcpyHostToDevice));
+        return MPL_OK;
+    };
+    std::vector<int> lo_t, lo_k, hi_t, hi_k;
+    MPL_CHECK(sorted(ctx->t_lo_list, ctx->n_lo_tiles, lo_t, lo_k));
+    MPL_CHECK(sorted(ctx->t_hi_list, ctx->n_hi_tiles, hi_t, hi_k));
+    const bool lo = ctx->rank > 0, hi = ctx->rank < ctx->nranks - 1;
+    unsigned long long from_lo = 0, from_hi = 0;
+    MPL_CHECK(exchange_counts(ctx, lo ? ctx->n_lo_tiles : 0, hi ? ctx->n_hi_tiles : 0, &from_lo, &from_hi));
+    ctx->n_lo_recv = (int)from_lo;  // the lower neighbour's upper-face tiles
+    ctx->n_hi_recv = (int)from_hi;  // the upper neighbour's lower-face tiles
+    DevBuf ks_lo, ks_hi, kr_lo, kr_hi;
+    auto cleanup = [&]() {
+        for (DevBuf *b : {&ks_lo, &ks_hi, &kr_lo, &kr_hi})
+            if (b->p) cudaFree(b->p);
+    };
+    std::vector<int> rl(ctx->n_lo_recv), rh(ctx->n_hi_recv);
+    {
+        mpl_status e = MPL_OK;
+        if (ensure(ctx, ks_lo, lo_k.size() * 4 + 16) || ensure(ctx, ks_hi, hi_k.size() * 4 + 16) ||
+            ensure(ctx, kr_lo, rl.size() * 4 + 16) || ensure(ctx, kr_hi, rh.size() * 4 + 16))
+            e = MPL_ERR_OOM;
+        if (e == MPL_OK && !lo_k.empty()) e = cudaMemcpy(ks_lo.p, lo_k.data(), lo_k.size() * 4, cudaMemcpyHostToDevice) ? MPL_ERR_CUDA : MPL_OK;
+        if (e == MPL_OK && !hi_k.empty()) e = cudaMemcpy(ks_hi.p, hi_k.data(), hi_k.size() * 4, cudaMemcpyHostToDevice) ? MPL_ERR_CUDA : MPL_OK;
+        if (e == MPL_OK)
+            e = ctx->comm->neighbors(ctx, ks_lo.p, lo ? lo_k.size() * 4 : 0, kr_lo.p, lo ? rl.size() * 4 : 0, ks_hi.p,
+                                     hi ? hi_k.size() * 4 : 0, kr_hi.p, hi ? rh.size() * 4 : 0);
+        if (e == MPL_OK && !rl.empty()) e = cudaMemcpy(rl.data(), kr_lo.p, rl.size() * 4, cudaMemcpyDeviceToHost) ? MPL_ERR_CUDA : MPL_OK;
+        if (e == MPL_OK && !rh.empty()) e = cudaMemcpy(rh.data(), kr_hi.p, rh.size() * 4, cudaMemcpyDeviceToHost) ? MPL_ERR_CUDA : MPL_OK;
+        cleanup();
+        if (e != MPL_OK) return e;
+    }
+    // received keys (sorted) -> local tile of the same (by, bz) on that face, or -1
+    auto match = [&](const std::vector<int> &recv, const std::vector<int> &keys, const std::vector<int> &tiles,
+                     DevBuf &map) -> mpl_status {
+        std::vector<int> m(recv.size(), -1);
+        size_t j = 0;
+        for (size_t i = 0; i < recv.size(); i++) {
+            while (j < keys.size() && keys[j] < recv[i]) j++;
+            if (j < keys.size() && keys[j] == recv[i]) m[i] = tiles[j];
+        }
+        MPL_CHECK(ensure(ctx, map, m.size() * 4 + 16));
+        if (!m.empty()) MPL_CUDA(cudaMemcpy(map.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice));
+        return MPL_OK;
+    };
+    MPL_CHECK(match(rl, lo_k, lo_t, ctx->t_lo_map));
+    MPL_CHECK(match(rh, hi_k, hi_t, ctx->t_hi_map));
     return MPL_OK;
 }
 
 namespace {
-size_t plane_points(mpl_ctx ctx) { return (size_t)(4 * ctx->grid.nb[1]) * (4 * ctx->grid.nb[2]); }
-
+// compact face buffers: send = this rank's face tiles, recv = the neighbour's (16 nodes x nv vectors each)
 template <class T>
-mpl_status ensure_planes(mpl_ctx ctx, int nv) {
-    const size_t b = plane_points(ctx) * nv * sizeof(vec4<T>);
-    MPL_CHECK(ensure(ctx, ctx->pl_send_lo, b));
-    MPL_CHECK(ensure(ctx, ctx->pl_send_hi, b));
-    MPL_CHECK(ensure(ctx, ctx->pl_recv_lo, b));
-    MPL_CHECK(ensure(ctx, ctx->pl_recv_hi, b));
+mpl_status ensure_faces(mpl_ctx ctx, int nv) {
+    const size_t per = (size_t)16 * nv * sizeof(vec4<T>);
+    MPL_CHECK(ensure(ctx, ctx->pl_send_lo, per * ctx->n_lo_tiles + 16));
+    MPL_CHECK(ensure(ctx, ctx->pl_send_hi, per * ctx->n_hi_tiles + 16));
+    MPL_CHECK(ensure(ctx, ctx->pl_recv_lo, per * ctx->n_lo_recv + 16));
+    MPL_CHECK(ensure(ctx, ctx->pl_recv_hi, per * ctx->n_hi_recv + 16));
     return MPL_OK;
 }
 }  // namespace
 
+// Sum of the partials of a (and b) on the shared node planes: pack this rank's face tiles (plane
+// lx = 0 of the lower and upper face lists), exchange with both neighbours, add what arrives into the
+// matching local tiles.  Bytes per message: 16 nodes x nv x 16 B (fp32) per face tile.
 template <class T>
 mpl_status halo_sum_nodes(mpl_ctx ctx, void *a_tile, void *b_tile) {
     if (!multi(ctx)) return MPL_OK;
     const int nv = b_tile ? 2 : 1;
-    MPL_CHECK(ensure_planes<T>(ctx, nv));
+    MPL_CHECK(ensure_faces<T>(ctx, nv));
     cudaStream_t st = ctx->stream;
-    const size_t bytes = plane_points(ctx) * nv * sizeof(vec4<T>);
+    const size_t per = (size_t)16 * nv * sizeof(vec4<T>);
     const bool lo = ctx->rank > 0, hi = ctx->rank < ctx->nranks - 1;
-    const GridP &g = ctx->grid;
-    const int *coord = (const int *)ctx->t_coord.p;
-    if (lo) {
-        MPL_CUDA(cudaMemsetAsync(ctx->pl_send_lo.p, 0, bytes, st));
-        if (ctx->n_lo_tiles)
-            k_plane_pack<T><<<ctx->n_lo_tiles, 16, 0, st>>>(g, (const int *)ctx->t_lo_list.p, coord, 0, nv,
-                                                             (const vec4<T> *)a_tile, (const vec4<T> *)b_tile,
-                                                             (vec4<T> *)ctx->pl_send_lo.p), ctx->launches++;
-    }
-    if (hi) {
-        MPL_CUDA(cudaMemsetAsync(ctx->pl_send_hi.p, 0, bytes, st));
-        if (ctx->n_hi_tiles)
-            k_plane_pack<T><<<ctx->n_hi_tiles, 16, 0, st>>>(g, (const int *)ctx->t_hi_list.p, coord, 0, nv,
-                                                             (const vec4<T> *)a_tile, (const vec4<T> *)b_tile,
-                                                             (vec4<T> *)ctx->pl_send_hi.p), ctx->launches++;
-    }
-    MPL_CUDA(cudaGetLastError());
-    MPL_CHECK(ctx->comm->neighbors(ctx, ctx->pl_send_lo.p, lo ? bytes : 0, ctx->pl_recv_lo.p, lo ? bytes : 0,
-                                   ctx->pl_send_hi.p, hi ? bytes : 0, ctx->pl_recv_hi.p, hi ? bytes : 0));
     if (lo && ctx->n_lo_tiles)
-        k_plane_unpack<T, 0><<<ctx->n_lo_tiles, 16, 0, st>>>(g, (const int *)ctx->t_lo_list.p, coord, 0, nv,
-                                                             (const vec4<T> *)ctx->pl_recv_lo.p, (vec4<T> *)a_tile,
-                                                             (vec4<T> *)b_tile), ctx->launches++;
+        k_face_pack<T><<<ctx->n_lo_tiles, 16, 0, st>>>((const int *)ctx->t_lo_list.p, 0, nv, (const vec4<T> *)a_tile,
+                                                       (const vec4<T> *)b_tile, (vec4<T> *)ctx->pl_send_lo.p),
+            ctx->launches++;
     if (hi && ctx->n_hi_tiles)
-        k_plane_unpack<T, 0><<<ctx->n_hi_tiles, 16, 0, st>>>(g, (const int *)ctx->t_hi_list.p, coord, 0, nv,
-                                                             (const vec4<T> *)ctx->pl_recv_hi.p, (vec4<T> *)a_tile,
-                                                             (vec4<T> *)b_tile), ctx->launches++;
+        k_face_pack<T><<<ctx->n_hi_tiles, 16, 0, st>>>((const int *)ctx->t_hi_list.p, 0, nv, (const vec4<T> *)a_tile,
+                                                       (const vec4<T> *)b_tile, (vec4<T> *)ctx->pl_send_hi.p),
+            ctx->launches++;
+    MPL_CUDA(cudaGetLastError());
+    MPL_CHECK(ctx->comm->neighbors(ctx, ctx->pl_send_lo.p, lo ? per * ctx->n_lo_tiles : 0, ctx->pl_recv_lo.p,
+                                   lo ? per * ctx->n_lo_recv : 0, ctx->pl_send_hi.p, hi ? per * ctx->n_hi_tiles : 0,
+                                   ctx->pl_recv_hi.p, hi ? per * ctx->n_hi_recv : 0));
+    if (lo && ctx->n_lo_recv)
+        k_face_unpack<T, 0><<<ctx->n_lo_recv, 16, 0, st>>>((const int *)ctx->t_lo_map.p, 0, nv,
+                                                           (const vec4<T> *)ctx->pl_recv_lo.p, (vec4<T> *)a_tile,
+                                                           (vec4<T> *)b_tile),
+            ctx->launches++;
+    if (hi && ctx->n_hi_recv)
+        k_face_unpack<T, 0><<<ctx->n_hi_recv, 16, 0, st>>>((const int *)ctx->t_hi_map.p, 0, nv,
+                                                           (const vec4<T> *)ctx->pl_recv_hi.p, (vec4<T> *)a_tile,
+                                                           (vec4<T> *)b_tile),
+            ctx->launches++;
     MPL_CUDA(cudaGetLastError());
     return MPL_OK;
 }
 
+// G2P ghosts: the upper neighbour's second node plane (x = 4 X_{r+1} + 1, its lower face at lx = 1)
 template <class T>
 mpl_status ghost_nodes_from_upper(mpl_ctx ctx, void *v_tile) {
     if (!multi(ctx)) return MPL_OK;
-    MPL_CHECK(ensure_planes<T>(ctx, 1));
+    MPL_CHECK(ensure_faces<T>(ctx, 1));
     cudaStream_t st = ctx->stream;
-    const size_t bytes = plane_points(ctx) * sizeof(vec4<T>);
+    const size_t per = (size_t)16 * sizeof(vec4<T>);
     const bool lo = ctx->rank > 0, hi = ctx->rank < ctx->nranks - 1;
-    const GridP &g = ctx->grid;
-    const int *coord = (const int *)ctx->t_coord.p;
-    if (lo) {  // my second node plane (x = 4 X_r + 1) -> rank-1
-        MPL_CUDA(cudaMemsetAsync(ctx->pl_send_lo.p, 0, bytes, st));
-        if (ctx->n_lo_tiles)
-            k_plane_pack<T><<<ctx->n_lo_tiles, 16, 0, st>>>(g, (const int *)ctx->t_lo_list.p, coord, 1, 1,
-                                                             (const vec4<T> *)v_tile, nullptr,
-                                                             (vec4<T> *)ctx->pl_send_lo.p), ctx->launches++;
-    }
+    if (lo && ctx->n_lo_tiles)
+        k_face_pack<T><<<ctx->n_lo_tiles, 16, 0, st>>>((const int *)ctx->t_lo_list.p, 1, 1, (const vec4<T> *)v_tile,
+                                                       nullptr, (vec4<T> *)ctx->pl_send_lo.p),
+            ctx->launches++;
     MPL_CUDA(cudaGetLastError());
-    MPL_CHECK(ctx->comm->neighbors(ctx, ctx->pl_send_lo.p, lo ? bytes : 0, nullptr, 0, nullptr, 0, ctx->pl_recv_hi.p,
-                                   hi ? bytes : 0));
-    if (hi && ctx->n_hi_tiles)
-        k_plane_unpack<T, 1><<<ctx->n_hi_tiles, 16, 0, st>>>(g, (const int *)ctx->t_hi_list.p, coord, 1, 1,
-                                                             (const vec4<T> *)ctx->pl_recv_hi.p, (vec4<T> *)v_tile,
-                                                             nullptr), ctx->launches++;
+    MPL_CHECK(ctx->comm->neighbors(ctx, ctx->pl_send_lo.p, lo ? per * ctx->n_lo_tiles : 0, nullptr, 0, nullptr, 0,
+                                   ctx->pl_recv_hi.p, hi ? per * ctx->n_hi_recv : 0));
+    if (hi && ctx->n_hi_recv)
+        k_face_unpack<T, 1><<<ctx->n_hi_recv, 16, 0, st>>>((const int *)ctx->t_hi_map.p, 1, 1,
+                                                           (const vec4<T> *)ctx->pl_recv_hi.p, (vec4<T> *)v_tile,
+                                                           nullptr),
+            ctx->launches++;
     MPL_CUDA(cudaGetLastError());
     return MPL_OK;
 }
@@ -668,57 +728,37 @@ mpl_status ghost_nodes_from_upper(mpl_ctx ctx, void *v_tile) {
 template <class T>
 mpl_status c2n_halo(mpl_ctx ctx) {
     if (!multi(ctx)) return MPL_OK;
-    MPL_CHECK(ensure_planes<T>(ctx, 2));
+    MPL_CHECK(ensure_faces<T>(ctx, 1));
     cudaStream_t st = ctx->stream;
-    const size_t bytes = plane_points(ctx) * 2 * sizeof(vec4<T>);
+    const size_t per = (size_t)16 * sizeof(vec4<T>);
     const bool lo = ctx->rank > 0, hi = ctx->rank < ctx->nranks - 1;
-    const GridP &g = ctx->grid;
-    const int *coord = (const int *)ctx->t_coord.p;
     vec4<T> *mvm = (vec4<T> *)ctx->n_vn.p;
-    if (lo) {
-        MPL_CUDA(cudaMemsetAsync(ctx->pl_send_lo.p, 0, bytes, st));
-        if (ctx->n_lo_tiles)
-            k_c2n_pack<T><<<ctx->n_lo_tiles, 16, 0, st>>>(g, (const int *)ctx->t_lo_list.p, coord, mvm,
-                                                           (vec4<T> *)ctx->pl_send_lo.p), ctx->launches++;
-    }
-    if (hi) {
-        MPL_CUDA(cudaMemsetAsync(ctx->pl_send_hi.p, 0, bytes, st));
-        if (ctx->n_hi_tiles)
-            k_c2n_pack<T><<<ctx->n_hi_tiles, 16, 0, st>>>(g, (const int *)ctx->t_hi_list.p, coord, mvm,
-                                                           (vec4<T> *)ctx->pl_send_hi.p), ctx->launches++;
-    }
-    MPL_CUDA(cudaGetLastError());
-    MPL_CHECK(ctx->comm->neighbors(ctx, ctx->pl_send_lo.p, lo ? bytes : 0, ctx->pl_recv_lo.p, lo ? bytes : 0,
-                                   ctx->pl_send_hi.p, hi ? bytes : 0, ctx->pl_recv_hi.p, hi ? bytes : 0));
     if (lo && ctx->n_lo_tiles)
-        k_c2n_unpack<T><<<ctx->n_lo_tiles, 16, 0, st>>>(g, (const int *)ctx->t_lo_list.p, coord, 0,
-                                                        (const vec4<T> *)ctx->pl_recv_lo.p, mvm,
-                                                        (uint8_t *)ctx->n_own.p), ctx->launches++;
+        k_face_pack<T><<<ctx->n_lo_tiles, 16, 0, st>>>((const int *)ctx->t_lo_list.p, 0, 1, mvm, nullptr,
+                                                       (vec4<T> *)ctx->pl_send_lo.p),
+            ctx->launches++;
     if (hi && ctx->n_hi_tiles)
-        k_c2n_unpack<T><<<ctx->n_hi_tiles, 16, 0, st>>>(g, (const int *)ctx->t_hi_list.p, coord, 1,
-                                                        (const vec4<T> *)ctx->pl_recv_hi.p, mvm,
-                                                        (uint8_t *)ctx->n_own.p), ctx->launches++;
+        k_face_pack<T><<<ctx->n_hi_tiles, 16, 0, st>>>((const int *)ctx->t_hi_list.p, 0, 1, mvm, nullptr,
+                                                       (vec4<T> *)ctx->pl_send_hi.p),
+            ctx->launches++;
+    MPL_CUDA(cudaGetLastError());
+    MPL_CHECK(ctx->comm->neighbors(ctx, ctx->pl_send_lo.p, lo ? per * ctx->n_lo_tiles : 0, ctx->pl_recv_lo.p,
+                                   lo ? per * ctx->n_lo_recv : 0, ctx->pl_send_hi.p, hi ? per * ctx->n_hi_tiles : 0,
+                                   ctx->pl_recv_hi.p, hi ? per * ctx->n_hi_recv : 0));
+    if (lo && ctx->n_lo_recv)
+        k_c2n_face_unpack<T><<<ctx->n_lo_recv, 16, 0, st>>>((const int *)ctx->t_lo_map.p, 0,
+                                                            (const vec4<T> *)ctx->pl_recv_lo.p, mvm,
+                                                            (uint8_t *)ctx->n_own.p),
+            ctx->launches++;
+    if (hi && ctx->n_hi_recv)
+        k_c2n_face_unpack<T><<<ctx->n_hi_recv, 16, 0, st>>>((const int *)ctx->t_hi_map.p, 1,
+                                                            (const vec4<T> *)ctx->pl_recv_hi.p, mvm,
+                                                            (uint8_t *)ctx->n_own.p),
+            ctx->launches++;
     MPL_CUDA(cudaGetLastError());
     return MPL_OK;
 }
 
-namespace {
-// exchange one int64 count with each neighbour: returns (from lower, from upper)
-mpl_status exchange_counts(mpl_ctx ctx, unsigned long long to_lo, unsigned long long to_hi, unsigned long long *from_lo,
-                           unsigned long long *from_hi) {
-    MPL_CHECK(ensure(ctx, ctx->mig_cnt, 256));
-    unsigned long long h[4] = {to_lo, to_hi, 0, 0};
-    unsigned long long *d = (unsigned long long *)ctx->mig_cnt.p + 24;
-    MPL_CUDA(cudaMemcpyAsync(d, h, 16, cudaMemcpyHostToDevice, ctx->stream));
-    MPL_CUDA(cudaMemsetAsync(d + 2, 0, 16, ctx->stream));
-    MPL_CHECK(ctx->comm->neighbors(ctx, d + 0, 8, d + 2, 8, d + 1, 8, d + 3, 8));
-    MPL_CUDA(cudaMemcpyAsync(h, d, 32, cudaMemcpyDeviceToHost, ctx->stream));
-    MPL_CUDA(cudaStreamSynchronize(ctx->stream));
-    *from_lo = ctx->rank > 0 ? h[2] : 0;
-    *from_hi = ctx->rank < ctx->nranks - 1 ? h[3] : 0;
-    return MPL_OK;
-}
-}  // namespace
 
 // Start of every resample on a slab rank: drop last step's ghosts, send particles that left the slab
 // to the neighbour that now owns them, then copy the last owned cell plane to the upper neighbour as

@@ -375,7 +375,8 @@ struct DevBuf {
 struct CGSlot {
     double rz[NSTRIPE];   // r_j . z_j   (striped)
     double rr[NSTRIPE];   // r_j . r_j
-    double pHp[NSTRIPE];  // p_j . H p_j
+    double pHp[NSTRIPE];  // p_j . H p_j  (single-reduction PCG: u_j . H u_j)
+    double alpha, pad;    // single-reduction PCG: the step alpha_j, written by iteration j's vector kernel
 };
 
 // device-side scalar block (fp64 accumulators and flags)
@@ -414,9 +415,12 @@ struct mpl_ctx_s {
     int64_t np_own = 0;                    // owned particles (the rest of np are ghosts, pid < 0)
     DevBuf pv_alt, pG_alt;                 // redistribution targets for v, G
     DevBuf mig_send_lo, mig_send_hi, mig_recv_lo, mig_recv_hi, mig_cnt;
-    DevBuf pl_send_lo, pl_send_hi, pl_recv_lo, pl_recv_hi;  // dense node-plane halo buffers
-    DevBuf t_lo_list, t_hi_list;           // tiles on the lower / upper interface node-block planes
-    int n_lo_tiles = 0, n_hi_tiles = 0;
+    DevBuf pl_send_lo, pl_send_hi, pl_recv_lo, pl_recv_hi;  // compact interface-face halo buffers
+    // Interface faces: this rank's tiles on the lower / upper shared node-block planes,
+    // sorted by (by, bz); the neighbour's list in the same order arrives once per resample and is matched
+    // to local tiles (map: received entry -> local tile or -1).  A halo message is 16 nodes per listed tile.
+    DevBuf t_lo_list, t_hi_list, t_lo_map, t_hi_map;
+    int n_lo_tiles = 0, n_hi_tiles = 0, n_lo_recv = 0, n_hi_recv = 0;
     DevBuf n_own, n_mown;                  // per node: owner flag (uint8), owned mass (m if owner else 0)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -478,6 +482,7 @@ struct mpl_ctx_s {
     DevBuf n_mass, n_flag, n_vn, n_vhat, n_v, n_vt, n_g, n_diag, n_invD, n_x, n_r, n_p, n_Hp, n_u, n_u2, n_act;
     // canonical node index per tile-dense node (-1 inactive)
     DevBuf n_canon, n_list;  // n_list: canonical -> tile-dense index
+    DevBuf n_ps;             // single-reduction PCG: p and s (= H p) compact SoA, 6 x SA reals
     DevBuf scalars, cg_slots, io_stage, io_stage2;
     int cg_slot_cap = 0;
     DevBuf host_pinned;  // small pinned staging
@@ -623,6 +628,7 @@ template <class F> void for_each_buf(mpl_ctx ctx, F f) {
         {"n_x", ctx->n_x},
         {"n_r", ctx->n_r},
         {"n_p", ctx->n_p},
+        {"n_ps", ctx->n_ps},
         {"n_Hp", ctx->n_Hp},
         {"n_u", ctx->n_u},
         {"n_u2", ctx->n_u2},
@@ -646,6 +652,8 @@ template <class F> void for_each_buf(mpl_ctx ctx, F f) {
         {"pl_recv_hi", ctx->pl_recv_hi},
         {"t_lo_list", ctx->t_lo_list},
         {"t_hi_list", ctx->t_hi_list},
+        {"t_lo_map", ctx->t_lo_map},
+        {"t_hi_map", ctx->t_hi_map},
         {"n_own", ctx->n_own},
         {"n_mown", ctx->n_mown}
     };

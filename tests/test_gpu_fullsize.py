@@ -12,6 +12,8 @@ Cases: cfg2, cfg3 (PPC 8), cfg4 and cfg5B (512^3, ~93M particles: wheel rim, whe
 plate's Dirichlet layer) in fp32 — the bench's configuration — and cfg4 / cfg5B in fp64 (the fp64 HVP
 kernel; cfg5B's "fp64 check" of BASELINE.json config 5).
 Bars: BASELINE.json's (1e-5 fp32 / 1e-10 fp64 on unload / gradient / HVP; the step bars for G2P)."""
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -181,3 +183,37 @@ def test_step_converges_and_g2p_windows(full):
         # deforms (the stiff slab) rounding of v alone is ~eps |v|/dx, so scale by that too (reading r2-b)
         scale = max(np.linalg.norm(G_o[inner]), np.linalg.norm(v_o[inner]) / sc.dx)
         assert np.linalg.norm(G_g[idx] - G_o[inner]) <= tol * scale
+
+
+def test_cfg5_fp32_step_checked_in_fp64():
+    """BASELINE.json config 5, "fp32 solver with an fp64 check": the fp32 implicit step's v^{n+1} is put into
+    an fp64 context of the same (fp32-quantised) scene and its gradient evaluated there; the fp64
+    gradient over the free DOFs must meet the solver's Newton tolerance (x2 for the fp32 evaluation of
+    the stopping test): ||g64(v32)|| <= 2 eps_N ||g64(v0)||."""
+    sc32 = scenes.by_name("cfg5B", 32)
+    ctx = mpl.from_scene(sc32, 0)
+    ctx.resample(sc32.dt)
+    st = ctx.newton_step(sc32.solver)
+    assert st["converged"] == 1
+    ijk32, _, _, _ = ctx.get_nodes()
+    v32 = ctx.get_velocity().astype(np.float64)
+    ctx.close()
+    sc64 = dataclasses.replace(sc32, precision=64, x=sc32.x.astype(np.float64), v=sc32.v.astype(np.float64),
+                               F=sc32.F.astype(np.float64), G=sc32.G.astype(np.float64),
+                               vol=sc32.vol.astype(np.float64))
+    ctx = mpl.from_scene(sc64, 0)
+    ctx.resample(sc64.dt)
+    ijk, _, _, free = ctx.get_nodes()
+    n1, n2 = sc32.n[1] + 1, sc32.n[2] + 1
+    k64 = (ijk[:, 0].astype(np.int64) * n1 + ijk[:, 1]) * n2 + ijk[:, 2]
+    k32 = (ijk32[:, 0].astype(np.int64) * n1 + ijk32[:, 1]) * n2 + ijk32[:, 2]
+    assert np.array_equal(np.sort(k32), np.sort(k64))
+    pos = np.empty(k32.size, np.int64)
+    pos[np.argsort(k64)] = np.argsort(k32)  # fp64 entry i <- fp32 entry pos[i]
+    v0 = ctx.get_velocity()
+    g0, _ = ctx.gradient(v0)
+    g, _ = ctx.gradient(np.ascontiguousarray(v32[pos]))
+    ctx.close()
+    fr = free.astype(bool)
+    ratio = np.linalg.norm(g[fr]) / np.linalg.norm(g0[fr])
+    assert ratio <= 2 * sc32.solver.eps_newton, ratio

@@ -19,6 +19,11 @@ CASES = [
     ({"MPL_PCG_MAP": "group"}, "mix_fp32"),
     ({"MPL_PDL": "0", "MPL_L2WIN": "0"}, "mix_fp32"),
     ({"MPL_PCG_MAP": "warp"}, "mix_fp64"),
+    # single-reduction PCG (the slab-rank default) on one GPU; classic is the one-GPU default
+    ({"MPL_PCG": "cg1"}, "mix_fp32"),
+    ({"MPL_PCG": "cg1", "MPL_CG1_E": "4"}, "mix_fp32"),
+    ({"MPL_PCG": "cg1"}, "mix_fp64"),
+    ({"MPL_PCG": "cg1"}, "psd_fp64"),
 ]
 
 
@@ -27,10 +32,22 @@ CASES = [
     "-".join(f"{k[4:].lower()}={v}" for k, v in e.items()) + f"-{s}" for e, s in CASES])  # noqa: E501
 def test_hvp_variant_parity(env, scene):
     e = dict(os.environ)
-    for k in ("MPL_HVP_KERNEL", "MPL_PCG_MAP", "MPL_PDL", "MPL_L2WIN"):
+    for k in ("MPL_HVP_KERNEL", "MPL_PCG_MAP", "MPL_PDL", "MPL_L2WIN", "MPL_PCG", "MPL_CG1_E"):
         e.pop(k, None)
     e.update(env)
     r = subprocess.run([sys.executable, "-m", "tests._hvp_variant_check", scene], cwd=ROOT, env=e,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "OK" in r.stdout
+
+
+@pytest.mark.gpu
+def test_slab_ranks_with_classic_pcg():
+    """The slab decomposition (loopback ranks) with the two-kernel PCG instead of the slab default
+    (single-reduction): replayed step and multi-step migration parity (tests/test_gpu_slabs.py)."""
+    e = dict(os.environ)
+    e["MPL_PCG"] = "classic"
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "tests/test_gpu_slabs.py", "-k",
+                        "replayed_step or migration_multistep_matches_one_rank"], cwd=ROOT, env=e,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

@@ -12,8 +12,8 @@ halo sum and p.Hp allreduce and is the max over ranks.  `ms_per_step` = implicit
 clock, max over ranks).  Inputs are resident in HBM when the timed region starts; the
 HVP's tangent stream (>= 392 MB at cfg4) is larger than the 126 MB L2.
 
---impl reference times the CPU oracle (oracle/, plain fp64 C, 1 core) on a bounded window of the
-same workload; it is the deliberately slow baseline, not a target.
+--impl reference times the CPU oracle (oracle/, plain fp64 C, OpenMP colour loops on all host cores) on a
+bounded window of the same workload; it is the deliberately slow baseline, not a target.
 """
 from __future__ import annotations
 
@@ -372,8 +372,28 @@ def oracle_window(sc, lo, size):
     return grid, un, S, prob, v0
 
 
-def cpu_baseline(sc, args, budget_s=12.0):
-    """Oracle HVP (plain fp64 C, 1 thread) on a bounded window of the same workload."""
+def _omp_threads(n: int) -> None:
+    """Thread count of the oracle's OpenMP colour loops (libgomp is loaded with liboracle.so)."""
+    import ctypes
+    try:
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+    except OSError:
+        pass
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(sc, args, budget_s=10.0):
+    """Oracle HVP (plain fp64 C; OpenMP colour loops, identical results at any thread count) on a bounded
+    window of the same workload, on all host cores and on one core (SURVEY §8(d) timing protocol)."""
     import oracle
     lo, size = _window_for(sc)
     grid, un, S, prob, v0 = oracle_window(sc, lo, size)
@@ -381,17 +401,28 @@ def cpu_baseline(sc, args, budget_s=12.0):
     act = (prob.m_i > 0)
     u = rng.normal(size=v0.shape) * act[:, None]
     n_free = int(prob.freed.sum())
-    t0 = time.perf_counter()
-    reps = 0
-    while True:
-        prob.hvp(v0, u)
-        reps += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    t = (time.perf_counter() - t0) / reps
-    return {"value": round(3.0 * n_free / t / 1e9, 6), "unit": "GDOF/s", "cores": 1, "kind": "oracle",
-            "sample": f"{reps} oracle HVPs on the {size}^3-cell window at cells {list(map(int, lo))} of {sc.name} "
-                      f"({int((un.m_c > 0).sum())} quadrature points, {n_free} free nodes), {t * 1e3:.1f} ms each"}
+    ncores = os.cpu_count() or 1
+    out = {}
+    for cores in (ncores, 1):
+        _omp_threads(cores)
+        prob.hvp(v0, u)  # warm-up
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            prob.hvp(v0, u)
+            reps += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        out[cores] = ((time.perf_counter() - t0) / reps, reps)
+    _omp_threads(ncores)
+    t, reps = out[ncores]
+    t1, reps1 = out[1]
+    sample = (f"oracle HVPs on the {size}^3-cell window at cells {list(map(int, lo))} of {sc.name} "
+              f"({int((un.m_c > 0).sum())} quadrature points, {n_free} free nodes): {reps} runs on {ncores} threads, "
+              f"{t * 1e3:.2f} ms each; {reps1} runs on 1 thread, {t1 * 1e3:.2f} ms each")
+    return {"value": round(3.0 * n_free / t / 1e9, 6), "unit": "GDOF/s", "cores": ncores, "kind": "oracle",
+            "sample": sample, "cpu_model": _cpu_model(), "nproc": ncores,
+            "single_core": {"value": round(3.0 * n_free / t1 / 1e9, 6), "cores": 1}}
 
 
 def _window_for(sc):
@@ -416,6 +447,8 @@ def run_reference(args):
     rng = np.random.default_rng(4)
     u = rng.normal(size=v0.shape) * (prob.m_i > 0)[:, None]
     n_free = int(prob.freed.sum())
+    ncores = os.cpu_count() or 1
+    _omp_threads(ncores)
     for _ in range(args.warmup):
         prob.hvp(v0, u)
     t0 = time.perf_counter()
@@ -424,7 +457,7 @@ def run_reference(args):
     t = (time.perf_counter() - t0) / args.steps
     val = 3.0 * n_free / t / 1e9
     sample = (f"one oracle HVP per step on the {size}^3-cell window at cells {list(map(int, lo))} of {sc.name} "
-              f"({n_free} free nodes)")
+              f"({n_free} free nodes), {ncores} OpenMP threads")
     print(json.dumps({
         "impl": "reference",
         "metric": "HVP GDOF/s (matrix-free incremental-potential Hessian-vector product inside Newton-PCG)",
@@ -433,7 +466,8 @@ def run_reference(args):
         "dtype": "f64", "data": "synthetic (same seeded scene, windowed)",
         "config": {"workload": workload_name(sc), "sample": sample, "grid": list(sc.n),
                    "particles": sc.n_particles},
-        "cpu_baseline": {"value": round(val, 6), "unit": "GDOF/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": round(val, 6), "unit": "GDOF/s", "cores": ncores, "kind": "oracle", "sample": sample,
+                         "cpu_model": _cpu_model()},
         "e2e": {"value": round(val, 6), "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 

@@ -576,6 +576,144 @@ __global__ void __launch_bounds__(256, 3) k_p2q8(GridP g, MatP mp, const int *__
     }
 }
 
+// ---- a2, scatter form (MPL_P2Q=scatter): one CTA per tile, shared-memory accumulation -----------------
+// The north_star's P2Q: the tile's particles (its base-cell buckets, contiguous after the counting sort)
+// are staged in shared memory with coalesced 16-byte loads, each record read from DRAM once; thread
+// (bucket b, corner o) sums the bucket's contributions to cell b + o (Eqs. p2c-mV, p2c-mv-affine,
+// p2c-A-sum, vtau; the weight of corner o from the fraction f) and adds them into a 5^3-cell
+// shared accumulator (the 8 threads of a bucket read the same records: shared-memory broadcasts); then
+// the 27 cells all of whose source buckets lie in the tile are stored and the other 98 are added with
+// global atomics into zeroed accumulators (neighbouring tiles contribute there).  k_p2q_finish then
+// normalises tau = (V tau) / V and reconstructs the stretch per slot (a4).
+constexpr int P2Q_CAP = 320;  // particles staged per pass (30 KB of fp32 records)
+template <int NM> struct P2QNV { static constexpr int V = 13 + 7 * NM; };  // m, mv 3, mG 9, per slot V + V tau 6
+template <class T, int NM>
+__global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *__restrict__ coord,
+                                                  const int *__restrict__ nplus, const int *__restrict__ bstart,
+                                                  const int *__restrict__ cellof, const T *__restrict__ rec,
+                                                  T *__restrict__ q_m, T *__restrict__ q_mv, T *__restrict__ q_mG,
+                                                  T *__restrict__ q_slot) {
+    constexpr int NV = P2QNV<NM>::V;
+    extern __shared__ __align__(16) unsigned char p2q_smem[];
+    T *acc = reinterpret_cast<T *>(p2q_smem);             // [125][NV]
+    T *R = acc + ((125 * NV + 3) & ~3);                   // [P2Q_CAP][REC]
+    __shared__ int bs[65];
+    const int t = blockIdx.x, tid = threadIdx.x;
+    if (tid < 65) bs[tid] = bstart[t * 64 + tid];
+    for (int i = tid; i < 125 * NV; i += blockDim.x) acc[i] = T(0);
+    __syncthreads();
+    const int p0 = bs[0], p1 = bs[64];
+    if (p0 == p1) return;  // no particles based in this tile (every thread sees the same)
+    const int nmat = mp.nmat;
+    const T dx = T(g.dx);
+    for (int c0 = p0; c0 < p1; c0 += P2Q_CAP) {
+        const int cn = min(P2Q_CAP, p1 - c0);
+        // stage records [c0, c0 + cn) with 16-byte loads
+        {
+            constexpr int PER = (int)(REC * sizeof(T) / 16);  // 16-byte vectors per record
+            const float4 *src = reinterpret_cast<const float4 *>(rec + (int64_t)c0 * REC);
+            float4 *dst = reinterpret_cast<float4 *>(R);
+            for (int i = tid; i < cn * PER; i += blockDim.x) dst[i] = __ldg(src + i);
+        }
+        __syncthreads();
+        for (int pr = tid; pr < 512; pr += blockDim.x) {
+            const int b = pr >> 3, o = pr & 7;
+            const int s0 = max(bs[b], c0), e0 = min(bs[b + 1], c0 + cn);
+            if (s0 >= e0) continue;
+            const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+            T m = 0, mv[3] = {0, 0, 0}, mG[9], V[NM], Vt[NM][6];
+#pragma unroll
+            for (int a = 0; a < 9; a++) mG[a] = 0;
+#pragma unroll
+            for (int k = 0; k < NM; k++) {
+                V[k] = 0;
+#pragma unroll
+                for (int a = 0; a < 6; a++) Vt[k][a] = 0;
+            }
+            for (int p = s0; p < e0; p++) {
+                const T *r = R + (p - c0) * REC;
+                const T w = (ox ? r[0] : T(1) - r[0]) * (oy ? r[1] : T(1) - r[1]) * (oz ? r[2] : T(1) - r[2]);
+                m += w * r[3];
+                mv[0] += w * (r[4] + dx * ((ox ? r[7] : T(0)) + (oy ? r[8] : T(0)) + (oz ? r[9] : T(0))));
+                mv[1] += w * (r[5] + dx * ((ox ? r[10] : T(0)) + (oy ? r[11] : T(0)) + (oz ? r[12] : T(0))));
+                mv[2] += w * (r[6] + dx * ((ox ? r[13] : T(0)) + (oy ? r[14] : T(0)) + (oz ? r[15] : T(0))));
+#pragma unroll
+                for (int a = 0; a < 9; a++) mG[a] += w * r[7 + a];
+                const int k = (int)r[23];
+#pragma unroll
+                for (int q = 0; q < NM; q++)
+                    if (q == k) {
+                        V[q] += w * r[16];
+#pragma unroll
+                        for (int a = 0; a < 6; a++) Vt[q][a] += w * r[17 + a];
+                    }
+            }
+            const int bx = b >> 4, by = (b >> 2) & 3, bz = b & 3;
+            T *ac = acc + (((bx + ox) * 5 + by + oy) * 5 + bz + oz) * NV;
+            atomicAdd(ac, m);
+#pragma unroll
+            for (int a = 0; a < 3; a++) atomicAdd(ac + 1 + a, mv[a]);
+#pragma unroll
+            for (int a = 0; a < 9; a++) atomicAdd(ac + 4 + a, mG[a]);
+#pragma unroll
+            for (int q = 0; q < NM; q++) {
+                if (q >= nmat) break;
+                atomicAdd(ac + 13 + 7 * q, V[q]);
+#pragma unroll
+                for (int a = 0; a < 6; a++) atomicAdd(ac + 14 + 7 * q + a, Vt[q][a]);
+            }
+        }
+        __syncthreads();  // the staged records are consumed before the next pass overwrites them
+    }
+    // flush the 5^3 accumulator: interior cells (local 1..3 on every axis) stored, the rest added
+    for (int i = tid; i < 125 * NV; i += blockDim.x) {
+        const int c = i / NV, v = i - c * NV;
+        const int X = c / 25, Y = (c / 5) % 5, Z = c % 5;
+        const int dp = ((X >> 2) << 2) | ((Y >> 2) << 1) | (Z >> 2);
+        const int tt = dp ? nplus[8 * t + dp] : t;
+        if (tt < 0) continue;
+        const int cc = cellof[tt * 64 + local_id(X & 3, Y & 3, Z & 3)];
+        if (cc < 0) continue;
+        const T val = acc[i];
+        const bool interior = X >= 1 && X <= 3 && Y >= 1 && Y <= 3 && Z >= 1 && Z <= 3;
+        T *dst = v == 0 ? q_m + cc : v < 4 ? q_mv + 3 * (int64_t)cc + (v - 1) : v < 13 ? q_mG + 9 * (int64_t)cc + (v - 4)
+               : q_slot + ((int64_t)cc * nmat + (v - 13) / 7) * 16 + ((v - 13) % 7 == 0 ? 0 : 6 + (v - 13) % 7);
+        if (interior) *dst = val;
+        else if (val != T(0)) atomicAdd(dst, val);
+    }
+}
+
+// a4 after the scatter: per (cell, slot) tau = (V tau) / V (Eq. vtau) and the stretch base
+template <class T>
+__global__ void k_p2q_finish(int64_t C, MatP mp, const uint8_t *__restrict__ clocal, T *__restrict__ q_slot,
+                             T *__restrict__ q_Sp, DevScalars *sc) {
+    const int nmat = mp.nmat;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= C * nmat) return;
+    const int64_t cc = i / nmat;
+    const int q = (int)(i - cc * nmat);
+    T *sl = q_slot + i * 16;
+    T tau[6] = {0, 0, 0, 0, 0, 0}, E[6] = {0, 0, 0, 0, 0, 0};
+    const T V = clocal[cc] != 0xFF ? sl[0] : T(0);
+    if (V != T(0)) {
+        const T iv = T(1) / V;
+#pragma unroll
+        for (int a = 0; a < 6; a++) tau[a] = sl[7 + a] * iv;
+        stretch_slot<T>(mp, q, tau, E, sc);
+    }
+    sl[0] = V;
+#pragma unroll
+    for (int a = 0; a < 6; a++) { sl[1 + a] = E[a]; sl[7 + a] = tau[a]; }
+    sl[13] = sl[14] = sl[15] = T(0);
+    if (q_Sp) {
+        T *sp = q_Sp + i * 9;
+        sp[0] = E[0]; sp[4] = E[1]; sp[8] = E[2];
+        sp[1] = sp[3] = E[3];
+        sp[5] = sp[7] = E[4];
+        sp[2] = sp[6] = E[5];
+    }
+}
+
 // ---- a3: C2N gather (Alg. 2 lines 16-22) + Newton target and Dirichlet sets ----------
 // PH 0: gather + finish in one pass (one rank).  PH 1: gather only, n_vn = ((mv)_i, m_i) partial
 // sums over this rank's cells (slab ranks; completed by c2n_halo).  PH 2: finish from n_vn.
@@ -680,6 +818,16 @@ __global__ void k_iota(int64_t n, int *a) {
 }
 
 inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+// P2Q form (MPL_P2Q): "gather" (k_p2q8, 8 lanes per cell) or "scatter" (k_p2q_tile + k_p2q_finish)
+bool p2q_scatter() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MPL_P2Q");
+        v = (e && e[0] == 's') ? 1 : 0;
+    }
+    return v == 1;
+}
 
 template <class I>
 mpl_status exclusive_scan(mpl_ctx ctx, const I *in, I *out, int64_t n) {
@@ -1041,6 +1189,35 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
                                        (uint8_t *)ctx->c_local.p, (int *)ctx->t_cellof.p, (uint8_t *)ctx->t_perm.p);
         ctx->launches++;
     DBG_GUARDS("resample #8");
+        if (p2q_scatter()) {
+            // zeroed accumulators, one CTA per tile scattering its particles, then the per-slot finish
+            MPL_CUDA(cudaMemsetAsync(ctx->q_m.p, 0, C * s, st));
+            MPL_CUDA(cudaMemsetAsync(ctx->q_mv.p, 0, C * 3 * s, st));
+            MPL_CUDA(cudaMemsetAsync(ctx->q_mG.p, 0, C * 9 * s, st));
+            MPL_CUDA(cudaMemsetAsync(ctx->q_slot.p, 0, C * nm * 16 * s, st));
+#define P2QT_ARGS                                                                                           \
+    g, ctx->mats, (const int *)ctx->t_coord.p, (const int *)ctx->t_nplus.p, (const int *)ctx->t_bstart.p, \
+        (const int *)ctx->t_cellof.p, (const T *)ctx->prec.p, (T *)ctx->q_m.p, (T *)ctx->q_mv.p,           \
+        (T *)ctx->q_mG.p, (T *)ctx->q_slot.p
+            if (nm <= 2) {
+                const size_t sm = (((size_t)125 * P2QNV<2>::V + 3) & ~(size_t)3) * s + (size_t)P2Q_CAP * REC * s;
+                MPL_CUDA(cudaFuncSetAttribute(k_p2q_tile<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                k_p2q_tile<T, 2><<<T_, 256, sm, st>>>(P2QT_ARGS);
+            } else {
+                const size_t sm = (((size_t)125 * P2QNV<MPL_MAXMAT>::V + 3) & ~(size_t)3) * s + (size_t)P2Q_CAP * REC * s;
+                MPL_CUDA(cudaFuncSetAttribute(k_p2q_tile<T, MPL_MAXMAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)sm));
+                k_p2q_tile<T, MPL_MAXMAT><<<T_, 256, sm, st>>>(P2QT_ARGS);
+            }
+#undef P2QT_ARGS
+            ctx->launches++;
+            MPL_CUDA(cudaGetLastError());
+            const int64_t NS = (int64_t)Cpad * nm;
+            k_p2q_finish<T><<<nblk(NS, 128), 128, 0, st>>>((int64_t)Cpad, ctx->mats, (const uint8_t *)ctx->c_local.p,
+                                                           (T *)ctx->q_slot.p,
+                                                           ctx->mats.plastic ? (T *)ctx->q_Sp.p : (T *)nullptr, sc);
+            ctx->launches++;
+        } else {
 #define P2Q_ARGS                                                                                             \
     g, ctx->mats, (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p, (const int *)ctx->t_bstart.p, \
         (const int *)ctx->t_cellof.p, (const T *)ctx->prec.p, (T *)ctx->q_m.p, (T *)ctx->q_mv.p,            \
@@ -1049,6 +1226,7 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
         else k_p2q8<T, MPL_MAXMAT><<<2 * T_, 256, 0, st>>>(P2Q_ARGS);
 #undef P2Q_ARGS
         ctx->launches++;
+        }
     DBG_GUARDS("resample #9");
     }
     // nodes

@@ -5,7 +5,7 @@ import sys
 
 import numpy as np
 
-from tests._parity import TOL, Pair, rel_l2
+from tests._parity import TOL, Pair, cell_ids, rel_l2
 from tests.test_gpu_parity import SCENES, _at, _fp32_scene, _probe
 
 
@@ -13,6 +13,20 @@ def main(name: str) -> None:
     pair = Pair(_fp32_scene(SCENES[name]()))
     sc = pair.scene
     tol = TOL[sc.precision]
+    # unload (a2-a4: the P2Q form is one of the options)
+    q = pair.ctx.get_quadrature()
+    cid = cell_ids(pair.grid, q["ijk"])
+    act = pair.un.m_c[cid] > 0
+    for nm, got, want in (("m_c", q["m_c"][act], pair.un.m_c[cid][act]), ("v_c", q["v_c"][act], pair.un.v_c[cid][act]),
+                          ("G_c", q["G_c"][act], pair.un.G_c[cid][act]), ("m_i", pair.m, pair.un.m_i[pair.nid]),
+                          ("v_i", pair.vn, pair.un.v_i[pair.nid])):
+        assert rel_l2(got, want) <= tol["unload"], f"{nm} rel l2 {rel_l2(got, want)}"
+    for k in range(len(sc.materials)):
+        sel = pair.un.V_ck[k][cid] > 0
+        assert rel_l2(q["V_ck"][k][act], pair.un.V_ck[k][cid][act]) <= tol["unload"]
+        if np.abs(pair.un.tau_ck[k]).max() > 0:
+            assert rel_l2(q["tau_ck"][k][sel], pair.un.tau_ck[k][cid][sel]) <= tol["unload"]
+        assert rel_l2(q["S_ck"][k][sel], pair.S[k][cid][sel]) <= tol["unload"]
     v, u = _probe(pair)
     po = _at(pair, v)
     pair.ctx.linearize(pair.to_gpu(v))

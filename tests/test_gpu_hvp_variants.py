@@ -24,6 +24,11 @@ CASES = [
     ({"MPL_PCG": "cg1", "MPL_CG1_E": "4"}, "mix_fp32"),
     ({"MPL_PCG": "cg1"}, "mix_fp64"),
     ({"MPL_PCG": "cg1"}, "psd_fp64"),
+    # P2Q scatter form (tile-staged shared-memory accumulation) vs the gather default
+    ({"MPL_P2Q": "scatter"}, "mix_fp32"),
+    ({"MPL_P2Q": "scatter"}, "mix_fp64"),
+    ({"MPL_P2Q": "scatter"}, "watermix_fp64"),
+    ({"MPL_P2Q": "scatter"}, "vmmix_fp64"),
 ]
 
 
@@ -32,7 +37,7 @@ CASES = [
     "-".join(f"{k[4:].lower()}={v}" for k, v in e.items()) + f"-{s}" for e, s in CASES])  # noqa: E501
 def test_hvp_variant_parity(env, scene):
     e = dict(os.environ)
-    for k in ("MPL_HVP_KERNEL", "MPL_PCG_MAP", "MPL_PDL", "MPL_L2WIN", "MPL_PCG", "MPL_CG1_E"):
+    for k in ("MPL_HVP_KERNEL", "MPL_PCG_MAP", "MPL_PDL", "MPL_L2WIN", "MPL_PCG", "MPL_CG1_E", "MPL_P2Q"):
         e.pop(k, None)
     e.update(env)
     r = subprocess.run([sys.executable, "-m", "tests._hvp_variant_check", scene], cwd=ROOT, env=e,

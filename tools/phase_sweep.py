@@ -24,10 +24,12 @@ def measure(name: str) -> dict:
     ctx = mpl.from_scene(sc, 0)
     fixed = dict(fixed_newton=1, fixed_cg=[50], fixed_ls=[0])
     ctx.step(sc.dt, sc.solver, **fixed)  # warm-up (allocations, first launches)
-    ctx.set_particles(sc.x, sc.v, sc.F, sc.G, sc.vol, sc.mat)
-    t0 = time.perf_counter()
-    c = ctx.resample(sc.dt)
-    t_res = time.perf_counter() - t0
+    t_res = 1e9
+    for _ in range(3):  # best of 3 (each from the same particle state)
+        ctx.set_particles(sc.x, sc.v, sc.F, sc.G, sc.vol, sc.mat)
+        t0 = time.perf_counter()
+        c = ctx.resample(sc.dt)
+        t_res = min(t_res, time.perf_counter() - t0)
     v0 = ctx.get_velocity()
     t0 = time.perf_counter()
     ctx.linearize(v0)
@@ -41,7 +43,7 @@ def measure(name: str) -> dict:
     t_g2p = time.perf_counter() - t0
     ctx.close()
     nbytes = c.n_cells * 45 * 4 + c.n_nodes * 7 * 4
-    return {"config": name, "particles": sc.n_particles, "quadrature_points": c.n_cells, "active_nodes": c.n_nodes,
+    return {"config": name, "p2q": os.environ.get("MPL_P2Q", "gather"), "particles": sc.n_particles, "quadrature_points": c.n_cells, "active_nodes": c.n_nodes,
             "resample_ms": round(t_res * 1e3, 3), "g2p_ms": round(t_g2p * 1e3, 3),
             "linearize_ms": round(t_lin * 1e3, 3), "hvp_us": round(hvp_ms * 1e3, 2),
             "hvp_alg_GBps": round(nbytes / (hvp_ms * 1e-3) / 1e9, 1),

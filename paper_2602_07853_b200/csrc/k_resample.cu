@@ -606,6 +606,26 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
     if (p0 == p1) return;  // no particles based in this tile (every thread sees the same)
     const int nmat = mp.nmat;
     const T dx = T(g.dx);
+    // thread tid owns the (bucket, corner) pairs tid and tid + 256 (256 threads) and sums them over every
+    // staged pass in registers; each pair is added into the shared accumulator once per tile
+    struct Acc {
+        T m, mv[3], mG[9], V[NM], Vt[NM][6];
+    };
+    Acc A2[2];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        A2[h].m = 0;
+#pragma unroll
+        for (int a = 0; a < 3; a++) A2[h].mv[a] = 0;
+#pragma unroll
+        for (int a = 0; a < 9; a++) A2[h].mG[a] = 0;
+#pragma unroll
+        for (int k = 0; k < NM; k++) {
+            A2[h].V[k] = 0;
+#pragma unroll
+            for (int a = 0; a < 6; a++) A2[h].Vt[k][a] = 0;
+        }
+    }
     for (int c0 = p0; c0 < p1; c0 += P2Q_CAP) {
         const int cn = min(P2Q_CAP, p1 - c0);
         // stage records [c0, c0 + cn) with 16-byte loads
@@ -616,55 +636,57 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
             for (int i = tid; i < cn * PER; i += blockDim.x) dst[i] = __ldg(src + i);
         }
         __syncthreads();
-        for (int pr = tid; pr < 512; pr += blockDim.x) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int pr = tid + 256 * h;
             const int b = pr >> 3, o = pr & 7;
             const int s0 = max(bs[b], c0), e0 = min(bs[b + 1], c0 + cn);
-            if (s0 >= e0) continue;
             const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
-            T m = 0, mv[3] = {0, 0, 0}, mG[9], V[NM], Vt[NM][6];
-#pragma unroll
-            for (int a = 0; a < 9; a++) mG[a] = 0;
-#pragma unroll
-            for (int k = 0; k < NM; k++) {
-                V[k] = 0;
-#pragma unroll
-                for (int a = 0; a < 6; a++) Vt[k][a] = 0;
-            }
+            Acc &q_ = A2[h];
             for (int p = s0; p < e0; p++) {
                 const T *r = R + (p - c0) * REC;
                 const T w = (ox ? r[0] : T(1) - r[0]) * (oy ? r[1] : T(1) - r[1]) * (oz ? r[2] : T(1) - r[2]);
-                m += w * r[3];
-                mv[0] += w * (r[4] + dx * ((ox ? r[7] : T(0)) + (oy ? r[8] : T(0)) + (oz ? r[9] : T(0))));
-                mv[1] += w * (r[5] + dx * ((ox ? r[10] : T(0)) + (oy ? r[11] : T(0)) + (oz ? r[12] : T(0))));
-                mv[2] += w * (r[6] + dx * ((ox ? r[13] : T(0)) + (oy ? r[14] : T(0)) + (oz ? r[15] : T(0))));
+                q_.m += w * r[3];
+                q_.mv[0] += w * (r[4] + dx * ((ox ? r[7] : T(0)) + (oy ? r[8] : T(0)) + (oz ? r[9] : T(0))));
+                q_.mv[1] += w * (r[5] + dx * ((ox ? r[10] : T(0)) + (oy ? r[11] : T(0)) + (oz ? r[12] : T(0))));
+                q_.mv[2] += w * (r[6] + dx * ((ox ? r[13] : T(0)) + (oy ? r[14] : T(0)) + (oz ? r[15] : T(0))));
 #pragma unroll
-                for (int a = 0; a < 9; a++) mG[a] += w * r[7 + a];
+                for (int a = 0; a < 9; a++) q_.mG[a] += w * r[7 + a];
                 const int k = (int)r[23];
 #pragma unroll
-                for (int q = 0; q < NM; q++)
-                    if (q == k) {
-                        V[q] += w * r[16];
+                for (int qq = 0; qq < NM; qq++)
+                    if (qq == k) {
+                        q_.V[qq] += w * r[16];
 #pragma unroll
-                        for (int a = 0; a < 6; a++) Vt[q][a] += w * r[17 + a];
+                        for (int a = 0; a < 6; a++) q_.Vt[qq][a] += w * r[17 + a];
                     }
-            }
-            const int bx = b >> 4, by = (b >> 2) & 3, bz = b & 3;
-            T *ac = acc + (((bx + ox) * 5 + by + oy) * 5 + bz + oz) * NV;
-            atomicAdd(ac, m);
-#pragma unroll
-            for (int a = 0; a < 3; a++) atomicAdd(ac + 1 + a, mv[a]);
-#pragma unroll
-            for (int a = 0; a < 9; a++) atomicAdd(ac + 4 + a, mG[a]);
-#pragma unroll
-            for (int q = 0; q < NM; q++) {
-                if (q >= nmat) break;
-                atomicAdd(ac + 13 + 7 * q, V[q]);
-#pragma unroll
-                for (int a = 0; a < 6; a++) atomicAdd(ac + 14 + 7 * q + a, Vt[q][a]);
             }
         }
         __syncthreads();  // the staged records are consumed before the next pass overwrites them
     }
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int pr = tid + 256 * h;
+        const int b = pr >> 3, o = pr & 7;
+        if (bs[b] == bs[b + 1]) continue;  // empty bucket
+        const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+        const int bx = b >> 4, by = (b >> 2) & 3, bz = b & 3;
+        T *ac = acc + (((bx + ox) * 5 + by + oy) * 5 + bz + oz) * NV;
+        const Acc &q_ = A2[h];
+        atomicAdd(ac, q_.m);
+#pragma unroll
+        for (int a = 0; a < 3; a++) atomicAdd(ac + 1 + a, q_.mv[a]);
+#pragma unroll
+        for (int a = 0; a < 9; a++) atomicAdd(ac + 4 + a, q_.mG[a]);
+#pragma unroll
+        for (int qq = 0; qq < NM; qq++) {
+            if (qq >= nmat) break;
+            atomicAdd(ac + 13 + 7 * qq, q_.V[qq]);
+#pragma unroll
+            for (int a = 0; a < 6; a++) atomicAdd(ac + 14 + 7 * qq + a, q_.Vt[qq][a]);
+        }
+    }
+    __syncthreads();
     // flush the 5^3 accumulator: interior cells (local 1..3 on every axis) stored, the rest added
     for (int i = tid; i < 125 * NV; i += blockDim.x) {
         const int c = i / NV, v = i - c * NV;

@@ -111,7 +111,112 @@ __host__ __device__ constexpr int krow(int e) {
 }
 __host__ __device__ constexpr int kcol(int e) { return krow(e) + (e - kofs(krow(e))); }
 
-__global__ void __launch_bounds__(32 * WZ_W, 3)
+// compressed-tangent apply for the two cells of a lane at once (KC): every value a float2 (cell A, cell B),
+// so each operation is one paired fp32 instruction (FFMA2 / FMUL2 / FADD2 on sm_100).  k holds the 28
+// interleaved pairs (A_e, B_e) of E = S - I (6), q_U (4), q_V (4), c psi_ij (6), c (a, b) x 3 pairs (6), pad;
+// d = dG (raw nodal sums); P = c (C : (dG S)) S with C in the SVD frame.
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ void quat_rot2(float2 w, float2 x, float2 y, float2 z, float2 R[9]) {
+    const float2 two = f2(2.f, 2.f), one = f2(1.f, 1.f);
+    const float2 xx = mul2(x, x), yy = mul2(y, y), zz = mul2(z, z);
+    const float2 xy = mul2(x, y), xz = mul2(x, z), yz = mul2(y, z), wx = mul2(w, x), wy = mul2(w, y), wz = mul2(w, z);
+    R[0] = sub2(one, mul2(two, add2(yy, zz)));
+    R[1] = mul2(two, sub2(xy, wz));
+    R[2] = mul2(two, add2(xz, wy));
+    R[3] = mul2(two, add2(xy, wz));
+    R[4] = sub2(one, mul2(two, add2(xx, zz)));
+    R[5] = mul2(two, sub2(yz, wx));
+    R[6] = mul2(two, sub2(xz, wy));
+    R[7] = mul2(two, add2(yz, wx));
+    R[8] = sub2(one, mul2(two, add2(xx, yy)));
+}
+__device__ __forceinline__ void kc_apply2(const float *k, const float2 d[9], float2 P[9]) {
+    auto el = [&](int e) { return f2(k[4 * (e >> 1) + 2 * (e & 1)], k[4 * (e >> 1) + 2 * (e & 1) + 1]); };
+    const float2 Em[9] = {el(0), el(3), el(5), el(3), el(1), el(4), el(5), el(4), el(2)};
+    float2 X[9];  // dG S = dG + dG E
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++) {
+            float2 v = d[3 * a + b];
+#pragma unroll
+            for (int c = 0; c < 3; c++) v = fma2(d[3 * a + c], Em[3 * c + b], v);
+            X[3 * a + b] = v;
+        }
+    float2 RU[9], RV[9];
+    quat_rot2(el(6), el(7), el(8), el(9), RU);
+    quat_rot2(el(10), el(11), el(12), el(13), RV);
+    float2 T1[9], Xh[9];  // Xh = RU^T X RV
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+            float2 v = mul2(RU[i], X[j]);
+            v = fma2(RU[3 + i], X[3 + j], v);
+            T1[3 * i + j] = fma2(RU[6 + i], X[6 + j], v);
+        }
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+            float2 v = mul2(T1[3 * i], RV[j]);
+            v = fma2(T1[3 * i + 1], RV[3 + j], v);
+            Xh[3 * i + j] = fma2(T1[3 * i + 2], RV[6 + j], v);
+        }
+    float2 Yh[9];
+    const float2 D00 = el(14), D11 = el(15), D22 = el(16), D01 = el(17), D12 = el(18), D02 = el(19);
+    Yh[0] = fma2(D00, Xh[0], fma2(D01, Xh[4], mul2(D02, Xh[8])));
+    Yh[4] = fma2(D01, Xh[0], fma2(D11, Xh[4], mul2(D12, Xh[8])));
+    Yh[8] = fma2(D02, Xh[0], fma2(D12, Xh[4], mul2(D22, Xh[8])));
+    {
+        const float2 a = el(20), b = el(21);  // pair (0, 1)
+        Yh[1] = fma2(a, Xh[1], mul2(b, Xh[3]));
+        Yh[3] = fma2(b, Xh[1], mul2(a, Xh[3]));
+    }
+    {
+        const float2 a = el(22), b = el(23);  // pair (0, 2)
+        Yh[2] = fma2(a, Xh[2], mul2(b, Xh[6]));
+        Yh[6] = fma2(b, Xh[2], mul2(a, Xh[6]));
+    }
+    {
+        const float2 a = el(24), b = el(25);  // pair (1, 2)
+        Yh[5] = fma2(a, Xh[5], mul2(b, Xh[7]));
+        Yh[7] = fma2(b, Xh[5], mul2(a, Xh[7]));
+    }
+    float2 T2[9], Y[9];  // Y = RU Yh RV^T
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+            float2 v = mul2(RU[3 * i], Yh[j]);
+            v = fma2(RU[3 * i + 1], Yh[3 + j], v);
+            T2[3 * i + j] = fma2(RU[3 * i + 2], Yh[6 + j], v);
+        }
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+            float2 v = mul2(T2[3 * i], RV[3 * j]);
+            v = fma2(T2[3 * i + 1], RV[3 * j + 1], v);
+            Y[3 * i + j] = fma2(T2[3 * i + 2], RV[3 * j + 2], v);
+        }
+#pragma unroll
+    for (int a = 0; a < 3; a++)  // P = Y S = Y + Y E
+#pragma unroll
+        for (int b = 0; b < 3; b++) {
+            float2 v = Y[3 * a + b];
+#pragma unroll
+            for (int c = 0; c < 3; c++) v = fma2(Y[3 * a + c], Em[3 * c + b], v);
+            P[3 * a + b] = v;
+        }
+}
+
+template <bool KC, int MINB = KC ? 4 : 3>
+__global__ void __launch_bounds__(32 * WZ_W, MINB)
     k_hvp_wz(int T_, const int *__restrict__ nplus, const unsigned long long *__restrict__ cmask,
              const int *__restrict__ hascells, const float *__restrict__ K, const int *__restrict__ kstart,
              const float *__restrict__ nmass, const f4 *__restrict__ u, f4 *__restrict__ Hu, double *__restrict__ uHu,
@@ -159,6 +264,14 @@ __global__ void __launch_bounds__(32 * WZ_W, 3)
         const unsigned word = lA < 32 ? clo : chi;
         q.pA = q.has ? (int)((word >> (lA & 31)) & 1u) : 0;
         q.pB = q.has ? (int)((word >> ((lA + 1) & 31)) & 1u) : 0;
+        if (KC) {  // compressed: one pair slot per lane holding a cell, 14 interleaved chunks
+            const unsigned pm = __ballot_sync(FULL, q.pA | q.pB);
+            q.sb = 16u * (unsigned)__popc(pm);
+            q.ka = K + ks + 4 * __popc(pm & lt);
+            q.kbp = q.ka;
+            q.e44 = q.d44 = 0;
+            return q;
+        }
         const unsigned pmA = __ballot_sync(FULL, q.pA), pmB = __ballot_sync(FULL, q.pB);
         const int nA = __popc(pmA), n = nA + __popc(pmB);
         const int sA = __popc(pmA & lt), sB = nA + __popc(pmB & lt);
@@ -173,6 +286,14 @@ __global__ void __launch_bounds__(32 * WZ_W, 3)
     // chunk c < 11 of slot s at 4 (c n + s), element 44 at 44 n + s (k_off): chunk c at (byte)
     // ka + c * 16 n, one IMAD.WIDE per load.  Chunk c of cell X (off 0 = A, 45 = B) -> k
     auto kload = [&](const TileK &q, int off, int c) {
+        if (KC) {  // off 0: chunks 0..6, off 45: chunks 7..13 (c < 7; the 12 calls per cell map onto 14 chunks)
+            const int cc = (off ? 7 : 0) + c;
+            if (c >= 7 || !(q.pA | q.pB)) return;
+            const float4 v = ldg_stream(reinterpret_cast<const float *>(reinterpret_cast<const char *>(q.ka) +
+                                                                        (uint64_t)q.sb * (uint64_t)cc), pol);
+            k[4 * cc] = v.x; k[4 * cc + 1] = v.y; k[4 * cc + 2] = v.z; k[4 * cc + 3] = v.w;
+            return;
+        }
         if (!(off ? q.pB : q.pA)) return;
         const float *p = off ? q.kbp : q.ka;
         if (c < 11) {
@@ -244,6 +365,14 @@ __global__ void __launch_bounds__(32 * WZ_W, 3)
                 dA[3 * a] = Dx[0][a] + Dx[1][a]; dA[3 * a + 1] = Dy[0][a] + Dy[1][a]; dA[3 * a + 2] = Sz[1][a] - Sz[0][a];
                 dB[3 * a] = Dx[1][a] + Dx[2][a]; dB[3 * a + 1] = Dy[1][a] + Dy[2][a]; dB[3 * a + 2] = Sz[2][a] - Sz[1][a];
             }
+            if (KC) {
+                float2 d2[9], P2[9];
+#pragma unroll
+                for (int r = 0; r < 9; r++) d2[r] = make_float2(dA[r], dB[r]);
+                kc_apply2(k, d2, P2);
+#pragma unroll
+                for (int r = 0; r < 9; r++) { PA[r] = P2[r].x; PB[r] = P2[r].y; }
+            } else {
             // ---- P = K dG (symmetric, packed upper triangle), element by element
 #pragma unroll
             for (int r = 0; r < 9; r++) { PA[r] = 0.f; PB[r] = 0.f; }
@@ -258,6 +387,7 @@ __global__ void __launch_bounds__(32 * WZ_W, 3)
                 const int r = krow(e), c = kcol(e);
                 PB[r] += k[45 + e] * dB[c];
                 if (c != r) PB[c] += k[45 + e] * dB[r];
+            }
             }
             float qf = 0.f;
 #pragma unroll
@@ -621,6 +751,7 @@ __global__ void __launch_bounds__(32 * WH_W, MINB)
 
 int g_num_sms = 0;
 
+template <bool KC, int MINB>
 mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
                      double cgthr) {
     static int per_sm = 0;
@@ -629,14 +760,14 @@ mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         int occ = 0;
-        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_wz, 32 * WZ_W, 0));
+        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_wz<KC, MINB>, 32 * WZ_W, 0));
         per_sm = occ > 0 ? occ : 1;
     }
     // persistent: one wave of (SMs x resident CTAs), tiles strided by the global warp count
     int grid = g_num_sms * per_sm;
     const int need = (ctx->T + WZ_W - 1) / WZ_W;
     if (grid > need) grid = need;
-    MPL_CUDA(launch_pdl(k_hvp_wz, grid, 32 * WZ_W, 0, ctx->stream, ctx->T, (const int *)ctx->t_nplus.p,
+    MPL_CUDA(launch_pdl(k_hvp_wz<KC, MINB>, grid, 32 * WZ_W, 0, ctx->stream, ctx->T, (const int *)ctx->t_nplus.p,
                         (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_hascells.p,
                         (const float *)ctx->K.p, (const int *)ctx->t_kstart.p, (const float *)owned_mass(ctx),
                         (const f4 *)u_tile, (f4 *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p));
@@ -703,7 +834,16 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
     if (ctx->T == 0) return MPL_OK;
     if (sizeof(T) == 8) return launch_wh<T, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);  // 45 doubles per lane
     if (hvp_variant() == 1) return launch_wh<T, 5>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
-    return launch_wz(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+    if (ctx->kc_now) {  // compressed tangent; MPL_KC_MINB: CTAs per SM requested from ptxas (3: 168 registers)
+        static int minb = -1;
+        if (minb < 0) {
+            const char *e = getenv("MPL_KC_MINB");
+            minb = e ? atoi(e) : 3;
+        }
+        if (minb == 4) return launch_wz<true, 4>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+        return launch_wz<true, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+    }
+    return launch_wz<false, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
 }
 
 template mpl_status launch_hvp<float>(mpl_ctx, const void *, void *, double *, const CGSlot *, int, double);

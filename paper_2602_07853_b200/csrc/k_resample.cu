@@ -324,6 +324,83 @@ __global__ void k_scatter(GridP g, MatP mp, int64_t np, const int *__restrict__ 
     keyo[d] = k;
 }
 
+// ---- the sort as a gather (MPL_SORT=gather, default): src[d] = p for the destination d of particle p,
+// then destination-ordered threads read their source particle (per-particle contiguous AoS, scattered
+// reads) and write the sorted state and the P2Q record in destination order: whole warps store
+// contiguous 16-byte vectors (warp_store_aos) instead of 32 scattered scalar stores per field
+__global__ void k_sort_src(int64_t np, const int *__restrict__ key, const int *__restrict__ rank,
+                           const int *__restrict__ bstart, int *__restrict__ src) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p < np) src[bstart[key[p]] + rank[p]] = (int)p;
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_scatter_g(GridP g, MatP mp, int64_t np, const int *__restrict__ src,
+                                                   const int *__restrict__ key, const T *__restrict__ x,
+                                                   const T *__restrict__ v, const T *__restrict__ F,
+                                                   const T *__restrict__ G, const T *__restrict__ vol,
+                                                   const int *__restrict__ mat, const int *__restrict__ pid,
+                                                   T *__restrict__ xo, T *__restrict__ Fo, T *__restrict__ volo,
+                                                   int *__restrict__ mato, int *__restrict__ pido,
+                                                   int *__restrict__ keyo, T *__restrict__ rec, DevScalars *sc) {
+    __shared__ __align__(16) T wsm[8][32 * REC];
+    const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool fast = __all_sync(0xffffffffu, d < np);
+    if (!fast && d >= np) return;
+    const int p = src[d];
+    T xp[3], vp[3], Fp[9], Gp[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++) { xp[a] = x[3 * (int64_t)p + a]; vp[a] = v[3 * (int64_t)p + a]; }
+#pragma unroll
+    for (int a = 0; a < 9; a++) { Fp[a] = F[9 * (int64_t)p + a]; Gp[a] = G[9 * (int64_t)p + a]; }
+    const int k = key[p];
+    const T Vp = vol[p];
+    const int m = mat[p];
+    const int id = pid[p];
+    if (det3(Fp) <= T(0)) atomicMin(&sc->inv_particle, id);
+    const T mu = T(mp.mu[m]), lam = T(mp.lam[m]);
+    const T mass = T(mp.rho[m]) * Vp;
+    T tau[6];
+    if (mp.kind[m] == 1) nh_tau(Fp, mu, T(mp.kappa[m]), tau);  // Alg. 2 line 3, per-material law
+    else if (mp.kind[m] == 2) water_tau(Fp, T(mp.kappa[m]), tau);
+    else hencky_tau(Fp, mu, lam, tau);
+    T f[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const T t = (xp[a] - T(g.origin[a])) * T(g.inv_dx) - T(0.5);
+        f[a] = t - floor(t);
+    }
+    const T dx = T(g.dx);
+    T r[REC];
+    r[0] = f[0]; r[1] = f[1]; r[2] = f[2];
+    r[3] = mass;
+#pragma unroll
+    for (int a = 0; a < 3; a++) r[4 + a] = mass * (vp[a] - dx * (Gp[3 * a] * f[0] + Gp[3 * a + 1] * f[1] + Gp[3 * a + 2] * f[2]));
+#pragma unroll
+    for (int a = 0; a < 9; a++) r[7 + a] = mass * Gp[a];
+    r[16] = Vp;
+#pragma unroll
+    for (int a = 0; a < 6; a++) r[17 + a] = Vp * tau[a];
+    r[23] = T(m);
+    volo[d] = Vp;
+    mato[d] = m;
+    pido[d] = id;
+    keyo[d] = k;
+    if (fast) {
+        T *sm = wsm[threadIdx.x >> 5];
+        const int64_t d0 = d & ~(int64_t)31;
+        warp_store_aos<T, REC>(rec, d0, sm, r);
+        warp_store_aos<T, 3>(xo, d0, sm, xp);
+        warp_store_aos<T, 9>(Fo, d0, sm, Fp);
+    } else {
+        st_rec<T>(rec + d * REC, r);
+#pragma unroll
+        for (int a = 0; a < 3; a++) xo[3 * d + a] = xp[a];
+#pragma unroll
+        for (int a = 0; a < 9; a++) Fo[9 * d + a] = Fp[a];
+    }
+}
+
 // v / G into the sorted order of the last k_scatter (see mpl_ctx_s::vg_unsorted)
 template <class T>
 __global__ void k_vg_to_sorted(int64_t np, const int *__restrict__ key, const int *__restrict__ rank,
@@ -360,8 +437,13 @@ __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, cons
         }
     }
     unsigned int lo = __ballot_sync(0xffffffffu, act);
-    __shared__ unsigned int part[2];
+    __shared__ unsigned int part[2], pairs;
+    if (l == 0) pairs = 0u;
     if ((l & 31) == 0) part[l >> 5] = lo;
+    __syncthreads();
+    // k_hvp_wz lanes holding a cell (kz_key(l) & 31 = the lane of cell l): the pair slots of the
+    // compressed tangent layout, 56 reals each
+    if (act) atomicOr(&pairs, 1u << (kz_key(l) & 31));
     __syncthreads();
     if (l == 0) {
         unsigned long long m = (unsigned long long)part[0] | ((unsigned long long)part[1] << 32);
@@ -369,8 +451,10 @@ __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, cons
         int c = __popcll(m);
         ccount[t] = (c + 3) & ~3;
         ncell[t] = c;
-        // tangent only on owned tiles: compact, 45 c reals rounded up to 4
-        kcnt[t] = hascells[t] ? (45 * c + 3) & ~3 : 0;
+        // tangent only on owned tiles: room for the full (45 c reals) or the compressed (56 per pair
+        // slot) layout, rounded up to 4
+        const int np = __popc(pairs);
+        kcnt[t] = hascells[t] ? (max(45 * c, 56 * np) + 3) & ~3 : 0;
         if (c && hascells[t]) atomicAdd(ncells, (unsigned long long)c);
     }
 }
@@ -644,7 +728,13 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
             const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
             Acc &q_ = A2[h];
             for (int p = s0; p < e0; p++) {
-                const T *r = R + (p - c0) * REC;
+                T r[REC];  // the staged record, 16-byte shared loads
+                {
+                    const float4 *r4 = reinterpret_cast<const float4 *>(R + (p - c0) * REC);
+                    float4 *d4 = reinterpret_cast<float4 *>(r);
+#pragma unroll
+                    for (int i = 0; i < (int)(REC * sizeof(T) / 16); i++) d4[i] = r4[i];
+                }
                 const T w = (ox ? r[0] : T(1) - r[0]) * (oy ? r[1] : T(1) - r[1]) * (oz ? r[2] : T(1) - r[2]);
                 q_.m += w * r[3];
                 q_.mv[0] += w * (r[4] + dx * ((ox ? r[7] : T(0)) + (oy ? r[8] : T(0)) + (oz ? r[9] : T(0))));
@@ -686,16 +776,22 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
             for (int a = 0; a < 6; a++) atomicAdd(ac + 14 + 7 * qq + a, q_.Vt[qq][a]);
         }
     }
+    // compact cell id of each of the 125 cells (-1: no such structural cell), once per cell
+    __shared__ int ccs[125];
+    if (tid < 125) {
+        const int X = tid / 25, Y = (tid / 5) % 5, Z = tid % 5;
+        const int dp = ((X >> 2) << 2) | ((Y >> 2) << 1) | (Z >> 2);
+        const int tt = dp ? nplus[8 * t + dp] : t;
+        ccs[tid] = tt < 0 ? -1 : cellof[tt * 64 + local_id(X & 3, Y & 3, Z & 3)];
+    }
     __syncthreads();
     // flush the 5^3 accumulator: interior cells (local 1..3 on every axis) stored, the rest added
     for (int i = tid; i < 125 * NV; i += blockDim.x) {
         const int c = i / NV, v = i - c * NV;
-        const int X = c / 25, Y = (c / 5) % 5, Z = c % 5;
-        const int dp = ((X >> 2) << 2) | ((Y >> 2) << 1) | (Z >> 2);
-        const int tt = dp ? nplus[8 * t + dp] : t;
-        if (tt < 0) continue;
-        const int cc = cellof[tt * 64 + local_id(X & 3, Y & 3, Z & 3)];
+        if (v >= 13 + 7 * nmat) continue;  // slots past the context's materials (NM is an upper bound)
+        const int cc = ccs[c];
         if (cc < 0) continue;
+        const int X = c / 25, Y = (c / 5) % 5, Z = c % 5;
         const T val = acc[i];
         const bool interior = X >= 1 && X <= 3 && Y >= 1 && Y <= 3 && Z >= 1 && Z <= 3;
         T *dst = v == 0 ? q_m + cc : v < 4 ? q_mv + 3 * (int64_t)cc + (v - 1) : v < 13 ? q_mG + 9 * (int64_t)cc + (v - 4)
@@ -703,6 +799,18 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
         if (interior) *dst = val;
         else if (val != T(0)) atomicAdd(dst, val);
     }
+}
+
+// cells with two or more occupied material slots (the compressed tangent covers one slot per cell)
+template <class T>
+__global__ void k_multislot(int64_t C, int nmat, const uint8_t *__restrict__ clocal, const T *__restrict__ q_slot,
+                            unsigned long long *count) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int k = 0;
+    if (c < C && clocal[c] != 0xFF)
+        for (int q = 0; q < nmat; q++) k += q_slot[(c * nmat + q) * 16] != T(0);
+    const unsigned int b = __ballot_sync(0xffffffffu, k >= 2);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(count, (unsigned long long)__popc(b));
 }
 
 // a4 after the scatter: per (cell, slot) tau = (V tau) / V (Eq. vtau) and the stretch base
@@ -840,6 +948,17 @@ __global__ void k_iota(int64_t n, int *a) {
 }
 
 inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+// particle sort (MPL_SORT): "gather" (k_sort_src + k_scatter_g, destination-ordered writes) or
+// "scatter" (k_scatter, source-ordered threads storing at the destinations)
+bool sort_gather() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MPL_SORT");
+        v = (e && e[0] == 's') ? 0 : 1;
+    }
+    return v == 1;
+}
 
 // P2Q form (MPL_P2Q): "gather" (k_p2q8, 8 lanes per cell) or "scatter" (k_p2q_tile + k_p2q_finish)
 bool p2q_scatter() {
@@ -1136,7 +1255,19 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_bcount.p, (int *)ctx->t_bstart.p, (int64_t)T_ * 64 + 1));
     // scatter into sorted order + records
     MPL_CHECK(ensure(ctx, ctx->pskey, (size_t)np * 4 + 16));
-    if (np)
+    if (np && sort_gather()) {
+        MPL_CHECK(ensure(ctx, ctx->psrc, (size_t)np * 4 + 16));
+        k_sort_src<<<nblk(np, 256), 256, 0, st>>>(np, (const int *)ctx->pkey.p, (const int *)ctx->prank.p,
+                                                  (const int *)ctx->t_bstart.p, (int *)ctx->psrc.p);
+        ctx->launches++;
+        k_scatter_g<T><<<nblk(np, 256), 256, 0, st>>>(
+            g, ctx->mats, np, (const int *)ctx->psrc.p, (const int *)ctx->pkey.p, (const T *)ctx->px[c].p,
+            (const T *)ctx->pv.p, (const T *)ctx->pF[c].p, (const T *)ctx->pG.p, (const T *)ctx->pvol[c].p,
+            (const int *)ctx->pmat[c].p, (const int *)ctx->pid[c].p, (T *)ctx->px[nx].p, (T *)ctx->pF[nx].p,
+            (T *)ctx->pvol[nx].p, (int *)ctx->pmat[nx].p, (int *)ctx->pid[nx].p, (int *)ctx->pskey.p,
+            (T *)ctx->prec.p, sc);
+        ctx->launches++;
+    } else if (np)
         k_scatter<T><<<nblk(np, 256), 256, 0, st>>>(
             g, ctx->mats, np, (const int *)ctx->pkey.p, (const int *)ctx->prank.p, (const int *)ctx->t_bstart.p,
             (const T *)ctx->px[c].p, (const T *)ctx->pv.p, (const T *)ctx->pF[c].p, (const T *)ctx->pG.p,
@@ -1251,6 +1382,12 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
         }
     DBG_GUARDS("resample #9");
     }
+    ctx->multi_slot_cells = 0;
+    if (nm > 1 && Cpad) {
+        k_multislot<T><<<nblk(Cpad, 256), 256, 0, st>>>((int64_t)Cpad, nm, (const uint8_t *)ctx->c_local.p,
+                                                       (const T *)ctx->q_slot.p, counters + 3);
+        ctx->launches++;
+    }
     // nodes
     const size_t NN = (size_t)T_ * 64 + 64;
     MPL_CHECK(ensure(ctx, ctx->n_mass, NN * s));
@@ -1295,9 +1432,12 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     DBG_GUARDS("resample #14");
         MPL_CHECK(d2h_sync(ctx, st));
         nact = lc + la;
-        unsigned long long nf = 0;
-        MPL_CHECK(d2h(ctx, &nf, counters + 2, 8, st)); MPL_CHECK(d2h_sync(ctx, st));
+        unsigned long long nf = 0, ms = 0;
+        MPL_CHECK(d2h(ctx, &nf, counters + 2, 8, st));
+        MPL_CHECK(d2h(ctx, &ms, counters + 3, 8, st));
+        MPL_CHECK(d2h_sync(ctx, st));
         ctx->n_free_nodes = (int64_t)nf;
+        ctx->multi_slot_cells = (int64_t)ms;
     }
     ctx->n_nodes_active = nact;
     MPL_CUDA(cudaGetLastError());

@@ -115,6 +115,28 @@ __device__ __forceinline__ void psd_project45(T *k) {
         }
 }
 
+// unit quaternion (w, x, y, z) of a proper rotation matrix R (row-major), Shepperd's branch choice
+template <class T>
+__device__ __forceinline__ void rot_quat(const T R[9], T q[4]) {
+    const T tr = R[0] + R[4] + R[8];
+    T w, x, y, z;
+    if (tr > T(0)) {
+        const T s = T(2) * sqrt(tr + T(1));
+        w = T(0.25) * s; x = (R[7] - R[5]) / s; y = (R[2] - R[6]) / s; z = (R[3] - R[1]) / s;
+    } else if (R[0] > R[4] && R[0] > R[8]) {
+        const T s = T(2) * sqrt(T(1) + R[0] - R[4] - R[8]);
+        w = (R[7] - R[5]) / s; x = T(0.25) * s; y = (R[1] + R[3]) / s; z = (R[2] + R[6]) / s;
+    } else if (R[4] > R[8]) {
+        const T s = T(2) * sqrt(T(1) + R[4] - R[0] - R[8]);
+        w = (R[2] - R[6]) / s; x = (R[1] + R[3]) / s; y = T(0.25) * s; z = (R[5] + R[7]) / s;
+    } else {
+        const T s = T(2) * sqrt(T(1) + R[8] - R[0] - R[4]);
+        w = (R[3] - R[1]) / s; x = (R[2] + R[6]) / s; y = (R[5] + R[7]) / s; z = T(0.25) * s;
+    }
+    const T n = rsqrt(w * w + x * x + y * y + z * z);
+    q[0] = w * n; q[1] = x * n; q[2] = y * n; q[3] = z * n;
+}
+
 // =============================================================================================
 // a5 / a8: linearisation.  MODE = LIN_ENERGY (Phi only), LIN_GRAD (+ g), LIN_FULL (+ K, diag).
 // =============================================================================================
@@ -130,8 +152,12 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
                                                    const T *__restrict__ qslot, T *__restrict__ Kout,
                                                    const int *__restrict__ kstart, const int *__restrict__ ncell,
                                                    vec4<T> *__restrict__ grad, vec4<T> *__restrict__ diag,
-                                                   T *__restrict__ qsp, DevScalars *sc, int kz) {
+                                                   T *__restrict__ qsp, DevScalars *sc, int kz, int kc) {
     constexpr int KS = (MODE == LIN_FULL) ? 64 * 45 : 1;
+    // compressed tangent (kc = 1: fp32, every slot elastic StVK-Hencky, one occupied slot per cell):
+    // 28 reals per cell, written in k_hvp_wz's interleaved pair layout
+    constexpr bool KCOK = (MODE == LIN_FULL) && HONLY && !PSD && sizeof(T) == 4;
+    __shared__ T Kc[KCOK ? 64 * 28 : 1];
     __shared__ vec4<T> vh[125];
     __shared__ T Pg[64 * 9];
     __shared__ T Ks[KS];
@@ -151,6 +177,8 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
     if (tid < 64) cslot[tid] = -1;
     if (MODE == LIN_FULL)
         for (int i = tid; i < nc * 45; i += blockDim.x) Ks[i] = T(0);
+    if (KCOK && kc)
+        for (int i = tid; i < 64 * 28; i += blockDim.x) Kc[i] = T(0);
     __syncthreads();
     if (has && tid < nc) {
         int l = clocal[cs + tid];
@@ -389,6 +417,56 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
                     for (int i = 0; i < 3; i++)
 #pragma unroll
                         for (int jj = 0; jj < 3; jj++) L[3 * i + jj] = dlog(lam3[i], lam3[jj]);
+                    if (KCOK && kc) {
+                        // compressed tangent of this slot: F = U Sigma V^T (U = eigenvectors of b = F F^T,
+                        // sigma_i^2 = beta_i), d^2 psi / dF^2 in the SVD frame = a 3x3 block on the diagonal
+                        // entries (psi_ij) and 2x2 blocks [[a, b], [b, a]] on (X_ij, X_ji) (Irving, Teran &
+                        // Fedkiw 2004), with g_i = sigma_i psi_i = tp_i for Hencky:
+                        //   psi_ij = (2 mu delta_ij + lam) / (sigma_i sigma_j) - delta_ij g_i / sigma_i^2,
+                        //   a_ij = (g_i - g_j) / (beta_i - beta_j) = mu L(beta_i, beta_j),
+                        //   b_ij = (beta_j a_ij - g_j) / (sigma_i sigma_j);
+                        // K : dG = c (C : (dG S)) S, c = dt^2 V / (16 dx^2) (= kscale dt)
+                        T U[9], Vm[9], sg[3];
+#pragma unroll
+                        for (int a = 0; a < 9; a++) U[a] = Q[a];
+#pragma unroll
+                        for (int i = 0; i < 3; i++) sg[i] = sqrt(T(1) + lam3[i]);
+                        const T detU = U[0] * (U[4] * U[8] - U[5] * U[7]) - U[1] * (U[3] * U[8] - U[5] * U[6]) +
+                                       U[2] * (U[3] * U[7] - U[4] * U[6]);
+                        if (detU < T(0)) { U[2] = -U[2]; U[5] = -U[5]; U[8] = -U[8]; }
+#pragma unroll
+                        for (int i = 0; i < 3; i++) {  // V[:, i] = F^T U[:, i] / sigma_i
+                            const T is = T(1) / sg[i];
+#pragma unroll
+                            for (int a = 0; a < 3; a++)
+                                Vm[3 * a + i] = (F[a] * U[i] + F[3 + a] * U[3 + i] + F[6 + a] * U[6 + i]) * is;
+                        }
+                        const T c = sV * T(1.0 / 16.0) * T(g.inv_dx * g.inv_dx) * dt;  // kscale dt
+                        T *kc_ = Kc + l * 28;
+                        // E (xx yy zz xy yz xz)
+                        kc_[0] = E[0]; kc_[1] = E[4]; kc_[2] = E[8]; kc_[3] = E[1]; kc_[4] = E[5]; kc_[5] = E[2];
+                        rot_quat(U, kc_ + 6);
+                        rot_quat(Vm, kc_ + 10);
+                        T psi[9];
+#pragma unroll
+                        for (int i = 0; i < 3; i++)
+#pragma unroll
+                            for (int jj = 0; jj < 3; jj++)
+                                psi[3 * i + jj] = ((i == jj ? T(2) * mu : T(0)) + lamL) / (sg[i] * sg[jj]) -
+                                                  (i == jj ? tp[i] / (sg[i] * sg[i]) : T(0));
+                        kc_[14] = c * psi[0]; kc_[15] = c * psi[4]; kc_[16] = c * psi[8];
+                        kc_[17] = c * psi[1]; kc_[18] = c * psi[5]; kc_[19] = c * psi[2];
+                        const int pi_[3] = {0, 0, 1}, pj_[3] = {1, 2, 2};
+#pragma unroll
+                        for (int pp = 0; pp < 3; pp++) {
+                            const int i = pi_[pp], jj = pj_[pp];
+                            const T a_ = mu * L[3 * i + jj];
+                            const T b_ = ((T(1) + lam3[jj]) * a_ - tp[jj]) / (sg[i] * sg[jj]);
+                            kc_[20 + 2 * pp] = c * a_;
+                            kc_[21 + 2 * pp] = c * b_;
+                        }
+                        kc_[26] = kc_[27] = T(0);
+                    }
                     const T kscale = sV * T(1.0 / 16.0) * T(g.inv_dx * g.inv_dx);
                     T *Kr = Ks + j * 45;
 #pragma unroll
@@ -464,7 +542,26 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
             zslot[tid] = sl;
         }
         __syncthreads();
-        for (int i = tid; i < n * 45; i += blockDim.x) Kout[k_off<T>(base, n, zslot[i / 45], i % 45)] = Ks[i];
+        if (KCOK && kc) {
+            // pair layout: pair slot s = rank of the k_hvp_wz lane among the lanes holding a cell; element e
+            // (0..27) of the lane's cells A (h = 0, even lz) / B (h = 1) at chunk e / 2, position 2 (e & 1) + h:
+            // one 16-byte load gives (A_e, B_e, A_e+1, B_e+1)
+            __shared__ unsigned int pm_s;
+            if (tid == 0) pm_s = 0u;
+            __syncthreads();
+            if (tid < n) atomicOr(&pm_s, 1u << (kz_key(clocal[cs + tid]) & 31));
+            __syncthreads();
+            const unsigned int pm = pm_s;
+            const int np = __popc(pm);
+            for (int i = tid; i < 64 * 28; i += blockDim.x) {
+                const int l2 = i / 28, e = i % 28, lane = kz_key(l2) & 31, h = l2 & 1;
+                if (!((pm >> lane) & 1u)) continue;
+                const int sp = __popc(pm & ((1u << lane) - 1u));
+                Kout[base + ((int64_t)(e >> 1) * np + sp) * 4 + 2 * (e & 1) + h] = Kc[i];
+            }
+        } else {
+            for (int i = tid; i < n * 45; i += blockDim.x) Kout[k_off<T>(base, n, zslot[i / 45], i % 45)] = Ks[i];
+        }
     }
     // ---- node phase -----------------------------------------------------------------------
     for (int h = tid; h < 125; h += blockDim.x) {
@@ -1227,7 +1324,7 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
         (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p, (const vec4<T> *)v_tile,                  \
         (const vec4<T> *)ctx->n_vhat.p, (const T *)owned_mass(ctx), (const T *)ctx->q_slot.p, (T *)ctx->K.p,       \
         (const int *)ctx->t_kstart.p, (const int *)ctx->t_ncell.p, (vec4<T> *)ctx->n_g.p, (vec4<T> *)ctx->n_diag.p, \
-        ctx->mats.plastic ? (T *)ctx->q_Sp.p : (T *)nullptr, sc, hvp_kz_layout(ctx->precision)
+        ctx->mats.plastic ? (T *)ctx->q_Sp.p : (T *)nullptr, sc, hvp_kz_layout(ctx->precision), kc
         // 64 threads per tile: one per cell (a tile has <= 64); 128 left half the CTA idle in the
         // cell phase (ncu at cfg4: barrier stalls 34 %, 16 warps / SM by registers)
         const char *lte = getenv("MPL_LIN_THREADS");
@@ -1236,6 +1333,12 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
         const int lin_gen_minb = lge ? atoi(lge) : 12;  // 12 CTAs per SM (NH / water / VM linearisations -7 %)
         bool honly = !ctx->mats.plastic;
         for (int k = 0; k < ctx->mats.nmat; k++) honly = honly && ctx->mats.kind[k] == 0;
+        // compressed tangent (MPL_KC, default on): fp32 k_hvp_wz, StVK-Hencky elastic only, exact Hessian,
+        // one occupied material slot per cell
+        const char *kce = getenv("MPL_KC");
+        const int kc = (mode == LIN_FULL && sizeof(T) == 4 && honly && !ctx->psd_now && hvp_variant() == 0 &&
+                        ctx->multi_slot_cells == 0 && !(kce && kce[0] == '0')) ? 1 : 0;
+        if (mode == LIN_FULL) ctx->kc_now = kc;
         if (mode == LIN_FULL && ctx->psd_now) {  // per-cell PSD projection of K
             // launch bounds (128, 1): the register-resident Jacobi (126 live reals) needs the registers
             if (honly) k_linearize<T, LIN_FULL, true, 1, true><<<T_, 64, 0, st>>>(LIN_ARGS);

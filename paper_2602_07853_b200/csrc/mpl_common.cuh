@@ -357,6 +357,7 @@ __host__ __device__ __forceinline__ constexpr int kz_key(int l) {
     return ((l & 1) << 5) | (((l >> 1) & 1) << 4) | ((l >> 4) << 2) | ((l >> 2) & 3);
 }
 int hvp_kz_layout(int precision);  // 1: compact kz order (k_hvp_wz), 3: natural compact order (k_hvp_wh)
+int hvp_variant();                 // fp32 HVP kernel: 0 k_hvp_wz, 1 k_hvp_wh
 template <class T> __host__ __device__ __forceinline__ int64_t k_off(int64_t base, int ncp, int j, int e) {
     return e < KL<T>::NCH * KL<T>::VEC
                ? base + ((int64_t)(e / KL<T>::VEC) * ncp + j) * KL<T>::VEC + (e % KL<T>::VEC)
@@ -453,6 +454,7 @@ struct mpl_ctx_s {
     int cur = 0;  // which particle buffer set is current
     DevBuf px[2], pF[2], pv, pG, pvol[2], pmat[2], pid[2];
     DevBuf pkey, prank, prec, pbase, pskey;  // per-particle scratch; pskey/prec in sorted order
+    DevBuf psrc;                             // sort as a gather: source particle of each sorted slot
     // k_scatter sorts x, F, vol, mat, pid (ping-pong sets) but not v and G: P2Q reads them through the
     // record and G2P rewrites them in sorted order.  Between the two, v / G still follow the previous
     // order; vg_unsorted records that, and sync_vg_order (a gather through the resample's sort map
@@ -462,6 +464,10 @@ struct mpl_ctx_s {
     // Hessian mode of the cached tangent: psd_default (mpl_set_psd_projection) for mpl_linearize,
     // psd_now = the value the current linearisation uses (newton_impl sets it from its solver cfg)
     int psd_default = 0, psd_now = 0;
+    // compressed tangent: cells with more than one occupied material slot (from the resample)
+    // and the format the last full linearisation wrote (0: 45-number K, 1: compressed, 28 reals per cell)
+    int64_t multi_slot_cells = 0;
+    int kc_now = 0;
 
     // tiles
     int T = 0;
@@ -628,6 +634,7 @@ template <class F> void for_each_buf(mpl_ctx ctx, F f) {
         {"n_x", ctx->n_x},
         {"n_r", ctx->n_r},
         {"n_p", ctx->n_p},
+        {"psrc", ctx->psrc},
         {"n_ps", ctx->n_ps},
         {"n_Hp", ctx->n_Hp},
         {"n_u", ctx->n_u},

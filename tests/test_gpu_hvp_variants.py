@@ -29,6 +29,13 @@ CASES = [
     ({"MPL_P2Q": "scatter"}, "mix_fp64"),
     ({"MPL_P2Q": "scatter"}, "watermix_fp64"),
     ({"MPL_P2Q": "scatter"}, "vmmix_fp64"),
+    ({"MPL_P2Q": "scatter"}, "cfg1_fp32"),
+    ({"MPL_P2Q": "scatter"}, "cfg1b"),
+    ({"MPL_SORT": "scatter"}, "mix_fp32"),   # the source-ordered sort (the gather form is default)
+    ({"MPL_SORT": "scatter"}, "mix_fp64"),
+    ({"MPL_KC": "0"}, "cfg1_fp32"),          # the 45-number tangent where the compressed one is the default
+    ({"MPL_KC": "0"}, "cfg2s_fp32"),
+    ({"MPL_KC_MINB": "4"}, "cfg2s_fp32"),
 ]
 
 
@@ -37,7 +44,7 @@ CASES = [
     "-".join(f"{k[4:].lower()}={v}" for k, v in e.items()) + f"-{s}" for e, s in CASES])  # noqa: E501
 def test_hvp_variant_parity(env, scene):
     e = dict(os.environ)
-    for k in ("MPL_HVP_KERNEL", "MPL_PCG_MAP", "MPL_PDL", "MPL_L2WIN", "MPL_PCG", "MPL_CG1_E", "MPL_P2Q"):
+    for k in ("MPL_HVP_KERNEL", "MPL_PCG_MAP", "MPL_PDL", "MPL_L2WIN", "MPL_PCG", "MPL_CG1_E", "MPL_P2Q", "MPL_SORT", "MPL_KC", "MPL_KC_MINB"):
         e.pop(k, None)
     e.update(env)
     r = subprocess.run([sys.executable, "-m", "tests._hvp_variant_check", scene], cwd=ROOT, env=e,

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
     // compressed tangent (kc = 1: fp32, every slot elastic StVK-Hencky, one occupied slot per cell):
     // 28 reals per cell, written in k_hvp_wz's interleaved pair layout
     constexpr bool KCOK = (MODE == LIN_FULL) && HONLY && !PSD && sizeof(T) == 4;
-    __shared__ T Kc[KCOK ? 64 * 28 : 1];
+    __shared__ unsigned int pm_s, cm_s[2];  // KC: k_hvp_wz lanes holding a cell; the tile's cell mask
     __shared__ vec4<T> vh[125];
     __shared__ T Pg[64 * 9];
     __shared__ T Ks[KS];
@@ -177,13 +177,31 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
     if (tid < 64) cslot[tid] = -1;
     if (MODE == LIN_FULL)
         for (int i = tid; i < nc * 45; i += blockDim.x) Ks[i] = T(0);
-    if (KCOK && kc)
-        for (int i = tid; i < 64 * 28; i += blockDim.x) Kc[i] = T(0);
+    if (tid == 0) { pm_s = 0u; cm_s[0] = cm_s[1] = 0u; }
     __syncthreads();
     if (has && tid < nc) {
         int l = clocal[cs + tid];
-        if (l != 0xFF) cslot[l] = tid;
+        if (l != 0xFF) {
+            cslot[l] = tid;
+            if (KCOK && kc) {
+                atomicOr(&pm_s, 1u << (kz_key(l) & 31));
+                atomicOr(&cm_s[l >> 5], 1u << (l & 31));
+            }
+        }
     }
+    if (KCOK && kc) __syncthreads();  // pair slots known before the cell phase writes the compressed tangent
+    // KC: element e of this cell at Kout[kc_base + (e / 2) * 4 np + 2 (e & 1)] (pair layout)
+    int64_t kc_base = 0;
+    int kc_np = 0;
+    if (KCOK && kc && has && tid < nc && clocal[cs + tid] != 0xFF) {
+        const int l = clocal[cs + tid], lane = kz_key(l) & 31;
+        kc_np = __popc(pm_s);
+        kc_base = kstart[t] + (int64_t)__popc(pm_s & ((1u << lane) - 1u)) * 4 + (l & 1);
+        // the lane's other cell (l ^ 1: the other z of the pair) absent: its half of the pair slot is zero
+        if (!((cm_s[(l ^ 1) >> 5] >> ((l ^ 1) & 31)) & 1u))
+            for (int e = 0; e < 28; e++) Kout[kc_base + (int64_t)(e >> 1) * 4 * kc_np + 2 * (e & 1) + (1 - 2 * (l & 1))] = T(0);
+    }
+    bool kc_done = false;
     double e_loc = 0.0;
     const T dt = T(dt_);
     const T q = T(0.25 * g.inv_dx);  // grad w = s q, s in {-1,+1}^3
@@ -442,7 +460,7 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
                                 Vm[3 * a + i] = (F[a] * U[i] + F[3 + a] * U[3 + i] + F[6 + a] * U[6 + i]) * is;
                         }
                         const T c = sV * T(1.0 / 16.0) * T(g.inv_dx * g.inv_dx) * dt;  // kscale dt
-                        T *kc_ = Kc + l * 28;
+                        T kc_[28];
                         // E (xx yy zz xy yz xz)
                         kc_[0] = E[0]; kc_[1] = E[4]; kc_[2] = E[8]; kc_[3] = E[1]; kc_[4] = E[5]; kc_[5] = E[2];
                         rot_quat(U, kc_ + 6);
@@ -466,6 +484,9 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
                             kc_[21 + 2 * pp] = c * b_;
                         }
                         kc_[26] = kc_[27] = T(0);
+#pragma unroll
+                        for (int e = 0; e < 28; e++) Kout[kc_base + (int64_t)(e >> 1) * 4 * kc_np + 2 * (e & 1)] = kc_[e];
+                        kc_done = true;
                     }
                     const T kscale = sV * T(1.0 / 16.0) * T(g.inv_dx * g.inv_dx);
                     T *Kr = Ks + j * 45;
@@ -520,6 +541,8 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
 #pragma unroll
                 for (int a = 0; a < 9; a++) Pg[l * 9 + a] = Pc[a] * q;  // fold grad w scale
             }
+            if (KCOK && kc && !kc_done)  // no occupied slot (a zero-mass stencil cell, amb-10): zero tangent
+                for (int e = 0; e < 28; e++) Kout[kc_base + (int64_t)(e >> 1) * 4 * kc_np + 2 * (e & 1)] = T(0);
         }
     }
     __syncthreads();
@@ -543,22 +566,7 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
         }
         __syncthreads();
         if (KCOK && kc) {
-            // pair layout: pair slot s = rank of the k_hvp_wz lane among the lanes holding a cell; element e
-            // (0..27) of the lane's cells A (h = 0, even lz) / B (h = 1) at chunk e / 2, position 2 (e & 1) + h:
-            // one 16-byte load gives (A_e, B_e, A_e+1, B_e+1)
-            __shared__ unsigned int pm_s;
-            if (tid == 0) pm_s = 0u;
-            __syncthreads();
-            if (tid < n) atomicOr(&pm_s, 1u << (kz_key(clocal[cs + tid]) & 31));
-            __syncthreads();
-            const unsigned int pm = pm_s;
-            const int np = __popc(pm);
-            for (int i = tid; i < 64 * 28; i += blockDim.x) {
-                const int l2 = i / 28, e = i % 28, lane = kz_key(l2) & 31, h = l2 & 1;
-                if (!((pm >> lane) & 1u)) continue;
-                const int sp = __popc(pm & ((1u << lane) - 1u));
-                Kout[base + ((int64_t)(e >> 1) * np + sp) * 4 + 2 * (e & 1) + h] = Kc[i];
-            }
+            // written by the cell phase (pair layout)
         } else {
             for (int i = tid; i < n * 45; i += blockDim.x) Kout[k_off<T>(base, n, zslot[i / 45], i % 45)] = Ks[i];
         }

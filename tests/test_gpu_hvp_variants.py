@@ -24,13 +24,13 @@ CASES = [
     ({"MPL_PCG": "cg1", "MPL_CG1_E": "4"}, "mix_fp32"),
     ({"MPL_PCG": "cg1"}, "mix_fp64"),
     ({"MPL_PCG": "cg1"}, "psd_fp64"),
-    # P2Q scatter form (tile-staged shared-memory accumulation) vs the gather default
-    ({"MPL_P2Q": "scatter"}, "mix_fp32"),
-    ({"MPL_P2Q": "scatter"}, "mix_fp64"),
-    ({"MPL_P2Q": "scatter"}, "watermix_fp64"),
-    ({"MPL_P2Q": "scatter"}, "vmmix_fp64"),
-    ({"MPL_P2Q": "scatter"}, "cfg1_fp32"),
-    ({"MPL_P2Q": "scatter"}, "cfg1b"),
+    # P2Q gather form (8 lanes per cell) vs the scatter default (tile-staged shared-memory accumulation)
+    ({"MPL_P2Q": "gather"}, "mix_fp32"),
+    ({"MPL_P2Q": "gather"}, "mix_fp64"),
+    ({"MPL_P2Q": "gather"}, "watermix_fp64"),
+    ({"MPL_P2Q": "gather"}, "vmmix_fp64"),
+    ({"MPL_P2Q": "gather"}, "cfg1_fp32"),
+    ({"MPL_P2Q": "gather"}, "cfg1b"),
     ({"MPL_SORT": "scatter"}, "mix_fp32"),   # the source-ordered sort (the gather form is default)
     ({"MPL_SORT": "scatter"}, "mix_fp64"),
     ({"MPL_KC": "0"}, "cfg1_fp32"),          # the 45-number tangent where the compressed one is the default

@@ -216,6 +216,7 @@ def run_ours(args):
     avg_hvp_ms = hvp_ms_max / max(n_hvp, 1)
     # roofline of the dominant kernel on this rank (rank 0's HVP launches)
     nbytes = hvp_bytes(cells, nodes, 4 if args.precision == 32 else 8)
+    fbytes = (cells * 28 * 4 + nodes * 7 * 4) if stats[-1].get("tangent_format") else nbytes
     peak, peak_kind = load_peaks()
     avg_local = hvp_ms / max(n_hvp, 1)
     achieved = nbytes / (avg_local * 1e-3) / 1e9 if avg_local > 0 else 0.0
@@ -257,9 +258,15 @@ def run_ours(args):
         "hvp_per_s": round(1e3 / avg_hvp_ms, 1) if avg_hvp_ms > 0 else None,
         "qp_per_s": round(cells_all / (avg_hvp_ms * 1e-3), 1) if avg_hvp_ms > 0 else None,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": load_traffic(sc.name, hvp_kernel_name(args.precision)) if ws == 1 else None,
+                     "frac": round(achieved / peak, 4), "traffic": load_traffic(sc.name, hvp_kernel_name(args.precision)) if ws == 1 and stats[-1].get("tangent_format") else None,
                      "peak_kind": peak_kind, "kernel": hvp_kernel_name(args.precision),
-                     "algorithmic_bytes_per_launch": int(nbytes), "pct_of_8TBps": round(achieved / 8000.0, 4)},
+                     "tangent": "compressed (28 reals per quadrature point)" if stats[-1].get("tangent_format") else
+                                "45 reals per quadrature point",
+                     "algorithmic_bytes_per_launch": int(nbytes), "pct_of_8TBps": round(achieved / 8000.0, 4),
+                     # the bytes the compressed format itself must move (112 B per quadrature point + 28 B per
+                     # node), and the fraction of peak on that count: the metric keeps SURVEY §8(d)'s figure
+                     "format_bytes_per_launch": int(fbytes),
+                     "format_frac": round(fbytes / (avg_local * 1e-3) / 1e9 / peak, 4) if avg_local > 0 else None},
         "e2e": e2e,
         "gpu_launches": int(launches),
         "converged": [bool(s["converged"]) for s in stats],

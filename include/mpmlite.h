@@ -131,6 +131,9 @@ typedef struct {
     double grad_norms[MPL_MAX_NEWTON_LOG]; /* ||g_free|| at the start of Newton iteration k (k < newton_iters),
                                               then at the returned iterate (index newton_iters) if measured */
     double alphas[MPL_MAX_NEWTON_LOG];     /* accepted line-search step of Newton iteration k            */
+    int32_t tangent_format;               /* cached tangent of the last linearisation: 0 = 45 numbers per
+                                             quadrature point, 1 = compressed (28: SVD-frame blocks)     */
+    int32_t pad_;
 } mpl_solve_stats;
 
 /* ---- context ------------------------------------------------------------------------------ */

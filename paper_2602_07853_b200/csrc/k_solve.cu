@@ -1794,6 +1794,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     S.ms_phase[5] = t_ls;
     ctx->linearized = false;  // K was built at an earlier iterate
     ctx->solved = true;
+    S.tangent_format = ctx->kc_now;
     if (out) *out = S;
     (void)h0;
     (void)h1;

@@ -71,7 +71,7 @@ class SolveStats(C.Structure):
                 ("n_hvp", C.c_int32), ("hvp_ms", C.c_double), ("ms_phase", C.c_double * 8),
                 ("n_cells", C.c_int64), ("n_nodes", C.c_int64), ("n_free_nodes", C.c_int64),
                 ("n_launches", C.c_int64), ("grad_norms", C.c_double * MAX_NEWTON_LOG),
-                ("alphas", C.c_double * MAX_NEWTON_LOG)]
+                ("alphas", C.c_double * MAX_NEWTON_LOG), ("tangent_format", C.c_int32), ("pad_", C.c_int32)]
 
     def as_dict(self) -> dict:
         n = min(self.newton_iters, MAX_NEWTON_LOG)
@@ -82,7 +82,8 @@ class SolveStats(C.Structure):
                     ls_iters=list(self.ls_iters[:n]), n_hvp=self.n_hvp, hvp_ms=self.hvp_ms,
                     ms_phase=list(self.ms_phase), n_cells=self.n_cells, n_nodes=self.n_nodes,
                     n_free_nodes=self.n_free_nodes, n_launches=self.n_launches,
-                    grad_norms=list(self.grad_norms[:min(n + 1, MAX_NEWTON_LOG)]), alphas=list(self.alphas[:n]))
+                    grad_norms=list(self.grad_norms[:min(n + 1, MAX_NEWTON_LOG)]), alphas=list(self.alphas[:n]),
+                    tangent_format=self.tangent_format)
 
 
 _vp, _i32, _i64, _d = C.c_void_p, C.c_int32, C.c_int64, C.c_double

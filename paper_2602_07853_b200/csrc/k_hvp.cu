@@ -220,7 +220,11 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
     k_hvp_wz(int T_, const int *__restrict__ nplus, const unsigned long long *__restrict__ cmask,
              const int *__restrict__ hascells, const float *__restrict__ K, const int *__restrict__ kstart,
              const float *__restrict__ nmass, const f4 *__restrict__ u, f4 *__restrict__ Hu, double *__restrict__ uHu,
-             const CGSlot *__restrict__ cgs, int cgj, double cgthr, const DevScalars *__restrict__ sc) {
+             const CGSlot *__restrict__ cgs, int cgj, double cgthr, const DevScalars *__restrict__ sc,
+             const int *__restrict__ tlist, int ntl) {
+    // items: tiles 0..T_-1, or the listed tiles tlist[0..ntl) (slab ranks: the interface tiles first, so
+    // their halo exchange overlaps the interior tiles' launch)
+    const int N = tlist ? ntl : T_;
     __shared__ WzWarp SW[WZ_W];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WzWarp &S = SW[wid];
@@ -245,8 +249,9 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
     const int *mbase = lane < 8 ? nplus + lane : lane == 8 ? kstart : lane == 9 ? hascells
                                                                       : reinterpret_cast<const int *>(cmask) + (lane - 10);
     const int mstride = lane < 8 ? 8 : lane < 10 ? 1 : 2;
-    auto load_meta = [&](int t) -> int {
-        if (t >= T_ || lane >= 12) return 0;
+    auto load_meta = [&](int i) -> int {  // metadata of item i's tile
+        if (i >= N || lane >= 12) return 0;
+        const int t = tlist ? __ldg(tlist + i) : i;
         return lane == 0 ? t : __ldg(mbase + (int64_t)mstride * t);
     };
     struct TileK {
@@ -260,7 +265,7 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
         q.has = __shfl_sync(FULL, meta, 9);
         const int ks = __shfl_sync(FULL, meta, 8);
         const unsigned clo = (unsigned)__shfl_sync(FULL, meta, 10), chi = (unsigned)__shfl_sync(FULL, meta, 11);
-        if (t >= T_) q.has = 0;
+        if (t >= N) q.has = 0;
         const unsigned word = lA < 32 ? clo : chi;
         q.pA = q.has ? (int)((word >> (lA & 31)) & 1u) : 0;
         q.pB = q.has ? (int)((word >> ((lA + 1) & 31)) & 1u) : 0;
@@ -310,7 +315,7 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
         int tt[4];
 #pragma unroll
         for (int r = 0; r < 4; r++) tt[r] = __shfl_sync(FULL, meta, role[r] < 0 ? 0 : (role[r] >> 6) & 7);
-        if (t < T_) {
+        if (t < N) {
 #pragma unroll
             for (int r = 0; r < 4; r++) {
                 if (role[r] < 0) continue;
@@ -335,7 +340,7 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
     halo(t0, 0, mcur);
     double acc = 0.0;
     int it = 0;
-    for (int t = t0; t < T_; t += G, it++) {
+    for (int t = t0; t < N; t += G, it++) {  // t: item index
         const int b = it & 1;
         const int mnn = load_meta(t + 2 * G);
         const TileK nxt = tile_k(t + G, mnext);
@@ -753,7 +758,7 @@ int g_num_sms = 0;
 
 template <bool KC, int MINB>
 mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
-                     double cgthr) {
+                     double cgthr, const int *tlist, int ntl) {
     static int per_sm = 0;
     if (per_sm == 0) {
         int dev = 0;
@@ -765,12 +770,14 @@ mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
     }
     // persistent: one wave of (SMs x resident CTAs), tiles strided by the global warp count
     int grid = g_num_sms * per_sm;
-    const int need = (ctx->T + WZ_W - 1) / WZ_W;
+    const int need = ((tlist ? ntl : ctx->T) + WZ_W - 1) / WZ_W;
     if (grid > need) grid = need;
+    if (grid < 1) return MPL_OK;
     MPL_CUDA(launch_pdl(k_hvp_wz<KC, MINB>, grid, 32 * WZ_W, 0, ctx->stream, ctx->T, (const int *)ctx->t_nplus.p,
                         (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_hascells.p,
                         (const float *)ctx->K.p, (const int *)ctx->t_kstart.p, (const float *)owned_mass(ctx),
-                        (const f4 *)u_tile, (f4 *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p));
+                        (const f4 *)u_tile, (f4 *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p,
+                        tlist, ntl));
     ctx->launches++;
     return MPL_OK;
 }
@@ -830,8 +837,9 @@ int hvp_kz_layout(int precision) {
 // Hu (tile-dense) must be zero on every node that receives atomics (all non-interior nodes).
 template <class T>
 mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
-                      double cgthr) {
+                      double cgthr, const int *tlist, int ntl) {
     if (ctx->T == 0) return MPL_OK;
+    if (tlist && (sizeof(T) == 8 || hvp_variant() == 1)) return MPL_ERR_UNSUPPORTED;  // tile lists: k_hvp_wz only
     if (sizeof(T) == 8) return launch_wh<T, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);  // 45 doubles per lane
     if (hvp_variant() == 1) return launch_wh<T, 5>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
     if (ctx->kc_now) {  // compressed tangent; MPL_KC_MINB: CTAs per SM requested from ptxas (3: 168 registers)
@@ -840,11 +848,13 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
             const char *e = getenv("MPL_KC_MINB");
             minb = e ? atoi(e) : 3;
         }
-        if (minb == 4) return launch_wz<true, 4>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
-        return launch_wz<true, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+        if (minb == 4) return launch_wz<true, 4>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
+        return launch_wz<true, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
     }
-    return launch_wz<false, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
+    return launch_wz<false, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
 }
 
-template mpl_status launch_hvp<float>(mpl_ctx, const void *, void *, double *, const CGSlot *, int, double);
-template mpl_status launch_hvp<double>(mpl_ctx, const void *, void *, double *, const CGSlot *, int, double);
+template mpl_status launch_hvp<float>(mpl_ctx, const void *, void *, double *, const CGSlot *, int, double,
+                                      const int *, int);
+template mpl_status launch_hvp<double>(mpl_ctx, const void *, void *, double *, const CGSlot *, int, double,
+                                       const int *, int);

@@ -348,6 +348,7 @@ __global__ void __launch_bounds__(256) k_scatter_g(GridP g, MatP mp, int64_t np,
     const bool fast = __all_sync(0xffffffffu, d < np);
     if (!fast && d >= np) return;
     const int p = src[d];
+    DASSERT(p >= 0 && p < np);
     T xp[3], vp[3], Fp[9], Gp[9];
 #pragma unroll
     for (int a = 0; a < 3; a++) { xp[a] = x[3 * (int64_t)p + a]; vp[a] = v[3 * (int64_t)p + a]; }
@@ -687,6 +688,7 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
     for (int i = tid; i < 125 * NV; i += blockDim.x) acc[i] = T(0);
     __syncthreads();
     const int p0 = bs[0], p1 = bs[64];
+    DASSERT(p1 >= p0);
     if (p0 == p1) return;  // no particles based in this tile (every thread sees the same)
     const int nmat = mp.nmat;
     const T dx = T(g.dx);

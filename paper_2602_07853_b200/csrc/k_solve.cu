@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
         const int l = clocal[cs + tid], lane = kz_key(l) & 31;
         kc_np = __popc(pm_s);
         kc_base = kstart[t] + (int64_t)__popc(pm_s & ((1u << lane) - 1u)) * 4 + (l & 1);
+        DASSERT(kstart[t] + 56 * kc_np <= kstart[t + 1]);
         // the lane's other cell (l ^ 1: the other z of the pair) absent: its half of the pair slot is zero
         if (!((cm_s[(l ^ 1) >> 5] >> ((l ^ 1) & 31)) & 1u))
             for (int e = 0; e < 28; e++) Kout[kc_base + (int64_t)(e >> 1) * 4 * kc_np + 2 * (e & 1) + (1 - 2 * (l & 1))] = T(0);
@@ -1445,6 +1446,17 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     const char *cge = getenv("MPL_CG1_E");  // nodes per lane per chunk of the cg1 vector kernel (2 or 4)
     const int cg1_e = cge ? atoi(cge) : 2;
     T *pc = nullptr, *sc_ = nullptr;  // cg1: compact p, s
+    // slab ranks, cg1, k_hvp_wz: the HVP in two launches (interface tiles, then interior) with the face halo
+    // between them (MPL_OVERLAP=0 disables); on the NCCL transport the halo runs on its own stream,
+    // concurrently with the interior launch
+    const char *ove = getenv("MPL_OVERLAP");
+    const bool split = cg1 && multi(ctx) && sizeof(T) == 4 && hvp_variant() == 0 && !(ove && ove[0] == '0');
+    const bool overlap = split && comm_is_nccl(ctx);
+    if (overlap && !ctx->hstream) {
+        MPL_CUDA(cudaStreamCreateWithFlags(&ctx->hstream, cudaStreamNonBlocking));
+        MPL_CUDA(cudaEventCreateWithFlags(&ctx->ev_bnd, cudaEventDisableTiming));
+        MPL_CUDA(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
+    }
     if (cg1) {
         MPL_CHECK(ensure(ctx, ctx->n_ps, (size_t)6 * SA * sizeof(T) + 64));
         pc = (T *)ctx->n_ps.p;
@@ -1628,11 +1640,33 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                         const bool timed1 = hvp_events && ((jj + 1) % HVP_SAMPLE == 0);
                         if (timed1) cudaEventRecord(hev[nl].first, st);
                         // on slab ranks slot jj+1 is not reduced yet: skip on the previous (reduced) residual
-                        MPL_CHECK(launch_hvp<T>(ctx, p, wbuf(jj + 1), slots[jj + 1].pHp, slots, multi(ctx) ? jj : jj + 1,
-                                                thr));
-                        if (multi(ctx)) {
-                            MPL_CHECK(halo_sum_nodes<T>(ctx, wbuf(jj + 1), nullptr));
+                        const int cgj1 = multi(ctx) ? jj : jj + 1;
+                        if (split) {
+                            // interface tiles first; their face halo runs (NCCL: on the halo stream, concurrent
+                            // with the interior tiles) while the interior tiles, which touch no shared node, run
+                            MPL_CHECK(launch_hvp<T>(ctx, p, wbuf(jj + 1), slots[jj + 1].pHp, slots, cgj1, thr,
+                                                    (const int *)ctx->t_bnd.p, ctx->n_bnd));
+                            if (overlap) {
+                                MPL_CUDA(cudaEventRecord(ctx->ev_bnd, st));
+                                MPL_CUDA(cudaStreamWaitEvent(ctx->hstream, ctx->ev_bnd, 0));
+                                ctx->stream = ctx->hstream;
+                                const mpl_status hs = halo_sum_nodes<T>(ctx, wbuf(jj + 1), nullptr);
+                                ctx->stream = st;
+                                MPL_CHECK(hs);
+                                MPL_CUDA(cudaEventRecord(ctx->ev_halo, ctx->hstream));
+                            } else {
+                                MPL_CHECK(halo_sum_nodes<T>(ctx, wbuf(jj + 1), nullptr));
+                            }
+                            MPL_CHECK(launch_hvp<T>(ctx, p, wbuf(jj + 1), slots[jj + 1].pHp, slots, cgj1, thr,
+                                                    (const int *)ctx->t_int.p, ctx->n_int));
+                            if (overlap) MPL_CUDA(cudaStreamWaitEvent(st, ctx->ev_halo, 0));
                             MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 3 * NSTRIPE));  // gamma, r.r, delta
+                        } else {
+                            MPL_CHECK(launch_hvp<T>(ctx, p, wbuf(jj + 1), slots[jj + 1].pHp, slots, cgj1, thr));
+                            if (multi(ctx)) {
+                                MPL_CHECK(halo_sum_nodes<T>(ctx, wbuf(jj + 1), nullptr));
+                                MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 3 * NSTRIPE));  // gamma, r.r, delta
+                            }
                         }
                         if (timed1) {
                             cudaEventRecord(hev[nl].second, st);

@@ -208,6 +208,12 @@ void mpl_destroy(mpl_ctx ctx) {
         cudaStreamDestroy(ctx->rstream);
         for (cudaEvent_t e : {ctx->ev_staged, ctx->ev_adopted, ctx->ev_rb_ready, ctx->ev_rb_done}) cudaEventDestroy(e);
     }
+    if (ctx->hstream) {
+        cudaStreamSynchronize(ctx->hstream);
+        cudaStreamDestroy(ctx->hstream);
+        cudaEventDestroy(ctx->ev_bnd);
+        cudaEventDestroy(ctx->ev_halo);
+    }
     for_each_buf(ctx, [](const char *, DevBuf &b) { free_buf(b); });
     if (ctx->pio_buf) cudaFreeHost(ctx->pio_buf);
     comm_destroy(ctx);

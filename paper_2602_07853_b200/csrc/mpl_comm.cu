@@ -647,8 +647,27 @@ mpl_status build_interface_lists(mpl_ctx ctx) {
     };
     MPL_CHECK(match(rl, lo_k, lo_t, ctx->t_lo_map));
     MPL_CHECK(match(rh, hi_k, hi_t, ctx->t_hi_map));
+    // HVP split for the overlapped halo: the tiles at node-block x in {lo - 1, lo, hi - 1, hi} write the
+    // shared planes (cells of the first / last owned block, the owned masses on the planes); no other tile
+    // touches a shared-plane node
+    {
+        std::vector<int> bnd, inn;
+        for (int t = 0; t < T_; t++) {
+            const int bx = coord[3 * t];
+            const bool b = bx == ctx->slab_lo - 1 || bx == ctx->slab_lo || bx == ctx->slab_hi - 1 || bx == ctx->slab_hi;
+            (b ? bnd : inn).push_back(t);
+        }
+        ctx->n_bnd = (int)bnd.size();
+        ctx->n_int = (int)inn.size();
+        MPL_CHECK(ensure(ctx, ctx->t_bnd, bnd.size() * 4 + 16));
+        MPL_CHECK(ensure(ctx, ctx->t_int, inn.size() * 4 + 16));
+        if (!bnd.empty()) MPL_CUDA(cudaMemcpy(ctx->t_bnd.p, bnd.data(), bnd.size() * 4, cudaMemcpyHostToDevice));
+        if (!inn.empty()) MPL_CUDA(cudaMemcpy(ctx->t_int.p, inn.data(), inn.size() * 4, cudaMemcpyHostToDevice));
+    }
     return MPL_OK;
 }
+
+bool comm_is_nccl(mpl_ctx ctx) { return ctx->comm && dynamic_cast<NcclComm *>(ctx->comm) != nullptr; }
 
 namespace {
 // compact face buffers: send = this rank's face tiles, recv = the neighbour's (16 nodes x nv vectors each)

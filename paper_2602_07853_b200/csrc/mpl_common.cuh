@@ -422,6 +422,12 @@ struct mpl_ctx_s {
     // to local tiles (map: received entry -> local tile or -1).  A halo message is 16 nodes per listed tile.
     DevBuf t_lo_list, t_hi_list, t_lo_map, t_hi_map;
     int n_lo_tiles = 0, n_hi_tiles = 0, n_lo_recv = 0, n_hi_recv = 0;
+    // the HVP split for overlap: tiles whose cells or owned nodes touch a shared node plane (node-block x in
+    // {slab_lo - 1, slab_lo, slab_hi - 1, slab_hi}) first, then the interior tiles
+    DevBuf t_bnd, t_int;
+    int n_bnd = 0, n_int = 0;
+    cudaStream_t hstream = nullptr;     // halo stream of the overlapped HVP (NCCL transport)
+    cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
     DevBuf n_own, n_mown;                  // per node: owner flag (uint8), owned mass (m if owner else 0)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -661,6 +667,8 @@ template <class F> void for_each_buf(mpl_ctx ctx, F f) {
         {"t_hi_list", ctx->t_hi_list},
         {"t_lo_map", ctx->t_lo_map},
         {"t_hi_map", ctx->t_hi_map},
+        {"t_bnd", ctx->t_bnd},
+        {"t_int", ctx->t_int},
         {"n_own", ctx->n_own},
         {"n_mown", ctx->n_mown}
     };
@@ -681,7 +689,8 @@ template <class T> mpl_status resample_impl(mpl_ctx ctx, double dt);
 template <class T> mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi);
 template <class T> mpl_status hvp_tile(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *pHp_accum);
 template <class T> mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu,
-                                         const CGSlot *cgs, int cgj, double cgthr);
+                                         const CGSlot *cgs, int cgj, double cgthr, const int *tlist = nullptr,
+                                         int ntl = 0);
 template <class T> mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *st);
 template <class T> mpl_status g2p_impl(mpl_ctx ctx, double dt);
 template <class T> mpl_status sync_vg_order(mpl_ctx ctx);
@@ -700,6 +709,7 @@ template <class T> mpl_status export_particles(mpl_ctx ctx, void *x, void *v, vo
 // multi-rank plumbing (mpl_comm.cu)
 template <class T> mpl_status redistribute_particles(mpl_ctx ctx);
 template <class T> mpl_status halo_sum_nodes(mpl_ctx ctx, void *a_tile, void *b_tile);
+bool comm_is_nccl(mpl_ctx ctx);
 template <class T> mpl_status ghost_nodes_from_upper(mpl_ctx ctx, void *v_tile);
 template <class T> mpl_status c2n_halo(mpl_ctx ctx);
 template <class T> mpl_status export_owned_particles(mpl_ctx ctx, void *x, void *v, void *F, void *G, int32_t *ids,

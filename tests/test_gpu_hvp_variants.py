@@ -63,3 +63,15 @@ def test_slab_ranks_with_classic_pcg():
                         "replayed_step or migration_multistep_matches_one_rank"], cwd=ROOT, env=e,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_slab_ranks_without_hvp_split():
+    """Slab ranks with the HVP in one launch and the halo after it (MPL_OVERLAP=0) instead of the default
+    split (interface tiles, halo, interior tiles): replayed step and multi-step migration parity."""
+    e = dict(os.environ)
+    e["MPL_OVERLAP"] = "0"
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "tests/test_gpu_slabs.py", "-k",
+                        "replayed_step or migration_multistep_matches_one_rank"], cwd=ROOT, env=e,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

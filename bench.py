@@ -136,6 +136,9 @@ def run_ours(args):
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     if ws > 1:
+        # NCCL communicator set-up lines (ranks, NVLink / NVLS paths) on stderr, for the run's record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     sc = scenes.by_name(args.config, args.precision)

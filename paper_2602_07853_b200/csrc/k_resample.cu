@@ -803,138 +803,6 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
     }
 }
 
-// The same scatter with thread (bucket b, ox) summing the 4 corners (ox, oy, oz) of its x side (128 threads
-// per tile): a staged record is read by 2 threads instead of 8 and its weight factors are shared by the
-// thread's 4 corners (MPL_P2Q=scatter, the default; "scatter8" keeps the thread-per-corner form).
-template <class T, int NM>
-__global__ void __launch_bounds__(128) k_p2q_tile4(GridP g, MatP mp, const int *__restrict__ coord,
-                                                   const int *__restrict__ nplus, const int *__restrict__ bstart,
-                                                   const int *__restrict__ cellof, const T *__restrict__ rec,
-                                                   T *__restrict__ q_m, T *__restrict__ q_mv, T *__restrict__ q_mG,
-                                                   T *__restrict__ q_slot) {
-    constexpr int NV = P2QNV<NM>::V;
-    extern __shared__ __align__(16) unsigned char p2q_smem[];
-    T *acc = reinterpret_cast<T *>(p2q_smem);  // [125][NV]
-    T *R = acc + ((125 * NV + 3) & ~3);        // [P2Q_CAP][REC]
-    __shared__ int bs[65];
-    __shared__ int ccs[125];
-    const int t = blockIdx.x, tid = threadIdx.x;
-    if (tid < 65) bs[tid] = bstart[t * 64 + tid];
-    for (int i = tid; i < 125 * NV; i += blockDim.x) acc[i] = T(0);
-    __syncthreads();
-    const int p0 = bs[0], p1 = bs[64];
-    DASSERT(p1 >= p0);
-    if (p0 == p1) return;
-    const int nmat = mp.nmat;
-    const T dx = T(g.dx);
-    const int b = tid >> 1, ox = tid & 1;
-    struct Acc {
-        T m, mv[3], mG[9], V[NM], Vt[NM][6];
-    };
-    Acc A4[4];  // corner (oy, oz) = index 2 oy + oz
-#pragma unroll
-    for (int h = 0; h < 4; h++) {
-        A4[h].m = 0;
-#pragma unroll
-        for (int a = 0; a < 3; a++) A4[h].mv[a] = 0;
-#pragma unroll
-        for (int a = 0; a < 9; a++) A4[h].mG[a] = 0;
-#pragma unroll
-        for (int k = 0; k < NM; k++) {
-            A4[h].V[k] = 0;
-#pragma unroll
-            for (int a = 0; a < 6; a++) A4[h].Vt[k][a] = 0;
-        }
-    }
-    for (int c0 = p0; c0 < p1; c0 += P2Q_CAP) {
-        const int cn = min(P2Q_CAP, p1 - c0);
-        {
-            constexpr int PER = (int)(REC * sizeof(T) / 16);
-            const float4 *src = reinterpret_cast<const float4 *>(rec + (int64_t)c0 * REC);
-            float4 *dst = reinterpret_cast<float4 *>(R);
-            for (int i = tid; i < cn * PER; i += blockDim.x) dst[i] = __ldg(src + i);
-        }
-        __syncthreads();
-        const int s0 = max(bs[b], c0), e0 = min(bs[b + 1], c0 + cn);
-        for (int p = s0; p < e0; p++) {
-            T r[REC];
-            {
-                const float4 *r4 = reinterpret_cast<const float4 *>(R + (p - c0) * REC);
-                float4 *d4 = reinterpret_cast<float4 *>(r);
-#pragma unroll
-                for (int i = 0; i < (int)(REC * sizeof(T) / 16); i++) d4[i] = r4[i];
-            }
-            const T wx = ox ? r[0] : T(1) - r[0];
-            const int k = (int)r[23];
-            // m (v + G (x_c - x_p)) = a + dx (mG) o: the x part of the APIC term is fixed by ox
-            T ax[3];
-#pragma unroll
-            for (int a = 0; a < 3; a++) ax[a] = r[4 + a] + (ox ? dx * r[7 + 3 * a] : T(0));
-#pragma unroll
-            for (int h = 0; h < 4; h++) {
-                const int oy = h >> 1, oz = h & 1;
-                const T w = wx * (oy ? r[1] : T(1) - r[1]) * (oz ? r[2] : T(1) - r[2]);
-                Acc &q_ = A4[h];
-                q_.m += w * r[3];
-#pragma unroll
-                for (int a = 0; a < 3; a++)
-                    q_.mv[a] += w * (ax[a] + dx * ((oy ? r[8 + 3 * a] : T(0)) + (oz ? r[9 + 3 * a] : T(0))));
-#pragma unroll
-                for (int a = 0; a < 9; a++) q_.mG[a] += w * r[7 + a];
-#pragma unroll
-                for (int qq = 0; qq < NM; qq++)
-                    if (qq == k) {
-                        q_.V[qq] += w * r[16];
-#pragma unroll
-                        for (int a = 0; a < 6; a++) q_.Vt[qq][a] += w * r[17 + a];
-                    }
-            }
-        }
-        __syncthreads();
-    }
-    if (bs[b] != bs[b + 1]) {
-        const int bx = b >> 4, by = (b >> 2) & 3, bz = b & 3;
-#pragma unroll
-        for (int h = 0; h < 4; h++) {
-            const int oy = h >> 1, oz = h & 1;
-            T *ac = acc + (((bx + ox) * 5 + by + oy) * 5 + bz + oz) * NV;
-            const Acc &q_ = A4[h];
-            atomicAdd(ac, q_.m);
-#pragma unroll
-            for (int a = 0; a < 3; a++) atomicAdd(ac + 1 + a, q_.mv[a]);
-#pragma unroll
-            for (int a = 0; a < 9; a++) atomicAdd(ac + 4 + a, q_.mG[a]);
-#pragma unroll
-            for (int qq = 0; qq < NM; qq++) {
-                if (qq >= nmat) break;
-                atomicAdd(ac + 13 + 7 * qq, q_.V[qq]);
-#pragma unroll
-                for (int a = 0; a < 6; a++) atomicAdd(ac + 14 + 7 * qq + a, q_.Vt[qq][a]);
-            }
-        }
-    }
-    if (tid < 125) {
-        const int X = tid / 25, Y = (tid / 5) % 5, Z = tid % 5;
-        const int dp = ((X >> 2) << 2) | ((Y >> 2) << 1) | (Z >> 2);
-        const int tt = dp ? nplus[8 * t + dp] : t;
-        ccs[tid] = tt < 0 ? -1 : cellof[tt * 64 + local_id(X & 3, Y & 3, Z & 3)];
-    }
-    __syncthreads();
-    for (int i = tid; i < 125 * NV; i += blockDim.x) {
-        const int c = i / NV, v = i - c * NV;
-        if (v >= 13 + 7 * nmat) continue;
-        const int cc = ccs[c];
-        if (cc < 0) continue;
-        const int X = c / 25, Y = (c / 5) % 5, Z = c % 5;
-        const T val = acc[i];
-        const bool interior = X >= 1 && X <= 3 && Y >= 1 && Y <= 3 && Z >= 1 && Z <= 3;
-        T *dst = v == 0 ? q_m + cc : v < 4 ? q_mv + 3 * (int64_t)cc + (v - 1) : v < 13 ? q_mG + 9 * (int64_t)cc + (v - 4)
-               : q_slot + ((int64_t)cc * nmat + (v - 13) / 7) * 16 + ((v - 13) % 7 == 0 ? 0 : 6 + (v - 13) % 7);
-        if (interior) *dst = val;
-        else if (val != T(0)) atomicAdd(dst, val);
-    }
-}
-
 // cells with two or more occupied material slots (the compressed tangent covers one slot per cell)
 template <class T>
 __global__ void k_multislot(int64_t C, int nmat, const uint8_t *__restrict__ clocal, const T *__restrict__ q_slot,
@@ -1100,15 +968,6 @@ bool p2q_scatter() {
     if (v < 0) {
         const char *e = getenv("MPL_P2Q");
         v = (e && e[0] == 'g') ? 0 : 1;  // scatter default: cfg4 resample 4.15 vs 4.96 ms, cfg3 PPC 64 15.4 vs 21.1
-    }
-    return v == 1;
-}
-
-bool p2q_scatter4() {  // MPL_P2Q=scatter8: the thread-per-corner form of the scatter
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("MPL_P2Q");
-        v = (e && e[0] == 's' && e[7] == '8') ? 0 : 1;
     }
     return v == 1;
 }
@@ -1495,11 +1354,7 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     g, ctx->mats, (const int *)ctx->t_coord.p, (const int *)ctx->t_nplus.p, (const int *)ctx->t_bstart.p, \
         (const int *)ctx->t_cellof.p, (const T *)ctx->prec.p, (T *)ctx->q_m.p, (T *)ctx->q_mv.p,           \
         (T *)ctx->q_mG.p, (T *)ctx->q_slot.p
-            if (nm <= 2 && p2q_scatter4()) {
-                const size_t sm = (((size_t)125 * P2QNV<2>::V + 3) & ~(size_t)3) * s + (size_t)P2Q_CAP * REC * s;
-                MPL_CUDA(cudaFuncSetAttribute(k_p2q_tile4<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-                k_p2q_tile4<T, 2><<<T_, 128, sm, st>>>(P2QT_ARGS);
-            } else if (nm <= 2) {
+            if (nm <= 2) {
                 const size_t sm = (((size_t)125 * P2QNV<2>::V + 3) & ~(size_t)3) * s + (size_t)P2Q_CAP * REC * s;
                 MPL_CUDA(cudaFuncSetAttribute(k_p2q_tile<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
                 k_p2q_tile<T, 2><<<T_, 256, sm, st>>>(P2QT_ARGS);

@@ -31,8 +31,6 @@ CASES = [
     ({"MPL_P2Q": "gather"}, "vmmix_fp64"),
     ({"MPL_P2Q": "gather"}, "cfg1_fp32"),
     ({"MPL_P2Q": "gather"}, "cfg1b"),
-    ({"MPL_P2Q": "scatter8"}, "mix_fp32"),  # the thread-per-corner scatter
-    ({"MPL_P2Q": "scatter8"}, "cfg1b"),
     ({"MPL_SORT": "scatter"}, "mix_fp32"),   # the source-ordered sort (the gather form is default)
     ({"MPL_SORT": "scatter"}, "mix_fp64"),
     ({"MPL_KC": "0"}, "cfg1_fp32"),          # the 45-number tangent where the compressed one is the default

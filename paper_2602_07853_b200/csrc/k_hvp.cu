@@ -444,6 +444,7 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
                     }
         }
         // ---- node phase: forces + lumped mass term, stored (interior) or added atomically (faces)
+        float qm = 0.f;  // this lane's mass part of u . Hu for the tile (fp32 over <= 4 nodes, then fp64)
         int tt[4];
 #pragma unroll
         for (int r = 0; r < 4; r++) tt[r] = __shfl_sync(FULL, mcur, role[r] < 0 ? 0 : (role[r] >> 6) & 7);
@@ -459,17 +460,17 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
             }
             if (!(cur.has || owned) || tt[r] < 0) continue;
             if (owned) {
+                // branch-free: massless nodes have mm = 0 and a zero-filled halo slot
                 const float mm = S.mh[b][loc];
-                if (mm > 0.f) {
-                    const f4 w = uh[h];
-                    f.x += mm * w.x; f.y += mm * w.y; f.z += mm * w.z;
-                    acc += (double)(mm * (w.x * w.x + w.y * w.y + w.z * w.z));
-                }
+                const f4 w = uh[h];
+                f.x += mm * w.x; f.y += mm * w.y; f.z += mm * w.z;
+                qm += mm * (w.x * w.x + w.y * w.y + w.z * w.z);
             }
             const int64_t nd = (int64_t)tt[r] * 64 + loc;
             if (interior) Hu[nd] = mk4<float>(f.x, f.y, f.z, 0.f);
             else if (f.x != 0.f || f.y != 0.f || f.z != 0.f) atomic_add3<float>(Hu + nd, f.x, f.y, f.z);
         }
+        acc += (double)qm;
         __syncwarp();  // node phase done reading uh[b] / mh[b] before they are refilled
         mcur = mnext;
         mnext = mnn;
@@ -775,7 +776,8 @@ mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
     if (grid < 1) return MPL_OK;
     MPL_CUDA(launch_pdl(k_hvp_wz<KC, MINB>, grid, 32 * WZ_W, 0, ctx->stream, ctx->T, (const int *)ctx->t_nplus.p,
                         (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_hascells.p,
-                        (const float *)ctx->K.p, (const int *)ctx->t_kstart.p, (const float *)owned_mass(ctx),
+                        (const float *)ctx->K.p, (const int *)(KC ? ctx->t_kstart2.p : ctx->t_kstart.p),
+                        (const float *)owned_mass(ctx),
                         (const f4 *)u_tile, (f4 *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p,
                         tlist, ntl));
     ctx->launches++;

@@ -1,3 +1,4 @@
+#include <algorithm>
 // k_resample.cu — SURVEY §8(a) rows a0-a4: binning + activation, particle sort, P2Q scatter
 // (as a race-free per-cell gather over base-cell buckets), stretch reconstruction, C2N gather.
 //
@@ -420,7 +421,7 @@ __global__ void k_vg_to_sorted(int64_t np, const int *__restrict__ key, const in
 __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, const int *__restrict__ nminus,
                             const int *__restrict__ bcount, const int *__restrict__ hascells,
                             unsigned long long *__restrict__ cmask, int *__restrict__ ccount, int *__restrict__ ncell,
-                            int *__restrict__ kcnt, unsigned long long *ncells, int kz) {
+                            int *__restrict__ kcnt, unsigned long long *ncells, int *__restrict__ kcnt2) {
     int t = blockIdx.x;
     int l = threadIdx.x;  // 64 threads
     int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
@@ -455,7 +456,8 @@ __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, cons
         // tangent only on owned tiles: room for the full (45 c reals) or the compressed (56 per pair
         // slot) layout, rounded up to 4
         const int np = __popc(pairs);
-        kcnt[t] = hascells[t] ? (max(45 * c, 56 * np) + 3) & ~3 : 0;
+        kcnt[t] = hascells[t] ? (45 * c + 3) & ~3 : 0;  // the 45-number layout
+        kcnt2[t] = hascells[t] ? 56 * np : 0;           // the compressed layout (its own offsets)
         if (c && hascells[t]) atomicAdd(ncells, (unsigned long long)c);
     }
 }
@@ -1301,16 +1303,21 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CHECK(ensure(ctx, ctx->t_kcnt, (size_t)(T_ + 1) * 4 + 16));
     MPL_CHECK(ensure(ctx, ctx->t_kstart, (size_t)(T_ + 1) * 4 + 16));
     MPL_CUDA(cudaMemsetAsync(ctx->t_kcnt.p, 0, (size_t)(T_ + 1) * 4, st));
+    MPL_CHECK(ensure(ctx, ctx->t_kcnt2, (size_t)(T_ + 1) * 4 + 16));
+    MPL_CHECK(ensure(ctx, ctx->t_kstart2, (size_t)(T_ + 1) * 4 + 16));
+    MPL_CUDA(cudaMemsetAsync(ctx->t_kcnt2.p, 0, (size_t)(T_ + 1) * 4, st));
     if (T_) k_cell_mask<<<T_, 64, 0, st>>>(g, T_, (const int *)ctx->t_coord.p, (const int *)ctx->t_nminus.p,
                                           (const int *)ctx->t_bcount.p, (const int *)ctx->t_hascells.p,
                                           (unsigned long long *)ctx->t_cmask.p,
                                           (int *)ctx->t_ccount.p, (int *)ctx->t_ncell.p, (int *)ctx->t_kcnt.p,
-                                          counters + 1, hvp_kz_layout(ctx->precision)); ctx->launches++;
+                                          counters + 1, (int *)ctx->t_kcnt2.p); ctx->launches++;
     DBG_GUARDS("resample #7");
     MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_ccount.p, (int *)ctx->t_cstart.p, (int64_t)T_ + 1));
     MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_kcnt.p, (int *)ctx->t_kstart.p, (int64_t)T_ + 1));
-    int Cpad = 0, Ktot = 0;
+    MPL_CHECK(exclusive_scan<int>(ctx, (const int *)ctx->t_kcnt2.p, (int *)ctx->t_kstart2.p, (int64_t)T_ + 1));
+    int Cpad = 0, Ktot = 0, Ktot2 = 0;
     MPL_CHECK(d2h(ctx, &Ktot, (int *)ctx->t_kstart.p + T_, 4, st));
+    MPL_CHECK(d2h(ctx, &Ktot2, (int *)ctx->t_kstart2.p + T_, 4, st));
     unsigned long long ncells = 0;
     MPL_CHECK(d2h(ctx, &Cpad, (int *)ctx->t_cstart.p + T_, 4, st));
     MPL_CHECK(d2h(ctx, &ncells, counters + 1, 8, st));
@@ -1338,7 +1345,7 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     MPL_CHECK(ensure(ctx, ctx->q_slot, C * nm * 16 * s));
     if (ctx->mats.plastic) MPL_CHECK(ensure(ctx, ctx->q_Sp, C * nm * 9 * s));
     MPL_CHECK(ensure(ctx, ctx->q_vc, C * 12 * s));  // (v_c, G_c) per cell, written by Load's n2c
-    MPL_CHECK(ensure(ctx, ctx->K, (size_t)Ktot * s + 256));
+    MPL_CHECK(ensure(ctx, ctx->K, (size_t)std::max(Ktot, Ktot2) * s + 256));  // either tangent layout
     if (T_) {
         k_cell_list<<<T_, 64, 0, st>>>(T_, (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_cstart.p,
                                        (uint8_t *)ctx->c_local.p, (int *)ctx->t_cellof.p, (uint8_t *)ctx->t_perm.p);

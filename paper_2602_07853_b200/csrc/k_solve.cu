@@ -1332,7 +1332,8 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
     ctx->grid, ctx->mats, ctx->dt, (const int *)ctx->t_nplus.p, (const int *)ctx->t_cstart.p,                     \
         (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p, (const vec4<T> *)v_tile,                  \
         (const vec4<T> *)ctx->n_vhat.p, (const T *)owned_mass(ctx), (const T *)ctx->q_slot.p, (T *)ctx->K.p,       \
-        (const int *)ctx->t_kstart.p, (const int *)ctx->t_ncell.p, (vec4<T> *)ctx->n_g.p, (vec4<T> *)ctx->n_diag.p, \
+        (const int *)(kc ? ctx->t_kstart2.p : ctx->t_kstart.p), (const int *)ctx->t_ncell.p, (vec4<T> *)ctx->n_g.p, \
+        (vec4<T> *)ctx->n_diag.p,                                                                                 \
         ctx->mats.plastic ? (T *)ctx->q_Sp.p : (T *)nullptr, sc, hvp_kz_layout(ctx->precision), kc
         // 64 threads per tile: one per cell (a tile has <= 64); 128 left half the CTA idle in the
         // cell phase (ncu at cfg4: barrier stalls 34 %, 16 warps / SM by registers)

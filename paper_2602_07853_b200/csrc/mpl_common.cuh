@@ -484,6 +484,7 @@ struct mpl_ctx_s {
     DevBuf cflag, nflag, tile_of, scan_tmp;
     DevBuf t_coord, t_nplus, t_nminus, t_cstart, t_ccount, t_hascells, t_bcount, t_bstart, t_cellof, t_cmask, t_perm;
     DevBuf t_ncell, t_kcnt, t_kstart;  // real cells per tile; tangent reals per tile (rounded to 4) and offsets
+    DevBuf t_kcnt2, t_kstart2;         // the same for the compressed tangent (56 reals per pair slot)
     DevBuf c_local;
     // quadrature (compact cells)
     DevBuf q_m, q_mv, q_mG, q_slot;  // q_slot: C * nmat * 16 (V, E xx yy zz xy yz xz, tau (6), pad)
@@ -628,6 +629,8 @@ template <class F> void for_each_buf(mpl_ctx ctx, F f) {
         {"t_ncell", ctx->t_ncell},
         {"t_kcnt", ctx->t_kcnt},
         {"t_kstart", ctx->t_kstart},
+        {"t_kcnt2", ctx->t_kcnt2},
+        {"t_kstart2", ctx->t_kstart2},
         {"n_mass", ctx->n_mass},
         {"n_flag", ctx->n_flag},
         {"n_vn", ctx->n_vn},

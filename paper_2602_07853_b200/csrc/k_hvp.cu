@@ -444,7 +444,6 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
                     }
         }
         // ---- node phase: forces + lumped mass term, stored (interior) or added atomically (faces)
-        float qm = 0.f;  // this lane's mass part of u . Hu for the tile (fp32 over <= 4 nodes, then fp64)
         int tt[4];
 #pragma unroll
         for (int r = 0; r < 4; r++) tt[r] = __shfl_sync(FULL, mcur, role[r] < 0 ? 0 : (role[r] >> 6) & 7);
@@ -460,17 +459,17 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
             }
             if (!(cur.has || owned) || tt[r] < 0) continue;
             if (owned) {
-                // branch-free: massless nodes have mm = 0 and a zero-filled halo slot
                 const float mm = S.mh[b][loc];
-                const f4 w = uh[h];
-                f.x += mm * w.x; f.y += mm * w.y; f.z += mm * w.z;
-                qm += mm * (w.x * w.x + w.y * w.y + w.z * w.z);
+                if (mm > 0.f) {
+                    const f4 w = uh[h];
+                    f.x += mm * w.x; f.y += mm * w.y; f.z += mm * w.z;
+                    acc += (double)(mm * (w.x * w.x + w.y * w.y + w.z * w.z));
+                }
             }
             const int64_t nd = (int64_t)tt[r] * 64 + loc;
             if (interior) Hu[nd] = mk4<float>(f.x, f.y, f.z, 0.f);
             else if (f.x != 0.f || f.y != 0.f || f.z != 0.f) atomic_add3<float>(Hu + nd, f.x, f.y, f.z);
         }
-        acc += (double)qm;
         __syncwarp();  // node phase done reading uh[b] / mh[b] before they are refilled
         mcur = mnext;
         mnext = mnn;

@@ -215,7 +215,7 @@ __device__ __forceinline__ void kc_apply2(const float *k, const float2 d[9], flo
         }
 }
 
-template <bool KC, int MINB = KC ? 4 : 3>
+template <bool KC, int MINB = KC ? 4 : 3, bool LIST = false>
 __global__ void __launch_bounds__(32 * WZ_W, MINB)
     k_hvp_wz(int T_, const int *__restrict__ nplus, const unsigned long long *__restrict__ cmask,
              const int *__restrict__ hascells, const float *__restrict__ K, const int *__restrict__ kstart,
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
              const int *__restrict__ tlist, int ntl) {
     // items: tiles 0..T_-1, or the listed tiles tlist[0..ntl) (slab ranks: the interface tiles first, so
     // their halo exchange overlaps the interior tiles' launch)
-    const int N = tlist ? ntl : T_;
+    const int N = LIST ? ntl : T_;
     __shared__ WzWarp SW[WZ_W];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WzWarp &S = SW[wid];
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
     const int mstride = lane < 8 ? 8 : lane < 10 ? 1 : 2;
     auto load_meta = [&](int i) -> int {  // metadata of item i's tile
         if (i >= N || lane >= 12) return 0;
-        const int t = tlist ? __ldg(tlist + i) : i;
+        const int t = LIST ? __ldg(tlist + i) : i;
         return lane == 0 ? t : __ldg(mbase + (int64_t)mstride * t);
     };
     struct TileK {
@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(32 * WH_W, MINB)
 
 int g_num_sms = 0;
 
-template <bool KC, int MINB>
+template <bool KC, int MINB, bool LIST>
 mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
                      double cgthr, const int *tlist, int ntl) {
     static int per_sm = 0;
@@ -765,7 +765,7 @@ mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         int occ = 0;
-        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_wz<KC, MINB>, 32 * WZ_W, 0));
+        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_wz<KC, MINB, LIST>, 32 * WZ_W, 0));
         per_sm = occ > 0 ? occ : 1;
     }
     // persistent: one wave of (SMs x resident CTAs), tiles strided by the global warp count
@@ -773,7 +773,7 @@ mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
     const int need = ((tlist ? ntl : ctx->T) + WZ_W - 1) / WZ_W;
     if (grid > need) grid = need;
     if (grid < 1) return MPL_OK;
-    MPL_CUDA(launch_pdl(k_hvp_wz<KC, MINB>, grid, 32 * WZ_W, 0, ctx->stream, ctx->T, (const int *)ctx->t_nplus.p,
+    MPL_CUDA(launch_pdl(k_hvp_wz<KC, MINB, LIST>, grid, 32 * WZ_W, 0, ctx->stream, ctx->T, (const int *)ctx->t_nplus.p,
                         (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_hascells.p,
                         (const float *)ctx->K.p, (const int *)(KC ? ctx->t_kstart2.p : ctx->t_kstart.p),
                         (const float *)owned_mass(ctx),
@@ -849,10 +849,12 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
             const char *e = getenv("MPL_KC_MINB");
             minb = e ? atoi(e) : 3;
         }
-        if (minb == 4) return launch_wz<true, 4>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
-        return launch_wz<true, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
+        if (tlist) return launch_wz<true, 3, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
+        if (minb == 4) return launch_wz<true, 4, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
+        return launch_wz<true, 3, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
     }
-    return launch_wz<false, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
+    if (tlist) return launch_wz<false, 3, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
+    return launch_wz<false, 3, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
 }
 
 template mpl_status launch_hvp<float>(mpl_ctx, const void *, void *, double *, const CGSlot *, int, double,

@@ -964,9 +964,9 @@ __global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, int64_t S, const
 // the nodes l + 32 e, so every SoA component load, list load and tile-dense p / Hp access of one
 // instruction is contiguous across the warp (the group mapping above writes p / Hp at a 64-byte lane
 // stride).  Full chunks run without per-node bounds checks.
-constexpr int PCG_E = 4;
-template <class T>
-__global__ void __launch_bounds__(256, 2) k_pcg_update1w(int64_t n, int64_t S, const int *__restrict__ list, int j,
+constexpr int PCG_E = 4;  // default nodes per lane per chunk (MPL_PCG_E: 2, 4)
+template <class T, int E = PCG_E>
+__global__ void __launch_bounds__(256, E <= 2 ? 4 : 2) k_pcg_update1w(int64_t n, int64_t S, const int *__restrict__ list, int j,
                                                          double thr, const T *__restrict__ invD,
                                                          const vec4<T> *__restrict__ p, vec4<T> *__restrict__ Hp,
                                                          T *__restrict__ x, T *__restrict__ r,
@@ -995,11 +995,11 @@ __global__ void __launch_bounds__(256, 2) k_pcg_update1w(int64_t n, int64_t S, c
     T rz = 0, rr = 0;
     auto chunk = [&](int64_t base, auto full) {
         constexpr bool FULL = decltype(full)::value;
-        int li[PCG_E];
-        T iv[PCG_E][3], rv[PCG_E][3];
-        vec4<T> hv[PCG_E];
+        int li[E];
+        T iv[E][3], rv[E][3];
+        vec4<T> hv[E];
 #pragma unroll
-        for (int e = 0; e < PCG_E; e++) {
+        for (int e = 0; e < E; e++) {
             const int64_t i = base + 32 * e + lane;
             if (FULL || i < n) {
                 li[e] = list[i];
@@ -1010,10 +1010,10 @@ __global__ void __launch_bounds__(256, 2) k_pcg_update1w(int64_t n, int64_t S, c
             }
         }
 #pragma unroll
-        for (int e = 0; e < PCG_E; e++)
+        for (int e = 0; e < E; e++)
             if (FULL || li[e] >= 0) hv[e] = Hp[li[e]];
 #pragma unroll
-        for (int e = 0; e < PCG_E; e++) {
+        for (int e = 0; e < E; e++) {
             if (!FULL && li[e] < 0) continue;
             const int64_t i = base + 32 * e + lane;
             Hp[li[e]] = mk4<T>(0, 0, 0, 0);
@@ -1026,17 +1026,17 @@ __global__ void __launch_bounds__(256, 2) k_pcg_update1w(int64_t n, int64_t S, c
             rr += w * (rv[e][0] * rv[e][0] + rv[e][1] * rv[e][1] + rv[e][2] * rv[e][2]);
         }
     };
-    for (int64_t ch = w0; ch * 32 * PCG_E < n; ch += nw) {
-        const int64_t base = ch * 32 * PCG_E;
-        if (base + 32 * PCG_E <= n) chunk(base, std::true_type{});
+    for (int64_t ch = w0; ch * 32 * E < n; ch += nw) {
+        const int64_t base = ch * 32 * E;
+        if (base + 32 * E <= n) chunk(base, std::true_type{});
         else chunk(base, std::false_type{});
     }
     block_add((double)rz, slot[j + 1].rz);
     block_add((double)rr, slot[j + 1].rr);
 }
 
-template <class T>
-__global__ void __launch_bounds__(256, 2) k_pcg_update2w(int64_t n, int64_t S, const int *__restrict__ list, int j,
+template <class T, int E = PCG_E>
+__global__ void __launch_bounds__(256, E <= 2 ? 4 : 2) k_pcg_update2w(int64_t n, int64_t S, const int *__restrict__ list, int j,
                                                          double thr, const T *__restrict__ invD,
                                                          const T *__restrict__ r, vec4<T> *__restrict__ p,
                                                          T *__restrict__ x, const CGSlot *slot, const DevScalars *sc) {
@@ -1052,11 +1052,11 @@ __global__ void __launch_bounds__(256, 2) k_pcg_update2w(int64_t n, int64_t S, c
     const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     auto chunk = [&](int64_t base, auto full) {
         constexpr bool FULL = decltype(full)::value;
-        int li[PCG_E];
-        T xv[PCG_E][3], rv[PCG_E][3], iv[PCG_E][3];
-        vec4<T> pv[PCG_E];
+        int li[E];
+        T xv[E][3], rv[E][3], iv[E][3];
+        vec4<T> pv[E];
 #pragma unroll
-        for (int e = 0; e < PCG_E; e++) {
+        for (int e = 0; e < E; e++) {
             const int64_t i = base + 32 * e + lane;
             if (FULL || i < n) {
                 li[e] = list[i];
@@ -1070,10 +1070,10 @@ __global__ void __launch_bounds__(256, 2) k_pcg_update2w(int64_t n, int64_t S, c
             }
         }
 #pragma unroll
-        for (int e = 0; e < PCG_E; e++)
+        for (int e = 0; e < E; e++)
             if (FULL || li[e] >= 0) pv[e] = p[li[e]];
 #pragma unroll
-        for (int e = 0; e < PCG_E; e++) {
+        for (int e = 0; e < E; e++) {
             if (!FULL && li[e] < 0) continue;
             const int64_t i = base + 32 * e + lane;
             x[i] = xv[e][0] + alpha * pv[e].x;
@@ -1084,9 +1084,9 @@ __global__ void __launch_bounds__(256, 2) k_pcg_update2w(int64_t n, int64_t S, c
                                   rv[e][2] * iv[e][2] + beta * pv[e].z, T(0));
         }
     };
-    for (int64_t ch = w0; ch * 32 * PCG_E < n; ch += nw) {
-        const int64_t base = ch * 32 * PCG_E;
-        if (base + 32 * PCG_E <= n) chunk(base, std::true_type{});
+    for (int64_t ch = w0; ch * 32 * E < n; ch += nw) {
+        const int64_t base = ch * 32 * E;
+        if (base + 32 * E <= n) chunk(base, std::true_type{});
         else chunk(base, std::false_type{});
     }
 }
@@ -1476,6 +1476,9 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         cudaDeviceGetAttribute(&nsm_, cudaDevAttrMultiProcessorCount, dev);
     }
     const unsigned VAP = std::min<unsigned>(VA1, (unsigned)nsm_ * 8);  // persistent update kernels
+    const char *pee = getenv("MPL_PCG_E");  // nodes per lane per chunk of the classic fp32 kernels (2 or 4)
+    const int pcg_e = pee ? atoi(pee) : 4;
+    const unsigned VAP2 = std::min<unsigned>(VA1, (unsigned)nsm_ * 16);  // E = 2: 4 CTAs per SM
     const int *list = (const int *)ctx->n_list.p;
     // L2 persisting access-policy window for the Newton solve over p (MPL_L2WIN=p, default: the HVP's
     // gathered input, read by update2), Hp (=h: the HVP's atomics target) or both at half hit ratio
@@ -1687,7 +1690,10 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     if (timed) sampled.push_back({nl, jj});
                     nl++;
                     if (vec_events) cudaEventRecord(vev[nl - 1][0], st);
-                    if (pcg_warp_map)
+                    if (pcg_warp_map && pcg_e == 2)
+                        MPL_CUDA(launch_pdl(k_pcg_update1w<T, 2>, VAP2, 256, 0, st, NA, SA, list, jj, thr, invD, p, Hp, x,
+                                            r, own_w, slots, sc));
+                    else if (pcg_warp_map)
                         MPL_CUDA(launch_pdl(k_pcg_update1w<T>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p, Hp, x,
                                             r, own_w, slots, sc));
                     else
@@ -1696,7 +1702,10 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     ctx->launches++;
                     MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
                     if (vec_events) cudaEventRecord(vev[nl - 1][1], st);
-                    if (pcg_warp_map)
+                    if (pcg_warp_map && pcg_e == 2)
+                        MPL_CUDA(launch_pdl(k_pcg_update2w<T, 2>, VAP2, 256, 0, st, NA, SA, list, jj, thr, invD, r, p, x,
+                                            slots, sc));
+                    else if (pcg_warp_map)
                         MPL_CUDA(launch_pdl(k_pcg_update2w<T>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, r, p, x,
                                             slots, sc));
                     else

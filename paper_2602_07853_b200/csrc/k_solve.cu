@@ -964,9 +964,9 @@ __global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, int64_t S, const
 // the nodes l + 32 e, so every SoA component load, list load and tile-dense p / Hp access of one
 // instruction is contiguous across the warp (the group mapping above writes p / Hp at a 64-byte lane
 // stride).  Full chunks run without per-node bounds checks.
-constexpr int PCG_E = 4;  // default nodes per lane per chunk (MPL_PCG_E: 2, 4)
+constexpr int PCG_E = 4;  // nodes per lane per chunk (2 with 4 CTAs per SM measured slower: cfg4 step 65.2 vs 59.1 ms)
 template <class T, int E = PCG_E>
-__global__ void __launch_bounds__(256, E <= 2 ? 4 : 2) k_pcg_update1w(int64_t n, int64_t S, const int *__restrict__ list, int j,
+__global__ void __launch_bounds__(256, 2) k_pcg_update1w(int64_t n, int64_t S, const int *__restrict__ list, int j,
                                                          double thr, const T *__restrict__ invD,
                                                          const vec4<T> *__restrict__ p, vec4<T> *__restrict__ Hp,
                                                          T *__restrict__ x, T *__restrict__ r,
@@ -1036,7 +1036,7 @@ __global__ void __launch_bounds__(256, E <= 2 ? 4 : 2) k_pcg_update1w(int64_t n,
 }
 
 template <class T, int E = PCG_E>
-__global__ void __launch_bounds__(256, E <= 2 ? 4 : 2) k_pcg_update2w(int64_t n, int64_t S, const int *__restrict__ list, int j,
+__global__ void __launch_bounds__(256, 2) k_pcg_update2w(int64_t n, int64_t S, const int *__restrict__ list, int j,
                                                          double thr, const T *__restrict__ invD,
                                                          const T *__restrict__ r, vec4<T> *__restrict__ p,
                                                          T *__restrict__ x, const CGSlot *slot, const DevScalars *sc) {
@@ -1476,9 +1476,6 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         cudaDeviceGetAttribute(&nsm_, cudaDevAttrMultiProcessorCount, dev);
     }
     const unsigned VAP = std::min<unsigned>(VA1, (unsigned)nsm_ * 8);  // persistent update kernels
-    const char *pee = getenv("MPL_PCG_E");  // nodes per lane per chunk of the classic fp32 kernels (2 or 4)
-    const int pcg_e = pee ? atoi(pee) : 4;
-    const unsigned VAP2 = std::min<unsigned>(VA1, (unsigned)nsm_ * 16);  // E = 2: 4 CTAs per SM
     const int *list = (const int *)ctx->n_list.p;
     // L2 persisting access-policy window for the Newton solve over p (MPL_L2WIN=p, default: the HVP's
     // gathered input, read by update2), Hp (=h: the HVP's atomics target) or both at half hit ratio
@@ -1690,10 +1687,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     if (timed) sampled.push_back({nl, jj});
                     nl++;
                     if (vec_events) cudaEventRecord(vev[nl - 1][0], st);
-                    if (pcg_warp_map && pcg_e == 2)
-                        MPL_CUDA(launch_pdl(k_pcg_update1w<T, 2>, VAP2, 256, 0, st, NA, SA, list, jj, thr, invD, p, Hp, x,
-                                            r, own_w, slots, sc));
-                    else if (pcg_warp_map)
+                    if (pcg_warp_map)
                         MPL_CUDA(launch_pdl(k_pcg_update1w<T>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p, Hp, x,
                                             r, own_w, slots, sc));
                     else
@@ -1702,10 +1696,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     ctx->launches++;
                     MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
                     if (vec_events) cudaEventRecord(vev[nl - 1][1], st);
-                    if (pcg_warp_map && pcg_e == 2)
-                        MPL_CUDA(launch_pdl(k_pcg_update2w<T, 2>, VAP2, 256, 0, st, NA, SA, list, jj, thr, invD, r, p, x,
-                                            slots, sc));
-                    else if (pcg_warp_map)
+                    if (pcg_warp_map)
                         MPL_CUDA(launch_pdl(k_pcg_update2w<T>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, r, p, x,
                                             slots, sc));
                     else

@@ -806,15 +806,26 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
 }
 
 // cells with two or more occupied material slots (the compressed tangent covers one slot per cell)
+// and cells with an occupied slot whose stretch base is not I (E = S - I != 0): the compressed tangent's
+// PSD projection is exact only at S = I
 template <class T>
 __global__ void k_multislot(int64_t C, int nmat, const uint8_t *__restrict__ clocal, const T *__restrict__ q_slot,
-                            unsigned long long *count) {
+                            unsigned long long *count, unsigned long long *nonid) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int k = 0;
+    bool ni = false;
     if (c < C && clocal[c] != 0xFF)
-        for (int q = 0; q < nmat; q++) k += q_slot[(c * nmat + q) * 16] != T(0);
-    const unsigned int b = __ballot_sync(0xffffffffu, k >= 2);
+        for (int q = 0; q < nmat; q++) {
+            const T *sl = q_slot + (c * nmat + q) * 16;
+            if (sl[0] != T(0)) {
+                k++;
+#pragma unroll
+                for (int a = 1; a < 7; a++) ni = ni || sl[a] != T(0);
+            }
+        }
+    const unsigned int b = __ballot_sync(0xffffffffu, k >= 2), bn = __ballot_sync(0xffffffffu, ni);
     if ((threadIdx.x & 31) == 0 && b) atomicAdd(count, (unsigned long long)__popc(b));
+    if ((threadIdx.x & 31) == 0 && bn) atomicAdd(nonid, (unsigned long long)__popc(bn));
 }
 
 // a4 after the scatter: per (cell, slot) tau = (V tau) / V (Eq. vtau) and the stretch base
@@ -1392,9 +1403,10 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     DBG_GUARDS("resample #9");
     }
     ctx->multi_slot_cells = 0;
-    if (nm > 1 && Cpad) {
+    ctx->nonid_base_cells = 0;
+    if (Cpad) {
         k_multislot<T><<<nblk(Cpad, 256), 256, 0, st>>>((int64_t)Cpad, nm, (const uint8_t *)ctx->c_local.p,
-                                                       (const T *)ctx->q_slot.p, counters + 3);
+                                                       (const T *)ctx->q_slot.p, counters + 3, counters + 4);
         ctx->launches++;
     }
     // nodes
@@ -1441,12 +1453,14 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     DBG_GUARDS("resample #14");
         MPL_CHECK(d2h_sync(ctx, st));
         nact = lc + la;
-        unsigned long long nf = 0, ms = 0;
+        unsigned long long nf = 0, ms = 0, ni = 0;
         MPL_CHECK(d2h(ctx, &nf, counters + 2, 8, st));
         MPL_CHECK(d2h(ctx, &ms, counters + 3, 8, st));
+        MPL_CHECK(d2h(ctx, &ni, counters + 4, 8, st));
         MPL_CHECK(d2h_sync(ctx, st));
         ctx->n_free_nodes = (int64_t)nf;
         ctx->multi_slot_cells = (int64_t)ms;
+        ctx->nonid_base_cells = (int64_t)ni;
     }
     ctx->n_nodes_active = nact;
     MPL_CUDA(cudaGetLastError());

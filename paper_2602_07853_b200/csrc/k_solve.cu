@@ -156,7 +156,9 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
     constexpr int KS = (MODE == LIN_FULL) ? 64 * 45 : 1;
     // compressed tangent (kc = 1: fp32, every slot elastic StVK-Hencky, one occupied slot per cell):
     // 28 reals per cell, written in k_hvp_wz's interleaved pair layout
-    constexpr bool KCOK = (MODE == LIN_FULL) && HONLY && !PSD && sizeof(T) == 4;
+    // with PSD only when every base S is I (the resample counts the other cells): then K = c C(A) exactly, and
+    // its per-cell projection is the blockwise clamping of C in the SVD frame
+    constexpr bool KCOK = (MODE == LIN_FULL) && HONLY && sizeof(T) == 4;
     __shared__ unsigned int pm_s, cm_s[2];  // KC: k_hvp_wz lanes holding a cell; the tile's cell mask
     __shared__ vec4<T> vh[125];
     __shared__ T Pg[64 * 9];
@@ -485,12 +487,71 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
                             kc_[21 + 2 * pp] = c * b_;
                         }
                         kc_[26] = kc_[27] = T(0);
+                        if (PSD) {
+                            // S = I: the per-cell PSD projection of K = c C is C's blockwise clamping (amb-6b):
+                            // the 3x3 block by its eigenvalues, each [[a, b], [b, a]] by a + b and a - b
+                            T Dm[9] = {kc_[14], kc_[17], kc_[19], kc_[17], kc_[15], kc_[18], kc_[19], kc_[18], kc_[16]};
+                            T dw[3], DQ[9];
+                            sym_eig3(Dm, dw, DQ);
+#pragma unroll
+                            for (int i = 0; i < 3; i++) dw[i] = dw[i] > T(0) ? dw[i] : T(0);
+                            auto dent = [&](int r, int cc) {
+                                return DQ[3 * r] * DQ[3 * cc] * dw[0] + DQ[3 * r + 1] * DQ[3 * cc + 1] * dw[1] +
+                                       DQ[3 * r + 2] * DQ[3 * cc + 2] * dw[2];
+                            };
+                            kc_[14] = dent(0, 0); kc_[15] = dent(1, 1); kc_[16] = dent(2, 2);
+                            kc_[17] = dent(0, 1); kc_[18] = dent(1, 2); kc_[19] = dent(0, 2);
+#pragma unroll
+                            for (int pp = 0; pp < 3; pp++) {
+                                const T a_ = kc_[20 + 2 * pp], b_ = kc_[21 + 2 * pp];
+                                const T lp = a_ + b_ > T(0) ? a_ + b_ : T(0), lm = a_ - b_ > T(0) ? a_ - b_ : T(0);
+                                kc_[20 + 2 * pp] = T(0.5) * (lp + lm);
+                                kc_[21 + 2 * pp] = T(0.5) * (lp - lm);
+                            }
+                            // K+ (45 numbers, for the Jacobi diagonal): column (e, f) = U (C+ : U^T E_ef V) V^T
+                            T *Kr = Ks + j * 45;
+                            const T Dp[9] = {kc_[14], kc_[17], kc_[19], kc_[17], kc_[15], kc_[18], kc_[19], kc_[18], kc_[16]};
+#pragma unroll
+                            for (int ef = 0; ef < 9; ef++) {
+                                const int e_ = ef / 3, f_ = ef % 3;
+                                T Xh[9], Yh[9];
+#pragma unroll
+                                for (int i = 0; i < 3; i++)
+#pragma unroll
+                                    for (int jj = 0; jj < 3; jj++) Xh[3 * i + jj] = U[3 * e_ + i] * Vm[3 * f_ + jj];
+#pragma unroll
+                                for (int i = 0; i < 3; i++)
+                                    Yh[4 * i] = Dp[3 * i] * Xh[0] + Dp[3 * i + 1] * Xh[4] + Dp[3 * i + 2] * Xh[8];
+                                const int pi2[3] = {0, 0, 1}, pj2[3] = {1, 2, 2};
+#pragma unroll
+                                for (int pp = 0; pp < 3; pp++) {
+                                    const int i = pi2[pp], jj = pj2[pp];
+                                    const T a_ = kc_[20 + 2 * pp], b_ = kc_[21 + 2 * pp];
+                                    Yh[3 * i + jj] = a_ * Xh[3 * i + jj] + b_ * Xh[3 * jj + i];
+                                    Yh[3 * jj + i] = b_ * Xh[3 * i + jj] + a_ * Xh[3 * jj + i];
+                                }
+#pragma unroll
+                                for (int a = 0; a < 3; a++)
+#pragma unroll
+                                    for (int b = 0; b < 3; b++) {
+                                        T y = T(0);
+#pragma unroll
+                                        for (int i = 0; i < 3; i++)
+#pragma unroll
+                                            for (int jj = 0; jj < 3; jj++) y += U[3 * a + i] * Yh[3 * i + jj] * Vm[3 * b + jj];
+                                        const int r = 3 * a + b;
+                                        if (r <= ef) Kr[kidx(r, ef)] += (r == ef ? y : T(0.5) * y);
+                                        if (r > ef) Kr[kidx(ef, r)] += T(0.5) * y;
+                                    }
+                            }
+                        }
 #pragma unroll
                         for (int e = 0; e < 28; e++) Kout[kc_base + (int64_t)(e >> 1) * 4 * kc_np + 2 * (e & 1)] = kc_[e];
                         kc_done = true;
                     }
                     const T kscale = sV * T(1.0 / 16.0) * T(g.inv_dx * g.inv_dx);
                     T *Kr = Ks + j * 45;
+                    if (!(KCOK && PSD && kc))  // (KC + PSD: K+ assembled above from the projected blocks)
 #pragma unroll
                     for (int a = 0; a < 3; a++)
 #pragma unroll
@@ -548,7 +609,8 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
     }
     __syncthreads();
     if (PSD && MODE == LIN_FULL && has) {  // per-cell PSD projection before the K write and the diagonal
-        if (tid < nc && clocal[cs + tid] != 0xFF) psd_project45<T>(Ks + tid * 45);  // fp64: spills, acceptable
+        if (!(KCOK && kc) && tid < nc && clocal[cs + tid] != 0xFF)
+            psd_project45<T>(Ks + tid * 45);  // fp64: spills, acceptable
         __syncthreads();
     }
     if (MODE == LIN_FULL && has) {  // tile's tangent block, permuted into the chunked (coalesced) layout
@@ -1346,8 +1408,8 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
         // compressed tangent (MPL_KC, default on): fp32 k_hvp_wz, StVK-Hencky elastic only, exact Hessian,
         // one occupied material slot per cell
         const char *kce = getenv("MPL_KC");
-        const int kc = (mode == LIN_FULL && sizeof(T) == 4 && honly && !ctx->psd_now && hvp_variant() == 0 &&
-                        ctx->multi_slot_cells == 0 && !(kce && kce[0] == '0')) ? 1 : 0;
+        const int kc = (mode == LIN_FULL && sizeof(T) == 4 && honly && (!ctx->psd_now || ctx->nonid_base_cells == 0) &&
+                        hvp_variant() == 0 && ctx->multi_slot_cells == 0 && !(kce && kce[0] == '0')) ? 1 : 0;
         if (mode == LIN_FULL) ctx->kc_now = kc;
         if (mode == LIN_FULL && ctx->psd_now) {  // per-cell PSD projection of K
             // launch bounds (128, 1): the register-resident Jacobi (126 live reals) needs the registers

@@ -473,6 +473,7 @@ struct mpl_ctx_s {
     // compressed tangent: cells with more than one occupied material slot (from the resample)
     // and the format the last full linearisation wrote (0: 45-number K, 1: compressed, 28 reals per cell)
     int64_t multi_slot_cells = 0;
+    int64_t nonid_base_cells = 0;  // cells with an occupied slot whose base S is not I (E != 0)
     int kc_now = 0;
 
     // tiles

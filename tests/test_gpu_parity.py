@@ -83,6 +83,17 @@ def compressed_cube(precision=64):
                                solver=dataclasses.replace(sc.solver, psd=True))
 
 
+def compressing_cube(precision=32):
+    """cfg1's cube at rest (F_p = I, so every stretch base S = I) with a converging velocity field v = -5 (x - c):
+    the trial deformation compresses the cells and the exact Hessian turns indefinite; with the PSD-projected
+    Hessian and S = I the fp32 path projects the compressed tangent blockwise (amb-6b)."""
+    sc = scenes.cfg1(prestrain=False, precision=precision)
+    v = -5.0 * (sc.x - 0.5)
+    floor = scenes.DirichletBox((-1e9, -1e9, -1e9), (1e9, 4.5 / 16, 1e9), (0.0, 0.0, 0.0))
+    return dataclasses.replace(sc, name="psdI", v=v, materials=[scenes.Material(1e6, 0.3, 1000.0)], dirichlet=[floor],
+                               solver=dataclasses.replace(sc.solver, psd=True))
+
+
 SCENES = {
     "cfg1": lambda: scenes.cfg1(),
     "cfg1b": lambda: scenes.cfg1(prestrain=True),
@@ -108,6 +119,8 @@ SCENES = {
     # per-cell PSD-projected Hessian on an indefinite (compressed) state
     "psd_fp64": lambda: compressed_cube(64),
     "psd_fp32": lambda: compressed_cube(32),
+    "psdI_fp32": lambda: compressing_cube(32),
+    "psdI_fp64": lambda: compressing_cube(64),
 }
 
 

@@ -363,7 +363,10 @@ def run_e2e(ctx, sc, solver, args, sel, ws):
         n_hvp_dofs, h2d, d2h = pdist.reduce_scalars([n_hvp_dofs, h2d, d2h], "sum", device="cuda")
     val = n_hvp_dofs / wall / 1e9
     return {"value": round(val, 3), "unit": "GDOF/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "ms_per_step": round(wall * 1e3 / steps, 3), "steps": steps}
+            "ms_per_step": round(wall * 1e3 / steps, 3), "steps": steps,
+            "mode": ("pipelined: every step uploads the same host particle state (independent steps), so step s+1's "
+                     "upload overlaps step s's solve and step s's readback overlaps step s+1" if single else
+                     "synchronous per step on slab ranks (set_particles, step, get_particles)")}
 
 
 # ------------------------------------------------------------------------------------------------

@@ -215,7 +215,7 @@ __device__ __forceinline__ void kc_apply2(const float *k, const float2 d[9], flo
         }
 }
 
-template <bool KC, int MINB = KC ? 4 : 3, bool LIST = false, bool SPLITK = false>
+template <bool KC, int MINB = 3, bool LIST = false>
 __global__ void __launch_bounds__(32 * WZ_W, MINB)
     k_hvp_wz(int T_, const int *__restrict__ nplus, const unsigned long long *__restrict__ cmask,
              const int *__restrict__ hascells, const float *__restrict__ K, const int *__restrict__ kstart,
@@ -403,15 +403,10 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
             }
             acc += (double)qf;
         }
-        // k is free: start the next tile's loads; they overlap the scatter and the node phase (KC with
-        // SPLITK: the second half after the scatter, so fewer prefetch registers are live during it)
-        if (KC && SPLITK) {
+        // k is free: start the next tile's loads; they overlap the scatter and the node phase (issuing the
+        // second half after the scatter measured slower: 87.3 vs 86.2 us at cfg4)
 #pragma unroll
-            for (int c = 0; c < 12; c++) kload(nxt, 0, c);
-        } else {
-#pragma unroll
-            for (int c = 0; c < 12; c++) { kload(nxt, 0, c); kload(nxt, 45, c); }
-        }
+        for (int c = 0; c < 12; c++) { kload(nxt, 0, c); kload(nxt, 45, c); }
         halo(t + G, b ^ 1, mnext);
         // corner force of cell X at (sx, sy, sz) = +-(Px +- Py) +- Pz per component: 4 sums g; the value
         // of corner (ox, oy, oz): (sx, sy) = (+,+) -> g0/g1, (-,-) -> -g1/-g0, (+,-) -> g2/g3,
@@ -448,10 +443,6 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
                         *fp = mk4<float>(o.x + f.x, o.y + f.y, o.z + f.z, 0.f);
                         __syncwarp();
                     }
-        }
-        if (KC && SPLITK) {
-#pragma unroll
-            for (int c = 0; c < 12; c++) kload(nxt, 45, c);
         }
         // ---- node phase: forces + lumped mass term, stored (interior) or added atomically (faces)
         int tt[4];
@@ -766,7 +757,7 @@ __global__ void __launch_bounds__(32 * WH_W, MINB)
 
 int g_num_sms = 0;
 
-template <bool KC, int MINB, bool LIST, bool SPLITK = false>
+template <bool KC, int MINB, bool LIST>
 mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
                      double cgthr, const int *tlist, int ntl) {
     static int per_sm = 0;
@@ -775,7 +766,7 @@ mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         int occ = 0;
-        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_wz<KC, MINB, LIST, SPLITK>, 32 * WZ_W, 0));
+        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_wz<KC, MINB, LIST>, 32 * WZ_W, 0));
         per_sm = occ > 0 ? occ : 1;
     }
     // persistent: one wave of (SMs x resident CTAs), tiles strided by the global warp count
@@ -783,7 +774,7 @@ mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
     const int need = ((tlist ? ntl : ctx->T) + WZ_W - 1) / WZ_W;
     if (grid > need) grid = need;
     if (grid < 1) return MPL_OK;
-    MPL_CUDA(launch_pdl(k_hvp_wz<KC, MINB, LIST, SPLITK>, grid, 32 * WZ_W, 0, ctx->stream, ctx->T, (const int *)ctx->t_nplus.p,
+    MPL_CUDA(launch_pdl(k_hvp_wz<KC, MINB, LIST>, grid, 32 * WZ_W, 0, ctx->stream, ctx->T, (const int *)ctx->t_nplus.p,
                         (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_hascells.p,
                         (const float *)ctx->K.p, (const int *)(KC ? ctx->t_kstart2.p : ctx->t_kstart.p),
                         (const float *)owned_mass(ctx),
@@ -861,8 +852,6 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
         }
         if (tlist) return launch_wz<true, 3, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
         if (minb == 4) return launch_wz<true, 4, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
-        if (minb == 5) return launch_wz<true, 4, false, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
-        if (minb == 6) return launch_wz<true, 3, false, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
         return launch_wz<true, 3, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
     }
     if (tlist) return launch_wz<false, 3, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);

@@ -672,7 +672,34 @@ __global__ void __launch_bounds__(256, 3) k_p2q8(GridP g, MatP mp, const int *__
 // the 27 cells all of whose source buckets lie in the tile are stored and the other 98 are added with
 // global atomics into zeroed accumulators (neighbouring tiles contribute there).  k_p2q_finish then
 // normalises tau = (V tau) / V and reconstructs the stretch per slot (a4).
-constexpr int P2Q_CAP = 320;  // particles staged per pass (30 KB of fp32 records)
+// ---- bulk copy (TMA, cp.async.bulk) into shared memory completing on an mbarrier ----------------
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+constexpr int P2Q_CAP = 256;  // particles staged per pass, double-buffered (2 x 24 KB of fp32 records)
 template <int NM> struct P2QNV { static constexpr int V = 13 + 7 * NM; };  // m, mv 3, mG 9, per slot V + V tau 6
 template <class T, int NM>
 __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *__restrict__ coord,
@@ -683,11 +710,17 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
     constexpr int NV = P2QNV<NM>::V;
     extern __shared__ __align__(16) unsigned char p2q_smem[];
     T *acc = reinterpret_cast<T *>(p2q_smem);             // [125][NV]
-    T *R = acc + ((125 * NV + 3) & ~3);                   // [P2Q_CAP][REC]
+    T *Rb = acc + ((125 * NV + 3) & ~3);                  // [2][P2Q_CAP][REC]: the staged passes
     __shared__ int bs[65];
+    __shared__ __align__(8) uint64_t bar[2];
     const int t = blockIdx.x, tid = threadIdx.x;
     if (tid < 65) bs[tid] = bstart[t * 64 + tid];
     for (int i = tid; i < 125 * NV; i += blockDim.x) acc[i] = T(0);
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
     __syncthreads();
     const int p0 = bs[0], p1 = bs[64];
     DASSERT(p1 >= p0);
@@ -714,16 +747,21 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
             for (int a = 0; a < 6; a++) A2[h].Vt[k][a] = 0;
         }
     }
-    for (int c0 = p0; c0 < p1; c0 += P2Q_CAP) {
-        const int cn = min(P2Q_CAP, p1 - c0);
-        // stage records [c0, c0 + cn) with 16-byte loads
-        {
-            constexpr int PER = (int)(REC * sizeof(T) / 16);  // 16-byte vectors per record
-            const float4 *src = reinterpret_cast<const float4 *>(rec + (int64_t)c0 * REC);
-            float4 *dst = reinterpret_cast<float4 *>(R);
-            for (int i = tid; i < cn * PER; i += blockDim.x) dst[i] = __ldg(src + i);
-        }
-        __syncthreads();
+    // the records of pass k (particles [p0 + k CAP, ...)) arrive in buffer k & 1 by one bulk copy (TMA),
+    // issued a pass ahead so it overlaps the previous pass's arithmetic
+    auto issue = [&](int k) {
+        const int c0 = p0 + k * P2Q_CAP, cn = min(P2Q_CAP, p1 - c0);
+        const uint32_t bytes = (uint32_t)(cn * REC * sizeof(T));
+        mbar_expect_tx(&bar[k & 1], bytes);
+        bulk_g2s(Rb + (k & 1) * P2Q_CAP * REC, rec + (int64_t)c0 * REC, bytes, &bar[k & 1]);
+    };
+    const int npass = (p1 - p0 + P2Q_CAP - 1) / P2Q_CAP;
+    if (tid == 0) issue(0);
+    for (int k = 0; k < npass; k++) {
+        const int c0 = p0 + k * P2Q_CAP, cn = min(P2Q_CAP, p1 - c0);
+        if (tid == 0 && k + 1 < npass) issue(k + 1);  // buffer (k + 1) & 1 was released by the last barrier
+        mbar_wait(&bar[k & 1], (uint32_t)((k >> 1) & 1));
+        const T *R = Rb + (k & 1) * P2Q_CAP * REC;
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int pr = tid + 256 * h;
@@ -756,7 +794,7 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
                     }
             }
         }
-        __syncthreads();  // the staged records are consumed before the next pass overwrites them
+        __syncthreads();  // buffer k & 1 consumed before pass k + 2 refills it
     }
 #pragma unroll
     for (int h = 0; h < 2; h++) {
@@ -1373,11 +1411,11 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
         (const int *)ctx->t_cellof.p, (const T *)ctx->prec.p, (T *)ctx->q_m.p, (T *)ctx->q_mv.p,           \
         (T *)ctx->q_mG.p, (T *)ctx->q_slot.p
             if (nm <= 2) {
-                const size_t sm = (((size_t)125 * P2QNV<2>::V + 3) & ~(size_t)3) * s + (size_t)P2Q_CAP * REC * s;
+                const size_t sm = (((size_t)125 * P2QNV<2>::V + 3) & ~(size_t)3) * s + (size_t)2 * P2Q_CAP * REC * s;
                 MPL_CUDA(cudaFuncSetAttribute(k_p2q_tile<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
                 k_p2q_tile<T, 2><<<T_, 256, sm, st>>>(P2QT_ARGS);
             } else {
-                const size_t sm = (((size_t)125 * P2QNV<MPL_MAXMAT>::V + 3) & ~(size_t)3) * s + (size_t)P2Q_CAP * REC * s;
+                const size_t sm = (((size_t)125 * P2QNV<MPL_MAXMAT>::V + 3) & ~(size_t)3) * s + (size_t)2 * P2Q_CAP * REC * s;
                 MPL_CUDA(cudaFuncSetAttribute(k_p2q_tile<T, MPL_MAXMAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)sm));
                 k_p2q_tile<T, MPL_MAXMAT><<<T_, 256, sm, st>>>(P2QT_ARGS);

@@ -43,7 +43,7 @@ def measure(name: str) -> dict:
     t_g2p = time.perf_counter() - t0
     ctx.close()
     nbytes = c.n_cells * 45 * 4 + c.n_nodes * 7 * 4
-    return {"config": name, "p2q": os.environ.get("MPL_P2Q", "gather"), "particles": sc.n_particles, "quadrature_points": c.n_cells, "active_nodes": c.n_nodes,
+    return {"config": name, "p2q": os.environ.get("MPL_P2Q", "scatter"), "particles": sc.n_particles, "quadrature_points": c.n_cells, "active_nodes": c.n_nodes,
             "resample_ms": round(t_res * 1e3, 3), "g2p_ms": round(t_g2p * 1e3, 3),
             "linearize_ms": round(t_lin * 1e3, 3), "hvp_us": round(hvp_ms * 1e3, 2),
             "hvp_alg_GBps": round(nbytes / (hvp_ms * 1e-3) / 1e9, 1),

@@ -17,5 +17,5 @@ ctx.resample(sc.dt)
 ctx.set_particles(sc.x, sc.v, sc.F, sc.G, sc.vol, sc.mat)
 t0 = time.perf_counter()
 ctx.resample(sc.dt)
-print(f"{name}: resample {1e3 * (time.perf_counter() - t0):.3f} ms ({os.environ.get('MPL_P2Q', 'gather')})")
+print(f"{name}: resample {1e3 * (time.perf_counter() - t0):.3f} ms ({os.environ.get("MPL_P2Q", "scatter")})")
 ctx.close()

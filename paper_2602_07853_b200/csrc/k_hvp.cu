@@ -112,9 +112,11 @@ __host__ __device__ constexpr int krow(int e) {
 __host__ __device__ constexpr int kcol(int e) { return krow(e) + (e - kofs(krow(e))); }
 
 // compressed-tangent apply for the two cells of a lane at once (KC): every value a float2 (cell A, cell B),
-// so each operation is one paired fp32 instruction (FFMA2 / FMUL2 / FADD2 on sm_100).  k holds the 28
-// interleaved pairs (A_e, B_e) of E = S - I (6), q_U (4), q_V (4), c psi_ij (6), c (a, b) x 3 pairs (6), pad;
-// d = dG (raw nodal sums); P = c (C : (dG S)) S with C in the SVD frame.
+// so each operation is one paired fp32 instruction (FFMA2 / FMUL2 / FADD2 on sm_100).  k holds the 24
+// interleaved pairs (A_e, B_e) of q_U = (x, y, z) (3; w = sqrt(1 - x^2 - y^2 - z^2) >= 1/2), W = S V (9,
+// row-major), c psi_ij (6), c (a, b) x 3 pairs (6); d = dG (raw nodal sums);
+// P = c U (C : (U^T dG W)) W^T = c (C_F : (dG S)) S with C in the SVD frame (S symmetric, so V^T S = W^T;
+// DESIGN §4).
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
@@ -134,60 +136,55 @@ __device__ __forceinline__ void quat_rot2(float2 w, float2 x, float2 y, float2 z
     R[7] = mul2(two, add2(yz, wx));
     R[8] = sub2(one, mul2(two, add2(xx, yy)));
 }
+constexpr int KC_CHUNKS = KC_REALS / 2;  // 12 chunks of (A_e, B_e, A_e+1, B_e+1) per pair slot
 __device__ __forceinline__ void kc_apply2(const float *k, const float2 d[9], float2 P[9]) {
     auto el = [&](int e) { return f2(k[4 * (e >> 1) + 2 * (e & 1)], k[4 * (e >> 1) + 2 * (e & 1) + 1]); };
-    const float2 Em[9] = {el(0), el(3), el(5), el(3), el(1), el(4), el(5), el(4), el(2)};
-    float2 X[9];  // dG S = dG + dG E
-#pragma unroll
-    for (int a = 0; a < 3; a++)
-#pragma unroll
-        for (int b = 0; b < 3; b++) {
-            float2 v = d[3 * a + b];
-#pragma unroll
-            for (int c = 0; c < 3; c++) v = fma2(d[3 * a + c], Em[3 * c + b], v);
-            X[3 * a + b] = v;
-        }
-    float2 RU[9], RV[9];
-    quat_rot2(el(6), el(7), el(8), el(9), RU);
-    quat_rot2(el(10), el(11), el(12), el(13), RV);
-    float2 T1[9], Xh[9];  // Xh = RU^T X RV
+    float2 RU[9];
+    {
+        const float2 x = el(0), y = el(1), z = el(2);
+        const float2 s = fma2(x, x, fma2(y, y, mul2(z, z)));
+        const float2 t = sub2(f2(1.f, 1.f), s);  // = w^2 >= 1/4 (an absent partner: 1)
+        const float2 w = mul2(t, f2(rsqrtf(t.x), rsqrtf(t.y)));
+        quat_rot2(w, x, y, z, RU);
+    }
+    float2 T1[9], Xh[9];  // Xh = RU^T dG W
 #pragma unroll
     for (int i = 0; i < 3; i++)
 #pragma unroll
         for (int j = 0; j < 3; j++) {
-            float2 v = mul2(RU[i], X[j]);
-            v = fma2(RU[3 + i], X[3 + j], v);
-            T1[3 * i + j] = fma2(RU[6 + i], X[6 + j], v);
+            float2 v = mul2(RU[i], d[j]);
+            v = fma2(RU[3 + i], d[3 + j], v);
+            T1[3 * i + j] = fma2(RU[6 + i], d[6 + j], v);
         }
 #pragma unroll
     for (int i = 0; i < 3; i++)
 #pragma unroll
         for (int j = 0; j < 3; j++) {
-            float2 v = mul2(T1[3 * i], RV[j]);
-            v = fma2(T1[3 * i + 1], RV[3 + j], v);
-            Xh[3 * i + j] = fma2(T1[3 * i + 2], RV[6 + j], v);
+            float2 v = mul2(T1[3 * i], el(3 + j));
+            v = fma2(T1[3 * i + 1], el(6 + j), v);
+            Xh[3 * i + j] = fma2(T1[3 * i + 2], el(9 + j), v);
         }
     float2 Yh[9];
-    const float2 D00 = el(14), D11 = el(15), D22 = el(16), D01 = el(17), D12 = el(18), D02 = el(19);
+    const float2 D00 = el(12), D11 = el(13), D22 = el(14), D01 = el(15), D12 = el(16), D02 = el(17);
     Yh[0] = fma2(D00, Xh[0], fma2(D01, Xh[4], mul2(D02, Xh[8])));
     Yh[4] = fma2(D01, Xh[0], fma2(D11, Xh[4], mul2(D12, Xh[8])));
     Yh[8] = fma2(D02, Xh[0], fma2(D12, Xh[4], mul2(D22, Xh[8])));
     {
-        const float2 a = el(20), b = el(21);  // pair (0, 1)
+        const float2 a = el(18), b = el(19);  // pair (0, 1)
         Yh[1] = fma2(a, Xh[1], mul2(b, Xh[3]));
         Yh[3] = fma2(b, Xh[1], mul2(a, Xh[3]));
     }
     {
-        const float2 a = el(22), b = el(23);  // pair (0, 2)
+        const float2 a = el(20), b = el(21);  // pair (0, 2)
         Yh[2] = fma2(a, Xh[2], mul2(b, Xh[6]));
         Yh[6] = fma2(b, Xh[2], mul2(a, Xh[6]));
     }
     {
-        const float2 a = el(24), b = el(25);  // pair (1, 2)
+        const float2 a = el(22), b = el(23);  // pair (1, 2)
         Yh[5] = fma2(a, Xh[5], mul2(b, Xh[7]));
         Yh[7] = fma2(b, Xh[5], mul2(a, Xh[7]));
     }
-    float2 T2[9], Y[9];  // Y = RU Yh RV^T
+    float2 T2[9];  // P = RU Yh W^T
 #pragma unroll
     for (int i = 0; i < 3; i++)
 #pragma unroll
@@ -200,18 +197,9 @@ __device__ __forceinline__ void kc_apply2(const float *k, const float2 d[9], flo
     for (int i = 0; i < 3; i++)
 #pragma unroll
         for (int j = 0; j < 3; j++) {
-            float2 v = mul2(T2[3 * i], RV[3 * j]);
-            v = fma2(T2[3 * i + 1], RV[3 * j + 1], v);
-            Y[3 * i + j] = fma2(T2[3 * i + 2], RV[3 * j + 2], v);
-        }
-#pragma unroll
-    for (int a = 0; a < 3; a++)  // P = Y S = Y + Y E
-#pragma unroll
-        for (int b = 0; b < 3; b++) {
-            float2 v = Y[3 * a + b];
-#pragma unroll
-            for (int c = 0; c < 3; c++) v = fma2(Y[3 * a + c], Em[3 * c + b], v);
-            P[3 * a + b] = v;
+            float2 v = mul2(T2[3 * i], el(3 + 3 * j));
+            v = fma2(T2[3 * i + 1], el(4 + 3 * j), v);
+            P[3 * i + j] = fma2(T2[3 * i + 2], el(5 + 3 * j), v);
         }
 }
 
@@ -269,7 +257,7 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
         const unsigned word = lA < 32 ? clo : chi;
         q.pA = q.has ? (int)((word >> (lA & 31)) & 1u) : 0;
         q.pB = q.has ? (int)((word >> ((lA + 1) & 31)) & 1u) : 0;
-        if (KC) {  // compressed: one pair slot per lane holding a cell, 14 interleaved chunks
+        if (KC) {  // compressed: one pair slot per lane holding a cell, KC_CHUNKS interleaved chunks
             const unsigned pm = __ballot_sync(FULL, q.pA | q.pB);
             q.sb = 16u * (unsigned)__popc(pm);
             q.ka = K + ks + 4 * __popc(pm & lt);
@@ -291,9 +279,9 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
     // chunk c < 11 of slot s at 4 (c n + s), element 44 at 44 n + s (k_off): chunk c at (byte)
     // ka + c * 16 n, one IMAD.WIDE per load.  Chunk c of cell X (off 0 = A, 45 = B) -> k
     auto kload = [&](const TileK &q, int off, int c) {
-        if (KC) {  // off 0: chunks 0..6, off 45: chunks 7..13 (c < 7; the 12 calls per cell map onto 14 chunks)
+        if (KC) {  // off 0: chunks 0..6, off 45: chunks 7..11 (the 12 calls per cell map onto 12 chunks)
             const int cc = (off ? 7 : 0) + c;
-            if (c >= 7 || !(q.pA | q.pB)) return;
+            if (c >= 7 || cc >= KC_CHUNKS || !(q.pA | q.pB)) return;
             const float4 v = ldg_stream(reinterpret_cast<const float *>(reinterpret_cast<const char *>(q.ka) +
                                                                         (uint64_t)q.sb * (uint64_t)cc), pol);
             k[4 * cc] = v.x; k[4 * cc + 1] = v.y; k[4 * cc + 2] = v.z; k[4 * cc + 3] = v.w;
@@ -844,15 +832,16 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
     if (tlist && (sizeof(T) == 8 || hvp_variant() == 1)) return MPL_ERR_UNSUPPORTED;  // tile lists: k_hvp_wz only
     if (sizeof(T) == 8) return launch_wh<T, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);  // 45 doubles per lane
     if (hvp_variant() == 1) return launch_wh<T, 5>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
-    if (ctx->kc_now) {  // compressed tangent; MPL_KC_MINB: CTAs per SM requested from ptxas (3: 168 registers)
+    if (ctx->kc_now) {  // compressed tangent; MPL_KC_MINB: CTAs per SM requested from ptxas (4: 128 registers,
+                        // 44 B spilled; 3: 148 registers — cfg4 in-step 84.1 vs 85.0 us)
         static int minb = -1;
         if (minb < 0) {
             const char *e = getenv("MPL_KC_MINB");
-            minb = e ? atoi(e) : 3;
+            minb = e ? atoi(e) : 4;
         }
-        if (tlist) return launch_wz<true, 3, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
-        if (minb == 4) return launch_wz<true, 4, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
-        return launch_wz<true, 3, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
+        if (tlist) return launch_wz<true, 4, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
+        if (minb == 3) return launch_wz<true, 3, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
+        return launch_wz<true, 4, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
     }
     if (tlist) return launch_wz<false, 3, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
     return launch_wz<false, 3, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);

@@ -444,7 +444,7 @@ __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, cons
     if ((l & 31) == 0) part[l >> 5] = lo;
     __syncthreads();
     // k_hvp_wz lanes holding a cell (kz_key(l) & 31 = the lane of cell l): the pair slots of the
-    // compressed tangent layout, 56 reals each
+    // compressed tangent layout, 2 KC_REALS reals each
     if (act) atomicOr(&pairs, 1u << (kz_key(l) & 31));
     __syncthreads();
     if (l == 0) {
@@ -453,11 +453,11 @@ __global__ void k_cell_mask(GridP g, int T_, const int *__restrict__ coord, cons
         int c = __popcll(m);
         ccount[t] = (c + 3) & ~3;
         ncell[t] = c;
-        // tangent only on owned tiles: room for the full (45 c reals) or the compressed (56 per pair
-        // slot) layout, rounded up to 4
+        // tangent only on owned tiles: room for the full (45 c reals) or the compressed (2 KC_REALS per
+        // pair slot) layout, rounded up to 4
         const int np = __popc(pairs);
         kcnt[t] = hascells[t] ? (45 * c + 3) & ~3 : 0;  // the 45-number layout
-        kcnt2[t] = hascells[t] ? 56 * np : 0;           // the compressed layout (its own offsets)
+        kcnt2[t] = hascells[t] ? 2 * KC_REALS * np : 0;  // the compressed layout (its own offsets)
         if (c && hascells[t]) atomicAdd(ncells, (unsigned long long)c);
     }
 }

@@ -144,7 +144,7 @@ __device__ __forceinline__ void rot_quat(const T R[9], T q[4]) {
 // compiled out: a third of the code, and ncu showed 20 % instruction-fetch stalls on the general kernel)
 // LMINB > 1: 64-thread launch with LMINB CTAs per SM requested from ptxas (the Hencky-only full
 // linearisation at 12: 80 registers, small spills, 24 warps / SM: cfg4 3.89 -> 3.62 ms per step; 16: 3.84)
-template <class T, int MODE, bool HONLY = false, int LMINB = 1, bool PSD = false>
+template <class T, int MODE, bool HONLY = false, int LMINB = 1, bool PSD = false, bool KCT = false>
 __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP g, MatP mp, double dt_, const int *__restrict__ nplus,
                                                    const int *__restrict__ cstart, const uint8_t *__restrict__ clocal,
                                                    const int *__restrict__ hascells, const vec4<T> *__restrict__ v,
@@ -155,10 +155,12 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
                                                    T *__restrict__ qsp, DevScalars *sc, int kz, int kc) {
     constexpr int KS = (MODE == LIN_FULL) ? 64 * 45 : 1;
     // compressed tangent (kc = 1: fp32, every slot elastic StVK-Hencky, one occupied slot per cell):
-    // 28 reals per cell, written in k_hvp_wz's interleaved pair layout
+    // KC_REALS (24) reals per cell, written in k_hvp_wz's interleaved pair layout
     // with PSD only when every base S is I (the resample counts the other cells): then K = c C(A) exactly, and
     // its per-cell projection is the blockwise clamping of C in the SVD frame
-    constexpr bool KCOK = (MODE == LIN_FULL) && HONLY && sizeof(T) == 4;
+    // (a template instance per format: each carries only its own tangent code, see DESIGN §5 linearize)
+    constexpr bool KC = KCT && (MODE == LIN_FULL) && HONLY && sizeof(T) == 4;
+    DASSERT(kc == (KC ? 1 : 0));
     __shared__ unsigned int pm_s, cm_s[2];  // KC: k_hvp_wz lanes holding a cell; the tile's cell mask
     __shared__ vec4<T> vh[125];
     __shared__ T Pg[64 * 9];
@@ -185,24 +187,24 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
         int l = clocal[cs + tid];
         if (l != 0xFF) {
             cslot[l] = tid;
-            if (KCOK && kc) {
+            if (KC) {
                 atomicOr(&pm_s, 1u << (kz_key(l) & 31));
                 atomicOr(&cm_s[l >> 5], 1u << (l & 31));
             }
         }
     }
-    if (KCOK && kc) __syncthreads();  // pair slots known before the cell phase writes the compressed tangent
+    if (KC) __syncthreads();  // pair slots known before the cell phase writes the compressed tangent
     // KC: element e of this cell at Kout[kc_base + (e / 2) * 4 np + 2 (e & 1)] (pair layout)
     int64_t kc_base = 0;
     int kc_np = 0;
-    if (KCOK && kc && has && tid < nc && clocal[cs + tid] != 0xFF) {
+    if (KC && has && tid < nc && clocal[cs + tid] != 0xFF) {
         const int l = clocal[cs + tid], lane = kz_key(l) & 31;
         kc_np = __popc(pm_s);
         kc_base = kstart[t] + (int64_t)__popc(pm_s & ((1u << lane) - 1u)) * 4 + (l & 1);
-        DASSERT(kstart[t] + 56 * kc_np <= kstart[t + 1]);
+        DASSERT(kstart[t] + 2 * KC_REALS * kc_np <= kstart[t + 1]);
         // the lane's other cell (l ^ 1: the other z of the pair) absent: its half of the pair slot is zero
         if (!((cm_s[(l ^ 1) >> 5] >> ((l ^ 1) & 31)) & 1u))
-            for (int e = 0; e < 28; e++) Kout[kc_base + (int64_t)(e >> 1) * 4 * kc_np + 2 * (e & 1) + (1 - 2 * (l & 1))] = T(0);
+            for (int e = 0; e < KC_REALS; e++) Kout[kc_base + (int64_t)(e >> 1) * 4 * kc_np + 2 * (e & 1) + (1 - 2 * (l & 1))] = T(0);
     }
     bool kc_done = false;
     double e_loc = 0.0;
@@ -438,7 +440,7 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
                     for (int i = 0; i < 3; i++)
 #pragma unroll
                         for (int jj = 0; jj < 3; jj++) L[3 * i + jj] = dlog(lam3[i], lam3[jj]);
-                    if (KCOK && kc) {
+                    if (KC) {
                         // compressed tangent of this slot: F = U Sigma V^T (U = eigenvectors of b = F F^T,
                         // sigma_i^2 = beta_i), d^2 psi / dF^2 in the SVD frame = a 3x3 block on the diagonal
                         // entries (psi_ij) and 2x2 blocks [[a, b], [b, a]] on (X_ij, X_ji) (Irving, Teran &
@@ -462,35 +464,57 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
                             for (int a = 0; a < 3; a++)
                                 Vm[3 * a + i] = (F[a] * U[i] + F[3 + a] * U[3 + i] + F[6 + a] * U[6 + i]) * is;
                         }
+                        // U D, V D with D = diag(+-1), det D = 1, leave F = U Sigma V^T and C unchanged (the pair
+                        // blocks see both X_ij, X_ji scaled by D_i D_j): flip the column pair that makes U's
+                        // largest quaternion component w (q (x) i, j, k move x, y, z there), so |w| >= 1/2 and
+                        // q_U is stored as (x, y, z) with w = sqrt(1 - x^2 - y^2 - z^2)
+                        T qU[4];
+                        {
+                            rot_quat(U, qU);
+                            const T aw = fabs(qU[0]), ax = fabs(qU[1]), ay = fabs(qU[2]), az = fabs(qU[3]);
+                            int m = 0;
+                            T best = aw;
+                            if (ax > best) { m = 1; best = ax; }
+                            if (ay > best) { m = 2; best = ay; }
+                            if (az > best) m = 3;
+                            if (m) {
+                                const T d0 = m == 1 ? T(1) : T(-1), d1 = m == 2 ? T(1) : T(-1), d2 = m == 3 ? T(1) : T(-1);
+#pragma unroll
+                                for (int a = 0; a < 3; a++) {
+                                    U[3 * a] *= d0; U[3 * a + 1] *= d1; U[3 * a + 2] *= d2;
+                                    Vm[3 * a] *= d0; Vm[3 * a + 1] *= d1; Vm[3 * a + 2] *= d2;
+                                }
+                                rot_quat(U, qU);
+                            }
+                            if (qU[0] < T(0)) { qU[1] = -qU[1]; qU[2] = -qU[2]; qU[3] = -qU[3]; }
+                        }
                         const T c = sV * T(1.0 / 16.0) * T(g.inv_dx * g.inv_dx) * dt;  // kscale dt
-                        T kc_[28];
-                        // E (xx yy zz xy yz xz)
-                        kc_[0] = E[0]; kc_[1] = E[4]; kc_[2] = E[8]; kc_[3] = E[1]; kc_[4] = E[5]; kc_[5] = E[2];
-                        rot_quat(U, kc_ + 6);
-                        rot_quat(Vm, kc_ + 10);
-                        T psi[9];
+                        // c psi (00 11 22 01 12 02) and c (a, b) of the pairs (0,1) (0,2) (1,2)
+                        T ps[6], ab[6];
+                        {
+                            T psi[9];
 #pragma unroll
-                        for (int i = 0; i < 3; i++)
+                            for (int i = 0; i < 3; i++)
 #pragma unroll
-                            for (int jj = 0; jj < 3; jj++)
-                                psi[3 * i + jj] = ((i == jj ? T(2) * mu : T(0)) + lamL) / (sg[i] * sg[jj]) -
-                                                  (i == jj ? tp[i] / (sg[i] * sg[i]) : T(0));
-                        kc_[14] = c * psi[0]; kc_[15] = c * psi[4]; kc_[16] = c * psi[8];
-                        kc_[17] = c * psi[1]; kc_[18] = c * psi[5]; kc_[19] = c * psi[2];
+                                for (int jj = 0; jj < 3; jj++)
+                                    psi[3 * i + jj] = ((i == jj ? T(2) * mu : T(0)) + lamL) / (sg[i] * sg[jj]) -
+                                                      (i == jj ? tp[i] / (sg[i] * sg[i]) : T(0));
+                            ps[0] = c * psi[0]; ps[1] = c * psi[4]; ps[2] = c * psi[8];
+                            ps[3] = c * psi[1]; ps[4] = c * psi[5]; ps[5] = c * psi[2];
+                        }
                         const int pi_[3] = {0, 0, 1}, pj_[3] = {1, 2, 2};
 #pragma unroll
                         for (int pp = 0; pp < 3; pp++) {
                             const int i = pi_[pp], jj = pj_[pp];
                             const T a_ = mu * L[3 * i + jj];
                             const T b_ = ((T(1) + lam3[jj]) * a_ - tp[jj]) / (sg[i] * sg[jj]);
-                            kc_[20 + 2 * pp] = c * a_;
-                            kc_[21 + 2 * pp] = c * b_;
+                            ab[2 * pp] = c * a_;
+                            ab[2 * pp + 1] = c * b_;
                         }
-                        kc_[26] = kc_[27] = T(0);
                         if (PSD) {
                             // S = I: the per-cell PSD projection of K = c C is C's blockwise clamping (amb-6b):
                             // the 3x3 block by its eigenvalues, each [[a, b], [b, a]] by a + b and a - b
-                            T Dm[9] = {kc_[14], kc_[17], kc_[19], kc_[17], kc_[15], kc_[18], kc_[19], kc_[18], kc_[16]};
+                            T Dm[9] = {ps[0], ps[3], ps[5], ps[3], ps[1], ps[4], ps[5], ps[4], ps[2]};
                             T dw[3], DQ[9];
                             sym_eig3(Dm, dw, DQ);
 #pragma unroll
@@ -499,59 +523,68 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
                                 return DQ[3 * r] * DQ[3 * cc] * dw[0] + DQ[3 * r + 1] * DQ[3 * cc + 1] * dw[1] +
                                        DQ[3 * r + 2] * DQ[3 * cc + 2] * dw[2];
                             };
-                            kc_[14] = dent(0, 0); kc_[15] = dent(1, 1); kc_[16] = dent(2, 2);
-                            kc_[17] = dent(0, 1); kc_[18] = dent(1, 2); kc_[19] = dent(0, 2);
+                            ps[0] = dent(0, 0); ps[1] = dent(1, 1); ps[2] = dent(2, 2);
+                            ps[3] = dent(0, 1); ps[4] = dent(1, 2); ps[5] = dent(0, 2);
 #pragma unroll
                             for (int pp = 0; pp < 3; pp++) {
-                                const T a_ = kc_[20 + 2 * pp], b_ = kc_[21 + 2 * pp];
+                                const T a_ = ab[2 * pp], b_ = ab[2 * pp + 1];
                                 const T lp = a_ + b_ > T(0) ? a_ + b_ : T(0), lm = a_ - b_ > T(0) ? a_ - b_ : T(0);
-                                kc_[20 + 2 * pp] = T(0.5) * (lp + lm);
-                                kc_[21 + 2 * pp] = T(0.5) * (lp - lm);
-                            }
-                            // K+ (45 numbers, for the Jacobi diagonal): column (e, f) = U (C+ : U^T E_ef V) V^T
-                            T *Kr = Ks + j * 45;
-                            const T Dp[9] = {kc_[14], kc_[17], kc_[19], kc_[17], kc_[15], kc_[18], kc_[19], kc_[18], kc_[16]};
-#pragma unroll
-                            for (int ef = 0; ef < 9; ef++) {
-                                const int e_ = ef / 3, f_ = ef % 3;
-                                T Xh[9], Yh[9];
-#pragma unroll
-                                for (int i = 0; i < 3; i++)
-#pragma unroll
-                                    for (int jj = 0; jj < 3; jj++) Xh[3 * i + jj] = U[3 * e_ + i] * Vm[3 * f_ + jj];
-#pragma unroll
-                                for (int i = 0; i < 3; i++)
-                                    Yh[4 * i] = Dp[3 * i] * Xh[0] + Dp[3 * i + 1] * Xh[4] + Dp[3 * i + 2] * Xh[8];
-                                const int pi2[3] = {0, 0, 1}, pj2[3] = {1, 2, 2};
-#pragma unroll
-                                for (int pp = 0; pp < 3; pp++) {
-                                    const int i = pi2[pp], jj = pj2[pp];
-                                    const T a_ = kc_[20 + 2 * pp], b_ = kc_[21 + 2 * pp];
-                                    Yh[3 * i + jj] = a_ * Xh[3 * i + jj] + b_ * Xh[3 * jj + i];
-                                    Yh[3 * jj + i] = b_ * Xh[3 * i + jj] + a_ * Xh[3 * jj + i];
-                                }
-#pragma unroll
-                                for (int a = 0; a < 3; a++)
-#pragma unroll
-                                    for (int b = 0; b < 3; b++) {
-                                        T y = T(0);
-#pragma unroll
-                                        for (int i = 0; i < 3; i++)
-#pragma unroll
-                                            for (int jj = 0; jj < 3; jj++) y += U[3 * a + i] * Yh[3 * i + jj] * Vm[3 * b + jj];
-                                        const int r = 3 * a + b;
-                                        if (r <= ef) Kr[kidx(r, ef)] += (r == ef ? y : T(0.5) * y);
-                                        if (r > ef) Kr[kidx(ef, r)] += T(0.5) * y;
-                                    }
+                                ab[2 * pp] = T(0.5) * (lp + lm);
+                                ab[2 * pp + 1] = T(0.5) * (lp - lm);
                             }
                         }
+                        // W = S V (S symmetric: the elastic base), so K : dG = c U (C : (U^T dG W)) W^T
+                        T Wm[9];
 #pragma unroll
-                        for (int e = 0; e < 28; e++) Kout[kc_base + (int64_t)(e >> 1) * 4 * kc_np + 2 * (e & 1)] = kc_[e];
+                        for (int a = 0; a < 3; a++)
+#pragma unroll
+                            for (int jj = 0; jj < 3; jj++)
+                                Wm[3 * a + jj] = S[3 * a] * Vm[jj] + S[3 * a + 1] * Vm[3 + jj] + S[3 * a + 2] * Vm[6 + jj];
+                        // the Jacobi diagonal (node phase) reads only K's blocks K[(a,b),(a,e)]:
+                        // K[(a,b),(a,e)] = c X_b : C : X_e with X_b = U^T e_a e_b^T W = u_a w_b^T, u_a = U[a][:],
+                        // w_b = W[b][:]
+                        T *Kr = Ks + j * 45;
+#pragma unroll
+                        for (int a = 0; a < 3; a++) {
+                            T X[3][9];
+#pragma unroll
+                            for (int b = 0; b < 3; b++)
+#pragma unroll
+                                for (int i = 0; i < 3; i++)
+#pragma unroll
+                                    for (int jj = 0; jj < 3; jj++) X[b][3 * i + jj] = U[3 * a + i] * Wm[3 * b + jj];
+#pragma unroll
+                            for (int b = 0; b < 3; b++)
+#pragma unroll
+                                for (int e = b; e < 3; e++) {
+                                    const T *x = X[b], *y = X[e];
+                                    T val = ps[0] * x[0] * y[0] + ps[1] * x[4] * y[4] + ps[2] * x[8] * y[8] +
+                                            ps[3] * (x[0] * y[4] + x[4] * y[0]) + ps[4] * (x[4] * y[8] + x[8] * y[4]) +
+                                            ps[5] * (x[0] * y[8] + x[8] * y[0]);
+#pragma unroll
+                                    for (int pp = 0; pp < 3; pp++) {
+                                        const int ij = 3 * pi_[pp] + pj_[pp], ji = 3 * pj_[pp] + pi_[pp];
+                                        val += ab[2 * pp] * (x[ij] * y[ij] + x[ji] * y[ji]) +
+                                               ab[2 * pp + 1] * (x[ij] * y[ji] + x[ji] * y[ij]);
+                                    }
+                                    Kr[kidx(3 * a + b, 3 * a + e)] += val;
+                                }
+                        }
+                        // the 24 reals: q_U's (x, y, z) (3), W (9, row-major), c psi (6), c (a, b) x 3 (6)
+                        // (k_hvp_wz kc_apply2)
+                        T kc_[KC_REALS];
+                        kc_[0] = qU[1]; kc_[1] = qU[2]; kc_[2] = qU[3];
+#pragma unroll
+                        for (int e = 0; e < 9; e++) kc_[3 + e] = Wm[e];
+#pragma unroll
+                        for (int e = 0; e < 6; e++) { kc_[12 + e] = ps[e]; kc_[18 + e] = ab[e]; }
+#pragma unroll
+                        for (int e = 0; e < KC_REALS; e++) Kout[kc_base + (int64_t)(e >> 1) * 4 * kc_np + 2 * (e & 1)] = kc_[e];
                         kc_done = true;
                     }
                     const T kscale = sV * T(1.0 / 16.0) * T(g.inv_dx * g.inv_dx);
                     T *Kr = Ks + j * 45;
-                    if (!(KCOK && PSD && kc))  // (KC + PSD: K+ assembled above from the projected blocks)
+                    if (!KC)  // (KC: the diagonal blocks were assembled above from the compressed form)
 #pragma unroll
                     for (int a = 0; a < 3; a++)
 #pragma unroll
@@ -603,13 +636,13 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
 #pragma unroll
                 for (int a = 0; a < 9; a++) Pg[l * 9 + a] = Pc[a] * q;  // fold grad w scale
             }
-            if (KCOK && kc && !kc_done)  // no occupied slot (a zero-mass stencil cell, amb-10): zero tangent
-                for (int e = 0; e < 28; e++) Kout[kc_base + (int64_t)(e >> 1) * 4 * kc_np + 2 * (e & 1)] = T(0);
+            if (KC && !kc_done)  // no occupied slot (a zero-mass stencil cell, amb-10): zero tangent
+                for (int e = 0; e < KC_REALS; e++) Kout[kc_base + (int64_t)(e >> 1) * 4 * kc_np + 2 * (e & 1)] = T(0);
         }
     }
     __syncthreads();
     if (PSD && MODE == LIN_FULL && has) {  // per-cell PSD projection before the K write and the diagonal
-        if (!(KCOK && kc) && tid < nc && clocal[cs + tid] != 0xFF)
+        if (!(KC) && tid < nc && clocal[cs + tid] != 0xFF)
             psd_project45<T>(Ks + tid * 45);  // fp64: spills, acceptable
         __syncthreads();
     }
@@ -628,7 +661,7 @@ __global__ void __launch_bounds__(LMINB > 1 ? 64 : 128, LMINB) k_linearize(GridP
             zslot[tid] = sl;
         }
         __syncthreads();
-        if (KCOK && kc) {
+        if (KC) {
             // written by the cell phase (pair layout)
         } else {
             for (int i = tid; i < n * 45; i += blockDim.x) Kout[k_off<T>(base, n, zslot[i / 45], i % 45)] = Ks[i];
@@ -1027,8 +1060,8 @@ __global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, int64_t S, const
 // instruction is contiguous across the warp (the group mapping above writes p / Hp at a 64-byte lane
 // stride).  Full chunks run without per-node bounds checks.
 constexpr int PCG_E = 4;  // nodes per lane per chunk (2 with 4 CTAs per SM measured slower: cfg4 step 65.2 vs 59.1 ms)
-template <class T, int E = PCG_E>
-__global__ void __launch_bounds__(256, 2) k_pcg_update1w(int64_t n, int64_t S, const int *__restrict__ list, int j,
+template <class T, int E = PCG_E, int MB = 2>
+__global__ void __launch_bounds__(256, MB) k_pcg_update1w(int64_t n, int64_t S, const int *__restrict__ list, int j,
                                                          double thr, const T *__restrict__ invD,
                                                          const vec4<T> *__restrict__ p, vec4<T> *__restrict__ Hp,
                                                          T *__restrict__ x, T *__restrict__ r,
@@ -1097,8 +1130,8 @@ __global__ void __launch_bounds__(256, 2) k_pcg_update1w(int64_t n, int64_t S, c
     block_add((double)rr, slot[j + 1].rr);
 }
 
-template <class T, int E = PCG_E>
-__global__ void __launch_bounds__(256, 2) k_pcg_update2w(int64_t n, int64_t S, const int *__restrict__ list, int j,
+template <class T, int E = PCG_E, int MB = 2>
+__global__ void __launch_bounds__(256, MB) k_pcg_update2w(int64_t n, int64_t S, const int *__restrict__ list, int j,
                                                          double thr, const T *__restrict__ invD,
                                                          const T *__restrict__ r, vec4<T> *__restrict__ p,
                                                          T *__restrict__ x, const CGSlot *slot, const DevScalars *sc) {
@@ -1413,12 +1446,15 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
         if (mode == LIN_FULL) ctx->kc_now = kc;
         if (mode == LIN_FULL && ctx->psd_now) {  // per-cell PSD projection of K
             // launch bounds (128, 1): the register-resident Jacobi (126 live reals) needs the registers
-            if (honly) k_linearize<T, LIN_FULL, true, 1, true><<<T_, 64, 0, st>>>(LIN_ARGS);
+            if (honly && kc) k_linearize<T, LIN_FULL, true, 1, true, true><<<T_, 64, 0, st>>>(LIN_ARGS);
+            else if (honly) k_linearize<T, LIN_FULL, true, 1, true><<<T_, 64, 0, st>>>(LIN_ARGS);
             else k_linearize<T, LIN_FULL, false, 1, true><<<T_, 64, 0, st>>>(LIN_ARGS);
         } else if (honly) {
             if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY, true><<<T_, lt, 0, st>>>(LIN_ARGS);
             else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD, true><<<T_, lt, 0, st>>>(LIN_ARGS);
+            else if (lt == 64 && kc) k_linearize<T, LIN_FULL, true, 12, false, true><<<T_, lt, 0, st>>>(LIN_ARGS);
             else if (lt == 64) k_linearize<T, LIN_FULL, true, 12><<<T_, lt, 0, st>>>(LIN_ARGS);
+            else if (kc) k_linearize<T, LIN_FULL, true, 1, false, true><<<T_, lt, 0, st>>>(LIN_ARGS);
             else k_linearize<T, LIN_FULL, true><<<T_, lt, 0, st>>>(LIN_ARGS);
         } else {
             if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY><<<T_, lt, 0, st>>>(LIN_ARGS);
@@ -1528,6 +1564,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     const char *pme = getenv("MPL_PCG_MAP");
     // warp-interleaved update kernels (fp32 default; the fp64 instances spill, MPL_PCG_MAP=group / warp)
     const bool pcg_warp_map = pme ? pme[0] == 'w' : sizeof(T) == 4;
+    const char *pmb = getenv("MPL_PCG_MINB");  // CTAs of 256 per SM requested from ptxas (2: <= 128 registers)
+    const int pcg_minb = pmb ? atoi(pmb) : 2;
     const unsigned VG = vgrid(NT);
     const unsigned VA = vgrid(NA);
     const unsigned VA1 = nblk(NA > 0 ? NA : 1, 256);
@@ -1749,7 +1787,13 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     if (timed) sampled.push_back({nl, jj});
                     nl++;
                     if (vec_events) cudaEventRecord(vev[nl - 1][0], st);
-                    if (pcg_warp_map)
+                    if (pcg_warp_map && pcg_minb == 3)
+                        MPL_CUDA(launch_pdl(k_pcg_update1w<T, PCG_E, 3>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p,
+                                            Hp, x, r, own_w, slots, sc));
+                    else if (pcg_warp_map && pcg_minb == 4)
+                        MPL_CUDA(launch_pdl(k_pcg_update1w<T, PCG_E, 4>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p,
+                                            Hp, x, r, own_w, slots, sc));
+                    else if (pcg_warp_map)
                         MPL_CUDA(launch_pdl(k_pcg_update1w<T>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p, Hp, x,
                                             r, own_w, slots, sc));
                     else
@@ -1758,7 +1802,13 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     ctx->launches++;
                     MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
                     if (vec_events) cudaEventRecord(vev[nl - 1][1], st);
-                    if (pcg_warp_map)
+                    if (pcg_warp_map && pcg_minb == 3)
+                        MPL_CUDA(launch_pdl(k_pcg_update2w<T, PCG_E, 3>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, r,
+                                            p, x, slots, sc));
+                    else if (pcg_warp_map && pcg_minb == 4)
+                        MPL_CUDA(launch_pdl(k_pcg_update2w<T, PCG_E, 4>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, r,
+                                            p, x, slots, sc));
+                    else if (pcg_warp_map)
                         MPL_CUDA(launch_pdl(k_pcg_update2w<T>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, r, p, x,
                                             slots, sc));
                     else

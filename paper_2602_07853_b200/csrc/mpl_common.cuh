@@ -356,6 +356,9 @@ template <class T> struct KL {
 __host__ __device__ __forceinline__ constexpr int kz_key(int l) {
     return ((l & 1) << 5) | (((l >> 1) & 1) << 4) | ((l >> 4) << 2) | ((l >> 2) & 3);
 }
+// compressed tangent (fp32, k_hvp_wz): KC_REALS reals per cell (q_U's x, y, z 3, W = S V 9,
+// c psi 6, c (a, b) 6), per tile one pair slot per wz lane holding a cell, 2 KC_REALS reals per slot
+constexpr int KC_REALS = 24;
 int hvp_kz_layout(int precision);  // 1: compact kz order (k_hvp_wz), 3: natural compact order (k_hvp_wh)
 int hvp_variant();                 // fp32 HVP kernel: 0 k_hvp_wz, 1 k_hvp_wh
 template <class T> __host__ __device__ __forceinline__ int64_t k_off(int64_t base, int ncp, int j, int e) {

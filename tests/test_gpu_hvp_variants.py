@@ -35,7 +35,7 @@ CASES = [
     ({"MPL_SORT": "scatter"}, "mix_fp64"),
     ({"MPL_KC": "0"}, "cfg1_fp32"),          # the 45-number tangent where the compressed one is the default
     ({"MPL_KC": "0"}, "cfg2s_fp32"),
-    ({"MPL_KC_MINB": "4"}, "cfg2s_fp32"),
+    ({"MPL_KC_MINB": "3"}, "cfg2s_fp32"),
 ]
 
 

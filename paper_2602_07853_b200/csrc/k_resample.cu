@@ -811,8 +811,7 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
 #pragma unroll
         for (int a = 0; a < 9; a++) atomicAdd(ac + 4 + a, q_.mG[a]);
 #pragma unroll
-        for (int qq = 0; qq < NM; qq++) {
-            if (qq >= nmat) break;
+        for (int qq = 0; qq < NM; qq++) {  // slots past nmat hold zeros (material ids are < nmat)
             atomicAdd(ac + 13 + 7 * qq, q_.V[qq]);
 #pragma unroll
             for (int a = 0; a < 6; a++) atomicAdd(ac + 14 + 7 * qq + a, q_.Vt[qq][a]);
@@ -827,19 +826,35 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
         ccs[tid] = tt < 0 ? -1 : cellof[tt * 64 + local_id(X & 3, Y & 3, Z & 3)];
     }
     __syncthreads();
-    // flush the 5^3 accumulator: interior cells (local 1..3 on every axis) stored, the rest added
-    for (int i = tid; i < 125 * NV; i += blockDim.x) {
-        const int c = i / NV, v = i - c * NV;
-        if (v >= 13 + 7 * nmat) continue;  // slots past the context's materials (NM is an upper bound)
-        const int cc = ccs[c];
-        if (cc < 0) continue;
+    // flush the 5^3 accumulator: interior cells (local 1..3 on every axis) stored, the rest added.  Thread
+    // c < 125 of each half-CTA owns cell c: the first half writes m, mv, mG (13 values), the second the
+    // material slots (7 per slot), every destination offset a compile-time constant of the unrolled loops
+    const int c = tid & 127, half = tid >> 7;
+    if (c < 125 && ccs[c] >= 0) {
+        const int64_t cc = ccs[c];
         const int X = c / 25, Y = (c / 5) % 5, Z = c % 5;
-        const T val = acc[i];
         const bool interior = X >= 1 && X <= 3 && Y >= 1 && Y <= 3 && Z >= 1 && Z <= 3;
-        T *dst = v == 0 ? q_m + cc : v < 4 ? q_mv + 3 * (int64_t)cc + (v - 1) : v < 13 ? q_mG + 9 * (int64_t)cc + (v - 4)
-               : q_slot + ((int64_t)cc * nmat + (v - 13) / 7) * 16 + ((v - 13) % 7 == 0 ? 0 : 6 + (v - 13) % 7);
-        if (interior) *dst = val;
-        else if (val != T(0)) atomicAdd(dst, val);
+        const T *a = acc + c * NV;
+        auto put = [&](T *dst, T val) {
+            if (interior) *dst = val;
+            else if (val != T(0)) atomicAdd(dst, val);
+        };
+        if (half == 0) {
+            put(q_m + cc, a[0]);
+#pragma unroll
+            for (int k = 0; k < 3; k++) put(q_mv + 3 * cc + k, a[1 + k]);
+#pragma unroll
+            for (int k = 0; k < 9; k++) put(q_mG + 9 * cc + k, a[4 + k]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < NM; q++) {
+                if (q >= nmat) break;  // slots past the context's materials (NM is an upper bound)
+                T *sl = q_slot + (cc * nmat + q) * 16;
+                put(sl, a[13 + 7 * q]);
+#pragma unroll
+                for (int k = 0; k < 6; k++) put(sl + 7 + k, a[14 + 7 * q + k]);
+            }
+        }
     }
 }
 
@@ -877,17 +892,22 @@ __global__ void k_p2q_finish(int64_t C, MatP mp, const uint8_t *__restrict__ clo
     const int q = (int)(i - cc * nmat);
     T *sl = q_slot + i * 16;
     T tau[6] = {0, 0, 0, 0, 0, 0}, E[6] = {0, 0, 0, 0, 0, 0};
-    const T V = clocal[cc] != 0xFF ? sl[0] : T(0);
+    const T V0 = sl[0];
+    const T V = clocal[cc] != 0xFF ? V0 : T(0);
     if (V != T(0)) {
         const T iv = T(1) / V;
 #pragma unroll
         for (int a = 0; a < 6; a++) tau[a] = sl[7 + a] * iv;
         stretch_slot<T>(mp, q, tau, E, sc);
     }
-    sl[0] = V;
+    // an empty slot of a local cell is all zeros already (zeroed accumulators, P2Q adds nothing): only
+    // occupied slots and non-local cells are written (sl[1..6] of an occupied slot held zeros, 13..15 stay 0)
+    if (V != T(0) || V0 != T(0)) {
+        sl[0] = V;
 #pragma unroll
-    for (int a = 0; a < 6; a++) { sl[1 + a] = E[a]; sl[7 + a] = tau[a]; }
-    sl[13] = sl[14] = sl[15] = T(0);
+        for (int a = 0; a < 6; a++) { sl[1 + a] = E[a]; sl[7 + a] = tau[a]; }
+        sl[13] = sl[14] = sl[15] = T(0);
+    }
     if (q_Sp) {
         T *sp = q_Sp + i * 9;
         sp[0] = E[0]; sp[4] = E[1]; sp[8] = E[2];

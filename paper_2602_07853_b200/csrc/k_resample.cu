@@ -21,6 +21,7 @@ template <class T>
 __global__ void k_bin_flags(GridP g, int64_t np, const T *__restrict__ x, const int *__restrict__ pid,
                             int *__restrict__ base, int *__restrict__ cflag, DevScalars *sc) {
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const unsigned live = __ballot_sync(0xffffffffu, p < np);
     if (p >= np) return;
     int b[3];
     bool ok = true;
@@ -31,18 +32,25 @@ __global__ void k_bin_flags(GridP g, int64_t np, const T *__restrict__ x, const 
         b[a] = (int)fb;
         ok = ok && (fb >= T(0)) && (b[a] <= g.n[a] - 2) && (t == t);
     }
+    const int key = (b[0] << 20) | (b[1] << 10) | b[2];
+    // particles arrive sorted by base cell (the previous step's order): only the first lane of a run of
+    // equal base cells flags the run's (1-8) cell blocks, with plain stores (no read of the flag)
+    const unsigned ok_m = __ballot_sync(live, ok);
+    const int prev = __shfl_up_sync(live, key, 1);
     if (!ok) {
         atomicMin(&sc->oob_particle, pid[p]);
         base[p] = -1;
         return;
     }
-    base[p] = (b[0] << 20) | (b[1] << 10) | b[2];
+    base[p] = key;
+    const int lane = threadIdx.x & 31;
+    const bool first = lane == 0 || !((ok_m >> (lane - 1)) & 1u) || prev != key;
+    if (!first) return;
     int b0[3] = {b[0] >> 2, b[1] >> 2, b[2] >> 2}, b1[3] = {(b[0] + 1) >> 2, (b[1] + 1) >> 2, (b[2] + 1) >> 2};
     for (int o = 0; o < 8; o++) {
         int bx = (o & 4) ? b1[0] : b0[0], by = (o & 2) ? b1[1] : b0[1], bz = (o & 1) ? b1[2] : b0[2];
         if (((o & 4) && b1[0] == b0[0]) || ((o & 2) && b1[1] == b0[1]) || ((o & 1) && b1[2] == b0[2])) continue;
-        int d = dense_id(g, bx, by, bz);
-        if (cflag[d] == 0) cflag[d] = 1;
+        cflag[dense_id(g, bx, by, bz)] = 1;
     }
 }
 

@@ -723,7 +723,13 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
     __shared__ __align__(8) uint64_t bar[2];
     const int t = blockIdx.x, tid = threadIdx.x;
     if (tid < 65) bs[tid] = bstart[t * 64 + tid];
-    for (int i = tid; i < 125 * NV; i += blockDim.x) acc[i] = T(0);
+    // PV: the pair sums go to private shared slots after the last pass (no shared atomics: sm_100 has no
+    // native shared fp32 add, atomicAdd there is a CAS loop), reusing the accumulator + record space
+    constexpr int PV_ROW = 8 * 68;  // value-major rows of 8 corner columns of 68 (64 buckets + pad)
+    constexpr bool PV = (size_t)NV * PV_ROW * sizeof(T) <=
+                        (size_t)((125 * NV + 3) & ~3) * sizeof(T) + (size_t)2 * P2Q_CAP * REC * sizeof(T);
+    if (!PV)
+        for (int i = tid; i < 125 * NV; i += blockDim.x) acc[i] = T(0);
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -804,6 +810,28 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
         }
         __syncthreads();  // buffer k & 1 consumed before pass k + 2 refills it
     }
+    if constexpr (PV) {
+        // pair (b, o) -> column 68 o + b of every value row: a warp's 32 pairs (4 buckets x 8 corners) hit
+        // 32 distinct banks (4 o + b mod 32), and the flush's reads of one corner over consecutive cells too
+        T *P = acc;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int pr = tid + 256 * h;
+            T *col = P + (pr & 7) * 68 + (pr >> 3);
+            const Acc &q_ = A2[h];
+            col[0] = q_.m;
+#pragma unroll
+            for (int a = 0; a < 3; a++) col[(1 + a) * PV_ROW] = q_.mv[a];
+#pragma unroll
+            for (int a = 0; a < 9; a++) col[(4 + a) * PV_ROW] = q_.mG[a];
+#pragma unroll
+            for (int qq = 0; qq < NM; qq++) {
+                col[(13 + 7 * qq) * PV_ROW] = q_.V[qq];
+#pragma unroll
+                for (int a = 0; a < 6; a++) col[(14 + 7 * qq + a) * PV_ROW] = q_.Vt[qq][a];
+            }
+        }
+    } else {
 #pragma unroll
     for (int h = 0; h < 2; h++) {
         const int pr = tid + 256 * h;
@@ -825,6 +853,7 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
             for (int a = 0; a < 6; a++) atomicAdd(ac + 14 + 7 * qq + a, q_.Vt[qq][a]);
         }
     }
+    }
     // compact cell id of each of the 125 cells (-1: no such structural cell), once per cell
     __shared__ int ccs[125];
     if (tid < 125) {
@@ -842,25 +871,42 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
         const int64_t cc = ccs[c];
         const int X = c / 25, Y = (c / 5) % 5, Z = c % 5;
         const bool interior = X >= 1 && X <= 3 && Y >= 1 && Y <= 3 && Z >= 1 && Z <= 3;
-        const T *a = acc + c * NV;
-        auto put = [&](T *dst, T val) {
-            if (interior) *dst = val;
-            else if (val != T(0)) atomicAdd(dst, val);
+        // PV: value v of cell c = sum over the (up to 8) source pairs (bucket c - o, corner o)
+        int src[8];
+#pragma unroll
+        for (int o = 0; o < 8; o++) {
+            const int bx = X - ((o >> 2) & 1), by = Y - ((o >> 1) & 1), bz = Z - (o & 1);
+            src[o] = (bx >= 0 && bx < 4 && by >= 0 && by < 4 && bz >= 0 && bz < 4) ? o * 68 + (bx * 16 + by * 4 + bz) : -1;
+        }
+        auto val = [&](int v) -> T {
+            if constexpr (PV) {
+                T sum = T(0);
+#pragma unroll
+                for (int o = 0; o < 8; o++)
+                    if (src[o] >= 0) sum += acc[v * PV_ROW + src[o]];
+                return sum;
+            } else {
+                return acc[c * NV + v];
+            }
+        };
+        auto put = [&](T *dst, T x) {
+            if (interior) *dst = x;
+            else if (x != T(0)) atomicAdd(dst, x);
         };
         if (half == 0) {
-            put(q_m + cc, a[0]);
+            put(q_m + cc, val(0));
 #pragma unroll
-            for (int k = 0; k < 3; k++) put(q_mv + 3 * cc + k, a[1 + k]);
+            for (int k = 0; k < 3; k++) put(q_mv + 3 * cc + k, val(1 + k));
 #pragma unroll
-            for (int k = 0; k < 9; k++) put(q_mG + 9 * cc + k, a[4 + k]);
+            for (int k = 0; k < 9; k++) put(q_mG + 9 * cc + k, val(4 + k));
         } else {
 #pragma unroll
             for (int q = 0; q < NM; q++) {
                 if (q >= nmat) break;  // slots past the context's materials (NM is an upper bound)
                 T *sl = q_slot + (cc * nmat + q) * 16;
-                put(sl, a[13 + 7 * q]);
+                put(sl, val(13 + 7 * q));
 #pragma unroll
-                for (int k = 0; k < 6; k++) put(sl + 7 + k, a[14 + 7 * q + k]);
+                for (int k = 0; k < 6; k++) put(sl + 7 + k, val(14 + 7 * q + k));
             }
         }
     }

@@ -793,9 +793,11 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
                 }
                 const T w = (ox ? r[0] : T(1) - r[0]) * (oy ? r[1] : T(1) - r[1]) * (oz ? r[2] : T(1) - r[2]);
                 q_.m += w * r[3];
-                q_.mv[0] += w * (r[4] + dx * ((ox ? r[7] : T(0)) + (oy ? r[8] : T(0)) + (oz ? r[9] : T(0))));
-                q_.mv[1] += w * (r[5] + dx * ((ox ? r[10] : T(0)) + (oy ? r[11] : T(0)) + (oz ? r[12] : T(0))));
-                q_.mv[2] += w * (r[6] + dx * ((ox ? r[13] : T(0)) + (oy ? r[14] : T(0)) + (oz ? r[15] : T(0))));
+                // the affine term dx (mG)_p o of Eq. p2c-mv-affine is added after the loop from the mG sum
+                // (sum_p w m G_p o = (sum_p w m G_p) o): only the o-independent part here
+                q_.mv[0] += w * r[4];
+                q_.mv[1] += w * r[5];
+                q_.mv[2] += w * r[6];
 #pragma unroll
                 for (int a = 0; a < 9; a++) q_.mG[a] += w * r[7 + a];
                 const int k = (int)r[23];
@@ -809,6 +811,15 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
             }
         }
         __syncthreads();  // buffer k & 1 consumed before pass k + 2 refills it
+    }
+#pragma unroll
+    for (int h = 0; h < 2; h++) {  // sum_p w m (v_p + G_p (x_c - x_p)) = sum_p w a_p + dx (sum_p w m G_p) o
+        const int o = (tid + 256 * h) & 7;
+        const T ox = T((o >> 2) & 1), oy = T((o >> 1) & 1), oz = T(o & 1);
+        Acc &q_ = A2[h];
+#pragma unroll
+        for (int a = 0; a < 3; a++)
+            q_.mv[a] += dx * (ox * q_.mG[3 * a] + oy * q_.mG[3 * a + 1] + oz * q_.mG[3 * a + 2]);
     }
     if constexpr (PV) {
         // pair (b, o) -> column 68 o + b of every value row: a warp's 32 pairs (4 buckets x 8 corners) hit
@@ -1484,7 +1495,11 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     g, ctx->mats, (const int *)ctx->t_coord.p, (const int *)ctx->t_nplus.p, (const int *)ctx->t_bstart.p, \
         (const int *)ctx->t_cellof.p, (const T *)ctx->prec.p, (T *)ctx->q_m.p, (T *)ctx->q_mv.p,           \
         (T *)ctx->q_mG.p, (T *)ctx->q_slot.p
-            if (nm <= 2) {
+            if (nm == 1) {
+                const size_t sm = (((size_t)125 * P2QNV<1>::V + 3) & ~(size_t)3) * s + (size_t)2 * P2Q_CAP * REC * s;
+                MPL_CUDA(cudaFuncSetAttribute(k_p2q_tile<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                k_p2q_tile<T, 1><<<T_, 256, sm, st>>>(P2QT_ARGS);
+            } else if (nm <= 2) {
                 const size_t sm = (((size_t)125 * P2QNV<2>::V + 3) & ~(size_t)3) * s + (size_t)2 * P2Q_CAP * REC * s;
                 MPL_CUDA(cudaFuncSetAttribute(k_p2q_tile<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
                 k_p2q_tile<T, 2><<<T_, 256, sm, st>>>(P2QT_ARGS);

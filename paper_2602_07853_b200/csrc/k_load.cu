@@ -84,58 +84,14 @@ __global__ void __launch_bounds__(128) k_n2c(GridP g, const int *__restrict__ np
     st_vec12<T>(vG + 12 * cc, out);
 }
 
-// per particle (sorted order): interpolate, advect, update F
-template <class T, int CMINB = 1>
-__global__ void __launch_bounds__(256, CMINB) k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ skey, const int *__restrict__ pid,
-                      const int *__restrict__ nplus,
-                      const int *__restrict__ cellof, const T *__restrict__ vG,
-                      T *__restrict__ x, T *__restrict__ v, T *__restrict__ F, T *__restrict__ G,
-                      const int *__restrict__ mat, MatP mp) {
-    // full warps without ghosts move x, F (in) and x, v, F, G (out) with 16-byte accesses through
-    // shared memory; others per lane
-    __shared__ __align__(16) T wsm[8][32 * 9];
-    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool valid = p < np && pid[p] >= 0;  // ghosts (slab ranks) are advected by their owner
-    const bool fast = __all_sync(0xffffffffu, valid);
-    T *sm = wsm[threadIdx.x >> 5];
-    const int64_t p0 = p & ~(int64_t)31;
-    if (!valid) return;
-    const int key = skey[p];
-    const int t = key >> 6, l = key & 63;
-    const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
-    T xp[3], f[3];
-    if (fast) warp_load_aos<T, 3>(x, p0, sm, xp);
-    else
-#pragma unroll
-        for (int a = 0; a < 3; a++) xp[a] = x[3 * p + a];
-#pragma unroll
-    for (int a = 0; a < 3; a++) {
-        T tt = (xp[a] - T(g.origin[a])) * T(g.inv_dx) - T(0.5);
-        f[a] = tt - floor(tt);
-    }
-    T vp[3] = {0, 0, 0}, Gp[9];
-#pragma unroll
-    for (int a = 0; a < 9; a++) Gp[a] = T(0);
-#pragma unroll
-    for (int o = 0; o < 8; o++) {
-        int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
-        int cx = lx + ox, cy = ly + oy, cz = lz + oz;
-        int dp = ((cx >> 2) << 2) | ((cy >> 2) << 1) | (cz >> 2);
-        int tt = dp ? nplus[8 * t + dp] : t;
-        int cc = cellof[tt * 64 + local_id(cx & 3, cy & 3, cz & 3)];
-        T w = (ox ? f[0] : T(1) - f[0]) * (oy ? f[1] : T(1) - f[1]) * (oz ? f[2] : T(1) - f[2]);
-        T c[12];
-        ld_vec12<T>(vG + 12 * (int64_t)cc, c);
-        vp[0] += w * c[0]; vp[1] += w * c[1]; vp[2] += w * c[2];
-#pragma unroll
-        for (int a = 0; a < 9; a++) Gp[a] += w * c[3 + a];
-    }
+// the per-particle part of G2P once v_p, G_p are interpolated: advect, update F (per material law), store
+template <class T>
+__device__ __forceinline__ void c2p_finish(int64_t p, int64_t p0, bool fast, T *sm, double dt_, const T xp[3],
+                                           const T vp[3], const T Gp[9], const T Fp[9], T *__restrict__ x,
+                                           T *__restrict__ v, T *__restrict__ F, T *__restrict__ G,
+                                           const int *__restrict__ mat, const MatP &mp) {
     const T dt = T(dt_);
-    T Fp[9], A[9], Fn[9];
-    if (fast) warp_load_aos<T, 9>(F, p0, sm, Fp);
-    else
-#pragma unroll
-        for (int a = 0; a < 9; a++) Fp[a] = F[9 * p + a];
+    T A[9], Fn[9];
 #pragma unroll
     for (int a = 0; a < 9; a++) A[a] = dt * Gp[a] + ((a % 4 == 0) ? T(1) : T(0));
     const int mk = mat[p];
@@ -183,6 +139,166 @@ __global__ void __launch_bounds__(256, CMINB) k_c2p(GridP g, double dt_, int64_t
     for (int a = 0; a < 9; a++) {
         F[9 * p + a] = Fn[a];
         G[9 * p + a] = Gp[a];
+    }
+}
+
+// per particle (sorted order): interpolate, advect, update F
+template <class T, int CMINB = 1>
+__global__ void __launch_bounds__(256, CMINB) k_c2p(GridP g, double dt_, int64_t np, const int *__restrict__ skey, const int *__restrict__ pid,
+                      const int *__restrict__ nplus,
+                      const int *__restrict__ cellof, const T *__restrict__ vG,
+                      T *__restrict__ x, T *__restrict__ v, T *__restrict__ F, T *__restrict__ G,
+                      const int *__restrict__ mat, MatP mp) {
+    // full warps without ghosts move x, F (in) and x, v, F, G (out) with 16-byte accesses through
+    // shared memory; others per lane
+    __shared__ __align__(16) T wsm[8][32 * 9];
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool valid = p < np && pid[p] >= 0;  // ghosts (slab ranks) are advected by their owner
+    const bool fast = __all_sync(0xffffffffu, valid);
+    T *sm = wsm[threadIdx.x >> 5];
+    const int64_t p0 = p & ~(int64_t)31;
+    if (!valid) return;
+    const int key = skey[p];
+    const int t = key >> 6, l = key & 63;
+    const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+    T xp[3], f[3];
+    if (fast) warp_load_aos<T, 3>(x, p0, sm, xp);
+    else
+#pragma unroll
+        for (int a = 0; a < 3; a++) xp[a] = x[3 * p + a];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        T tt = (xp[a] - T(g.origin[a])) * T(g.inv_dx) - T(0.5);
+        f[a] = tt - floor(tt);
+    }
+    T vp[3] = {0, 0, 0}, Gp[9];
+#pragma unroll
+    for (int a = 0; a < 9; a++) Gp[a] = T(0);
+#pragma unroll
+    for (int o = 0; o < 8; o++) {
+        int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+        int cx = lx + ox, cy = ly + oy, cz = lz + oz;
+        int dp = ((cx >> 2) << 2) | ((cy >> 2) << 1) | (cz >> 2);
+        int tt = dp ? nplus[8 * t + dp] : t;
+        int cc = cellof[tt * 64 + local_id(cx & 3, cy & 3, cz & 3)];
+        T w = (ox ? f[0] : T(1) - f[0]) * (oy ? f[1] : T(1) - f[1]) * (oz ? f[2] : T(1) - f[2]);
+        T c[12];
+        ld_vec12<T>(vG + 12 * (int64_t)cc, c);
+        vp[0] += w * c[0]; vp[1] += w * c[1]; vp[2] += w * c[2];
+#pragma unroll
+        for (int a = 0; a < 9; a++) Gp[a] += w * c[3 + a];
+    }
+    T Fp[9];
+    if (fast) warp_load_aos<T, 9>(F, p0, sm, Fp);
+    else
+#pragma unroll
+        for (int a = 0; a < 9; a++) Fp[a] = F[9 * p + a];
+    c2p_finish<T>(p, p0, fast, sm, dt_, xp, vp, Gp, Fp, x, v, F, G, mat, mp);
+}
+
+
+// G2P per tile (default, MPL_G2P=tile): one CTA per tile stages the (v_c, G_c) of the 5^3 cells its
+// particles' stencils reach in shared memory once (a per-particle gather looked up 8 cells through the
+// neighbour table and the cell map: three dependent loads each), then its warps take the aligned
+// 32-particle chunks of the tile's particle range [bstart[64 t], bstart[64 t + 64]) (particles are sorted
+// by tile and base cell); chunks straddling a range end are processed lane by lane.
+template <class T>
+__global__ void __launch_bounds__(128, sizeof(T) == 4 ? 8 : 4) k_c2p_tile(GridP g, double dt_, const int *__restrict__ bstart,
+                                                  const int *__restrict__ skey, const int *__restrict__ pid,
+                                                  const int *__restrict__ nplus, const int *__restrict__ cellof,
+                                                  const T *__restrict__ vG, T *__restrict__ x, T *__restrict__ v,
+                                                  T *__restrict__ F, T *__restrict__ G, const int *__restrict__ mat,
+                                                  MatP mp) {
+    __shared__ __align__(16) T cv[125 * 12];
+    __shared__ __align__(16) T wsm[4][32 * 12];
+    const int t = blockIdx.x, tid = threadIdx.x;
+    const int pb = bstart[64 * t], pe = bstart[64 * t + 64];
+    if (pb == pe) return;
+    if (tid < 125) {
+        const int X = tid / 25, Y = (tid / 5) % 5, Z = tid % 5;
+        const int dp = ((X >> 2) << 2) | ((Y >> 2) << 1) | (Z >> 2);
+        const int tt = dp ? nplus[8 * t + dp] : t;
+        const int cc = tt < 0 ? -1 : cellof[tt * 64 + local_id(X & 3, Y & 3, Z & 3)];
+        T c[12];
+        if (cc >= 0) ld_vec12<T>(vG + 12 * (int64_t)cc, c);
+        else
+#pragma unroll
+            for (int a = 0; a < 12; a++) c[a] = T(0);
+        st_vec12<T>(cv + 12 * tid, c);
+    }
+    __syncthreads();
+    const int w = tid >> 5, lane = tid & 31;
+    T *sm = wsm[w];
+    for (int64_t p0 = ((int64_t)pb & ~(int64_t)31) + 32 * w; p0 < pe; p0 += 128) {
+        const int64_t p = p0 + lane;
+        const bool valid = p >= pb && p < pe && pid[p] >= 0;  // ghosts (slab ranks) are advected by their owner
+        const bool fast = __all_sync(0xffffffffu, valid);
+        if (!valid) continue;
+        const int l = skey[p] & 63;
+        const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+        T xp[3], f[3], Fp[9];  // x and F requested together (one memory round trip per chunk)
+        if (fast) {
+            // the chunk's x (32 x 3) and F (32 x 9) as 16-byte vectors, all loads issued before any is used
+            constexpr int NX = (int)(32 * 3 * sizeof(T) / 16), NF = (int)(32 * 9 * sizeof(T) / 16);
+            constexpr int KX = (NX + 31) / 32, KF = (NF + 31) / 32;
+            const float4 *sx = reinterpret_cast<const float4 *>(x + 3 * p0);
+            const float4 *sF = reinterpret_cast<const float4 *>(F + 9 * p0);
+            float4 rx[KX], rF[KF];
+#pragma unroll
+            for (int k = 0; k < KX; k++)
+                if (lane + 32 * k < NX) rx[k] = sx[lane + 32 * k];
+#pragma unroll
+            for (int k = 0; k < KF; k++)
+                if (lane + 32 * k < NF) rF[k] = sF[lane + 32 * k];
+            float4 *dx4 = reinterpret_cast<float4 *>(sm), *dF4 = reinterpret_cast<float4 *>(sm + 32 * 3);
+#pragma unroll
+            for (int k = 0; k < KX; k++)
+                if (lane + 32 * k < NX) dx4[lane + 32 * k] = rx[k];
+#pragma unroll
+            for (int k = 0; k < KF; k++)
+                if (lane + 32 * k < NF) dF4[lane + 32 * k] = rF[k];
+            __syncwarp();
+#pragma unroll
+            for (int a = 0; a < 3; a++) xp[a] = sm[lane * 3 + a];
+#pragma unroll
+            for (int a = 0; a < 9; a++) Fp[a] = sm[32 * 3 + lane * 9 + a];
+            __syncwarp();
+        } else {
+#pragma unroll
+            for (int a = 0; a < 3; a++) xp[a] = x[3 * p + a];
+#pragma unroll
+            for (int a = 0; a < 9; a++) Fp[a] = F[9 * p + a];
+        }
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            T tt = (xp[a] - T(g.origin[a])) * T(g.inv_dx) - T(0.5);
+            f[a] = tt - floor(tt);
+        }
+        T vp[3] = {0, 0, 0}, Gp[9];
+#pragma unroll
+        for (int a = 0; a < 9; a++) Gp[a] = T(0);
+#pragma unroll
+        for (int o = 0; o < 8; o++) {
+            const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+            const T w8 = (ox ? f[0] : T(1) - f[0]) * (oy ? f[1] : T(1) - f[1]) * (oz ? f[2] : T(1) - f[2]);
+            const T *c = cv + 12 * (((lx + ox) * 5 + ly + oy) * 5 + lz + oz);
+            T cc[12];
+            if (sizeof(T) == 4) {
+                const float4 *c4 = reinterpret_cast<const float4 *>(c);
+#pragma unroll
+                for (int i = 0; i < 3; i++) {
+                    const float4 q = c4[i];
+                    cc[4 * i] = q.x; cc[4 * i + 1] = q.y; cc[4 * i + 2] = q.z; cc[4 * i + 3] = q.w;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 12; i++) cc[i] = c[i];
+            }
+            vp[0] += w8 * cc[0]; vp[1] += w8 * cc[1]; vp[2] += w8 * cc[2];
+#pragma unroll
+            for (int a = 0; a < 9; a++) Gp[a] += w8 * cc[3 + a];
+        }
+        c2p_finish<T>(p, p0, fast, sm, dt_, xp, vp, Gp, Fp, x, v, F, G, mat, mp);
     }
 }
 
@@ -261,7 +377,19 @@ mpl_status g2p_impl(mpl_ctx ctx, double dt) {
                                      (const uint8_t *)ctx->c_local.p, (const int *)ctx->t_hascells.p,
                                      (const T *)ctx->q_m.p, (const vec4<T> *)ctx->n_v.p, (T *)ctx->q_vc.p);
         ctx->launches++;
-    if (ctx->np) {
+    static int g2p_tile = -1;
+    if (g2p_tile < 0) {
+        const char *e = getenv("MPL_G2P");
+        g2p_tile = (e && e[0] == 'p') ? 0 : 1;  // "particle": one thread per particle with its own cell lookups
+    }
+    if (ctx->np && g2p_tile && T_) {
+        k_c2p_tile<T><<<T_, 128, 0, st>>>(ctx->grid, dt, (const int *)ctx->t_bstart.p, (const int *)ctx->pskey.p,
+                                          (const int *)ctx->pid[c].p, (const int *)ctx->t_nplus.p,
+                                          (const int *)ctx->t_cellof.p, (const T *)ctx->q_vc.p, (T *)ctx->px[c].p,
+                                          (T *)ctx->pv.p, (T *)ctx->pF[c].p, (T *)ctx->pG.p,
+                                          (const int *)ctx->pmat[c].p, ctx->mats);
+        ctx->launches++;
+    } else if (ctx->np) {
         static int cmb = -1;
         if (cmb < 0) {
             const char *e = getenv("MPL_C2P_MINB");

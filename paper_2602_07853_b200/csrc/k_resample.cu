@@ -707,6 +707,70 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  : "memory");
 }
 
+// P2Q flush (both scatter kernels): compact cell ids of the tile's 5^3 accumulator cells, then interior
+// cells (local 1..3 on every axis) stored, the rest added.  Thread c < 125 of each half-CTA owns cell c: the
+// first half writes m, mv, mG (13 values), the second the material slots (7 per slot), every destination
+// offset a compile-time constant of the unrolled loops.  PV: value v of cell c = the sum over its (up to
+// 8) source pairs (bucket c - o, corner o) at acc[v * 8 * 68 + 68 o + bucket]; else acc[c * NV + v].
+// Needs 256 threads; ends the kernel (no barrier after it).
+template <class T, int NM, bool PV>
+__device__ __forceinline__ void p2q_flush(int t, int tid, int nmat, const int *__restrict__ nplus,
+                                          const int *__restrict__ cellof, const T *acc, T *__restrict__ q_m,
+                                          T *__restrict__ q_mv, T *__restrict__ q_mG, T *__restrict__ q_slot) {
+    constexpr int NV = 13 + 7 * NM, PV_ROW = 8 * 68;
+    __shared__ int ccs[125];
+    if (tid < 125) {
+        const int X = tid / 25, Y = (tid / 5) % 5, Z = tid % 5;
+        const int dp = ((X >> 2) << 2) | ((Y >> 2) << 1) | (Z >> 2);
+        const int tt = dp ? nplus[8 * t + dp] : t;
+        ccs[tid] = tt < 0 ? -1 : cellof[tt * 64 + local_id(X & 3, Y & 3, Z & 3)];
+    }
+    __syncthreads();
+    const int c = tid & 127, half = tid >> 7;
+    if (c < 125 && ccs[c] >= 0) {
+        const int64_t cc = ccs[c];
+        const int X = c / 25, Y = (c / 5) % 5, Z = c % 5;
+        const bool interior = X >= 1 && X <= 3 && Y >= 1 && Y <= 3 && Z >= 1 && Z <= 3;
+        int src[8];
+#pragma unroll
+        for (int o = 0; o < 8; o++) {
+            const int bx = X - ((o >> 2) & 1), by = Y - ((o >> 1) & 1), bz = Z - (o & 1);
+            src[o] = (bx >= 0 && bx < 4 && by >= 0 && by < 4 && bz >= 0 && bz < 4) ? o * 68 + (bx * 16 + by * 4 + bz) : -1;
+        }
+        auto val = [&](int v) -> T {
+            if constexpr (PV) {
+                T sum = T(0);
+#pragma unroll
+                for (int o = 0; o < 8; o++)
+                    if (src[o] >= 0) sum += acc[v * PV_ROW + src[o]];
+                return sum;
+            } else {
+                return acc[c * NV + v];
+            }
+        };
+        auto put = [&](T *dst, T x) {
+            if (interior) *dst = x;
+            else if (x != T(0)) atomicAdd(dst, x);
+        };
+        if (half == 0) {
+            put(q_m + cc, val(0));
+#pragma unroll
+            for (int k = 0; k < 3; k++) put(q_mv + 3 * cc + k, val(1 + k));
+#pragma unroll
+            for (int k = 0; k < 9; k++) put(q_mG + 9 * cc + k, val(4 + k));
+        } else {
+#pragma unroll
+            for (int q = 0; q < NM; q++) {
+                if (q >= nmat) break;  // slots past the context's materials (NM is an upper bound)
+                T *sl = q_slot + (cc * nmat + q) * 16;
+                put(sl, val(13 + 7 * q));
+#pragma unroll
+                for (int k = 0; k < 6; k++) put(sl + 7 + k, val(14 + 7 * q + k));
+            }
+        }
+    }
+}
+
 constexpr int P2Q_CAP = 256;  // particles staged per pass, double-buffered (2 x 24 KB of fp32 records)
 template <int NM> struct P2QNV { static constexpr int V = 13 + 7 * NM; };  // m, mv 3, mG 9, per slot V + V tau 6
 template <class T, int NM>
@@ -865,62 +929,140 @@ __global__ void __launch_bounds__(256) k_p2q_tile(GridP g, MatP mp, const int *_
         }
     }
     }
-    // compact cell id of each of the 125 cells (-1: no such structural cell), once per cell
-    __shared__ int ccs[125];
-    if (tid < 125) {
-        const int X = tid / 25, Y = (tid / 5) % 5, Z = tid % 5;
-        const int dp = ((X >> 2) << 2) | ((Y >> 2) << 1) | (Z >> 2);
-        const int tt = dp ? nplus[8 * t + dp] : t;
-        ccs[tid] = tt < 0 ? -1 : cellof[tt * 64 + local_id(X & 3, Y & 3, Z & 3)];
-    }
+    p2q_flush<T, NM, PV>(t, tid, nmat, nplus, cellof, acc, q_m, q_mv, q_mG, q_slot);
+}
+
+// ---- a2, scatter form for dense particle buckets (MPL_P2Q_HI, mean >= P2Q_HI_PPC particles per occupied
+// base cell, e.g. cfg3 at PPC 27 / 64): in k_p2q_tile a staged pass of 256 consecutive particles covers only
+// a few buckets when buckets hold tens of particles, so most (bucket, corner) threads idle.  Here warp w
+// owns buckets 8w .. 8w + 7 (contiguous records) and walks them one at a time with all 32 lanes: lane
+// (slot j, corner o) = 8 j + o sums corner o over the bucket's particles j, j + 4, ...; the records arrive
+// in 32-record chunks cp.async double-buffered per warp; the 4 slot sums are combined by shuffles and the
+// (bucket, corner) sum is written to the private slot of the same layout as k_p2q_tile's, then the same
+// flush.  No CTA barrier inside the particle loop.
+__device__ __forceinline__ void cp_async16_g2s(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait_() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+constexpr double P2Q_HI_PPC = 40.0;  // cfg3: PPC 64 (61 per cell) 11.4 -> 9.4 ms; PPC 27 (26 per cell) 4.86 -> 5.05 ms
+template <class T, int NM>
+__global__ void __launch_bounds__(256) k_p2q_hi(GridP g, MatP mp, const int *__restrict__ coord,
+                                                const int *__restrict__ nplus, const int *__restrict__ bstart,
+                                                const int *__restrict__ cellof, const T *__restrict__ rec,
+                                                T *__restrict__ q_m, T *__restrict__ q_mv, T *__restrict__ q_mG,
+                                                T *__restrict__ q_slot) {
+    constexpr int NV = P2QNV<NM>::V, PV_ROW = 8 * 68;
+    extern __shared__ __align__(16) unsigned char p2q_smem[];
+    T *P = reinterpret_cast<T *>(p2q_smem);  // [NV][PV_ROW] pair sums
+    T *stg = P + NV * PV_ROW;                  // [8 warps][2][32 REC] record chunks
+    __shared__ int bs[65];
+    const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid < 65) bs[tid] = bstart[t * 64 + tid];
     __syncthreads();
-    // flush the 5^3 accumulator: interior cells (local 1..3 on every axis) stored, the rest added.  Thread
-    // c < 125 of each half-CTA owns cell c: the first half writes m, mv, mG (13 values), the second the
-    // material slots (7 per slot), every destination offset a compile-time constant of the unrolled loops
-    const int c = tid & 127, half = tid >> 7;
-    if (c < 125 && ccs[c] >= 0) {
-        const int64_t cc = ccs[c];
-        const int X = c / 25, Y = (c / 5) % 5, Z = c % 5;
-        const bool interior = X >= 1 && X <= 3 && Y >= 1 && Y <= 3 && Z >= 1 && Z <= 3;
-        // PV: value v of cell c = sum over the (up to 8) source pairs (bucket c - o, corner o)
-        int src[8];
+    if (bs[0] == bs[64]) return;  // no particles based in this tile (every thread sees the same)
+    const int nmat = mp.nmat;
+    const T dx = T(g.dx);
+    const int o = lane & 7, j = lane >> 3;
+    const int ox = (o >> 2) & 1, oy = (o >> 1) & 1, oz = o & 1;
+    T *S = stg + w * 2 * 32 * REC;
+    constexpr int NC = (int)(REC * sizeof(T) / 16);  // 16-byte pieces per record
+    for (int bb = 0; bb < 8; bb++) {
+        const int b = 8 * w + bb;
+        const int s0 = bs[b], e0 = bs[b + 1];
+        T m = 0, mv[3] = {0, 0, 0}, mG[9], V[NM], Vt[NM][6];
 #pragma unroll
-        for (int o = 0; o < 8; o++) {
-            const int bx = X - ((o >> 2) & 1), by = Y - ((o >> 1) & 1), bz = Z - (o & 1);
-            src[o] = (bx >= 0 && bx < 4 && by >= 0 && by < 4 && bz >= 0 && bz < 4) ? o * 68 + (bx * 16 + by * 4 + bz) : -1;
+        for (int a = 0; a < 9; a++) mG[a] = 0;
+#pragma unroll
+        for (int k = 0; k < NM; k++) {
+            V[k] = 0;
+#pragma unroll
+            for (int a = 0; a < 6; a++) Vt[k][a] = 0;
         }
-        auto val = [&](int v) -> T {
-            if constexpr (PV) {
-                T sum = T(0);
+        const int nch = (e0 - s0 + 31) >> 5;
+        auto issue = [&](int k) {  // lane i: record s0 + 32 k + i
+            const int p = s0 + 32 * k + lane;
+            if (p < e0) {
+                const char *src = reinterpret_cast<const char *>(rec + (int64_t)p * REC);
+                char *dst = reinterpret_cast<char *>(S + ((k & 1) * 32 + lane) * REC);
 #pragma unroll
-                for (int o = 0; o < 8; o++)
-                    if (src[o] >= 0) sum += acc[v * PV_ROW + src[o]];
-                return sum;
-            } else {
-                return acc[c * NV + v];
+                for (int i = 0; i < NC; i++) cp_async16_g2s(dst + 16 * i, src + 16 * i);
             }
+            cp_async_commit_();
         };
-        auto put = [&](T *dst, T x) {
-            if (interior) *dst = x;
-            else if (x != T(0)) atomicAdd(dst, x);
+        if (nch > 0) issue(0);
+        for (int k = 0; k < nch; k++) {
+            if (k + 1 < nch) {
+                issue(k + 1);  // buffer (k + 1) & 1 was released by the __syncwarp closing chunk k - 1
+                cp_async_wait_<1>();
+            } else {
+                cp_async_wait_<0>();
+            }
+            __syncwarp();
+            const T *R = S + (k & 1) * 32 * REC;
+            const int n = min(32, e0 - s0 - 32 * k);
+            for (int q = j; q < n; q += 4) {
+                T r[REC];
+                {
+                    const float4 *r4 = reinterpret_cast<const float4 *>(R + q * REC);
+                    float4 *d4 = reinterpret_cast<float4 *>(r);
+#pragma unroll
+                    for (int i = 0; i < NC; i++) d4[i] = r4[i];
+                }
+                const T wt = (ox ? r[0] : T(1) - r[0]) * (oy ? r[1] : T(1) - r[1]) * (oz ? r[2] : T(1) - r[2]);
+                m += wt * r[3];
+#pragma unroll
+                for (int a = 0; a < 3; a++) mv[a] += wt * r[4 + a];  // affine term below, from the mG sum
+#pragma unroll
+                for (int a = 0; a < 9; a++) mG[a] += wt * r[7 + a];
+                const int km = (int)r[23];
+#pragma unroll
+                for (int qq = 0; qq < NM; qq++)
+                    if (qq == km || NM == 1) {
+                        V[qq] += wt * r[16];
+#pragma unroll
+                        for (int a = 0; a < 6; a++) Vt[qq][a] += wt * r[17 + a];
+                    }
+            }
+            __syncwarp();  // chunk consumed before it is refilled
+        }
+        // combine the 4 slots of each corner (lanes o, o + 8, o + 16, o + 24); slot 0 writes the pair
+        auto red = [&](T x) {
+            x += __shfl_xor_sync(0xffffffffu, x, 8);
+            x += __shfl_xor_sync(0xffffffffu, x, 16);
+            return x;
         };
-        if (half == 0) {
-            put(q_m + cc, val(0));
+        m = red(m);
 #pragma unroll
-            for (int k = 0; k < 3; k++) put(q_mv + 3 * cc + k, val(1 + k));
+        for (int a = 0; a < 3; a++) mv[a] = red(mv[a]);
 #pragma unroll
-            for (int k = 0; k < 9; k++) put(q_mG + 9 * cc + k, val(4 + k));
-        } else {
+        for (int a = 0; a < 9; a++) mG[a] = red(mG[a]);
 #pragma unroll
-            for (int q = 0; q < NM; q++) {
-                if (q >= nmat) break;  // slots past the context's materials (NM is an upper bound)
-                T *sl = q_slot + (cc * nmat + q) * 16;
-                put(sl, val(13 + 7 * q));
+        for (int qq = 0; qq < NM; qq++) {
+            V[qq] = red(V[qq]);
 #pragma unroll
-                for (int k = 0; k < 6; k++) put(sl + 7 + k, val(14 + 7 * q + k));
+            for (int a = 0; a < 6; a++) Vt[qq][a] = red(Vt[qq][a]);
+        }
+        if (j == 0) {
+            // sum_p w m (v_p + G_p (x_c - x_p)) = sum_p w a_p + dx (sum_p w m G_p) o
+#pragma unroll
+            for (int a = 0; a < 3; a++)
+                mv[a] += dx * (T(ox) * mG[3 * a] + T(oy) * mG[3 * a + 1] + T(oz) * mG[3 * a + 2]);
+            T *col = P + o * 68 + b;
+            col[0] = m;
+#pragma unroll
+            for (int a = 0; a < 3; a++) col[(1 + a) * PV_ROW] = mv[a];
+#pragma unroll
+            for (int a = 0; a < 9; a++) col[(4 + a) * PV_ROW] = mG[a];
+#pragma unroll
+            for (int qq = 0; qq < NM; qq++) {
+                col[(13 + 7 * qq) * PV_ROW] = V[qq];
+#pragma unroll
+                for (int a = 0; a < 6; a++) col[(14 + 7 * qq + a) * PV_ROW] = Vt[qq][a];
             }
         }
     }
+    p2q_flush<T, NM, true>(t, tid, nmat, nplus, cellof, P, q_m, q_mv, q_mG, q_slot);
 }
 
 // cells with two or more occupied material slots (the compressed tangent covers one slot per cell)
@@ -1495,7 +1637,24 @@ mpl_status resample_impl(mpl_ctx ctx, double dt) {
     g, ctx->mats, (const int *)ctx->t_coord.p, (const int *)ctx->t_nplus.p, (const int *)ctx->t_bstart.p, \
         (const int *)ctx->t_cellof.p, (const T *)ctx->prec.p, (T *)ctx->q_m.p, (T *)ctx->q_mv.p,           \
         (T *)ctx->q_mG.p, (T *)ctx->q_slot.p
-            if (nm == 1) {
+            // dense buckets (MPL_P2Q_HI: 0 off, 1 on, default when np / cells >= P2Q_HI_PPC): k_p2q_hi
+            static int hi_mode = -1;
+            if (hi_mode < 0) {
+                const char *e = getenv("MPL_P2Q_HI");
+                hi_mode = e ? (e[0] == '1' ? 1 : 0) : 2;
+            }
+            const bool hi = nm <= 2 && (hi_mode == 1 || (hi_mode == 2 && ncells > 0 &&
+                                                        (double)ctx->np >= P2Q_HI_PPC * (double)ncells));
+            if (hi) {
+                const size_t sm = (size_t)(13 + 7 * (nm == 1 ? 1 : 2)) * 8 * 68 * s + (size_t)8 * 2 * 32 * REC * s;
+                if (nm == 1) {
+                    MPL_CUDA(cudaFuncSetAttribute(k_p2q_hi<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                    k_p2q_hi<T, 1><<<T_, 256, sm, st>>>(P2QT_ARGS);
+                } else {
+                    MPL_CUDA(cudaFuncSetAttribute(k_p2q_hi<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                    k_p2q_hi<T, 2><<<T_, 256, sm, st>>>(P2QT_ARGS);
+                }
+            } else if (nm == 1) {
                 const size_t sm = (((size_t)125 * P2QNV<1>::V + 3) & ~(size_t)3) * s + (size_t)2 * P2Q_CAP * REC * s;
                 MPL_CUDA(cudaFuncSetAttribute(k_p2q_tile<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
                 k_p2q_tile<T, 1><<<T_, 256, sm, st>>>(P2QT_ARGS);

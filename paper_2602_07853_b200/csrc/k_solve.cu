@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(256) k_pcg_init(int64_t n, int64_t S, const in
                                                   const vec4<T> *__restrict__ g,
                                                   const vec4<T> *__restrict__ D, T *__restrict__ invD,
                                                   T *__restrict__ r, vec4<T> *__restrict__ p,
-                                                  T *__restrict__ x, CGSlot *slot) {
+                                                  T *__restrict__ x, CGSlot *slot, bool zform) {
     T rz = 0, rr = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x) {
         T rv[3] = {0, 0, 0}, iv[3] = {0, 0, 0};
@@ -878,7 +878,7 @@ __global__ void __launch_bounds__(256) k_pcg_init(int64_t n, int64_t S, const in
 #pragma unroll
         for (int c = 0; c < 3; c++) {
             invD[c * S + i] = iv[c];
-            r[c * S + i] = rv[c];
+            r[c * S + i] = zform ? rv[c] * iv[c] : rv[c];  // zform: the buffer holds z = D^-1 r
             x[c * S + i] = T(0);
         }
     }
@@ -1060,7 +1060,7 @@ __global__ void __launch_bounds__(256) k_pcg_update2(int64_t n, int64_t S, const
 // instruction is contiguous across the warp (the group mapping above writes p / Hp at a 64-byte lane
 // stride).  Full chunks run without per-node bounds checks.
 constexpr int PCG_E = 4;  // nodes per lane per chunk (2 with 4 CTAs per SM measured slower: cfg4 step 65.2 vs 59.1 ms)
-template <class T, int E = PCG_E, int MB = 2>
+template <class T, int E = PCG_E, int MB = 2, bool ZF = false>
 __global__ void __launch_bounds__(256, MB) k_pcg_update1w(int64_t n, int64_t S, const int *__restrict__ list, int j,
                                                          double thr, const T *__restrict__ invD,
                                                          const vec4<T> *__restrict__ p, vec4<T> *__restrict__ Hp,
@@ -1112,11 +1112,23 @@ __global__ void __launch_bounds__(256, MB) k_pcg_update1w(int64_t n, int64_t S, 
             if (!FULL && li[e] < 0) continue;
             const int64_t i = base + 32 * e + lane;
             Hp[li[e]] = mk4<T>(0, 0, 0, 0);
+            const T w = own ? T(own[li[e]]) : T(1);
+            if (ZF) {  // the buffer holds z = D^-1 r: z -= (alpha D^-1) Hp; prescribed DOFs have D^-1 = 0, z = 0
+                const T hc[3] = {hv[e].x, hv[e].y, hv[e].z};
+#pragma unroll
+                for (int c = 0; c < 3; c++) {
+                    const T zc = rv[e][c] - (alpha * iv[e][c]) * hc[c];
+                    r[c * S + i] = zc;
+                    const T rc = iv[e][c] != T(0) ? __fdividef(zc, iv[e][c]) : T(0);  // r = D z
+                    rz += w * (rc * zc);
+                    rr += w * (rc * rc);
+                }
+                continue;
+            }
             const T aw = iv[e][0] != T(0) ? alpha : T(0);  // prescribed DOFs keep r = 0
             rv[e][0] -= aw * hv[e].x; rv[e][1] -= aw * hv[e].y; rv[e][2] -= aw * hv[e].z;
 #pragma unroll
             for (int c = 0; c < 3; c++) r[c * S + i] = rv[e][c];
-            const T w = own ? T(own[li[e]]) : T(1);
             rz += w * (rv[e][0] * rv[e][0] * iv[e][0] + rv[e][1] * rv[e][1] * iv[e][1] + rv[e][2] * rv[e][2] * iv[e][2]);
             rr += w * (rv[e][0] * rv[e][0] + rv[e][1] * rv[e][1] + rv[e][2] * rv[e][2]);
         }
@@ -1130,7 +1142,7 @@ __global__ void __launch_bounds__(256, MB) k_pcg_update1w(int64_t n, int64_t S, 
     block_add((double)rr, slot[j + 1].rr);
 }
 
-template <class T, int E = PCG_E, int MB = 2>
+template <class T, int E = PCG_E, int MB = 2, bool ZF = false>
 __global__ void __launch_bounds__(256, MB) k_pcg_update2w(int64_t n, int64_t S, const int *__restrict__ list, int j,
                                                          double thr, const T *__restrict__ invD,
                                                          const T *__restrict__ r, vec4<T> *__restrict__ p,
@@ -1158,7 +1170,10 @@ __global__ void __launch_bounds__(256, MB) k_pcg_update2w(int64_t n, int64_t S, 
 #pragma unroll
                 for (int c = 0; c < 3; c++) {
                     xv[e][c] = x[c * S + i];
-                    if (more) { rv[e][c] = r[c * S + i]; iv[e][c] = invD[c * S + i]; }
+                    if (more) {
+                        rv[e][c] = r[c * S + i];
+                        iv[e][c] = ZF ? T(1) : invD[c * S + i];  // ZF: r holds z = D^-1 r already
+                    }
                 }
             } else {
                 li[e] = -1;
@@ -1566,6 +1581,11 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     const bool pcg_warp_map = pme ? pme[0] == 'w' : sizeof(T) == 4;
     const char *pmb = getenv("MPL_PCG_MINB");  // CTAs of 256 per SM requested from ptxas (2: <= 128 registers)
     const int pcg_minb = pmb ? atoi(pmb) : 2;
+    // MPL_PCG_Z (fp32 warp-map kernels, default 1): the residual buffer holds z = D^-1 r instead of r
+    // (update2 then reads z instead of r and D^-1: 12 B per node less; r = D z for the dot products).
+    // cfg4: update2 10.75 -> 9.43 ms, update1 12.15 -> 12.55 ms per step (the divisions), step 54.5 -> 53.7 ms
+    const char *pze = getenv("MPL_PCG_Z");
+    const bool pcg_z = !cg1 && sizeof(T) == 4 && pcg_warp_map && pcg_minb == 2 && !(pze && pze[0] == '0');
     const unsigned VG = vgrid(NT);
     const unsigned VA = vgrid(NA);
     const unsigned VA1 = nblk(NA > 0 ? NA : 1, 256);
@@ -1661,7 +1681,7 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         MPL_CUDA(cudaMemsetAsync(&sc->neg_curv, 0, sizeof(int), st));
         MPL_CUDA(cudaMemsetAsync(&sc->cg_done_iter, 0xff, sizeof(int), st));
         MPL_CUDA(cudaMemsetAsync(p, 0, NT * sizeof(vec4<T>), st));
-        k_pcg_init<T><<<vgrid(SA), 256, 0, st>>>(NA, SA, list, flag, own_w, g, D, invD, r, p, x, slots);
+        k_pcg_init<T><<<vgrid(SA), 256, 0, st>>>(NA, SA, list, flag, own_w, g, D, invD, r, p, x, slots, pcg_z);
         ctx->launches++;
         MPL_CHECK(allreduce_d(ctx, slots[0].rz, 3 * NSTRIPE));
         MPL_CUDA(cudaMemsetAsync(Hp, 0, NT * sizeof(vec4<T>), st));
@@ -1787,7 +1807,10 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     if (timed) sampled.push_back({nl, jj});
                     nl++;
                     if (vec_events) cudaEventRecord(vev[nl - 1][0], st);
-                    if (pcg_warp_map && pcg_minb == 3)
+                    if (pcg_z)
+                        MPL_CUDA(launch_pdl(k_pcg_update1w<T, PCG_E, 2, true>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD,
+                                            p, Hp, x, r, own_w, slots, sc));
+                    else if (pcg_warp_map && pcg_minb == 3)
                         MPL_CUDA(launch_pdl(k_pcg_update1w<T, PCG_E, 3>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p,
                                             Hp, x, r, own_w, slots, sc));
                     else if (pcg_warp_map && pcg_minb == 4)
@@ -1802,7 +1825,10 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     ctx->launches++;
                     MPL_CHECK(allreduce_d(ctx, slots[jj + 1].rz, 2 * NSTRIPE));  // rz, rr of iteration jj+1
                     if (vec_events) cudaEventRecord(vev[nl - 1][1], st);
-                    if (pcg_warp_map && pcg_minb == 3)
+                    if (pcg_z)
+                        MPL_CUDA(launch_pdl(k_pcg_update2w<T, PCG_E, 2, true>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD,
+                                            r, p, x, slots, sc));
+                    else if (pcg_warp_map && pcg_minb == 3)
                         MPL_CUDA(launch_pdl(k_pcg_update2w<T, PCG_E, 3>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, r,
                                             p, x, slots, sc));
                     else if (pcg_warp_map && pcg_minb == 4)

@@ -41,6 +41,9 @@ CASES = [
     ({"MPL_P2Q_HI": "1"}, "mix_fp32"),       # the dense-bucket P2Q kernel (default only at >= 40 particles per cell)
     ({"MPL_P2Q_HI": "1"}, "mix_fp64"),
     ({"MPL_P2Q_HI": "1"}, "cfg1_fp32"),
+    # fp32 PCG vector kernels with the residual buffer holding r instead of the default z = D^-1 r
+    ({"MPL_PCG_Z": "0"}, "mix_fp32"),
+    ({"MPL_PCG_Z": "0"}, "psd_fp32"),
 ]
 
 
@@ -49,7 +52,7 @@ CASES = [
     "-".join(f"{k[4:].lower()}={v}" for k, v in e.items()) + f"-{s}" for e, s in CASES])  # noqa: E501
 def test_hvp_variant_parity(env, scene):
     e = dict(os.environ)
-    for k in ("MPL_HVP_KERNEL", "MPL_PCG_MAP", "MPL_PDL", "MPL_L2WIN", "MPL_PCG", "MPL_CG1_E", "MPL_P2Q", "MPL_SORT", "MPL_KC", "MPL_KC_MINB", "MPL_G2P", "MPL_P2Q_HI"):
+    for k in ("MPL_HVP_KERNEL", "MPL_PCG_MAP", "MPL_PDL", "MPL_L2WIN", "MPL_PCG", "MPL_CG1_E", "MPL_P2Q", "MPL_SORT", "MPL_KC", "MPL_KC_MINB", "MPL_G2P", "MPL_P2Q_HI", "MPL_PCG_Z"):
         e.pop(k, None)
     e.update(env)
     r = subprocess.run([sys.executable, "-m", "tests._hvp_variant_check", scene], cwd=ROOT, env=e,

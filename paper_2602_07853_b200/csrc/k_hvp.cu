@@ -57,10 +57,11 @@ template <> __device__ __forceinline__ void cp_async_real<double>(double *dst, c
 //     each in lane order, so a warp's 16-byte loads of one chunk are contiguous; the 90 tangent
 //     numbers of the next tile are loaded (L2 evict-first) as soon as the current tile's K dG is done;
 //   * the u halo (shared slot 5x + 26y + z: conflict-free 16-byte accesses for every quarter-warp)
-//     and the owned masses are cp.async double-buffered per warp; the 12 scatter passes are
-//     read-modify-writes of a per-warp force buffer in the same slot map, separated by __syncwarp
-//     only (each pass is injective over the lanes); then a node phase (4 nodes per lane) stores the
-//     27 tile-interior nodes and adds the others with one red.global.add.v4.f32 each.
+//     and the owned masses are cp.async double-buffered per warp; the 12 corner-plane passes into a
+//     per-warp force buffer in the same slot map run as 8 groups separated by __syncwarp only (each pass
+//     is injective over the lanes, passes of different z parity never meet; the first group stores the
+//     64 owned nodes, the others read-modify-write); then a node phase (4 nodes per lane) stores the 27
+//     tile-interior nodes and adds the others with one red.global.add.v4.f32 each.
 // ---------------------------------------------------------------------------------------------
 constexpr int WZ_W = 4;  // independent warps per CTA
 struct WzWarp {
@@ -414,23 +415,46 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
                 const float f1 = PB[3 * a] + PB[3 * a + 1], f2 = PB[3 * a] - PB[3 * a + 1], y = PB[3 * a + 2];
                 gB[a][0] = f1 + y; gB[a][1] = f1 - y; gB[a][2] = f2 + y; gB[a][3] = f2 - y;
             }
+            auto cf = [&](int ox, int oy, int q) -> f4 {  // this lane's force on node (ox, oy, plane q)
+                f4 f = mk4<float>(0.f, 0.f, 0.f, 0.f);
+                if (q < 2) { f.x = corner(gA[0], ox, oy, q); f.y = corner(gA[1], ox, oy, q); f.z = corner(gA[2], ox, oy, q); }
+                if (q > 0) {
+                    f.x += corner(gB[0], ox, oy, q - 1); f.y += corner(gB[1], ox, oy, q - 1);
+                    f.z += corner(gB[2], ox, oy, q - 1);
+                }
+                return f;
+            };
+            {
+                // 8 groups: node z = 2 zp + q, so passes of different q parity never meet the same node; a
+                // group pairs an even-q pass with an odd-q pass (two independent read-modify-writes), and
+                // the first group (ox, oy) = (0, 0), q = 0, 1 covers the 64 nodes x, y, z < 4 exactly once:
+                // plain stores (those nodes are not zeroed by the node phase)
+                {
+                    const f4 f0 = cf(0, 0, 0), f1 = cf(0, 0, 1);
+                    S.F[hb] = f0;
+                    S.F[hb + 1] = f1;
+                    __syncwarp();
+                }
 #pragma unroll
-            for (int ox = 0; ox < 2; ox++)
-#pragma unroll
-                for (int oy = 0; oy < 2; oy++)
-#pragma unroll
-                    for (int q = 0; q < 3; q++) {
-                        f4 f = mk4<float>(0.f, 0.f, 0.f, 0.f);
-                        if (q < 2) { f.x = corner(gA[0], ox, oy, q); f.y = corner(gA[1], ox, oy, q); f.z = corner(gA[2], ox, oy, q); }
-                        if (q > 0) {
-                            f.x += corner(gB[0], ox, oy, q - 1); f.y += corner(gB[1], ox, oy, q - 1);
-                            f.z += corner(gB[2], ox, oy, q - 1);
-                        }
-                        f4 *fp = &S.F[hb + 5 * ox + 26 * oy + q];
-                        const f4 o = *fp;
-                        *fp = mk4<float>(o.x + f.x, o.y + f.y, o.z + f.z, 0.f);
-                        __syncwarp();
+                for (int g = 0; g < 7; g++) {
+                    // even passes after (0,0,0): (0,0,2) (0,1,0) (0,1,2) (1,0,0) (1,0,2) (1,1,0) (1,1,2);
+                    // odd passes (0,1,1) (1,0,1) (1,1,1) with the first three groups that start a new (ox, oy)
+                    const int e = g + 1, eox = e >> 2, eoy = (e >> 1) & 1, eq = (e & 1) * 2;
+                    f4 *fe = &S.F[hb + 5 * eox + 26 * eoy + eq];
+                    const f4 fe_ = cf(eox, eoy, eq);
+                    if ((g & 1) == 1) {  // g = 1, 3, 5: odd pass (ox, oy) = e's
+                        f4 *fo = &S.F[hb + 5 * eox + 26 * eoy + 1];
+                        const f4 fo_ = cf(eox, eoy, 1);
+                        const f4 a = *fe, b = *fo;
+                        *fe = mk4<float>(a.x + fe_.x, a.y + fe_.y, a.z + fe_.z, 0.f);
+                        *fo = mk4<float>(b.x + fo_.x, b.y + fo_.y, b.z + fo_.z, 0.f);
+                    } else {
+                        const f4 a = *fe;
+                        *fe = mk4<float>(a.x + fe_.x, a.y + fe_.y, a.z + fe_.z, 0.f);
                     }
+                    __syncwarp();
+                }
+            }
         }
         // ---- node phase: forces + lumped mass term, stored (interior) or added atomically (faces)
         int tt[4];
@@ -444,7 +468,7 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
             f4 f = mk4<float>(0.f, 0.f, 0.f, 0.f);
             if (cur.has) {
                 f = S.F[h];
-                S.F[h] = mk4<float>(0.f, 0.f, 0.f, 0.f);
+                if (!owned) S.F[h] = mk4<float>(0.f, 0.f, 0.f, 0.f);  // owned nodes: stored by the scatter
             }
             if (!(cur.has || owned) || tt[r] < 0) continue;
             if (owned) {

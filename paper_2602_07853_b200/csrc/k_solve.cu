@@ -1595,7 +1595,11 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm_, cudaDevAttrMultiProcessorCount, dev);
     }
-    const unsigned VAP = std::min<unsigned>(VA1, (unsigned)nsm_ * 8);  // persistent update kernels
+    // persistent update kernels: MPL_PCG_CPS CTAs per SM; the fp32 warp-map kernels default to the 2 that
+    // are resident (one wave; cfg4 vector kernels 22.1 -> 21.3 ms per step against 8 = four waves)
+    const char *cpse = getenv("MPL_PCG_CPS");
+    const int cps = cpse ? atoi(cpse) : (sizeof(T) == 4 && pcg_warp_map && pcg_minb == 2) ? 2 : 8;
+    const unsigned VAP = std::min<unsigned>(VA1, (unsigned)nsm_ * cps);
     const int *list = (const int *)ctx->n_list.p;
     // L2 persisting access-policy window for the Newton solve over p (MPL_L2WIN=p, default: the HVP's
     // gathered input, read by update2), Hp (=h: the HVP's atomics target) or both at half hit ratio

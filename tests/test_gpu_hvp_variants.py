@@ -44,6 +44,7 @@ CASES = [
     # fp32 PCG vector kernels with the residual buffer holding r instead of the default z = D^-1 r
     ({"MPL_PCG_Z": "0"}, "mix_fp32"),
     ({"MPL_PCG_Z": "0"}, "psd_fp32"),
+    ({"MPL_PCG_CPS": "8"}, "mix_fp32"),      # four waves of update CTAs instead of the one resident wave
 ]
 
 
@@ -52,6 +53,8 @@ CASES = [
     "-".join(f"{k[4:].lower()}={v}" for k, v in e.items()) + f"-{s}" for e, s in CASES])  # noqa: E501
 def test_hvp_variant_parity(env, scene):
     e = dict(os.environ)
+    for k in ("MPL_HVP_KERNEL", "MPL_PCG_MAP", "MPL_PDL", "MPL_L2WIN", "MPL_PCG", "MPL_CG1_E", "MPL_P2Q", "MPL_SORT",
+              "MPL_KC", "MPL_KC_MINB", "MPL_G2P", "MPL_P2Q_HI", "MPL_PCG_Z", "MPL_PCG_CPS"):
         e.pop(k, None)
     e.update(env)
     r = subprocess.run([sys.executable, "-m", "tests._hvp_variant_check", scene], cwd=ROOT, env=e,

@@ -301,15 +301,19 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
     // tile t: u halo + owned masses -> shared buffer b (cp.async, one group)
     auto halo = [&](int t, int b, int meta) {
         const int has = __shfl_sync(FULL, meta, 9);
+        // node-phase nodes n = lane + 32 r: r < 2 are the tile's own 64 nodes (X, Y, Z < 4: owned, the
+        // tile itself, tt >= 0), r >= 2 the 61 face nodes of neighbour tiles
         int tt[4];
+        tt[0] = tt[1] = __shfl_sync(FULL, meta, 0);
 #pragma unroll
-        for (int r = 0; r < 4; r++) tt[r] = __shfl_sync(FULL, meta, role[r] < 0 ? 0 : (role[r] >> 6) & 7);
+        for (int r = 2; r < 4; r++) tt[r] = __shfl_sync(FULL, meta, role[r] < 0 ? 0 : (role[r] >> 6) & 7);
         if (t < N) {
 #pragma unroll
             for (int r = 0; r < 4; r++) {
                 if (role[r] < 0) continue;
-                const int loc = role[r] & 63, owned = (role[r] >> 9) & 1, h = role[r] >> 11;
-                if ((has || owned) && tt[r] >= 0) {
+                const int loc = role[r] & 63, h = role[r] >> 11;
+                const bool owned = r < 2;
+                if (owned || (has && tt[r] >= 0)) {
                     const int64_t nd = (int64_t)tt[r] * 64 + loc;
                     cp_async16(&S.uh[b][h], u + nd);
                     if (owned) cp_async4(&S.mh[b][loc], nmass + nd);
@@ -458,19 +462,20 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
         }
         // ---- node phase: forces + lumped mass term, stored (interior) or added atomically (faces)
         int tt[4];
+        tt[0] = tt[1] = __shfl_sync(FULL, mcur, 0);
 #pragma unroll
-        for (int r = 0; r < 4; r++) tt[r] = __shfl_sync(FULL, mcur, role[r] < 0 ? 0 : (role[r] >> 6) & 7);
+        for (int r = 2; r < 4; r++) tt[r] = __shfl_sync(FULL, mcur, role[r] < 0 ? 0 : (role[r] >> 6) & 7);
 #pragma unroll
         for (int r = 0; r < 4; r++) {
             if (role[r] < 0) continue;
-            const int loc = role[r] & 63, owned = (role[r] >> 9) & 1, interior = (role[r] >> 10) & 1,
-                      h = role[r] >> 11;
+            const bool owned = r < 2;  // (see halo)
+            const int loc = role[r] & 63, interior = owned ? (role[r] >> 10) & 1 : 0, h = role[r] >> 11;
             f4 f = mk4<float>(0.f, 0.f, 0.f, 0.f);
             if (cur.has) {
                 f = S.F[h];
                 if (!owned) S.F[h] = mk4<float>(0.f, 0.f, 0.f, 0.f);  // owned nodes: stored by the scatter
             }
-            if (!(cur.has || owned) || tt[r] < 0) continue;
+            if (!owned && (!cur.has || tt[r] < 0)) continue;
             if (owned) {
                 const float mm = S.mh[b][loc];
                 if (mm > 0.f) {

@@ -43,6 +43,26 @@ __device__ __forceinline__ void cp_async4(void *dst, const void *src) {
 __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16s(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4s(uint32_t dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ f4 lds4(uint32_t a) {
+    f4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lds1(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts4z(uint32_t a) {
+    asm volatile("st.shared.v4.f32 [%0], {%1,%1,%1,%1};" ::"r"(a), "f"(0.f) : "memory");
+}
+__device__ __forceinline__ void sts1z(uint32_t a) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(0.f) : "memory"); }
 template <class T> __device__ __forceinline__ void cp_async_real(T *dst, const T *src);
 template <> __device__ __forceinline__ void cp_async_real<float>(float *dst, const float *src) { cp_async4(dst, src); }
 template <> __device__ __forceinline__ void cp_async_real<double>(double *dst, const double *src) { cp_async8(dst, src); }
@@ -298,29 +318,33 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
             k[off + 44] = ldg_stream1(p + q.e44 - (off ? 3 * q.d44 : 0), pol);
         }
     };
-    // tile t: u halo + owned masses -> shared buffer b (cp.async, one group)
+    // shared addresses: this warp's halo / mass buffers (buffer b at + b UHB / + b MHB) and force buffer
+    const uint32_t s_uh = smem_u32(&S.uh[0][0]), s_mh = smem_u32(&S.mh[0][0]), s_F = smem_u32(&S.F[0]);
+    constexpr uint32_t UHB = 132 * 16, MHB = 64 * 4;
+    // tile t: u halo + owned masses -> shared buffer b (cp.async, one group).  Node-phase nodes
+    // n = lane + 32 r: r < 2 are the tile's own 64 nodes (X, Y, Z < 4: owned, the tile itself), r >= 2 the
+    // 61 face nodes of neighbour tiles
     auto halo = [&](int t, int b, int meta) {
-        const int has = __shfl_sync(FULL, meta, 9);
-        // node-phase nodes n = lane + 32 r: r < 2 are the tile's own 64 nodes (X, Y, Z < 4: owned, the
-        // tile itself, tt >= 0), r >= 2 the 61 face nodes of neighbour tiles
+        const int has = __shfl_sync(FULL, meta, 9), ts = __shfl_sync(FULL, meta, 0);
         int tt[4];
-        tt[0] = tt[1] = __shfl_sync(FULL, meta, 0);
 #pragma unroll
         for (int r = 2; r < 4; r++) tt[r] = __shfl_sync(FULL, meta, role[r] < 0 ? 0 : (role[r] >> 6) & 7);
         if (t < N) {
+            const uint32_t bu = s_uh + (uint32_t)b * UHB, bm = s_mh + (uint32_t)b * MHB;
+            const f4 *ut = u + (int64_t)ts * 64;
+            const float *mt = nmass + (int64_t)ts * 64;
 #pragma unroll
-            for (int r = 0; r < 4; r++) {
+            for (int r = 0; r < 2; r++) {
+                const int loc = role[r] & 63, h = role[r] >> 11;
+                cp_async16s(bu + 16u * h, ut + loc);
+                cp_async4s(bm + 4u * loc, mt + loc);
+            }
+#pragma unroll
+            for (int r = 2; r < 4; r++) {
                 if (role[r] < 0) continue;
                 const int loc = role[r] & 63, h = role[r] >> 11;
-                const bool owned = r < 2;
-                if (owned || (has && tt[r] >= 0)) {
-                    const int64_t nd = (int64_t)tt[r] * 64 + loc;
-                    cp_async16(&S.uh[b][h], u + nd);
-                    if (owned) cp_async4(&S.mh[b][loc], nmass + nd);
-                } else {
-                    S.uh[b][h] = mk4<float>(0.f, 0.f, 0.f, 0.f);
-                    if (owned) S.mh[b][loc] = 0.f;
-                }
+                if (has && tt[r] >= 0) cp_async16s(bu + 16u * h, u + ((int64_t)tt[r] * 64 + loc));
+                else sts4z(bu + 16u * h);
             }
         }
         cp_async_commit();
@@ -461,32 +485,38 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
             }
         }
         // ---- node phase: forces + lumped mass term, stored (interior) or added atomically (faces)
-        int tt[4];
-        tt[0] = tt[1] = __shfl_sync(FULL, mcur, 0);
+        {
+            const uint32_t bu = s_uh + (uint32_t)b * UHB, bm = s_mh + (uint32_t)b * MHB;
+            const int ts = __shfl_sync(FULL, mcur, 0);
+            f4 *Ht = Hu + (int64_t)ts * 64;
+            float am = 0.f;  // sum of m |u|^2 over this lane's owned nodes
 #pragma unroll
-        for (int r = 2; r < 4; r++) tt[r] = __shfl_sync(FULL, mcur, role[r] < 0 ? 0 : (role[r] >> 6) & 7);
-#pragma unroll
-        for (int r = 0; r < 4; r++) {
-            if (role[r] < 0) continue;
-            const bool owned = r < 2;  // (see halo)
-            const int loc = role[r] & 63, interior = owned ? (role[r] >> 10) & 1 : 0, h = role[r] >> 11;
-            f4 f = mk4<float>(0.f, 0.f, 0.f, 0.f);
-            if (cur.has) {
-                f = S.F[h];
-                if (!owned) S.F[h] = mk4<float>(0.f, 0.f, 0.f, 0.f);  // owned nodes: stored by the scatter
+            for (int r = 0; r < 2; r++) {  // the tile's own nodes: scatter stored them; plus m_i u_i
+                const int loc = role[r] & 63, h = role[r] >> 11;
+                f4 f = mk4<float>(0.f, 0.f, 0.f, 0.f);
+                if (cur.has) f = lds4(s_F + 16u * h);
+                const float mm = lds1(bm + 4u * loc);
+                const f4 w = lds4(bu + 16u * h);
+                f.x = fmaf(mm, w.x, f.x); f.y = fmaf(mm, w.y, f.y); f.z = fmaf(mm, w.z, f.z);
+                am = fmaf(mm, fmaf(w.x, w.x, fmaf(w.y, w.y, w.z * w.z)), am);
+                if ((role[r] >> 10) & 1) Ht[loc] = mk4<float>(f.x, f.y, f.z, 0.f);
+                else if (f.x != 0.f || f.y != 0.f || f.z != 0.f) atomic_add3<float>(Ht + loc, f.x, f.y, f.z);
             }
-            if (!owned && (!cur.has || tt[r] < 0)) continue;
-            if (owned) {
-                const float mm = S.mh[b][loc];
-                if (mm > 0.f) {
-                    const f4 w = uh[h];
-                    f.x += mm * w.x; f.y += mm * w.y; f.z += mm * w.z;
-                    acc += (double)(mm * (w.x * w.x + w.y * w.y + w.z * w.z));
+            acc += (double)am;
+            if (cur.has) {
+                int tt[4];
+#pragma unroll
+                for (int r = 2; r < 4; r++) tt[r] = __shfl_sync(FULL, mcur, role[r] < 0 ? 0 : (role[r] >> 6) & 7);
+#pragma unroll
+                for (int r = 2; r < 4; r++) {  // face nodes of the neighbour tiles: added atomically
+                    if (role[r] < 0) continue;
+                    const int loc = role[r] & 63, h = role[r] >> 11;
+                    const f4 f = lds4(s_F + 16u * h);
+                    sts4z(s_F + 16u * h);
+                    if (tt[r] >= 0 && (f.x != 0.f || f.y != 0.f || f.z != 0.f))
+                        atomic_add3<float>(Hu + ((int64_t)tt[r] * 64 + loc), f.x, f.y, f.z);
                 }
             }
-            const int64_t nd = (int64_t)tt[r] * 64 + loc;
-            if (interior) Hu[nd] = mk4<float>(f.x, f.y, f.z, 0.f);
-            else if (f.x != 0.f || f.y != 0.f || f.z != 0.f) atomic_add3<float>(Hu + nd, f.x, f.y, f.z);
         }
         __syncwarp();  // node phase done reading uh[b] / mh[b] before they are refilled
         mcur = mnext;
@@ -861,14 +891,15 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
     if (tlist && (sizeof(T) == 8 || hvp_variant() == 1)) return MPL_ERR_UNSUPPORTED;  // tile lists: k_hvp_wz only
     if (sizeof(T) == 8) return launch_wh<T, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);  // 45 doubles per lane
     if (hvp_variant() == 1) return launch_wh<T, 5>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
-    if (ctx->kc_now) {  // compressed tangent; MPL_KC_MINB: CTAs per SM requested from ptxas (4: 128 registers,
-                        // 44 B spilled; 3: 148 registers — cfg4 in-step 84.1 vs 85.0 us)
+    if (ctx->kc_now) {  // compressed tangent; MPL_KC_MINB: CTAs per SM requested from ptxas (3: 150 registers,
+                        // 12 warps per SM, the default — cfg4 72.4 us isolated / 76.9 in the solve; 4: 128
+                        // registers + 8 B spilled, 73.0 / 77.4; 5: 96 registers + 192 B spilled, 117 us)
         static int minb = -1;
         if (minb < 0) {
             const char *e = getenv("MPL_KC_MINB");
-            minb = e ? atoi(e) : 4;
+            minb = e ? atoi(e) : 3;
         }
-        if (tlist) return launch_wz<true, 4, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
+        if (tlist) return launch_wz<true, 3, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
         if (minb == 3) return launch_wz<true, 3, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
         return launch_wz<true, 4, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
     }

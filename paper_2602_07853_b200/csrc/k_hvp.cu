@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
         cp_async_wait<0>();
         __syncwarp();
         const f4 *uh = S.uh[b];
-        float PA[9], PB[9];
+        float2 P2[9];  // (cell A, cell B) pairs
         if (cur.has) {
             // ---- dG of cells A and B from the 12 nodes (ox, oy) x z-plane q = 0, 1, 2
             float Dx[3][3], Dy[3][3], Sz[3][3];  // [plane][component]
@@ -387,14 +387,13 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
                 dA[3 * a] = Dx[0][a] + Dx[1][a]; dA[3 * a + 1] = Dy[0][a] + Dy[1][a]; dA[3 * a + 2] = Sz[1][a] - Sz[0][a];
                 dB[3 * a] = Dx[1][a] + Dx[2][a]; dB[3 * a + 1] = Dy[1][a] + Dy[2][a]; dB[3 * a + 2] = Sz[2][a] - Sz[1][a];
             }
+            float2 d2[9];
+#pragma unroll
+            for (int r = 0; r < 9; r++) d2[r] = make_float2(dA[r], dB[r]);
             if (KC) {
-                float2 d2[9], P2[9];
-#pragma unroll
-                for (int r = 0; r < 9; r++) d2[r] = make_float2(dA[r], dB[r]);
                 kc_apply2(k, d2, P2);
-#pragma unroll
-                for (int r = 0; r < 9; r++) { PA[r] = P2[r].x; PB[r] = P2[r].y; }
             } else {
+            float PA[9], PB[9];
             // ---- P = K dG (symmetric, packed upper triangle), element by element
 #pragma unroll
             for (int r = 0; r < 9; r++) { PA[r] = 0.f; PB[r] = 0.f; }
@@ -410,15 +409,17 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
                 PB[r] += k[45 + e] * dB[c];
                 if (c != r) PB[c] += k[45 + e] * dB[r];
             }
+#pragma unroll
+            for (int r = 0; r < 9; r++) P2[r] = make_float2(PA[r], PB[r]);
             }
-            float qf = 0.f;
+            float2 q2 = f2(0.f, 0.f);
 #pragma unroll
             for (int r = 0; r < 9; r++) {
-                PA[r] = cur.pA ? PA[r] : 0.f;  // absent cells: k holds stale numbers
-                PB[r] = cur.pB ? PB[r] : 0.f;
-                qf += PA[r] * dA[r] + PB[r] * dB[r];
+                P2[r].x = cur.pA ? P2[r].x : 0.f;  // absent cells: k holds stale numbers
+                P2[r].y = cur.pB ? P2[r].y : 0.f;
+                q2 = fma2(P2[r], d2[r], q2);
             }
-            acc += (double)qf;
+            acc += (double)(q2.x + q2.y);
         }
         // k is free: start the next tile's loads; they overlap the scatter and the node phase (issuing the
         // second half after the scatter measured slower: 87.3 vs 86.2 us at cfg4)
@@ -437,18 +438,23 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
         if (cur.has) {
             float gA[3][4], gB[3][4];
 #pragma unroll
-            for (int a = 0; a < 3; a++) {
-                const float e1 = PA[3 * a] + PA[3 * a + 1], e2 = PA[3 * a] - PA[3 * a + 1], z = PA[3 * a + 2];
-                gA[a][0] = e1 + z; gA[a][1] = e1 - z; gA[a][2] = e2 + z; gA[a][3] = e2 - z;
-                const float f1 = PB[3 * a] + PB[3 * a + 1], f2 = PB[3 * a] - PB[3 * a + 1], y = PB[3 * a + 2];
-                gB[a][0] = f1 + y; gB[a][1] = f1 - y; gB[a][2] = f2 + y; gB[a][3] = f2 - y;
+            for (int a = 0; a < 3; a++) {  // both cells at once (paired adds)
+                const float2 e1 = add2(P2[3 * a], P2[3 * a + 1]), e2 = sub2(P2[3 * a], P2[3 * a + 1]), z = P2[3 * a + 2];
+                const float2 g0 = add2(e1, z), g1 = sub2(e1, z), g2 = add2(e2, z), g3 = sub2(e2, z);
+                gA[a][0] = g0.x; gA[a][1] = g1.x; gA[a][2] = g2.x; gA[a][3] = g3.x;
+                gB[a][0] = g0.y; gB[a][1] = g1.y; gB[a][2] = g2.y; gB[a][3] = g3.y;
             }
             auto cf = [&](int ox, int oy, int q) -> f4 {  // this lane's force on node (ox, oy, plane q)
-                f4 f = mk4<float>(0.f, 0.f, 0.f, 0.f);
-                if (q < 2) { f.x = corner(gA[0], ox, oy, q); f.y = corner(gA[1], ox, oy, q); f.z = corner(gA[2], ox, oy, q); }
-                if (q > 0) {
-                    f.x += corner(gB[0], ox, oy, q - 1); f.y += corner(gB[1], ox, oy, q - 1);
-                    f.z += corner(gB[2], ox, oy, q - 1);
+                f4 f;
+                f.w = 0.f;
+                if (q == 0) {
+                    f.x = corner(gA[0], ox, oy, 0); f.y = corner(gA[1], ox, oy, 0); f.z = corner(gA[2], ox, oy, 0);
+                } else if (q == 2) {
+                    f.x = corner(gB[0], ox, oy, 1); f.y = corner(gB[1], ox, oy, 1); f.z = corner(gB[2], ox, oy, 1);
+                } else {
+                    f.x = corner(gA[0], ox, oy, 1) + corner(gB[0], ox, oy, 0);
+                    f.y = corner(gA[1], ox, oy, 1) + corner(gB[1], ox, oy, 0);
+                    f.z = corner(gA[2], ox, oy, 1) + corner(gB[2], ox, oy, 0);
                 }
                 return f;
             };

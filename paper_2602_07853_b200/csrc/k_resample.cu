@@ -105,6 +105,7 @@ __global__ void k_tile_nbrs(GridP g, int T, const int *__restrict__ coord, const
 __global__ void k_count(GridP g, int64_t np, const int *__restrict__ base, const int *__restrict__ tile_of,
                         int *__restrict__ key, int *__restrict__ rank, int *__restrict__ bcount) {
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const unsigned act = __ballot_sync(0xffffffffu, p < np);
     if (p >= np) return;
     int b = base[p];
     int bx = b >> 20, by = (b >> 10) & 1023, bz = b & 1023;
@@ -112,7 +113,14 @@ __global__ void k_count(GridP g, int64_t np, const int *__restrict__ base, const
     DASSERT(t >= 0 && b >= 0);
     int k = t * 64 + local_id(bx & 3, by & 3, bz & 3);
     key[p] = k;
-    rank[p] = atomicAdd(&bcount[k], 1);
+    // warp-aggregated: the lanes of one bucket (particles arrive sorted by the previous step's buckets, so
+    // runs are long at high PPC) take one atomic for the run and ranks in lane order
+    const unsigned peers = __match_any_sync(act, k);
+    const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+    int r0 = 0;
+    if (lane == leader) r0 = atomicAdd(&bcount[k], __popc(peers));
+    r0 = __shfl_sync(peers, r0, leader);
+    rank[p] = r0 + __popc(peers & ((1u << lane) - 1u));
 }
 
 // ---- Kirchhoff stress of a particle, StVK-Hencky ------------------------

@@ -230,15 +230,21 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
              const int *__restrict__ hascells, const float *__restrict__ K, const int *__restrict__ kstart,
              const float *__restrict__ nmass, const f4 *__restrict__ u, f4 *__restrict__ Hu, double *__restrict__ uHu,
              const CGSlot *__restrict__ cgs, int cgj, double cgthr, const DevScalars *__restrict__ sc,
-             const int *__restrict__ tlist, int ntl) {
+             const int *__restrict__ tlist, int ntl, const int *__restrict__ jdev) {
     // items: tiles 0..T_-1, or the listed tiles tlist[0..ntl) (slab ranks: the interface tiles first, so
-    // their halo exchange overlaps the interior tiles' launch)
+    // their halo exchange overlaps the interior tiles' launch).  jdev (graph-captured PCG): the
+    // iteration index, its p.Hp slot and the threshold come from device memory
     const int N = LIST ? ntl : T_;
     __shared__ WzWarp SW[WZ_W];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WzWarp &S = SW[wid];
     pdl_trigger();
     pdl_wait();
+    if (jdev != nullptr) {
+        cgj = *jdev;
+        uHu = const_cast<double *>(cgs[cgj].pHp);
+        cgthr = sc->cg_thr;
+    }
     if (cgs != nullptr) {  // inside PCG: nothing to do once converged / stopped at negative curvature
         const double rr = warp_sum(cgs[cgj].rr[lane]);
         if (sc->neg_curv || (cgj > 0 && rr <= cgthr)) return;
@@ -812,7 +818,7 @@ int g_num_sms = 0;
 
 template <bool KC, int MINB, bool LIST>
 mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
-                     double cgthr, const int *tlist, int ntl) {
+                     double cgthr, const int *tlist, int ntl, const int *jdev = nullptr) {
     static int per_sm = 0;
     if (per_sm == 0) {
         int dev = 0;
@@ -832,7 +838,7 @@ mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
                         (const float *)ctx->K.p, (const int *)(KC ? ctx->t_kstart2.p : ctx->t_kstart.p),
                         (const float *)owned_mass(ctx),
                         (const f4 *)u_tile, (f4 *)Hu_tile, uHu, cgs, cgj, cgthr, (const DevScalars *)ctx->scalars.p,
-                        tlist, ntl));
+                        tlist, ntl, jdev));
     ctx->launches++;
     return MPL_OK;
 }
@@ -892,8 +898,12 @@ int hvp_kz_layout(int precision) {
 // Hu (tile-dense) must be zero on every node that receives atomics (all non-interior nodes).
 template <class T>
 mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
-                      double cgthr, const int *tlist, int ntl) {
+                      double cgthr, const int *tlist, int ntl, const int *jdev) {
     if (ctx->T == 0) return MPL_OK;
+    if (jdev) {  // graph-captured PCG: fp32 compressed-tangent k_hvp_wz only
+        if (sizeof(T) == 8 || hvp_variant() == 1 || !ctx->kc_now || tlist) return MPL_ERR_UNSUPPORTED;
+        return launch_wz<true, 3, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0, jdev);
+    }
     if (tlist && (sizeof(T) == 8 || hvp_variant() == 1)) return MPL_ERR_UNSUPPORTED;  // tile lists: k_hvp_wz only
     if (sizeof(T) == 8) return launch_wh<T, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);  // 45 doubles per lane
     if (hvp_variant() == 1) return launch_wh<T, 5>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
@@ -914,6 +924,6 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
 }
 
 template mpl_status launch_hvp<float>(mpl_ctx, const void *, void *, double *, const CGSlot *, int, double,
-                                      const int *, int);
+                                      const int *, int, const int *);
 template mpl_status launch_hvp<double>(mpl_ctx, const void *, void *, double *, const CGSlot *, int, double,
-                                       const int *, int);
+                                       const int *, int, const int *);

@@ -1066,9 +1066,13 @@ __global__ void __launch_bounds__(256, MB) k_pcg_update1w(int64_t n, int64_t S, 
                                                          const vec4<T> *__restrict__ p, vec4<T> *__restrict__ Hp,
                                                          T *__restrict__ x, T *__restrict__ r,
                                                          const uint8_t *__restrict__ own, CGSlot *slot,
-                                                         DevScalars *sc) {
+                                                         DevScalars *sc, const int *__restrict__ jdev = nullptr) {
     pdl_trigger();
     pdl_wait();
+    if (jdev) {  // graph-captured PCG: iteration index and threshold from device memory
+        j = *jdev;
+        thr = sc->cg_thr;
+    }
     const CGScal cs = cg_scalars(slot, j, false);
     const int done = sc->cg_done_iter;
     if ((done >= 0 && done <= j) || (j > 0 && cs.rr <= thr)) return;
@@ -1146,9 +1150,16 @@ template <class T, int E = PCG_E, int MB = 2, bool ZF = false>
 __global__ void __launch_bounds__(256, MB) k_pcg_update2w(int64_t n, int64_t S, const int *__restrict__ list, int j,
                                                          double thr, const T *__restrict__ invD,
                                                          const T *__restrict__ r, vec4<T> *__restrict__ p,
-                                                         T *__restrict__ x, const CGSlot *slot, const DevScalars *sc) {
+                                                         T *__restrict__ x, const CGSlot *slot, const DevScalars *sc,
+                                                         const int *__restrict__ jdev = nullptr,
+                                                         int *__restrict__ jout = nullptr) {
     pdl_trigger();
     pdl_wait();
+    if (jdev) {  // graph-captured PCG: this iteration's index; the next iteration's kernels read jout
+        j = *jdev;
+        thr = sc->cg_thr;
+        if (blockIdx.x == 0 && threadIdx.x == 0) *jout = j + 1;
+    }
     const CGScal cs = cg_scalars(slot, j, true);
     const int done = sc->cg_done_iter;
     if ((done >= 0 && done <= j + 1) || (j > 0 && cs.rr <= thr)) return;
@@ -1339,6 +1350,13 @@ __global__ void k_axpy_compact(int64_t n, int64_t S, const int *__restrict__ lis
 }
 
 // HVP wrapper used inside PCG: skips work once converged
+// graph-captured PCG: iteration counter and threshold of a Newton iteration's solve
+__global__ void k_set_cg(DevScalars *sc, double thr) {
+    sc->cg_j[0] = 0;
+    sc->cg_j[1] = 0;
+    sc->cg_thr = thr;
+}
+
 template <class T>
 __global__ void k_zero4(int64_t N, vec4<T> *a) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
@@ -1510,7 +1528,7 @@ mpl_status energy_at(mpl_ctx ctx, const void *v_tile, double *phi) {
 }
 }  // namespace
 
-constexpr int HVP_SAMPLE = 4;
+constexpr int HVP_SAMPLE = 16;  // every 16th HVP bracketed by events (each pair ~6 us and a broken PDL overlap)
 
 template <class T>
 mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *out) {
@@ -1586,6 +1604,20 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     // cfg4: update2 10.75 -> 9.43 ms, update1 12.15 -> 12.55 ms per step (the divisions), step 54.5 -> 53.7 ms
     const char *pze = getenv("MPL_PCG_Z");
     const bool pcg_z = !cg1 && sizeof(T) == 4 && pcg_warp_map && pcg_minb == 2 && !(pze && pze[0] == '0');
+    // MPL_PCG_GRAPH=1 (one GPU, fp32 compressed tangent, classic z-form PCG): two PCG iterations (HVP,
+    // update1, update2 each, with their programmatic-launch edges) captured once per step into a CUDA graph
+    // and replayed; the kernels read the iteration index and threshold from device memory, update2
+    // advancing it (no per-iteration launch arguments), and the convergence test stays on the device.
+    // Not the default: the HVP sampling events of the bench need the stream path.
+    const char *pge = getenv("MPL_PCG_GRAPH");
+    const bool pcg_graph = pge && pge[0] == '1' && pcg_z && !multi(ctx) && ctx->kc_now && hvp_variant() == 0;
+    cudaGraphExec_t pcg_gexec = nullptr;
+    struct GraphGuard {
+        cudaGraphExec_t *g;
+        ~GraphGuard() {
+            if (*g) cudaGraphExecDestroy(*g);
+        }
+    } pcg_gguard{&pcg_gexec};
     const unsigned VG = vgrid(NT);
     const unsigned VA = vgrid(NA);
     const unsigned VA1 = nblk(NA > 0 ? NA : 1, 256);
@@ -1715,12 +1747,47 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         const double thr = cfg->fixed_cg_iters ? -1.0 : cfg->cg_rtol * cfg->cg_rtol * rr0;
         int launched = 0, its = 0;
         cudaEventRecord(e0, st);
+        if (pcg_graph && rr0 > 0.0 && itmax > 0) {
+            k_set_cg<<<1, 1, 0, st>>>(sc, thr);
+            ctx->launches++;
+            if (!pcg_gexec) {  // capture two iterations (even: reads cg_j[0], writes cg_j[1]; odd: back)
+                cudaGraph_t gr = nullptr;
+                MPL_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+                mpl_status cs_ = MPL_OK;
+                for (int par = 0; par < 2 && cs_ == MPL_OK; par++) {
+                    const int *jin = &sc->cg_j[par];
+                    int *jo = &sc->cg_j[par ^ 1];
+                    cs_ = launch_hvp<T>(ctx, p, Hp, nullptr, slots, 0, thr, nullptr, 0, jin);
+                    if (cs_ == MPL_OK &&
+                        launch_pdl(k_pcg_update1w<T, PCG_E, 2, true>, VAP, 256, 0, st, NA, SA, list, 0, thr, invD, p,
+                                   Hp, x, r, own_w, slots, sc, jin) != cudaSuccess)
+                        cs_ = MPL_ERR_CUDA;
+                    if (cs_ == MPL_OK &&
+                        launch_pdl(k_pcg_update2w<T, PCG_E, 2, true>, VAP, 256, 0, st, NA, SA, list, 0, thr, invD, r,
+                                   p, x, slots, sc, jin, jo) != cudaSuccess)
+                        cs_ = MPL_ERR_CUDA;
+                }
+                const cudaError_t ce = cudaStreamEndCapture(st, &gr);
+                MPL_CHECK(cs_);
+                MPL_CUDA(ce);
+                const cudaError_t ie = cudaGraphInstantiate(&pcg_gexec, gr, 0);
+                cudaGraphDestroy(gr);
+                MPL_CUDA(ie);
+                ctx->launches -= 2;  // launch_hvp counted the captured HVPs
+            }
+        }
         if (rr0 > 0.0 && itmax > 0) {
             int chunk = 4;
             bool done = false;
             while (!done && launched < itmax) {
                 int n = std::min(chunk, itmax - launched);
-                for (int jj = launched; jj < launched + n; jj++) {
+                if (pcg_graph) {  // pairs of iterations by graph replay; an odd last iteration on the stream path
+                    n = std::min((chunk + 1) & ~1, itmax - launched);
+                    for (int q = 0; q < n / 2; q++) MPL_CUDA(cudaGraphLaunch(pcg_gexec, st));
+                    ctx->launches += 6 * (n / 2);
+                    nl += 2 * (n / 2);
+                }
+                for (int jj = launched + (pcg_graph ? 2 * (n / 2) : 0); jj < launched + n; jj++) {
                     if ((int)hev.size() <= nl) {
                         cudaEvent_t a, b;
                         cudaEventCreate(&a);
@@ -1813,16 +1880,16 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     if (vec_events) cudaEventRecord(vev[nl - 1][0], st);
                     if (pcg_z)
                         MPL_CUDA(launch_pdl(k_pcg_update1w<T, PCG_E, 2, true>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD,
-                                            p, Hp, x, r, own_w, slots, sc));
+                                            p, Hp, x, r, own_w, slots, sc, (const int *)nullptr));
                     else if (pcg_warp_map && pcg_minb == 3)
                         MPL_CUDA(launch_pdl(k_pcg_update1w<T, PCG_E, 3>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p,
-                                            Hp, x, r, own_w, slots, sc));
+                                            Hp, x, r, own_w, slots, sc, (const int *)nullptr));
                     else if (pcg_warp_map && pcg_minb == 4)
                         MPL_CUDA(launch_pdl(k_pcg_update1w<T, PCG_E, 4>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p,
-                                            Hp, x, r, own_w, slots, sc));
+                                            Hp, x, r, own_w, slots, sc, (const int *)nullptr));
                     else if (pcg_warp_map)
                         MPL_CUDA(launch_pdl(k_pcg_update1w<T>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p, Hp, x,
-                                            r, own_w, slots, sc));
+                                            r, own_w, slots, sc, (const int *)nullptr));
                     else
                         MPL_CUDA(launch_pdl(k_pcg_update1<T, PCG_U>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, p,
                                             Hp, x, r, own_w, slots, sc));
@@ -1831,16 +1898,16 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                     if (vec_events) cudaEventRecord(vev[nl - 1][1], st);
                     if (pcg_z)
                         MPL_CUDA(launch_pdl(k_pcg_update2w<T, PCG_E, 2, true>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD,
-                                            r, p, x, slots, sc));
+                                            r, p, x, slots, sc, (const int *)nullptr, (int *)nullptr));
                     else if (pcg_warp_map && pcg_minb == 3)
                         MPL_CUDA(launch_pdl(k_pcg_update2w<T, PCG_E, 3>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, r,
-                                            p, x, slots, sc));
+                                            p, x, slots, sc, (const int *)nullptr, (int *)nullptr));
                     else if (pcg_warp_map && pcg_minb == 4)
                         MPL_CUDA(launch_pdl(k_pcg_update2w<T, PCG_E, 4>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, r,
-                                            p, x, slots, sc));
+                                            p, x, slots, sc, (const int *)nullptr, (int *)nullptr));
                     else if (pcg_warp_map)
                         MPL_CUDA(launch_pdl(k_pcg_update2w<T>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, r, p, x,
-                                            slots, sc));
+                                            slots, sc, (const int *)nullptr, (int *)nullptr));
                     else
                         MPL_CUDA(launch_pdl(k_pcg_update2<T, PCG_U>, VAP, 256, 0, st, NA, SA, list, jj, thr, invD, r,
                                             p, x, slots, sc));

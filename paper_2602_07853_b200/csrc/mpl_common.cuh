@@ -394,7 +394,9 @@ struct DevScalars {
     int inv_particle;  // min index of an inverted particle
     int neg_curv;      // PCG breakdown (p.Hp <= 0)
     int cg_done_iter;  // first iteration index at which PCG converged (or -1)
-    int pad[2];
+    int cg_j[2];       // graph-captured PCG (MPL_PCG_GRAPH): iteration index read by the kernels of an even /
+                       // odd iteration, advanced on the device by its update2
+    double cg_thr;     // graph-captured PCG: the convergence threshold of the current Newton iteration
 };
 
 // Communicator between the slab ranks.  Every method is collective over the ranks and
@@ -697,7 +699,7 @@ template <class T> mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, in
 template <class T> mpl_status hvp_tile(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *pHp_accum);
 template <class T> mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu,
                                          const CGSlot *cgs, int cgj, double cgthr, const int *tlist = nullptr,
-                                         int ntl = 0);
+                                         int ntl = 0, const int *jdev = nullptr);
 template <class T> mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *st);
 template <class T> mpl_status g2p_impl(mpl_ctx ctx, double dt);
 template <class T> mpl_status sync_vg_order(mpl_ctx ctx);

@@ -45,6 +45,10 @@ CASES = [
     ({"MPL_PCG_Z": "0"}, "mix_fp32"),
     ({"MPL_PCG_Z": "0"}, "psd_fp32"),
     ({"MPL_PCG_CPS": "8"}, "mix_fp32"),      # four waves of update CTAs instead of the one resident wave
+    # two PCG iterations captured into a CUDA graph and replayed (device-side iteration index)
+    ({"MPL_PCG_GRAPH": "1"}, "cfg1_fp32"),
+    ({"MPL_PCG_GRAPH": "1"}, "cfg2s_fp32"),
+    ({"MPL_PCG_GRAPH": "1"}, "psd_fp32"),
 ]
 
 
@@ -54,7 +58,7 @@ CASES = [
 def test_hvp_variant_parity(env, scene):
     e = dict(os.environ)
     for k in ("MPL_HVP_KERNEL", "MPL_PCG_MAP", "MPL_PDL", "MPL_L2WIN", "MPL_PCG", "MPL_CG1_E", "MPL_P2Q", "MPL_SORT",
-              "MPL_KC", "MPL_KC_MINB", "MPL_G2P", "MPL_P2Q_HI", "MPL_PCG_Z", "MPL_PCG_CPS"):
+              "MPL_KC", "MPL_KC_MINB", "MPL_G2P", "MPL_P2Q_HI", "MPL_PCG_Z", "MPL_PCG_CPS", "MPL_PCG_GRAPH"):
         e.pop(k, None)
     e.update(env)
     r = subprocess.run([sys.executable, "-m", "tests._hvp_variant_check", scene], cwd=ROOT, env=e,

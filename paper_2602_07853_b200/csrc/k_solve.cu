@@ -1485,7 +1485,6 @@ mpl_status linearize_impl(mpl_ctx ctx, const void *v_tile, int mode, double *phi
         } else if (honly) {
             if (mode == LIN_ENERGY) k_linearize<T, LIN_ENERGY, true><<<T_, lt, 0, st>>>(LIN_ARGS);
             else if (mode == LIN_GRAD) k_linearize<T, LIN_GRAD, true><<<T_, lt, 0, st>>>(LIN_ARGS);
-            else if (lt == 64 && kc && lin_gen_minb == 8) k_linearize<T, LIN_FULL, true, 8, false, true><<<T_, lt, 0, st>>>(LIN_ARGS);
             else if (lt == 64 && kc) k_linearize<T, LIN_FULL, true, 12, false, true><<<T_, lt, 0, st>>>(LIN_ARGS);
             else if (lt == 64) k_linearize<T, LIN_FULL, true, 12><<<T_, lt, 0, st>>>(LIN_ARGS);
             else if (kc) k_linearize<T, LIN_FULL, true, 1, false, true><<<T_, lt, 0, st>>>(LIN_ARGS);

@@ -469,11 +469,38 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
                 // group pairs an even-q pass with an odd-q pass (two independent read-modify-writes), and
                 // the first group (ox, oy) = (0, 0), q = 0, 1 covers the 64 nodes x, y, z < 4 exactly once:
                 // plain stores (those nodes are not zeroed by the node phase)
+#ifdef MPL_DEBUG
+                // race check of the __syncwarp-only scatter (debug build): every force-buffer slot written in
+                // a group is claimed once in a per-warp bitmap; a second claim in the same group traps
+                __shared__ unsigned dbg_claim[WZ_W][5];
+                auto claim = [&](int slot) {
+                    const unsigned bit = 1u << (slot & 31), old = atomicOr(&dbg_claim[wid][slot >> 5], bit);
+                    DASSERT(slot >= 0 && slot < 132 && !(old & bit));
+                };
+                auto release = [&]() {
+                    __syncwarp();
+                    if (lane < 5) dbg_claim[wid][lane] = 0u;
+                    __syncwarp();
+                };
+                release();
+#define MPL_CLAIM(s) claim(s)
+#define MPL_RELEASE() release()
+#else
+#define MPL_CLAIM(s) \
+    do {             \
+    } while (0)
+#define MPL_RELEASE() \
+    do {              \
+    } while (0)
+#endif
                 {
                     const f4 f0 = cf(0, 0, 0), f1 = cf(0, 0, 1);
+                    MPL_CLAIM(hb);
+                    MPL_CLAIM(hb + 1);
                     S.F[hb] = f0;
                     S.F[hb + 1] = f1;
                     __syncwarp();
+                    MPL_RELEASE();
                 }
 #pragma unroll
                 for (int g = 0; g < 7; g++) {
@@ -482,7 +509,9 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
                     const int e = g + 1, eox = e >> 2, eoy = (e >> 1) & 1, eq = (e & 1) * 2;
                     f4 *fe = &S.F[hb + 5 * eox + 26 * eoy + eq];
                     const f4 fe_ = cf(eox, eoy, eq);
+                    MPL_CLAIM(hb + 5 * eox + 26 * eoy + eq);
                     if ((g & 1) == 1) {  // g = 1, 3, 5: odd pass (ox, oy) = e's
+                        MPL_CLAIM(hb + 5 * eox + 26 * eoy + 1);
                         f4 *fo = &S.F[hb + 5 * eox + 26 * eoy + 1];
                         const f4 fo_ = cf(eox, eoy, 1);
                         const f4 a = *fe, b = *fo;
@@ -493,7 +522,10 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
                         *fe = mk4<float>(a.x + fe_.x, a.y + fe_.y, a.z + fe_.z, 0.f);
                     }
                     __syncwarp();
+                    MPL_RELEASE();
                 }
+#undef MPL_CLAIM
+#undef MPL_RELEASE
             }
         }
         // ---- node phase: forces + lumped mass term, stored (interior) or added atomically (faces)

@@ -1,8 +1,6 @@
-# A/B driver for one gpurun call (scratch; edited per experiment)
+# debug build (device asserts + the HVP scatter's race claims) over the parity / variant / slab suites
 set -u
 mkdir -p gpurun_out
-for v in 12 8 12 8; do
-  MPL_LIN_GEN_MINB=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 5 --warmup 3 >> gpurun_out/ab_lin$v.json 2>> gpurun_out/ab_lin.err
-done
-MPL_LIN_GEN_MINB=8 python -m tests._hvp_variant_check cfg2s_fp32 > gpurun_out/ab_lincheck.txt 2>&1
+MPL_LIB=dbg timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_hvp_variants.py tests/test_gpu_slabs.py tests/test_gpu_edge.py -m gpu -x -q > gpurun_out/pytest_dbg.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_dbg.log
+MPL_LIB=dbg timeout 600 python tools/prof_hvp.py --config cfg4 --reps 3 >> gpurun_out/pytest_dbg.log 2>&1; echo "prof rc=$?" >> gpurun_out/pytest_dbg.log
 echo done

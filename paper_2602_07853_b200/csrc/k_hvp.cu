@@ -238,17 +238,13 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
     __shared__ WzWarp SW[WZ_W];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WzWarp &S = SW[wid];
+    // programmatic dependent launch: everything up to the first tile's tangent and metadata reads data the
+    // previous kernel does not write (the tangent, tile tables), so it runs before griddepcontrol.wait and
+    // overlaps the previous kernel's tail; u, the CG scalars and the iteration index are read after it.
+    // In a captured graph (jdev) the wait comes first: with the prologue ahead of it the replayed iteration
+    // counts broke (the index read raced with the previous node's write), DESIGN §5
     pdl_trigger();
-    pdl_wait();
-    if (jdev != nullptr) {
-        cgj = *jdev;
-        uHu = const_cast<double *>(cgs[cgj].pHp);
-        cgthr = sc->cg_thr;
-    }
-    if (cgs != nullptr) {  // inside PCG: nothing to do once converged / stopped at negative curvature
-        const double rr = warp_sum(cgs[cgj].rr[lane]);
-        if (sc->neg_curv || (cgj > 0 && rr <= cgthr)) return;
-    }
+    if (jdev != nullptr) pdl_wait();
     const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
     const int zp = lane >> 4, lx = (lane >> 2) & 3, ly = lane & 3;
     const int lA = lx * 16 + ly * 4 + 2 * zp;  // cell A's local position (B = lA + 1)
@@ -360,6 +356,16 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
     TileK cur = tile_k(t0, mcur);
 #pragma unroll
     for (int c = 0; c < 12; c++) { kload(cur, 0, c); kload(cur, 45, c); }
+    if (jdev == nullptr) pdl_wait();
+    if (jdev != nullptr) {
+        cgj = *jdev;
+        uHu = const_cast<double *>(cgs[cgj].pHp);
+        cgthr = sc->cg_thr;
+    }
+    if (cgs != nullptr) {  // inside PCG: nothing to do once converged / stopped at negative curvature
+        const double rr = warp_sum(cgs[cgj].rr[lane]);
+        if (sc->neg_curv || (cgj > 0 && rr <= cgthr)) return;
+    }
     halo(t0, 0, mcur);
     double acc = 0.0;
     int it = 0;

@@ -1,8 +1,7 @@
-# ncu --set full of the HVP at cfg5B (the scaling config) and cfg3 PPC 8 at the final kernel
 set -u
 mkdir -p gpurun_out
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hvp -s 2 -c 1 -o gpurun_out/hvp5_full -f \
-  python tools/prof_hvp.py --config cfg5B --reps 3 > gpurun_out/ncu_hvp5.log 2>&1
-timeout 600 python tools/prof_hvp.py --config cfg5B --reps 20 >> gpurun_out/prof5.txt 2>&1
-timeout 600 python tools/prof_hvp.py --config cfg3_ppc8 --reps 30 >> gpurun_out/prof5.txt 2>&1
+timeout 1200 python -m pytest tests/test_gpu_hvp_variants.py tests/test_gpu_parity.py tests/test_gpu_slabs.py -m gpu -x -q > gpurun_out/pytest_ab.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_ab.log
+for v in 1 0; do
+  MPL_PCG_GRAPH=$v MPL_HVP_EVENTS=0 timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 5 --warmup 3 >> gpurun_out/ab_g$v.json 2>> gpurun_out/ab_g.err
+done
 echo done

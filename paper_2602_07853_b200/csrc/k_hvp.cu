@@ -224,7 +224,7 @@ __device__ __forceinline__ void kc_apply2(const float *k, const float2 d[9], flo
         }
 }
 
-template <bool KC, int MINB = 3, bool LIST = false>
+template <bool KC, int MINB = 3, bool LIST = false, bool GR = false>
 __global__ void __launch_bounds__(32 * WZ_W, MINB)
     k_hvp_wz(int T_, const int *__restrict__ nplus, const unsigned long long *__restrict__ cmask,
              const int *__restrict__ hascells, const float *__restrict__ K, const int *__restrict__ kstart,
@@ -241,10 +241,12 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
     // programmatic dependent launch: everything up to the first tile's tangent and metadata reads data the
     // previous kernel does not write (the tangent, tile tables), so it runs before griddepcontrol.wait and
     // overlaps the previous kernel's tail; u, the CG scalars and the iteration index are read after it.
-    // In a captured graph (jdev) the wait comes first: with the prologue ahead of it the replayed iteration
-    // counts broke (the index read raced with the previous node's write), DESIGN §5
+    // In a captured graph (GR, jdev) the wait comes first: with the prologue ahead of it the replayed
+    // iteration counts broke (the index read raced with the previous node's write); the
+    // 45-number form (!KC) also waits first (its 90 prefetched tangent registers spilled ahead of the wait)
+    constexpr bool EARLY = KC && !GR;
     pdl_trigger();
-    if (jdev != nullptr) pdl_wait();
+    if (!EARLY) pdl_wait();
     const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
     const int zp = lane >> 4, lx = (lane >> 2) & 3, ly = lane & 3;
     const int lA = lx * 16 + ly * 4 + 2 * zp;  // cell A's local position (B = lA + 1)
@@ -356,8 +358,8 @@ __global__ void __launch_bounds__(32 * WZ_W, MINB)
     TileK cur = tile_k(t0, mcur);
 #pragma unroll
     for (int c = 0; c < 12; c++) { kload(cur, 0, c); kload(cur, 45, c); }
-    if (jdev == nullptr) pdl_wait();
-    if (jdev != nullptr) {
+    if (EARLY) pdl_wait();
+    if (GR) {
         cgj = *jdev;
         uHu = const_cast<double *>(cgs[cgj].pHp);
         cgthr = sc->cg_thr;
@@ -854,7 +856,7 @@ __global__ void __launch_bounds__(32 * WH_W, MINB)
 
 int g_num_sms = 0;
 
-template <bool KC, int MINB, bool LIST>
+template <bool KC, int MINB, bool LIST, bool GR = false>
 mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu, const CGSlot *cgs, int cgj,
                      double cgthr, const int *tlist, int ntl, const int *jdev = nullptr) {
     static int per_sm = 0;
@@ -863,7 +865,7 @@ mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         int occ = 0;
-        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_wz<KC, MINB, LIST>, 32 * WZ_W, 0));
+        MPL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hvp_wz<KC, MINB, LIST, GR>, 32 * WZ_W, 0));
         per_sm = occ > 0 ? occ : 1;
     }
     // persistent: one wave of (SMs x resident CTAs), tiles strided by the global warp count
@@ -871,7 +873,7 @@ mpl_status launch_wz(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uHu
     const int need = ((tlist ? ntl : ctx->T) + WZ_W - 1) / WZ_W;
     if (grid > need) grid = need;
     if (grid < 1) return MPL_OK;
-    MPL_CUDA(launch_pdl(k_hvp_wz<KC, MINB, LIST>, grid, 32 * WZ_W, 0, ctx->stream, ctx->T, (const int *)ctx->t_nplus.p,
+    MPL_CUDA(launch_pdl(k_hvp_wz<KC, MINB, LIST, GR>, grid, 32 * WZ_W, 0, ctx->stream, ctx->T, (const int *)ctx->t_nplus.p,
                         (const unsigned long long *)ctx->t_cmask.p, (const int *)ctx->t_hascells.p,
                         (const float *)ctx->K.p, (const int *)(KC ? ctx->t_kstart2.p : ctx->t_kstart.p),
                         (const float *)owned_mass(ctx),
@@ -940,7 +942,7 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
     if (ctx->T == 0) return MPL_OK;
     if (jdev) {  // graph-captured PCG: fp32 compressed-tangent k_hvp_wz only
         if (sizeof(T) == 8 || hvp_variant() == 1 || !ctx->kc_now || tlist) return MPL_ERR_UNSUPPORTED;
-        return launch_wz<true, 3, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0, jdev);
+        return launch_wz<true, 3, false, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0, jdev);
     }
     if (tlist && (sizeof(T) == 8 || hvp_variant() == 1)) return MPL_ERR_UNSUPPORTED;  // tile lists: k_hvp_wz only
     if (sizeof(T) == 8) return launch_wh<T, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);  // 45 doubles per lane

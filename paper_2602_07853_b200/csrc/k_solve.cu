@@ -1709,6 +1709,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
     };
     std::vector<CGSlot> hslots;
     double phi0 = 0;
+    double phi_v = 0;       // Phi at the current v when known (the linearisation at v, or the accepted trial)
+    bool phi_known = false;
     for (int k = 0; k < kmax; k++) {
         // ---- linearise at v^k -------------------------------------------------------------
         cudaEventRecord(e0, st);
@@ -1733,6 +1735,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         MPL_CHECK(d2h_sync(ctx, st));
         t_lin += elapsed(e0, e1);
         phi0 = e[NSTRIPE] != 0.0 ? __builtin_inf() : host_stripes(e);
+        phi_v = phi0;
+        phi_known = true;
         const double rr0 = host_stripes(s0.rr);
         const double gn = sqrt(rr0);
         if (k == 0) S.grad_norm0 = gn;
@@ -1973,6 +1977,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         const double gp = host_stripes(gps);
         double alpha = 1.0;
         int h = 0;
+        double phi_acc = 0;
+        bool phi_acc_known = false;
         if (cfg->fixed_ls_halvings) {
             for (h = 0; h < cfg->fixed_ls_halvings[k]; h++) alpha *= 0.5;
             MPL_CUDA(cudaMemcpyAsync(vt, v, NT * sizeof(vec4<T>), cudaMemcpyDeviceToDevice, st));
@@ -1984,6 +1990,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
                 double phi = 0;
                 MPL_CHECK(energy_at<T>(ctx, vt, &phi));
                 if (std::isinf(phi)) S.n_inverted_trials++;
+                phi_acc = phi;
+                phi_acc_known = true;
                 if (phi <= phi0 + cfg->armijo_c * alpha * gp + cfg->ls_slack * fabs(phi0)) break;
                 if (h >= cfg->ls_max) break;
                 alpha *= 0.5;
@@ -1998,6 +2006,8 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         S.ls_halvings += h;
         std::swap(v, vt);
         std::swap(ctx->n_v, ctx->n_vt);
+        phi_v = phi_acc;
+        phi_known = phi_acc_known;
         S.newton_iters = k + 1;
     }
     if (!fixed && S.newton_iters == kmax && !S.converged) {
@@ -2012,7 +2022,10 @@ mpl_status newton_impl(mpl_ctx ctx, const mpl_solver_cfg *cfg, mpl_solve_stats *
         if (kmax < MPL_MAX_NEWTON_LOG) S.grad_norms[kmax] = S.grad_norm;
         if (S.grad_norm <= cfg->newton_rtol * S.grad_norm0) S.converged = 1;
     }
-    MPL_CHECK(energy_at<T>(ctx, v, &S.energy));
+    // Phi at the returned v: already known from its linearisation or from the accepted line-search trial
+    // (one energy pass per step less); computed only after replayed (fixed) line searches
+    if (phi_known) S.energy = phi_v;
+    else MPL_CHECK(energy_at<T>(ctx, v, &S.energy));
     double hsum = 0;
     if (hvp_events && hvp_sample_n > 0)  // mean of the timed executed HVPs x executed HVPs
         hsum = hvp_sample_ms / hvp_sample_n * S.n_hvp;

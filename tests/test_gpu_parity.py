@@ -261,3 +261,7 @@ def test_adaptive_solve_converges(pair):
     # two independent adaptive solves (own counts), each stopped at ||g|| <= eps_N ||g_0||: they agree to
     # the solver tolerance, not to rounding (DESIGN.md §9 reading r2-c)
     assert rel_l2(ctx.get_velocity(), v_o[pair.nid]) <= (1e-7 if sc.precision == 64 else 1e-3)
+    # the reported Phi is the energy at the returned velocity (reused from the last linearisation / accepted
+    # line-search trial, not recomputed): it matches a fresh energy evaluation there
+    e_now = ctx.energy(ctx.get_velocity())
+    assert abs(st["energy"] - e_now) <= (1e-12 if sc.precision == 64 else 1e-6) * abs(e_now)

@@ -947,16 +947,18 @@ mpl_status launch_hvp(mpl_ctx ctx, const void *u_tile, void *Hu_tile, double *uH
     if (tlist && (sizeof(T) == 8 || hvp_variant() == 1)) return MPL_ERR_UNSUPPORTED;  // tile lists: k_hvp_wz only
     if (sizeof(T) == 8) return launch_wh<T, 3>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);  // 45 doubles per lane
     if (hvp_variant() == 1) return launch_wh<T, 5>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr);
-    if (ctx->kc_now) {  // compressed tangent; MPL_KC_MINB: CTAs per SM requested from ptxas (3: 150 registers,
-                        // 12 warps per SM, the default — cfg4 72.4 us isolated / 76.9 in the solve; 4: 128
-                        // registers + 8 B spilled, 73.0 / 77.4; 5: 96 registers + 192 B spilled, 117 us)
+    if (ctx->kc_now) {  // compressed tangent; MPL_KC_MINB: CTAs per SM requested from ptxas (2, the default:
+                        // ptxas takes 168 registers, 3 CTAs of 4 warps still fit, cfg4 68.9 us isolated / 75.4
+                        // in the solve; 3: 148 registers, 70.2 / 76.5; 4: 128 + 8 B spilled, 16 warps, 73.0 /
+                        // 77.4; 5: 96 registers + 192 B spilled, 117 us)
         static int minb = -1;
         if (minb < 0) {
             const char *e = getenv("MPL_KC_MINB");
-            minb = e ? atoi(e) : 3;
+            minb = e ? atoi(e) : 2;
         }
         if (tlist) return launch_wz<true, 3, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);
         if (minb == 3) return launch_wz<true, 3, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
+        if (minb == 2) return launch_wz<true, 2, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
         return launch_wz<true, 4, false>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, nullptr, 0);
     }
     if (tlist) return launch_wz<false, 3, true>(ctx, u_tile, Hu_tile, uHu, cgs, cgj, cgthr, tlist, ntl);

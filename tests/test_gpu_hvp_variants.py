@@ -36,6 +36,7 @@ CASES = [
     ({"MPL_KC": "0"}, "cfg1_fp32"),          # the 45-number tangent where the compressed one is the default
     ({"MPL_KC": "0"}, "cfg2s_fp32"),
     ({"MPL_KC_MINB": "4"}, "cfg2s_fp32"),   # 16 warps per SM (128 registers) instead of the default 12
+    ({"MPL_KC_MINB": "3"}, "cfg2s_fp32"),   # ptxas capped at 148 registers (the default asks for 2 CTAs per SM: 168)
     ({"MPL_G2P": "particle"}, "mix_fp32"),   # one thread per particle with its own cell lookups (tile default)
     ({"MPL_G2P": "particle"}, "watermix_fp64"),
     ({"MPL_P2Q_HI": "1"}, "mix_fp32"),       # the dense-bucket P2Q kernel (default only at >= 40 particles per cell)

@@ -8,7 +8,8 @@ element by element:
   * a5 gradient and a6 HVP + Jacobi diagonal at a probe v = v^0 + 0.01 n(key), direction u = n(key)
     (key-indexed normal draws, so window and full run use identical probes);
   * a9 G2P of the window's particles from the GPU's own v^{n+1} after one adaptive implicit step.
-Cases: cfg2, cfg3 (PPC 8), cfg4 and cfg5B (512^3, ~93M particles: wheel rim, wheel-slab contact, the
+Cases: cfg2, cfg3 (PPC 8, 27 and 64: the PPC sweep of BASELINE.json config 3; PPC 1 is the full-scene
+step of test_gpu_fullstep.py; PPC 64 runs the dense-bucket P2Q kernel by default), cfg4 and cfg5B (512^3, ~93M particles: wheel rim, wheel-slab contact, the
 plate's Dirichlet layer) in fp32 — the bench's configuration — and cfg4 / cfg5B in fp64 (the fp64 HVP
 kernel; cfg5B's "fp64 check" of BASELINE.json config 5).
 Bars: BASELINE.json's (1e-5 fp32 / 1e-10 fp64 on unload / gradient / HVP; the step bars for G2P)."""
@@ -29,13 +30,16 @@ SIZE = 20
 WINDOWS = {
     "cfg2": [(22, 22, 22), (44, 10, 30)],
     "cfg3": [(54, 54, 54), (100, 60, 2)],
+    "cfg3_ppc27": [(54, 54, 54), (100, 60, 2)],
+    "cfg3_ppc64": [(54, 54, 54), (100, 60, 2)],
     "cfg4": [(54, 80, 118), (180, 80, 118), (118, 2, 118)],  # left sphere, right sphere, slab + floor
     # cfg5B (dx = 1/512; wheel axis z through (256, 182.6, 256) cells, R = 153.6, r = 51.2 cells, z in
     # [217.6, 294.4); slab y in [3, 29); plate: nodes with y >= 336.2): outer rim, inner rim, wheel-slab
     # contact + floor, the plate layer at the wheel's top
     "cfg5B": [(395, 172, 246), (296, 172, 246), (246, 20, 246), (246, 322, 246)],
 }
-CASES = [("cfg2", 32), ("cfg3", 32), ("cfg4", 32), ("cfg5B", 32), ("cfg4", 64), ("cfg5B", 64)]
+CASES = [("cfg2", 32), ("cfg3", 32), ("cfg3_ppc27", 32), ("cfg3_ppc64", 32), ("cfg4", 32), ("cfg5B", 32),
+         ("cfg4", 64), ("cfg5B", 64)]
 
 
 # elastic part of the HVP: the fp32 bar times this slack (DESIGN.md §9 reading r2-a); fp64: none

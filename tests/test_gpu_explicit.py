@@ -125,3 +125,56 @@ def test_explicit_slabs_match_oracle(cuts):
     assert np.array_equal(ids[order], np.arange(sc.n_particles))
     for key, ref in (("x", parts[0]), ("pv", parts[1]), ("F", parts[2])):
         assert rel_l2(np.concatenate([o[key] for o in res])[order], ref) <= TOL[64]["step"]
+
+
+def test_explicit_full_size_windows():
+    """The explicit path at the jelly workload's full size (256^3 grid, 1.12 M particles, fp32: the
+    configuration of profiles/r01_explicit_jelly.json), pre-strained so that f_i != 0: the oracle recomputes
+    v^{n+1} = v-hat + dt f / m on 20^3-cell windows (a cube corner, the cube's interior) and Load of the
+    window's particles from the GPU's own v^{n+1}; nodes / particles whose support lies inside a window
+    are compared element by element (the windowing of tests/test_gpu_fullsize.py)."""
+    import types
+
+    from .test_gpu_fullsize import SIZE, _window
+
+    sc = scenes.by_name("jelly", 32)
+    sc = dataclasses.replace(sc, F=scenes._prestrain(sc.n_particles, 7).astype(sc.F.dtype))
+    ctx = mpl.from_scene(sc, 0)
+    ctx.resample(sc.dt)
+    ijk, m, vn, fr = ctx.get_nodes()
+    ctx.explicit_velocity()
+    v_g = ctx.get_velocity().astype(np.float64)
+    ctx.transfer_to_particles(sc.dt)
+    x_g, vp_g, F_g, G_g = ctx.get_particles()
+    ctx.close()
+    n1, n2 = sc.n[1] + 1, sc.n[2] + 1
+    key = (ijk[:, 0].astype(np.int64) * n1 + ijk[:, 1]) * n2 + ijk[:, 2]
+    full = types.SimpleNamespace(sc=sc, pos={int(k): i for i, k in enumerate(key)})
+    tol, ptol = TOL[32]["grad"], TOL[32]["step"]
+    for lo in [(100, 38, 100), (118, 56, 118)]:
+        w = _window(full, lo)
+        un, prob, grid, gpos = w["un"], w["prob"], w["grid"], w["gpos"]
+        act = w["complete"] & (un.m_i > 0)
+        assert act.sum() > 100 and np.all(gpos[act] >= 0)
+        f = oracle.explicit_force(grid, len(sc.materials), un.m_c, un.V_ck, un.tau_ck)
+        free = act & (prob.freed != 0)
+        v1 = prob.vhat.copy()
+        v1[free] = prob.vhat[free] + sc.dt * f[free] / un.m_i[free][:, None]
+        assert np.linalg.norm(sc.dt * f[free] / un.m_i[free][:, None]) > 1e-4 * np.linalg.norm(v1[free])
+        assert rel_l2(v_g[gpos[act]], v1[act]) <= tol
+        sub = w["sub"]
+        lo_ = np.asarray(lo)
+        base = np.floor(sub.x.astype(np.float64) / sc.dx - 0.5).astype(np.int64)
+        inner = np.all((base >= lo_ + 1) & (base <= lo_ + SIZE - 2), axis=1)
+        assert inner.sum() > 100
+        vnew = np.zeros((grid.nnodes, 3))
+        have = gpos >= 0
+        vnew[have] = v_g[gpos[have]]
+        x_o, v_o, F_o, G_o = oracle.g2p(grid, sc.dt, un.m_c, vnew, sub.x, sub.v, sub.F, sub.G, clip=True,
+                                        mat=sub.mat, materials=sc.materials)
+        idx = w["keep"][inner]
+        assert rel_l2(x_g[idx], x_o[inner]) <= 1e-2 * ptol
+        assert rel_l2(vp_g[idx], v_o[inner]) <= ptol
+        assert rel_l2(F_g[idx], F_o[inner]) <= ptol
+        scale = max(np.linalg.norm(G_o[inner]), np.linalg.norm(v_o[inner]) / sc.dx)
+        assert np.linalg.norm(G_g[idx] - G_o[inner]) <= ptol * scale  # reading r2-b, as at full size

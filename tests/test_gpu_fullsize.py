@@ -10,7 +10,7 @@ element by element:
   * a9 G2P of the window's particles from the GPU's own v^{n+1} after one adaptive implicit step.
 Cases: cfg2, cfg3 (PPC 8, 27 and 64: the PPC sweep of BASELINE.json config 3; PPC 1 is the full-scene
 step of test_gpu_fullstep.py; PPC 64 runs the dense-bucket P2Q kernel by default), cfg4 and cfg5B (512^3, ~93M particles: wheel rim, wheel-slab contact, the
-plate's Dirichlet layer) in fp32 — the bench's configuration — and cfg4 / cfg5B in fp64 (the fp64 HVP
+plate's Dirichlet layer) in fp32 — the bench's configuration — and cfg2 / cfg3 / cfg4 / cfg5B in fp64 (the fp64 HVP
 kernel; cfg5B's "fp64 check" of BASELINE.json config 5), and cfg4's geometry with the split Neo-Hookean law
 (SURVEY f1), with a J-based water sphere (f4) and with von Mises spheres (f2) in fp32, the general-law kernels at full size.
 Bars: BASELINE.json's (1e-5 fp32 / 1e-10 fp64 on unload / gradient / HVP; the step bars for G2P)."""
@@ -45,7 +45,7 @@ WINDOWS = {
     "cfg5B": [(395, 172, 246), (296, 172, 246), (246, 20, 246), (246, 322, 246)],
 }
 CASES = [("cfg2", 32), ("cfg3", 32), ("cfg3_ppc27", 32), ("cfg3_ppc64", 32), ("cfg4", 32), ("cfg5B", 32),
-         ("cfg4", 64), ("cfg5B", 64), ("cfg4_nh", 32), ("cfg4_water", 32),
+         ("cfg2", 64), ("cfg3", 64), ("cfg4", 64), ("cfg5B", 64), ("cfg4_nh", 32), ("cfg4_water", 32),
          ("cfg4_vm", 32)]
 
 
